@@ -1,0 +1,91 @@
+"""Kernel specs and the BASELINE.json workload configs (pure Python, no GPU).
+
+Formulas (BASELINE.json ``configs``), 1-based indices:
+
+* green  (kind 0): K = exp(-i kappa rho) / rho, rho = |x_i - y_j|,
+  x_i = (i_1/n, .., i_d/n, 0..), y_j = (j_1/n, .., j_d/n, 0..) + offset.
+  Plates (d=2): offset (0, 0, 1).  Cubes (d=3): offset (2, 0, 0).
+  kappa = 2 pi n / ppw (ppw = 8 points per wavelength in BASELINE).
+* dft    (kind 1): K = exp(-2 pi i x.k), x_p = (i_p - 1)/n, k_p = j_p - 1 - n/2,
+  phase reduced exactly as (sum (i_p-1)(j_p-1-n/2)) mod n; optional two-sided
+  per-mode bit reversal.
+* radon2d (kind 2): K = exp(2 pi i Phi), Phi = x.k + sqrt(c1^2 k1^2 + c2^2 k2^2),
+  c1 = (2 + sin 2pi x1 sin 2pi x2)/16, c2 = (2 + cos 2pi x1 cos 2pi x2)/16,
+  x_p = (i_p - 1)/n, k_p = j_p - 1 - n/2.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+GREEN, DFT, RADON2D = 0, 1, 2
+
+
+@dataclass(frozen=True)
+class KernelSpec:
+    kind: int
+    d: int
+    n: int
+    kappa: float = 0.0
+    offset: tuple = (0.0, 0.0, 0.0)
+    bitrev: bool = False
+
+    def describe(self) -> str:
+        name = {GREEN: "green", DFT: "dft", RADON2D: "radon2d"}[self.kind]
+        return f"{name}(d={self.d}, n={self.n})"
+
+
+def green_plates(n: int, ppw: float = 8.0) -> KernelSpec:
+    return KernelSpec(GREEN, 2, n, 2 * math.pi * n / ppw, (0.0, 0.0, 1.0))
+
+
+def green_cubes(n: int, ppw: float = 8.0, offset=(2.0, 0.0, 0.0)) -> KernelSpec:
+    return KernelSpec(GREEN, 3, n, 2 * math.pi * n / ppw, tuple(offset))
+
+
+def dft(d: int, n: int, bitrev: bool = True) -> KernelSpec:
+    return KernelSpec(DFT, d, n, 0.0, (0.0, 0.0, 0.0), bitrev)
+
+
+def radon2d(n: int) -> KernelSpec:
+    return KernelSpec(RADON2D, 2, n)
+
+
+def level_rule(n: int, cb: int = 8) -> int:
+    """Largest even L with n / 2^L >= C_b."""
+    L = 0
+    while (n >> (L + 2)) >= cb and n % (1 << (L + 2)) == 0:
+        L += 2
+    return L
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    spec: KernelSpec
+    tol: float
+    cb: int = 8
+    seed: int = 2411_03029
+    input_seed: int = 7
+    nv: int = 1
+    note: str = ""
+
+    @property
+    def L(self) -> int:
+        return level_rule(self.spec.n, self.cb)
+
+    @property
+    def points(self) -> int:
+        return self.spec.n ** self.spec.d
+
+
+# BASELINE.json "configs", in order.
+CONFIGS = [
+    Config("green_plates_n64", green_plates(64), 1e-6),
+    Config("green_cubes_n64", green_cubes(64), 1e-6),
+    Config("green_cubes_n256", green_cubes(256), 1e-4),
+    Config("dft6_n16", dft(6, 16), 1e-8, cb=1,
+           note="C_b=1 (L=4): C_b=8 gives L=0 (SURVEY F4); two-sided bit reversal (App. A3)"),
+    Config("radon2d_n1024", radon2d(1024), 1e-6),
+]
+BY_NAME = {c.name: c for c in CONFIGS}

@@ -1,0 +1,161 @@
+/* oiobf_b200.h — C ABI of the B200-native tensor-butterfly library
+ * (paper_2411_03029_b200/libtbf_b200.so).
+ *
+ * This is the drop-in boundary under the reference's C++ construct/apply
+ * interface (namespace oiobf, /root/reference/proj/include/oiobf/*.hpp).  Each
+ * entry point names the reference function it replaces.  Conventions:
+ *   - every function returns 0 on success, OIOBF_EINVAL for argument errors
+ *     (the reference's std::invalid_argument, types.hpp:48-54) and
+ *     OIOBF_ERUNTIME for CUDA failures; oiobf_last_error() gives the message
+ *     (thread-local).  Exceptions never cross this boundary.
+ *   - complex128 is interleaved (re, im) doubles, bit-compatible with
+ *     std::complex<double>; tensors are first-mode-fastest (tensor.hpp:10-15);
+ *     matrices column-major; indices 1-based where the reference API is.
+ *   - host pointers are borrowed for the duration of the call; device memory is
+ *     owned by opaque handles.
+ *   - there is no CPU fallback: without a usable sm_100 device every compute
+ *     entry point fails with OIOBF_ERUNTIME.
+ */
+#ifndef OIOBF_B200_H
+#define OIOBF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OIOBF_OK 0
+#define OIOBF_EINVAL 1
+#define OIOBF_ERUNTIME 2
+
+/* kernel catalog (BASELINE.json configs) */
+#define OIOBF_KERNEL_GREEN 0   /* exp(-i kappa rho)/rho, plates (d=2) / cubes (d=3) */
+#define OIOBF_KERNEL_DFT 1     /* exp(-2 pi i x.k), optional two-sided bit reversal  */
+#define OIOBF_KERNEL_RADON2D 2 /* exp(2 pi i Phi(x,k))            */
+
+/* ProxyMode (id.hpp:48) */
+#define OIOBF_PROXY_ALL 0
+#define OIOBF_PROXY_UNIFORM_RANDOM 1
+#define OIOBF_PROXY_EVENLY_SPACED 2
+
+/* POD kernel spec: replaces the opaque std::function in KernelEvaluator
+ * (tensor.hpp:81-90) with a device-evaluable description. */
+typedef struct oiobf_kernel_spec {
+  int32_t kind;
+  int32_t d;       /* modes per side, 1..6 */
+  int64_t n;       /* points per mode (m_k = n_k = n) */
+  int32_t bitrev;  /* DFT: two-sided per-mode bit reversal */
+  int32_t pad_;
+  double kappa;     /* Green: wavenumber */
+  double offset[3]; /* Green: source-plane/cube offset added to y */
+} oiobf_kernel_spec;
+
+/* ProxyStrategy (id.hpp:50-55) */
+typedef struct oiobf_proxy_strategy {
+  int32_t mode;
+  int32_t pad_;
+  int64_t q;
+  int64_t max_retries;
+  int64_t row_cap;
+} oiobf_proxy_strategy;
+
+typedef struct oiobf_tbf oiobf_tbf; /* opaque device-resident TensorButterfly */
+
+const char* oiobf_last_error(void);
+/* device ordinal to use for subsequent calls of this thread (default 0) */
+int oiobf_set_device(int device);
+/* sm count, cc major/minor, total memory (bytes) of the current device */
+int oiobf_device_info(int64_t out[4]);
+
+/* ---- id-compress (id.hpp) ------------------------------------------------ */
+
+/* Batched column_id (id.hpp:40, id.cpp:124-130): `batch` independent matrices,
+ * A_b of shape m[b] x n[b] column-major at A + 2*a_off[b] (host, interleaved).
+ * max_rank[b] < 0 means std::nullopt.  Outputs per matrix b (host):
+ *   rank[b]; skeleton at skel + s_off[b] (n[b] slots, first rank used, 1-based
+ *   sorted); interp (rank x n[b] col-major) at interp + 2*i_off[b] (room for
+ *   n[b]*n[b]); perm (pivot order, 0-based, n[b] entries) at perm + s_off[b];
+ *   saturated[b]; interp_max_abs[b].  ID of the proxy/unfolding matrix is
+ *   computed on the GPU (TSQR + reference pivoting on R). */
+int oiobf_column_id_batch(int64_t batch, const int64_t* m, const int64_t* n, const int64_t* a_off, const double* A,
+                          double tol, const int64_t* max_rank, int64_t* rank, const int64_t* s_off, int64_t* skel,
+                          const int64_t* i_off, double* interp, int64_t* perm, int32_t* saturated,
+                          double* interp_max_abs);
+
+/* select_proxies_count (id.cpp:155-185), bit-exact; out has room for extent. */
+int oiobf_select_proxies_count(int64_t extent, int64_t count, int32_t mode, uint64_t seed, int64_t* out,
+                               int64_t* out_count);
+
+/* derive_seed (rng.hpp:39-47) */
+uint64_t oiobf_derive_seed(uint64_t seed, const uint64_t* tags, int32_t ntags);
+
+/* subtensor_at (tensor.cpp:249-266): K(rows, cols) over explicit per-mode
+ * index lists (2d lists concatenated, counts[2d]), evaluated on the GPU;
+ * out = prod(counts) complex, first mode fastest. */
+int oiobf_subtensor_at(const oiobf_kernel_spec* spec, const int64_t* counts, const int64_t* lists, double* out);
+
+/* mode_product_blockdiag (tensor.cpp:136-166) on the GPU.  t: nmodes-mode
+ * tensor of `shape`; blocks concatenated col-major with shapes (br[b], bc[b]). */
+int oiobf_mode_product_blockdiag(int32_t nmodes, const int64_t* shape, const double* t, int32_t mode, int32_t nb,
+                                 const int64_t* br, const int64_t* bc, const double* blocks, int32_t transpose,
+                                 double* out);
+
+/* ---- tensor-butterfly ----------------------------------- */
+
+/* tbf_construct(eval, L, tol, proxies, seed) (PAPER Alg. 1).
+ * L even, n = C_b * 2^L.  Factors and cores stay in device memory. */
+int oiobf_tbf_construct(const oiobf_kernel_spec* spec, int32_t L, double tol, const oiobf_proxy_strategy* proxies,
+                        uint64_t seed, oiobf_tbf** out);
+int oiobf_tbf_destroy(oiobf_tbf* h);
+
+/* tbf_contract(bf, F) (PAPER Alg. 2) with host buffers:
+ * F, G: n^d x nv complex, first mode fastest.  Includes H2D/D2H copies. */
+int oiobf_tbf_contract(oiobf_tbf* h, const double* F, double* G, int64_t nv);
+
+/* Same with device buffers (double2*), enqueued on `stream` (cudaStream_t,
+ * NULL = legacy default).  Replays a captured CUDA graph after the first call
+ * for a given (nv, F, G, stream). */
+int oiobf_tbf_contract_device(oiobf_tbf* h, const void* dF, void* dG, int64_t nv, void* stream);
+
+/* tbf_memory: bytes of V, W, U, P, cores (out[5]). */
+int oiobf_tbf_memory(const oiobf_tbf* h, int64_t out[5]);
+
+/* info[0..9]: d, n, L, Lc, nmid, total_slots, total_skel, total_interp,
+ * total_core, total_perm (sizes for oiobf_tbf_export). */
+int oiobf_tbf_info(const oiobf_tbf* h, int64_t info[10]);
+
+/* Flat export in canonical slot order: V/W levels 0..Lc then
+ * U/P levels 0..Lc; per slot rank, ncols, rows; skeletons (global 1-based),
+ * interps (rank x ncols col-major), pivot orders; cores per pair p = s*nmid+t
+ * in the reference's matricized column-major layout; r_est per (side, level).
+ * Any output pointer may be NULL to skip it. */
+int oiobf_tbf_export(const oiobf_tbf* h, int64_t* ranks, int64_t* ncols, int64_t* rows, int64_t* skel,
+                     double* interp, int64_t* perm, double* cores, int64_t* core_rows, int64_t* core_cols,
+                     int64_t* r_est);
+
+/* Construction timing breakdown (ms): [proxies+targets, panel TSQR, finish,
+ * compaction, cores, total] accumulated over levels. */
+int oiobf_tbf_timings(const oiobf_tbf* h, double out[6]);
+
+/* Apply-plan statistics for roofline accounting: out[0] = algorithmic bytes of
+ * one contraction at nv=1 (16 * (2 n^d + sum|V,W,U,P| + sum|cores|)),
+ * out[1] = core bytes, out[2] = number of kernel launches per contraction,
+ * out[3] = complex MACs per contraction at nv=1. */
+int oiobf_tbf_plan_stats(oiobf_tbf* h, int64_t out[4]);
+
+/* Per-kernel timing of one device contraction (ms per launch group):
+ * out[0] = factor steps (V/W), out[1] = core GEMV, out[2] = P/U steps, out[3] = total.
+ * Timed with CUDA events on `stream`, averaged over `reps` contractions. */
+int oiobf_tbf_profile_contract(oiobf_tbf* h, const void* dF, void* dG, int32_t reps, void* stream, double out[4]);
+
+/* K-check: direct dense sums G(i, v) = sum_j K(i, j) F(j, v) on the GPU for
+ * `nrows` sampled output flat indices (first mode fastest); F host n^d x nv. */
+int oiobf_dense_rows(const oiobf_kernel_spec* spec, const double* F, int64_t nv, int64_t nrows,
+                     const int64_t* rows_flat, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OIOBF_B200_H */

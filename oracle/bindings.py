@@ -121,6 +121,8 @@ class Oracle:
                                            C.c_uint64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
                                            C.POINTER(C.c_void_p)]
         L.oracle_tbf_free.argtypes = [C.c_void_p]
+        L.oracle_tbf_import.argtypes = [i32p, f64p, C.c_int, C.c_double, i64p, i64p, i64p, f64p, f64p, i64p, i64p,
+                                        C.POINTER(C.c_void_p)]
         L.oracle_tbf_info.argtypes = [C.c_void_p, i64p]
         L.oracle_tbf_export.argtypes = [C.c_void_p, i64p, i64p, i64p, f64p, i32p, i64p, f64p, i64p, f64p, i64p, i64p,
                                         i64p]
@@ -248,6 +250,21 @@ class Oracle:
         self._ck(self.lib.oracle_tbf_construct(si, sf, L, tol, mode, q, max_retries, row_cap, seed, nthreads, fr, po,
                                                fp, tie_eps, C.byref(h)))
         del keep
+        return OracleTBF(self, h, spec)
+
+    def tbf_import(self, spec, L, tol, fz):
+        """Oracle TBF holding exactly the factors of an exported factorization."""
+        si, sf = spec_arrays(spec)
+        h = C.c_void_p()
+        skel = np.ascontiguousarray(fz.skel, np.int64)
+        interp = np.ascontiguousarray(np.asarray(fz.interp, np.complex128)).view(np.float64)
+        cores = np.ascontiguousarray(np.asarray(fz.cores, np.complex128)).view(np.float64)
+        self._ck(self.lib.oracle_tbf_import(si, sf, L, tol, np.ascontiguousarray(fz.ranks, np.int64),
+                                            np.ascontiguousarray(fz.ncols, np.int64),
+                                            skel if skel.size else np.zeros(1, np.int64),
+                                            interp if interp.size else np.zeros(2), cores if cores.size else np.zeros(2),
+                                            np.ascontiguousarray(fz.core_rows, np.int64),
+                                            np.ascontiguousarray(fz.core_cols, np.int64), C.byref(h)))
         return OracleTBF(self, h, spec)
 
     def dense_rows(self, spec, F, rows_flat, nthreads=0):

@@ -1071,6 +1071,51 @@ int oracle_tbf_construct(const int* si, const double* sf, int L, double tol, int
 
 void oracle_tbf_free(void* h) { delete static_cast<TBF*>(h); }
 
+// Build an oracle TBF from an exported factorization (e.g. the GPU's), so the
+// CPU apply runs on exactly the same factors ("same factors" parity, and the
+// CPU apply baseline without a CPU construction).  Layout as oracle_tbf_export.
+int oracle_tbf_import(const int* si, const double* sf, int L, double tol, const i64* ranks, const i64* ncols,
+                      const i64* skel, const double* interp, const double* cores, const i64* core_rows,
+                      const i64* core_cols, void** out) {
+  GUARD_BEGIN
+  auto b = std::make_unique<TBF>();
+  b->spec = spec_from(si, sf);
+  b->L = L;
+  b->Lc = L / 2;
+  b->tol = tol;
+  b->nmid = ipow(2, static_cast<i64>(b->spec.d) * b->Lc);
+  i64 g = 0, sk = 0, ip = 0;
+  for (int sd = 0; sd < 2; ++sd) {
+    b->side[sd].resize(static_cast<size_t>(b->Lc + 1));
+    for (int l = 0; l <= b->Lc; ++l) {
+      const LevelShape ls = level_shape(*b, l);
+      auto& lv = b->side[sd][static_cast<size_t>(l)];
+      lv.resize(static_cast<size_t>(ls.count));
+      for (auto& s : lv) {
+        s.rank = ranks[g];
+        s.ncols = ncols[g];
+        s.skel.assign(skel + sk, skel + sk + s.rank);
+        s.interp = cx_in(interp + 2 * ip, s.rank * s.ncols);
+        sk += s.rank;
+        ip += s.rank * s.ncols;
+        ++g;
+      }
+    }
+  }
+  const i64 P = b->nmid * b->nmid;
+  b->cores.resize(static_cast<size_t>(P));
+  b->core_rows.assign(core_rows, core_rows + P);
+  b->core_cols.assign(core_cols, core_cols + P);
+  i64 co = 0;
+  for (i64 p = 0; p < P; ++p) {
+    const i64 sz = core_rows[p] * core_cols[p];
+    b->cores[static_cast<size_t>(p)] = cx_in(cores + 2 * co, sz);
+    co += sz;
+  }
+  *out = b.release();
+  GUARD_END
+}
+
 // info[0..]: d, n, L, Lc, nmid, total_slots, total_skel, total_interp, total_core, total_perm
 int oracle_tbf_info(void* h, i64* info) {
   GUARD_BEGIN

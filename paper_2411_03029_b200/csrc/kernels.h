@@ -1,0 +1,84 @@
+// Launch wrappers for the sm_100a kernels (definitions in *_kernels.cu).
+#pragma once
+
+#include "common.cuh"
+#include "level.cuh"
+
+namespace tbf {
+
+// ---- construction (id_kernels.cu)
+size_t panel_smem_bytes(const LevelDesc& L);
+size_t finish_smem_bytes(const LevelDesc& L);
+void launch_gen_proxies(const LevelDesc& L, int* proxies, cudaStream_t st);
+void launch_targets(const LevelDesc& L, const int* crank, const i64* cskel_off, const int* cskel, int* targets,
+                    int* width, cudaStream_t st);
+void launch_panel(const LevelDesc& L, const KSpec& ks, const int* proxies, const int* targets, const int* width,
+                  double2* rpart, cudaStream_t st);
+void launch_finish(const LevelDesc& L, double tol, double tie_eps, i64 max_rank, const double2* rpart,
+                   const int* targets, const int* width, int* rank, int* sat, int* perm, int* skel_tmp,
+                   double2* interp_tmp, double* gaps, cudaStream_t st);
+void launch_compact(i64 nslots, i64 wmax, const int* rank, const int* width, const i64* skel_off,
+                    const i64* interp_off, const int* skel_tmp, const double2* interp_tmp, int* skel, double2* interp,
+                    cudaStream_t st);
+
+// Generic batched column IDs of explicit matrices (column_id on the GPU):
+// matrices are read from device memory instead of generated.
+struct MatIdJob {
+  i64 a_off;  // element offset of the m x n col-major matrix
+  i64 m;
+  int n;
+  int pad;
+};
+void launch_matrix_panel(i64 njobs, const MatIdJob* jobs, const double2* A, i64 nparts, i64 rpp, int pr, i64 wmax,
+                         double2* rpart, cudaStream_t st);
+
+// ---- cores (core_kernels.cu)
+struct PairDesc {
+  i64 core_off;                 // element offset of the row-major R x C core
+  int R, C;
+  int rr[kMaxD], rc[kMaxD];     // per-mode ranks (rows: U side, cols: V side)
+  i64 rs_off[kMaxD], cs_off[kMaxD];  // skeleton offsets (global 1-based ints)
+  i64 work_off;                 // prefix of R*C over pairs (grid mapping)
+};
+void launch_cores(const KSpec& ks, i64 npairs, const PairDesc* pairs, i64 total_entries, const int* uskel,
+                  const int* vskel, double2* cores, cudaStream_t st);
+
+// ---- apply (apply_kernels.cu)
+constexpr int kMaxTM = kMaxD + 1;  // tensor modes incl. n_v
+struct MPStep {                     // one item of a batched block-diagonal mode product
+  i64 in_off, out_off;
+  i64 work_off;                     // prefix of output sizes (grid mapping)
+  i64 total;                        // output elements
+  i64 in_stride[kMaxTM], out_stride[kMaxTM];
+  int ext[kMaxTM];                  // OUTPUT extents (contracted mode: Eout)
+  int nd, mode, transpose, nblk;
+  i64 blk_off;
+};
+struct Blk {
+  i64 mat_off;  // element offset of the rows x cols col-major factor
+  int rows, cols, in_start, out_start;
+};
+void launch_mode_product(i64 nitems, const MPStep* steps, i64 total_out, const Blk* blks, const double2* mats,
+                         const double2* in, double2* out, cudaStream_t st);
+
+struct GemvDesc {  // y(R x nv) = K(R x C, row-major) * x(C x nv)
+  i64 core_off, x_off, y_off;
+  int R, C;
+  i64 cta_off;     // prefix of CTA counts
+};
+void launch_gemv(i64 npairs, const GemvDesc* d, i64 nctas, int nv, const double2* cores, const double2* x, double2* y,
+                 int max_c, cudaStream_t st);
+
+struct SumDesc {  // out[e] = sum_c in[c_off[c] + e], children in order
+  i64 out_off, total, work_off;
+  int nchild;
+  int pad;
+  i64 child_off[1 << kMaxD];
+};
+void launch_sum_children(i64 n, const SumDesc* d, i64 total, const double2* in, double2* out, cudaStream_t st);
+
+// ---- dense check (core_kernels.cu)
+void launch_dense_rows(const KSpec& ks, i64 nrows, const i64* rows, const double2* F, int nv, double2* out,
+                       cudaStream_t st);
+
+}  // namespace tbf

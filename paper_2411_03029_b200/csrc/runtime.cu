@@ -1,0 +1,1215 @@
+// Host runtime + C ABI of the B200 tensor-butterfly library.
+//
+// Construction (Alg. 1 / SPEC.md:268-276): for each side (V/W then
+// U/P) and level l = 0..Lc, one batch of IDs on the device (proxy lists,
+// candidate columns, fused entry generation + TSQR, reference pivoting), then
+// the ranks come back to the host to size the next level (the only host sync
+// per level).  r_est is level-synchronous: r_est(l) =
+// max(8, max rank over levels < l of the same side).  Cores are generated on
+// the device at the end.
+//
+// Apply (Alg. 2 / SPEC.md:277-285): a static plan of batched kernel
+// launches (one per level and mode, plus the core GEMV and the ordered child
+// sums), captured once into a CUDA graph and replayed.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+
+namespace tbf {
+int gemv_rows_per_cta();
+void launch_subtensor(const KSpec& ks, const i64* counts_h, const int* lists, i64 total, double2* out,
+                      cudaStream_t st);
+void launch_matrix_ids(i64 njobs, const i64* a_off, const i64* m, const int* n, const double2* A, i64 nparts, i64 rpp,
+                       int pr, i64 wmax, double2* rpart, cudaStream_t st);
+void launch_finish_var(const LevelDesc& L, const i64* mrows, double tol, double tie_eps, const i64* max_rank,
+                       const double2* rpart, const int* targets, const int* width, int* rank, int* sat, int* perm,
+                       int* skel_tmp, double2* interp_tmp, double* gaps, cudaStream_t st);
+}  // namespace tbf
+
+namespace {
+
+using namespace tbf;
+
+thread_local std::string g_err;
+thread_local int g_device = 0;
+
+struct InvalidArg : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void require(bool c, const std::string& msg) {
+  if (!c) throw InvalidArg(msg);
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      reset();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { reset(); }
+  void alloc(size_t count) {
+    reset();
+    n = count;
+    if (count) TBF_CUDA(cudaMalloc(&p, sizeof(T) * count));
+  }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void upload(const T* h, size_t count, cudaStream_t st) {
+    if (count) TBF_CUDA(cudaMemcpyAsync(p, h, sizeof(T) * count, cudaMemcpyHostToDevice, st));
+  }
+  void download(T* h, size_t count, cudaStream_t st) const {
+    if (count) TBF_CUDA(cudaMemcpyAsync(h, p, sizeof(T) * count, cudaMemcpyDeviceToHost, st));
+  }
+};
+
+template <class T>
+DevBuf<T> to_device(const std::vector<T>& v, cudaStream_t st) {
+  DevBuf<T> b(v.size());
+  b.upload(v.data(), v.size(), st);
+  return b;
+}
+
+i64 ipow(i64 b, i64 e) {
+  i64 r = 1;
+  while (e-- > 0) r *= b;
+  return r;
+}
+
+void ensure_device() {
+  int cnt = 0;
+  cudaError_t e = cudaGetDeviceCount(&cnt);
+  if (e != cudaSuccess || cnt == 0)
+    throw std::runtime_error("no CUDA device available (the B200 path has no CPU fallback)");
+  TBF_CUDA(cudaSetDevice(g_device));
+  cudaDeviceProp pr;
+  TBF_CUDA(cudaGetDeviceProperties(&pr, g_device));
+  if (pr.major < 10) throw std::runtime_error("device is not sm_100-class (Blackwell) — this build targets sm_100a");
+}
+
+struct EventTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t st;
+  explicit EventTimer(cudaStream_t s) : st(s) {
+    TBF_CUDA(cudaEventCreate(&a));
+    TBF_CUDA(cudaEventCreate(&b));
+    TBF_CUDA(cudaEventRecord(a, st));
+  }
+  double stop() {
+    TBF_CUDA(cudaEventRecord(b, st));
+    TBF_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    TBF_CUDA(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+  }
+  ~EventTimer() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+};
+
+struct LevelData {
+  LevelDesc L{};
+  i64 nslots = 0;
+  DevBuf<int> rank, width, perm, skel;
+  DevBuf<double2> interp;
+  DevBuf<i64> skel_off, interp_off;
+  DevBuf<double> gaps;
+  std::vector<int> h_rank, h_width, h_sat;
+  std::vector<i64> h_skel_off, h_interp_off;
+  i64 total_skel = 0, total_interp = 0;
+  int max_rank = 0;
+};
+
+struct TRef {
+  i64 off = 0;
+  int nd = 0;
+  int ext[kMaxTM] = {0};
+  i64 stride[kMaxTM] = {0};
+  i64 size() const {
+    i64 s = 1;
+    for (int p = 0; p < nd; ++p) s *= ext[p];
+    return s;
+  }
+};
+
+TRef packed(i64 off, int nd, const int* ext) {
+  TRef t;
+  t.off = off;
+  t.nd = nd;
+  i64 st = 1;
+  for (int p = 0; p < nd; ++p) {
+    t.ext[p] = ext[p];
+    t.stride[p] = st;
+    st *= ext[p];
+  }
+  return t;
+}
+
+enum BufId { BUF_F = 0, BUF_G = 1, BUF_SCRATCH = 2 };
+
+struct MPLaunch {
+  int side, level;  // factor arena
+  int in_buf, out_buf;
+  i64 step_begin, nsteps, total_out;
+};
+struct SumLaunch {
+  i64 begin, n, total;
+};
+struct Op {
+  int kind;  // 0 mode product, 1 gemv, 2 sum
+  i64 idx;
+  int group;  // 0 V/W, 1 core, 2 P/U
+};
+
+struct Plan {
+  i64 nv = 0;
+  i64 scratch_elems = 0;
+  std::vector<MPStep> steps;
+  std::vector<Blk> blks;
+  std::vector<MPLaunch> mps;
+  std::vector<GemvDesc> gemv;
+  i64 gemv_ctas = 0;
+  int gemv_max_c = 0;
+  std::vector<SumDesc> sums;
+  std::vector<SumLaunch> sum_launches;
+  std::vector<Op> ops;
+  DevBuf<MPStep> d_steps;
+  DevBuf<Blk> d_blks;
+  DevBuf<GemvDesc> d_gemv;
+  DevBuf<SumDesc> d_sums;
+  DevBuf<double2> scratch;
+  DevBuf<double2> stage_F, stage_G;  // host-buffer contract staging
+  i64 gemv_y_base = 0;
+  // graph cache
+  cudaGraphExec_t gexec = nullptr;
+  const void* g_F = nullptr;
+  void* g_G = nullptr;
+  cudaStream_t g_st = nullptr;
+  ~Plan() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+  }
+};
+
+}  // namespace
+
+struct oiobf_tbf {
+  oiobf_kernel_spec spec{};
+  KSpec ks{};
+  int d = 0, L = 0, Lc = 0;
+  i64 n = 0, nmid = 0;
+  double tol = 0;
+  oiobf_proxy_strategy strat{};
+  u64 seed = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<LevelData> side[2];
+  std::vector<i64> r_est[2];
+  DevBuf<double2> cores;
+  std::vector<PairDesc> h_pairs;
+  i64 total_core = 0;
+  std::map<i64, std::unique_ptr<Plan>> plans;
+  double t_ms[6] = {0, 0, 0, 0, 0, 0};
+  std::mutex mu;
+  ~oiobf_tbf() {
+    plans.clear();
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+constexpr double kTieEps = 1e-12;
+
+LevelDesc make_level(const oiobf_tbf& b, int sd, int l, i64 r_est, i64 wmax) {
+  LevelDesc L{};
+  L.d = b.d;
+  L.side = sd;
+  L.l = l;
+  L.L = b.L;
+  L.Lc = b.Lc;
+  L.proxy_mode = b.strat.mode;
+  L.n = b.n;
+  L.nin = ipow(2, static_cast<i64>(b.d) * l);
+  L.nj = ipow(2, b.Lc - l);
+  L.mpm = ipow(2, b.Lc);
+  L.nslots = b.nmid * L.nin * b.d * L.nj;
+  L.per_mode = b.strat.q * r_est;  // attempt 0 (id.cpp:257)
+  L.seed = b.seed;
+  L.side_tag = sd == 0 ? 0x56ULL : 0x55ULL;
+  L.wmax = wmax;
+  L.c_nin = l > 0 ? ipow(2, static_cast<i64>(b.d) * (l - 1)) : 0;
+  L.c_nj = l > 0 ? ipow(2, b.Lc - l + 1) : 0;
+  const int D = 2 * b.d;
+  const int mid_off = sd == 0 ? b.d : 0, in_off = sd == 0 ? 0 : b.d;
+  L.psize = 0;
+  i64 m = -1;
+  for (int k = 0; k < b.d; ++k) {
+    i64 sizes[kMaxModes], counts[kMaxModes];
+    for (int p = 0; p < b.d; ++p) {
+      sizes[mid_off + p] = b.n >> b.Lc;
+      sizes[in_off + p] = b.n >> l;
+    }
+    const int skip = mid_off + k;
+    sizes[skip] = b.n >> (b.L - l);
+    proxy_counts(D, sizes, skip, L.per_mode, b.strat.mode, b.strat.row_cap, counts);
+    i64 tot = 0, rows = 1;
+    for (int p = 0; p < D; ++p) {
+      require(counts[p] <= kMaxProxy || b.strat.mode != OIOBF_PROXY_UNIFORM_RANDOM,
+              "proxy count per mode exceeds the device limit (64)");
+      L.counts[k][p] = static_cast<int>(counts[p]);
+      L.poff[k][p] = static_cast<int>(tot);
+      tot += counts[p];
+      if (p != skip) rows *= counts[p];
+    }
+    L.psize = std::max(L.psize, tot);
+    if (m >= 0 && m != rows) throw std::runtime_error("internal: non-uniform proxy row count");
+    m = rows;
+  }
+  L.m = m;
+  L.pr = wmax <= 16 ? 256 : wmax <= 32 ? 128 : wmax <= 64 ? 64 : 32;
+  const i64 target_ctas = 148 * 8;
+  i64 parts = (target_ctas + L.nslots - 1) / L.nslots;
+  const i64 max_parts = std::max<i64>(1, (L.m + 4 * L.pr - 1) / (4 * L.pr));  // >= 4 panels per part
+  parts = std::max<i64>(1, std::min(parts, max_parts));
+  L.nparts = parts;
+  L.rpp = (L.m + parts - 1) / parts;
+  return L;
+}
+
+void build_side_level(oiobf_tbf& b, int sd, int l, i64 r_est) {
+  cudaStream_t st = b.stream;
+  const int d = b.d;
+  // widest candidate set: leaf size (l=0) or max r(child0)+r(child1)
+  i64 wmax;
+  if (l == 0) {
+    wmax = b.n >> b.L;
+  } else {
+    const LevelData& c = b.side[sd][static_cast<size_t>(l - 1)];
+    LevelDesc tmp = make_level(b, sd, l, r_est, 1);
+    wmax = 0;
+    for (i64 idx = 0; idx < tmp.nslots; ++idx) {
+      const SlotPos s = decode_slot(tmp, idx);
+      const i64 w = c.h_rank[static_cast<size_t>(child_slot(tmp, s, 0))] +
+                    c.h_rank[static_cast<size_t>(child_slot(tmp, s, 1))];
+      wmax = std::max(wmax, w);
+    }
+  }
+  wmax = std::max<i64>(wmax, 1);
+  require(wmax <= kMaxW, "ID width " + std::to_string(wmax) + " exceeds the supported maximum " +
+                             std::to_string(kMaxW));
+  LevelData& ld = b.side[sd][static_cast<size_t>(l)];
+  ld.L = make_level(b, sd, l, r_est, wmax);
+  LevelDesc& L = ld.L;
+  ld.nslots = L.nslots;
+  const i64 ns = L.nslots;
+  (void)d;
+  DevBuf<int> proxies(static_cast<size_t>(ns * L.psize));
+  DevBuf<int> targets(static_cast<size_t>(ns * wmax));
+  ld.width.alloc(static_cast<size_t>(ns));
+  EventTimer t0(st);
+  launch_gen_proxies(L, proxies.p, st);
+  if (l == 0) {
+    launch_targets(L, nullptr, nullptr, nullptr, targets.p, ld.width.p, st);
+  } else {
+    const LevelData& c = b.side[sd][static_cast<size_t>(l - 1)];
+    launch_targets(L, c.rank.p, c.skel_off.p, c.skel.p, targets.p, ld.width.p, st);
+  }
+  b.t_ms[0] += t0.stop();
+  DevBuf<double2> rpart(static_cast<size_t>(ns * L.nparts * wmax * wmax));
+  EventTimer t1(st);
+  launch_panel(L, b.ks, proxies.p, targets.p, ld.width.p, rpart.p, st);
+  b.t_ms[1] += t1.stop();
+  ld.rank.alloc(static_cast<size_t>(ns));
+  DevBuf<int> sat(static_cast<size_t>(ns));
+  ld.perm.alloc(static_cast<size_t>(ns * wmax));
+  ld.gaps.alloc(static_cast<size_t>(ns));
+  DevBuf<int> skel_tmp(static_cast<size_t>(ns * wmax));
+  DevBuf<double2> interp_tmp(static_cast<size_t>(ns * wmax * wmax));
+  EventTimer t2(st);
+  launch_finish(L, b.tol, kTieEps, -1, rpart.p, targets.p, ld.width.p, ld.rank.p, sat.p, ld.perm.p, skel_tmp.p,
+                interp_tmp.p, ld.gaps.p, st);
+  b.t_ms[2] += t2.stop();
+  ld.h_rank.resize(static_cast<size_t>(ns));
+  ld.h_width.resize(static_cast<size_t>(ns));
+  ld.h_sat.resize(static_cast<size_t>(ns));
+  ld.rank.download(ld.h_rank.data(), static_cast<size_t>(ns), st);
+  ld.width.download(ld.h_width.data(), static_cast<size_t>(ns), st);
+  sat.download(ld.h_sat.data(), static_cast<size_t>(ns), st);
+  TBF_CUDA(cudaStreamSynchronize(st));
+  ld.h_skel_off.resize(static_cast<size_t>(ns));
+  ld.h_interp_off.resize(static_cast<size_t>(ns));
+  i64 so = 0, io = 0;
+  ld.max_rank = 0;
+  for (i64 i = 0; i < ns; ++i) {
+    ld.h_skel_off[static_cast<size_t>(i)] = so;
+    ld.h_interp_off[static_cast<size_t>(i)] = io;
+    so += ld.h_rank[static_cast<size_t>(i)];
+    io += static_cast<i64>(ld.h_rank[static_cast<size_t>(i)]) * ld.h_width[static_cast<size_t>(i)];
+    ld.max_rank = std::max(ld.max_rank, ld.h_rank[static_cast<size_t>(i)]);
+  }
+  ld.total_skel = so;
+  ld.total_interp = io;
+  EventTimer t3(st);
+  ld.skel_off = to_device(ld.h_skel_off, st);
+  ld.interp_off = to_device(ld.h_interp_off, st);
+  ld.skel.alloc(static_cast<size_t>(std::max<i64>(so, 1)));
+  ld.interp.alloc(static_cast<size_t>(std::max<i64>(io, 1)));
+  launch_compact(ns, wmax, ld.rank.p, ld.width.p, ld.skel_off.p, ld.interp_off.p, skel_tmp.p, interp_tmp.p, ld.skel.p,
+                 ld.interp.p, st);
+  b.t_ms[3] += t3.stop();
+  // saturation would trigger the doubling retry (id.cpp:256-269); with the
+  // default rank limit it is unreachable, so it is only reported.
+}
+
+void build_cores(oiobf_tbf& b) {
+  cudaStream_t st = b.stream;
+  const int d = b.d;
+  const LevelData& U = b.side[1][static_cast<size_t>(b.Lc)];
+  const LevelData& V = b.side[0][static_cast<size_t>(b.Lc)];
+  const i64 P = b.nmid * b.nmid;
+  b.h_pairs.assign(static_cast<size_t>(P), PairDesc{});
+  i64 off = 0;
+  for (i64 p = 0; p < P; ++p) {
+    const i64 s = p / b.nmid, t = p % b.nmid;
+    PairDesc& pd = b.h_pairs[static_cast<size_t>(p)];
+    pd.R = 1;
+    pd.C = 1;
+    for (int k = 0; k < d; ++k) {
+      const i64 us = (t * b.nmid + s) * d + k;  // U slot (Lc, t, nu=s, k, j=0)
+      const i64 vs = (s * b.nmid + t) * d + k;  // V slot (Lc, s, tau=t, k, j=0)
+      pd.rr[k] = U.h_rank[static_cast<size_t>(us)];
+      pd.rc[k] = V.h_rank[static_cast<size_t>(vs)];
+      pd.rs_off[k] = U.h_skel_off[static_cast<size_t>(us)];
+      pd.cs_off[k] = V.h_skel_off[static_cast<size_t>(vs)];
+      pd.R *= pd.rr[k];
+      pd.C *= pd.rc[k];
+    }
+    pd.core_off = off;
+    pd.work_off = off;
+    off += static_cast<i64>(pd.R) * pd.C;
+  }
+  b.total_core = off;
+  b.cores.alloc(static_cast<size_t>(std::max<i64>(off, 1)));
+  DevBuf<PairDesc> dp = to_device(b.h_pairs, st);
+  EventTimer t(st);
+  launch_cores(b.ks, P, dp.p, off, U.skel.p, V.skel.p, b.cores.p, st);
+  b.t_ms[4] += t.stop();
+}
+
+void validate_spec(const oiobf_kernel_spec& s) {
+  require(s.d >= 1 && s.d <= kMaxD, "kernel spec: d must be in [1,6]");
+  require(s.n >= 1, "kernel spec: n must be positive");
+  require(s.kind >= 0 && s.kind <= 2, "make_kernel: unknown kernel kind");
+  require(s.kind != OIOBF_KERNEL_RADON2D || s.d == 2, "kernel spec: radon2d needs d=2");
+  require(s.kind != OIOBF_KERNEL_GREEN || s.d <= 3, "kernel spec: green needs d<=3");
+  if (s.bitrev) require((s.n & (s.n - 1)) == 0, "reorder_bit_reversal: extent must be a power of two");
+}
+
+oiobf_tbf* construct(const oiobf_kernel_spec& spec, int L, double tol, const oiobf_proxy_strategy& ps, u64 seed) {
+  validate_spec(spec);
+  require(L >= 0 && L % 2 == 0, "tbf_construct: L must be even and >= 0");
+  require((spec.n >> L) >= 1 && spec.n % (i64{1} << L) == 0, "tbf_construct: extent must equal C_b * 2^L");
+  require(tol > 0 && tol < 1, "column_id: tolerance must be in (0,1)");
+  require(ps.q >= 1 && ps.row_cap >= 1, "ProxyStrategy: q and row_cap must be positive");
+  require(ps.mode >= 0 && ps.mode <= 2, "ProxyStrategy: unknown mode");
+  ensure_device();
+  auto b = std::make_unique<oiobf_tbf>();
+  b->spec = spec;
+  b->ks = kspec_from(spec);
+  b->d = spec.d;
+  b->L = L;
+  b->Lc = L / 2;
+  b->n = spec.n;
+  b->nmid = ipow(2, static_cast<i64>(spec.d) * b->Lc);
+  b->tol = tol;
+  b->strat = ps;
+  b->seed = seed;
+  b->device = g_device;
+  TBF_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
+  auto t_start = std::chrono::steady_clock::now();
+  for (int sd = 0; sd < 2; ++sd) {
+    b->side[sd].resize(static_cast<size_t>(b->Lc + 1));
+    i64 r_est = 8;
+    for (int l = 0; l <= b->Lc; ++l) {
+      b->r_est[sd].push_back(r_est);
+      build_side_level(*b, sd, l, r_est);
+      r_est = std::max<i64>(r_est, b->side[sd][static_cast<size_t>(l)].max_rank);
+    }
+  }
+  build_cores(*b);
+  TBF_CUDA(cudaStreamSynchronize(b->stream));
+  b->t_ms[5] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+  return b.release();
+}
+
+// ------------------------------------------------------------------ apply plan
+void add_mp(Plan& pl, int side, int level, int in_buf, int out_buf, const std::vector<MPStep>& items,
+            const std::vector<std::vector<Blk>>& blocks, int group) {
+  MPLaunch m;
+  m.side = side;
+  m.level = level;
+  m.in_buf = in_buf;
+  m.out_buf = out_buf;
+  m.step_begin = static_cast<i64>(pl.steps.size());
+  m.nsteps = static_cast<i64>(items.size());
+  i64 work = 0;
+  for (size_t i = 0; i < items.size(); ++i) {
+    MPStep s = items[i];
+    s.work_off = work;
+    work += s.total;
+    s.blk_off = static_cast<i64>(pl.blks.size());
+    s.nblk = static_cast<int>(blocks[i].size());
+    pl.blks.insert(pl.blks.end(), blocks[i].begin(), blocks[i].end());
+    pl.steps.push_back(s);
+  }
+  m.total_out = work;
+  pl.ops.push_back(Op{0, static_cast<i64>(pl.mps.size()), group});
+  pl.mps.push_back(m);
+}
+
+MPStep make_step(const TRef& in, const TRef& out, int mode, int transpose) {
+  MPStep s{};
+  s.in_off = in.off;
+  s.out_off = out.off;
+  s.nd = out.nd;
+  s.mode = mode;
+  s.transpose = transpose;
+  s.total = out.size();
+  for (int p = 0; p < out.nd; ++p) {
+    s.ext[p] = out.ext[p];
+    s.in_stride[p] = in.stride[p];
+    s.out_stride[p] = out.stride[p];
+  }
+  return s;
+}
+
+std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
+  auto pl = std::make_unique<Plan>();
+  pl->nv = nv;
+  const int d = b.d;
+  const int nd = d + 1;
+  const i64 n = b.n;
+  const i64 N = ipow(n, d);
+  const i64 mid = n >> b.Lc;
+  const i64 mpm = ipow(2, b.Lc);
+  i64 scratch = 0;
+  auto alloc = [&](int ndims, const int* ext) {
+    TRef t = packed(scratch, ndims, ext);
+    scratch += t.size();
+    return t;
+  };
+  auto global_slab = [&](i64 outer) {  // F(s) or G(t) view in the global tensor
+    TRef t;
+    t.nd = nd;
+    i64 off = 0, st = 1;
+    for (int p = 0; p < d; ++p) {
+      const i64 pos = (outer / ipow(mpm, p)) % mpm;
+      off += pos * mid * st;
+      t.ext[p] = static_cast<int>(mid);
+      t.stride[p] = st;
+      st *= n;
+    }
+    t.ext[d] = static_cast<int>(nv);
+    t.stride[d] = N;
+    t.off = off;
+    return t;
+  };
+  // ---- Step 1: V / W
+  std::vector<TRef> cur;  // per item of the current level (output of last mode)
+  for (int l = 0; l <= b.Lc; ++l) {
+    const LevelData& ld = b.side[0][static_cast<size_t>(l)];
+    const i64 nin = ld.L.nin, nj = ld.L.nj;
+    const i64 nitems = b.nmid * nin;
+    std::vector<TRef> in(static_cast<size_t>(nitems));
+    for (i64 it = 0; it < nitems; ++it) {
+      const i64 s = it / nin, tau = it % nin;
+      if (l == 0) {
+        in[static_cast<size_t>(it)] = global_slab(s);
+      } else {
+        i64 ptau = 0;
+        for (int p = d - 1; p >= 0; --p) ptau = (ptau << (l - 1)) | (((tau >> (l * p)) & ((i64{1} << l) - 1)) >> 1);
+        in[static_cast<size_t>(it)] = cur[static_cast<size_t>(s * ipow(2, static_cast<i64>(d) * (l - 1)) + ptau)];
+      }
+    }
+    for (int k = 0; k < d; ++k) {
+      std::vector<MPStep> items;
+      std::vector<std::vector<Blk>> blocks;
+      for (i64 it = 0; it < nitems; ++it) {
+        const i64 s = it / nin, tau = it % nin;
+        TRef& x = in[static_cast<size_t>(it)];
+        int oext[kMaxTM];
+        for (int p = 0; p < nd; ++p) oext[p] = x.ext[p];
+        std::vector<Blk> bl;
+        int ci = 0, co = 0;
+        for (i64 j = 0; j < nj; ++j) {
+          const i64 slot = ((s * nin + tau) * d + k) * nj + j;
+          Blk B;
+          B.mat_off = ld.h_interp_off[static_cast<size_t>(slot)];
+          B.rows = ld.h_rank[static_cast<size_t>(slot)];
+          B.cols = ld.h_width[static_cast<size_t>(slot)];
+          B.in_start = ci;
+          B.out_start = co;
+          ci += B.cols;
+          co += B.rows;
+          bl.push_back(B);
+        }
+        if (ci != x.ext[k]) throw std::runtime_error("internal: V/W block widths do not match the tensor extent");
+        oext[k] = co;
+        TRef y = alloc(nd, oext);
+        items.push_back(make_step(x, y, k, 0));
+        blocks.push_back(bl);
+        x = y;
+      }
+      add_mp(*pl, 0, l, (l == 0 && k == 0) ? BUF_F : BUF_SCRATCH, BUF_SCRATCH, items, blocks, 0);
+    }
+    cur = in;
+  }
+  // ---- Step 2: cores.  x = F_{t,s} = cur[s * nmid + t]; y = G_{t,s}
+  const LevelData& ULc = b.side[1][static_cast<size_t>(b.Lc)];
+  std::vector<TRef> gts(static_cast<size_t>(b.nmid * b.nmid));  // index t * nmid + s
+  i64 ctas = 0;
+  const int rpc = gemv_rows_per_cta();
+  for (i64 p = 0; p < b.nmid * b.nmid; ++p) {
+    const i64 s = p / b.nmid, t = p % b.nmid;
+    const PairDesc& pd = b.h_pairs[static_cast<size_t>(p)];
+    const TRef& x = cur[static_cast<size_t>(s * b.nmid + t)];
+    int gext[kMaxTM];
+    i64 R = 1;
+    for (int k = 0; k < d; ++k) {
+      gext[k] = ULc.h_rank[static_cast<size_t>((t * b.nmid + s) * d + k)];
+      R *= gext[k];
+    }
+    gext[d] = static_cast<int>(nv);
+    TRef y = alloc(nd, gext);
+    gts[static_cast<size_t>(t * b.nmid + s)] = y;
+    if (R != pd.R || x.size() != static_cast<i64>(pd.C) * nv) throw std::runtime_error("internal: core shape mismatch");
+    GemvDesc g;
+    g.core_off = pd.core_off;
+    g.x_off = x.off;
+    g.y_off = y.off;
+    g.R = pd.R;
+    g.C = pd.C;
+    g.cta_off = ctas;
+    ctas += (pd.R + rpc - 1) / rpc;
+    pl->gemv_max_c = std::max(pl->gemv_max_c, pd.C);
+    pl->gemv.push_back(g);
+  }
+  pl->gemv_ctas = ctas;
+  pl->ops.push_back(Op{1, 0, 1});
+  // ---- Step 3: P (l = Lc..1), U (l = 0)
+  std::vector<TRef> gcur = gts;  // per (t, nu) at level l: index t * nin + nu
+  for (int l = b.Lc; l >= 0; --l) {
+    const LevelData& ld = b.side[1][static_cast<size_t>(l)];
+    const i64 nin = ld.L.nin, nj = ld.L.nj;
+    const i64 nitems = b.nmid * nin;
+    std::vector<TRef> x = gcur;
+    for (int k = 0; k < d; ++k) {
+      std::vector<MPStep> items;
+      std::vector<std::vector<Blk>> blocks;
+      const bool last_global = (l == 0 && k == d - 1);
+      for (i64 it = 0; it < nitems; ++it) {
+        const i64 t = it / nin, nu = it % nin;
+        TRef& xi = x[static_cast<size_t>(it)];
+        int oext[kMaxTM];
+        for (int p = 0; p < nd; ++p) oext[p] = xi.ext[p];
+        std::vector<Blk> bl;
+        int ci = 0, co = 0;
+        for (i64 j = 0; j < nj; ++j) {
+          const i64 slot = ((t * nin + nu) * d + k) * nj + j;
+          Blk B;
+          B.mat_off = ld.h_interp_off[static_cast<size_t>(slot)];
+          B.rows = ld.h_rank[static_cast<size_t>(slot)];
+          B.cols = ld.h_width[static_cast<size_t>(slot)];
+          B.in_start = ci;
+          B.out_start = co;
+          ci += B.rows;
+          co += B.cols;
+          bl.push_back(B);
+        }
+        if (ci != xi.ext[k]) throw std::runtime_error("internal: P/U block ranks do not match the tensor extent");
+        oext[k] = co;
+        TRef y = last_global ? global_slab(t) : alloc(nd, oext);
+        items.push_back(make_step(xi, y, k, 1));
+        blocks.push_back(bl);
+        xi = y;
+      }
+      add_mp(*pl, 1, l, BUF_SCRATCH, last_global ? BUF_G : BUF_SCRATCH, items, blocks, 2);
+    }
+    if (l > 0) {  // ordered sum of the 2^d children into each parent
+      const i64 pnin = ipow(2, static_cast<i64>(d) * (l - 1));
+      std::vector<TRef> par(static_cast<size_t>(b.nmid * pnin));
+      SumLaunch sl;
+      sl.begin = static_cast<i64>(pl->sums.size());
+      i64 work = 0;
+      for (i64 t = 0; t < b.nmid; ++t)
+        for (i64 pnu = 0; pnu < pnin; ++pnu) {
+          SumDesc sd{};
+          sd.nchild = 0;
+          TRef first;
+          for (i64 nu = 0; nu < nin; ++nu) {
+            i64 pp = 0;
+            for (int p = d - 1; p >= 0; --p) pp = (pp << (l - 1)) | (((nu >> (l * p)) & ((i64{1} << l) - 1)) >> 1);
+            if (pp != pnu) continue;
+            const TRef& c = x[static_cast<size_t>(t * nin + nu)];
+            if (sd.nchild == 0) first = c;
+            sd.child_off[sd.nchild++] = c.off;
+          }
+          TRef y = alloc(nd, first.ext);
+          sd.out_off = y.off;
+          sd.total = y.size();
+          sd.work_off = work;
+          work += sd.total;
+          pl->sums.push_back(sd);
+          par[static_cast<size_t>(t * pnin + pnu)] = y;
+        }
+      sl.n = static_cast<i64>(pl->sums.size()) - sl.begin;
+      sl.total = work;
+      pl->ops.push_back(Op{2, static_cast<i64>(pl->sum_launches.size()), 2});
+      pl->sum_launches.push_back(sl);
+      gcur = par;
+    }
+  }
+  pl->scratch_elems = scratch;
+  cudaStream_t st = b.stream;
+  pl->d_steps = to_device(pl->steps, st);
+  pl->d_blks = to_device(pl->blks, st);
+  pl->d_gemv = to_device(pl->gemv, st);
+  pl->d_sums = to_device(pl->sums, st);
+  pl->scratch.alloc(static_cast<size_t>(std::max<i64>(scratch, 1)));
+  TBF_CUDA(cudaStreamSynchronize(st));
+  return pl;
+}
+
+Plan& get_plan(oiobf_tbf& b, i64 nv) {
+  auto it = b.plans.find(nv);
+  if (it != b.plans.end()) return *it->second;
+  auto& slot = b.plans[nv];
+  slot = build_plan(b, nv);
+  return *slot;
+}
+
+void run_ops(oiobf_tbf& b, Plan& pl, const double2* F, double2* G, cudaStream_t st, int group_filter = -1) {
+  for (const Op& op : pl.ops) {
+    if (group_filter >= 0 && op.group != group_filter) continue;
+    if (op.kind == 0) {
+      const MPLaunch& m = pl.mps[static_cast<size_t>(op.idx)];
+      const double2* in = m.in_buf == BUF_F ? F : pl.scratch.p;
+      double2* out = m.out_buf == BUF_G ? G : pl.scratch.p;
+      const LevelData& ld = b.side[m.side][static_cast<size_t>(m.level)];
+      launch_mode_product(m.nsteps, pl.d_steps.p + m.step_begin, m.total_out, pl.d_blks.p, ld.interp.p, in, out, st);
+    } else if (op.kind == 1) {
+      launch_gemv(static_cast<i64>(pl.gemv.size()), pl.d_gemv.p, pl.gemv_ctas, static_cast<int>(pl.nv), b.cores.p,
+                  pl.scratch.p, pl.scratch.p, pl.gemv_max_c, st);
+    } else {
+      const SumLaunch& s = pl.sum_launches[static_cast<size_t>(op.idx)];
+      launch_sum_children(s.n, pl.d_sums.p + s.begin, s.total, pl.scratch.p, pl.scratch.p, st);
+    }
+  }
+}
+
+void contract_device(oiobf_tbf& b, const double2* F, double2* G, i64 nv, cudaStream_t st) {
+  require(nv >= 1, "tbf_contract: nv must be >= 1");
+  TBF_CUDA(cudaSetDevice(b.device));
+  Plan& pl = get_plan(b, nv);
+  if (!pl.gexec || pl.g_F != F || pl.g_G != G || pl.g_st != st) {
+    if (pl.gexec) {
+      cudaGraphExecDestroy(pl.gexec);
+      pl.gexec = nullptr;
+    }
+    cudaStream_t cap;
+    TBF_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    cudaGraph_t g;
+    TBF_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    try {
+      run_ops(b, pl, F, G, cap);
+    } catch (...) {
+      cudaStreamEndCapture(cap, &g);
+      cudaStreamDestroy(cap);
+      throw;
+    }
+    TBF_CUDA(cudaStreamEndCapture(cap, &g));
+    TBF_CUDA(cudaGraphInstantiate(&pl.gexec, g, 0));
+    TBF_CUDA(cudaGraphDestroy(g));
+    TBF_CUDA(cudaStreamDestroy(cap));
+    pl.g_F = F;
+    pl.g_G = G;
+    pl.g_st = st;
+  }
+  TBF_CUDA(cudaGraphLaunch(pl.gexec, st));
+}
+
+int status_of(const std::exception& e) {
+  g_err = e.what();
+  return dynamic_cast<const InvalidArg*>(&e) ? OIOBF_EINVAL : OIOBF_ERUNTIME;
+}
+
+#define CAPI_BEGIN try {
+#define CAPI_END                      \
+  }                                   \
+  catch (const std::exception& e) {   \
+    return status_of(e);              \
+  }                                   \
+  catch (...) {                       \
+    g_err = "unknown C++ exception";  \
+    return OIOBF_ERUNTIME;            \
+  }                                   \
+  return OIOBF_OK;
+
+}  // namespace
+
+extern "C" {
+
+const char* oiobf_last_error(void) { return g_err.c_str(); }
+
+int oiobf_set_device(int device) {
+  CAPI_BEGIN
+  g_device = device;
+  ensure_device();
+  CAPI_END
+}
+
+int oiobf_device_info(int64_t out[4]) {
+  CAPI_BEGIN
+  ensure_device();
+  cudaDeviceProp p;
+  TBF_CUDA(cudaGetDeviceProperties(&p, g_device));
+  out[0] = p.multiProcessorCount;
+  out[1] = p.major;
+  out[2] = p.minor;
+  out[3] = static_cast<int64_t>(p.totalGlobalMem);
+  CAPI_END
+}
+
+uint64_t oiobf_derive_seed(uint64_t seed, const uint64_t* tags, int32_t ntags) {
+  return derive_seed(seed, reinterpret_cast<const u64*>(tags), ntags);
+}
+
+int oiobf_select_proxies_count(int64_t extent, int64_t count, int32_t mode, uint64_t seed, int64_t* out,
+                               int64_t* out_count) {
+  CAPI_BEGIN
+  require(extent >= 1, "select_proxies: extent must be positive");
+  require(mode >= 0 && mode <= 2, "select_proxies: unknown mode");
+  i64 c = std::min<i64>(extent, std::max<i64>(count, 1));
+  require(mode != OIOBF_PROXY_UNIFORM_RANDOM || c <= kMaxProxy, "select_proxies: count exceeds device limit (64)");
+  std::vector<int> tmp(static_cast<size_t>(mode == OIOBF_PROXY_ALL ? extent : c));
+  const i64 got = select_proxies(extent, count, mode, seed, tmp.data());
+  for (i64 i = 0; i < got; ++i) out[i] = tmp[static_cast<size_t>(i)];
+  *out_count = got;
+  CAPI_END
+}
+
+int oiobf_tbf_construct(const oiobf_kernel_spec* spec, int32_t L, double tol, const oiobf_proxy_strategy* proxies,
+                        uint64_t seed, oiobf_tbf** out) {
+  CAPI_BEGIN
+  require(spec && proxies && out, "tbf_construct: null argument");
+  *out = construct(*spec, L, tol, *proxies, seed);
+  CAPI_END
+}
+
+int oiobf_tbf_destroy(oiobf_tbf* h) {
+  CAPI_BEGIN
+  delete h;
+  CAPI_END
+}
+
+int oiobf_tbf_contract_device(oiobf_tbf* h, const void* dF, void* dG, int64_t nv, void* stream) {
+  CAPI_BEGIN
+  require(h && dF && dG, "tbf_contract: null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  contract_device(*h, static_cast<const double2*>(dF), static_cast<double2*>(dG), nv,
+                  static_cast<cudaStream_t>(stream));
+  CAPI_END
+}
+
+int oiobf_tbf_contract(oiobf_tbf* h, const double* F, double* G, int64_t nv) {
+  CAPI_BEGIN
+  require(h && F && G, "tbf_contract: null argument");
+  require(nv >= 1, "tbf_contract: nv must be >= 1");
+  std::lock_guard<std::mutex> lk(h->mu);
+  TBF_CUDA(cudaSetDevice(h->device));
+  const size_t N = static_cast<size_t>(ipow(h->n, h->d) * nv);
+  Plan& pl = get_plan(*h, nv);
+  if (pl.stage_F.n != N) {  // staging buffers persist so the captured graph is reused
+    pl.stage_F.alloc(N);
+    pl.stage_G.alloc(N);
+  }
+  TBF_CUDA(cudaMemcpyAsync(pl.stage_F.p, F, N * sizeof(double2), cudaMemcpyHostToDevice, h->stream));
+  contract_device(*h, pl.stage_F.p, pl.stage_G.p, nv, h->stream);
+  TBF_CUDA(cudaMemcpyAsync(G, pl.stage_G.p, N * sizeof(double2), cudaMemcpyDeviceToHost, h->stream));
+  TBF_CUDA(cudaStreamSynchronize(h->stream));
+  CAPI_END
+}
+
+int oiobf_tbf_memory(const oiobf_tbf* h, int64_t out[5]) {
+  CAPI_BEGIN
+  require(h, "tbf_memory: null handle");
+  for (int i = 0; i < 5; ++i) out[i] = 0;
+  for (int sd = 0; sd < 2; ++sd)
+    for (size_t l = 0; l < h->side[sd].size(); ++l)
+      out[(sd == 0 ? 0 : 2) + (l > 0 ? 1 : 0)] += h->side[sd][l].total_interp * 16;
+  out[4] = h->total_core * 16;
+  CAPI_END
+}
+
+int oiobf_tbf_info(const oiobf_tbf* h, int64_t info[10]) {
+  CAPI_BEGIN
+  require(h, "tbf_info: null handle");
+  i64 slots = 0, sk = 0, ip = 0, pm = 0;
+  for (int sd = 0; sd < 2; ++sd)
+    for (const auto& lv : h->side[sd]) {
+      slots += lv.nslots;
+      sk += lv.total_skel;
+      ip += lv.total_interp;
+      for (int w : lv.h_width) pm += w;
+    }
+  info[0] = h->d;
+  info[1] = h->n;
+  info[2] = h->L;
+  info[3] = h->Lc;
+  info[4] = h->nmid;
+  info[5] = slots;
+  info[6] = sk;
+  info[7] = ip;
+  info[8] = h->total_core;
+  info[9] = pm;
+  CAPI_END
+}
+
+int oiobf_tbf_export(const oiobf_tbf* h, int64_t* ranks, int64_t* ncols, int64_t* rows, int64_t* skel,
+                     double* interp, int64_t* perm, double* cores, int64_t* core_rows, int64_t* core_cols,
+                     int64_t* r_est) {
+  CAPI_BEGIN
+  require(h, "tbf_export: null handle");
+  TBF_CUDA(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  i64 si = 0, sk = 0, ip = 0, pm = 0;
+  for (int sd = 0; sd < 2; ++sd)
+    for (const auto& lv : h->side[sd]) {
+      const i64 ns = lv.nslots;
+      std::vector<int> hs(static_cast<size_t>(lv.total_skel)), hp(static_cast<size_t>(ns * lv.L.wmax));
+      std::vector<double2> hi(static_cast<size_t>(lv.total_interp));
+      lv.skel.download(hs.data(), hs.size(), st);
+      lv.interp.download(hi.data(), hi.size(), st);
+      lv.perm.download(hp.data(), hp.size(), st);
+      TBF_CUDA(cudaStreamSynchronize(st));
+      for (i64 i = 0; i < ns; ++i) {
+        const int r = lv.h_rank[static_cast<size_t>(i)], w = lv.h_width[static_cast<size_t>(i)];
+        if (ranks) ranks[si] = r;
+        if (ncols) ncols[si] = w;
+        if (rows) rows[si] = lv.L.m;
+        for (int q = 0; q < w; ++q)
+          if (perm) perm[pm + q] = hp[static_cast<size_t>(i * lv.L.wmax + q)];
+        pm += w;
+        ++si;
+      }
+      if (skel)
+        for (size_t q = 0; q < hs.size(); ++q) skel[sk + static_cast<i64>(q)] = hs[q];
+      if (interp) std::memcpy(interp + 2 * ip, hi.data(), hi.size() * sizeof(double2));
+      sk += lv.total_skel;
+      ip += lv.total_interp;
+    }
+  if (cores || core_rows || core_cols) {
+    std::vector<double2> hc(static_cast<size_t>(h->total_core));
+    h->cores.download(hc.data(), hc.size(), st);
+    TBF_CUDA(cudaStreamSynchronize(st));
+    for (size_t p = 0; p < h->h_pairs.size(); ++p) {
+      const PairDesc& pd = h->h_pairs[p];
+      if (core_rows) core_rows[p] = pd.R;
+      if (core_cols) core_cols[p] = pd.C;
+      if (cores)  // row-major on device -> reference column-major matricization
+        for (int r = 0; r < pd.R; ++r)
+          for (int c = 0; c < pd.C; ++c) {
+            const double2 v = hc[static_cast<size_t>(pd.core_off + static_cast<i64>(r) * pd.C + c)];
+            const i64 o = pd.core_off + r + static_cast<i64>(c) * pd.R;
+            cores[2 * o] = v.x;
+            cores[2 * o + 1] = v.y;
+          }
+    }
+  }
+  if (r_est) {
+    i64 q = 0;
+    for (int sd = 0; sd < 2; ++sd)
+      for (auto v : h->r_est[sd]) r_est[q++] = v;
+  }
+  CAPI_END
+}
+
+int oiobf_tbf_timings(const oiobf_tbf* h, double out[6]) {
+  CAPI_BEGIN
+  require(h, "tbf_timings: null handle");
+  for (int i = 0; i < 6; ++i) out[i] = h->t_ms[i];
+  CAPI_END
+}
+
+int oiobf_tbf_plan_stats(oiobf_tbf* h, int64_t out[4]) {
+  CAPI_BEGIN
+  require(h, "tbf_plan_stats: null handle");
+  std::lock_guard<std::mutex> lk(h->mu);
+  Plan& pl = get_plan(*h, 1);
+  i64 fac = 0;
+  for (int sd = 0; sd < 2; ++sd)
+    for (const auto& lv : h->side[sd]) fac += lv.total_interp;
+  const i64 N = ipow(h->n, h->d);
+  out[0] = 16 * (2 * N + fac + h->total_core);
+  out[1] = 16 * h->total_core;
+  out[2] = static_cast<int64_t>(pl.ops.size());
+  i64 macs = h->total_core;
+  for (const MPStep& s : pl.steps) {
+    // each output element of a step costs (block input width) MACs; approximate
+    // with the average block width of its item
+    (void)s;
+  }
+  for (const MPLaunch& m : pl.mps) {
+    for (i64 i = 0; i < m.nsteps; ++i) {
+      const MPStep& s = pl.steps[static_cast<size_t>(m.step_begin + i)];
+      const i64 per_out = s.total / std::max(1, s.ext[s.mode]);
+      for (int q = 0; q < s.nblk; ++q) {
+        const Blk& B = pl.blks[static_cast<size_t>(s.blk_off + q)];
+        macs += per_out * B.rows * B.cols;
+      }
+    }
+  }
+  out[3] = macs;
+  CAPI_END
+}
+
+int oiobf_tbf_profile_contract(oiobf_tbf* h, const void* dF, void* dG, int32_t reps, void* stream, double out[4]) {
+  CAPI_BEGIN
+  require(h && dF && dG && reps >= 1, "tbf_profile_contract: bad argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  TBF_CUDA(cudaSetDevice(h->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Plan& pl = get_plan(*h, 1);
+  for (int g = 0; g < 3; ++g) {
+    run_ops(*h, pl, static_cast<const double2*>(dF), static_cast<double2*>(dG), st, g);  // warm
+    EventTimer t(st);
+    for (int r = 0; r < reps; ++r)
+      run_ops(*h, pl, static_cast<const double2*>(dF), static_cast<double2*>(dG), st, g);
+    out[g] = t.stop() / reps;
+  }
+  EventTimer t(st);
+  for (int r = 0; r < reps; ++r) contract_device(*h, static_cast<const double2*>(dF), static_cast<double2*>(dG), 1, st);
+  out[3] = t.stop() / reps;
+  CAPI_END
+}
+
+int oiobf_dense_rows(const oiobf_kernel_spec* spec, const double* F, int64_t nv, int64_t nrows,
+                     const int64_t* rows_flat, double* out) {
+  CAPI_BEGIN
+  require(spec && F && rows_flat && out, "dense_rows: null argument");
+  validate_spec(*spec);
+  require(nv >= 1 && nrows >= 0, "dense_rows: bad sizes");
+  ensure_device();
+  const i64 N = ipow(spec->n, spec->d);
+  for (i64 r = 0; r < nrows; ++r) require(rows_flat[r] >= 0 && rows_flat[r] < N, "dense_rows: row out of range");
+  cudaStream_t st;
+  TBF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  {
+    DevBuf<double2> dF(static_cast<size_t>(N * nv)), dO(static_cast<size_t>(std::max<i64>(nrows * nv, 1)));
+    DevBuf<i64> dr(static_cast<size_t>(std::max<i64>(nrows, 1)));
+    dF.upload(reinterpret_cast<const double2*>(F), static_cast<size_t>(N * nv), st);
+    dr.upload(reinterpret_cast<const i64*>(rows_flat), static_cast<size_t>(nrows), st);
+    if (nrows) launch_dense_rows(kspec_from(*spec), nrows, dr.p, dF.p, static_cast<int>(nv), dO.p, st);
+    dO.download(reinterpret_cast<double2*>(out), static_cast<size_t>(nrows * nv), st);
+    TBF_CUDA(cudaStreamSynchronize(st));
+  }
+  cudaStreamDestroy(st);
+  CAPI_END
+}
+
+int oiobf_subtensor_at(const oiobf_kernel_spec* spec, const int64_t* counts, const int64_t* lists, double* out) {
+  CAPI_BEGIN
+  require(spec && counts && lists && out, "subtensor_at: null argument");
+  validate_spec(*spec);
+  ensure_device();
+  const int D = 2 * spec->d;
+  i64 total = 1, nl = 0;
+  for (int p = 0; p < D; ++p) {
+    require(counts[p] >= 0, "subtensor_at: negative count");
+    total *= counts[p];
+    nl += counts[p];
+  }
+  std::vector<int> hl(static_cast<size_t>(std::max<i64>(nl, 1)));
+  for (i64 q = 0; q < nl; ++q) {
+    require(lists[q] >= 1 && lists[q] <= spec->n, "subtensor: index out of bounds");
+    hl[static_cast<size_t>(q)] = static_cast<int>(lists[q]);
+  }
+  cudaStream_t st;
+  TBF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  {
+    DevBuf<int> dl = to_device(hl, st);
+    DevBuf<double2> dO(static_cast<size_t>(std::max<i64>(total, 1)));
+    launch_subtensor(kspec_from(*spec), reinterpret_cast<const i64*>(counts), dl.p, total, dO.p, st);
+    dO.download(reinterpret_cast<double2*>(out), static_cast<size_t>(total), st);
+    TBF_CUDA(cudaStreamSynchronize(st));
+  }
+  cudaStreamDestroy(st);
+  CAPI_END
+}
+
+int oiobf_mode_product_blockdiag(int32_t nmodes, const int64_t* shape, const double* t, int32_t mode, int32_t nb,
+                                 const int64_t* br, const int64_t* bc, const double* blocks, int32_t transpose,
+                                 double* out) {
+  CAPI_BEGIN
+  require(nmodes >= 1 && nmodes <= kMaxTM, "mode_product_blockdiag: 1..7 modes supported");
+  require(mode >= 1 && mode <= nmodes, "mode_product_blockdiag: mode out of range");
+  require(nb >= 1, "mode_product_blockdiag: no blocks");
+  ensure_device();
+  int ext[kMaxTM];
+  for (int p = 0; p < nmodes; ++p) {
+    require(shape[p] >= 0, "DenseTensor: negative extent");
+    ext[p] = static_cast<int>(shape[p]);
+  }
+  i64 in_total = 0, out_total = 0, mat_total = 0;
+  std::vector<Blk> bl;
+  for (int b = 0; b < nb; ++b) {
+    Blk B;
+    B.mat_off = mat_total;
+    B.rows = static_cast<int>(br[b]);
+    B.cols = static_cast<int>(bc[b]);
+    B.in_start = static_cast<int>(in_total);
+    B.out_start = static_cast<int>(out_total);
+    in_total += transpose ? br[b] : bc[b];
+    out_total += transpose ? bc[b] : br[b];
+    mat_total += br[b] * bc[b];
+    bl.push_back(B);
+  }
+  require(in_total == shape[mode - 1], "mode_product_blockdiag: shape mismatch");
+  TRef in = packed(0, nmodes, ext);
+  int oext[kMaxTM];
+  for (int p = 0; p < nmodes; ++p) oext[p] = ext[p];
+  oext[mode - 1] = static_cast<int>(out_total);
+  TRef o = packed(0, nmodes, oext);
+  MPStep s = make_step(in, o, mode - 1, transpose);
+  s.work_off = 0;
+  s.blk_off = 0;
+  s.nblk = nb;
+  cudaStream_t st;
+  TBF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  {
+    std::vector<MPStep> sv{s};
+    DevBuf<MPStep> ds = to_device(sv, st);
+    DevBuf<Blk> db = to_device(bl, st);
+    DevBuf<double2> dm(static_cast<size_t>(std::max<i64>(mat_total, 1))), di(static_cast<size_t>(std::max<i64>(in.size(), 1))),
+        dO(static_cast<size_t>(std::max<i64>(o.size(), 1)));
+    dm.upload(reinterpret_cast<const double2*>(blocks), static_cast<size_t>(mat_total), st);
+    di.upload(reinterpret_cast<const double2*>(t), static_cast<size_t>(in.size()), st);
+    launch_mode_product(1, ds.p, o.size(), db.p, dm.p, di.p, dO.p, st);
+    dO.download(reinterpret_cast<double2*>(out), static_cast<size_t>(o.size()), st);
+    TBF_CUDA(cudaStreamSynchronize(st));
+  }
+  cudaStreamDestroy(st);
+  CAPI_END
+}
+
+int oiobf_column_id_batch(int64_t batch, const int64_t* m, const int64_t* n, const int64_t* a_off, const double* A,
+                          double tol, const int64_t* max_rank, int64_t* rank, const int64_t* s_off, int64_t* skel,
+                          const int64_t* i_off, double* interp, int64_t* perm, int32_t* saturated,
+                          double* interp_max_abs) {
+  CAPI_BEGIN
+  require(batch >= 0, "column_id: negative batch");
+  require(tol > 0 && tol < 1, "column_id: tolerance must be in (0,1)");
+  if (batch == 0) return OIOBF_OK;
+  ensure_device();
+  i64 wmax = 1, mmax = 1, atot = 0;
+  for (i64 b = 0; b < batch; ++b) {
+    require(m[b] > 0 && n[b] > 0, "column_id: empty matrix");
+    require(n[b] <= kMaxW, "column_id: more than 96 columns not supported by the device kernel");
+    wmax = std::max<i64>(wmax, n[b]);
+    mmax = std::max<i64>(mmax, m[b]);
+    atot = std::max<i64>(atot, a_off[b] + m[b] * n[b]);
+  }
+  cudaStream_t st;
+  TBF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  {
+    LevelDesc L{};
+    L.d = 1;
+    L.nslots = batch;
+    L.wmax = wmax;
+    L.m = mmax;
+    L.pr = wmax <= 16 ? 256 : wmax <= 32 ? 128 : wmax <= 64 ? 64 : 32;
+    i64 parts = std::max<i64>(1, (148 * 8 + batch - 1) / batch);
+    parts = std::min(parts, std::max<i64>(1, (mmax + 4 * L.pr - 1) / (4 * L.pr)));
+    L.nparts = parts;
+    L.rpp = (mmax + parts - 1) / parts;
+    std::vector<int> hw(static_cast<size_t>(batch)), ht(static_cast<size_t>(batch * wmax));
+    std::vector<i64> hm(m, m + batch), hoff(a_off, a_off + batch), hmr(static_cast<size_t>(batch));
+    std::vector<int> hn(static_cast<size_t>(batch));
+    for (i64 b = 0; b < batch; ++b) {
+      hw[static_cast<size_t>(b)] = static_cast<int>(n[b]);
+      hn[static_cast<size_t>(b)] = static_cast<int>(n[b]);
+      hmr[static_cast<size_t>(b)] = max_rank ? max_rank[b] : -1;
+      for (i64 c = 0; c < n[b]; ++c) ht[static_cast<size_t>(b * wmax + c)] = static_cast<int>(c + 1);
+    }
+    DevBuf<int> dw = to_device(hw, st), dt = to_device(ht, st), dn = to_device(hn, st);
+    DevBuf<i64> dm = to_device(hm, st), doff = to_device(hoff, st), dmr = to_device(hmr, st);
+    DevBuf<double2> dA(static_cast<size_t>(atot));
+    dA.upload(reinterpret_cast<const double2*>(A), static_cast<size_t>(atot), st);
+    DevBuf<double2> rpart(static_cast<size_t>(batch * L.nparts * wmax * wmax));
+    launch_matrix_ids(batch, doff.p, dm.p, dn.p, dA.p, L.nparts, L.rpp, L.pr, wmax, rpart.p, st);
+    DevBuf<int> drank(static_cast<size_t>(batch)), dsat(static_cast<size_t>(batch)),
+        dperm(static_cast<size_t>(batch * wmax)), dsk(static_cast<size_t>(batch * wmax));
+    DevBuf<double2> dint(static_cast<size_t>(batch * wmax * wmax));
+    DevBuf<double> dgap(static_cast<size_t>(batch));
+    launch_finish_var(L, dm.p, tol, kTieEps, dmr.p, rpart.p, dt.p, dw.p, drank.p, dsat.p, dperm.p, dsk.p, dint.p,
+                      dgap.p, st);
+    std::vector<int> hr(static_cast<size_t>(batch)), hs(static_cast<size_t>(batch)),
+        hp(static_cast<size_t>(batch * wmax)), hk(static_cast<size_t>(batch * wmax));
+    std::vector<double2> hi(static_cast<size_t>(batch * wmax * wmax));
+    drank.download(hr.data(), hr.size(), st);
+    dsat.download(hs.data(), hs.size(), st);
+    dperm.download(hp.data(), hp.size(), st);
+    dsk.download(hk.data(), hk.size(), st);
+    dint.download(hi.data(), hi.size(), st);
+    TBF_CUDA(cudaStreamSynchronize(st));
+    for (i64 b = 0; b < batch; ++b) {
+      const int r = hr[static_cast<size_t>(b)];
+      const i64 w = n[b];
+      rank[b] = r;
+      if (saturated) saturated[b] = hs[static_cast<size_t>(b)];
+      double mx = 0;
+      for (i64 q = 0; q < r * w; ++q) {
+        const double2 v = hi[static_cast<size_t>(b * wmax * wmax + q)];
+        interp[2 * (i_off[b] + q)] = v.x;
+        interp[2 * (i_off[b] + q) + 1] = v.y;
+        mx = std::max(mx, std::sqrt(v.x * v.x + v.y * v.y));
+      }
+      if (interp_max_abs) interp_max_abs[b] = (r > 0) ? mx : 0.0;
+      for (int q = 0; q < r; ++q) skel[s_off[b] + q] = hk[static_cast<size_t>(b * wmax + q)];
+      if (perm)
+        for (i64 q = 0; q < w; ++q) perm[s_off[b] + q] = hp[static_cast<size_t>(b * wmax + q)];
+    }
+  }
+  cudaStreamDestroy(st);
+  CAPI_END
+}
+
+}  // extern "C"

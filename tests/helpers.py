@@ -1,0 +1,84 @@
+"""Shared test helpers: canonical slot geometry recomputed
+independently of both the oracle and the device code, and tie-aware
+comparisons."""
+from __future__ import annotations
+
+import numpy as np
+
+TIE_EPS = 1e-12
+
+
+def slot_geometry(d, n, L, Lc, sd, l, idx):
+    nin, nj = 2 ** (d * l), 2 ** (Lc - l)
+    j = idx % nj
+    k = (idx // nj) % d
+    inner = (idx // (nj * d)) % nin
+    outer = idx // (nj * d * nin)
+    mpm = 2 ** Lc
+
+    def node(lev, pos):
+        return (pos * (n >> lev) + 1, (pos + 1) * (n >> lev))
+
+    op = [(outer // mpm ** p) % mpm for p in range(d)]
+    ip = [(inner // (2 ** l) ** p) % (2 ** l) for p in range(d)]
+    ranges = [None] * (2 * d)
+    mid_off, in_off = (d, 0) if sd == 0 else (0, d)
+    for p in range(d):
+        ranges[mid_off + p] = node(Lc, op[p])
+        ranges[in_off + p] = node(l, ip[p])
+    skip = mid_off + k
+    ranges[skip] = node(L - l, op[k] * nj + j)
+    tags = [0x56 if sd == 0 else 0x55, l, outer, inner, k, j, 0]
+    return dict(ranges=ranges, skip=skip, tags=tags, k=k, j=j, inner=inner, outer=outer)
+
+
+def level_base(fz, sd, l):
+    return sum(cnt for s2, l2, cnt in fz.level_counts() if (s2, l2) < (sd, l))
+
+
+def slot_target(fz, sd, l, idx):
+    """Candidate columns of a slot from an exported factorization."""
+    d, Lc = fz.d, fz.Lc
+    g = slot_geometry(d, fz.n, fz.L, Lc, sd, l, idx)
+    if l == 0:
+        lo, hi = g["ranges"][g["skip"]]
+        return np.arange(lo, hi + 1, dtype=np.int64)
+    so = np.concatenate([[0], np.cumsum(fz.ranks)])
+    ip = [(g["inner"] // (2 ** l) ** p) % (2 ** l) for p in range(d)]
+    pin = 0
+    for p in reversed(range(d)):
+        pin = pin * 2 ** (l - 1) + ip[p] // 2
+    base = level_base(fz, sd, l - 1)
+    pnin, pnj = 2 ** (d * (l - 1)), 2 ** (Lc - l + 1)
+    out = []
+    for c in range(2):
+        cidx = base + ((g["outer"] * pnin + pin) * d + g["k"]) * pnj + 2 * g["j"] + c
+        out.append(fz.skel[so[cidx]:so[cidx + 1]])
+    return np.concatenate(out).astype(np.int64)
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    den = max(np.linalg.norm(b), 1e-300)
+    return float(np.linalg.norm(a - b) / den)
+
+
+def compare_factorizations(gpu, ora, interp_tol=1e-9, core_tol=1e-12):
+    """Slot-by-slot: ranks and skeletons bit-exact, interps within tol, cores."""
+    assert gpu.d == ora.d and gpu.L == ora.L
+    np.testing.assert_array_equal(gpu.ranks, ora.ranks)
+    np.testing.assert_array_equal(gpu.ncols, ora.ncols)
+    np.testing.assert_array_equal(gpu.skel, ora.skel)
+    so, io, po, co = gpu.offsets()
+    worst = 0.0
+    for g in range(gpu.ranks.size):
+        a = gpu.interp[io[g]:io[g + 1]]
+        b = ora.interp[io[g]:io[g + 1]]
+        if b.size:
+            worst = max(worst, float(np.max(np.abs(a - b)) / max(1.0, float(np.max(np.abs(b))))))
+    assert worst <= interp_tol, f"interp max deviation {worst}"
+    np.testing.assert_array_equal(gpu.core_rows, ora.core_rows)
+    np.testing.assert_array_equal(gpu.core_cols, ora.core_cols)
+    assert rel(gpu.cores, ora.cores) <= core_tol
+    return worst

@@ -1,0 +1,249 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star): skeletons / ranks bit-exact wherever pivots
+are not tied within 1e-12 (ties replayed); apply within 1e-10
+relative L2 of the oracle's apply; both within tolerance of direct dense sums.
+"""
+import numpy as np
+import pytest
+
+import paper_2411_03029_b200 as tb
+from paper_2411_03029_b200.configs import BY_NAME, dft, green_cubes, green_plates, radon2d
+
+from helpers import TIE_EPS, compare_factorizations, rel, slot_geometry, slot_target
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    from paper_2411_03029_b200.build import build
+    build()
+    tb._lib.load()
+
+
+def rand_c(rng, shape):
+    return (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)) / np.sqrt(2)
+
+
+# ------------------------------------------------------------------ primitives
+def test_column_id_matches_oracle(oracle):
+    rng = np.random.default_rng(10)
+    mats = []
+    for _ in range(30):
+        m = int(rng.integers(1, 3000))
+        n = int(rng.integers(1, 48))
+        r = int(rng.integers(1, min(m, n) + 1))
+        U = rand_c(rng, (m, r)) * (0.3 ** np.arange(r))
+        mats.append(U @ rand_c(rng, (r, n)))
+    mats.append(np.eye(5, dtype=complex))
+    for tol in (1e-4, 1e-8):
+        got = tb.column_id_batch(mats, tol)
+        for A, g in zip(mats, got):
+            o = oracle.column_id(A, tol, forced_perm=g.perm, forced_rank=g.rank, tie_eps=TIE_EPS)
+            assert not o["mismatch"], "GPU pivot/rank differs from oracle outside a tie"
+            assert g.rank == o["rank"]
+            np.testing.assert_array_equal(g.skeleton, o["skeleton"])
+            # T = R11^{-1} R12 is only determined to ~eps*cond(R11) (cond up to
+            # 1/tol here); the well-posed quantity is the interpolation itself:
+            # A(:, skel) @ interp must agree to rounding level.
+            if g.rank:
+                Ask = A[:, g.skeleton - 1]
+                d = np.linalg.norm(Ask @ (g.interp - o["interp"])) / np.linalg.norm(A)
+                assert d <= 1e-12, f"interpolation differs by {d:.2e}"
+            assert not g.saturated
+
+
+def test_column_id_max_rank_and_errors(oracle):
+    rng = np.random.default_rng(11)
+    A = rand_c(rng, (200, 10)) @ rand_c(rng, (10, 12))
+    g = tb.column_id(A, 1e-10, max_rank=4)
+    o = oracle.column_id(A, 1e-10, max_rank=4)
+    assert g.saturated and o["saturated"] and g.rank == 4
+    with pytest.raises(ValueError):
+        tb.column_id(A, 0.0)
+    with pytest.raises(ValueError):
+        tb.column_id(np.zeros((0, 3)), 1e-3)
+
+
+@pytest.mark.parametrize("spec", [green_plates(64), green_cubes(16), dft(3, 8), radon2d(64)],
+                         ids=lambda s: s.describe())
+def test_subtensor_entries(oracle, spec):
+    rng = np.random.default_rng(12)
+    lists = [np.sort(rng.choice(np.arange(1, spec.n + 1), size=4, replace=False)) for _ in range(2 * spec.d)]
+    got = tb.subtensor_at(spec, lists[:spec.d], lists[spec.d:])
+    ref = np.moveaxis(oracle.unfolding(spec, lists, 0).reshape([len(l) for l in lists[1:]] + [len(lists[0])],
+                                                                 order="F"), -1, 0)
+    assert rel(got, ref) < 1e-14
+
+
+def test_mode_product_blockdiag(oracle):
+    rng = np.random.default_rng(13)
+    for tr in (False, True):
+        T = rand_c(rng, (5, 6, 4, 2))
+        blocks = [rand_c(rng, (3, 2) if tr else (2, 3)), rand_c(rng, (1, 4) if tr else (4, 1)),
+                  rand_c(rng, (2, 2))]
+        # mode 3 has extent 4 = in-widths 3+1? choose widths to match
+        widths = [b.shape[0] if tr else b.shape[1] for b in blocks]
+        T = rand_c(rng, (5, 6, sum(widths), 2))
+        for mode in (3,):
+            g = tb.mode_product_blockdiag(T, mode, blocks, tr)
+            o = oracle.mode_product_blockdiag(T, mode, blocks, tr)
+            assert rel(g, o) < 1e-14
+
+
+def test_proxies_and_seeds(oracle):
+    rng = np.random.default_rng(14)
+    for _ in range(300):
+        extent = int(rng.integers(1, 1024))
+        count = int(rng.integers(0, 40))
+        mode = int(rng.integers(0, 3))
+        seed = int(rng.integers(0, 2**63))
+        np.testing.assert_array_equal(tb.select_proxies_count(extent, count, mode, seed),
+                                      oracle.select_proxies_count(extent, count, mode, seed))
+    for _ in range(50):
+        tags = [int(x) for x in rng.integers(0, 2**32, size=7)]
+        s = int(rng.integers(0, 2**63))
+        assert tb.derive_seed(s, tags) == oracle.derive_seed(s, tags)
+
+
+def test_dense_rows_matches_oracle(oracle):
+    spec = green_plates(32)
+    rng = np.random.default_rng(15)
+    F = rand_c(rng, (32, 32))
+    rows = rng.choice(32 * 32, 50, replace=False)
+    assert rel(tb.dense_rows(spec, F, rows), oracle.dense_rows(spec, F, rows)) < 1e-13
+
+
+# ------------------------------------------------------------------ butterfly
+CASES = [
+    ("plates32", green_plates(32), 1e-6, 2),
+    ("plates64_cfg1", BY_NAME["green_plates_n64"].spec, 1e-6, 2),
+    ("cubes16", green_cubes(16), 1e-4, 2),
+    ("cubes32", green_cubes(32), 1e-6, 2),
+    ("radon64", radon2d(64), 1e-6, 2),
+    ("dft2_16", dft(2, 16), 1e-8, 4),
+    ("dft3_8", dft(3, 8), 1e-8, 2),
+    ("plates64_L4", green_plates(64), 1e-4, 4),
+]
+
+
+@pytest.mark.parametrize("name,spec,tol,L", CASES, ids=[c[0] for c in CASES])
+def test_butterfly_parity(oracle, name, spec, tol, L):
+    bf = tb.tbf_construct(spec, L, tol, seed=3)
+    gz = bf.export()
+    tbo = oracle.tbf_construct(spec, L, tol, seed=3, replay=gz)
+    oz = tbo.export()
+    assert not np.any(oz.flags & 2), "oracle saw a non-tie disagreement with the GPU pivots/ranks"
+    assert not np.any(oz.flags & 1)
+    np.testing.assert_array_equal(gz.r_est, oz.r_est)
+    compare_factorizations(gz, oz)
+    # memory accounting
+    assert bf.memory() == tbo.memory()
+    # apply parity at 1e-10 (BASELINE north_star), nv = 1 and nv = 3
+    rng = np.random.default_rng(4)
+    for nv in (1, 3):
+        shape = (spec.n,) * spec.d + ((nv,) if nv > 1 else ())
+        F = rand_c(rng, shape)
+        g = bf.contract(F)
+        o = tbo.contract(F)
+        assert rel(g, o) < 1e-10, f"apply parity {rel(g, o)}"
+
+
+@pytest.mark.parametrize("name,spec,tol,L", CASES[:5], ids=[c[0] for c in CASES[:5]])
+def test_butterfly_dense_accuracy(oracle, name, spec, tol, L):
+    bf = tb.tbf_construct(spec, L, tol, seed=3)
+    rng = np.random.default_rng(5)
+    F = rand_c(rng, (spec.n,) * spec.d)
+    G = bf.contract(F).reshape(-1, order="F")
+    rows = rng.choice(spec.n ** spec.d, min(1000, spec.n ** spec.d), replace=False)
+    exact = tb.dense_rows(spec, F, rows)[:, 0]
+    err = rel(G[rows], exact)
+    # SPEC.md:452 gate is 10*tol (the paper's own errors exceed tol)
+    assert err <= 10 * tol, f"sampled relative error {err:.3e} > 10*tol"
+
+
+def test_contract_zero_and_linearity():
+    spec = green_plates(32)
+    bf = tb.tbf_construct(spec, 2, 1e-6, seed=1)
+    rng = np.random.default_rng(6)
+    Z = np.zeros((32, 32), complex)
+    assert np.all(bf.contract(Z) == 0)
+    A, B = rand_c(rng, (32, 32)), rand_c(rng, (32, 32))
+    a, b = 0.3 - 1.1j, 2.0 + 0.5j
+    lhs = bf.contract(a * A + b * B)
+    rhs = a * bf.contract(A) + b * bf.contract(B)
+    assert rel(lhs, rhs) < 1e-12
+
+
+def test_error_estimate_monotone():
+    spec = green_plates(32)
+    e2 = tb.tbf_error_estimate(tb.tbf_construct(spec, 2, 1e-2, seed=1), n_samples=5, seed=2)
+    e5 = tb.tbf_error_estimate(tb.tbf_construct(spec, 2, 1e-5, seed=1), n_samples=5, seed=2)
+    assert e5 < e2 and e5 <= 1e-4
+
+
+def test_invalid_arguments():
+    with pytest.raises(ValueError):
+        tb.tbf_construct(green_plates(64), 3, 1e-6)
+    with pytest.raises(ValueError):
+        tb.tbf_construct(green_plates(64), 2, 0.0)
+    with pytest.raises(ValueError):
+        tb.tbf_construct(green_plates(48), 6, 1e-3)
+
+
+# ------------------------------------------------- full-size configs (sampled)
+@pytest.mark.parametrize("cfg", ["green_plates_n64", "green_cubes_n64"])
+def test_full_config_sampled_slots(oracle, cfg):
+    """At BASELINE sizes: every rank/skeleton of a random sample of slots is
+    recomputed by the oracle from the same proxies and candidate columns."""
+    c = BY_NAME[cfg]
+    spec = c.spec
+    bf = tb.tbf_construct(spec, c.L, c.tol, seed=c.seed)
+    fz = bf.export()
+    so, io, po, _ = fz.offsets()
+    rng = np.random.default_rng(7)
+    for sd, l, cnt in fz.level_counts():
+        base = sum(x for s2, l2, x in fz.level_counts() if (s2, l2) < (sd, l))
+        r_est = int(fz.r_est[sd * (fz.Lc + 1) + l])
+        for idx in rng.choice(cnt, size=min(cnt, 4), replace=False):
+            g = base + int(idx)
+            geo = slot_geometry(fz.d, fz.n, fz.L, fz.Lc, sd, l, int(idx))
+            target = slot_target(fz, sd, l, int(idx))
+            lists = oracle.proxy_lists(geo["ranges"], geo["skip"], 3 * r_est,
+                                       seed=oracle.derive_seed(c.seed, geo["tags"]))
+            lists[geo["skip"]] = target
+            A = oracle.unfolding(spec, lists, geo["skip"])
+            assert A.shape[0] == fz.rows[g]
+            o = oracle.column_id(A, c.tol, forced_perm=fz.perm[po[g]:po[g + 1]], forced_rank=int(fz.ranks[g]))
+            assert not o["mismatch"]
+            assert o["rank"] == fz.ranks[g]
+            np.testing.assert_array_equal(target[o["skeleton"] - 1], fz.skel[so[g]:so[g + 1]])
+            gi = fz.interp[io[g]:io[g + 1]].reshape((fz.ranks[g], fz.ncols[g]), order="F")
+            assert np.max(np.abs(gi - o["interp"])) <= 1e-8 * max(1, np.max(np.abs(o["interp"])))
+
+
+@pytest.mark.parametrize("cfg,gate", [("green_plates_n64", 10), ("green_cubes_n64", 30)])
+def test_full_config_accuracy(oracle, cfg, gate):
+    """1000 sampled outputs vs direct dense sums (BASELINE check).  The error is
+    a property of the reference's proxy strategy: the GPU must
+    reproduce the oracle's error on the same factors; the ratio to tol is
+    reported and gated loosely."""
+    c = BY_NAME[cfg]
+    spec = c.spec
+    bf = tb.tbf_construct(spec, c.L, c.tol, seed=c.seed)
+    rng = np.random.default_rng(8)
+    F = rand_c(rng, (spec.n,) * spec.d)
+    G = bf.contract(F).reshape(-1, order="F")
+    rows = rng.choice(spec.n ** spec.d, 1000, replace=False)
+    exact = tb.dense_rows(spec, F, rows)[:, 0]
+    exact_cpu = oracle.dense_rows(spec, F, rows)[:, 0]
+    assert rel(exact, exact_cpu) < 1e-13
+    err = rel(G[rows], exact)
+    ob = oracle.tbf_import(spec, c.L, c.tol, bf.export())
+    Go = ob.contract(F).reshape(-1, order="F")
+    assert rel(G, Go) < 1e-10
+    err_o = rel(Go[rows], exact)
+    print(f"{cfg}: sampled rel err gpu {err:.3e} oracle {err_o:.3e} (tol {c.tol:g}, ratio {err / c.tol:.1f})")
+    assert abs(err - err_o) <= 1e-3 * err_o
+    assert err <= gate * c.tol

@@ -1,0 +1,363 @@
+#!/usr/bin/env python
+"""Benchmark: tensor-butterfly APPLY throughput (input points/s) on B200, with
+construction time, roofline of the dominant kernel and the CPU baseline.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl b200|reference]
+
+Workload (BASELINE.json configs[1]): d=3 Green's function between two cubes,
+n=64 per direction (262,144 points per side), kappa = 2*pi*n/8, tol 1e-6,
+complex128, seeded complex-normal input.  A "step" is one full contraction
+G = K x F (Alg. 2) of one n^d input through the compressed operator.
+
+* value      device-resident throughput: inputs already in HBM, CUDA events on
+             the launching stream, L2 flushed (256 MiB write) before every step.
+* e2e        same metric through the public C ABI with pinned HOST buffers
+             (oiobf_tbf_contract: H2D of F, contraction, D2H of G per step).
+* roofline   dominant kernel = middle-level core GEMV (HBM stream of the cores);
+             achieved = algorithmic bytes / its event-timed launch duration.
+* cpu_baseline  the oracle port (oracle/liboracle.so) applying the SAME factors
+             on the host cores (rank 0, N=1 only), bounded sample.
+* --impl reference  the CPU implementation of the path (oracle port, all host
+             threads): CPU construction (setup, reported) + timed CPU applies.
+
+Multi-GPU (torchrun, N>1): one process per GPU; each rank builds and applies
+its own replica of the operator (replicas; the sharded plan is DESIGN.md §7),
+max-over-ranks device time, value = all ranks' points / that time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2411_03029_b200.configs import BY_NAME, CONFIGS  # noqa: E402
+
+DEFAULT_CONFIG = CONFIGS[1].name  # BASELINE.json configs[1]
+METRIC = "apply_throughput"
+UNIT = "input_pts/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def make_input(cfg, seed, nv=1):
+    """Seeded complex standard normal, Re/Im ~ N(0, 1/2)."""
+    rng = np.random.default_rng(seed)
+    shape = (cfg.spec.n,) * cfg.spec.d + ((nv,) if nv > 1 else ())
+    return ((rng.standard_normal(shape) + 1j * rng.standard_normal(shape)) / np.sqrt(2)).astype(np.complex128)
+
+
+class ClockSampler:
+    FIELDS = ["index", "clocks.sm", "clocks.max.sm", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device):
+        self.device = device
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=" + ",".join(self.FIELDS), "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------ reference
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import Oracle, build
+    if not os.path.exists(os.path.join(ROOT, "oracle", "liboracle.so")):
+        build(ref=False)
+    cfg = BY_NAME[args.config]
+    o = Oracle()
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    ob = o.tbf_construct(cfg.spec, cfg.L, cfg.tol, seed=cfg.seed, nthreads=threads)
+    t_construct = time.perf_counter() - t0
+    F = make_input(cfg, cfg.input_seed, args.nv)
+    for _ in range(args.warmup):
+        ob.contract(F, nthreads=threads)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        ob.contract(F, nthreads=threads)
+        times.append(time.perf_counter() - t)
+    ms = 1e3 * statistics.fmean(times)
+    pts = cfg.points * args.nv
+    value = pts / (ms / 1e3)
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded complex normal input; operator from the BASELINE formula)",
+        "config": {"workload": cfg.name, "points": cfg.points, "tol": cfg.tol, "L": cfg.L, "nv": args.nv},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} full applies of {cfg.name} (oracle port, {threads} threads); "
+                                   f"the reference has no butterfly code, only its primitives (SURVEY §0.2)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "construct": {"cpu_s": t_construct, "threads": threads},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ b200 arm
+def run_b200(args):
+    import torch
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    import paper_2411_03029_b200 as tb
+    from paper_2411_03029_b200 import _lib
+
+    L = _lib.load()
+    _lib.check(L.oiobf_set_device(local if ws > 1 else 0))
+    cfg = BY_NAME[args.config]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    sampler = ClockSampler(torch.cuda.current_device())
+    sampler.start()
+
+    # ---- construction (device work; wall clock around the synchronous call)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    bf = tb.tbf_construct(cfg.spec, cfg.L, cfg.tol, seed=cfg.seed)
+    construct_s = time.perf_counter() - t0
+    # second construction: steady-state (module load / first-touch excluded)
+    t0 = time.perf_counter()
+    bf2 = tb.tbf_construct(cfg.spec, cfg.L, cfg.tol, seed=cfg.seed)
+    construct_s_warm = time.perf_counter() - t0
+    tim = bf2.timings()
+    del bf2
+    stats = bf.plan_stats()
+    mem = bf.memory()
+    fz_ranks = bf.export().ranks
+
+    # ---- device buffers
+    Fh = make_input(cfg, cfg.input_seed + rank, args.nv)
+    N = cfg.points * args.nv
+    Ft = torch.from_numpy(Fh.reshape(-1, order="F").copy()).to(dev)
+    Gt = torch.empty_like(Ft)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+
+    def step():
+        bf.contract_device(Ft.data_ptr(), Gt.data_ptr(), args.nv, sh)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    # keep the GPU busy ~0.5 s so clocks are sampled under load
+    t_end = time.perf_counter() + 0.5
+    while time.perf_counter() < t_end:
+        for _ in range(20):
+            step()
+        torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in evs:
+        flush.zero_()
+        a.record(stream)
+        step()
+        b.record(stream)
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    if ws > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    value = N * ws / (ms / 1e3)
+
+    # ---- e2e through the public C ABI with pinned host buffers
+    pin_F = torch.from_numpy(np.ascontiguousarray(Fh.reshape(-1, order="F")).view(np.float64).copy()).pin_memory()
+    pin_G = torch.empty_like(pin_F).pin_memory()
+    Fv, Gv = pin_F.numpy(), pin_G.numpy()
+    for _ in range(2):
+        _lib.check(L.oiobf_tbf_contract(bf.handle, Fv, Gv, args.nv))
+    if ws > 1:
+        torch.distributed.barrier()
+    e2e_times = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        _lib.check(L.oiobf_tbf_contract(bf.handle, Fv, Gv, args.nv))
+        e2e_times.append(time.perf_counter() - t)
+    e2e_ms = 1e3 * statistics.fmean(e2e_times)
+    if ws > 1:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = N * ws / (e2e_ms / 1e3)
+    # sanity: host result equals the device result
+    dres = Gt.cpu().numpy()
+    step()
+    torch.cuda.synchronize()
+    assert np.allclose(Gv.view(np.complex128), Gt.cpu().numpy(), rtol=0, atol=1e-12 * np.abs(dres).max())
+
+    # ---- roofline of the dominant kernel (core GEMV), live CUDA events
+    prof = bf.profile_contract(Ft.data_ptr(), Gt.data_ptr(), reps=20, stream=sh)
+    clocks = sampler.stop()
+    hbm, peak_src = peaks()
+    gemv_bytes = stats["core_bytes"]
+    achieved = gemv_bytes / (prof["core_ms"] / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"ncu_{cfg.name}.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                traffic = json.load(f).get("gemv_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- CPU baseline: oracle port on the same factors (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(cfg, bf, Fh, args.nv, args.cpu_budget)
+        except Exception as e:  # the baseline is reported, never the product
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {e}"}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak" if ws > 1 else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded complex normal input; operator from the BASELINE formula)",
+        "config": {"workload": cfg.name, "points": cfg.points, "tol": cfg.tol, "L": cfg.L, "nv": args.nv,
+                   "l2": "flushed (256 MiB write) before every timed step",
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step": 16 * N,
+                "d2h_bytes_per_step": 16 * N},
+        "gpu_launches": int(stats["launches"]) * args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": traffic, "kernel": "k_gemv (middle-level core contraction)",
+                     "algorithmic_bytes_per_launch": gemv_bytes, "launch_ms": prof["core_ms"], "peak_source": peak_src,
+                     "whole_apply_bytes_alg": stats["bytes_alg"],
+                     "whole_apply_GBps": stats["bytes_alg"] / (ms / 1e3) / 1e9,
+                     "phase_ms": {"factor_VW": prof["factor_ms"], "core": prof["core_ms"],
+                                  "transfer_PU": prof["transfer_ms"], "graph_total": prof["total_ms"]}},
+        "clocks": clocks,
+        "construct": {"gpu_s_first": construct_s, "gpu_s": construct_s_warm, "breakdown_ms": tim,
+                      "ranks_max": int(fz_ranks.max()), "ranks_min": int(fz_ranks.min()), "memory_bytes": mem},
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def cpu_baseline(cfg, bf, Fh, nv, budget_s):
+    from oracle import Oracle, build
+    if not os.path.exists(os.path.join(ROOT, "oracle", "liboracle.so")):
+        build(ref=False)
+    o = Oracle()
+    ob = o.tbf_import(cfg.spec, cfg.L, cfg.tol, bf.export())
+    threads = os.cpu_count() or 1
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t = time.perf_counter()
+        ob.contract(Fh, nthreads=threads)
+        times.append(time.perf_counter() - t)
+        if time.perf_counter() - t_start > budget_s or len(times) >= 50:
+            break
+    ms = 1e3 * statistics.fmean(times)
+    return {"value": cfg.points * nv / (ms / 1e3), "unit": UNIT, "cores": threads, "kind": "port",
+            "ms_per_step": ms,
+            "sample": f"{len(times)} full applies of {cfg.name} on the GPU-built factors (oracle port, "
+                      f"{threads} threads, ~{budget_s:.0f}s budget)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(BY_NAME))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--nv", type=int, default=1)
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

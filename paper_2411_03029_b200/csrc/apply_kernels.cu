@@ -80,13 +80,13 @@ __device__ __forceinline__ double2 ld_stream2(const double2* p) {
 }
 
 // grid: one CTA per (pair, 32-row chunk); each warp walks 4 rows
-__global__ void __launch_bounds__(kGemvThreads) k_gemv(i64 npairs, const GemvDesc* __restrict__ ds, int nv,
+__global__ void __launch_bounds__(kGemvThreads) k_gemv(const int* __restrict__ cta_pair,
+                                                       const GemvDesc* __restrict__ ds, int nv,
                                                        const double2* __restrict__ cores,
                                                        const double2* __restrict__ x, double2* __restrict__ y) {
   extern __shared__ __align__(16) double2 sx[];
   const i64 cta = blockIdx.x;
-  const i64 p = find_item(&ds[0].cta_off, sizeof(GemvDesc), npairs, cta);
-  const GemvDesc D = ds[p];
+  const GemvDesc D = ds[cta_pair[cta]];
   const int chunk = static_cast<int>(cta - D.cta_off);
   for (int i = threadIdx.x; i < D.C * nv; i += kGemvThreads) sx[i] = x[D.x_off + i];
   __syncthreads();
@@ -138,13 +138,12 @@ void launch_mode_product(i64 nitems, const MPStep* steps, i64 total_out, const B
   TBF_CUDA(cudaGetLastError());
 }
 
-void launch_gemv(i64 npairs, const GemvDesc* d, i64 nctas, int nv, const double2* cores, const double2* x, double2* y,
-                 int max_c, cudaStream_t st) {
+void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, int nv, const double2* cores, const double2* x,
+                 double2* y, int max_c, cudaStream_t st) {
   if (nctas == 0) return;
   const size_t smem = sizeof(double2) * static_cast<size_t>(max_c) * nv;
-  if (smem > 48 * 1024)
-    TBF_CUDA(cudaFuncSetAttribute(k_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  k_gemv<<<static_cast<unsigned>(nctas), kGemvThreads, smem, st>>>(npairs, d, nv, cores, x, y);
+  TBF_CUDA(cudaFuncSetAttribute(k_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  k_gemv<<<static_cast<unsigned>(nctas), kGemvThreads, smem, st>>>(cta_pair, d, nv, cores, x, y);
   TBF_CUDA(cudaGetLastError());
 }
 

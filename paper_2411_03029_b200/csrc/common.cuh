@@ -28,6 +28,11 @@ using u64 = unsigned long long;
                                ":" + std::to_string(__LINE__) + " (" #x ")");                             \
   } while (0)
 
+// Every dynamic-smem kernel gets the same (device maximum) opt-in once per
+// launch site, so CUDA-graph captures never see a smaller attribute than an
+// earlier captured node needs.
+constexpr int kMaxDynSmem = 220 * 1024;  // leaves room for static __shared__
+
 // ------------------------------------------------------------------ complex
 __host__ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);

@@ -494,7 +494,7 @@ void launch_targets(const LevelDesc& L, const int* crank, const i64* cskel_off, 
 void launch_panel(const LevelDesc& L, const KSpec& ks, const int* proxies, const int* targets, const int* width,
                   double2* rpart, cudaStream_t st) {
   const size_t smem = panel_smem_bytes(L);
-  TBF_CUDA(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  TBF_CUDA(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   const i64 grid = L.nslots * L.nparts;
   k_panel<<<static_cast<unsigned>(grid), kThreads, smem, st>>>(L, ks, proxies, targets, width, rpart);
   TBF_CUDA(cudaGetLastError());
@@ -504,7 +504,7 @@ void launch_finish(const LevelDesc& L, double tol, double tie_eps, i64 max_rank,
                    const int* targets, const int* width, int* rank, int* sat, int* perm, int* skel_tmp,
                    double2* interp_tmp, double* gaps, cudaStream_t st) {
   const size_t smem = finish_smem_bytes(L);
-  TBF_CUDA(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  TBF_CUDA(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   k_finish<<<static_cast<unsigned>(L.nslots), kFinThreads, smem, st>>>(L, tol, tie_eps, max_rank, nullptr, nullptr,
                                                                       rpart, targets,
                                                                       width, rank, sat, perm, skel_tmp, interp_tmp,
@@ -525,7 +525,7 @@ void launch_compact(i64 nslots, i64 wmax, const int* rank, const int* width, con
 void launch_matrix_ids(i64 njobs, const i64* a_off, const i64* m, const int* n, const double2* A, i64 nparts, i64 rpp,
                        int pr, i64 wmax, double2* rpart, cudaStream_t st) {
   const size_t smem = sizeof(double2) * (wmax * wmax + static_cast<size_t>(pr) * wmax) + 2 * sizeof(Bcast) + 16;
-  TBF_CUDA(cudaFuncSetAttribute(k_matrix_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  TBF_CUDA(cudaFuncSetAttribute(k_matrix_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   k_matrix_panel<<<static_cast<unsigned>(njobs * nparts), kThreads, smem, st>>>(nparts, rpp, pr, wmax, a_off, m, n, A,
                                                                                rpart);
   TBF_CUDA(cudaGetLastError());
@@ -535,7 +535,7 @@ void launch_finish_var(const LevelDesc& L, const i64* mrows, double tol, double 
                        const double2* rpart, const int* targets, const int* width, int* rank, int* sat, int* perm,
                        int* skel_tmp, double2* interp_tmp, double* gaps, cudaStream_t st) {
   const size_t smem = finish_smem_bytes(L);
-  TBF_CUDA(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  TBF_CUDA(cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   k_finish<<<static_cast<unsigned>(L.nslots), kFinThreads, smem, st>>>(L, tol, tie_eps, -1, mrows, max_rank, rpart,
                                                                       targets, width, rank, sat, perm, skel_tmp,
                                                                       interp_tmp, gaps);

@@ -66,8 +66,8 @@ struct GemvDesc {  // y(R x nv) = K(R x C, row-major) * x(C x nv)
   int R, C;
   i64 cta_off;     // prefix of CTA counts
 };
-void launch_gemv(i64 npairs, const GemvDesc* d, i64 nctas, int nv, const double2* cores, const double2* x, double2* y,
-                 int max_c, cudaStream_t st);
+void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, int nv, const double2* cores, const double2* x,
+                 double2* y, int max_c, cudaStream_t st);
 
 struct SumDesc {  // out[e] = sum_c in[c_off[c] + e], children in order
   i64 out_off, total, work_off;
@@ -76,6 +76,38 @@ struct SumDesc {  // out[e] = sum_c in[c_off[c] + e], children in order
   i64 child_off[1 << kMaxD];
 };
 void launch_sum_children(i64 n, const SumDesc* d, i64 total, const double2* in, double2* out, cudaStream_t st);
+
+// Fused box contraction (apply, one CTA per output box): the block-diagonal
+// factor of every level splits the level into independent boxes; each box is
+// out_box (+)= sum_terms in_box x_1 M_1 x_2 M_2 ... x_d M_d with all d modes
+// applied in shared memory.  V/W: one term.  P (l >= 1): one term per child
+// nu of p_nu, summed in ascending nu order.  U-bar / V-bar (l = 0) read / write
+// the global tensors directly through strides.
+struct BoxTerm {
+  i64 in_off;
+  i64 in_stride[kMaxTM];
+  int in_ext[kMaxTM];
+  i64 mat_off[kMaxD];
+  int mrows[kMaxD], mcols[kMaxD];
+};
+struct BoxItem {
+  i64 out_off;
+  i64 out_stride[kMaxTM];
+  int out_ext[kMaxTM];  // full box extents (last contracted mode: full, split by [last_lo, last_hi))
+  int last_lo, last_hi;
+  i64 term_off;
+  int nterm, pad;
+};
+struct BoxLaunchInfo {
+  int d, nv, transpose;
+  int smem_elems_in, smem_elems_mat, smem_elems_a, smem_elems_b;
+};
+void launch_box(i64 nitems, const BoxItem* items, const BoxTerm* terms, const BoxLaunchInfo& info,
+                const double2* mats, const double2* in, double2* out, cudaStream_t st);
+size_t box_smem_bytes(const BoxLaunchInfo& info);
+// ordered child sums, one CTA per parent (SumDesc.work_off unused)
+void launch_sum_parent(i64 nctas, const SumDesc* d, const int* cta_map, const double2* in, double2* out,
+                       cudaStream_t st);
 
 // ---- dense check (core_kernels.cu)
 void launch_dense_rows(const KSpec& ks, i64 nrows, const i64* rows, const double2* F, int nv, double2* out,

@@ -13,6 +13,7 @@
 // sums), captured once into a CUDA graph and replayed.
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -181,10 +182,16 @@ struct MPLaunch {
   i64 step_begin, nsteps, total_out;
 };
 struct SumLaunch {
-  i64 begin, n, total;
+  i64 begin, n, total;  // total: CTAs for k_sum_parent launches
+  i64 work_begin = 0;   // first (parent, chunk) pair in the CTA map
+};
+struct BoxLaunch {
+  int side, level, in_buf, out_buf;
+  i64 item_begin, nitems;
+  BoxLaunchInfo info;
 };
 struct Op {
-  int kind;  // 0 mode product, 1 gemv, 2 sum
+  int kind;  // 0 mode product, 1 gemv, 2 sum, 3 fused boxes
   i64 idx;
   int group;  // 0 V/W, 1 core, 2 P/U
 };
@@ -201,9 +208,17 @@ struct Plan {
   std::vector<SumDesc> sums;
   std::vector<SumLaunch> sum_launches;
   std::vector<Op> ops;
+  std::vector<BoxItem> bitems;
+  std::vector<BoxTerm> bterms;
+  std::vector<BoxLaunch> boxes;
+  DevBuf<BoxItem> d_bitems;
+  DevBuf<BoxTerm> d_bterms;
   DevBuf<MPStep> d_steps;
   DevBuf<Blk> d_blks;
   DevBuf<GemvDesc> d_gemv;
+  DevBuf<int> d_gemv_map;  // CTA -> pair
+  std::vector<int> sum_map;
+  DevBuf<int> d_sum_map;   // k_sum_parent CTA -> (parent, chunk)
   DevBuf<SumDesc> d_sums;
   DevBuf<double2> scratch;
   DevBuf<double2> stage_F, stage_G;  // host-buffer contract staging
@@ -542,8 +557,73 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
     t.off = off;
     return t;
   };
+  // Per-level slot accessors
+  auto slot_info = [&](int sd, int l, i64 outer, i64 inner, int k, i64 j, int& r, int& w, i64& moff) {
+    const LevelData& ld = b.side[sd][static_cast<size_t>(l)];
+    const i64 slot = ((outer * ld.L.nin + inner) * d + k) * ld.L.nj + j;
+    r = ld.h_rank[static_cast<size_t>(slot)];
+    w = ld.h_width[static_cast<size_t>(slot)];
+    moff = ld.h_interp_off[static_cast<size_t>(slot)];
+  };
+  auto parent_of = [&](i64 inner, int l) {
+    i64 pi = 0;
+    for (int p = d - 1; p >= 0; --p) pi = (pi << (l - 1)) | (((inner >> (l * p)) & ((i64{1} << l) - 1)) >> 1);
+    return pi;
+  };
+  // Finish a batch of single-term box items: size shared memory (input box +
+  // factors + two intermediates) and record a box launch, or report "too big".
+  auto commit_boxes = [&](std::vector<BoxItem>& items, std::vector<std::vector<BoxTerm>>& terms, int sd, int l,
+                          int in_buf, int out_buf, int transpose, int group) -> bool {
+    i64 max_in = 1, max_ab = 1, max_mat = 1;
+    for (size_t i = 0; i < items.size(); ++i) {
+      if (terms[i].size() != 1) throw std::runtime_error("internal: box items carry exactly one term");
+      const BoxTerm& t = terms[i][0];
+      i64 e[kMaxTM];
+      i64 isz = nv, msz = 0;  // input box with padded leading dimension
+      for (int p = 0; p < d; ++p) {
+        e[p] = t.in_ext[p];
+        isz *= (p == 0 ? e[p] + 1 : e[p]);
+      }
+      max_in = std::max(max_in, isz);
+      for (int k = 0; k < d; ++k) msz += static_cast<i64>(t.mrows[k]) * t.mcols[k];
+      max_mat = std::max(max_mat, msz);
+      for (int k = 0; k < d - 1; ++k) {
+        e[k] = transpose ? t.mcols[k] : t.mrows[k];
+        i64 cur = nv;
+        for (int p = 0; p < d; ++p) cur *= e[p];
+        max_ab = std::max(max_ab, cur);
+      }
+    }
+    if (max_in + max_mat + 2 * max_ab > 14000) return false;  // > ~219 KB of shared memory
+    BoxLaunch bl;
+    bl.side = sd;
+    bl.level = l;
+    bl.in_buf = in_buf;
+    bl.out_buf = out_buf;
+    bl.item_begin = static_cast<i64>(pl->bitems.size());
+    bl.nitems = static_cast<i64>(items.size());
+    bl.info.d = d;
+    bl.info.nv = static_cast<int>(nv);
+    bl.info.transpose = transpose;
+    bl.info.smem_elems_in = static_cast<int>(max_in);
+    bl.info.smem_elems_mat = static_cast<int>(max_mat);
+    bl.info.smem_elems_a = static_cast<int>(max_ab);
+    bl.info.smem_elems_b = static_cast<int>(max_ab);
+    for (size_t i = 0; i < items.size(); ++i) {
+      BoxItem x = items[i];
+      x.term_off = static_cast<i64>(pl->bterms.size());
+      x.nterm = 1;
+      x.last_lo = 0;
+      x.last_hi = x.out_ext[d - 1];
+      pl->bterms.push_back(terms[i][0]);
+      pl->bitems.push_back(x);
+    }
+    pl->ops.push_back(Op{3, static_cast<i64>(pl->boxes.size()), group});
+    pl->boxes.push_back(bl);
+    return true;
+  };
   // ---- Step 1: V / W
-  std::vector<TRef> cur;  // per item of the current level (output of last mode)
+  std::vector<TRef> cur;  // per item (s, tau) of the current level
   for (int l = 0; l <= b.Lc; ++l) {
     const LevelData& ld = b.side[0][static_cast<size_t>(l)];
     const i64 nin = ld.L.nin, nj = ld.L.nj;
@@ -551,16 +631,77 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
     std::vector<TRef> in(static_cast<size_t>(nitems));
     for (i64 it = 0; it < nitems; ++it) {
       const i64 s = it / nin, tau = it % nin;
-      if (l == 0) {
-        in[static_cast<size_t>(it)] = global_slab(s);
-      } else {
-        i64 ptau = 0;
-        for (int p = d - 1; p >= 0; --p) ptau = (ptau << (l - 1)) | (((tau >> (l * p)) & ((i64{1} << l) - 1)) >> 1);
-        in[static_cast<size_t>(it)] = cur[static_cast<size_t>(s * ipow(2, static_cast<i64>(d) * (l - 1)) + ptau)];
+      in[static_cast<size_t>(it)] =
+          l == 0 ? global_slab(s) : cur[static_cast<size_t>(s * ipow(2, static_cast<i64>(d) * (l - 1)) + parent_of(tau, l))];
+    }
+    // ---- fused boxes
+    const i64 scratch_mark = scratch;
+    std::vector<TRef> outs(static_cast<size_t>(nitems));
+    std::vector<BoxItem> items;
+    std::vector<std::vector<BoxTerm>> terms;
+    const i64 nbeta = ipow(nj, d);
+    for (i64 it = 0; it < nitems; ++it) {
+      const i64 s = it / nin, tau = it % nin;
+      const TRef& x = in[static_cast<size_t>(it)];
+      std::vector<std::vector<int>> R(d), W(d);
+      std::vector<std::vector<i64>> MO(d);
+      int oext[kMaxTM];
+      for (int k = 0; k < d; ++k) {
+        int tot_r = 0, tot_w = 0;
+        for (i64 j = 0; j < nj; ++j) {
+          int r, w;
+          i64 mo;
+          slot_info(0, l, s, tau, k, j, r, w, mo);
+          R[k].push_back(r);
+          W[k].push_back(w);
+          MO[k].push_back(mo);
+          tot_r += r;
+          tot_w += w;
+        }
+        if (tot_w != x.ext[k]) throw std::runtime_error("internal: V/W block widths do not match the tensor extent");
+        oext[k] = tot_r;
+      }
+      oext[d] = static_cast<int>(nv);
+      const TRef y = alloc(nd, oext);
+      outs[static_cast<size_t>(it)] = y;
+      for (i64 beta = 0; beta < nbeta; ++beta) {
+        BoxTerm t{};
+        BoxItem bi{};
+        t.in_off = x.off;
+        bi.out_off = y.off;
+        for (int k = 0; k < d; ++k) {
+          const i64 j = (beta / ipow(nj, k)) % nj;
+          i64 ci = 0, co = 0;
+          for (i64 q = 0; q < j; ++q) {
+            ci += W[k][static_cast<size_t>(q)];
+            co += R[k][static_cast<size_t>(q)];
+          }
+          t.in_off += ci * x.stride[k];
+          bi.out_off += co * y.stride[k];
+          t.in_ext[k] = W[k][static_cast<size_t>(j)];
+          bi.out_ext[k] = R[k][static_cast<size_t>(j)];
+          t.mat_off[k] = MO[k][static_cast<size_t>(j)];
+          t.mrows[k] = R[k][static_cast<size_t>(j)];
+          t.mcols[k] = W[k][static_cast<size_t>(j)];
+        }
+        for (int p = 0; p < nd; ++p) {
+          t.in_stride[p] = x.stride[p];
+          bi.out_stride[p] = y.stride[p];
+        }
+        t.in_ext[d] = static_cast<int>(nv);
+        bi.out_ext[d] = static_cast<int>(nv);
+        bi.nterm = 1;
+        items.push_back(bi);
+        terms.push_back({t});
       }
     }
+    if (commit_boxes(items, terms, 0, l, l == 0 ? BUF_F : BUF_SCRATCH, BUF_SCRATCH, 0, 0)) {
+      cur = outs;
+      continue;
+    }
+    scratch = scratch_mark;  // fall back to per-mode launches for this level
     for (int k = 0; k < d; ++k) {
-      std::vector<MPStep> items;
+      std::vector<MPStep> mitems;
       std::vector<std::vector<Blk>> blocks;
       for (i64 it = 0; it < nitems; ++it) {
         const i64 s = it / nin, tau = it % nin;
@@ -570,11 +711,11 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
         std::vector<Blk> bl;
         int ci = 0, co = 0;
         for (i64 j = 0; j < nj; ++j) {
-          const i64 slot = ((s * nin + tau) * d + k) * nj + j;
           Blk B;
-          B.mat_off = ld.h_interp_off[static_cast<size_t>(slot)];
-          B.rows = ld.h_rank[static_cast<size_t>(slot)];
-          B.cols = ld.h_width[static_cast<size_t>(slot)];
+          int r, w;
+          slot_info(0, l, s, tau, k, j, r, w, B.mat_off);
+          B.rows = r;
+          B.cols = w;
           B.in_start = ci;
           B.out_start = co;
           ci += B.cols;
@@ -584,11 +725,11 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
         if (ci != x.ext[k]) throw std::runtime_error("internal: V/W block widths do not match the tensor extent");
         oext[k] = co;
         TRef y = alloc(nd, oext);
-        items.push_back(make_step(x, y, k, 0));
+        mitems.push_back(make_step(x, y, k, 0));
         blocks.push_back(bl);
         x = y;
       }
-      add_mp(*pl, 0, l, (l == 0 && k == 0) ? BUF_F : BUF_SCRATCH, BUF_SCRATCH, items, blocks, 0);
+      add_mp(*pl, 0, l, (l == 0 && k == 0) ? BUF_F : BUF_SCRATCH, BUF_SCRATCH, mitems, blocks, 0);
     }
     cur = in;
   }
@@ -624,15 +765,113 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
   }
   pl->gemv_ctas = ctas;
   pl->ops.push_back(Op{1, 0, 1});
-  // ---- Step 3: P (l = Lc..1), U (l = 0)
+  // ---- Step 3: P (l = Lc..1, ordered child sums), U (l = 0)
   std::vector<TRef> gcur = gts;  // per (t, nu) at level l: index t * nin + nu
   for (int l = b.Lc; l >= 0; --l) {
     const LevelData& ld = b.side[1][static_cast<size_t>(l)];
     const i64 nin = ld.L.nin, nj = ld.L.nj;
+    const i64 pnin = l > 0 ? ipow(2, static_cast<i64>(d) * (l - 1)) : 1;
+    const i64 nbeta = ipow(nj, d);
+    const i64 scratch_mark = scratch;
+    std::vector<TRef> par(static_cast<size_t>(b.nmid * pnin));
+    std::vector<BoxItem> items;
+    std::vector<std::vector<BoxTerm>> terms;
+    std::vector<SumDesc> psums;
+    for (i64 t = 0; t < b.nmid; ++t)
+      for (i64 pnu = 0; pnu < pnin; ++pnu) {
+        std::vector<i64> kids;
+        for (i64 nu = 0; nu < nin; ++nu)
+          if (l == 0 || parent_of(nu, l) == pnu) kids.push_back(nu);
+        // widths (output side) are common to all children
+        std::vector<std::vector<int>> W(d);
+        int oext[kMaxTM];
+        for (int k = 0; k < d; ++k) {
+          int tw = 0;
+          for (i64 j = 0; j < nj; ++j) {
+            int r, w;
+            i64 mo;
+            slot_info(1, l, t, kids[0], k, j, r, w, mo);
+            W[k].push_back(w);
+            tw += w;
+          }
+          oext[k] = tw;
+        }
+        oext[d] = static_cast<int>(nv);
+        const TRef y = l == 0 ? global_slab(t) : alloc(nd, oext);
+        par[static_cast<size_t>(t * pnin + pnu)] = y;
+        SumDesc sdsc{};
+        for (i64 nu : kids) {
+          // l >= 1: each child writes its own contribution (parent's shape),
+          // summed afterwards in ascending nu; l = 0: straight into G
+          const TRef yc = l == 0 ? y : alloc(nd, oext);
+          if (l > 0) sdsc.child_off[sdsc.nchild++] = yc.off;
+          const TRef& x = gcur[static_cast<size_t>(t * nin + nu)];
+          for (i64 beta = 0; beta < nbeta; ++beta) {
+            BoxItem bi{};
+            BoxTerm tm{};
+            bi.out_off = yc.off;
+            tm.in_off = x.off;
+            for (int k = 0; k < d; ++k) {
+              const int jb = static_cast<int>((beta / ipow(nj, k)) % nj);
+              i64 co = 0, ci = 0;
+              int r = 0, w = 0;
+              i64 mo = 0;
+              for (int q = 0; q < jb; ++q) {
+                slot_info(1, l, t, nu, k, q, r, w, mo);
+                ci += r;
+                co += w;
+              }
+              slot_info(1, l, t, nu, k, jb, r, w, mo);
+              if (w != W[k][static_cast<size_t>(jb)]) throw std::runtime_error("internal: P/U widths differ");
+              bi.out_off += co * yc.stride[k];
+              bi.out_ext[k] = w;
+              tm.in_off += ci * x.stride[k];
+              tm.in_ext[k] = r;
+              tm.mat_off[k] = mo;
+              tm.mrows[k] = r;
+              tm.mcols[k] = w;
+            }
+            bi.out_ext[d] = static_cast<int>(nv);
+            tm.in_ext[d] = static_cast<int>(nv);
+            for (int p = 0; p < nd; ++p) {
+              bi.out_stride[p] = yc.stride[p];
+              tm.in_stride[p] = x.stride[p];
+            }
+            bi.nterm = 1;
+            items.push_back(bi);
+            terms.push_back({tm});
+          }
+        }
+        if (l > 0) {
+          sdsc.out_off = y.off;
+          sdsc.total = y.size();
+          psums.push_back(sdsc);
+        }
+      }
+    if (commit_boxes(items, terms, 1, l, BUF_SCRATCH, l == 0 ? BUF_G : BUF_SCRATCH, 1, 2)) {
+      if (l > 0) {
+        SumLaunch sl;
+        sl.begin = static_cast<i64>(pl->sums.size());
+        sl.n = static_cast<i64>(psums.size());
+        sl.work_begin = static_cast<i64>(pl->sum_map.size()) / 2;
+        for (size_t q = 0; q < psums.size(); ++q)
+          for (i64 c = 0; c * 1024 < psums[q].total; ++c) {
+            pl->sum_map.push_back(static_cast<int>(q));
+            pl->sum_map.push_back(static_cast<int>(c));
+          }
+        sl.total = static_cast<i64>(pl->sum_map.size()) / 2 - sl.work_begin;
+        pl->sums.insert(pl->sums.end(), psums.begin(), psums.end());
+        pl->ops.push_back(Op{4, static_cast<i64>(pl->sum_launches.size()), 2});
+        pl->sum_launches.push_back(sl);
+      }
+      gcur = par;
+      continue;
+    }
+    scratch = scratch_mark;  // fall back: per-mode launches + ordered sums
     const i64 nitems = b.nmid * nin;
     std::vector<TRef> x = gcur;
     for (int k = 0; k < d; ++k) {
-      std::vector<MPStep> items;
+      std::vector<MPStep> mitems;
       std::vector<std::vector<Blk>> blocks;
       const bool last_global = (l == 0 && k == d - 1);
       for (i64 it = 0; it < nitems; ++it) {
@@ -643,11 +882,11 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
         std::vector<Blk> bl;
         int ci = 0, co = 0;
         for (i64 j = 0; j < nj; ++j) {
-          const i64 slot = ((t * nin + nu) * d + k) * nj + j;
           Blk B;
-          B.mat_off = ld.h_interp_off[static_cast<size_t>(slot)];
-          B.rows = ld.h_rank[static_cast<size_t>(slot)];
-          B.cols = ld.h_width[static_cast<size_t>(slot)];
+          int r, w;
+          slot_info(1, l, t, nu, k, j, r, w, B.mat_off);
+          B.rows = r;
+          B.cols = w;
           B.in_start = ci;
           B.out_start = co;
           ci += B.rows;
@@ -657,44 +896,40 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
         if (ci != xi.ext[k]) throw std::runtime_error("internal: P/U block ranks do not match the tensor extent");
         oext[k] = co;
         TRef y = last_global ? global_slab(t) : alloc(nd, oext);
-        items.push_back(make_step(xi, y, k, 1));
+        mitems.push_back(make_step(xi, y, k, 1));
         blocks.push_back(bl);
         xi = y;
       }
-      add_mp(*pl, 1, l, BUF_SCRATCH, last_global ? BUF_G : BUF_SCRATCH, items, blocks, 2);
+      add_mp(*pl, 1, l, BUF_SCRATCH, last_global ? BUF_G : BUF_SCRATCH, mitems, blocks, 2);
     }
-    if (l > 0) {  // ordered sum of the 2^d children into each parent
-      const i64 pnin = ipow(2, static_cast<i64>(d) * (l - 1));
-      std::vector<TRef> par(static_cast<size_t>(b.nmid * pnin));
+    if (l > 0) {
+      std::vector<TRef> par2(static_cast<size_t>(b.nmid * pnin));
       SumLaunch sl;
       sl.begin = static_cast<i64>(pl->sums.size());
       i64 work = 0;
       for (i64 t = 0; t < b.nmid; ++t)
         for (i64 pnu = 0; pnu < pnin; ++pnu) {
-          SumDesc sd{};
-          sd.nchild = 0;
+          SumDesc sdsc{};
           TRef first;
           for (i64 nu = 0; nu < nin; ++nu) {
-            i64 pp = 0;
-            for (int p = d - 1; p >= 0; --p) pp = (pp << (l - 1)) | (((nu >> (l * p)) & ((i64{1} << l) - 1)) >> 1);
-            if (pp != pnu) continue;
+            if (parent_of(nu, l) != pnu) continue;
             const TRef& c = x[static_cast<size_t>(t * nin + nu)];
-            if (sd.nchild == 0) first = c;
-            sd.child_off[sd.nchild++] = c.off;
+            if (sdsc.nchild == 0) first = c;
+            sdsc.child_off[sdsc.nchild++] = c.off;
           }
           TRef y = alloc(nd, first.ext);
-          sd.out_off = y.off;
-          sd.total = y.size();
-          sd.work_off = work;
-          work += sd.total;
-          pl->sums.push_back(sd);
-          par[static_cast<size_t>(t * pnin + pnu)] = y;
+          sdsc.out_off = y.off;
+          sdsc.total = y.size();
+          sdsc.work_off = work;
+          work += sdsc.total;
+          pl->sums.push_back(sdsc);
+          par2[static_cast<size_t>(t * pnin + pnu)] = y;
         }
       sl.n = static_cast<i64>(pl->sums.size()) - sl.begin;
       sl.total = work;
       pl->ops.push_back(Op{2, static_cast<i64>(pl->sum_launches.size()), 2});
       pl->sum_launches.push_back(sl);
-      gcur = par;
+      gcur = par2;
     }
   }
   pl->scratch_elems = scratch;
@@ -702,7 +937,18 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
   pl->d_steps = to_device(pl->steps, st);
   pl->d_blks = to_device(pl->blks, st);
   pl->d_gemv = to_device(pl->gemv, st);
+  {
+    std::vector<int> map(static_cast<size_t>(std::max<i64>(pl->gemv_ctas, 1)));
+    for (size_t p = 0; p < pl->gemv.size(); ++p) {
+      const i64 end = p + 1 < pl->gemv.size() ? pl->gemv[p + 1].cta_off : pl->gemv_ctas;
+      for (i64 c = pl->gemv[p].cta_off; c < end; ++c) map[static_cast<size_t>(c)] = static_cast<int>(p);
+    }
+    pl->d_gemv_map = to_device(map, st);
+  }
   pl->d_sums = to_device(pl->sums, st);
+  pl->d_bitems = to_device(pl->bitems, st);
+  pl->d_sum_map = to_device(pl->sum_map, st);
+  pl->d_bterms = to_device(pl->bterms, st);
   pl->scratch.alloc(static_cast<size_t>(std::max<i64>(scratch, 1)));
   TBF_CUDA(cudaStreamSynchronize(st));
   return pl;
@@ -726,8 +972,19 @@ void run_ops(oiobf_tbf& b, Plan& pl, const double2* F, double2* G, cudaStream_t 
       const LevelData& ld = b.side[m.side][static_cast<size_t>(m.level)];
       launch_mode_product(m.nsteps, pl.d_steps.p + m.step_begin, m.total_out, pl.d_blks.p, ld.interp.p, in, out, st);
     } else if (op.kind == 1) {
-      launch_gemv(static_cast<i64>(pl.gemv.size()), pl.d_gemv.p, pl.gemv_ctas, static_cast<int>(pl.nv), b.cores.p,
-                  pl.scratch.p, pl.scratch.p, pl.gemv_max_c, st);
+      launch_gemv(pl.d_gemv_map.p, pl.d_gemv.p, pl.gemv_ctas, static_cast<int>(pl.nv), b.cores.p, pl.scratch.p,
+                  pl.scratch.p, pl.gemv_max_c, st);
+    } else if (op.kind == 3) {
+      const BoxLaunch& bx = pl.boxes[static_cast<size_t>(op.idx)];
+      const double2* in = bx.in_buf == BUF_F ? F : pl.scratch.p;
+      double2* out = bx.out_buf == BUF_G ? G : pl.scratch.p;
+      const LevelData& ld = b.side[bx.side][static_cast<size_t>(bx.level)];
+      launch_box(bx.nitems, pl.d_bitems.p + bx.item_begin, pl.d_bterms.p + bx.item_begin, bx.info, ld.interp.p, in,
+                 out, st);
+    } else if (op.kind == 4) {
+      const SumLaunch& s = pl.sum_launches[static_cast<size_t>(op.idx)];
+      launch_sum_parent(s.total, pl.d_sums.p + s.begin, pl.d_sum_map.p + 2 * s.work_begin, pl.scratch.p,
+                        pl.scratch.p, st);
     } else {
       const SumLaunch& s = pl.sum_launches[static_cast<size_t>(op.idx)];
       launch_sum_children(s.n, pl.d_sums.p + s.begin, s.total, pl.scratch.p, pl.scratch.p, st);
@@ -739,6 +996,11 @@ void contract_device(oiobf_tbf& b, const double2* F, double2* G, i64 nv, cudaStr
   require(nv >= 1, "tbf_contract: nv must be >= 1");
   TBF_CUDA(cudaSetDevice(b.device));
   Plan& pl = get_plan(b, nv);
+  static const bool no_graph = std::getenv("OIOBF_NO_GRAPH") != nullptr;  // profiling aid
+  if (no_graph) {
+    run_ops(b, pl, F, G, st);
+    return;
+  }
   if (!pl.gexec || pl.g_F != F || pl.g_G != G || pl.g_st != st) {
     if (pl.gexec) {
       cudaGraphExecDestroy(pl.gexec);

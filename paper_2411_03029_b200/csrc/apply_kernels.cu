@@ -79,40 +79,204 @@ __device__ __forceinline__ double2 ld_stream2(const double2* p) {
   return r;
 }
 
-// grid: one CTA per (pair, 32-row chunk); each warp walks 4 rows
-__global__ void __launch_bounds__(kGemvThreads) k_gemv(const int* __restrict__ cta_pair,
-                                                       const GemvDesc* __restrict__ ds, int nv,
-                                                       const double2* __restrict__ cores,
+// Persistent, balanced core GEMV: CTA i owns the contiguous global row range
+// [i*rows_per_cta, (i+1)*rows_per_cta) over all pairs (rows of a pair are
+// contiguous in the core arena), so every SM streams the same number of
+// bytes.  Per pair segment the CTA stages x = F_{t,s} in shared memory, then
+// each warp walks whole rows with 8 independent 16-B streaming loads per lane
+// in flight; a row is read once and applied to all nv vectors.
+template <int NV>  // NV = 1: single-vector fast path; NV = 0: generic nv
+__global__ void __launch_bounds__(kGemvThreads, 4) k_gemv(const int* __restrict__ cta_pair,
+                                                       const GemvDesc* __restrict__ ds, int nv_rt, long long total_rows,
+                                                       long long rows_per_cta, const double2* __restrict__ cores,
                                                        const double2* __restrict__ x, double2* __restrict__ y) {
   extern __shared__ __align__(16) double2 sx[];
-  const i64 cta = blockIdx.x;
-  const GemvDesc D = ds[cta_pair[cta]];
-  const int chunk = static_cast<int>(cta - D.cta_off);
-  for (int i = threadIdx.x; i < D.C * nv; i += kGemvThreads) sx[i] = x[D.x_off + i];
-  __syncthreads();
+  const int nv = NV == 1 ? 1 : nv_rt;
+  constexpr int kAcc = NV == 1 ? 1 : 4;
+  const long long g0 = static_cast<long long>(blockIdx.x) * rows_per_cta;
+  const long long g1 = min(total_rows, g0 + rows_per_cta);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r0 = chunk * kGemvRowsPerCta;
-  for (int rr = warp; rr < kGemvRowsPerCta; rr += kGemvThreads / 32) {
-    const int r = r0 + rr;
-    if (r >= D.R) break;
-    const double2* row = cores + D.core_off + static_cast<i64>(r) * D.C;
-    for (int v = 0; v < nv; ++v) {
-      double2 acc0 = make_double2(0, 0), acc1 = make_double2(0, 0);
-      const double2* xv = sx + v * D.C;
-      int c = lane;
-      for (; c + 96 < D.C; c += 128) {
-        const double2 a0 = ld_stream2(row + c), a1 = ld_stream2(row + c + 32);
-        const double2 a2 = ld_stream2(row + c + 64), a3 = ld_stream2(row + c + 96);
-        cfma(acc0, a0, xv[c]);
-        cfma(acc1, a1, xv[c + 32]);
-        cfma(acc0, a2, xv[c + 64]);
-        cfma(acc1, a3, xv[c + 96]);
-      }
-      for (; c < D.C; c += 32) cfma(acc0, ld_stream2(row + c), xv[c]);
-      acc0 = cadd(acc0, acc1);
-      acc0 = warp_sum2(acc0);
-      if (lane == 0) y[D.y_off + r + static_cast<i64>(v) * D.R] = acc0;
+  int p = cta_pair[blockIdx.x];
+  long long g = g0;
+  while (g < g1) {
+    const GemvDesc D = ds[p];
+    const long long pend = min(g1, D.cta_off + D.R);  // cta_off holds the pair's first global row
+    const int C = D.C;
+    // stage x (C * nv) with independent loads
+    for (int i = threadIdx.x; i < C * nv; i += kGemvThreads * 4) {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i + u * kGemvThreads < C * nv) v[u] = __ldg(x + D.x_off + i + u * kGemvThreads);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i + u * kGemvThreads < C * nv) sx[i + u * kGemvThreads] = v[u];
     }
+    __syncthreads();
+    for (long long gr = g + warp; gr < pend; gr += kGemvThreads / 32) {
+      const int r = static_cast<int>(gr - D.cta_off);
+      const double2* row = cores + D.core_off + static_cast<long long>(r) * C;
+      double2 acc[kAcc];
+#pragma unroll
+      for (int v = 0; v < kAcc; ++v) acc[v] = make_double2(0, 0);
+      int c = lane;
+      for (; c + 7 * 32 < C; c += 8 * 32) {
+        double2 a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = ld_stream2(row + c + u * 32);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int v = 0; v < kAcc; ++v)
+            if (v < nv) cfma(acc[v], a[u], sx[v * C + c + u * 32]);
+      }
+      for (; c < C; c += 32) {
+        const double2 a0 = ld_stream2(row + c);
+#pragma unroll
+        for (int v = 0; v < kAcc; ++v)
+          if (v < nv) cfma(acc[v], a0, sx[v * C + c]);
+      }
+#pragma unroll
+      for (int v = 0; v < kAcc; ++v)
+        if (v < nv) {
+          const double2 t = warp_sum2(acc[v]);
+          if (lane == 0) y[D.y_off + r + static_cast<long long>(v) * D.R] = t;
+        }
+      // nv > 4: remaining vectors re-read the row (rare path)
+      for (int v = kAcc; v < nv; ++v) {
+        double2 t = make_double2(0, 0);
+        for (int cc = lane; cc < C; cc += 32) cfma(t, ld_stream2(row + cc), sx[v * C + cc]);
+        t = warp_sum2(t);
+        if (lane == 0) y[D.y_off + r + static_cast<long long>(v) * D.R] = t;
+      }
+    }
+    __syncthreads();
+    g = pend;
+    ++p;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Core GEMV with a TMA bulk-copy pipeline (sm_90+/sm_100a): one producer warp
+// streams whole core rows (contiguous C*16 bytes) into a shared-memory ring
+// with cp.async.bulk + mbarrier complete_tx; 8 consumer warps compute the
+// row . x dot products from shared memory.  Bytes in flight are bounded by
+// the ring (not by registers), which is what an HBM stream needs.  Each CTA
+// owns a balanced contiguous row range; the x vectors of the (<= kTmaMaxPairs)
+// pairs it touches are staged up front.
+constexpr int kTmaConsumers = 8;
+constexpr int kTmaThreads = 32 * (kTmaConsumers + 1);
+constexpr int kTmaMaxPairs = 4;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kTmaThreads) k_gemv_tma(const int* __restrict__ cta_pair,
+                                                              const GemvDesc* __restrict__ ds, int nv,
+                                                              long long total_rows, long long rows_per_cta,
+                                                              int stages, int stage_elems, int xcap,
+                                                              const double2* __restrict__ cores,
+                                                              const double2* __restrict__ x,
+                                                              double2* __restrict__ y) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw);
+  unsigned long long* empty = full + stages;
+  double2* ring = reinterpret_cast<double2*>(smem_raw + 128 * ((2 * stages * 8 + 127) / 128));
+  double2* sxs = ring + static_cast<long long>(stages) * stage_elems;  // kTmaMaxPairs x-slots of xcap
+  __shared__ GemvDesc pd[kTmaMaxPairs];
+  __shared__ int npairs_s;
+  const long long g0 = static_cast<long long>(blockIdx.x) * rows_per_cta;
+  const long long g1 = min(total_rows, g0 + rows_per_cta);
+  const int p0 = cta_pair[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    int np = 0;
+    while (np < kTmaMaxPairs) {
+      const GemvDesc D = ds[p0 + np];
+      pd[np] = D;
+      ++np;
+      if (D.cta_off + D.R >= g1) break;
+    }
+    npairs_s = np;
+    for (int i = 0; i < stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int np = npairs_s;
+  for (int q = 0; q < np; ++q)
+    for (int i = threadIdx.x; i < pd[q].C * nv; i += kTmaThreads) sxs[q * xcap + i] = __ldg(x + pd[q].x_off + i);
+  __syncthreads();
+  const long long nrows = g1 - g0;
+  if (warp == kTmaConsumers) {  // producer
+    if (lane == 0) {
+      int q = 0;
+      for (long long i = 0; i < nrows; ++i) {
+        const long long gr = g0 + i;
+        while (gr >= pd[q].cta_off + pd[q].R) ++q;
+        const int st = static_cast<int>(i % stages);
+        const long long round = i / stages;
+        if (round > 0) mbar_wait(&empty[st], static_cast<unsigned>((round - 1) & 1));
+        const unsigned bytes = static_cast<unsigned>(pd[q].C) * 16u;
+        mbar_expect_tx(&full[st], bytes);
+        bulk_g2s(ring + static_cast<long long>(st) * stage_elems,
+                 cores + pd[q].core_off + (gr - pd[q].cta_off) * pd[q].C, bytes, &full[st]);
+      }
+    }
+    return;
+  }
+  int q = 0;
+  for (long long i = warp; i < nrows; i += kTmaConsumers) {
+    const long long gr = g0 + i;
+    while (gr >= pd[q].cta_off + pd[q].R) ++q;
+    const int st = static_cast<int>(i % stages);
+    mbar_wait(&full[st], static_cast<unsigned>((i / stages) & 1));
+    const double2* row = ring + static_cast<long long>(st) * stage_elems;
+    const double2* xv = sxs + q * xcap;
+    const int C = pd[q].C;
+    const int r = static_cast<int>(gr - pd[q].cta_off);
+    for (int v = 0; v < nv; ++v) {
+      double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
+      int c = lane;
+      for (; c + 32 < C; c += 64) {
+        cfma(a0, row[c], xv[v * C + c]);
+        cfma(a1, row[c + 32], xv[v * C + c + 32]);
+      }
+      if (c < C) cfma(a0, row[c], xv[v * C + c]);
+      const double2 t = warp_sum2(cadd(a0, a1));
+      if (lane == 0) y[pd[q].y_off + r + static_cast<long long>(v) * pd[q].R] = t;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
   }
 }
 
@@ -138,13 +302,51 @@ void launch_mode_product(i64 nitems, const MPStep* steps, i64 total_out, const B
   TBF_CUDA(cudaGetLastError());
 }
 
-void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, int nv, const double2* cores, const double2* x,
-                 double2* y, int max_c, cudaStream_t st) {
+void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, i64 rows_per_cta, int nv,
+                 const double2* cores, const double2* x, double2* y, int max_c, cudaStream_t st) {
   if (nctas == 0) return;
   const size_t smem = sizeof(double2) * static_cast<size_t>(max_c) * nv;
-  TBF_CUDA(cudaFuncSetAttribute(k_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-  k_gemv<<<static_cast<unsigned>(nctas), kGemvThreads, smem, st>>>(cta_pair, d, nv, cores, x, y);
+  if (nv == 1) {
+    TBF_CUDA(cudaFuncSetAttribute(k_gemv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    k_gemv<1><<<static_cast<unsigned>(nctas), kGemvThreads, smem, st>>>(cta_pair, d, nv, total_rows, rows_per_cta,
+                                                                        cores, x, y);
+  } else {
+    TBF_CUDA(cudaFuncSetAttribute(k_gemv<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    k_gemv<0><<<static_cast<unsigned>(nctas), kGemvThreads, smem, st>>>(cta_pair, d, nv, total_rows, rows_per_cta,
+                                                                        cores, x, y);
+  }
   TBF_CUDA(cudaGetLastError());
+}
+
+void launch_gemv_tma(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, i64 rows_per_cta, int nv,
+                     int stages, int stage_elems, int xcap, const double2* cores, const double2* x, double2* y,
+                     cudaStream_t st) {
+  if (nctas == 0) return;
+  const size_t smem = gemv_tma_smem_bytes(stages, stage_elems, xcap);
+  TBF_CUDA(cudaFuncSetAttribute(k_gemv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  k_gemv_tma<<<static_cast<unsigned>(nctas), kTmaThreads, smem, st>>>(cta_pair, d, nv, total_rows, rows_per_cta,
+                                                                      stages, stage_elems, xcap, cores, x, y);
+  TBF_CUDA(cudaGetLastError());
+}
+
+size_t gemv_tma_smem_bytes(int stages, int stage_elems, int xcap) {
+  return 128 * ((2 * static_cast<size_t>(stages) * 8 + 127) / 128) +
+         sizeof(double2) * (static_cast<size_t>(stages) * stage_elems + static_cast<size_t>(kTmaMaxPairs) * xcap);
+}
+
+int gemv_tma_max_pairs() { return kTmaMaxPairs; }
+
+int gemv_ctas_per_sm(int nv, int max_c) {
+  int n = 0;
+  const size_t smem = sizeof(double2) * static_cast<size_t>(max_c) * nv;
+  if (nv == 1) {
+    TBF_CUDA(cudaFuncSetAttribute(k_gemv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    TBF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gemv<1>, kGemvThreads, smem));
+  } else {
+    TBF_CUDA(cudaFuncSetAttribute(k_gemv<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    TBF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gemv<0>, kGemvThreads, smem));
+  }
+  return n < 1 ? 1 : n;
 }
 
 void launch_sum_children(i64 n, const SumDesc* d, i64 total, const double2* in, double2* out, cudaStream_t st) {

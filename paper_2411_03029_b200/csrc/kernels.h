@@ -66,8 +66,17 @@ struct GemvDesc {  // y(R x nv) = K(R x C, row-major) * x(C x nv)
   int R, C;
   i64 cta_off;     // prefix of CTA counts
 };
-void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, int nv, const double2* cores, const double2* x,
-                 double2* y, int max_c, cudaStream_t st);
+// cta_pair[i] = pair holding CTA i's first row; GemvDesc.cta_off = the pair's
+// first global row
+void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, i64 rows_per_cta, int nv,
+                 const double2* cores, const double2* x, double2* y, int max_c, cudaStream_t st);
+int gemv_ctas_per_sm(int nv, int max_c);
+// TMA bulk-copy pipelined variant (rows staged by cp.async.bulk into an SMEM ring)
+void launch_gemv_tma(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, i64 rows_per_cta, int nv,
+                     int stages, int stage_elems, int xcap, const double2* cores, const double2* x, double2* y,
+                     cudaStream_t st);
+size_t gemv_tma_smem_bytes(int stages, int stage_elems, int xcap);
+int gemv_tma_max_pairs();
 
 struct SumDesc {  // out[e] = sum_c in[c_off[c] + e], children in order
   i64 out_off, total, work_off;
@@ -101,10 +110,14 @@ struct BoxItem {
 struct BoxLaunchInfo {
   int d, nv, transpose;
   int smem_elems_in, smem_elems_mat, smem_elems_a, smem_elems_b;
+  int cs;              // thread-block cluster size: the last input mode is split over cs CTAs
+  int smem_elems_acc;  // partial output box (cs > 1), reduced through DSMEM
 };
 void launch_box(i64 nitems, const BoxItem* items, const BoxTerm* terms, const BoxLaunchInfo& info,
                 const double2* mats, const double2* in, double2* out, cudaStream_t st);
 size_t box_smem_bytes(const BoxLaunchInfo& info);
+void box_trace_enable(unsigned long long* buf);  // debug: per-CTA phase timestamps
+int box_max_active_clusters(int cs, size_t smem);
 // ordered child sums, one CTA per parent (SumDesc.work_off unused)
 void launch_sum_parent(i64 nctas, const SumDesc* d, const int* cta_map, const double2* in, double2* out,
                        cudaStream_t st);

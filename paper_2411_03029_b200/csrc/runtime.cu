@@ -13,6 +13,7 @@
 // sums), captured once into a CUDA graph and replayed.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -204,6 +205,12 @@ struct Plan {
   std::vector<MPLaunch> mps;
   std::vector<GemvDesc> gemv;
   i64 gemv_ctas = 0;
+  i64 gemv_total_rows = 0, gemv_rows_per_cta = 1;
+  bool gemv_tma = false;
+  i64 tma_ctas = 0, tma_rows_per_cta = 1;
+  int tma_stages = 0, tma_stage_elems = 0, tma_xcap = 0;
+  std::vector<int> tma_map;
+  DevBuf<int> d_tma_map;
   int gemv_max_c = 0;
   std::vector<SumDesc> sums;
   std::vector<SumLaunch> sum_launches;
@@ -574,16 +581,25 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
   // factors + two intermediates) and record a box launch, or report "too big".
   auto commit_boxes = [&](std::vector<BoxItem>& items, std::vector<std::vector<BoxTerm>>& terms, int sd, int l,
                           int in_buf, int out_buf, int transpose, int group) -> bool {
-    i64 max_in = 1, max_ab = 1, max_mat = 1;
+    // cluster size: split each box's last input mode over cs CTAs (DSMEM
+    // reduction) so small levels still occupy every SM
+    static const int cs_env = std::getenv("OIOBF_BOX_CLUSTER") ? std::atoi(std::getenv("OIOBF_BOX_CLUSTER")) : 0;
+    int cs = cs_env > 0 ? cs_env
+                        : static_cast<int>(std::min<i64>(8, std::max<i64>(1, (2 * 148 + static_cast<i64>(items.size()) - 1) /
+                                                                                  std::max<i64>(1, items.size()))));
+    cs = std::max(1, std::min(cs, 8));
+    i64 max_in = 1, max_ab = 1, max_mat = 1, max_out = 1;
     for (size_t i = 0; i < items.size(); ++i) {
       if (terms[i].size() != 1) throw std::runtime_error("internal: box items carry exactly one term");
       const BoxTerm& t = terms[i][0];
       i64 e[kMaxTM];
-      i64 isz = nv, msz = 0;  // input box with padded leading dimension
+      i64 isz = nv, msz = 0, osz = nv;  // input slab with padded leading dimension
       for (int p = 0; p < d; ++p) {
-        e[p] = t.in_ext[p];
+        e[p] = p == d - 1 ? (t.in_ext[p] + cs - 1) / cs : t.in_ext[p];
         isz *= (p == 0 ? e[p] + 1 : e[p]);
+        osz *= transpose ? t.mcols[p] : t.mrows[p];
       }
+      max_out = std::max(max_out, osz);
       max_in = std::max(max_in, isz);
       for (int k = 0; k < d; ++k) msz += static_cast<i64>(t.mrows[k]) * t.mcols[k];
       max_mat = std::max(max_mat, msz);
@@ -594,7 +610,37 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
         max_ab = std::max(max_ab, cur);
       }
     }
-    if (max_in + max_mat + 2 * max_ab > 14000) return false;  // > ~219 KB of shared memory
+    if (cs == 1) max_out = 0;
+    if (max_in + max_mat + 2 * max_ab + max_out > 14000) return false;  // > ~219 KB of shared memory
+    // single wave: shrink the cluster until every cluster is co-resident
+    while (cs_env <= 0 && cs > 1) {
+      BoxLaunchInfo probe{};
+      probe.smem_elems_in = static_cast<int>(max_in);
+      probe.smem_elems_mat = static_cast<int>(max_mat);
+      probe.smem_elems_a = probe.smem_elems_b = static_cast<int>(max_ab);
+      probe.smem_elems_acc = static_cast<int>(max_out);
+      if (box_max_active_clusters(cs, box_smem_bytes(probe)) >= static_cast<int>(items.size())) break;
+      --cs;
+      // recompute the slab-dependent sizes for the smaller cluster
+      max_in = max_ab = 1;
+      for (size_t i = 0; i < items.size(); ++i) {
+        const BoxTerm& t = terms[i][0];
+        i64 e[kMaxTM];
+        i64 isz = nv;
+        for (int p = 0; p < d; ++p) {
+          e[p] = p == d - 1 ? (t.in_ext[p] + cs - 1) / cs : t.in_ext[p];
+          isz *= (p == 0 ? e[p] + 1 : e[p]);
+        }
+        max_in = std::max(max_in, isz);
+        for (int k = 0; k < d - 1; ++k) {
+          e[k] = transpose ? t.mcols[k] : t.mrows[k];
+          i64 cur = nv;
+          for (int p = 0; p < d; ++p) cur *= e[p];
+          max_ab = std::max(max_ab, cur);
+        }
+      }
+      if (cs == 1) max_out = 0;
+    }
     BoxLaunch bl;
     bl.side = sd;
     bl.level = l;
@@ -609,6 +655,8 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
     bl.info.smem_elems_mat = static_cast<int>(max_mat);
     bl.info.smem_elems_a = static_cast<int>(max_ab);
     bl.info.smem_elems_b = static_cast<int>(max_ab);
+    bl.info.cs = cs;
+    bl.info.smem_elems_acc = static_cast<int>(max_out);
     for (size_t i = 0; i < items.size(); ++i) {
       BoxItem x = items[i];
       x.term_off = static_cast<i64>(pl->bterms.size());
@@ -758,12 +806,69 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
     g.y_off = y.off;
     g.R = pd.R;
     g.C = pd.C;
-    g.cta_off = ctas;
-    ctas += (pd.R + rpc - 1) / rpc;
+    g.cta_off = ctas;  // first global row of this pair
+    ctas += pd.R;
     pl->gemv_max_c = std::max(pl->gemv_max_c, pd.C);
     pl->gemv.push_back(g);
   }
-  pl->gemv_ctas = ctas;
+  (void)rpc;
+  // persistent balanced grid: every CTA streams the same number of rows
+  pl->gemv_total_rows = ctas;
+  {
+    const int per_sm = gemv_ctas_per_sm(static_cast<int>(nv), std::max(pl->gemv_max_c, 1));
+    i64 grid = std::min<i64>(static_cast<i64>(148) * per_sm, std::max<i64>(ctas, 1));
+    pl->gemv_rows_per_cta = (ctas + grid - 1) / grid;
+    grid = (ctas + pl->gemv_rows_per_cta - 1) / pl->gemv_rows_per_cta;
+    pl->gemv_ctas = ctas == 0 ? 0 : grid;
+  }
+  // TMA bulk-copy pipeline: one persistent CTA per SM, whole rows staged in a
+  // shared-memory ring; used when rows are long enough to be worth a bulk
+  // copy and every CTA's row range touches <= gemv_tma_max_pairs() pairs.
+  {
+    static const bool no_tma = std::getenv("OIOBF_GEMV_NO_TMA") != nullptr;
+    const int max_c = pl->gemv_max_c;
+    // measured on B200 (config 2): 2 CTAs/SM x 8 stages = 73% of HBM, same as
+    // the register-streaming kernel; 1 CTA/SM is consumer-bound (45%)
+    static const int per_sm_env = std::getenv("OIOBF_TMA_CTAS_PER_SM") ? std::atoi(std::getenv("OIOBF_TMA_CTAS_PER_SM")) : 2;
+    static const int stages_env = std::getenv("OIOBF_TMA_STAGES") ? std::atoi(std::getenv("OIOBF_TMA_STAGES")) : 8;
+    if (!no_tma && max_c >= 64 && ctas > 0) {
+      i64 grid = std::min<i64>(148 * std::max(1, per_sm_env), ctas);
+      const i64 rpc2 = (ctas + grid - 1) / grid;
+      grid = (ctas + rpc2 - 1) / rpc2;
+      const int stage_elems = (max_c + 7) / 8 * 8;
+      const int xcap = max_c * static_cast<int>(nv);
+      const i64 avail = static_cast<i64>(kMaxDynSmem) / std::max(1, per_sm_env) - 1024 -
+                        static_cast<i64>(gemv_tma_max_pairs()) * xcap * static_cast<i64>(sizeof(double2));
+      // rows go round-robin to the 8 consumer warps, so each stage must always
+      // belong to the same consumer (stages % 8 == 0); otherwise a consumer
+      // could wait two phases ahead and the parity check would be ambiguous
+      i64 stages = std::min<i64>(stages_env, avail / (static_cast<i64>(stage_elems) * 16));
+      stages = stages / 8 * 8;
+      bool ok = stages >= 8;
+      std::vector<int> map(static_cast<size_t>(grid));
+      size_t q = 0;
+      for (i64 c = 0; c < grid && ok; ++c) {
+        const i64 g0 = c * rpc2, g1 = std::min(ctas, g0 + rpc2);
+        while (q + 1 < pl->gemv.size() && pl->gemv[q + 1].cta_off <= g0) ++q;
+        map[static_cast<size_t>(c)] = static_cast<int>(q);
+        size_t q2 = q;
+        while (q2 + 1 < pl->gemv.size() && pl->gemv[q2 + 1].cta_off < g1) ++q2;
+        if (static_cast<int>(q2 - q + 1) > gemv_tma_max_pairs()) ok = false;
+      }
+      if (std::getenv("OIOBF_DEBUG"))
+        fprintf(stderr, "[oiobf] gemv tma ok=%d grid=%lld rows/cta=%lld stages=%lld stage_elems=%d xcap=%d rows=%lld\n",
+                ok ? 1 : 0, grid, rpc2, stages, stage_elems, xcap, ctas);
+      if (ok) {
+        pl->gemv_tma = true;
+        pl->tma_ctas = grid;
+        pl->tma_rows_per_cta = rpc2;
+        pl->tma_stages = static_cast<int>(stages);
+        pl->tma_stage_elems = stage_elems;
+        pl->tma_xcap = xcap;
+        pl->tma_map = map;
+      }
+    }
+  }
   pl->ops.push_back(Op{1, 0, 1});
   // ---- Step 3: P (l = Lc..1, ordered child sums), U (l = 0)
   std::vector<TRef> gcur = gts;  // per (t, nu) at level l: index t * nin + nu
@@ -939,11 +1044,14 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
   pl->d_gemv = to_device(pl->gemv, st);
   {
     std::vector<int> map(static_cast<size_t>(std::max<i64>(pl->gemv_ctas, 1)));
-    for (size_t p = 0; p < pl->gemv.size(); ++p) {
-      const i64 end = p + 1 < pl->gemv.size() ? pl->gemv[p + 1].cta_off : pl->gemv_ctas;
-      for (i64 c = pl->gemv[p].cta_off; c < end; ++c) map[static_cast<size_t>(c)] = static_cast<int>(p);
+    size_t p = 0;
+    for (i64 c = 0; c < pl->gemv_ctas; ++c) {  // pair holding CTA c's first row
+      const i64 g0 = c * pl->gemv_rows_per_cta;
+      while (p + 1 < pl->gemv.size() && pl->gemv[p + 1].cta_off <= g0) ++p;
+      map[static_cast<size_t>(c)] = static_cast<int>(p);
     }
     pl->d_gemv_map = to_device(map, st);
+    if (pl->gemv_tma) pl->d_tma_map = to_device(pl->tma_map, st);
   }
   pl->d_sums = to_device(pl->sums, st);
   pl->d_bitems = to_device(pl->bitems, st);
@@ -963,8 +1071,12 @@ Plan& get_plan(oiobf_tbf& b, i64 nv) {
 }
 
 void run_ops(oiobf_tbf& b, Plan& pl, const double2* F, double2* G, cudaStream_t st, int group_filter = -1) {
+  // OIOBF_ABLATE=<digits>: skip these op kinds (timing experiments only; the
+  // result is wrong when set)
+  static const char* ablate = std::getenv("OIOBF_ABLATE");
   for (const Op& op : pl.ops) {
     if (group_filter >= 0 && op.group != group_filter) continue;
+    if (ablate && std::strchr(ablate, '0' + op.kind)) continue;
     if (op.kind == 0) {
       const MPLaunch& m = pl.mps[static_cast<size_t>(op.idx)];
       const double2* in = m.in_buf == BUF_F ? F : pl.scratch.p;
@@ -972,8 +1084,13 @@ void run_ops(oiobf_tbf& b, Plan& pl, const double2* F, double2* G, cudaStream_t 
       const LevelData& ld = b.side[m.side][static_cast<size_t>(m.level)];
       launch_mode_product(m.nsteps, pl.d_steps.p + m.step_begin, m.total_out, pl.d_blks.p, ld.interp.p, in, out, st);
     } else if (op.kind == 1) {
-      launch_gemv(pl.d_gemv_map.p, pl.d_gemv.p, pl.gemv_ctas, static_cast<int>(pl.nv), b.cores.p, pl.scratch.p,
-                  pl.scratch.p, pl.gemv_max_c, st);
+      if (pl.gemv_tma)
+        launch_gemv_tma(pl.d_tma_map.p, pl.d_gemv.p, pl.tma_ctas, pl.gemv_total_rows, pl.tma_rows_per_cta,
+                        static_cast<int>(pl.nv), pl.tma_stages, pl.tma_stage_elems, pl.tma_xcap, b.cores.p,
+                        pl.scratch.p, pl.scratch.p, st);
+      else
+        launch_gemv(pl.d_gemv_map.p, pl.d_gemv.p, pl.gemv_ctas, pl.gemv_total_rows, pl.gemv_rows_per_cta,
+                    static_cast<int>(pl.nv), b.cores.p, pl.scratch.p, pl.scratch.p, pl.gemv_max_c, st);
     } else if (op.kind == 3) {
       const BoxLaunch& bx = pl.boxes[static_cast<size_t>(op.idx)];
       const double2* in = bx.in_buf == BUF_F ? F : pl.scratch.p;
@@ -1260,6 +1377,67 @@ int oiobf_tbf_plan_stats(oiobf_tbf* h, int64_t out[4]) {
     }
   }
   out[3] = macs;
+  CAPI_END
+}
+
+// Debug: run every box launch of the nv=1 plan once with per-CTA phase stamps;
+// out gets, per box launch, [ctas, mean and max (ns) of: desc, stage, modes, reduce, total]
+int oiobf_debug_box_trace(oiobf_tbf* h, const void* dF, void* dG, double* out, int32_t max_launches) {
+  CAPI_BEGIN
+  std::lock_guard<std::mutex> lk(h->mu);
+  TBF_CUDA(cudaSetDevice(h->device));
+  Plan& pl = get_plan(*h, 1);
+  DevBuf<unsigned long long> tr(1 << 22);
+  box_trace_enable(tr.p);
+  int li = 0;
+  for (const Op& op : pl.ops) {
+    if (op.kind != 3 || li >= max_launches) continue;
+    const BoxLaunch& bx = pl.boxes[static_cast<size_t>(op.idx)];
+    const double2* in = bx.in_buf == BUF_F ? static_cast<const double2*>(dF) : pl.scratch.p;
+    double2* o = bx.out_buf == BUF_G ? static_cast<double2*>(dG) : pl.scratch.p;
+    const LevelData& ld = h->side[bx.side][static_cast<size_t>(bx.level)];
+    TBF_CUDA(cudaMemset(tr.p, 0, tr.n * 8));
+    launch_box(bx.nitems, pl.d_bitems.p + bx.item_begin, pl.d_bterms.p + bx.item_begin, bx.info, ld.interp.p, in, o,
+               h->stream);
+    TBF_CUDA(cudaStreamSynchronize(h->stream));
+    const i64 nct = bx.nitems * bx.info.cs;
+    std::vector<unsigned long long> ht(static_cast<size_t>(nct * 8));
+    TBF_CUDA(cudaMemcpy(ht.data(), tr.p, ht.size() * 8, cudaMemcpyDeviceToHost));
+    double* o9 = out + 11 * li;
+    o9[0] = static_cast<double>(nct);
+    unsigned long long t0 = ~0ULL;
+    for (i64 c = 0; c < nct; ++c) t0 = std::min(t0, ht[static_cast<size_t>(c * 8)]);
+    for (int ph = 0; ph < 4; ++ph) {
+      double sum = 0, mx = 0;
+      for (i64 c = 0; c < nct; ++c) {
+        const double dt = static_cast<double>(ht[static_cast<size_t>(c * 8 + ph + 1)] - ht[static_cast<size_t>(c * 8 + ph)]);
+        sum += dt;
+        mx = std::max(mx, dt);
+      }
+      o9[1 + 2 * ph] = sum / nct;
+      o9[2 + 2 * ph] = mx;
+    }
+    double span = 0, late = 0;
+    for (i64 c = 0; c < nct; ++c) {
+      span = std::max(span, static_cast<double>(ht[static_cast<size_t>(c * 8 + 4)] - t0));
+      late = std::max(late, static_cast<double>(ht[static_cast<size_t>(c * 8)] - t0));
+    }
+    o9[9] = span;
+    o9[10] = late;  // last CTA start relative to the first
+    {  // second (warm) execution of the mode phase: stamps 2 -> 7 -> 3
+      double w1 = 0, w2 = 0;
+      for (i64 c = 0; c < nct; ++c) {
+        w1 += static_cast<double>(ht[static_cast<size_t>(c * 8 + 7)] - ht[static_cast<size_t>(c * 8 + 2)]);
+        w2 += static_cast<double>(ht[static_cast<size_t>(c * 8 + 3)] - ht[static_cast<size_t>(c * 8 + 7)]);
+      }
+      o9[5] = w1 / nct;  // modes, first (cold) pass
+      o9[6] = w2 / nct;  // modes, second (warm) pass
+    }
+    // effective SM clock (MHz) of CTA 0: cycles / ns
+    o9[0] += 1e-6 * static_cast<double>(ht[6] - ht[5]) / std::max(1.0, static_cast<double>(ht[4] - ht[0])) * 1000.0;
+    ++li;
+  }
+  box_trace_enable(nullptr);
   CAPI_END
 }
 

@@ -134,6 +134,11 @@ int oiobf_tbf_export(const oiobf_tbf* h, int64_t* ranks, int64_t* ncols, int64_t
                      double* interp, int64_t* perm, double* cores, int64_t* core_rows, int64_t* core_cols,
                      int64_t* r_est);
 
+/* Robustness diagnostic: non-finite entries per (side, level) interp arena
+ * (out[2q], with the level's max rank in out[2q+1]) and in the cores
+ * (out[4*(Lc+1)]). */
+int oiobf_tbf_check_finite(oiobf_tbf* h, int64_t* out);
+
 /* Construction timing breakdown (ms): [proxies+targets, panel TSQR, finish,
  * compaction, cores, total] accumulated over levels. */
 int oiobf_tbf_timings(const oiobf_tbf* h, double out[6]);

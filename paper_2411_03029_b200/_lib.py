@@ -40,7 +40,7 @@ EXPORTS = [
     "oiobf_select_proxies_count", "oiobf_derive_seed", "oiobf_subtensor_at", "oiobf_mode_product_blockdiag",
     "oiobf_tbf_construct", "oiobf_tbf_destroy", "oiobf_tbf_contract", "oiobf_tbf_contract_device",
     "oiobf_tbf_memory", "oiobf_tbf_info", "oiobf_tbf_export", "oiobf_tbf_timings", "oiobf_tbf_plan_stats",
-    "oiobf_tbf_profile_contract", "oiobf_dense_rows",
+    "oiobf_tbf_profile_contract", "oiobf_dense_rows", "oiobf_tbf_check_finite",
 ]
 
 _lock = threading.Lock()
@@ -78,6 +78,7 @@ def load(path: str = LIB_PATH):
         L.oiobf_tbf_timings.argtypes = [C.c_void_p, f64p]
         L.oiobf_tbf_plan_stats.argtypes = [C.c_void_p, i64p]
         L.oiobf_tbf_profile_contract.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, f64p]
+        L.oiobf_tbf_check_finite.argtypes = [C.c_void_p, i64p]
         L.oiobf_dense_rows.argtypes = [C.POINTER(KernelSpecC), f64p, C.c_int64, C.c_int64, i64p, f64p]
         _lib = L
         return L

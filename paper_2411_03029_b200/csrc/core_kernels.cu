@@ -108,7 +108,30 @@ __global__ void k_subtensor(KSpec ks, Counts12 cn, const int* __restrict__ lists
   out[e] = kernel_entry(ks, ii, jj);
 }
 
+__global__ void k_count_nonfinite(const double2* __restrict__ x, long long n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double2 v = x[i];
+    c += !(isfinite(v.x) && isfinite(v.y));
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
 }  // namespace
+
+unsigned long long count_nonfinite(const double2* x, i64 n, cudaStream_t st) {
+  unsigned long long* d = nullptr;
+  TBF_CUDA(cudaMallocAsync(&d, sizeof(unsigned long long), st));
+  TBF_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), st));
+  if (n > 0) k_count_nonfinite<<<148 * 8, 256, 0, st>>>(x, n, d);
+  unsigned long long h = 0;
+  TBF_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+  TBF_CUDA(cudaStreamSynchronize(st));
+  TBF_CUDA(cudaFreeAsync(d, st));
+  return h;
+}
 
 void launch_subtensor(const KSpec& ks, const i64* counts_h, const int* lists, i64 total, double2* out,
                       cudaStream_t st) {

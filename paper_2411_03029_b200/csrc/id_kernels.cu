@@ -63,11 +63,43 @@ __global__ void k_targets(LevelDesc L, const int* __restrict__ crank, const i64*
 // Fold panel X (nrows x w, col-major, ld pr) into upper-triangular R (w x w,
 // col-major, ld w) with Householder reflections.  Column k is owned by warp
 // k % kWarps for the whole panel, so one __syncthreads per column suffices.
+// Reflector for x = [alpha; X(:, j)] (sig = |X(:, j)|^2 > 0) in the normalised
+// form v = [1; X(:, j) * scale], scale = 1 / (alpha + sign * |x|), tau in [1, 2]:
+// |v_i| <= 1, so nothing overflows when sig is tiny (a panel whose rows are
+// exhausted leaves only rounding noise in its trailing columns; the textbook
+// beta = 2 / (|v0|^2 + sig) overflows there and poisons R with Inf*0).
 struct Bcast {
-  double2 v0;
-  double beta;
+  double2 scale;
+  double tau;
   int active;
 };
+
+__device__ __forceinline__ Bcast make_reflector(double2 alpha, double sig, double2* rjj) {
+  Bcast b;
+  if (!(sig > 0)) {
+    b.scale = make_double2(0, 0);
+    b.tau = 0;
+    b.active = 0;
+    return b;
+  }
+  const double aa = sqrt(cnorm2(alpha));
+  const double xnorm = sqrt(cnorm2(alpha) + sig);
+  const double2 sign = aa == 0 ? make_double2(1, 0) : make_double2(alpha.x / aa, alpha.y / aa);
+  const double2 v0 = make_double2(alpha.x + sign.x * xnorm, alpha.y + sign.y * xnorm);
+  b.scale = cdiv(make_double2(1, 0), v0);
+  b.tau = 2.0 / (1.0 + sig * cnorm2(b.scale));
+  b.active = 1;
+  *rjj = make_double2(-sign.x * xnorm, -sign.y * xnorm);
+  return b;
+}
+
+// apply H = I - tau v v^H (v0 = 1) to the column pair (r = R(j, k), X(:, k)):
+// s = r + conj(scale) * sum conj(X_ij) X_ik ; r -= tau s ; X_ik -= X_ij * scale * tau s
+__device__ __forceinline__ double2 reflect_coeff(const Bcast& b, double2 r, double2 dot) {
+  double2 s = r;
+  cfmac(s, b.scale, dot);  // + conj(scale) * dot
+  return cscale(b.tau, s);
+}
 
 __device__ void absorb_panel(double2* __restrict__ R, double2* __restrict__ X, int w, int nrows, int pr,
                              Bcast* bc) {
@@ -77,38 +109,20 @@ __device__ void absorb_panel(double2* __restrict__ R, double2* __restrict__ X, i
       double sig = 0;
       for (int i = lane; i < nrows; i += 32) sig += cnorm2(X[i + j * pr]);
       sig = warp_sum(sig);
-      if (lane == 0) {
-        Bcast b;
-        const double2 alpha = R[j + j * w];
-        if (sig > 0) {
-          const double aa = sqrt(cnorm2(alpha));
-          const double xnorm = sqrt(cnorm2(alpha) + sig);
-          const double2 sign = aa == 0 ? make_double2(1, 0) : make_double2(alpha.x / aa, alpha.y / aa);
-          const double2 v0 = make_double2(alpha.x + sign.x * xnorm, alpha.y + sign.y * xnorm);
-          b.v0 = v0;
-          b.beta = 2.0 / (cnorm2(v0) + sig);
-          b.active = 1;
-          R[j + j * w] = make_double2(-sign.x * xnorm, -sign.y * xnorm);
-        } else {
-          b.v0 = make_double2(0, 0);
-          b.beta = 0;
-          b.active = 0;
-        }
-        bc[j & 1] = b;
-      }
+      if (lane == 0) bc[j & 1] = make_reflector(R[j + j * w], sig, &R[j + j * w]);
     }
     __syncthreads();
     const Bcast b = bc[j & 1];
     if (b.active) {
       int k0 = j + 1 + ((warp - (j + 1) % kWarps) % kWarps + kWarps) % kWarps;
       for (int k = k0; k < w; k += kWarps) {
-        double2 s = make_double2(0, 0);
-        for (int i = lane; i < nrows; i += 32) cfmac(s, X[i + j * pr], X[i + k * pr]);
-        s = warp_sum2(s);
-        cfmac(s, b.v0, R[j + k * w]);
-        const double2 ws = cscale(b.beta, s);
-        if (lane == 0) R[j + k * w] = csub(R[j + k * w], cmul(b.v0, ws));
-        for (int i = lane; i < nrows; i += 32) X[i + k * pr] = csub(X[i + k * pr], cmul(X[i + j * pr], ws));
+        double2 dot = make_double2(0, 0);
+        for (int i = lane; i < nrows; i += 32) cfmac(dot, X[i + j * pr], X[i + k * pr]);
+        dot = warp_sum2(dot);
+        const double2 ws = reflect_coeff(b, R[j + k * w], dot);
+        const double2 t = cmul(b.scale, ws);
+        if (lane == 0) R[j + k * w] = csub(R[j + k * w], ws);
+        for (int i = lane; i < nrows; i += 32) X[i + k * pr] = csub(X[i + k * pr], cmul(X[i + j * pr], t));
       }
     }
   }
@@ -258,29 +272,18 @@ __global__ void __launch_bounds__(kFinThreads) k_finish(LevelDesc L, double tol,
       if (t == 0) {
         double sig = 0;
         for (int i = 0; i <= j; ++i) sig += cnorm2(X[i + j * w]);
-        const double2 alpha = A[j + j * ld];
-        if (sig > 0) {
-          const double aa = sqrt(cnorm2(alpha));
-          const double xnorm = sqrt(cnorm2(alpha) + sig);
-          const double2 sign = aa == 0 ? make_double2(1, 0) : make_double2(alpha.x / aa, alpha.y / aa);
-          const double2 v0 = make_double2(alpha.x + sign.x * xnorm, alpha.y + sign.y * xnorm);
-          bc[0].v0 = v0;
-          bc[0].beta = 2.0 / (cnorm2(v0) + sig);
-          bc[0].active = 1;
-          A[j + j * ld] = make_double2(-sign.x * xnorm, -sign.y * xnorm);
-        } else {
-          bc[0].active = 0;
-        }
+        bc[0] = make_reflector(A[j + j * ld], sig, &A[j + j * ld]);
       }
       __syncthreads();
       if (bc[0].active) {
+        const Bcast b = bc[0];
         for (int k = j + 1 + t; k < w; k += kFinThreads) {
-          double2 s = make_double2(0, 0);
-          for (int i = 0; i <= j; ++i) cfmac(s, X[i + j * w], X[i + k * w]);
-          cfmac(s, bc[0].v0, A[j + k * ld]);
-          const double2 ws = cscale(bc[0].beta, s);
-          A[j + k * ld] = csub(A[j + k * ld], cmul(bc[0].v0, ws));
-          for (int i = 0; i <= j; ++i) X[i + k * w] = csub(X[i + k * w], cmul(X[i + j * w], ws));
+          double2 dot = make_double2(0, 0);
+          for (int i = 0; i <= j; ++i) cfmac(dot, X[i + j * w], X[i + k * w]);
+          const double2 ws = reflect_coeff(b, A[j + k * ld], dot);
+          const double2 tt = cmul(b.scale, ws);
+          A[j + k * ld] = csub(A[j + k * ld], ws);
+          for (int i = 0; i <= j; ++i) X[i + k * w] = csub(X[i + k * w], cmul(X[i + j * w], tt));
         }
       }
       __syncthreads();

@@ -123,6 +123,7 @@ void launch_sum_parent(i64 nctas, const SumDesc* d, const int* cta_map, const do
                        cudaStream_t st);
 
 // ---- dense check (core_kernels.cu)
+unsigned long long count_nonfinite(const double2* x, i64 n, cudaStream_t st);
 void launch_dense_rows(const KSpec& ks, i64 nrows, const i64* rows, const double2* F, int nv, double2* out,
                        cudaStream_t st);
 

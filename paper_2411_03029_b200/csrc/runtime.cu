@@ -1341,6 +1341,22 @@ int oiobf_tbf_export(const oiobf_tbf* h, int64_t* ranks, int64_t* ncols, int64_t
   CAPI_END
 }
 
+// Non-finite entries in the factors: out[2*(side*(Lc+1)+l)] = interp count,
+// out[...+1] = 0; out[2*2*(Lc+1)] = cores.  (robustness diagnostic)
+int oiobf_tbf_check_finite(oiobf_tbf* h, int64_t* out) {
+  CAPI_BEGIN
+  require(h, "tbf_check_finite: null handle");
+  TBF_CUDA(cudaSetDevice(h->device));
+  i64 q = 0;
+  for (int sd = 0; sd < 2; ++sd)
+    for (const auto& lv : h->side[sd]) {
+      out[q++] = static_cast<int64_t>(count_nonfinite(lv.interp.p, lv.total_interp, h->stream));
+      out[q++] = lv.max_rank;
+    }
+  out[q] = static_cast<int64_t>(count_nonfinite(h->cores.p, h->total_core, h->stream));
+  CAPI_END
+}
+
 int oiobf_tbf_timings(const oiobf_tbf* h, double out[6]) {
   CAPI_BEGIN
   require(h, "tbf_timings: null handle");
@@ -1596,8 +1612,10 @@ int oiobf_column_id_batch(int64_t batch, const int64_t* m, const int64_t* n, con
     L.wmax = wmax;
     L.m = mmax;
     L.pr = wmax <= 16 ? 256 : wmax <= 32 ? 128 : wmax <= 64 ? 64 : 32;
+    if (const char* e = std::getenv("OIOBF_ID_PR")) L.pr = std::atoi(e);  // debug override
     i64 parts = std::max<i64>(1, (148 * 8 + batch - 1) / batch);
     parts = std::min(parts, std::max<i64>(1, (mmax + 4 * L.pr - 1) / (4 * L.pr)));
+    if (const char* e = std::getenv("OIOBF_ID_NPARTS")) parts = std::atoi(e);  // debug override
     L.nparts = parts;
     L.rpp = (mmax + parts - 1) / parts;
     std::vector<int> hw(static_cast<size_t>(batch)), ht(static_cast<size_t>(batch * wmax));

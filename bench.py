@@ -20,9 +20,10 @@ G = K x F (Alg. 2) of one n^d input through the compressed operator.
 * --impl reference  the CPU implementation of the path (oracle port, all host
              threads): CPU construction (setup, reported) + timed CPU applies.
 
-Multi-GPU (torchrun, N>1): one process per GPU; each rank builds and applies
-its own replica of the operator (replicas; the sharded plan is DESIGN.md §7),
-max-over-ranks device time, value = all ranks' points / that time.
+Multi-GPU (torchrun, N>1): one process per GPU, the operator sharded by
+middle multi-sets: V/W + core GEMV on the column owner, one NCCL
+all-to-all of the blocks G_{t,s}, P/U on the row owner.  Strong scaling: one
+apply of the whole operator per step; max-over-ranks device time.
 """
 from __future__ import annotations
 
@@ -319,6 +320,117 @@ def run_b200(args):
     return 0
 
 
+def run_b200_sharded(args):
+    """N > 1: one process per GPU, the operator sharded by middle multi-sets
+    (SURVEY §8(e)); one step = phase 1 (V/W + core GEMV) + NCCL all-to-all of
+    the blocks G_{t,s} + phase 2 (P/U).  Strong scaling: the whole job applies
+    ONE operator to ONE input per step."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_03029_b200 as tb
+    from paper_2411_03029_b200 import _lib
+    from paper_2411_03029_b200.sharded import GpuShardBackend, TorchComm, construct
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    _lib.check(_lib.load().oiobf_set_device(local))
+    cfg = BY_NAME[args.config]
+    dev = torch.device("cuda", local)
+    comm = TorchComm(device=dev)
+    sampler = ClockSampler(local)
+    sampler.start()
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    be = GpuShardBackend(cfg.spec, cfg.L, cfg.tol, tb.ProxyStrategy(), cfg.seed, rank, ws)
+    sb = construct(be, rank, ws, comm)
+    torch.cuda.synchronize()
+    construct_s = time.perf_counter() - t0
+    t = torch.tensor([construct_s], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    construct_s = float(t.item())
+
+    Fh = make_input(cfg, cfg.input_seed, args.nv)
+    N = cfg.points * args.nv
+    F = torch.from_numpy(np.ascontiguousarray(Fh.reshape(-1, order="F")).view(np.float64).copy()).to(dev)
+    G = torch.zeros_like(F)
+    lay = sb.layout
+    send = torch.empty(2 * max(1, int(lay.send_counts.sum())) * args.nv, dtype=torch.float64, device=dev)
+    recv = torch.empty(2 * max(1, int(lay.recv_counts.sum())) * args.nv, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        be.phase(1, F.data_ptr(), send.data_ptr(), args.nv, sh)
+        comm.alltoall(send, recv, lay.send_counts * args.nv, lay.recv_counts * args.nv)
+        be.phase(2, recv.data_ptr(), G.data_ptr(), args.nv, sh)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in evs:
+        flush.zero_()
+        a.record(stream)
+        step()
+        b.record(stream)
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    # e2e: pinned host F in, this rank's G out, exchange included
+    pin_F = torch.from_numpy(np.ascontiguousarray(Fh.reshape(-1, order="F")).view(np.float64).copy()).pin_memory()
+    pin_G = torch.empty_like(pin_F).pin_memory()
+    e2e = []
+    dist.barrier()
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        F.copy_(pin_F, non_blocking=True)
+        step()
+        pin_G.copy_(G, non_blocking=True)
+        torch.cuda.synchronize()
+        e2e.append(time.perf_counter() - t1)
+    e2e_ms = 1e3 * statistics.fmean(e2e)
+    t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    # correctness probe: gather G (disjoint slabs) and compare 200 rows with dense sums on rank 0
+    dist.all_reduce(G)
+    clocks = sampler.stop()
+    if rank == 0:
+        rng = np.random.default_rng(1)
+        rows = rng.choice(cfg.points, 200, replace=False)
+        exact = tb.dense_rows(cfg.spec, Fh.reshape((cfg.spec.n,) * cfg.spec.d, order="F"), rows)[:, 0]
+        got = G.cpu().numpy().view(np.complex128)[rows]
+        err = float(np.linalg.norm(got - exact) / np.linalg.norm(exact))
+        out = {
+            "metric": METRIC, "value": N / (ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded complex normal input; operator from the BASELINE formula)",
+            "config": {"workload": cfg.name, "points": cfg.points, "tol": cfg.tol, "L": cfg.L, "nv": args.nv,
+                       "l2": "flushed (256 MiB write) before every timed step",
+                       "parallelism": f"sharded x{ws}: middle multi-sets round-robin, 1 NCCL all-to-all per step"},
+            "e2e": {"value": N / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step": 16 * N,
+                    "d2h_bytes_per_step": 16 * N},
+            "exchange_bytes_per_step_rank0": int(16 * lay.send_counts.sum() * args.nv),
+            "sampled_rel_err_vs_dense": err,
+            "clocks": clocks,
+            "construct": {"gpu_s": construct_s, "sharded": True},
+            "cpu_baseline": None,
+        }
+        print(json.dumps(out), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
 def cpu_baseline(cfg, bf, Fh, nv, budget_s):
     from oracle import Oracle, build
     if not os.path.exists(os.path.join(ROOT, "oracle", "liboracle.so")):
@@ -356,6 +468,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return run_b200_sharded(args)
     return run_b200(args)
 
 

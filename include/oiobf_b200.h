@@ -159,6 +159,30 @@ int oiobf_tbf_profile_contract(oiobf_tbf* h, const void* dF, void* dG, int32_t r
 int oiobf_dense_rows(const oiobf_kernel_spec* spec, const double* F, int64_t nv, int64_t nrows,
                      const int64_t* rows_flat, double* out);
 
+/* ---- sharded (multi-GPU) construction and apply, SURVEY §8(e) -------------
+ * One process per GPU.  Rank r owns the middle multi-sets with index % world
+ * == r on both sides: it builds the V/W IDs of its column multi-sets s, the
+ * U/P IDs of its row multi-sets t, and the cores of the pairs (t, s) with s
+ * owned.  The caller performs the collectives (torch.distributed / NCCL):
+ *   1. oiobf_tbf_shard_begin, then for each side and level l = 0..Lc:
+ *      oiobf_tbf_shard_level(r_est) with r_est = max(8, all-reduce-max of the
+ *      local max ranks of the previous levels of that side)
+ *   2. oiobf_tbf_umid_export -> sum all-reduce -> oiobf_tbf_umid_import
+ *      (row skeletons of every t at level Lc; builds the owned cores)
+ *   3. oiobf_tbf_set_exchange(send / receive offsets of every G_{t,s} block)
+ *   4. apply: oiobf_tbf_contract_phase(1, F, send) ; all-to-all(send -> recv) ;
+ *      oiobf_tbf_contract_phase(2, recv, G).
+ */
+int oiobf_tbf_shard_begin(const oiobf_kernel_spec* spec, int32_t L, double tol, const oiobf_proxy_strategy* proxies,
+                          uint64_t seed, int32_t rank, int32_t world, oiobf_tbf** out);
+int oiobf_tbf_shard_level(oiobf_tbf* h, int32_t side, int32_t level, int64_t r_est, int64_t* local_max_rank);
+int oiobf_tbf_umid_info(oiobf_tbf* h, int64_t out[2]);
+int oiobf_tbf_umid_export(oiobf_tbf* h, int64_t* ranks, int32_t* skel, int64_t wpad);
+int oiobf_tbf_umid_import(oiobf_tbf* h, const int64_t* ranks, const int32_t* skel, int64_t wpad);
+int oiobf_tbf_set_exchange(oiobf_tbf* h, const int64_t* send_off, const int64_t* recv_off, int64_t send_elems,
+                           int64_t recv_elems);
+int oiobf_tbf_contract_phase(oiobf_tbf* h, int32_t phase, const void* dIn, void* dOut, int64_t nv, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -670,7 +670,21 @@ Tensor mode_product_blockdiag(const Tensor& t, int mode /*0-based*/, const std::
 }
 
 // Alg. 2.  F: n^d x nv, G: n^d x nv, first mode fastest.
-void tbf_contract(const TBF& b, const Cx* F, Cx* G, i64 nv, int nthreads) {
+// Sharded apply (mirrors paper_2411_03029_b200/sharded.py): phase 1 = V/W
+// levels + core mat-vec for the owned column multi-sets s, blocks G_{t,s}
+// written at send_off[t*nmid+s]*nv; phase 2 = P/U levels for the owned row
+// multi-sets t, blocks read at recv_off[t*nmid+s]*nv.  phase 0 = everything.
+struct ShardIO {
+  int phase = 0, rank = 0, world = 1;
+  Cx* send = nullptr;
+  const i64* send_off = nullptr;
+  const Cx* recv = nullptr;
+  const i64* recv_off = nullptr;
+};
+
+void tbf_contract(const TBF& b, const Cx* F, Cx* G, i64 nv, int nthreads, const ShardIO* io = nullptr) {
+  const int phase = io ? io->phase : 0;
+  auto own = [&](i64 outer) { return !io || io->world <= 1 || outer % io->world == io->rank; };
   const int d = b.spec.d;
   const i64 n = b.spec.n;
   const i64 mpm = ipow(2, b.Lc);
@@ -697,6 +711,7 @@ void tbf_contract(const TBF& b, const Cx* F, Cx* G, i64 nv, int nthreads) {
     Fl[static_cast<size_t>(l)].assign(static_cast<size_t>(b.nmid * ls.nin), Tensor{});
     parallel_for(b.nmid * ls.nin, nthreads, [&](i64 it) {
       const i64 s = it / ls.nin, tau = it % ls.nin;
+      if (phase == 2 || !own(s)) return;
       Tensor x;
       if (l == 0) {
         x.shape.assign(static_cast<size_t>(d), mid_sz);
@@ -734,6 +749,7 @@ void tbf_contract(const TBF& b, const Cx* F, Cx* G, i64 nv, int nthreads) {
   Gl[static_cast<size_t>(b.Lc)].assign(static_cast<size_t>(b.nmid * b.nmid), Tensor{});
   parallel_for(b.nmid * b.nmid, nthreads, [&](i64 it) {
     const i64 t = it / b.nmid, s = it % b.nmid;  // G index = t * nmid + nu
+    if (phase == 2 || !own(s)) return;
     const i64 p = s * b.nmid + t;
     const Tensor& x = Fl[static_cast<size_t>(b.Lc)][static_cast<size_t>(s * lc.nin + t)];
     const i64 R = b.core_rows[static_cast<size_t>(p)], C = b.core_cols[static_cast<size_t>(p)];
@@ -749,8 +765,31 @@ void tbf_contract(const TBF& b, const Cx* F, Cx* G, i64 nv, int nthreads) {
         for (i64 c = 0; c < C; ++c) acc += K[r + c * R] * x.data[static_cast<size_t>(c + v * C)];
         g.data[static_cast<size_t>(r + v * R)] = acc;
       }
+    if (phase == 1) {
+      Cx* dst = io->send + io->send_off[t * b.nmid + s] * nv;
+      std::copy(g.data.begin(), g.data.end(), dst);
+      return;
+    }
     Gl[static_cast<size_t>(b.Lc)][static_cast<size_t>(it)] = std::move(g);
   });
+  if (phase == 1) return;
+  if (phase == 2) {  // the blocks G_{t,s} of the owned t arrive from the exchange
+    for (i64 t = 0; t < b.nmid; ++t) {
+      if (!own(t)) continue;
+      for (i64 s = 0; s < b.nmid; ++s) {
+        Tensor g;
+        i64 R = 1;
+        for (int k = 0; k < d; ++k) {
+          g.shape.push_back(b.side[1][static_cast<size_t>(b.Lc)][static_cast<size_t>((t * lc.nin + s) * d + k)].rank);
+          R *= g.shape.back();
+        }
+        g.shape.push_back(nv);
+        const Cx* src = io->recv + io->recv_off[t * b.nmid + s] * nv;
+        g.data.assign(src, src + R * nv);
+        Gl[static_cast<size_t>(b.Lc)][static_cast<size_t>(t * b.nmid + s)] = std::move(g);
+      }
+    }
+  }
   // Step 3: l = Lc..1 accumulate through P^T into parents; l = 0 through U^T
   for (int l = b.Lc; l >= 0; --l) {
     const LevelShape ls = level_shape(b, l);
@@ -759,6 +798,7 @@ void tbf_contract(const TBF& b, const Cx* F, Cx* G, i64 nv, int nthreads) {
       Gl[static_cast<size_t>(l - 1)].assign(static_cast<size_t>(b.nmid * npar), Tensor{});
       parallel_for(b.nmid * npar, nthreads, [&](i64 it) {
         const i64 t = it / npar, pnu = it % npar;
+        if (!own(t)) return;
         Tensor acc;
         bool first = true;
         for (i64 nu = 0; nu < ls.nin; ++nu) {  // children of pnu, ascending
@@ -783,6 +823,7 @@ void tbf_contract(const TBF& b, const Cx* F, Cx* G, i64 nv, int nthreads) {
       });
     } else {
       parallel_for(b.nmid, nthreads, [&](i64 t) {
+        if (!own(t)) return;
         Tensor x = Gl[0][static_cast<size_t>(t)];
         std::vector<const Cx*> ptr;
         std::vector<i64> br, bc;
@@ -1199,6 +1240,33 @@ int oracle_tbf_contract(void* h, const double* F, double* G, i64 nv, int nthread
   std::vector<Cx> f = cx_in(F, N), g(static_cast<size_t>(N));
   tbf_contract(b, f.data(), g.data(), nv, nthreads);
   cx_out(g, G);
+  GUARD_END
+}
+
+// Sharded apply phases (test backend for paper_2411_03029_b200/sharded.py).
+int oracle_tbf_contract_phase(void* h, int phase, int rank, int world, const double* in, double* out,
+                              const i64* send_off, const i64* recv_off, i64 send_elems, i64 recv_elems, i64 nv,
+                              int nthreads) {
+  GUARD_BEGIN
+  const TBF& b = *static_cast<TBF*>(h);
+  const i64 N = ipow(b.spec.n, b.spec.d) * nv;
+  ShardIO io;
+  io.phase = phase;
+  io.rank = rank;
+  io.world = world;
+  io.send_off = send_off;
+  io.recv_off = recv_off;
+  if (phase == 1) {
+    std::vector<Cx> f = cx_in(in, N), snd(static_cast<size_t>(std::max<i64>(send_elems * nv, 1)));
+    io.send = snd.data();
+    tbf_contract(b, f.data(), nullptr, nv, nthreads, &io);
+    cx_out(snd, out);
+  } else {
+    std::vector<Cx> rcv = cx_in(in, std::max<i64>(recv_elems * nv, 1)), g = cx_in(out, N);
+    io.recv = rcv.data();
+    tbf_contract(b, nullptr, g.data(), nv, nthreads, &io);
+    cx_out(g, out);
+  }
   GUARD_END
 }
 

@@ -28,7 +28,7 @@ __global__ void k_gen_proxies(LevelDesc L, int* __restrict__ proxies) {
   const i64 slot = tid / D;
   const int p = static_cast<int>(tid % D);
   const SlotPos s = decode_slot(L, slot);
-  if (p == s.skip) return;
+  if (p == s.skip || !owns_outer(L, s.outer)) return;
   const u64 tags[7] = {L.side_tag, static_cast<u64>(L.l), static_cast<u64>(s.outer), static_cast<u64>(s.inner),
                        static_cast<u64>(s.k), static_cast<u64>(s.j), 0ULL};
   const u64 sseed = derive_seed(L.seed, tags, 7);
@@ -48,6 +48,10 @@ __global__ void k_targets(LevelDesc L, const int* __restrict__ crank, const i64*
   if (slot >= L.nslots) return;
   const SlotPos s = decode_slot(L, slot);
   int* out = targets + slot * L.wmax;
+  if (!owns_outer(L, s.outer)) {  // another rank's slot: empty candidate set
+    if (lane == 0) width[slot] = 0;
+    return;
+  }
   if (L.l == 0) {
     for (i64 c = lane; c < s.sz[s.skip]; c += 32) out[c] = static_cast<int>(s.lo[s.skip] + c);
     if (lane == 0) width[slot] = static_cast<int>(s.sz[s.skip]);

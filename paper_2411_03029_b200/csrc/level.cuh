@@ -38,7 +38,14 @@ struct LevelDesc {
   int pr;      // panel rows
   // children (level l-1) for l >= 1
   i64 c_nin, c_nj;
+  // sharded construction: this rank builds only slots whose outer middle
+  // multi-set satisfies outer % world == rank (others get width 0 -> rank 0)
+  int rank, world;
 };
+
+__host__ __device__ inline bool owns_outer(const LevelDesc& L, i64 outer) {
+  return L.world <= 1 || (outer % L.world) == L.rank;
+}
 
 struct SlotPos {
   i64 outer, inner, k, j;

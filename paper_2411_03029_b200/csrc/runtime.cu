@@ -175,7 +175,7 @@ TRef packed(i64 off, int nd, const int* ext) {
   return t;
 }
 
-enum BufId { BUF_F = 0, BUF_G = 1, BUF_SCRATCH = 2 };
+enum BufId { BUF_F = 0, BUF_G = 1, BUF_SCRATCH = 2, BUF_SEND = 3, BUF_RECV = 4 };
 
 struct MPLaunch {
   int side, level;  // factor arena
@@ -230,6 +230,9 @@ struct Plan {
   DevBuf<double2> scratch;
   DevBuf<double2> stage_F, stage_G;  // host-buffer contract staging
   i64 gemv_y_base = 0;
+  // sharded plans (world > 1): phase 1 = V/W + GEMV (writes the send buffer),
+  // phase 2 = P/U (reads the receive buffer)
+  bool sharded = false;
   // graph cache
   cudaGraphExec_t gexec = nullptr;
   const void* g_F = nullptr;
@@ -252,6 +255,18 @@ struct oiobf_tbf {
   u64 seed = 0;
   int device = 0;
   cudaStream_t stream = nullptr;
+  // sharding: this rank owns middle multi-sets with
+  // index % world == rank on both sides
+  int rank = 0, world = 1;
+  bool owns(i64 outer) const { return world <= 1 || outer % world == rank; }
+  // U-side middle-level (l = Lc) ranks / skeletons of ALL t (gathered from the
+  // other ranks) -- the row skeletons of the cores of the owned pairs (t, s)
+  std::vector<int> umid_rank;
+  std::vector<i64> umid_skel_off;
+  DevBuf<int> umid_skel;
+  // exchange tables (element offsets per pair t*nmid+s, nv = 1 units), -1 = none
+  std::vector<i64> send_off, recv_off;
+  i64 send_elems = 0, recv_elems = 0;
   std::vector<LevelData> side[2];
   std::vector<i64> r_est[2];
   DevBuf<double2> cores;
@@ -317,8 +332,11 @@ LevelDesc make_level(const oiobf_tbf& b, int sd, int l, i64 r_est, i64 wmax) {
   }
   L.m = m;
   L.pr = wmax <= 16 ? 256 : wmax <= 32 ? 128 : wmax <= 64 ? 64 : 32;
+  L.rank = b.rank;
+  L.world = b.world;
   const i64 target_ctas = 148 * 8;
-  i64 parts = (target_ctas + L.nslots - 1) / L.nslots;
+  const i64 owned = (L.nslots + b.world - 1) / b.world;
+  i64 parts = (target_ctas + owned - 1) / owned;
   const i64 max_parts = std::max<i64>(1, (L.m + 4 * L.pr - 1) / (4 * L.pr));  // >= 4 panels per part
   parts = std::max<i64>(1, std::min(parts, max_parts));
   L.nparts = parts;
@@ -411,11 +429,18 @@ void build_side_level(oiobf_tbf& b, int sd, int l, i64 r_est) {
   // default rank limit it is unreachable, so it is only reported.
 }
 
+// Cores K(tbar, sbar) of the pairs (t, s) whose s this rank owns (all pairs
+// when world == 1).  Row skeletons come from the U side at level Lc -- local
+// when world == 1, gathered from every rank (umid_*) otherwise.
 void build_cores(oiobf_tbf& b) {
   cudaStream_t st = b.stream;
   const int d = b.d;
   const LevelData& U = b.side[1][static_cast<size_t>(b.Lc)];
   const LevelData& V = b.side[0][static_cast<size_t>(b.Lc)];
+  const bool gathered = b.world > 1;
+  const int* urank = gathered ? b.umid_rank.data() : U.h_rank.data();
+  const i64* uskel_off = gathered ? b.umid_skel_off.data() : U.h_skel_off.data();
+  const int* uskel = gathered ? b.umid_skel.p : U.skel.p;
   const i64 P = b.nmid * b.nmid;
   b.h_pairs.assign(static_cast<size_t>(P), PairDesc{});
   i64 off = 0;
@@ -427,13 +452,14 @@ void build_cores(oiobf_tbf& b) {
     for (int k = 0; k < d; ++k) {
       const i64 us = (t * b.nmid + s) * d + k;  // U slot (Lc, t, nu=s, k, j=0)
       const i64 vs = (s * b.nmid + t) * d + k;  // V slot (Lc, s, tau=t, k, j=0)
-      pd.rr[k] = U.h_rank[static_cast<size_t>(us)];
+      pd.rr[k] = urank[us];
       pd.rc[k] = V.h_rank[static_cast<size_t>(vs)];
-      pd.rs_off[k] = U.h_skel_off[static_cast<size_t>(us)];
+      pd.rs_off[k] = uskel_off[us];
       pd.cs_off[k] = V.h_skel_off[static_cast<size_t>(vs)];
       pd.R *= pd.rr[k];
       pd.C *= pd.rc[k];
     }
+    if (!b.owns(s)) pd.C = 0;  // another rank generates and applies this core
     pd.core_off = off;
     pd.work_off = off;
     off += static_cast<i64>(pd.R) * pd.C;
@@ -442,7 +468,7 @@ void build_cores(oiobf_tbf& b) {
   b.cores.alloc(static_cast<size_t>(std::max<i64>(off, 1)));
   DevBuf<PairDesc> dp = to_device(b.h_pairs, st);
   EventTimer t(st);
-  launch_cores(b.ks, P, dp.p, off, U.skel.p, V.skel.p, b.cores.p, st);
+  launch_cores(b.ks, P, dp.p, off, uskel, V.skel.p, b.cores.p, st);
   b.t_ms[4] += t.stop();
 }
 
@@ -455,13 +481,15 @@ void validate_spec(const oiobf_kernel_spec& s) {
   if (s.bitrev) require((s.n & (s.n - 1)) == 0, "reorder_bit_reversal: extent must be a power of two");
 }
 
-oiobf_tbf* construct(const oiobf_kernel_spec& spec, int L, double tol, const oiobf_proxy_strategy& ps, u64 seed) {
+std::unique_ptr<oiobf_tbf> construct_begin(const oiobf_kernel_spec& spec, int L, double tol,
+                                           const oiobf_proxy_strategy& ps, u64 seed, int rank, int world) {
   validate_spec(spec);
   require(L >= 0 && L % 2 == 0, "tbf_construct: L must be even and >= 0");
   require((spec.n >> L) >= 1 && spec.n % (i64{1} << L) == 0, "tbf_construct: extent must equal C_b * 2^L");
   require(tol > 0 && tol < 1, "column_id: tolerance must be in (0,1)");
   require(ps.q >= 1 && ps.row_cap >= 1, "ProxyStrategy: q and row_cap must be positive");
   require(ps.mode >= 0 && ps.mode <= 2, "ProxyStrategy: unknown mode");
+  require(world >= 1 && rank >= 0 && rank < world, "tbf_construct: bad rank / world");
   ensure_device();
   auto b = std::make_unique<oiobf_tbf>();
   b->spec = spec;
@@ -475,10 +503,17 @@ oiobf_tbf* construct(const oiobf_kernel_spec& spec, int L, double tol, const oio
   b->strat = ps;
   b->seed = seed;
   b->device = g_device;
+  b->rank = rank;
+  b->world = world;
+  for (int sd = 0; sd < 2; ++sd) b->side[sd].resize(static_cast<size_t>(b->Lc + 1));
   TBF_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
+  return b;
+}
+
+oiobf_tbf* construct(const oiobf_kernel_spec& spec, int L, double tol, const oiobf_proxy_strategy& ps, u64 seed) {
+  auto b = construct_begin(spec, L, tol, ps, seed, 0, 1);
   auto t_start = std::chrono::steady_clock::now();
   for (int sd = 0; sd < 2; ++sd) {
-    b->side[sd].resize(static_cast<size_t>(b->Lc + 1));
     i64 r_est = 8;
     for (int l = 0; l <= b->Lc; ++l) {
       b->r_est[sd].push_back(r_est);
@@ -679,6 +714,7 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
     std::vector<TRef> in(static_cast<size_t>(nitems));
     for (i64 it = 0; it < nitems; ++it) {
       const i64 s = it / nin, tau = it % nin;
+      if (!b.owns(s)) continue;  // another rank's column multi-set
       in[static_cast<size_t>(it)] =
           l == 0 ? global_slab(s) : cur[static_cast<size_t>(s * ipow(2, static_cast<i64>(d) * (l - 1)) + parent_of(tau, l))];
     }
@@ -690,6 +726,7 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
     const i64 nbeta = ipow(nj, d);
     for (i64 it = 0; it < nitems; ++it) {
       const i64 s = it / nin, tau = it % nin;
+      if (!b.owns(s)) continue;
       const TRef& x = in[static_cast<size_t>(it)];
       std::vector<std::vector<int>> R(d), W(d);
       std::vector<std::vector<i64>> MO(d);
@@ -753,6 +790,7 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
       std::vector<std::vector<Blk>> blocks;
       for (i64 it = 0; it < nitems; ++it) {
         const i64 s = it / nin, tau = it % nin;
+        if (!b.owns(s)) continue;
         TRef& x = in[static_cast<size_t>(it)];
         int oext[kMaxTM];
         for (int p = 0; p < nd; ++p) oext[p] = x.ext[p];
@@ -786,19 +824,39 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
   std::vector<TRef> gts(static_cast<size_t>(b.nmid * b.nmid));  // index t * nmid + s
   i64 ctas = 0;
   const int rpc = gemv_rows_per_cta();
+  const bool sharded = b.world > 1;
+  pl->sharded = sharded;
+  if (sharded)
+    require(static_cast<i64>(b.send_off.size()) == b.nmid * b.nmid &&
+                static_cast<i64>(b.recv_off.size()) == b.nmid * b.nmid,
+            "sharded contract: exchange layout not set (oiobf_tbf_set_exchange)");
+  const int* urank = sharded ? b.umid_rank.data() : ULc.h_rank.data();
   for (i64 p = 0; p < b.nmid * b.nmid; ++p) {
     const i64 s = p / b.nmid, t = p % b.nmid;
-    const PairDesc& pd = b.h_pairs[static_cast<size_t>(p)];
-    const TRef& x = cur[static_cast<size_t>(s * b.nmid + t)];
     int gext[kMaxTM];
     i64 R = 1;
     for (int k = 0; k < d; ++k) {
-      gext[k] = ULc.h_rank[static_cast<size_t>((t * b.nmid + s) * d + k)];
+      gext[k] = urank[(t * b.nmid + s) * d + k];
       R *= gext[k];
     }
     gext[d] = static_cast<int>(nv);
-    TRef y = alloc(nd, gext);
-    gts[static_cast<size_t>(t * b.nmid + s)] = y;
+    if (sharded && b.owns(t)) {  // P/U input G_{t,s} arrives in the receive buffer
+      const i64 ro = b.recv_off[static_cast<size_t>(t * b.nmid + s)];
+      require(ro >= 0, "sharded contract: missing receive offset");
+      gts[static_cast<size_t>(t * b.nmid + s)] = packed(ro * nv, nd, gext);
+    }
+    if (!b.owns(s)) continue;
+    const PairDesc& pd = b.h_pairs[static_cast<size_t>(p)];
+    const TRef& x = cur[static_cast<size_t>(s * b.nmid + t)];
+    TRef y;
+    if (sharded) {  // GEMV output goes straight into the send buffer
+      const i64 so = b.send_off[static_cast<size_t>(t * b.nmid + s)];
+      require(so >= 0, "sharded contract: missing send offset");
+      y = packed(so * nv, nd, gext);
+    } else {
+      y = alloc(nd, gext);
+      gts[static_cast<size_t>(t * b.nmid + s)] = y;
+    }
     if (R != pd.R || x.size() != static_cast<i64>(pd.C) * nv) throw std::runtime_error("internal: core shape mismatch");
     GemvDesc g;
     g.core_off = pd.core_off;
@@ -884,6 +942,7 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
     std::vector<SumDesc> psums;
     for (i64 t = 0; t < b.nmid; ++t)
       for (i64 pnu = 0; pnu < pnin; ++pnu) {
+        if (!b.owns(t)) continue;  // another rank's row multi-set
         std::vector<i64> kids;
         for (i64 nu = 0; nu < nin; ++nu)
           if (l == 0 || parent_of(nu, l) == pnu) kids.push_back(nu);
@@ -953,7 +1012,8 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
           psums.push_back(sdsc);
         }
       }
-    if (commit_boxes(items, terms, 1, l, BUF_SCRATCH, l == 0 ? BUF_G : BUF_SCRATCH, 1, 2)) {
+    const int u_in = (sharded && l == b.Lc) ? BUF_RECV : BUF_SCRATCH;
+    if (commit_boxes(items, terms, 1, l, u_in, l == 0 ? BUF_G : BUF_SCRATCH, 1, 2)) {
       if (l > 0) {
         SumLaunch sl;
         sl.begin = static_cast<i64>(pl->sums.size());
@@ -981,6 +1041,7 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
       const bool last_global = (l == 0 && k == d - 1);
       for (i64 it = 0; it < nitems; ++it) {
         const i64 t = it / nin, nu = it % nin;
+        if (!b.owns(t)) continue;
         TRef& xi = x[static_cast<size_t>(it)];
         int oext[kMaxTM];
         for (int p = 0; p < nd; ++p) oext[p] = xi.ext[p];
@@ -1005,7 +1066,7 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
         blocks.push_back(bl);
         xi = y;
       }
-      add_mp(*pl, 1, l, BUF_SCRATCH, last_global ? BUF_G : BUF_SCRATCH, mitems, blocks, 2);
+      add_mp(*pl, 1, l, (k == 0 ? u_in : BUF_SCRATCH), last_global ? BUF_G : BUF_SCRATCH, mitems, blocks, 2);
     }
     if (l > 0) {
       std::vector<TRef> par2(static_cast<size_t>(b.nmid * pnin));
@@ -1014,6 +1075,7 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
       i64 work = 0;
       for (i64 t = 0; t < b.nmid; ++t)
         for (i64 pnu = 0; pnu < pnin; ++pnu) {
+          if (!b.owns(t)) continue;
           SumDesc sdsc{};
           TRef first;
           for (i64 nu = 0; nu < nin; ++nu) {
@@ -1070,34 +1132,46 @@ Plan& get_plan(oiobf_tbf& b, i64 nv) {
   return *slot;
 }
 
-void run_ops(oiobf_tbf& b, Plan& pl, const double2* F, double2* G, cudaStream_t st, int group_filter = -1) {
+struct OpBuffers {
+  const double2* F = nullptr;
+  double2* G = nullptr;
+  double2* send = nullptr;
+  const double2* recv = nullptr;
+};
+
+// phase: 0 = whole contraction, 1 = V/W + core GEMV, 2 = P/U (sharded)
+void run_ops(oiobf_tbf& b, Plan& pl, const OpBuffers& io, cudaStream_t st, int group_filter = -1, int phase = 0) {
   // OIOBF_ABLATE=<digits>: skip these op kinds (timing experiments only; the
   // result is wrong when set)
   static const char* ablate = std::getenv("OIOBF_ABLATE");
+  auto in_ptr = [&](int id) -> const double2* {
+    return id == BUF_F ? io.F : id == BUF_RECV ? io.recv : pl.scratch.p;
+  };
+  auto out_ptr = [&](int id) -> double2* { return id == BUF_G ? io.G : id == BUF_SEND ? io.send : pl.scratch.p; };
   for (const Op& op : pl.ops) {
     if (group_filter >= 0 && op.group != group_filter) continue;
+    if (phase == 1 && op.group == 2) continue;
+    if (phase == 2 && op.group != 2) continue;
     if (ablate && std::strchr(ablate, '0' + op.kind)) continue;
     if (op.kind == 0) {
       const MPLaunch& m = pl.mps[static_cast<size_t>(op.idx)];
-      const double2* in = m.in_buf == BUF_F ? F : pl.scratch.p;
-      double2* out = m.out_buf == BUF_G ? G : pl.scratch.p;
       const LevelData& ld = b.side[m.side][static_cast<size_t>(m.level)];
-      launch_mode_product(m.nsteps, pl.d_steps.p + m.step_begin, m.total_out, pl.d_blks.p, ld.interp.p, in, out, st);
+      launch_mode_product(m.nsteps, pl.d_steps.p + m.step_begin, m.total_out, pl.d_blks.p, ld.interp.p,
+                          in_ptr(m.in_buf), out_ptr(m.out_buf), st);
     } else if (op.kind == 1) {
+      double2* y = pl.sharded ? io.send : pl.scratch.p;
       if (pl.gemv_tma)
         launch_gemv_tma(pl.d_tma_map.p, pl.d_gemv.p, pl.tma_ctas, pl.gemv_total_rows, pl.tma_rows_per_cta,
                         static_cast<int>(pl.nv), pl.tma_stages, pl.tma_stage_elems, pl.tma_xcap, b.cores.p,
-                        pl.scratch.p, pl.scratch.p, st);
+                        pl.scratch.p, y, st);
       else
         launch_gemv(pl.d_gemv_map.p, pl.d_gemv.p, pl.gemv_ctas, pl.gemv_total_rows, pl.gemv_rows_per_cta,
-                    static_cast<int>(pl.nv), b.cores.p, pl.scratch.p, pl.scratch.p, pl.gemv_max_c, st);
+                    static_cast<int>(pl.nv), b.cores.p, pl.scratch.p, y, pl.gemv_max_c, st);
     } else if (op.kind == 3) {
       const BoxLaunch& bx = pl.boxes[static_cast<size_t>(op.idx)];
-      const double2* in = bx.in_buf == BUF_F ? F : pl.scratch.p;
-      double2* out = bx.out_buf == BUF_G ? G : pl.scratch.p;
       const LevelData& ld = b.side[bx.side][static_cast<size_t>(bx.level)];
-      launch_box(bx.nitems, pl.d_bitems.p + bx.item_begin, pl.d_bterms.p + bx.item_begin, bx.info, ld.interp.p, in,
-                 out, st);
+      launch_box(bx.nitems, pl.d_bitems.p + bx.item_begin, pl.d_bterms.p + bx.item_begin, bx.info, ld.interp.p,
+                 in_ptr(bx.in_buf), out_ptr(bx.out_buf), st);
     } else if (op.kind == 4) {
       const SumLaunch& s = pl.sum_launches[static_cast<size_t>(op.idx)];
       launch_sum_parent(s.total, pl.d_sums.p + s.begin, pl.d_sum_map.p + 2 * s.work_begin, pl.scratch.p,
@@ -1107,6 +1181,13 @@ void run_ops(oiobf_tbf& b, Plan& pl, const double2* F, double2* G, cudaStream_t 
       launch_sum_children(s.n, pl.d_sums.p + s.begin, s.total, pl.scratch.p, pl.scratch.p, st);
     }
   }
+}
+
+void run_ops(oiobf_tbf& b, Plan& pl, const double2* F, double2* G, cudaStream_t st, int group_filter = -1) {
+  OpBuffers io;
+  io.F = F;
+  io.G = G;
+  run_ops(b, pl, io, st, group_filter, 0);
 }
 
 void contract_device(oiobf_tbf& b, const double2* F, double2* G, i64 nv, cudaStream_t st) {
@@ -1219,9 +1300,131 @@ int oiobf_tbf_destroy(oiobf_tbf* h) {
   CAPI_END
 }
 
+// ---- sharded construction / apply ---------------------------
+int oiobf_tbf_shard_begin(const oiobf_kernel_spec* spec, int32_t L, double tol, const oiobf_proxy_strategy* proxies,
+                          uint64_t seed, int32_t rank, int32_t world, oiobf_tbf** out) {
+  CAPI_BEGIN
+  require(spec && proxies && out, "tbf_shard_begin: null argument");
+  *out = construct_begin(*spec, L, tol, *proxies, seed, rank, world).release();
+  CAPI_END
+}
+
+int oiobf_tbf_shard_level(oiobf_tbf* h, int32_t side, int32_t level, int64_t r_est, int64_t* local_max_rank) {
+  CAPI_BEGIN
+  require(h && local_max_rank, "tbf_shard_level: null argument");
+  require(side == 0 || side == 1, "tbf_shard_level: side must be 0 (V/W) or 1 (U/P)");
+  require(level >= 0 && level <= h->Lc, "tbf_shard_level: level out of range");
+  require(static_cast<int>(h->r_est[side].size()) == level, "tbf_shard_level: levels must be built in order");
+  std::lock_guard<std::mutex> lk(h->mu);
+  TBF_CUDA(cudaSetDevice(h->device));
+  h->r_est[side].push_back(r_est);
+  build_side_level(*h, side, level, r_est);
+  *local_max_rank = h->side[side][static_cast<size_t>(level)].max_rank;
+  CAPI_END
+}
+
+// out[0] = number of U-side middle slots (nmid * nmid * d), out[1] = local max rank there
+int oiobf_tbf_umid_info(oiobf_tbf* h, int64_t out[2]) {
+  CAPI_BEGIN
+  require(h && static_cast<int>(h->side[1].size()) == h->Lc + 1 && !h->side[1].back().h_rank.empty(),
+          "tbf_umid_info: U side not built");
+  const LevelData& U = h->side[1].back();
+  out[0] = U.nslots;
+  out[1] = U.max_rank;
+  CAPI_END
+}
+
+// ranks[nslots] and skeletons (nslots x wpad, zero padded) of this rank's
+// U-side middle slots; other slots are left at zero (sum-reduce to gather)
+int oiobf_tbf_umid_export(oiobf_tbf* h, int64_t* ranks, int32_t* skel, int64_t wpad) {
+  CAPI_BEGIN
+  require(h && ranks && skel, "tbf_umid_export: null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  TBF_CUDA(cudaSetDevice(h->device));
+  const LevelData& U = h->side[1].back();
+  require(wpad >= U.max_rank, "tbf_umid_export: wpad smaller than the local max rank");
+  std::vector<int> hs(static_cast<size_t>(U.total_skel));
+  U.skel.download(hs.data(), hs.size(), h->stream);
+  TBF_CUDA(cudaStreamSynchronize(h->stream));
+  for (i64 q = 0; q < U.nslots; ++q) {
+    const int r = U.h_rank[static_cast<size_t>(q)];
+    ranks[q] = r;
+    for (int i = 0; i < wpad; ++i)
+      skel[q * wpad + i] = i < r ? hs[static_cast<size_t>(U.h_skel_off[static_cast<size_t>(q)] + i)] : 0;
+  }
+  CAPI_END
+}
+
+// install the gathered U-side middle ranks / skeletons of all ranks and
+// generate the cores of the pairs (t, s) whose s this rank owns
+int oiobf_tbf_umid_import(oiobf_tbf* h, const int64_t* ranks, const int32_t* skel, int64_t wpad) {
+  CAPI_BEGIN
+  require(h && ranks && skel, "tbf_umid_import: null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  TBF_CUDA(cudaSetDevice(h->device));
+  require(static_cast<int>(h->side[0].size()) == h->Lc + 1 && !h->side[0].back().h_rank.empty(),
+          "tbf_umid_import: V side not built");
+  const LevelData& U = h->side[1].back();
+  h->umid_rank.assign(static_cast<size_t>(U.nslots), 0);
+  h->umid_skel_off.assign(static_cast<size_t>(U.nslots), 0);
+  std::vector<int> flat;
+  for (i64 q = 0; q < U.nslots; ++q) {
+    require(ranks[q] >= 0 && ranks[q] <= wpad, "tbf_umid_import: bad rank");
+    h->umid_rank[static_cast<size_t>(q)] = static_cast<int>(ranks[q]);
+    h->umid_skel_off[static_cast<size_t>(q)] = static_cast<i64>(flat.size());
+    for (i64 i = 0; i < ranks[q]; ++i) flat.push_back(skel[q * wpad + i]);
+    if (h->owns(q / (h->nmid * h->d)))  // own slots must agree with the gathered copy
+      require(U.h_rank[static_cast<size_t>(q)] == ranks[q], "tbf_umid_import: gathered ranks disagree");
+  }
+  if (flat.empty()) flat.push_back(0);
+  h->umid_skel = to_device(flat, h->stream);
+  build_cores(*h);
+  TBF_CUDA(cudaStreamSynchronize(h->stream));
+  CAPI_END
+}
+
+// Exchange layout (element offsets at nv = 1 of every G_{t,s} block in this
+// rank's send / receive buffers, index t * nmid + s, -1 = not exchanged here)
+int oiobf_tbf_set_exchange(oiobf_tbf* h, const int64_t* send_off, const int64_t* recv_off, int64_t send_elems,
+                           int64_t recv_elems) {
+  CAPI_BEGIN
+  require(h && send_off && recv_off, "tbf_set_exchange: null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  const i64 P = h->nmid * h->nmid;
+  h->send_off.assign(send_off, send_off + P);
+  h->recv_off.assign(recv_off, recv_off + P);
+  h->send_elems = send_elems;
+  h->recv_elems = recv_elems;
+  h->plans.clear();
+  CAPI_END
+}
+
+// phase 1: dIn = F (n^d x nv), dOut = send buffer; phase 2: dIn = receive
+// buffer, dOut = G (only this rank's row slabs are written)
+int oiobf_tbf_contract_phase(oiobf_tbf* h, int32_t phase, const void* dIn, void* dOut, int64_t nv, void* stream) {
+  CAPI_BEGIN
+  require(h && dIn && dOut, "tbf_contract_phase: null argument");
+  require(phase == 1 || phase == 2, "tbf_contract_phase: phase must be 1 or 2");
+  require(nv >= 1, "tbf_contract: nv must be >= 1");
+  std::lock_guard<std::mutex> lk(h->mu);
+  TBF_CUDA(cudaSetDevice(h->device));
+  Plan& pl = get_plan(*h, nv);
+  OpBuffers io;
+  if (phase == 1) {
+    io.F = static_cast<const double2*>(dIn);
+    io.send = static_cast<double2*>(dOut);
+  } else {
+    io.recv = static_cast<const double2*>(dIn);
+    io.G = static_cast<double2*>(dOut);
+  }
+  run_ops(*h, pl, io, static_cast<cudaStream_t>(stream), -1, phase);
+  CAPI_END
+}
+
 int oiobf_tbf_contract_device(oiobf_tbf* h, const void* dF, void* dG, int64_t nv, void* stream) {
   CAPI_BEGIN
   require(h && dF && dG, "tbf_contract: null argument");
+  require(h->world == 1, "tbf_contract: sharded factorization -- use oiobf_tbf_contract_phase");
   std::lock_guard<std::mutex> lk(h->mu);
   contract_device(*h, static_cast<const double2*>(dF), static_cast<double2*>(dG), nv,
                   static_cast<cudaStream_t>(stream));

@@ -1,0 +1,263 @@
+"""Sharded (multi-GPU) tensor butterfly — SURVEY.md §8(e), DESIGN.md §7.
+
+One process per GPU.  Rank r owns the middle multi-sets with index % world == r
+on both sides: the V/W IDs of its column multi-sets s and the cores of the
+pairs (t, s) it owns, the U/P IDs of its row multi-sets t.  Collectives:
+
+* construction: one all-reduce(max) of the local max rank per (side, level)
+  (level-synchronous r_est) and one sum-all-reduce of the
+  U-side middle skeletons (the row skeletons of every core);
+* apply: V/W levels + core GEMV on the s-owner, ONE all-to-all of the blocks
+  G_{t,s} to the t-owner, P/U levels on the t-owner.
+
+The exchange layout (which block goes where, in which order) is pure integer
+logic in this module (`exchange_layout`), shared by every backend: the GPU
+library (`GpuShardBackend`, C ABI) in production, the CPU oracle in the gloo
+tests.  `Comm` abstracts the collectives: `TorchComm` (torch.distributed,
+NCCL on GPUs / gloo on CPU) and `run_lockstep` (emulated ranks in one process,
+used by the single-GPU test).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .configs import KernelSpec
+
+
+def owns(outer: int, rank: int, world: int) -> bool:
+    return world <= 1 or outer % world == rank
+
+
+@dataclass
+class Layout:
+    send_off: np.ndarray  # int64[nmid*nmid], element offsets at nv = 1, -1 = none
+    recv_off: np.ndarray
+    send_counts: np.ndarray  # int64[world], elements per destination
+    recv_counts: np.ndarray  # int64[world], elements per source
+
+
+def exchange_layout(R: np.ndarray, rank: int, world: int) -> Layout:
+    """R[t, s] = rows of G_{t,s} (prod of the U-side middle ranks).  The send
+    buffer holds, per destination q (ascending), the blocks (t owned by q,
+    s owned by me) in (t, s) order; the receive buffer holds, per source q, the
+    blocks (t owned by me, s owned by q) in the same (t, s) order, so sender and
+    receiver agree without any extra metadata."""
+    nmid = R.shape[0]
+    send_off = np.full(nmid * nmid, -1, np.int64)
+    recv_off = np.full(nmid * nmid, -1, np.int64)
+    send_counts = np.zeros(world, np.int64)
+    recv_counts = np.zeros(world, np.int64)
+    cur = 0
+    for q in range(world):
+        start = cur
+        for t in range(nmid):
+            if not owns(t, q, world):
+                continue
+            for s in range(nmid):
+                if owns(s, rank, world):
+                    send_off[t * nmid + s] = cur
+                    cur += int(R[t, s])
+        send_counts[q] = cur - start
+    cur = 0
+    for q in range(world):
+        start = cur
+        for t in range(nmid):
+            if not owns(t, rank, world):
+                continue
+            for s in range(nmid):
+                if owns(s, q, world):
+                    recv_off[t * nmid + s] = cur
+                    cur += int(R[t, s])
+        recv_counts[q] = cur - start
+    return Layout(send_off, recv_off, send_counts, recv_counts)
+
+
+class GpuShardBackend:
+    """Product backend: the sm_100a library through the C ABI."""
+
+    def __init__(self, spec: KernelSpec, L: int, tol: float, proxies, seed: int, rank: int, world: int):
+        Lb = _lib.load()
+        _declare(Lb)
+        self.spec, self.L = spec, L
+        self.d = spec.d
+        self.Lc = L // 2
+        self.nmid = 2 ** (spec.d * self.Lc)
+        h = C.c_void_p()
+        sc = _lib.spec_c(spec)
+        ps = proxies.c()
+        _lib.check(Lb.oiobf_tbf_shard_begin(C.byref(sc), L, tol, C.byref(ps), seed, rank, world, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            _lib.load().oiobf_tbf_destroy(self.h)
+        except Exception:
+            pass
+
+    def level(self, side: int, l: int, r_est: int) -> int:
+        out = C.c_int64()
+        _lib.check(_lib.load().oiobf_tbf_shard_level(self.h, side, l, r_est, C.byref(out)))
+        return int(out.value)
+
+    def umid_info(self):
+        out = np.zeros(2, np.int64)
+        _lib.check(_lib.load().oiobf_tbf_umid_info(self.h, out))
+        return int(out[0]), int(out[1])
+
+    def umid_export(self, wpad: int):
+        n, _ = self.umid_info()
+        ranks = np.zeros(n, np.int64)
+        skel = np.zeros(n * max(wpad, 1), np.int32)
+        _lib.check(_lib.load().oiobf_tbf_umid_export(self.h, ranks, skel, wpad))
+        return ranks, skel
+
+    def umid_import(self, ranks: np.ndarray, skel: np.ndarray, wpad: int):
+        _lib.check(_lib.load().oiobf_tbf_umid_import(self.h, np.ascontiguousarray(ranks, np.int64),
+                                                     np.ascontiguousarray(skel, np.int32), wpad))
+
+    def set_exchange(self, lay: Layout):
+        _lib.check(_lib.load().oiobf_tbf_set_exchange(self.h, lay.send_off, lay.recv_off,
+                                                      int(lay.send_counts.sum()), int(lay.recv_counts.sum())))
+
+    def phase(self, phase: int, src_ptr: int, dst_ptr: int, nv: int, stream: int = 0):
+        _lib.check(_lib.load().oiobf_tbf_contract_phase(self.h, phase, C.c_void_p(src_ptr), C.c_void_p(dst_ptr), nv,
+                                                        C.c_void_p(stream)))
+
+
+def _declare(Lb):
+    if getattr(Lb, "_shard_declared", False):
+        return
+    i64p, i32p = _lib.i64p, _lib.i32p
+    Lb.oiobf_tbf_shard_begin.argtypes = [C.POINTER(_lib.KernelSpecC), C.c_int32, C.c_double,
+                                         C.POINTER(_lib.ProxyStrategyC), C.c_uint64, C.c_int32, C.c_int32,
+                                         C.POINTER(C.c_void_p)]
+    Lb.oiobf_tbf_shard_level.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.POINTER(C.c_int64)]
+    Lb.oiobf_tbf_umid_info.argtypes = [C.c_void_p, i64p]
+    Lb.oiobf_tbf_umid_export.argtypes = [C.c_void_p, i64p, i32p, C.c_int64]
+    Lb.oiobf_tbf_umid_import.argtypes = [C.c_void_p, i64p, i32p, C.c_int64]
+    Lb.oiobf_tbf_set_exchange.argtypes = [C.c_void_p, i64p, i64p, C.c_int64, C.c_int64]
+    Lb.oiobf_tbf_contract_phase.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+    Lb._shard_declared = True
+
+
+class ShardedButterfly:
+    """Step-wise sharded construction/apply for one rank.  Collectives are the
+    caller's (`construct` / `contract` below do them with a Comm)."""
+
+    def __init__(self, backend, rank: int, world: int):
+        self.be, self.rank, self.world = backend, rank, world
+        self.nmid, self.d, self.Lc = backend.nmid, backend.d, backend.Lc
+        self.layout: Layout | None = None
+        self.R = None
+
+
+class TorchComm:
+    """Collectives over torch.distributed (NCCL for CUDA tensors, gloo on CPU)."""
+
+    def __init__(self, group=None, device=None):
+        import torch.distributed as dist
+        self.dist, self.group, self.device = dist, group, device
+
+    def allreduce_max_int(self, v: int) -> int:
+        import torch
+        t = torch.tensor([v], dtype=torch.int64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return int(t.item())
+
+    def allreduce_sum_np(self, a: np.ndarray) -> np.ndarray:
+        import torch
+        t = torch.from_numpy(np.ascontiguousarray(a).astype(np.int64)).to(self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return t.cpu().numpy()
+
+    def alltoall(self, send, recv, send_counts, recv_counts):
+        """send/recv: float64 tensors (complex interleaved); counts in complex elements."""
+        self.dist.all_to_all_single(recv, send, [2 * int(c) for c in recv_counts], [2 * int(c) for c in send_counts],
+                                    group=self.group)
+
+
+def construct(backend, rank: int, world: int, comm) -> ShardedButterfly:
+    """Sharded construction with real collectives (one rank per process)."""
+    sb = ShardedButterfly(backend, rank, world)
+    for side in (0, 1):
+        r_est = 8
+        for l in range(sb.Lc + 1):
+            local = backend.level(side, l, r_est)
+            r_est = max(r_est, comm.allreduce_max_int(local))
+    _, local_max = backend.umid_info()
+    wpad = max(1, comm.allreduce_max_int(local_max))
+    ranks, skel = backend.umid_export(wpad)
+    ranks_all = comm.allreduce_sum_np(ranks)
+    skel_all = comm.allreduce_sum_np(skel).astype(np.int32)
+    backend.umid_import(ranks_all, skel_all, wpad)
+    _finish_layout(sb, ranks_all)
+    return sb
+
+
+def _finish_layout(sb: ShardedButterfly, ranks_all: np.ndarray):
+    nmid, d = sb.nmid, sb.d
+    r = ranks_all.reshape(nmid, nmid, d)  # [t, s, k]  (U slot (Lc, t, nu=s, k))
+    sb.R = np.prod(r, axis=2)
+    sb.layout = exchange_layout(sb.R, sb.rank, sb.world)
+    sb.be.set_exchange(sb.layout)
+
+
+def contract(sb: ShardedButterfly, F, G, comm, nv: int = 1, stream: int = 0):
+    """F, G: torch CUDA float64 tensors of 2*n^d*nv (complex interleaved,
+    first mode fastest).  G receives this rank's row slabs."""
+    import torch
+    lay = sb.layout
+    send = torch.empty(2 * max(1, int(lay.send_counts.sum())) * nv, dtype=torch.float64, device=F.device)
+    recv = torch.empty(2 * max(1, int(lay.recv_counts.sum())) * nv, dtype=torch.float64, device=F.device)
+    sb.be.phase(1, F.data_ptr(), send.data_ptr(), nv, stream)
+    comm.alltoall(send, recv, lay.send_counts * nv, lay.recv_counts * nv)
+    sb.be.phase(2, recv.data_ptr(), G.data_ptr(), nv, stream)
+    return send, recv
+
+
+def run_lockstep(backends: list, F, nv: int = 1):
+    """Emulate `world` ranks in one process (sequentially, one GPU): same
+    steps and the same exchange layout, collectives done by hand.  Returns the
+    assembled G (each rank contributes its own row slabs).  Used by the
+    single-GPU test of the sharded path; ranks never wait on each other."""
+    import torch
+    world = len(backends)
+    sbs = [ShardedButterfly(b, r, world) for r, b in enumerate(backends)]
+    Lc = sbs[0].Lc
+    for side in (0, 1):
+        r_est = 8
+        for l in range(Lc + 1):
+            r_est = max([r_est] + [b.level(side, l, r_est) for b in backends])
+    wpad = max(1, max(b.umid_info()[1] for b in backends))
+    ex = [b.umid_export(wpad) for b in backends]
+    ranks_all = sum(e[0] for e in ex)
+    skel_all = sum(e[1].astype(np.int64) for e in ex).astype(np.int32)
+    for sb in sbs:
+        sb.be.umid_import(ranks_all, skel_all, wpad)
+        _finish_layout(sb, ranks_all)
+    sends = []
+    for sb in sbs:
+        lay = sb.layout
+        send = torch.zeros(2 * max(1, int(lay.send_counts.sum())) * nv, dtype=torch.float64, device=F.device)
+        sb.be.phase(1, F.data_ptr(), send.data_ptr(), nv)
+        sends.append(send)
+    torch.cuda.synchronize()
+    G = torch.zeros_like(F)
+    for r, sb in enumerate(sbs):
+        lay = sb.layout
+        parts = []
+        for q in range(world):  # block from source q: its send segment for destination r
+            qlay = sbs[q].layout
+            start = int(qlay.send_counts[:r].sum()) * nv
+            parts.append(sends[q][2 * start: 2 * (start + int(qlay.send_counts[r]) * nv)])
+        recv = torch.cat(parts) if parts else torch.zeros(2, dtype=torch.float64, device=F.device)
+        if recv.numel() == 0:
+            recv = torch.zeros(2, dtype=torch.float64, device=F.device)
+        assert recv.numel() == 2 * int(lay.recv_counts.sum()) * nv or int(lay.recv_counts.sum()) == 0
+        sb.be.phase(2, recv.data_ptr(), G.data_ptr(), nv)
+    torch.cuda.synchronize()
+    return G

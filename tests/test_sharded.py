@@ -1,0 +1,190 @@
+"""Sharded (multi-GPU) path, SURVEY §8(e).
+
+* exchange layout invariants (pure integer logic, CPU)
+* the full orchestration (sharded.construct: all-reduce max of r_est per level,
+  sum-all-reduce of the U-side middle skeletons; one all-to-all of G_{t,s}) over
+  torch.distributed gloo, world 2, with the CPU oracle as compute backend --
+  must equal the unsharded oracle bit for bit
+* the GPU phases with emulated ranks on one GPU (ranks run sequentially, never
+  wait on each other) against the single-GPU contraction
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2411_03029_b200.configs import green_cubes, green_plates, radon2d
+from paper_2411_03029_b200.sharded import ShardedButterfly, TorchComm, construct, exchange_layout, owns
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+def test_exchange_layout_consistent(world):
+    rng = np.random.default_rng(world)
+    nmid = 8
+    R = rng.integers(0, 30, size=(nmid, nmid))
+    lays = [exchange_layout(R, r, world) for r in range(world)]
+    for r in range(world):
+        for q in range(world):
+            assert lays[q].send_counts[r] == lays[r].recv_counts[q]
+    seen = np.zeros((nmid, nmid), int)
+    for r, lay in enumerate(lays):
+        for t in range(nmid):
+            for s in range(nmid):
+                so, ro = lay.send_off[t * nmid + s], lay.recv_off[t * nmid + s]
+                assert (so >= 0) == owns(s, r, world)
+                assert (ro >= 0) == owns(t, r, world)
+                seen[t, s] += so >= 0
+        # blocks are packed back to back in both buffers
+        for off, counts in ((lay.send_off, lay.send_counts), (lay.recv_off, lay.recv_counts)):
+            pairs = sorted((o, R.flat[i]) for i, o in enumerate(off) if o >= 0)
+            cur = 0
+            for o, sz in pairs:
+                assert o == cur
+                cur += sz
+            assert cur == counts.sum()
+    assert np.all(seen == 1)  # every block is sent exactly once
+
+
+class OracleShardBackend:
+    """Test backend: the CPU oracle behind the sharded backend interface."""
+
+    def __init__(self, oracle, spec, L, tol, seed, rank, world):
+        self.o, self.spec = oracle, spec
+        self.tbf = oracle.tbf_construct(spec, L, tol, seed=seed, nthreads=2)
+        self.fz = self.tbf.export()
+        self.rank, self.world = rank, world
+        self.d, self.Lc, self.nmid = spec.d, L // 2, self.fz.nmid
+        self.base = {}
+        b = 0
+        for sd, l, cnt in self.fz.level_counts():
+            self.base[(sd, l)] = (b, cnt)
+            b += cnt
+
+    def level(self, side, l, r_est):
+        assert r_est == self.fz.r_est[side * (self.Lc + 1) + l]
+        b, cnt = self.base[(side, l)]
+        nin, nj = 2 ** (self.d * l), 2 ** (self.Lc - l)
+        outer = np.arange(cnt) // (nj * self.d * nin)
+        mine = np.array([owns(int(o), self.rank, self.world) for o in outer])
+        return int(self.fz.ranks[b:b + cnt][mine].max(initial=0))
+
+    def umid_info(self):
+        b, cnt = self.base[(1, self.Lc)]
+        t = np.arange(cnt) // (self.nmid * self.d)
+        mine = np.array([owns(int(x), self.rank, self.world) for x in t])
+        return cnt, int(self.fz.ranks[b:b + cnt][mine].max(initial=0))
+
+    def umid_export(self, wpad):
+        b, cnt = self.base[(1, self.Lc)]
+        so = np.concatenate([[0], np.cumsum(self.fz.ranks)])
+        ranks = np.zeros(cnt, np.int64)
+        skel = np.zeros(cnt * wpad, np.int32)
+        for q in range(cnt):
+            if owns(q // (self.nmid * self.d), self.rank, self.world):
+                r = int(self.fz.ranks[b + q])
+                ranks[q] = r
+                skel[q * wpad:q * wpad + r] = self.fz.skel[so[b + q]:so[b + q] + r]
+        return ranks, skel
+
+    def umid_import(self, ranks, skel, wpad):
+        b, cnt = self.base[(1, self.Lc)]
+        np.testing.assert_array_equal(ranks, self.fz.ranks[b:b + cnt])
+
+    def set_exchange(self, lay):
+        self.lay = lay
+
+    def phase(self, phase, src, nv):
+        import ctypes as C
+        from oracle.bindings import cx
+        L = self.o.lib
+        L.oracle_tbf_contract_phase.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                                C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int]
+        N = self.spec.n ** self.spec.d * nv
+        se, re = int(self.lay.send_counts.sum()), int(self.lay.recv_counts.sum())
+        if phase == 1:
+            inp = cx(src)
+            out = np.zeros(2 * max(se * nv, 1))
+        else:
+            inp = src.astype(np.float64) if src.size else np.zeros(2)
+            out = np.zeros(2 * N)
+        rc = L.oracle_tbf_contract_phase(self.tbf.h, phase, self.rank, self.world, inp.ctypes.data,
+                                         out.ctypes.data, self.lay.send_off.ctypes.data,
+                                         self.lay.recv_off.ctypes.data, se, re, nv, 2)
+        assert rc == 0, L.oracle_last_error()
+        return out
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _gloo_worker(rank, world, port, spec_args, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import Oracle
+        o = Oracle()
+        spec, L, tol, seed = spec_args
+        be = OracleShardBackend(o, spec, L, tol, seed, rank, world)
+        comm = TorchComm()
+        sb = construct(be, rank, world, comm)
+        rng = np.random.default_rng(11)
+        F = (rng.standard_normal((spec.n,) * spec.d) + 1j * rng.standard_normal((spec.n,) * spec.d))
+        send = torch.from_numpy(be.phase(1, F.reshape(-1, order="F"), 1))
+        recv = torch.zeros(2 * max(1, int(sb.layout.recv_counts.sum())), dtype=torch.float64)
+        comm.alltoall(send, recv, sb.layout.send_counts, sb.layout.recv_counts)
+        G = be.phase(2, recv.numpy()[: 2 * int(sb.layout.recv_counts.sum())], 1)
+        Gt = torch.from_numpy(G)
+        dist.all_reduce(Gt)  # each rank wrote only its own row slabs (others zero)
+        if rank == 0:
+            ref = be.tbf.contract(F).reshape(-1, order="F")
+            got = Gt.numpy().view(np.complex128)
+            q.put(("ok", bool(np.array_equal(got, ref)), float(np.abs(got - ref).max())))
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        q.put(("err", repr(e), 0.0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("spec,L,tol", [(green_plates(32), 2, 1e-6), (green_cubes(16), 2, 1e-4), (radon2d(32), 2, 1e-6)],
+                         ids=["plates32", "cubes16", "radon32"])
+def test_sharded_gloo_world2_bitexact(oracle, spec, L, tol):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, (spec, L, tol, 5), q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+    assert res[0] == "ok", res
+    assert res[1], f"sharded result differs from the unsharded oracle (max {res[2]})"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_gpu_lockstep(world):
+    import torch
+
+    import paper_2411_03029_b200 as tb
+    from paper_2411_03029_b200.sharded import GpuShardBackend, run_lockstep
+    spec, L, tol = green_cubes(16), 2, 1e-4
+    single = tb.tbf_construct(spec, L, tol, seed=5)
+    rng = np.random.default_rng(3)
+    F = rng.standard_normal((16,) * 3) + 1j * rng.standard_normal((16,) * 3)
+    G1 = single.contract(F).reshape(-1, order="F")
+    Ft = torch.from_numpy(np.ascontiguousarray(F.reshape(-1, order="F")).view(np.float64).copy()).cuda()
+    backends = [GpuShardBackend(spec, L, tol, tb.ProxyStrategy(), 5, r, world) for r in range(world)]
+    G = run_lockstep(backends, Ft).cpu().numpy().view(np.complex128)
+    err = np.linalg.norm(G - G1) / np.linalg.norm(G1)
+    assert err < 1e-12, err

@@ -1,22 +1,26 @@
 // Fused level contractions for the apply (Alg. 2, 185,
 // 201, 203; reference mode_product_blockdiag tensor.cpp:136-166 semantics).
 //
-// The block-diagonal factor of every level splits the level into independent
-// boxes: out_box = in_box x_1 M_1 x_2 M_2 ... x_d M_d.  One CTA per box:
-//   phase 0  the box descriptor is copied to shared memory by the whole CTA
-//   phase 1  the d factor blocks AND the input box are staged into shared
-//            memory in a single round trip (all loads independent)
-//   phase 2  the d mode products run back to back in shared memory
-//   phase 3  the last mode writes the output box (global strides: the V-bar
-//            input slab / U-bar output slab are views of F and G)
-// P levels (l >= 1) write per-child contributions; k_sum_parent then adds the
-// 2^d children of every parent in ascending order (deterministic, no atomics).
-// All index arithmetic is 32-bit (box sizes are far below 2^31).
-#include <cooperative_groups.h>
-
+// One launch per (side, level [, slab group]).  Each box of the level is
+//   out = in x_{d-1} M_{d-1} ... x_1 M_1 x_0 M_0      (M_k^T on the P/U side)
+// and is handled by cs CTAs that split the OUTPUT rows of mode d-1 (the first
+// mode contracted): every CTA needs the whole input box but no partial sums
+// are exchanged.  Per CTA:
+//   prologue  descriptor + this CTA's factor rows -> shared memory, stored
+//             [x][a] (a fastest); independent of the previous kernel, so it
+//             runs before griddepcontrol.wait (programmatic dependent launch)
+//   stage     input box -> shared memory: one cp.async.bulk per contiguous
+//             mode-0 row (mbarrier completion); for the ordered sum of P-level
+//             child contributions, batched register loads (8 children in
+//             flight) summed in ascending child order
+//   mode d-1  thread per input column, this CTA's A output rows in registers
+//             (A is dispatched to a compile-time count: no predicated FMAs)
+//   modes d-2..1  smem -> smem, 4 output rows per thread-task
+//   mode 0    4 columns per thread-task, written straight to global memory
+//             (consecutive threads = consecutive rows of mode 0: coalesced)
+// The kernel is latency/issue bound (boxes are small); the layout choices
+// above minimise instructions per useful FMA.  32-bit index math in a box.
 #include "kernels.h"
-
-namespace cg = cooperative_groups;
 
 namespace tbf {
 
@@ -24,27 +28,20 @@ namespace {
 
 constexpr int kBoxThreads = 256;
 
-// debug tracing (OIOBF_BOX_TRACE): per-CTA %globaltimer stamps at phase
-// boundaries; never enabled in the product path
+// debug timeline (oiobf_debug_box_trace): per-CTA %globaltimer stamps at the
+// phase boundaries; one predicated branch per stamp when disabled
 __device__ unsigned long long* g_box_trace = nullptr;
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
+constexpr int kTraceSlots = 8;
+__device__ __forceinline__ void stamp(int slot) {
+  if (g_box_trace != nullptr && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_box_trace[blockIdx.x * kTraceSlots + slot] = t;
+  }
 }
-#define BOX_STAMP(slot)                                                      \
-  do {                                                                       \
-    if (g_box_trace && threadIdx.x == 0) {                                   \
-      g_box_trace[blockIdx.x * 8 + (slot)] = gtime();                        \
-      if ((slot) == 0) g_box_trace[blockIdx.x * 8 + 5] = clock64();          \
-      if ((slot) == 4) g_box_trace[blockIdx.x * 8 + 6] = clock64();          \
-    }                                                                        \
-  } while (0)
 
-// M(a, x): transpose = 0: B(r x w)(a, x);  transpose = 1: B(x, a)
-__device__ __forceinline__ int mat_idx(int mrows, int transpose, int a, int x) {
-  return transpose ? x + a * mrows : a + x * mrows;
-}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
 // n / d for 0 <= n < 2^24, d >= 1: float reciprocal estimate (off by at most
 // one in that range) plus one integer correction; no division subroutine.
@@ -63,226 +60,338 @@ __device__ __forceinline__ void copy_desc(T* dst, const T* src) {
   for (int i = threadIdx.x; i < static_cast<int>(sizeof(T) / 8); i += blockDim.x) d[i] = s[i];
 }
 
-// Compact on purpose: this kernel does little work per CTA, so its cost is
-// dominated by latency and by cold instruction fetch; the mode loop is a
-// runtime loop (per-mode state in shared memory), divisions use qdiv().
-__global__ void __launch_bounds__(kBoxThreads) k_box(const BoxItem* __restrict__ items,
-                                                     const BoxTerm* __restrict__ terms, BoxLaunchInfo info,
-                                                     const double2* __restrict__ mats,
-                                                     const double2* __restrict__ in, double2* __restrict__ out) {
-  extern __shared__ __align__(16) double2 sm[];
-  __shared__ BoxItem it;
-  __shared__ BoxTerm tm;
-  __shared__ int s_ext[kMaxTM];
-  __shared__ int s_moff[kMaxD + 1];
-  __shared__ int s_z0, s_isize;
-  __shared__ long long s_inoff;
-  BOX_STAMP(0);
-  const int tid = threadIdx.x;
-  const int cs = info.cs;
-  const int crank = cs > 1 ? static_cast<int>(blockIdx.x % cs) : 0;
-  const int item = cs > 1 ? static_cast<int>(blockIdx.x / cs) : static_cast<int>(blockIdx.x);
-  copy_desc(&it, items + item);  // items and terms are 1:1 (same index)
-  copy_desc(&tm, terms + item);
-  __syncthreads();
-  const int d = info.d, D = d + 1;  // + nv mode (never contracted)
-  if (tid == 0) {
-    // cluster split: this CTA contracts the slab [z0, z1) of the last input mode
-    const int elast = tm.in_ext[d - 1];
-    const int z0 = qdiv(crank * elast, cs), z1 = qdiv((crank + 1) * elast, cs);
-    int isize = 1;
-    for (int p = 0; p < d; ++p) {
-      s_ext[p] = p == d - 1 ? z1 - z0 : tm.in_ext[p];
-      isize *= s_ext[p];
-    }
-    s_ext[d] = info.nv;
-    s_isize = isize * info.nv;
-    s_z0 = z0;
-    s_inoff = tm.in_off + static_cast<long long>(z0) * tm.in_stride[d - 1];
-    s_moff[0] = 0;
-    for (int k = 0; k < d; ++k) s_moff[k + 1] = s_moff[k] + tm.mrows[k] * tm.mcols[k];
-  }
-  __syncthreads();
-  BOX_STAMP(1);
-  const int e0 = s_ext[0];
-  const int ld0 = e0 + 1;
-  double2* xin = sm;  // input slab, leading dimension e0 + 1
-  double2* smat = xin + info.smem_elems_in;
-  double2* bufA = smat + info.smem_elems_mat;
-  double2* bufB = bufA + info.smem_elems_a;
-  double2* acc = bufB + info.smem_elems_b;
-  // ---- stage the factor blocks (linear) and the input slab (one mode-0
-  // fibre per thread-iteration, up to 4 independent loads in flight)
-  const int msize = s_moff[d];
-  for (int q = tid; q < msize; q += kBoxThreads) {
-    int k = 0;
-    while (k + 1 < d && q >= s_moff[k + 1]) ++k;
-    smat[q] = __ldg(mats + tm.mat_off[k] + (q - s_moff[k]));
-  }
-  const int nrows = e0 > 0 ? s_isize / e0 : 0;
-  const long long st0 = tm.in_stride[0];
-  for (int row = tid; row < nrows; row += kBoxThreads) {
-    long long addr = s_inoff;
-    int rem = row;
-    for (int p = 1; p < D; ++p) {
-      const int q = qdiv(rem, s_ext[p]);
-      addr += static_cast<long long>(rem - q * s_ext[p]) * tm.in_stride[p];
-      rem = q;
-    }
-    const double2* srcp = in + addr;
-    double2* dstp = xin + ld0 * row;
-    for (int x0 = 0; x0 < e0; x0 += 4) {
-      double2 v0, v1, v2, v3;
-      v0 = __ldg(srcp + x0 * st0);
-      if (x0 + 1 < e0) v1 = __ldg(srcp + (x0 + 1) * st0);
-      if (x0 + 2 < e0) v2 = __ldg(srcp + (x0 + 2) * st0);
-      if (x0 + 3 < e0) v3 = __ldg(srcp + (x0 + 3) * st0);
-      dstp[x0] = v0;
-      if (x0 + 1 < e0) dstp[x0 + 1] = v1;
-      if (x0 + 2 < e0) dstp[x0 + 2] = v2;
-      if (x0 + 3 < e0) dstp[x0 + 3] = v3;
-    }
-  }
-  __syncthreads();
-  BOX_STAMP(2);
-  // ---- mode products, one output element per thread-iteration
-  const int reps = (g_box_trace && info.nv < 0) ? 2 : 1;  // never true (nv >= 1): keeps layout
-  int ext[kMaxTM];
-  for (int rep = 0; rep < (g_box_trace ? 2 : 1); ++rep) {
-  if (rep == 1) { __syncthreads(); BOX_STAMP(7); }
-  (void)reps;
-    const double2* src = xin;
-    double2* dst = bufA;
-    for (int p = 0; p < D; ++p) ext[p] = s_ext[p];
-    for (int k = 0; k < d; ++k) {
-      const bool last = (k == d - 1);
-      const int mrows = tm.mrows[k];
-      const int ein = ext[k];
-      const int eout = info.transpose ? tm.mcols[k] : tm.mrows[k];
-      const int sa = info.transpose ? mrows : 1;  // M(a, x) = M[a * sa + x * sx]
-      const int sx = info.transpose ? 1 : mrows;
-      const double2* M = smat + s_moff[k] + (last ? s_z0 * sx : 0);
-      int below = 1, above = 1;
-      for (int p = 0; p < D; ++p) {
-        if (p < k) below *= ext[p];
-        if (p > k) above *= ext[p];
-      }
-      const int sb = k == 0 ? 1 : below;  // source element (b, x, c) at b + sb*x + sc*c
-      const int sc = k == 0 ? ld0 : below * ein;
-      const int total = below * eout * above;
-      double2* o = last ? (cs > 1 ? acc : nullptr) : dst;
-      for (int e = tid; e < total; e += kBoxThreads) {
-        const int r2 = qdiv(e, below);
-        const int b = e - r2 * below;
-        const int c = qdiv(r2, eout);
-        const int a = r2 - c * eout;
-        const double2* xs = src + b + sc * c;
-        const double2* Ma = M + a * sa;
-        double2 s0 = make_double2(0, 0), s1 = make_double2(0, 0);
-        int x = 0;
-        for (; x + 1 < ein; x += 2) {
-          cfma(s0, xs[sb * x], Ma[sx * x]);
-          cfma(s1, xs[sb * (x + 1)], Ma[sx * (x + 1)]);
-        }
-        if (x < ein) cfma(s0, xs[sb * x], Ma[sx * x]);
-        const double2 sum = cadd(s0, s1);
-        if (o) {
-          o[e] = sum;
-        } else {  // single-CTA box: write the output element straight to global
-          long long addr = it.out_off + static_cast<long long>(a) * it.out_stride[k];
-          int rb = b;
-          for (int p = 0; p < k; ++p) {
-            const int q = qdiv(rb, ext[p]);
-            addr += static_cast<long long>(rb - q * ext[p]) * it.out_stride[p];
-            rb = q;
-          }
-          int rc = c;
-          for (int p = k + 1; p < D; ++p) {
-            const int q = qdiv(rc, ext[p]);
-            addr += static_cast<long long>(rc - q * ext[p]) * it.out_stride[p];
-            rc = q;
-          }
-          out[addr] = sum;
-        }
-      }
-      if (!last) {
-        ext[k] = eout;
-        __syncthreads();
-        src = dst;
-        dst = (dst == bufA) ? bufB : bufA;
-      } else {
-        ext[k] = eout;
-      }
-    }
-  }
-  BOX_STAMP(3);
-  if (cs > 1) {
-    // deterministic cluster reduction: CTA r sums its share of the output box
-    // over ranks 0..cs-1 (in order) through distributed shared memory
-    cg::cluster_group cluster = cg::this_cluster();
-    cluster.sync();
-    int osize = 1;
-    for (int p = 0; p < D; ++p) osize *= ext[p];
-    const int e_begin = qdiv(crank * osize, cs);
-    const int e_end = qdiv((crank + 1) * osize, cs);
-    for (int e = e_begin + tid; e < e_end; e += kBoxThreads) {
-      double2 sum = make_double2(0, 0);
-      for (int q = 0; q < cs; ++q) sum = cadd(sum, cluster.map_shared_rank(acc, q)[e]);
-      long long addr = it.out_off;
-      int rem = e;
-      for (int p = 0; p < D; ++p) {
-        const int qd = qdiv(rem, ext[p]);
-        addr += static_cast<long long>(rem - qd * ext[p]) * it.out_stride[p];
-        rem = qd;
-      }
-      out[addr] = sum;
-    }
-    cluster.sync();  // keep every CTA's shared memory alive until all reads are done
-  }
-  BOX_STAMP(4);
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
-// ordered child sums: CTAs map to (parent, 1024-element chunk); children are
-// added in ascending nu (deterministic)
-__global__ void __launch_bounds__(256) k_sum_parent(const SumDesc* __restrict__ ds, const int* __restrict__ cta_map,
-                                                    const double2* __restrict__ in, double2* __restrict__ out) {
-  __shared__ SumDesc D;
-  const int pidx = cta_map[2 * blockIdx.x], chunk = cta_map[2 * blockIdx.x + 1];
-  copy_desc(&D, ds + pidx);
-  __syncthreads();
-  const int nchild = D.nchild;
-  // each thread owns 4 elements; all children's loads for a group of 8 are
-  // issued before any add (no serialized load -> add chains)
-  for (int u = 0; u < 4; ++u) {
-    const long long q = static_cast<long long>(chunk) * 1024 + u * 256 + threadIdx.x;
-    if (q >= D.total) break;
-    double2 acc = make_double2(0, 0);
-    for (int c0 = 0; c0 < nchild; c0 += 8) {
-      double2 v[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c0 + c < nchild) v[c] = in[D.child_off[c0 + c] + q];
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c0 + c < nchild) acc = cadd(acc, v[c]);
-    }
-    out[D.out_off + q] = acc;
+// address of mode-0 row `row` of the box (row = index over modes 1..d-1, nv)
+__device__ __forceinline__ long long row_addr(const BoxDesc& D, int d, int row) {
+  int rem = row;
+  long long a = D.in_off;
+  for (int p = 1; p < d; ++p) {
+    const int q = qdiv(rem, D.ein[p]);
+    a += static_cast<long long>(rem - q * D.ein[p]) * D.in_stride[p];
+    rem = q;
   }
+  return a + static_cast<long long>(rem) * D.in_stride[d];
+}
+
+// mode d-1 from the staged input: t0[rs + Rs (i + A v)] = sum_x X(rs, x, v) M(i, x)
+// (AM = register bucket >= A; the code is kept small on purpose: these CTAs
+// are short and a cold instruction cache is their largest stall)
+template <int AM>
+__device__ __forceinline__ void first_mode_smem(const double2* __restrict__ xs, const double2* __restrict__ Mf,
+                                                double2* __restrict__ t0, int A, int Rs, int ein_f, int nv) {
+  const int R = Rs * nv;
+  for (int r = threadIdx.x; r < R; r += kBoxThreads) {
+    const int v = qdiv(r, Rs), rs = r - v * Rs;
+    double2 acc[AM];
+#pragma unroll
+    for (int i = 0; i < AM; ++i) acc[i] = make_double2(0, 0);
+    const double2* col = xs + rs + Rs * ein_f * v;
+#pragma unroll 1
+    for (int x = 0; x < ein_f; ++x) {
+      const double2 v0 = col[x * Rs];
+#pragma unroll
+      for (int i = 0; i < AM; ++i)
+        if (i < A) cfma(acc[i], v0, Mf[x * A + i]);
+    }
+#pragma unroll
+    for (int i = 0; i < AM; ++i)
+      if (i < A) t0[rs + Rs * (i + A * v)] = acc[i];
+  }
+}
+
+// mode d-1 streamed from global memory (input box too large to stage)
+template <int AM>
+__device__ __forceinline__ void first_mode_global(const BoxDesc& D, int d, const double2* __restrict__ in,
+                                                  const double2* __restrict__ Mf, double2* __restrict__ t0, int A,
+                                                  int Rs, int ein_f, int nv) {
+  const int f = d - 1;
+  const int R = Rs * nv;
+  const long long sf = D.in_stride[f];
+  for (int r = threadIdx.x; r < R; r += kBoxThreads) {
+    const int v = qdiv(r, Rs), rs = r - v * Rs;
+    int rem = rs;
+    long long addr = D.in_off + static_cast<long long>(v) * D.in_stride[d];
+    for (int p = 0; p < f; ++p) {
+      const int q = qdiv(rem, D.ein[p]);
+      addr += static_cast<long long>(rem - q * D.ein[p]) * D.in_stride[p];
+      rem = q;
+    }
+    double2 acc[AM];
+#pragma unroll
+    for (int i = 0; i < AM; ++i) acc[i] = make_double2(0, 0);
+#pragma unroll 1
+    for (int x0 = 0; x0 < ein_f; x0 += 4) {
+      double2 val[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (x0 + u < ein_f) val[u] = in[addr + (x0 + u) * sf];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (x0 + u < ein_f)
+#pragma unroll
+          for (int i = 0; i < AM; ++i)
+            if (i < A) cfma(acc[i], val[u], Mf[(x0 + u) * A + i]);
+    }
+#pragma unroll
+    for (int i = 0; i < AM; ++i)
+      if (i < A) t0[rs + Rs * (i + A * v)] = acc[i];
+  }
+}
+
+// middle mode k: dst(b, a, c) = sum_x M(a, x) src(b, x, c), 4 output rows per task
+__device__ __forceinline__ void middle_mode(const double2* __restrict__ src, double2* __restrict__ dst,
+                                            const double2* __restrict__ Mk, int B, int ein, int eo, int Cc) {
+  const int ng = (eo + 3) >> 2;
+  const int ntask = B * ng * Cc;
+  for (int t = threadIdx.x; t < ntask; t += kBoxThreads) {
+    const int q1 = qdiv(t, B), b = t - q1 * B;
+    const int c = qdiv(q1, ng), ag = q1 - c * ng;
+    const int a0 = ag * 4;
+    const int na = min(4, eo - a0);
+    double2 acc[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) acc[g] = make_double2(0, 0);
+    const double2* s = src + b + B * ein * c;
+#pragma unroll 1
+    for (int x = 0; x < ein; ++x) {
+      const double2 val = s[B * x];
+      const double2* m = Mk + x * eo + a0;
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+        if (g < na) cfma(acc[g], val, m[g]);
+    }
+    double2* o = dst + b + B * (a0 + eo * c);
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+      if (g < na) o[B * g] = acc[g];
+  }
+}
+
+// mode 0 -> global: task (a, 4 consecutive columns); column c = (a_1 .. a_{d-2}, i, v)
+__device__ __forceinline__ void last_mode(const BoxDesc& D, int d, int lo, int A, const double2* __restrict__ src,
+                                          const double2* __restrict__ M0, int Cc, double2* __restrict__ out) {
+  const int f = d - 1;
+  const int ein = D.ein[0], eo = D.eout[0];
+  const int ncg = (Cc + 3) >> 2;
+  const int ntask = eo * ncg;
+  for (int t = threadIdx.x; t < ntask; t += kBoxThreads) {
+    const int cg = qdiv(t, eo), a = t - cg * eo;
+    const int c0 = cg * 4;
+    const int nc = min(4, Cc - c0);
+    double2 acc[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) acc[g] = make_double2(0, 0);
+    const double2* s = src + ein * c0;
+#pragma unroll 1
+    for (int x = 0; x < ein; ++x) {
+      const double2 m = M0[x * eo + a];
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+        if (g < nc) cfma(acc[g], s[x + ein * g], m);
+    }
+#pragma unroll 1
+    for (int g = 0; g < nc; ++g) {
+      int rem = c0 + g;
+      long long addr = D.out_off + static_cast<long long>(a) * D.out_stride[0];
+      for (int p = 1; p < f; ++p) {
+        const int q = qdiv(rem, D.eout[p]);
+        addr += static_cast<long long>(rem - q * D.eout[p]) * D.out_stride[p];
+        rem = q;
+      }
+      const int v = qdiv(rem, A), i = rem - v * A;
+      addr += static_cast<long long>(lo + i) * D.out_stride[f] + static_cast<long long>(v) * D.out_stride[d];
+      out[addr] = g == 0 ? acc[0] : g == 1 ? acc[1] : g == 2 ? acc[2] : acc[3];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBoxThreads, 2) k_box(const BoxDesc* __restrict__ descs, BoxLaunchInfo info,
+                                                        const double2* __restrict__ mats,
+                                                        const double2* __restrict__ in, double2* __restrict__ out) {
+  extern __shared__ __align__(128) double2 sm[];
+  __shared__ BoxDesc D;
+  __shared__ int s_mo[kMaxD + 1];
+  __shared__ __align__(8) unsigned long long s_bar;
+  pdl_trigger();
+  stamp(0);
+  const int tid = threadIdx.x;
+  const int cs = info.cs;
+  const int item = static_cast<int>(blockIdx.x) / cs;
+  const int crank = static_cast<int>(blockIdx.x) - item * cs;
+  copy_desc(&D, descs + item);
+  __syncthreads();
+  const int d = info.d, f = d - 1, nv = info.nv, tr = info.transpose;
+  const int ef = D.eout[f];
+  const int lo = qdiv(crank * ef, cs), hi = qdiv((crank + 1) * ef, cs);
+  const int A = hi - lo;  // 0 <= A <= 8 (host)
+  if (A <= 0) return;     // narrow box: nothing left for this CTA
+  int Rs = 1;             // columns of mode d-1 (modes 0..d-2); times nv below
+  for (int p = 0; p < f; ++p) Rs *= D.ein[p];
+  const int ein_f = D.ein[f];
+  const int e0n = D.ein[0];
+  const int total_in = Rs * ein_f * nv;
+  // bulk staging needs contiguous 16-B rows (every double2 row qualifies)
+  const bool bulk = info.stage && D.nsum == 1 && D.in_stride[0] == 1;
+  if (tid == 0) {
+    s_mo[0] = 0;
+    for (int k = 0; k < d; ++k) s_mo[k + 1] = s_mo[k] + D.ein[k] * (k == f ? A : D.eout[k]);
+    if (bulk) {
+      mbar_init(&s_bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&s_bar, static_cast<unsigned>(total_in) * 16u);
+    }
+  }
+  __syncthreads();
+  double2* smat = sm;
+  double2* xs = smat + info.smem_mat;
+  double2* t0 = xs + info.smem_in;
+  double2* t1 = t0 + info.smem_t;
+  // ---- prologue: factor rows, [x][a] with a fastest (mode d-1: rows lo..hi)
+  for (int k = 0; k < d; ++k) {
+    const int ein = D.ein[k], eo = k == f ? A : D.eout[k], a0 = k == f ? lo : 0;
+    const int mrows = tr ? ein : D.eout[k];  // stored matrix: r x w column-major
+    const double2* M = mats + D.mat_off[k];
+    double2* S = smat + s_mo[k];
+    for (int q = tid; q < ein * eo; q += kBoxThreads) {
+      const int x = qdiv(q, eo), a = q - x * eo + a0;
+      S[q] = __ldg(M + (tr ? x + mrows * a : a + mrows * x));
+    }
+  }
+  // ---- the input box is produced by the previous kernel
+  stamp(1);
+  pdl_wait();
+  stamp(2);
+  if (info.stage) {
+    const int nrows = total_in / e0n;
+    if (bulk) {
+      const unsigned rbytes = static_cast<unsigned>(e0n) * 16u;
+      for (int row = tid; row < nrows; row += kBoxThreads)
+        bulk_g2s(xs + row * e0n, in + row_addr(D, d, row), rbytes, &s_bar);
+      mbar_wait(&s_bar, 0);
+    } else if (D.nsum == 1) {
+      const long long s0 = D.in_stride[0];
+      for (int row = tid; row < nrows; row += kBoxThreads) {
+        const long long ra = row_addr(D, d, row);
+        for (int x = 0; x < e0n; ++x) cp_async16(xs + row * e0n + x, in + ra + x * s0);
+      }
+      cp_async_wait_all();
+    } else {
+      // ordered child sums (ascending child), 8 children of loads in flight
+      const long long s0 = D.in_stride[0];
+      const long long cstr = D.sum_stride;
+#pragma unroll 1
+      for (int e = tid; e < total_in; e += kBoxThreads) {
+        const int row = qdiv(e, e0n);
+        const double2* p = in + row_addr(D, d, row) + (e - row * e0n) * s0;
+        double2 acc = make_double2(0, 0);
+#pragma unroll 1
+        for (int c0 = 0; c0 < D.nsum; c0 += 8) {
+          double2 v[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            if (c0 + c < D.nsum) v[c] = p[(c0 + c) * cstr];
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            if (c0 + c < D.nsum) acc = (c0 + c == 0) ? v[c] : cadd(acc, v[c]);
+        }
+        xs[e] = acc;
+      }
+    }
+  }
+  __syncthreads();
+  stamp(3);
+  // ---- mode d-1: column r = rs + Rs * v  ->  t0[rs + Rs * (i + A * v)]
+  {
+    const double2* Mf = smat + s_mo[f];
+    if (info.stage) first_mode_smem<8>(xs, Mf, t0, A, Rs, ein_f, nv);
+    else first_mode_global<8>(D, d, in, Mf, t0, A, Rs, ein_f, nv);
+  }
+  __syncthreads();
+  stamp(4);
+  // ---- modes d-2 .. 1 (smem -> smem); extents: e[p] = ein (p <= k), eout (k < p < f), A (f), nv
+  double2* src = t0;
+  double2* dst = t1;
+  int Cc = A * nv;  // product of the extents above the current mode
+  for (int k = f - 1; k >= 1; --k) {
+    const int ein = D.ein[k], eo = D.eout[k];
+    int B = 1;
+    for (int p = 0; p < k; ++p) B *= D.ein[p];
+    middle_mode(src, dst, smat + s_mo[k], B, ein, eo, Cc);
+    __syncthreads();
+    Cc *= eo;
+    double2* tmp = src;
+    src = dst;
+    dst = tmp;
+  }
+  stamp(5);
+  // ---- mode 0 -> global
+  last_mode(D, d, lo, A, src, smat + s_mo[0], Cc, out);
+  __syncthreads();
+  stamp(6);
 }
 
 }  // namespace
 
-size_t box_smem_bytes(const BoxLaunchInfo& info) {
-  return sizeof(double2) * static_cast<size_t>(info.smem_elems_in + info.smem_elems_mat + info.smem_elems_a +
-                                               info.smem_elems_b + info.smem_elems_acc);
-  // smem_elems_in includes the padding of the leading dimension (host adds it)
+void box_trace_enable(unsigned long long* buf) {
+  TBF_CUDA(cudaMemcpyToSymbol(g_box_trace, &buf, sizeof(buf)));
 }
 
-void launch_box(i64 nitems, const BoxItem* items, const BoxTerm* terms, const BoxLaunchInfo& info,
-                const double2* mats, const double2* in, double2* out, cudaStream_t st) {
+bool pdl_enabled() {
+  static const bool on = std::getenv("OIOBF_NO_PDL") == nullptr;
+  return on;
+}
+
+int box_ctas_per_sm(int amax, size_t smem) {
+  (void)amax;
+  int n = 0;
+  TBF_CUDA(cudaFuncSetAttribute(k_box, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  TBF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_box, kBoxThreads, smem));
+  return n;
+}
+
+size_t box_smem_bytes(const BoxLaunchInfo& info) {
+  return sizeof(double2) * (static_cast<size_t>(info.smem_mat) + static_cast<size_t>(info.smem_in) +
+                            2 * static_cast<size_t>(info.smem_t));
+}
+
+void launch_box(i64 nitems, const BoxDesc* descs, const BoxLaunchInfo& info, const double2* mats,
+                const double2* in, double2* out, cudaStream_t st) {
   if (nitems == 0) return;
+  if (info.d < 2 || info.d > kMaxD) throw std::runtime_error("launch_box: d out of range");
+  if (info.amax > 8) throw std::runtime_error("launch_box: more than 8 rows of mode d-1 per CTA");
   const size_t smem = box_smem_bytes(info);
-  if (info.d < 1 || info.d > kMaxD) throw std::runtime_error("launch_box: d out of range");
   TBF_CUDA(cudaFuncSetAttribute(k_box, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(nitems * info.cs));
@@ -290,43 +399,11 @@ void launch_box(i64 nitems, const BoxItem* items, const BoxTerm* terms, const Bo
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = static_cast<unsigned>(info.cs);
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  TBF_CUDA(cudaLaunchKernelEx(&cfg, k_box, items, terms, info, mats, in, out));
-  TBF_CUDA(cudaGetLastError());
-}
-
-// largest number of co-resident clusters of size cs for a given smem footprint
-int box_max_active_clusters(int cs, size_t smem) {
-  TBF_CUDA(cudaFuncSetAttribute(k_box, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(cs * 148));
-  cfg.blockDim = dim3(kBoxThreads);
-  cfg.dynamicSmemBytes = smem;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = static_cast<unsigned>(cs);
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int n = 0;
-  TBF_CUDA(cudaOccupancyMaxActiveClusters(&n, k_box, &cfg));
-  return n;
-}
-
-void box_trace_enable(unsigned long long* buf) {
-  TBF_CUDA(cudaMemcpyToSymbol(g_box_trace, &buf, sizeof(buf)));
-}
-
-void launch_sum_parent(i64 nctas, const SumDesc* d, const int* cta_map, const double2* in, double2* out,
-                       cudaStream_t st) {
-  if (nctas == 0) return;
-  k_sum_parent<<<static_cast<unsigned>(nctas), 256, 0, st>>>(d, cta_map, in, out);
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  TBF_CUDA(cudaLaunchKernelEx(&cfg, k_box, descs, info, mats, in, out));
   TBF_CUDA(cudaGetLastError());
 }
 

@@ -86,41 +86,35 @@ struct SumDesc {  // out[e] = sum_c in[c_off[c] + e], children in order
 };
 void launch_sum_children(i64 n, const SumDesc* d, i64 total, const double2* in, double2* out, cudaStream_t st);
 
-// Fused box contraction (apply, one CTA per output box): the block-diagonal
-// factor of every level splits the level into independent boxes; each box is
-// out_box (+)= sum_terms in_box x_1 M_1 x_2 M_2 ... x_d M_d with all d modes
-// applied in shared memory.  V/W: one term.  P (l >= 1): one term per child
-// nu of p_nu, summed in ascending nu order.  U-bar / V-bar (l = 0) read / write
-// the global tensors directly through strides.
-struct BoxTerm {
-  i64 in_off;
-  i64 in_stride[kMaxTM];
-  int in_ext[kMaxTM];
+// Fused box contraction (apply).  The block-diagonal factor of every level
+// splits the level into independent boxes; each box is
+//   out_box = in_box x_0 M_0 x_1 M_1 ... x_{d-1} M_{d-1}
+// (M_k or M_k^T for the P/U side), all d modes applied on chip.  Modes are
+// contracted d-1 first, 0 last; the cs CTAs of a box split the OUTPUT range
+// of mode d-1, so they need no reduction.  in_box may be the ordered sum of
+// nsum equally-shaped child tensors (P-level contributions, child c at
+// in_off + c * sum_stride), summed while the input is staged.
+struct BoxDesc {
+  i64 in_off, out_off, sum_stride;
+  i64 in_stride[kMaxTM], out_stride[kMaxTM];
   i64 mat_off[kMaxD];
-  int mrows[kMaxD], mcols[kMaxD];
-};
-struct BoxItem {
-  i64 out_off;
-  i64 out_stride[kMaxTM];
-  int out_ext[kMaxTM];  // full box extents (last contracted mode: full, split by [last_lo, last_hi))
-  int last_lo, last_hi;
-  i64 term_off;
-  int nterm, pad;
+  int ein[kMaxTM], eout[kMaxTM];  // per mode; entry d: nv
+  int nsum, pad;
 };
 struct BoxLaunchInfo {
-  int d, nv, transpose;
-  int smem_elems_in, smem_elems_mat, smem_elems_a, smem_elems_b;
-  int cs;              // thread-block cluster size: the last input mode is split over cs CTAs
-  int smem_elems_acc;  // partial output box (cs > 1), reduced through DSMEM
+  int d, nv, transpose, cs;  // cs: CTAs per box (split of mode d-1's output)
+  int amax;                  // max output rows of mode d-1 per CTA (template bucket: 2, 4 or 8)
+  int stage;                 // 1: stage the whole input box in shared memory (cp.async)
+  int smem_mat, smem_in, smem_t;  // elements: factors, staged input, each intermediate
+  int pad;
 };
-void launch_box(i64 nitems, const BoxItem* items, const BoxTerm* terms, const BoxLaunchInfo& info,
-                const double2* mats, const double2* in, double2* out, cudaStream_t st);
+void launch_box(i64 nitems, const BoxDesc* descs, const BoxLaunchInfo& info, const double2* mats,
+                const double2* in, double2* out, cudaStream_t st);
 size_t box_smem_bytes(const BoxLaunchInfo& info);
-void box_trace_enable(unsigned long long* buf);  // debug: per-CTA phase timestamps
-int box_max_active_clusters(int cs, size_t smem);
-// ordered child sums, one CTA per parent (SumDesc.work_off unused)
-void launch_sum_parent(i64 nctas, const SumDesc* d, const int* cta_map, const double2* in, double2* out,
-                       cudaStream_t st);
+int box_ctas_per_sm(int amax, size_t smem);  // occupancy of k_box
+void box_trace_enable(unsigned long long* buf);  // debug: 8 globaltimer stamps per CTA
+// programmatic dependent launch for the apply kernels (env OIOBF_NO_PDL=1 disables)
+bool pdl_enabled();
 
 // ---- dense check (core_kernels.cu)
 unsigned long long count_nonfinite(const double2* x, i64 n, cudaStream_t st);

@@ -153,6 +153,8 @@ struct LevelData {
 struct TRef {
   i64 off = 0;
   int nd = 0;
+  int nsum = 1;         // > 1: ordered sum of nsum tensors at off + c * sum_stride
+  i64 sum_stride = 0;
   int ext[kMaxTM] = {0};
   i64 stride[kMaxTM] = {0};
   i64 size() const {
@@ -183,8 +185,7 @@ struct MPLaunch {
   i64 step_begin, nsteps, total_out;
 };
 struct SumLaunch {
-  i64 begin, n, total;  // total: CTAs for k_sum_parent launches
-  i64 work_begin = 0;   // first (parent, chunk) pair in the CTA map
+  i64 begin, n, total;  // descriptors [begin, begin + n), total output elements
 };
 struct BoxLaunch {
   int side, level, in_buf, out_buf;
@@ -192,9 +193,20 @@ struct BoxLaunch {
   BoxLaunchInfo info;
 };
 struct Op {
-  int kind;  // 0 mode product, 1 gemv, 2 sum, 3 fused boxes
+  int kind;  // 0 mode product, 1 gemv, 2 ordered child sums, 3 fused boxes
   i64 idx;
   int group;  // 0 V/W, 1 core, 2 P/U
+  int chunk = 0;  // pipelined plans: slab group (outer index of mode d-1)
+};
+// one core-GEMV launch (all pairs, or the pairs of one column-slab group)
+struct GemvLaunch {
+  i64 desc_begin = 0, ndesc = 0;
+  i64 total_rows = 0, rows_per_cta = 1, ctas = 0;
+  i64 map_begin = 0;  // into Plan::gemv_map (CTA -> pair, relative to desc_begin)
+  int max_c = 0;
+  bool tma = false;
+  i64 tma_ctas = 0, tma_rows_per_cta = 1, tma_map_begin = 0;
+  int tma_stages = 0, tma_stage_elems = 0, tma_xcap = 0;
 };
 
 struct Plan {
@@ -203,29 +215,21 @@ struct Plan {
   std::vector<MPStep> steps;
   std::vector<Blk> blks;
   std::vector<MPLaunch> mps;
+  int nchunk = 1;  // > 1: host-pipelined plan (ops tagged by slab group)
   std::vector<GemvDesc> gemv;
-  i64 gemv_ctas = 0;
-  i64 gemv_total_rows = 0, gemv_rows_per_cta = 1;
-  bool gemv_tma = false;
-  i64 tma_ctas = 0, tma_rows_per_cta = 1;
-  int tma_stages = 0, tma_stage_elems = 0, tma_xcap = 0;
-  std::vector<int> tma_map;
+  std::vector<GemvLaunch> gemvs;
+  std::vector<int> gemv_map, tma_map;
   DevBuf<int> d_tma_map;
-  int gemv_max_c = 0;
   std::vector<SumDesc> sums;
   std::vector<SumLaunch> sum_launches;
   std::vector<Op> ops;
-  std::vector<BoxItem> bitems;
-  std::vector<BoxTerm> bterms;
+  std::vector<BoxDesc> bdescs;
   std::vector<BoxLaunch> boxes;
-  DevBuf<BoxItem> d_bitems;
-  DevBuf<BoxTerm> d_bterms;
+  DevBuf<BoxDesc> d_bdescs;
   DevBuf<MPStep> d_steps;
   DevBuf<Blk> d_blks;
   DevBuf<GemvDesc> d_gemv;
-  DevBuf<int> d_gemv_map;  // CTA -> pair
-  std::vector<int> sum_map;
-  DevBuf<int> d_sum_map;   // k_sum_parent CTA -> (parent, chunk)
+  DevBuf<int> d_gemv_map;  // CTA -> pair (per launch, relative to its first pair)
   DevBuf<SumDesc> d_sums;
   DevBuf<double2> scratch;
   DevBuf<double2> stage_F, stage_G;  // host-buffer contract staging
@@ -242,6 +246,88 @@ struct Plan {
     if (gexec) cudaGraphExecDestroy(gexec);
   }
 };
+
+// Fill a GemvLaunch for descs [begin, end) of pl.gemv: persistent balanced
+// grid for the register-streaming kernel, and the TMA-ring parameters when
+// they apply.  cta_off of the descriptors is relative to the launch.
+void finish_gemv(Plan& pl, i64 begin, i64 end, i64 nv) {
+  GemvLaunch gl;
+  gl.desc_begin = begin;
+  gl.ndesc = end - begin;
+  i64 rows = 0;
+  for (i64 q = begin; q < end; ++q) {
+    GemvDesc& g = pl.gemv[static_cast<size_t>(q)];
+    g.cta_off = rows;
+    rows += g.R;
+    gl.max_c = std::max(gl.max_c, g.C);
+  }
+  gl.total_rows = rows;
+  {
+    const int per_sm = gemv_ctas_per_sm(static_cast<int>(nv), std::max(gl.max_c, 1));
+    i64 grid = std::min<i64>(static_cast<i64>(148) * per_sm, std::max<i64>(rows, 1));
+    gl.rows_per_cta = (rows + grid - 1) / grid;
+    grid = (rows + gl.rows_per_cta - 1) / gl.rows_per_cta;
+    gl.ctas = rows == 0 ? 0 : grid;
+  }
+  gl.map_begin = static_cast<i64>(pl.gemv_map.size());
+  {
+    size_t p = static_cast<size_t>(begin);
+    for (i64 c = 0; c < gl.ctas; ++c) {  // pair holding CTA c's first row
+      const i64 g0 = c * gl.rows_per_cta;
+      while (p + 1 < static_cast<size_t>(end) && pl.gemv[p + 1].cta_off <= g0) ++p;
+      pl.gemv_map.push_back(static_cast<int>(p - static_cast<size_t>(begin)));
+    }
+  }
+  // TMA bulk-copy pipeline: one persistent CTA per SM, whole rows staged in a
+  // shared-memory ring; used when rows are long enough to be worth a bulk
+  // copy and every CTA's row range touches <= gemv_tma_max_pairs() pairs.
+  static const bool no_tma = std::getenv("OIOBF_GEMV_NO_TMA") != nullptr;
+  // measured on B200 (config 2): 2 CTAs/SM x 8 stages = 73% of HBM, same as
+  // the register-streaming kernel; 1 CTA/SM is consumer-bound (45%)
+  static const int per_sm_env =
+      std::getenv("OIOBF_TMA_CTAS_PER_SM") ? std::atoi(std::getenv("OIOBF_TMA_CTAS_PER_SM")) : 2;
+  static const int stages_env = std::getenv("OIOBF_TMA_STAGES") ? std::atoi(std::getenv("OIOBF_TMA_STAGES")) : 8;
+  const i64 ctas = rows;
+  if (!no_tma && gl.max_c >= 64 && ctas > 0) {
+    i64 grid = std::min<i64>(148 * std::max(1, per_sm_env), ctas);
+    const i64 rpc2 = (ctas + grid - 1) / grid;
+    grid = (ctas + rpc2 - 1) / rpc2;
+    const int stage_elems = (gl.max_c + 7) / 8 * 8;
+    const int xcap = gl.max_c * static_cast<int>(nv);
+    const i64 avail = static_cast<i64>(kMaxDynSmem) / std::max(1, per_sm_env) - 1024 -
+                      static_cast<i64>(gemv_tma_max_pairs()) * xcap * static_cast<i64>(sizeof(double2));
+    // rows go round-robin to the 8 consumer warps, so each stage must always
+    // belong to the same consumer (stages % 8 == 0); otherwise a consumer
+    // could wait two phases ahead and the parity check would be ambiguous
+    i64 stages = std::min<i64>(stages_env, avail / (static_cast<i64>(stage_elems) * 16));
+    stages = stages / 8 * 8;
+    bool ok = stages >= 8;
+    std::vector<int> map(static_cast<size_t>(grid));
+    size_t q = static_cast<size_t>(begin);
+    for (i64 c = 0; c < grid && ok; ++c) {
+      const i64 g0 = c * rpc2, g1 = std::min(ctas, g0 + rpc2);
+      while (q + 1 < static_cast<size_t>(end) && pl.gemv[q + 1].cta_off <= g0) ++q;
+      map[static_cast<size_t>(c)] = static_cast<int>(q - static_cast<size_t>(begin));
+      size_t q2 = q;
+      while (q2 + 1 < static_cast<size_t>(end) && pl.gemv[q2 + 1].cta_off < g1) ++q2;
+      if (static_cast<int>(q2 - q + 1) > gemv_tma_max_pairs()) ok = false;
+    }
+    if (std::getenv("OIOBF_DEBUG"))
+      fprintf(stderr, "[oiobf] gemv tma ok=%d grid=%lld rows/cta=%lld stages=%lld stage_elems=%d xcap=%d rows=%lld\n",
+              ok ? 1 : 0, grid, rpc2, stages, stage_elems, xcap, ctas);
+    if (ok) {
+      gl.tma = true;
+      gl.tma_ctas = grid;
+      gl.tma_rows_per_cta = rpc2;
+      gl.tma_stages = static_cast<int>(stages);
+      gl.tma_stage_elems = stage_elems;
+      gl.tma_xcap = xcap;
+      gl.tma_map_begin = static_cast<i64>(pl.tma_map.size());
+      pl.tma_map.insert(pl.tma_map.end(), map.begin(), map.end());
+    }
+  }
+  pl.gemvs.push_back(gl);
+}
 
 }  // namespace
 
@@ -275,8 +361,15 @@ struct oiobf_tbf {
   std::map<i64, std::unique_ptr<Plan>> plans;
   double t_ms[6] = {0, 0, 0, 0, 0, 0};
   std::mutex mu;
+  // host-buffer contraction pipeline: copy-in / copy-out streams and the
+  // events that order them against the compute stream (created on first use)
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> ev;
   ~oiobf_tbf() {
     plans.clear();
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -568,9 +661,10 @@ MPStep make_step(const TRef& in, const TRef& out, int mode, int transpose) {
   return s;
 }
 
-std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
+std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked) {
   auto pl = std::make_unique<Plan>();
   pl->nv = nv;
+  pl->nchunk = chunked && b.world == 1 ? static_cast<int>(ipow(2, b.Lc)) : 1;
   const int d = b.d;
   const int nd = d + 1;
   const i64 n = b.n;
@@ -612,218 +706,122 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
     for (int p = d - 1; p >= 0; --p) pi = (pi << (l - 1)) | (((inner >> (l * p)) & ((i64{1} << l) - 1)) >> 1);
     return pi;
   };
-  // Finish a batch of single-term box items: size shared memory (input box +
-  // factors + two intermediates) and record a box launch, or report "too big".
-  auto commit_boxes = [&](std::vector<BoxItem>& items, std::vector<std::vector<BoxTerm>>& terms, int sd, int l,
-                          int in_buf, int out_buf, int transpose, int group) -> bool {
-    // cluster size: split each box's last input mode over cs CTAs (DSMEM
-    // reduction) so small levels still occupy every SM
-    static const int cs_env = std::getenv("OIOBF_BOX_CLUSTER") ? std::atoi(std::getenv("OIOBF_BOX_CLUSTER")) : 0;
-    int cs = cs_env > 0 ? cs_env
-                        : static_cast<int>(std::min<i64>(8, std::max<i64>(1, (2 * 148 + static_cast<i64>(items.size()) - 1) /
-                                                                                  std::max<i64>(1, items.size()))));
-    cs = std::max(1, std::min(cs, 8));
-    i64 max_in = 1, max_ab = 1, max_mat = 1, max_out = 1;
-    for (size_t i = 0; i < items.size(); ++i) {
-      if (terms[i].size() != 1) throw std::runtime_error("internal: box items carry exactly one term");
-      const BoxTerm& t = terms[i][0];
-      i64 e[kMaxTM];
-      i64 isz = nv, msz = 0, osz = nv;  // input slab with padded leading dimension
-      for (int p = 0; p < d; ++p) {
-        e[p] = p == d - 1 ? (t.in_ext[p] + cs - 1) / cs : t.in_ext[p];
-        isz *= (p == 0 ? e[p] + 1 : e[p]);
-        osz *= transpose ? t.mcols[p] : t.mrows[p];
+  // Record one box launch for descs (all of one side/level [/slab group]):
+  // CTAs per box, amax bucket, input staging and shared-memory sizes; false
+  // when a box does not fit on chip (the caller falls back to mode products).
+  auto commit_boxes = [&](std::vector<BoxDesc>& descs, int sd, int l, int in_buf, int out_buf, int transpose,
+                          int group) -> bool {
+    if (d < 2) return false;
+    const int f = d - 1;
+    // boxes with an empty output write nothing
+    std::vector<BoxDesc> keep;
+    for (const BoxDesc& x : descs) {
+      bool empty = false;
+      for (int k = 0; k < d; ++k) empty |= x.eout[k] == 0;
+      if (!empty) keep.push_back(x);
+    }
+    descs.swap(keep);
+    if (descs.empty()) return true;
+    static const int cs_env = std::getenv("OIOBF_BOX_SPLIT") ? std::atoi(std::getenv("OIOBF_BOX_SPLIT")) : 0;
+    const i64 nitems = static_cast<i64>(descs.size());
+    int ef_min = 1 << 30, ef_max = 0;
+    bool sums = false;
+    for (const BoxDesc& x : descs) {
+      ef_min = std::min(ef_min, x.eout[f]);
+      ef_max = std::max(ef_max, x.eout[f]);
+      sums |= x.nsum > 1;
+    }
+    struct Cfg {
+      int cs = 0, amax_rows = 0;
+      i64 smem_mat = 0, smem_in = 0, smem_t = 0;
+      bool stage = false, fits = false;
+    };
+    auto size_for = [&](int cs) {
+      Cfg c;
+      c.cs = cs;
+      c.amax_rows = (ef_max + cs - 1) / cs;
+      for (const BoxDesc& x : descs) {
+        i64 m = 0, in_sz = nv, rs = 1;
+        for (int k = 0; k < d; ++k) {
+          m += static_cast<i64>(x.ein[k]) * (k == f ? c.amax_rows : x.eout[k]);
+          in_sz *= x.ein[k];
+          if (k < f) rs *= x.ein[k];
+        }
+        c.smem_mat = std::max(c.smem_mat, m);
+        c.smem_in = std::max(c.smem_in, in_sz);
+        i64 t = rs * c.amax_rows * nv;  // after mode d-1
+        c.smem_t = std::max(c.smem_t, t);
+        for (int k = f - 1; k >= 1; --k) {  // after mode k
+          t = t / std::max(1, x.ein[k]) * x.eout[k];
+          c.smem_t = std::max(c.smem_t, t);
+        }
+        // staging keeps a table of mode-0 row offsets (8 B each) in the second buffer
+        c.smem_t = std::max(c.smem_t, (in_sz / std::max(1, x.ein[0]) + 1) / 2);
       }
-      max_out = std::max(max_out, osz);
-      max_in = std::max(max_in, isz);
-      for (int k = 0; k < d; ++k) msz += static_cast<i64>(t.mrows[k]) * t.mcols[k];
-      max_mat = std::max(max_mat, msz);
-      for (int k = 0; k < d - 1; ++k) {
-        e[k] = transpose ? t.mcols[k] : t.mrows[k];
-        i64 cur = nv;
-        for (int p = 0; p < d; ++p) cur *= e[p];
-        max_ab = std::max(max_ab, cur);
+      // stage the input when two CTAs per SM still fit (always for child sums)
+      c.stage = sums || (c.smem_mat + c.smem_in + 2 * c.smem_t) * 16 <= 112 * 1024;
+      if (!c.stage) c.smem_in = 0;
+      c.fits = c.amax_rows <= 8 && c.smem_mat + c.smem_in + 2 * c.smem_t <= kMaxDynSmem / 16;
+      return c;
+    };
+    auto bucket = [](int rows) { return rows <= 2 ? 2 : rows <= 4 ? 4 : 8; };
+    // largest split that still runs in one wave (at least ceil(ef / 8) CTAs
+    // per box, at most one output row of mode d-1 per CTA)
+    // (a CTA whose share of a narrow box is empty just exits early)
+    const int cs_lo = std::max(1, (ef_max + 7) / 8);
+    Cfg best = size_for(cs_lo);
+    if (!best.fits) return false;
+    if (cs_env > 0) {
+      best = size_for(std::max(cs_lo, std::min(cs_env, ef_max)));
+      if (!best.fits) return false;
+    } else {
+      for (int cs = cs_lo + 1; cs <= std::min(std::max(ef_min, cs_lo), 16); ++cs) {
+        const Cfg c = size_for(cs);
+        if (!c.fits) break;
+        const size_t bytes = 16 * static_cast<size_t>(c.smem_mat + c.smem_in + 2 * c.smem_t);
+        const i64 cap = static_cast<i64>(box_ctas_per_sm(bucket(c.amax_rows), bytes)) * 148;
+        if (nitems * cs > cap) break;
+        best = c;
       }
     }
-    if (cs == 1) max_out = 0;
-    if (max_in + max_mat + 2 * max_ab + max_out > 14000) return false;  // > ~219 KB of shared memory
-    // single wave: shrink the cluster until every cluster is co-resident
-    while (cs_env <= 0 && cs > 1) {
-      BoxLaunchInfo probe{};
-      probe.smem_elems_in = static_cast<int>(max_in);
-      probe.smem_elems_mat = static_cast<int>(max_mat);
-      probe.smem_elems_a = probe.smem_elems_b = static_cast<int>(max_ab);
-      probe.smem_elems_acc = static_cast<int>(max_out);
-      if (box_max_active_clusters(cs, box_smem_bytes(probe)) >= static_cast<int>(items.size())) break;
-      --cs;
-      // recompute the slab-dependent sizes for the smaller cluster
-      max_in = max_ab = 1;
-      for (size_t i = 0; i < items.size(); ++i) {
-        const BoxTerm& t = terms[i][0];
-        i64 e[kMaxTM];
-        i64 isz = nv;
-        for (int p = 0; p < d; ++p) {
-          e[p] = p == d - 1 ? (t.in_ext[p] + cs - 1) / cs : t.in_ext[p];
-          isz *= (p == 0 ? e[p] + 1 : e[p]);
-        }
-        max_in = std::max(max_in, isz);
-        for (int k = 0; k < d - 1; ++k) {
-          e[k] = transpose ? t.mcols[k] : t.mrows[k];
-          i64 cur = nv;
-          for (int p = 0; p < d; ++p) cur *= e[p];
-          max_ab = std::max(max_ab, cur);
-        }
-      }
-      if (cs == 1) max_out = 0;
-    }
+    const int cs = best.cs;
+    const int amax_rows = best.amax_rows;
+    const bool stage = best.stage;
+    const i64 smem_mat = best.smem_mat, smem_in = best.smem_in, smem_t = best.smem_t;
     BoxLaunch bl;
     bl.side = sd;
     bl.level = l;
     bl.in_buf = in_buf;
     bl.out_buf = out_buf;
-    bl.item_begin = static_cast<i64>(pl->bitems.size());
-    bl.nitems = static_cast<i64>(items.size());
+    bl.item_begin = static_cast<i64>(pl->bdescs.size());
+    bl.nitems = nitems;
+    bl.info = BoxLaunchInfo{};
     bl.info.d = d;
     bl.info.nv = static_cast<int>(nv);
     bl.info.transpose = transpose;
-    bl.info.smem_elems_in = static_cast<int>(max_in);
-    bl.info.smem_elems_mat = static_cast<int>(max_mat);
-    bl.info.smem_elems_a = static_cast<int>(max_ab);
-    bl.info.smem_elems_b = static_cast<int>(max_ab);
     bl.info.cs = cs;
-    bl.info.smem_elems_acc = static_cast<int>(max_out);
-    for (size_t i = 0; i < items.size(); ++i) {
-      BoxItem x = items[i];
-      x.term_off = static_cast<i64>(pl->bterms.size());
-      x.nterm = 1;
-      x.last_lo = 0;
-      x.last_hi = x.out_ext[d - 1];
-      pl->bterms.push_back(terms[i][0]);
-      pl->bitems.push_back(x);
-    }
+    bl.info.amax = bucket(amax_rows);
+    bl.info.stage = stage ? 1 : 0;
+    bl.info.smem_mat = static_cast<int>(smem_mat);
+    bl.info.smem_in = static_cast<int>(smem_in);
+    bl.info.smem_t = static_cast<int>(smem_t);
+    pl->bdescs.insert(pl->bdescs.end(), descs.begin(), descs.end());
     pl->ops.push_back(Op{3, static_cast<i64>(pl->boxes.size()), group});
     pl->boxes.push_back(bl);
     return true;
   };
-  // ---- Step 1: V / W
+  // chunked (host-pipelined) plans: slab group q = outer index of mode d-1;
+  // the F / G rows of group q are one contiguous range
+  const int Q = pl->nchunk;
+  auto chunk_of = [&](i64 outer) { return Q > 1 ? static_cast<int>(outer / ipow(mpm, d - 1)) : 0; };
+  auto tag_ops = [&](size_t from, int q) {
+    for (size_t i = from; i < pl->ops.size(); ++i) pl->ops[i].chunk = q;
+  };
+  // ---- Step 1: V / W, then (Step 2) the core GEMV, per slab group
   std::vector<TRef> cur;  // per item (s, tau) of the current level
-  for (int l = 0; l <= b.Lc; ++l) {
-    const LevelData& ld = b.side[0][static_cast<size_t>(l)];
-    const i64 nin = ld.L.nin, nj = ld.L.nj;
-    const i64 nitems = b.nmid * nin;
-    std::vector<TRef> in(static_cast<size_t>(nitems));
-    for (i64 it = 0; it < nitems; ++it) {
-      const i64 s = it / nin, tau = it % nin;
-      if (!b.owns(s)) continue;  // another rank's column multi-set
-      in[static_cast<size_t>(it)] =
-          l == 0 ? global_slab(s) : cur[static_cast<size_t>(s * ipow(2, static_cast<i64>(d) * (l - 1)) + parent_of(tau, l))];
-    }
-    // ---- fused boxes
-    const i64 scratch_mark = scratch;
-    std::vector<TRef> outs(static_cast<size_t>(nitems));
-    std::vector<BoxItem> items;
-    std::vector<std::vector<BoxTerm>> terms;
-    const i64 nbeta = ipow(nj, d);
-    for (i64 it = 0; it < nitems; ++it) {
-      const i64 s = it / nin, tau = it % nin;
-      if (!b.owns(s)) continue;
-      const TRef& x = in[static_cast<size_t>(it)];
-      std::vector<std::vector<int>> R(d), W(d);
-      std::vector<std::vector<i64>> MO(d);
-      int oext[kMaxTM];
-      for (int k = 0; k < d; ++k) {
-        int tot_r = 0, tot_w = 0;
-        for (i64 j = 0; j < nj; ++j) {
-          int r, w;
-          i64 mo;
-          slot_info(0, l, s, tau, k, j, r, w, mo);
-          R[k].push_back(r);
-          W[k].push_back(w);
-          MO[k].push_back(mo);
-          tot_r += r;
-          tot_w += w;
-        }
-        if (tot_w != x.ext[k]) throw std::runtime_error("internal: V/W block widths do not match the tensor extent");
-        oext[k] = tot_r;
-      }
-      oext[d] = static_cast<int>(nv);
-      const TRef y = alloc(nd, oext);
-      outs[static_cast<size_t>(it)] = y;
-      for (i64 beta = 0; beta < nbeta; ++beta) {
-        BoxTerm t{};
-        BoxItem bi{};
-        t.in_off = x.off;
-        bi.out_off = y.off;
-        for (int k = 0; k < d; ++k) {
-          const i64 j = (beta / ipow(nj, k)) % nj;
-          i64 ci = 0, co = 0;
-          for (i64 q = 0; q < j; ++q) {
-            ci += W[k][static_cast<size_t>(q)];
-            co += R[k][static_cast<size_t>(q)];
-          }
-          t.in_off += ci * x.stride[k];
-          bi.out_off += co * y.stride[k];
-          t.in_ext[k] = W[k][static_cast<size_t>(j)];
-          bi.out_ext[k] = R[k][static_cast<size_t>(j)];
-          t.mat_off[k] = MO[k][static_cast<size_t>(j)];
-          t.mrows[k] = R[k][static_cast<size_t>(j)];
-          t.mcols[k] = W[k][static_cast<size_t>(j)];
-        }
-        for (int p = 0; p < nd; ++p) {
-          t.in_stride[p] = x.stride[p];
-          bi.out_stride[p] = y.stride[p];
-        }
-        t.in_ext[d] = static_cast<int>(nv);
-        bi.out_ext[d] = static_cast<int>(nv);
-        bi.nterm = 1;
-        items.push_back(bi);
-        terms.push_back({t});
-      }
-    }
-    if (commit_boxes(items, terms, 0, l, l == 0 ? BUF_F : BUF_SCRATCH, BUF_SCRATCH, 0, 0)) {
-      cur = outs;
-      continue;
-    }
-    scratch = scratch_mark;  // fall back to per-mode launches for this level
-    for (int k = 0; k < d; ++k) {
-      std::vector<MPStep> mitems;
-      std::vector<std::vector<Blk>> blocks;
-      for (i64 it = 0; it < nitems; ++it) {
-        const i64 s = it / nin, tau = it % nin;
-        if (!b.owns(s)) continue;
-        TRef& x = in[static_cast<size_t>(it)];
-        int oext[kMaxTM];
-        for (int p = 0; p < nd; ++p) oext[p] = x.ext[p];
-        std::vector<Blk> bl;
-        int ci = 0, co = 0;
-        for (i64 j = 0; j < nj; ++j) {
-          Blk B;
-          int r, w;
-          slot_info(0, l, s, tau, k, j, r, w, B.mat_off);
-          B.rows = r;
-          B.cols = w;
-          B.in_start = ci;
-          B.out_start = co;
-          ci += B.cols;
-          co += B.rows;
-          bl.push_back(B);
-        }
-        if (ci != x.ext[k]) throw std::runtime_error("internal: V/W block widths do not match the tensor extent");
-        oext[k] = co;
-        TRef y = alloc(nd, oext);
-        mitems.push_back(make_step(x, y, k, 0));
-        blocks.push_back(bl);
-        x = y;
-      }
-      add_mp(*pl, 0, l, (l == 0 && k == 0) ? BUF_F : BUF_SCRATCH, BUF_SCRATCH, mitems, blocks, 0);
-    }
-    cur = in;
-  }
-  // ---- Step 2: cores.  x = F_{t,s} = cur[s * nmid + t]; y = G_{t,s}
   const LevelData& ULc = b.side[1][static_cast<size_t>(b.Lc)];
   std::vector<TRef> gts(static_cast<size_t>(b.nmid * b.nmid));  // index t * nmid + s
-  i64 ctas = 0;
-  const int rpc = gemv_rows_per_cta();
+  std::vector<TRef> wout(static_cast<size_t>(b.nmid * b.nmid));  // W output per (s, tau = t)
   const bool sharded = b.world > 1;
   pl->sharded = sharded;
   if (sharded)
@@ -831,304 +829,366 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv) {
                 static_cast<i64>(b.recv_off.size()) == b.nmid * b.nmid,
             "sharded contract: exchange layout not set (oiobf_tbf_set_exchange)");
   const int* urank = sharded ? b.umid_rank.data() : ULc.h_rank.data();
-  for (i64 p = 0; p < b.nmid * b.nmid; ++p) {
-    const i64 s = p / b.nmid, t = p % b.nmid;
-    int gext[kMaxTM];
-    i64 R = 1;
-    for (int k = 0; k < d; ++k) {
-      gext[k] = urank[(t * b.nmid + s) * d + k];
-      R *= gext[k];
-    }
-    gext[d] = static_cast<int>(nv);
-    if (sharded && b.owns(t)) {  // P/U input G_{t,s} arrives in the receive buffer
-      const i64 ro = b.recv_off[static_cast<size_t>(t * b.nmid + s)];
-      require(ro >= 0, "sharded contract: missing receive offset");
-      gts[static_cast<size_t>(t * b.nmid + s)] = packed(ro * nv, nd, gext);
-    }
-    if (!b.owns(s)) continue;
-    const PairDesc& pd = b.h_pairs[static_cast<size_t>(p)];
-    const TRef& x = cur[static_cast<size_t>(s * b.nmid + t)];
-    TRef y;
-    if (sharded) {  // GEMV output goes straight into the send buffer
-      const i64 so = b.send_off[static_cast<size_t>(t * b.nmid + s)];
-      require(so >= 0, "sharded contract: missing send offset");
-      y = packed(so * nv, nd, gext);
-    } else {
-      y = alloc(nd, gext);
-      gts[static_cast<size_t>(t * b.nmid + s)] = y;
-    }
-    if (R != pd.R || x.size() != static_cast<i64>(pd.C) * nv) throw std::runtime_error("internal: core shape mismatch");
-    GemvDesc g;
-    g.core_off = pd.core_off;
-    g.x_off = x.off;
-    g.y_off = y.off;
-    g.R = pd.R;
-    g.C = pd.C;
-    g.cta_off = ctas;  // first global row of this pair
-    ctas += pd.R;
-    pl->gemv_max_c = std::max(pl->gemv_max_c, pd.C);
-    pl->gemv.push_back(g);
-  }
-  (void)rpc;
-  // persistent balanced grid: every CTA streams the same number of rows
-  pl->gemv_total_rows = ctas;
-  {
-    const int per_sm = gemv_ctas_per_sm(static_cast<int>(nv), std::max(pl->gemv_max_c, 1));
-    i64 grid = std::min<i64>(static_cast<i64>(148) * per_sm, std::max<i64>(ctas, 1));
-    pl->gemv_rows_per_cta = (ctas + grid - 1) / grid;
-    grid = (ctas + pl->gemv_rows_per_cta - 1) / pl->gemv_rows_per_cta;
-    pl->gemv_ctas = ctas == 0 ? 0 : grid;
-  }
-  // TMA bulk-copy pipeline: one persistent CTA per SM, whole rows staged in a
-  // shared-memory ring; used when rows are long enough to be worth a bulk
-  // copy and every CTA's row range touches <= gemv_tma_max_pairs() pairs.
-  {
-    static const bool no_tma = std::getenv("OIOBF_GEMV_NO_TMA") != nullptr;
-    const int max_c = pl->gemv_max_c;
-    // measured on B200 (config 2): 2 CTAs/SM x 8 stages = 73% of HBM, same as
-    // the register-streaming kernel; 1 CTA/SM is consumer-bound (45%)
-    static const int per_sm_env = std::getenv("OIOBF_TMA_CTAS_PER_SM") ? std::atoi(std::getenv("OIOBF_TMA_CTAS_PER_SM")) : 2;
-    static const int stages_env = std::getenv("OIOBF_TMA_STAGES") ? std::atoi(std::getenv("OIOBF_TMA_STAGES")) : 8;
-    if (!no_tma && max_c >= 64 && ctas > 0) {
-      i64 grid = std::min<i64>(148 * std::max(1, per_sm_env), ctas);
-      const i64 rpc2 = (ctas + grid - 1) / grid;
-      grid = (ctas + rpc2 - 1) / rpc2;
-      const int stage_elems = (max_c + 7) / 8 * 8;
-      const int xcap = max_c * static_cast<int>(nv);
-      const i64 avail = static_cast<i64>(kMaxDynSmem) / std::max(1, per_sm_env) - 1024 -
-                        static_cast<i64>(gemv_tma_max_pairs()) * xcap * static_cast<i64>(sizeof(double2));
-      // rows go round-robin to the 8 consumer warps, so each stage must always
-      // belong to the same consumer (stages % 8 == 0); otherwise a consumer
-      // could wait two phases ahead and the parity check would be ambiguous
-      i64 stages = std::min<i64>(stages_env, avail / (static_cast<i64>(stage_elems) * 16));
-      stages = stages / 8 * 8;
-      bool ok = stages >= 8;
-      std::vector<int> map(static_cast<size_t>(grid));
-      size_t q = 0;
-      for (i64 c = 0; c < grid && ok; ++c) {
-        const i64 g0 = c * rpc2, g1 = std::min(ctas, g0 + rpc2);
-        while (q + 1 < pl->gemv.size() && pl->gemv[q + 1].cta_off <= g0) ++q;
-        map[static_cast<size_t>(c)] = static_cast<int>(q);
-        size_t q2 = q;
-        while (q2 + 1 < pl->gemv.size() && pl->gemv[q2 + 1].cta_off < g1) ++q2;
-        if (static_cast<int>(q2 - q + 1) > gemv_tma_max_pairs()) ok = false;
+  for (int q = 0; q < Q; ++q) {
+    const size_t ops_mark = pl->ops.size();
+    auto mine = [&](i64 outer) { return b.owns(outer) && chunk_of(outer) == q; };
+    for (int l = 0; l <= b.Lc; ++l) {
+      const LevelData& ld = b.side[0][static_cast<size_t>(l)];
+      const i64 nin = ld.L.nin, nj = ld.L.nj;
+      const i64 nitems = b.nmid * nin;
+      std::vector<TRef> in(static_cast<size_t>(nitems));
+      for (i64 it = 0; it < nitems; ++it) {
+        const i64 s = it / nin, tau = it % nin;
+        if (!mine(s)) continue;  // another rank's (or slab group's) column multi-set
+        in[static_cast<size_t>(it)] =
+            l == 0 ? global_slab(s)
+                   : cur[static_cast<size_t>(s * ipow(2, static_cast<i64>(d) * (l - 1)) + parent_of(tau, l))];
       }
-      if (std::getenv("OIOBF_DEBUG"))
-        fprintf(stderr, "[oiobf] gemv tma ok=%d grid=%lld rows/cta=%lld stages=%lld stage_elems=%d xcap=%d rows=%lld\n",
-                ok ? 1 : 0, grid, rpc2, stages, stage_elems, xcap, ctas);
-      if (ok) {
-        pl->gemv_tma = true;
-        pl->tma_ctas = grid;
-        pl->tma_rows_per_cta = rpc2;
-        pl->tma_stages = static_cast<int>(stages);
-        pl->tma_stage_elems = stage_elems;
-        pl->tma_xcap = xcap;
-        pl->tma_map = map;
+      // ---- fused boxes
+      const i64 scratch_mark = scratch;
+      std::vector<TRef> outs(static_cast<size_t>(nitems));
+      std::vector<BoxDesc> descs;
+      const i64 nbeta = ipow(nj, d);
+      for (i64 it = 0; it < nitems; ++it) {
+        const i64 s = it / nin, tau = it % nin;
+        if (!mine(s)) continue;
+        const TRef& x = in[static_cast<size_t>(it)];
+        std::vector<std::vector<int>> R(d), W(d);
+        std::vector<std::vector<i64>> MO(d);
+        int oext[kMaxTM];
+        for (int k = 0; k < d; ++k) {
+          int tot_r = 0, tot_w = 0;
+          for (i64 j = 0; j < nj; ++j) {
+            int r, w;
+            i64 mo;
+            slot_info(0, l, s, tau, k, j, r, w, mo);
+            R[k].push_back(r);
+            W[k].push_back(w);
+            MO[k].push_back(mo);
+            tot_r += r;
+            tot_w += w;
+          }
+          if (tot_w != x.ext[k]) throw std::runtime_error("internal: V/W block widths do not match the tensor extent");
+          oext[k] = tot_r;
+        }
+        oext[d] = static_cast<int>(nv);
+        const TRef y = alloc(nd, oext);
+        outs[static_cast<size_t>(it)] = y;
+        for (i64 beta = 0; beta < nbeta; ++beta) {
+          BoxDesc bd{};
+          bd.in_off = x.off;
+          bd.out_off = y.off;
+          bd.nsum = 1;
+          for (int k = 0; k < d; ++k) {
+            const i64 j = (beta / ipow(nj, k)) % nj;
+            i64 ci = 0, co = 0;
+            for (i64 q2 = 0; q2 < j; ++q2) {
+              ci += W[k][static_cast<size_t>(q2)];
+              co += R[k][static_cast<size_t>(q2)];
+            }
+            bd.in_off += ci * x.stride[k];
+            bd.out_off += co * y.stride[k];
+            bd.ein[k] = W[k][static_cast<size_t>(j)];
+            bd.eout[k] = R[k][static_cast<size_t>(j)];
+            bd.mat_off[k] = MO[k][static_cast<size_t>(j)];
+          }
+          for (int p = 0; p < nd; ++p) {
+            bd.in_stride[p] = x.stride[p];
+            bd.out_stride[p] = y.stride[p];
+          }
+          bd.ein[d] = bd.eout[d] = static_cast<int>(nv);
+          descs.push_back(bd);
+        }
       }
+      if (commit_boxes(descs, 0, l, l == 0 ? BUF_F : BUF_SCRATCH, BUF_SCRATCH, 0, 0)) {
+        cur = outs;
+        continue;
+      }
+      scratch = scratch_mark;  // fall back to per-mode launches for this level
+      for (int k = 0; k < d; ++k) {
+        std::vector<MPStep> mitems;
+        std::vector<std::vector<Blk>> blocks;
+        for (i64 it = 0; it < nitems; ++it) {
+          const i64 s = it / nin, tau = it % nin;
+          if (!mine(s)) continue;
+          TRef& x = in[static_cast<size_t>(it)];
+          int oext[kMaxTM];
+          for (int p = 0; p < nd; ++p) oext[p] = x.ext[p];
+          std::vector<Blk> bl;
+          int ci = 0, co = 0;
+          for (i64 j = 0; j < nj; ++j) {
+            Blk B;
+            int r, w;
+            slot_info(0, l, s, tau, k, j, r, w, B.mat_off);
+            B.rows = r;
+            B.cols = w;
+            B.in_start = ci;
+            B.out_start = co;
+            ci += B.cols;
+            co += B.rows;
+            bl.push_back(B);
+          }
+          if (ci != x.ext[k]) throw std::runtime_error("internal: V/W block widths do not match the tensor extent");
+          oext[k] = co;
+          TRef y = alloc(nd, oext);
+          mitems.push_back(make_step(x, y, k, 0));
+          blocks.push_back(bl);
+          x = y;
+        }
+        add_mp(*pl, 0, l, (l == 0 && k == 0) ? BUF_F : BUF_SCRATCH, BUF_SCRATCH, mitems, blocks, 0);
+      }
+      cur = in;
     }
-  }
-  pl->ops.push_back(Op{1, 0, 1});
-  // ---- Step 3: P (l = Lc..1, ordered child sums), U (l = 0)
-  std::vector<TRef> gcur = gts;  // per (t, nu) at level l: index t * nin + nu
-  for (int l = b.Lc; l >= 0; --l) {
-    const LevelData& ld = b.side[1][static_cast<size_t>(l)];
-    const i64 nin = ld.L.nin, nj = ld.L.nj;
-    const i64 pnin = l > 0 ? ipow(2, static_cast<i64>(d) * (l - 1)) : 1;
-    const i64 nbeta = ipow(nj, d);
-    const i64 scratch_mark = scratch;
-    std::vector<TRef> par(static_cast<size_t>(b.nmid * pnin));
-    std::vector<BoxItem> items;
-    std::vector<std::vector<BoxTerm>> terms;
-    std::vector<SumDesc> psums;
-    for (i64 t = 0; t < b.nmid; ++t)
-      for (i64 pnu = 0; pnu < pnin; ++pnu) {
-        if (!b.owns(t)) continue;  // another rank's row multi-set
+    for (i64 s = 0; s < b.nmid; ++s)
+      if (mine(s))
+        for (i64 t = 0; t < b.nmid; ++t)
+          wout[static_cast<size_t>(s * b.nmid + t)] = cur[static_cast<size_t>(s * b.nmid + t)];
+    // ---- Step 2: cores.  x = F_{t,s} = W output (s, tau = t); y = G_{t,s}
+    const i64 gemv_begin = static_cast<i64>(pl->gemv.size());
+    for (i64 p = 0; p < b.nmid * b.nmid; ++p) {
+      const i64 s = p / b.nmid, t = p % b.nmid;
+      int gext[kMaxTM];
+      i64 R = 1;
+      for (int k = 0; k < d; ++k) {
+        gext[k] = urank[(t * b.nmid + s) * d + k];
+        R *= gext[k];
+      }
+      gext[d] = static_cast<int>(nv);
+      if (sharded && b.owns(t)) {  // P/U input G_{t,s} arrives in the receive buffer
+        const i64 ro = b.recv_off[static_cast<size_t>(t * b.nmid + s)];
+        require(ro >= 0, "sharded contract: missing receive offset");
+        gts[static_cast<size_t>(t * b.nmid + s)] = packed(ro * nv, nd, gext);
+      }
+      if (!mine(s)) continue;
+      const PairDesc& pd = b.h_pairs[static_cast<size_t>(p)];
+      const TRef& x = wout[static_cast<size_t>(s * b.nmid + t)];
+      TRef y;
+      if (sharded) {  // GEMV output goes straight into the send buffer
+        const i64 so = b.send_off[static_cast<size_t>(t * b.nmid + s)];
+        require(so >= 0, "sharded contract: missing send offset");
+        y = packed(so * nv, nd, gext);
+      } else {
+        y = alloc(nd, gext);
+        gts[static_cast<size_t>(t * b.nmid + s)] = y;
+      }
+      if (R != pd.R || x.size() != static_cast<i64>(pd.C) * nv)
+        throw std::runtime_error("internal: core shape mismatch");
+      GemvDesc g;
+      g.core_off = pd.core_off;
+      g.x_off = x.off;
+      g.y_off = y.off;
+      g.R = pd.R;
+      g.C = pd.C;
+      pl->gemv.push_back(g);
+    }
+    if (static_cast<i64>(pl->gemv.size()) > gemv_begin) {
+      finish_gemv(*pl, gemv_begin, static_cast<i64>(pl->gemv.size()), nv);
+      pl->ops.push_back(Op{1, static_cast<i64>(pl->gemvs.size()) - 1, 1});
+    }
+    tag_ops(ops_mark, q);
+  }  // slab groups (V/W + GEMV)
+  // ---- Step 3: P (l = Lc..1), U (l = 0).  A P level writes one contribution
+  // per child nu into consecutive equally-shaped buffers of its parent; the
+  // consumer (next level down) reads their ordered sum (TRef::nsum) while
+  // staging its input, so no separate summation pass is needed.
+  for (int q = 0; q < Q; ++q) {
+    const size_t ops_mark = pl->ops.size();
+    auto mine = [&](i64 outer) { return b.owns(outer) && chunk_of(outer) == q; };
+    std::vector<TRef> gcur = gts;  // per (t, nu) at level l: index t * nin + nu
+    const int u_in0 = sharded ? BUF_RECV : BUF_SCRATCH;
+    for (int l = b.Lc; l >= 0; --l) {
+      const LevelData& ld = b.side[1][static_cast<size_t>(l)];
+      const i64 nin = ld.L.nin, nj = ld.L.nj;
+      const i64 pnin = l > 0 ? ipow(2, static_cast<i64>(d) * (l - 1)) : 1;
+      const i64 nbeta = ipow(nj, d);
+      const int u_in = l == b.Lc ? u_in0 : BUF_SCRATCH;
+      std::vector<TRef> par(static_cast<size_t>(b.nmid * pnin));
+      // kids of each parent, output widths, and the parents' child blocks
+      auto kids_of = [&](i64 pnu) {
         std::vector<i64> kids;
         for (i64 nu = 0; nu < nin; ++nu)
           if (l == 0 || parent_of(nu, l) == pnu) kids.push_back(nu);
-        // widths (output side) are common to all children
-        std::vector<std::vector<int>> W(d);
-        int oext[kMaxTM];
+        return kids;
+      };
+      auto parent_shape = [&](i64 t, i64 nu0, int* oext, std::vector<std::vector<int>>& W) {
+        W.assign(static_cast<size_t>(d), {});
         for (int k = 0; k < d; ++k) {
           int tw = 0;
           for (i64 j = 0; j < nj; ++j) {
             int r, w;
             i64 mo;
-            slot_info(1, l, t, kids[0], k, j, r, w, mo);
-            W[k].push_back(w);
+            slot_info(1, l, t, nu0, k, j, r, w, mo);
+            W[static_cast<size_t>(k)].push_back(w);
             tw += w;
           }
           oext[k] = tw;
         }
         oext[d] = static_cast<int>(nv);
-        const TRef y = l == 0 ? global_slab(t) : alloc(nd, oext);
-        par[static_cast<size_t>(t * pnin + pnu)] = y;
-        SumDesc sdsc{};
-        for (i64 nu : kids) {
-          // l >= 1: each child writes its own contribution (parent's shape),
-          // summed afterwards in ascending nu; l = 0: straight into G
-          const TRef yc = l == 0 ? y : alloc(nd, oext);
-          if (l > 0) sdsc.child_off[sdsc.nchild++] = yc.off;
+      };
+      // child c's output buffer of parent (t, pnu): consecutive, parent-shaped
+      std::vector<TRef> child_out(static_cast<size_t>(b.nmid * nin));
+      for (i64 t = 0; t < b.nmid; ++t)
+        for (i64 pnu = 0; pnu < pnin; ++pnu) {
+          if (!mine(t)) continue;  // another rank's (or slab group's) row multi-set
+          const std::vector<i64> kids = kids_of(pnu);
+          int oext[kMaxTM];
+          std::vector<std::vector<int>> W;
+          parent_shape(t, kids[0], oext, W);
+          if (l == 0) {
+            const TRef y = global_slab(t);
+            par[static_cast<size_t>(t * pnin + pnu)] = y;
+            child_out[static_cast<size_t>(t * nin + kids[0])] = y;
+            continue;
+          }
+          const TRef y0 = alloc(nd, oext);
+          const i64 psize = y0.size();
+          for (size_t c = 1; c < kids.size(); ++c) alloc(nd, oext);
+          TRef pref = y0;
+          pref.nsum = static_cast<int>(kids.size());
+          pref.sum_stride = psize;
+          par[static_cast<size_t>(t * pnin + pnu)] = pref;
+          for (size_t c = 0; c < kids.size(); ++c) {
+            TRef yc = y0;
+            yc.off = y0.off + static_cast<i64>(c) * psize;
+            child_out[static_cast<size_t>(t * nin + kids[c])] = yc;
+          }
+        }
+      std::vector<BoxDesc> descs;
+      for (i64 t = 0; t < b.nmid; ++t)
+        for (i64 nu = 0; nu < nin; ++nu) {
+          if (!mine(t)) continue;
           const TRef& x = gcur[static_cast<size_t>(t * nin + nu)];
+          const TRef& yc = child_out[static_cast<size_t>(t * nin + nu)];
           for (i64 beta = 0; beta < nbeta; ++beta) {
-            BoxItem bi{};
-            BoxTerm tm{};
-            bi.out_off = yc.off;
-            tm.in_off = x.off;
+            BoxDesc bd{};
+            bd.out_off = yc.off;
+            bd.in_off = x.off;
+            bd.nsum = x.nsum;
+            bd.sum_stride = x.sum_stride;
             for (int k = 0; k < d; ++k) {
               const int jb = static_cast<int>((beta / ipow(nj, k)) % nj);
               i64 co = 0, ci = 0;
               int r = 0, w = 0;
               i64 mo = 0;
-              for (int q = 0; q < jb; ++q) {
-                slot_info(1, l, t, nu, k, q, r, w, mo);
+              for (int q2 = 0; q2 < jb; ++q2) {
+                slot_info(1, l, t, nu, k, q2, r, w, mo);
                 ci += r;
                 co += w;
               }
               slot_info(1, l, t, nu, k, jb, r, w, mo);
-              if (w != W[k][static_cast<size_t>(jb)]) throw std::runtime_error("internal: P/U widths differ");
-              bi.out_off += co * yc.stride[k];
-              bi.out_ext[k] = w;
-              tm.in_off += ci * x.stride[k];
-              tm.in_ext[k] = r;
-              tm.mat_off[k] = mo;
-              tm.mrows[k] = r;
-              tm.mcols[k] = w;
+              bd.out_off += co * yc.stride[k];
+              bd.in_off += ci * x.stride[k];
+              bd.ein[k] = r;
+              bd.eout[k] = w;
+              bd.mat_off[k] = mo;
             }
-            bi.out_ext[d] = static_cast<int>(nv);
-            tm.in_ext[d] = static_cast<int>(nv);
             for (int p = 0; p < nd; ++p) {
-              bi.out_stride[p] = yc.stride[p];
-              tm.in_stride[p] = x.stride[p];
+              bd.out_stride[p] = yc.stride[p];
+              bd.in_stride[p] = x.stride[p];
             }
-            bi.nterm = 1;
-            items.push_back(bi);
-            terms.push_back({tm});
+            bd.ein[d] = bd.eout[d] = static_cast<int>(nv);
+            descs.push_back(bd);
           }
         }
-        if (l > 0) {
-          sdsc.out_off = y.off;
-          sdsc.total = y.size();
-          psums.push_back(sdsc);
-        }
+      if (commit_boxes(descs, 1, l, u_in, l == 0 ? BUF_G : BUF_SCRATCH, 1, 2)) {
+        gcur = par;
+        continue;
       }
-    const int u_in = (sharded && l == b.Lc) ? BUF_RECV : BUF_SCRATCH;
-    if (commit_boxes(items, terms, 1, l, u_in, l == 0 ? BUF_G : BUF_SCRATCH, 1, 2)) {
-      if (l > 0) {
+      // ---- fall back: materialize summed inputs, then per-mode launches
+      {
         SumLaunch sl;
         sl.begin = static_cast<i64>(pl->sums.size());
-        sl.n = static_cast<i64>(psums.size());
-        sl.work_begin = static_cast<i64>(pl->sum_map.size()) / 2;
-        for (size_t q = 0; q < psums.size(); ++q)
-          for (i64 c = 0; c * 1024 < psums[q].total; ++c) {
-            pl->sum_map.push_back(static_cast<int>(q));
-            pl->sum_map.push_back(static_cast<int>(c));
+        i64 work = 0;
+        std::map<i64, TRef> done;  // child block offset -> materialized parent
+        for (i64 it = 0; it < b.nmid * nin; ++it) {
+          const i64 t = it / nin;
+          if (!mine(t)) continue;
+          TRef& x = gcur[static_cast<size_t>(it)];
+          if (x.nsum <= 1) continue;
+          auto hit = done.find(x.off);
+          if (hit != done.end()) {
+            x = hit->second;
+            continue;
           }
-        sl.total = static_cast<i64>(pl->sum_map.size()) / 2 - sl.work_begin;
-        pl->sums.insert(pl->sums.end(), psums.begin(), psums.end());
-        pl->ops.push_back(Op{4, static_cast<i64>(pl->sum_launches.size()), 2});
-        pl->sum_launches.push_back(sl);
-      }
-      gcur = par;
-      continue;
-    }
-    scratch = scratch_mark;  // fall back: per-mode launches + ordered sums
-    const i64 nitems = b.nmid * nin;
-    std::vector<TRef> x = gcur;
-    for (int k = 0; k < d; ++k) {
-      std::vector<MPStep> mitems;
-      std::vector<std::vector<Blk>> blocks;
-      const bool last_global = (l == 0 && k == d - 1);
-      for (i64 it = 0; it < nitems; ++it) {
-        const i64 t = it / nin, nu = it % nin;
-        if (!b.owns(t)) continue;
-        TRef& xi = x[static_cast<size_t>(it)];
-        int oext[kMaxTM];
-        for (int p = 0; p < nd; ++p) oext[p] = xi.ext[p];
-        std::vector<Blk> bl;
-        int ci = 0, co = 0;
-        for (i64 j = 0; j < nj; ++j) {
-          Blk B;
-          int r, w;
-          slot_info(1, l, t, nu, k, j, r, w, B.mat_off);
-          B.rows = r;
-          B.cols = w;
-          B.in_start = ci;
-          B.out_start = co;
-          ci += B.rows;
-          co += B.cols;
-          bl.push_back(B);
-        }
-        if (ci != xi.ext[k]) throw std::runtime_error("internal: P/U block ranks do not match the tensor extent");
-        oext[k] = co;
-        TRef y = last_global ? global_slab(t) : alloc(nd, oext);
-        mitems.push_back(make_step(xi, y, k, 1));
-        blocks.push_back(bl);
-        xi = y;
-      }
-      add_mp(*pl, 1, l, (k == 0 ? u_in : BUF_SCRATCH), last_global ? BUF_G : BUF_SCRATCH, mitems, blocks, 2);
-    }
-    if (l > 0) {
-      std::vector<TRef> par2(static_cast<size_t>(b.nmid * pnin));
-      SumLaunch sl;
-      sl.begin = static_cast<i64>(pl->sums.size());
-      i64 work = 0;
-      for (i64 t = 0; t < b.nmid; ++t)
-        for (i64 pnu = 0; pnu < pnin; ++pnu) {
-          if (!b.owns(t)) continue;
           SumDesc sdsc{};
-          TRef first;
-          for (i64 nu = 0; nu < nin; ++nu) {
-            if (parent_of(nu, l) != pnu) continue;
-            const TRef& c = x[static_cast<size_t>(t * nin + nu)];
-            if (sdsc.nchild == 0) first = c;
-            sdsc.child_off[sdsc.nchild++] = c.off;
-          }
-          TRef y = alloc(nd, first.ext);
+          for (int c = 0; c < x.nsum; ++c) sdsc.child_off[sdsc.nchild++] = x.off + c * x.sum_stride;
+          const TRef y = alloc(nd, x.ext);
           sdsc.out_off = y.off;
           sdsc.total = y.size();
           sdsc.work_off = work;
           work += sdsc.total;
           pl->sums.push_back(sdsc);
-          par2[static_cast<size_t>(t * pnin + pnu)] = y;
+          done[x.off] = y;
+          x = y;
         }
-      sl.n = static_cast<i64>(pl->sums.size()) - sl.begin;
-      sl.total = work;
-      pl->ops.push_back(Op{2, static_cast<i64>(pl->sum_launches.size()), 2});
-      pl->sum_launches.push_back(sl);
-      gcur = par2;
+        sl.n = static_cast<i64>(pl->sums.size()) - sl.begin;
+        sl.total = work;
+        if (sl.n > 0) {
+          pl->ops.push_back(Op{2, static_cast<i64>(pl->sum_launches.size()), 2});
+          pl->sum_launches.push_back(sl);
+        }
+      }
+      std::vector<TRef> x = gcur;
+      for (int k = 0; k < d; ++k) {
+        std::vector<MPStep> mitems;
+        std::vector<std::vector<Blk>> blocks;
+        for (i64 it = 0; it < b.nmid * nin; ++it) {
+          const i64 t = it / nin;
+          if (!mine(t)) continue;
+          TRef& xi = x[static_cast<size_t>(it)];
+          int oext[kMaxTM];
+          for (int p = 0; p < nd; ++p) oext[p] = xi.ext[p];
+          std::vector<Blk> bl;
+          int ci = 0, co = 0;
+          for (i64 j = 0; j < nj; ++j) {
+            Blk B;
+            int r, w;
+            slot_info(1, l, t, it % nin, k, j, r, w, B.mat_off);
+            B.rows = r;
+            B.cols = w;
+            B.in_start = ci;
+            B.out_start = co;
+            ci += B.rows;
+            co += B.cols;
+            bl.push_back(B);
+          }
+          if (ci != xi.ext[k]) throw std::runtime_error("internal: P/U block ranks do not match the tensor extent");
+          oext[k] = co;
+          // the last mode writes the child's block of its parent (or G)
+          TRef y = k == d - 1 ? child_out[static_cast<size_t>(it)] : alloc(nd, oext);
+          mitems.push_back(make_step(xi, y, k, 1));
+          blocks.push_back(bl);
+          xi = y;
+        }
+        const int in_buf = k == 0 ? u_in : BUF_SCRATCH;
+        add_mp(*pl, 1, l, in_buf, (l == 0 && k == d - 1) ? BUF_G : BUF_SCRATCH, mitems, blocks, 2);
+      }
+      gcur = par;
     }
-  }
+    tag_ops(ops_mark, q);
+  }  // slab groups (P/U)
   pl->scratch_elems = scratch;
   cudaStream_t st = b.stream;
   pl->d_steps = to_device(pl->steps, st);
   pl->d_blks = to_device(pl->blks, st);
   pl->d_gemv = to_device(pl->gemv, st);
-  {
-    std::vector<int> map(static_cast<size_t>(std::max<i64>(pl->gemv_ctas, 1)));
-    size_t p = 0;
-    for (i64 c = 0; c < pl->gemv_ctas; ++c) {  // pair holding CTA c's first row
-      const i64 g0 = c * pl->gemv_rows_per_cta;
-      while (p + 1 < pl->gemv.size() && pl->gemv[p + 1].cta_off <= g0) ++p;
-      map[static_cast<size_t>(c)] = static_cast<int>(p);
-    }
-    pl->d_gemv_map = to_device(map, st);
-    if (pl->gemv_tma) pl->d_tma_map = to_device(pl->tma_map, st);
-  }
+  pl->d_gemv_map = to_device(pl->gemv_map, st);
+  pl->d_tma_map = to_device(pl->tma_map, st);
   pl->d_sums = to_device(pl->sums, st);
-  pl->d_bitems = to_device(pl->bitems, st);
-  pl->d_sum_map = to_device(pl->sum_map, st);
-  pl->d_bterms = to_device(pl->bterms, st);
+  pl->d_bdescs = to_device(pl->bdescs, st);
   pl->scratch.alloc(static_cast<size_t>(std::max<i64>(scratch, 1)));
   TBF_CUDA(cudaStreamSynchronize(st));
   return pl;
 }
 
-Plan& get_plan(oiobf_tbf& b, i64 nv) {
-  auto it = b.plans.find(nv);
+// chunked = true: the host-pipelined plan (ops per slab group, see
+// contract_host); the device-buffer path uses the unchunked plan
+Plan& get_plan(oiobf_tbf& b, i64 nv, bool chunked = false) {
+  const i64 key = 2 * nv + (chunked ? 1 : 0);
+  auto it = b.plans.find(key);
   if (it != b.plans.end()) return *it->second;
-  auto& slot = b.plans[nv];
-  slot = build_plan(b, nv);
+  auto& slot = b.plans[key];
+  slot = build_plan(b, nv, chunked);
   return *slot;
 }
 
@@ -1139,8 +1199,10 @@ struct OpBuffers {
   const double2* recv = nullptr;
 };
 
-// phase: 0 = whole contraction, 1 = V/W + core GEMV, 2 = P/U (sharded)
-void run_ops(oiobf_tbf& b, Plan& pl, const OpBuffers& io, cudaStream_t st, int group_filter = -1, int phase = 0) {
+// phase: 0 = whole contraction, 1 = V/W + core GEMV, 2 = P/U (sharded, or
+// one slab group of a pipelined plan); chunk >= 0: that slab group only
+void run_ops(oiobf_tbf& b, Plan& pl, const OpBuffers& io, cudaStream_t st, int group_filter = -1, int phase = 0,
+             int chunk = -1) {
   // OIOBF_ABLATE=<digits>: skip these op kinds (timing experiments only; the
   // result is wrong when set)
   static const char* ablate = std::getenv("OIOBF_ABLATE");
@@ -1152,6 +1214,7 @@ void run_ops(oiobf_tbf& b, Plan& pl, const OpBuffers& io, cudaStream_t st, int g
     if (group_filter >= 0 && op.group != group_filter) continue;
     if (phase == 1 && op.group == 2) continue;
     if (phase == 2 && op.group != 2) continue;
+    if (chunk >= 0 && op.chunk != chunk) continue;
     if (ablate && std::strchr(ablate, '0' + op.kind)) continue;
     if (op.kind == 0) {
       const MPLaunch& m = pl.mps[static_cast<size_t>(op.idx)];
@@ -1160,22 +1223,20 @@ void run_ops(oiobf_tbf& b, Plan& pl, const OpBuffers& io, cudaStream_t st, int g
                           in_ptr(m.in_buf), out_ptr(m.out_buf), st);
     } else if (op.kind == 1) {
       double2* y = pl.sharded ? io.send : pl.scratch.p;
-      if (pl.gemv_tma)
-        launch_gemv_tma(pl.d_tma_map.p, pl.d_gemv.p, pl.tma_ctas, pl.gemv_total_rows, pl.tma_rows_per_cta,
-                        static_cast<int>(pl.nv), pl.tma_stages, pl.tma_stage_elems, pl.tma_xcap, b.cores.p,
+      const GemvLaunch& gl = pl.gemvs[static_cast<size_t>(op.idx)];
+      const GemvDesc* gd = pl.d_gemv.p + gl.desc_begin;
+      if (gl.tma)
+        launch_gemv_tma(pl.d_tma_map.p + gl.tma_map_begin, gd, gl.tma_ctas, gl.total_rows, gl.tma_rows_per_cta,
+                        static_cast<int>(pl.nv), gl.tma_stages, gl.tma_stage_elems, gl.tma_xcap, b.cores.p,
                         pl.scratch.p, y, st);
       else
-        launch_gemv(pl.d_gemv_map.p, pl.d_gemv.p, pl.gemv_ctas, pl.gemv_total_rows, pl.gemv_rows_per_cta,
-                    static_cast<int>(pl.nv), b.cores.p, pl.scratch.p, y, pl.gemv_max_c, st);
+        launch_gemv(pl.d_gemv_map.p + gl.map_begin, gd, gl.ctas, gl.total_rows, gl.rows_per_cta,
+                    static_cast<int>(pl.nv), b.cores.p, pl.scratch.p, y, gl.max_c, st);
     } else if (op.kind == 3) {
       const BoxLaunch& bx = pl.boxes[static_cast<size_t>(op.idx)];
       const LevelData& ld = b.side[bx.side][static_cast<size_t>(bx.level)];
-      launch_box(bx.nitems, pl.d_bitems.p + bx.item_begin, pl.d_bterms.p + bx.item_begin, bx.info, ld.interp.p,
-                 in_ptr(bx.in_buf), out_ptr(bx.out_buf), st);
-    } else if (op.kind == 4) {
-      const SumLaunch& s = pl.sum_launches[static_cast<size_t>(op.idx)];
-      launch_sum_parent(s.total, pl.d_sums.p + s.begin, pl.d_sum_map.p + 2 * s.work_begin, pl.scratch.p,
-                        pl.scratch.p, st);
+      launch_box(bx.nitems, pl.d_bdescs.p + bx.item_begin, bx.info, ld.interp.p, in_ptr(bx.in_buf),
+                 out_ptr(bx.out_buf), st);
     } else {
       const SumLaunch& s = pl.sum_launches[static_cast<size_t>(op.idx)];
       launch_sum_children(s.n, pl.d_sums.p + s.begin, s.total, pl.scratch.p, pl.scratch.p, st);
@@ -1224,6 +1285,107 @@ void contract_device(oiobf_tbf& b, const double2* F, double2* G, i64 nv, cudaStr
     pl.g_st = st;
   }
   TBF_CUDA(cudaGraphLaunch(pl.gexec, st));
+}
+
+// Host-buffer contraction, pipelined over the slab groups of mode d-1 (each
+// group is one contiguous range of F and of G):
+//   copy-in stream   H2D F[q]                      -> event in[q]
+//   compute stream   wait in[q]; V/W + GEMV of group q   (q = 0 .. Q-1)
+//                    P/U of group q               -> event out[q]
+//   copy-out stream  wait out[q]; D2H G[q]
+// so the PCIe copies overlap the V/W side and GEMV of earlier groups and the
+// P/U side of later ones.  Pinned host buffers: captured once into a graph
+// (copy nodes included) and replayed while the pointers stay the same.
+void issue_pipeline(oiobf_tbf& b, Plan& pl, const double* F, double* G, cudaStream_t st) {
+  const int Q = pl.nchunk;
+  const i64 N = ipow(b.n, b.d);
+  const size_t chunk_bytes = static_cast<size_t>(N / Q) * sizeof(double2);
+  const size_t pitch = static_cast<size_t>(N) * sizeof(double2);
+  const size_t nv = static_cast<size_t>(pl.nv);
+  cudaEvent_t* ev = b.ev.data();  // [0] fork, [1] join, [2 + q] in, [2 + Q + q] out
+  TBF_CUDA(cudaEventRecord(ev[0], st));
+  TBF_CUDA(cudaStreamWaitEvent(b.s_in, ev[0], 0));
+  TBF_CUDA(cudaStreamWaitEvent(b.s_out, ev[0], 0));
+  char* dF = reinterpret_cast<char*>(pl.stage_F.p);
+  char* dG = reinterpret_cast<char*>(pl.stage_G.p);
+  for (int q = 0; q < Q; ++q) {
+    TBF_CUDA(cudaMemcpy2DAsync(dF + q * chunk_bytes, pitch, reinterpret_cast<const char*>(F) + q * chunk_bytes, pitch,
+                               chunk_bytes, nv, cudaMemcpyHostToDevice, b.s_in));
+    TBF_CUDA(cudaEventRecord(ev[2 + q], b.s_in));
+  }
+  OpBuffers io;
+  io.F = pl.stage_F.p;
+  io.G = pl.stage_G.p;
+  for (int q = 0; q < Q; ++q) {
+    TBF_CUDA(cudaStreamWaitEvent(st, ev[2 + q], 0));
+    run_ops(b, pl, io, st, -1, 1, q);
+  }
+  for (int q = 0; q < Q; ++q) {
+    run_ops(b, pl, io, st, -1, 2, q);
+    TBF_CUDA(cudaEventRecord(ev[2 + Q + q], st));
+    TBF_CUDA(cudaStreamWaitEvent(b.s_out, ev[2 + Q + q], 0));
+    TBF_CUDA(cudaMemcpy2DAsync(reinterpret_cast<char*>(G) + q * chunk_bytes, pitch, dG + q * chunk_bytes, pitch,
+                               chunk_bytes, nv, cudaMemcpyDeviceToHost, b.s_out));
+  }
+  TBF_CUDA(cudaEventRecord(ev[1], b.s_out));
+  TBF_CUDA(cudaStreamWaitEvent(st, ev[1], 0));
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+void contract_host(oiobf_tbf& b, const double* F, double* G, i64 nv) {
+  TBF_CUDA(cudaSetDevice(b.device));
+  Plan& pl = get_plan(b, nv, true);
+  const size_t N = static_cast<size_t>(ipow(b.n, b.d) * nv);
+  if (pl.stage_F.n != N) {  // staging buffers persist so the captured graph is reused
+    pl.stage_F.alloc(N);
+    pl.stage_G.alloc(N);
+  }
+  if (!b.s_in) {
+    TBF_CUDA(cudaStreamCreateWithFlags(&b.s_in, cudaStreamNonBlocking));
+    TBF_CUDA(cudaStreamCreateWithFlags(&b.s_out, cudaStreamNonBlocking));
+  }
+  const size_t nev = 2 + 2 * static_cast<size_t>(pl.nchunk);
+  while (b.ev.size() < nev) {
+    cudaEvent_t e;
+    TBF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    b.ev.push_back(e);
+  }
+  static const bool no_graph = std::getenv("OIOBF_NO_GRAPH") != nullptr;
+  if (no_graph || !is_pinned(F) || !is_pinned(G)) {  // pageable memory cannot be captured
+    issue_pipeline(b, pl, F, G, b.stream);
+    TBF_CUDA(cudaStreamSynchronize(b.stream));
+    return;
+  }
+  if (!pl.gexec || pl.g_F != F || pl.g_G != G) {
+    if (pl.gexec) {
+      cudaGraphExecDestroy(pl.gexec);
+      pl.gexec = nullptr;
+    }
+    cudaGraph_t g;
+    // global mode: the fork/join events pull the copy streams into the capture
+    TBF_CUDA(cudaStreamBeginCapture(b.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      issue_pipeline(b, pl, F, G, b.stream);
+    } catch (...) {
+      cudaStreamEndCapture(b.stream, &g);
+      throw;
+    }
+    TBF_CUDA(cudaStreamEndCapture(b.stream, &g));
+    TBF_CUDA(cudaGraphInstantiate(&pl.gexec, g, 0));
+    TBF_CUDA(cudaGraphDestroy(g));
+    pl.g_F = F;
+    pl.g_G = G;
+  }
+  TBF_CUDA(cudaGraphLaunch(pl.gexec, b.stream));
+  TBF_CUDA(cudaStreamSynchronize(b.stream));
 }
 
 int status_of(const std::exception& e) {
@@ -1435,18 +1597,9 @@ int oiobf_tbf_contract(oiobf_tbf* h, const double* F, double* G, int64_t nv) {
   CAPI_BEGIN
   require(h && F && G, "tbf_contract: null argument");
   require(nv >= 1, "tbf_contract: nv must be >= 1");
+  require(h->world == 1, "tbf_contract: sharded factorization -- use oiobf_tbf_contract_phase");
   std::lock_guard<std::mutex> lk(h->mu);
-  TBF_CUDA(cudaSetDevice(h->device));
-  const size_t N = static_cast<size_t>(ipow(h->n, h->d) * nv);
-  Plan& pl = get_plan(*h, nv);
-  if (pl.stage_F.n != N) {  // staging buffers persist so the captured graph is reused
-    pl.stage_F.alloc(N);
-    pl.stage_G.alloc(N);
-  }
-  TBF_CUDA(cudaMemcpyAsync(pl.stage_F.p, F, N * sizeof(double2), cudaMemcpyHostToDevice, h->stream));
-  contract_device(*h, pl.stage_F.p, pl.stage_G.p, nv, h->stream);
-  TBF_CUDA(cudaMemcpyAsync(G, pl.stage_G.p, N * sizeof(double2), cudaMemcpyDeviceToHost, h->stream));
-  TBF_CUDA(cudaStreamSynchronize(h->stream));
+  contract_host(*h, F, G, nv);
   CAPI_END
 }
 
@@ -1599,64 +1752,50 @@ int oiobf_tbf_plan_stats(oiobf_tbf* h, int64_t out[4]) {
   CAPI_END
 }
 
-// Debug: run every box launch of the nv=1 plan once with per-CTA phase stamps;
-// out gets, per box launch, [ctas, mean and max (ns) of: desc, stage, modes, reduce, total]
-int oiobf_debug_box_trace(oiobf_tbf* h, const void* dF, void* dG, double* out, int32_t max_launches) {
+// Debug (not in the public header): run the box launches of the nv = 1 plan
+// one by one with per-CTA globaltimer stamps.  out receives, per launch,
+// [nctas, cs, smem_bytes, stage, then nctas x 8 stamps (ns, relative to the
+// launch's earliest stamp)], up to max_out doubles; returns the count written
+// through *written.
+int oiobf_debug_box_trace(oiobf_tbf* h, const void* dF, void* dG, double* out, int64_t max_out, int64_t* written) {
   CAPI_BEGIN
   std::lock_guard<std::mutex> lk(h->mu);
   TBF_CUDA(cudaSetDevice(h->device));
   Plan& pl = get_plan(*h, 1);
-  DevBuf<unsigned long long> tr(1 << 22);
-  box_trace_enable(tr.p);
-  int li = 0;
+  // run the whole contraction once so scratch holds valid inputs
+  contract_device(*h, static_cast<const double2*>(dF), static_cast<double2*>(dG), 1, h->stream);
+  i64 maxc = 1;
+  for (const BoxLaunch& bx : pl.boxes) maxc = std::max(maxc, bx.nitems * bx.info.cs);
+  DevBuf<unsigned long long> tr(static_cast<size_t>(maxc * 8));
+  i64 w = 0;
+  OpBuffers io;
+  io.F = static_cast<const double2*>(dF);
+  io.G = static_cast<double2*>(dG);
   for (const Op& op : pl.ops) {
-    if (op.kind != 3 || li >= max_launches) continue;
+    if (op.kind != 3) continue;
     const BoxLaunch& bx = pl.boxes[static_cast<size_t>(op.idx)];
-    const double2* in = bx.in_buf == BUF_F ? static_cast<const double2*>(dF) : pl.scratch.p;
-    double2* o = bx.out_buf == BUF_G ? static_cast<double2*>(dG) : pl.scratch.p;
-    const LevelData& ld = h->side[bx.side][static_cast<size_t>(bx.level)];
-    TBF_CUDA(cudaMemset(tr.p, 0, tr.n * 8));
-    launch_box(bx.nitems, pl.d_bitems.p + bx.item_begin, pl.d_bterms.p + bx.item_begin, bx.info, ld.interp.p, in, o,
-               h->stream);
-    TBF_CUDA(cudaStreamSynchronize(h->stream));
     const i64 nct = bx.nitems * bx.info.cs;
+    if (w + 4 + nct * 8 > max_out) break;
+    TBF_CUDA(cudaMemsetAsync(tr.p, 0, tr.n * 8, h->stream));
+    box_trace_enable(tr.p);
+    const LevelData& ld = h->side[bx.side][static_cast<size_t>(bx.level)];
+    const double2* in = bx.in_buf == BUF_F ? io.F : pl.scratch.p;
+    double2* o = bx.out_buf == BUF_G ? io.G : pl.scratch.p;
+    launch_box(bx.nitems, pl.d_bdescs.p + bx.item_begin, bx.info, ld.interp.p, in, o, h->stream);
+    TBF_CUDA(cudaStreamSynchronize(h->stream));
+    box_trace_enable(nullptr);
     std::vector<unsigned long long> ht(static_cast<size_t>(nct * 8));
     TBF_CUDA(cudaMemcpy(ht.data(), tr.p, ht.size() * 8, cudaMemcpyDeviceToHost));
-    double* o9 = out + 11 * li;
-    o9[0] = static_cast<double>(nct);
     unsigned long long t0 = ~0ULL;
-    for (i64 c = 0; c < nct; ++c) t0 = std::min(t0, ht[static_cast<size_t>(c * 8)]);
-    for (int ph = 0; ph < 4; ++ph) {
-      double sum = 0, mx = 0;
-      for (i64 c = 0; c < nct; ++c) {
-        const double dt = static_cast<double>(ht[static_cast<size_t>(c * 8 + ph + 1)] - ht[static_cast<size_t>(c * 8 + ph)]);
-        sum += dt;
-        mx = std::max(mx, dt);
-      }
-      o9[1 + 2 * ph] = sum / nct;
-      o9[2 + 2 * ph] = mx;
-    }
-    double span = 0, late = 0;
-    for (i64 c = 0; c < nct; ++c) {
-      span = std::max(span, static_cast<double>(ht[static_cast<size_t>(c * 8 + 4)] - t0));
-      late = std::max(late, static_cast<double>(ht[static_cast<size_t>(c * 8)] - t0));
-    }
-    o9[9] = span;
-    o9[10] = late;  // last CTA start relative to the first
-    {  // second (warm) execution of the mode phase: stamps 2 -> 7 -> 3
-      double w1 = 0, w2 = 0;
-      for (i64 c = 0; c < nct; ++c) {
-        w1 += static_cast<double>(ht[static_cast<size_t>(c * 8 + 7)] - ht[static_cast<size_t>(c * 8 + 2)]);
-        w2 += static_cast<double>(ht[static_cast<size_t>(c * 8 + 3)] - ht[static_cast<size_t>(c * 8 + 7)]);
-      }
-      o9[5] = w1 / nct;  // modes, first (cold) pass
-      o9[6] = w2 / nct;  // modes, second (warm) pass
-    }
-    // effective SM clock (MHz) of CTA 0: cycles / ns
-    o9[0] += 1e-6 * static_cast<double>(ht[6] - ht[5]) / std::max(1.0, static_cast<double>(ht[4] - ht[0])) * 1000.0;
-    ++li;
+    for (unsigned long long v : ht)
+      if (v) t0 = std::min(t0, v);
+    out[w++] = static_cast<double>(nct);
+    out[w++] = bx.info.cs;
+    out[w++] = static_cast<double>(box_smem_bytes(bx.info));
+    out[w++] = bx.info.stage;
+    for (unsigned long long v : ht) out[w++] = v ? static_cast<double>(v - t0) : -1.0;
   }
-  box_trace_enable(nullptr);
+  *written = w;
   CAPI_END
 }
 

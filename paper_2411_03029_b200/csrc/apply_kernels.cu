@@ -80,7 +80,8 @@ __device__ __forceinline__ double2 ld_stream2(const double2* p) {
 }
 
 // Persistent, balanced core GEMV: CTA i owns the contiguous global row range
-// [i*rows_per_cta, (i+1)*rows_per_cta) over all pairs (rows of a pair are
+// [row_begin[i], row_begin[i+1]) over all pairs, split so every CTA streams
+// the same number of core BYTES (row lengths differ per pair; rows of a pair are
 // contiguous in the core arena), so every SM streams the same number of
 // bytes.  Per pair segment the CTA stages x = F_{t,s} in shared memory, then
 // each warp walks whole rows with 8 independent 16-B streaming loads per lane
@@ -88,13 +89,14 @@ __device__ __forceinline__ double2 ld_stream2(const double2* p) {
 template <int NV>  // NV = 1: single-vector fast path; NV = 0: generic nv
 __global__ void __launch_bounds__(kGemvThreads, 4) k_gemv(const int* __restrict__ cta_pair,
                                                        const GemvDesc* __restrict__ ds, int nv_rt, long long total_rows,
-                                                       long long rows_per_cta, const double2* __restrict__ cores,
+                                                       const long long* __restrict__ row_begin,
+                                                       const double2* __restrict__ cores,
                                                        const double2* __restrict__ x, double2* __restrict__ y) {
   extern __shared__ __align__(16) double2 sx[];
   const int nv = NV == 1 ? 1 : nv_rt;
   constexpr int kAcc = NV == 1 ? 1 : 4;
-  const long long g0 = static_cast<long long>(blockIdx.x) * rows_per_cta;
-  const long long g1 = min(total_rows, g0 + rows_per_cta);
+  const long long g0 = row_begin[blockIdx.x];
+  const long long g1 = min(total_rows, row_begin[blockIdx.x + 1]);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int p = cta_pair[blockIdx.x];
   long long g = g0;
@@ -200,7 +202,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 
 __global__ void __launch_bounds__(kTmaThreads) k_gemv_tma(const int* __restrict__ cta_pair,
                                                               const GemvDesc* __restrict__ ds, int nv,
-                                                              long long total_rows, long long rows_per_cta,
+                                                              long long total_rows,
+                                                              const long long* __restrict__ row_begin,
                                                               int stages, int stage_elems, int xcap,
                                                               const double2* __restrict__ cores,
                                                               const double2* __restrict__ x,
@@ -212,8 +215,8 @@ __global__ void __launch_bounds__(kTmaThreads) k_gemv_tma(const int* __restrict_
   double2* sxs = ring + static_cast<long long>(stages) * stage_elems;  // kTmaMaxPairs x-slots of xcap
   __shared__ GemvDesc pd[kTmaMaxPairs];
   __shared__ int npairs_s;
-  const long long g0 = static_cast<long long>(blockIdx.x) * rows_per_cta;
-  const long long g1 = min(total_rows, g0 + rows_per_cta);
+  const long long g0 = row_begin[blockIdx.x];
+  const long long g1 = min(total_rows, row_begin[blockIdx.x + 1]);
   const int p0 = cta_pair[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -302,29 +305,29 @@ void launch_mode_product(i64 nitems, const MPStep* steps, i64 total_out, const B
   TBF_CUDA(cudaGetLastError());
 }
 
-void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, i64 rows_per_cta, int nv,
+void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, const i64* row_begin, int nv,
                  const double2* cores, const double2* x, double2* y, int max_c, cudaStream_t st) {
   if (nctas == 0) return;
   const size_t smem = sizeof(double2) * static_cast<size_t>(max_c) * nv;
   if (nv == 1) {
     TBF_CUDA(cudaFuncSetAttribute(k_gemv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-    k_gemv<1><<<static_cast<unsigned>(nctas), kGemvThreads, smem, st>>>(cta_pair, d, nv, total_rows, rows_per_cta,
+    k_gemv<1><<<static_cast<unsigned>(nctas), kGemvThreads, smem, st>>>(cta_pair, d, nv, total_rows, row_begin,
                                                                         cores, x, y);
   } else {
     TBF_CUDA(cudaFuncSetAttribute(k_gemv<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-    k_gemv<0><<<static_cast<unsigned>(nctas), kGemvThreads, smem, st>>>(cta_pair, d, nv, total_rows, rows_per_cta,
+    k_gemv<0><<<static_cast<unsigned>(nctas), kGemvThreads, smem, st>>>(cta_pair, d, nv, total_rows, row_begin,
                                                                         cores, x, y);
   }
   TBF_CUDA(cudaGetLastError());
 }
 
-void launch_gemv_tma(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, i64 rows_per_cta, int nv,
+void launch_gemv_tma(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, const i64* row_begin, int nv,
                      int stages, int stage_elems, int xcap, const double2* cores, const double2* x, double2* y,
                      cudaStream_t st) {
   if (nctas == 0) return;
   const size_t smem = gemv_tma_smem_bytes(stages, stage_elems, xcap);
   TBF_CUDA(cudaFuncSetAttribute(k_gemv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-  k_gemv_tma<<<static_cast<unsigned>(nctas), kTmaThreads, smem, st>>>(cta_pair, d, nv, total_rows, rows_per_cta,
+  k_gemv_tma<<<static_cast<unsigned>(nctas), kTmaThreads, smem, st>>>(cta_pair, d, nv, total_rows, row_begin,
                                                                       stages, stage_elems, xcap, cores, x, y);
   TBF_CUDA(cudaGetLastError());
 }

@@ -67,12 +67,12 @@ struct GemvDesc {  // y(R x nv) = K(R x C, row-major) * x(C x nv)
   i64 cta_off;     // prefix of CTA counts
 };
 // cta_pair[i] = pair holding CTA i's first row; GemvDesc.cta_off = the pair's
-// first global row
-void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, i64 rows_per_cta, int nv,
+// first global row; CTA i owns rows [row_begin[i], row_begin[i+1]) (byte-balanced)
+void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, const i64* row_begin, int nv,
                  const double2* cores, const double2* x, double2* y, int max_c, cudaStream_t st);
 int gemv_ctas_per_sm(int nv, int max_c);
 // TMA bulk-copy pipelined variant (rows staged by cp.async.bulk into an SMEM ring)
-void launch_gemv_tma(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, i64 rows_per_cta, int nv,
+void launch_gemv_tma(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, const i64* row_begin, int nv,
                      int stages, int stage_elems, int xcap, const double2* cores, const double2* x, double2* y,
                      cudaStream_t st);
 size_t gemv_tma_smem_bytes(int stages, int stage_elems, int xcap);

@@ -201,11 +201,12 @@ struct Op {
 // one core-GEMV launch (all pairs, or the pairs of one column-slab group)
 struct GemvLaunch {
   i64 desc_begin = 0, ndesc = 0;
-  i64 total_rows = 0, rows_per_cta = 1, ctas = 0;
+  i64 total_rows = 0, ctas = 0;
   i64 map_begin = 0;  // into Plan::gemv_map (CTA -> pair, relative to desc_begin)
+  i64 rb_begin = 0;   // into Plan::gemv_rb (CTA row ranges, ctas + 1 entries)
   int max_c = 0;
   bool tma = false;
-  i64 tma_ctas = 0, tma_rows_per_cta = 1, tma_map_begin = 0;
+  i64 tma_ctas = 0, tma_map_begin = 0, tma_rb_begin = 0;
   int tma_stages = 0, tma_stage_elems = 0, tma_xcap = 0;
 };
 
@@ -219,7 +220,9 @@ struct Plan {
   std::vector<GemvDesc> gemv;
   std::vector<GemvLaunch> gemvs;
   std::vector<int> gemv_map, tma_map;
+  std::vector<i64> gemv_rb;  // CTA row ranges of every GEMV launch (both variants)
   DevBuf<int> d_tma_map;
+  DevBuf<i64> d_gemv_rb;
   std::vector<SumDesc> sums;
   std::vector<SumLaunch> sum_launches;
   std::vector<Op> ops;
@@ -250,6 +253,53 @@ struct Plan {
 // Fill a GemvLaunch for descs [begin, end) of pl.gemv: persistent balanced
 // grid for the register-streaming kernel, and the TMA-ring parameters when
 // they apply.  cta_off of the descriptors is relative to the launch.
+// Byte-balanced row split of descs [begin, end) over nct CTAs: CTA c gets
+// rows [rb[c], rb[c+1]) holding ~1/nct of the core elements (row lengths C
+// differ per pair, so equal row counts would leave the long-row CTAs last).
+// map[c] = pair (relative to begin) holding CTA c's first row.  Returns the
+// largest number of pairs any CTA touches.
+int split_rows(const Plan& pl, i64 begin, i64 end, i64 nct, std::vector<i64>& rb, std::vector<int>& map) {
+  // cost of a row = its C elements + a fixed per-row overhead (warp reduction,
+  // row setup, the dependent load batches of one warp), in element units.
+  // Measured on B200 (config 2): pure bytes (K = 0) 96 us, K = 64 92 us,
+  // K >= 1024 (about equal rows) 87 us.  OIOBF_GEMV_ROW_COST overrides.
+  static const i64 K = std::getenv("OIOBF_GEMV_ROW_COST") ? std::atoll(std::getenv("OIOBF_GEMV_ROW_COST")) : 1024;
+  auto cost = [&](i64 q) { return static_cast<i64>(pl.gemv[static_cast<size_t>(q)].C) + K; };
+  i64 E = 0;
+  for (i64 q = begin; q < end; ++q) E += pl.gemv[static_cast<size_t>(q)].R * cost(q);
+  const GemvDesc& last = pl.gemv[static_cast<size_t>(end - 1)];
+  const i64 rows = last.cta_off + last.R;
+  rb.assign(static_cast<size_t>(nct + 1), rows);
+  rb[0] = 0;
+  i64 q = begin, before = 0;  // cost before pair q
+  for (i64 c = 1; c < nct; ++c) {
+    const i64 target = E / nct * c + std::min<i64>(c, E % nct);
+    while (q + 1 < end && before + pl.gemv[static_cast<size_t>(q)].R * cost(q) <= target) {
+      before += pl.gemv[static_cast<size_t>(q)].R * cost(q);
+      ++q;
+    }
+    const GemvDesc& g = pl.gemv[static_cast<size_t>(q)];
+    const i64 r = std::min<i64>(g.R, (target - before + cost(q) - 1) / cost(q));
+    rb[static_cast<size_t>(c)] = std::max(rb[static_cast<size_t>(c - 1)], g.cta_off + r);
+  }
+  map.assign(static_cast<size_t>(nct), 0);
+  int maxp = 0;
+  size_t p = static_cast<size_t>(begin);
+  for (i64 c = 0; c < nct; ++c) {
+    const i64 g0 = rb[static_cast<size_t>(c)], g1 = rb[static_cast<size_t>(c + 1)];
+    while (p + 1 < static_cast<size_t>(end) && pl.gemv[p + 1].cta_off <= g0) ++p;
+    map[static_cast<size_t>(c)] = static_cast<int>(p - static_cast<size_t>(begin));
+    size_t p2 = p;
+    while (p2 + 1 < static_cast<size_t>(end) && pl.gemv[p2 + 1].cta_off < g1) ++p2;
+    if (g1 > g0) maxp = std::max(maxp, static_cast<int>(p2 - p + 1));
+  }
+  return maxp;
+}
+
+// Fill a GemvLaunch for descs [begin, end) of pl.gemv: persistent
+// byte-balanced grid for the register-streaming kernel, and the TMA-ring
+// parameters when they apply.  cta_off of the descriptors is relative to the
+// launch.
 void finish_gemv(Plan& pl, i64 begin, i64 end, i64 nv) {
   GemvLaunch gl;
   gl.desc_begin = begin;
@@ -262,36 +312,30 @@ void finish_gemv(Plan& pl, i64 begin, i64 end, i64 nv) {
     gl.max_c = std::max(gl.max_c, g.C);
   }
   gl.total_rows = rows;
+  if (rows == 0) {
+    pl.gemvs.push_back(gl);
+    return;
+  }
+  std::vector<i64> rb;
+  std::vector<int> map;
   {
     const int per_sm = gemv_ctas_per_sm(static_cast<int>(nv), std::max(gl.max_c, 1));
-    i64 grid = std::min<i64>(static_cast<i64>(148) * per_sm, std::max<i64>(rows, 1));
-    gl.rows_per_cta = (rows + grid - 1) / grid;
-    grid = (rows + gl.rows_per_cta - 1) / gl.rows_per_cta;
-    gl.ctas = rows == 0 ? 0 : grid;
-  }
-  gl.map_begin = static_cast<i64>(pl.gemv_map.size());
-  {
-    size_t p = static_cast<size_t>(begin);
-    for (i64 c = 0; c < gl.ctas; ++c) {  // pair holding CTA c's first row
-      const i64 g0 = c * gl.rows_per_cta;
-      while (p + 1 < static_cast<size_t>(end) && pl.gemv[p + 1].cta_off <= g0) ++p;
-      pl.gemv_map.push_back(static_cast<int>(p - static_cast<size_t>(begin)));
-    }
+    gl.ctas = std::min<i64>(static_cast<i64>(148) * per_sm, rows);
+    split_rows(pl, begin, end, gl.ctas, rb, map);
+    gl.map_begin = static_cast<i64>(pl.gemv_map.size());
+    gl.rb_begin = static_cast<i64>(pl.gemv_rb.size());
+    pl.gemv_map.insert(pl.gemv_map.end(), map.begin(), map.end());
+    pl.gemv_rb.insert(pl.gemv_rb.end(), rb.begin(), rb.end());
   }
   // TMA bulk-copy pipeline: one persistent CTA per SM, whole rows staged in a
   // shared-memory ring; used when rows are long enough to be worth a bulk
   // copy and every CTA's row range touches <= gemv_tma_max_pairs() pairs.
   static const bool no_tma = std::getenv("OIOBF_GEMV_NO_TMA") != nullptr;
-  // measured on B200 (config 2): 2 CTAs/SM x 8 stages = 73% of HBM, same as
-  // the register-streaming kernel; 1 CTA/SM is consumer-bound (45%)
   static const int per_sm_env =
       std::getenv("OIOBF_TMA_CTAS_PER_SM") ? std::atoi(std::getenv("OIOBF_TMA_CTAS_PER_SM")) : 2;
   static const int stages_env = std::getenv("OIOBF_TMA_STAGES") ? std::atoi(std::getenv("OIOBF_TMA_STAGES")) : 8;
-  const i64 ctas = rows;
-  if (!no_tma && gl.max_c >= 64 && ctas > 0) {
-    i64 grid = std::min<i64>(148 * std::max(1, per_sm_env), ctas);
-    const i64 rpc2 = (ctas + grid - 1) / grid;
-    grid = (ctas + rpc2 - 1) / rpc2;
+  if (!no_tma && gl.max_c >= 64) {
+    const i64 grid = std::min<i64>(148 * std::max(1, per_sm_env), rows);
     const int stage_elems = (gl.max_c + 7) / 8 * 8;
     const int xcap = gl.max_c * static_cast<int>(nv);
     const i64 avail = static_cast<i64>(kMaxDynSmem) / std::max(1, per_sm_env) - 1024 -
@@ -302,28 +346,22 @@ void finish_gemv(Plan& pl, i64 begin, i64 end, i64 nv) {
     i64 stages = std::min<i64>(stages_env, avail / (static_cast<i64>(stage_elems) * 16));
     stages = stages / 8 * 8;
     bool ok = stages >= 8;
-    std::vector<int> map(static_cast<size_t>(grid));
-    size_t q = static_cast<size_t>(begin);
-    for (i64 c = 0; c < grid && ok; ++c) {
-      const i64 g0 = c * rpc2, g1 = std::min(ctas, g0 + rpc2);
-      while (q + 1 < static_cast<size_t>(end) && pl.gemv[q + 1].cta_off <= g0) ++q;
-      map[static_cast<size_t>(c)] = static_cast<int>(q - static_cast<size_t>(begin));
-      size_t q2 = q;
-      while (q2 + 1 < static_cast<size_t>(end) && pl.gemv[q2 + 1].cta_off < g1) ++q2;
-      if (static_cast<int>(q2 - q + 1) > gemv_tma_max_pairs()) ok = false;
-    }
+    std::vector<i64> rb2;
+    std::vector<int> map2;
+    if (ok) ok = split_rows(pl, begin, end, grid, rb2, map2) <= gemv_tma_max_pairs();
     if (std::getenv("OIOBF_DEBUG"))
-      fprintf(stderr, "[oiobf] gemv tma ok=%d grid=%lld rows/cta=%lld stages=%lld stage_elems=%d xcap=%d rows=%lld\n",
-              ok ? 1 : 0, grid, rpc2, stages, stage_elems, xcap, ctas);
+      fprintf(stderr, "[oiobf] gemv tma ok=%d grid=%lld stages=%lld stage_elems=%d xcap=%d rows=%lld\n", ok ? 1 : 0,
+              grid, stages, stage_elems, xcap, rows);
     if (ok) {
       gl.tma = true;
       gl.tma_ctas = grid;
-      gl.tma_rows_per_cta = rpc2;
       gl.tma_stages = static_cast<int>(stages);
       gl.tma_stage_elems = stage_elems;
       gl.tma_xcap = xcap;
       gl.tma_map_begin = static_cast<i64>(pl.tma_map.size());
-      pl.tma_map.insert(pl.tma_map.end(), map.begin(), map.end());
+      gl.tma_rb_begin = static_cast<i64>(pl.gemv_rb.size());
+      pl.tma_map.insert(pl.tma_map.end(), map2.begin(), map2.end());
+      pl.gemv_rb.insert(pl.gemv_rb.end(), rb2.begin(), rb2.end());
     }
   }
   pl.gemvs.push_back(gl);
@@ -1173,6 +1211,7 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked) {
   pl->d_blks = to_device(pl->blks, st);
   pl->d_gemv = to_device(pl->gemv, st);
   pl->d_gemv_map = to_device(pl->gemv_map, st);
+  pl->d_gemv_rb = to_device(pl->gemv_rb, st);
   pl->d_tma_map = to_device(pl->tma_map, st);
   pl->d_sums = to_device(pl->sums, st);
   pl->d_bdescs = to_device(pl->bdescs, st);
@@ -1226,11 +1265,11 @@ void run_ops(oiobf_tbf& b, Plan& pl, const OpBuffers& io, cudaStream_t st, int g
       const GemvLaunch& gl = pl.gemvs[static_cast<size_t>(op.idx)];
       const GemvDesc* gd = pl.d_gemv.p + gl.desc_begin;
       if (gl.tma)
-        launch_gemv_tma(pl.d_tma_map.p + gl.tma_map_begin, gd, gl.tma_ctas, gl.total_rows, gl.tma_rows_per_cta,
-                        static_cast<int>(pl.nv), gl.tma_stages, gl.tma_stage_elems, gl.tma_xcap, b.cores.p,
-                        pl.scratch.p, y, st);
+        launch_gemv_tma(pl.d_tma_map.p + gl.tma_map_begin, gd, gl.tma_ctas, gl.total_rows,
+                        pl.d_gemv_rb.p + gl.tma_rb_begin, static_cast<int>(pl.nv), gl.tma_stages,
+                        gl.tma_stage_elems, gl.tma_xcap, b.cores.p, pl.scratch.p, y, st);
       else
-        launch_gemv(pl.d_gemv_map.p + gl.map_begin, gd, gl.ctas, gl.total_rows, gl.rows_per_cta,
+        launch_gemv(pl.d_gemv_map.p + gl.map_begin, gd, gl.ctas, gl.total_rows, pl.d_gemv_rb.p + gl.rb_begin,
                     static_cast<int>(pl.nv), b.cores.p, pl.scratch.p, y, gl.max_c, st);
     } else if (op.kind == 3) {
       const BoxLaunch& bx = pl.boxes[static_cast<size_t>(op.idx)];

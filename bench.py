@@ -245,12 +245,20 @@ def run_b200(args):
     pin_F = torch.from_numpy(np.ascontiguousarray(Fh.reshape(-1, order="F")).view(np.float64).copy()).pin_memory()
     pin_G = torch.empty_like(pin_F).pin_memory()
     Fv, Gv = pin_F.numpy(), pin_G.numpy()
-    for _ in range(2):
+    # warm-up by time, not count: the host<->device path needs ~0.1 s of
+    # sustained traffic before the PCIe link reaches full speed (measured on
+    # the B200 box: the first ~120 calls run ~1.7x slower)
+    t_end = time.perf_counter() + 0.3
+    nw = 0
+    while nw < max(args.warmup, 2) or time.perf_counter() < t_end:
+        flush.zero_()
         _lib.check(L.oiobf_tbf_contract(bf.handle, Fv, Gv, args.nv))
+        nw += 1
     if ws > 1:
         torch.distributed.barrier()
     e2e_times = []
-    for _ in range(args.steps):
+    e2e_steps = max(args.steps, 50)
+    for _ in range(e2e_steps):
         flush.zero_()
         torch.cuda.synchronize()
         t = time.perf_counter()
@@ -299,7 +307,8 @@ def run_b200(args):
                    "l2": "flushed (256 MiB write) before every timed step",
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
         "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step": 16 * N,
-                "d2h_bytes_per_step": 16 * N},
+                "d2h_bytes_per_step": 16 * N, "steps": e2e_steps, "warmup_calls": nw,
+                "api": "oiobf_tbf_contract (pinned host F/G; copies pipelined over slab groups)"},
         "gpu_launches": int(stats["launches"]) * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "kernel": "k_gemv (middle-level core contraction)",
@@ -387,8 +396,18 @@ def run_b200_sharded(args):
     pin_F = torch.from_numpy(np.ascontiguousarray(Fh.reshape(-1, order="F")).view(np.float64).copy()).pin_memory()
     pin_G = torch.empty_like(pin_F).pin_memory()
     e2e = []
+
+    def e2e_step():
+        F.copy_(pin_F, non_blocking=True)
+        step()
+        pin_G.copy_(G, non_blocking=True)
+        torch.cuda.synchronize()
+
+    t_end = time.perf_counter() + 0.3  # PCIe link warm-up (see run_b200)
+    while time.perf_counter() < t_end:
+        e2e_step()
     dist.barrier()
-    for _ in range(args.steps):
+    for _ in range(max(args.steps, 50)):
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         F.copy_(pin_F, non_blocking=True)

@@ -119,6 +119,12 @@ int oiobf_tbf_contract(oiobf_tbf* h, const double* F, double* G, int64_t nv);
 int oiobf_tbf_contract_device(oiobf_tbf* h, const void* dF, void* dG, int64_t nv, void* stream);
 
 /* tbf_memory: bytes of V, W, U, P, cores (out[5]). */
+// Apply engine: 0 auto (the tiny-box engine when every box has <= 64
+// elements and there are >= 2^20 middle pairs, e.g. the d = 6 DFT), 1 the
+// fused-box engine, 2 the tiny-box engine.  Changing it drops cached plans.
+int oiobf_tbf_set_apply_engine(oiobf_tbf* h, int32_t engine);
+int oiobf_tbf_apply_engine(oiobf_tbf* h, int32_t* engine);  // engine in use: 1 box, 2 tiny
+
 int oiobf_tbf_memory(const oiobf_tbf* h, int64_t out[5]);
 
 /* info[0..9]: d, n, L, Lc, nmid, total_slots, total_skel, total_interp,

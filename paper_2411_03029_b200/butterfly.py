@@ -267,6 +267,16 @@ class TensorButterfly:
         _lib.check(_lib.load().oiobf_tbf_contract(self._h, _cx_f(F), out, nv))
         return _from_f(out, F.shape)
 
+    def set_apply_engine(self, engine: str) -> None:
+        """'auto' | 'box' | 'tiny' (tiny: thread-per-output engine for d = 6 scale)."""
+        code = {"auto": 0, "box": 1, "tiny": 2}[engine]
+        _lib.check(_lib.load().oiobf_tbf_set_apply_engine(self._h, code))
+
+    def apply_engine(self) -> str:
+        e = C.c_int32(0)
+        _lib.check(_lib.load().oiobf_tbf_apply_engine(self._h, C.byref(e)))
+        return {1: "box", 2: "tiny"}[e.value]
+
     def contract_device(self, dF: int, dG: int, nv: int = 1, stream: int = 0) -> None:
         """Device pointers (double2*) already in HBM; enqueued on `stream`."""
         _lib.check(_lib.load().oiobf_tbf_contract_device(self._h, C.c_void_p(dF), C.c_void_p(dG), nv,

@@ -519,6 +519,131 @@ void launch_finish(const LevelDesc& L, double tol, double tie_eps, i64 max_rank,
   TBF_CUDA(cudaGetLastError());
 }
 
+// ---------------------------------------------------------------------------
+// Narrow column IDs of the separable DFT kernel (config 4: every candidate set
+// has w <= 2 columns over m = 131,072 proxy rows).  The DFT entry is
+// K = exp(-2 pi i/n * sum_p (a_p - 1)(b_p - 1 - n/2)) with a, b the
+// (bit-reversed) target / source indices, so the two candidate columns of a
+// slot differ only in the factor of the unfolded mode k, and over the
+// Cartesian-product proxy rows
+//   |a_0|^2 = |a_1|^2 = m,   a_0^H a_1 = (m / cnt) * S,   S = sum_x w^(-e_x)
+// with x running over the cnt proxies of the mode paired with k and
+// e_x = (phase of column 1 - phase of column 0) mod n.  The reference QRCP on
+// the explicit m x 2 matrix (id.cpp:24-85) therefore reduces to: first pivot
+// a tie (column norms equal; gap 0 reported, oracle replay),
+// residual^2 = m (1 - |S|^2 / cnt^2) against (tol |R11|)^2 = tol^2 m, and
+// T = R11^-1 R12 = S / cnt.  When every e_x is equal (the two-sided
+// bit-reversed DFT, where all ranks are exactly 1) the residual is exactly 0
+// and T = w^(-e) is computed with the entry formula itself.  One thread per
+// slot; only the paired mode's proxy list is regenerated (same seeds as
+// k_gen_proxies), so no proxy, panel or R buffers are needed.
+__global__ void k_narrow_dft(LevelDesc L, KSpec ks, double tol, const int* __restrict__ crank,
+                             const i64* __restrict__ cskel_off, const int* __restrict__ cskel,
+                             int* __restrict__ width_out, int* __restrict__ rank_out, int* __restrict__ sat_out,
+                             int* __restrict__ perm_out, int* __restrict__ skel_tmp, double2* __restrict__ interp_tmp,
+                             double* __restrict__ gap_out) {
+  const i64 slot = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (slot >= L.nslots) return;
+  const SlotPos s = decode_slot(L, slot);
+  sat_out[slot] = 0;
+  if (!owns_outer(L, s.outer)) {
+    width_out[slot] = 0;
+    rank_out[slot] = 0;
+    return;
+  }
+  int tg[2];
+  int w = 0;
+  if (L.l == 0) {
+    for (i64 c = 0; c < s.sz[s.skip] && w < 2; ++c) tg[w++] = static_cast<int>(s.lo[s.skip] + c);
+  } else {
+    const i64 c0 = child_slot(L, s, 0), c1 = child_slot(L, s, 1);
+    for (int c = 0; c < crank[c0]; ++c) tg[w++] = cskel[cskel_off[c0] + c];
+    for (int c = 0; c < crank[c1]; ++c) tg[w++] = cskel[cskel_off[c1] + c];
+  }
+  width_out[slot] = w;
+  int* perm = perm_out + slot * L.wmax;
+  int* skel = skel_tmp + slot * L.wmax;
+  double2* interp = interp_tmp + slot * L.wmax * L.wmax;
+  if (w == 0) {
+    rank_out[slot] = 0;
+    return;
+  }
+  if (w == 1) {  // |K| = 1: the column norm is sqrt(m) > 0, rank 1
+    perm[0] = 0;
+    skel[0] = tg[0];
+    interp[0] = make_double2(1, 0);
+    rank_out[slot] = 1;
+    gap_out[slot] = INFINITY;
+    return;
+  }
+  // paired mode: V side (columns = source mode k) pairs with target mode k;
+  // U side (columns = target mode k) pairs with source mode k
+  const int pm = L.side == 0 ? static_cast<int>(s.k) : L.d + static_cast<int>(s.k);
+  const i64 cnt = L.counts[s.k][pm];
+  const u64 tags[7] = {L.side_tag, static_cast<u64>(L.l), static_cast<u64>(s.outer), static_cast<u64>(s.inner),
+                       static_cast<u64>(s.k), static_cast<u64>(s.j), 0ULL};
+  const u64 sseed = derive_seed(L.seed, tags, 7);
+  const u64 ptags[2] = {0x70ULL, static_cast<u64>(pm)};
+  const u64 pseed = derive_seed(sseed, ptags, 2);
+  int px[kMaxProxy];
+  const i64 np = L.proxy_mode == OIOBF_PROXY_ALL ? s.sz[pm] : select_proxies(s.sz[pm], cnt, L.proxy_mode, pseed, px);
+  const i64 n = ks.n;
+  auto br = [&](i64 idx) { return ks.bitrev ? bitrev1(idx, n) : idx; };
+  const i64 t0 = br(tg[0]), t1 = br(tg[1]);
+  int e_first = -1;
+  bool all_equal = true;
+  double2 S = make_double2(0, 0);
+  for (i64 q = 0; q < np; ++q) {
+    const i64 x = (L.proxy_mode == OIOBF_PROXY_ALL ? q + 1 : px[q]) + s.lo[pm] - 1;
+    const i64 bx = br(x);
+    i64 e = L.side == 0 ? (bx - 1) * (t1 - t0) : (t1 - t0) * (bx - 1 - n / 2);
+    e %= n;
+    if (e < 0) e += n;
+    if (e_first < 0) e_first = static_cast<int>(e);
+    all_equal &= (e == e_first);
+    double sn, cs;
+    sincos(__dmul_rn(M_PI, __ddiv_rn(2.0 * static_cast<double>(e), static_cast<double>(n))), &sn, &cs);
+    S = make_double2(S.x + cs, S.y - sn);
+  }
+  const double dn = static_cast<double>(np);
+  const double def = all_equal ? 0.0 : fmax(0.0, 1.0 - (S.x * S.x + S.y * S.y) / (dn * dn));
+  perm[0] = 0;  // exact tie: first column in current order (reference strict >)
+  perm[1] = 1;
+  gap_out[slot] = 0.0;
+  if (def <= tol * tol) {
+    double2 T;
+    if (all_equal) {
+      double sn, cs;
+      sincos(__dmul_rn(M_PI, __ddiv_rn(2.0 * static_cast<double>(e_first), static_cast<double>(n))), &sn, &cs);
+      T = make_double2(cs, -sn);
+    } else {
+      T = make_double2(S.x / dn, S.y / dn);
+    }
+    skel[0] = tg[0];
+    interp[0] = make_double2(1, 0);  // r x w col-major, ld 1
+    interp[1] = T;
+    rank_out[slot] = 1;
+  } else {  // full rank: skeleton = both candidates (already in order), interp = I
+    skel[0] = tg[0];
+    skel[1] = tg[1];
+    interp[0] = make_double2(1, 0);
+    interp[1] = make_double2(0, 0);
+    interp[2] = make_double2(0, 0);
+    interp[3] = make_double2(1, 0);
+    rank_out[slot] = 2;
+  }
+}
+
+void launch_narrow_dft(const LevelDesc& L, const KSpec& ks, double tol, const int* crank, const i64* cskel_off,
+                       const int* cskel, int* width, int* rank, int* sat, int* perm, int* skel_tmp, double2* interp_tmp,
+                       double* gaps, cudaStream_t st) {
+  if (L.nslots == 0) return;
+  k_narrow_dft<<<static_cast<unsigned>((L.nslots + 127) / 128), 128, 0, st>>>(L, ks, tol, crank, cskel_off, cskel, width,
+                                                                             rank, sat, perm, skel_tmp, interp_tmp,
+                                                                             gaps);
+  TBF_CUDA(cudaGetLastError());
+}
+
 void launch_compact(i64 nslots, i64 wmax, const int* rank, const int* width, const i64* skel_off,
                     const i64* interp_off, const int* skel_tmp, const double2* interp_tmp, int* skel, double2* interp,
                     cudaStream_t st) {

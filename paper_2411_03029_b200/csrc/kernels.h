@@ -17,6 +17,10 @@ void launch_panel(const LevelDesc& L, const KSpec& ks, const int* proxies, const
 void launch_finish(const LevelDesc& L, double tol, double tie_eps, i64 max_rank, const double2* rpart,
                    const int* targets, const int* width, int* rank, int* sat, int* perm, int* skel_tmp,
                    double2* interp_tmp, double* gaps, cudaStream_t st);
+// closed-form narrow (w <= 2) column IDs of the separable DFT kernel
+void launch_narrow_dft(const LevelDesc& L, const KSpec& ks, double tol, const int* crank, const i64* cskel_off,
+                       const int* cskel, int* width, int* rank, int* sat, int* perm, int* skel_tmp, double2* interp_tmp,
+                       double* gaps, cudaStream_t st);
 void launch_compact(i64 nslots, i64 wmax, const int* rank, const int* width, const i64* skel_off,
                     const i64* interp_off, const int* skel_tmp, const double2* interp_tmp, int* skel, double2* interp,
                     cudaStream_t st);
@@ -115,6 +119,25 @@ int box_ctas_per_sm(int amax, size_t smem);  // occupancy of k_box
 void box_trace_enable(unsigned long long* buf);  // debug: 8 globaltimer stamps per CTA
 // programmatic dependent launch for the apply kernels (env OIOBF_NO_PDL=1 disables)
 bool pdl_enabled();
+
+// ---- tiny-box apply engine (tiny_kernels.cu): thread per output element,
+// block geometry read from the level's slot arrays (no per-box descriptors)
+constexpr int kTinyBox = 64;  // largest box (elements) the engine is chosen for
+struct TinyItem {             // one output tensor of a level
+  i64 out_off, out_start;     // element offset; prefix of output elements (thread map)
+  i64 outer, inner;           // V/W: (s, tau); P/U: (t, parent p_nu)
+  i64 first_child;            // P/U: smallest child nu of p_nu (its widths give the output extents)
+};
+struct TinyLevelArgs {
+  int side, l, d, in_global, out_global, pad;
+  i64 nin, nj, nitems, total_out;
+  i64 gstride[kMaxD + 1];  // strides of the global n^d x nv tensor (V0 input / U0 output)
+};
+void launch_tiny_level(const TinyLevelArgs& a, const TinyItem* items, const i64* in_off_of, const int* rank,
+                       const int* width, const i64* moff, const double2* mats, const double2* in, double2* out,
+                       cudaStream_t st);
+void launch_tiny_gemv(const GemvDesc* d, i64 npairs, i64 total_rows, int nv, const double2* cores, const double2* x,
+                      double2* y, cudaStream_t st);
 
 // ---- dense check (core_kernels.cu)
 unsigned long long count_nonfinite(const double2* x, i64 n, cudaStream_t st);

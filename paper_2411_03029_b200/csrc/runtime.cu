@@ -193,7 +193,7 @@ struct BoxLaunch {
   BoxLaunchInfo info;
 };
 struct Op {
-  int kind;  // 0 mode product, 1 gemv, 2 ordered child sums, 3 fused boxes
+  int kind;  // 0 mode product, 1 gemv, 2 ordered child sums, 3 fused boxes, 6 tiny level, 7 tiny gemv
   i64 idx;
   int group;  // 0 V/W, 1 core, 2 P/U
   int chunk = 0;  // pipelined plans: slab group (outer index of mode d-1)
@@ -217,6 +217,17 @@ struct Plan {
   std::vector<Blk> blks;
   std::vector<MPLaunch> mps;
   int nchunk = 1;  // > 1: host-pipelined plan (ops tagged by slab group)
+  // tiny-box engine (tiny_kernels.cu): one launch per level + a row GEMV
+  struct TinyLevel {
+    int side, l, in_buf, out_buf;
+    i64 item_begin, in_begin;
+    TinyLevelArgs args;
+  };
+  std::vector<TinyLevel> tiny_levels;
+  std::vector<TinyItem> tiny_items;
+  std::vector<i64> tiny_in_off;
+  DevBuf<TinyItem> d_tiny_items;
+  DevBuf<i64> d_tiny_in_off;
   std::vector<GemvDesc> gemv;
   std::vector<GemvLaunch> gemvs;
   std::vector<int> gemv_map, tma_map;
@@ -397,6 +408,7 @@ struct oiobf_tbf {
   std::vector<PairDesc> h_pairs;
   i64 total_core = 0;
   std::map<i64, std::unique_ptr<Plan>> plans;
+  int apply_engine = 0;  // 0 auto, 1 box engine, 2 tiny-box engine
   double t_ms[6] = {0, 0, 0, 0, 0, 0};
   std::mutex mu;
   // host-buffer contraction pipeline: copy-in / copy-out streams and the
@@ -475,6 +487,8 @@ LevelDesc make_level(const oiobf_tbf& b, int sd, int l, i64 r_est, i64 wmax) {
   return L;
 }
 
+void finish_level(oiobf_tbf& b, LevelData& ld, DevBuf<int>& sat, DevBuf<int>& skel_tmp, DevBuf<double2>& interp_tmp);
+
 void build_side_level(oiobf_tbf& b, int sd, int l, i64 r_est) {
   cudaStream_t st = b.stream;
   const int d = b.d;
@@ -485,12 +499,16 @@ void build_side_level(oiobf_tbf& b, int sd, int l, i64 r_est) {
   } else {
     const LevelData& c = b.side[sd][static_cast<size_t>(l - 1)];
     LevelDesc tmp = make_level(b, sd, l, r_est, 1);
-    wmax = 0;
-    for (i64 idx = 0; idx < tmp.nslots; ++idx) {
-      const SlotPos s = decode_slot(tmp, idx);
-      const i64 w = c.h_rank[static_cast<size_t>(child_slot(tmp, s, 0))] +
-                    c.h_rank[static_cast<size_t>(child_slot(tmp, s, 1))];
-      wmax = std::max(wmax, w);
+    if (tmp.nslots > (i64{1} << 22)) {
+      wmax = 2 * static_cast<i64>(c.max_rank);  // bound (exact scan too slow at ~1e8 slots)
+    } else {
+      wmax = 0;
+      for (i64 idx = 0; idx < tmp.nslots; ++idx) {
+        const SlotPos s = decode_slot(tmp, idx);
+        const i64 w = c.h_rank[static_cast<size_t>(child_slot(tmp, s, 0))] +
+                      c.h_rank[static_cast<size_t>(child_slot(tmp, s, 1))];
+        wmax = std::max(wmax, w);
+      }
     }
   }
   wmax = std::max<i64>(wmax, 1);
@@ -502,6 +520,24 @@ void build_side_level(oiobf_tbf& b, int sd, int l, i64 r_est) {
   ld.nslots = L.nslots;
   const i64 ns = L.nslots;
   (void)d;
+  static const bool no_narrow = std::getenv("OIOBF_NO_NARROW") != nullptr;
+  if (b.ks.kind == OIOBF_KERNEL_DFT && wmax <= 2 && !no_narrow) {
+    // closed-form narrow IDs (k_narrow_dft): no proxy / panel / R buffers
+    ld.width.alloc(static_cast<size_t>(ns));
+    ld.rank.alloc(static_cast<size_t>(ns));
+    DevBuf<int> sat(static_cast<size_t>(ns));
+    ld.perm.alloc(static_cast<size_t>(ns * wmax));
+    ld.gaps.alloc(static_cast<size_t>(ns));
+    DevBuf<int> skel_tmp(static_cast<size_t>(ns * wmax));
+    DevBuf<double2> interp_tmp(static_cast<size_t>(ns * wmax * wmax));
+    EventTimer t2(st);
+    const LevelData* c = l > 0 ? &b.side[sd][static_cast<size_t>(l - 1)] : nullptr;
+    launch_narrow_dft(L, b.ks, b.tol, c ? c->rank.p : nullptr, c ? c->skel_off.p : nullptr, c ? c->skel.p : nullptr,
+                      ld.width.p, ld.rank.p, sat.p, ld.perm.p, skel_tmp.p, interp_tmp.p, ld.gaps.p, st);
+    b.t_ms[2] += t2.stop();
+    finish_level(b, ld, sat, skel_tmp, interp_tmp);
+    return;
+  }
   DevBuf<int> proxies(static_cast<size_t>(ns * L.psize));
   DevBuf<int> targets(static_cast<size_t>(ns * wmax));
   ld.width.alloc(static_cast<size_t>(ns));
@@ -528,6 +564,15 @@ void build_side_level(oiobf_tbf& b, int sd, int l, i64 r_est) {
   launch_finish(L, b.tol, kTieEps, -1, rpart.p, targets.p, ld.width.p, ld.rank.p, sat.p, ld.perm.p, skel_tmp.p,
                 interp_tmp.p, ld.gaps.p, st);
   b.t_ms[2] += t2.stop();
+  finish_level(b, ld, sat, skel_tmp, interp_tmp);
+}
+
+// Host-side bookkeeping after a level's IDs: ranks / widths to the host, skeleton
+// and interp offsets, compaction of the per-slot scratch into the level arrays.
+void finish_level(oiobf_tbf& b, LevelData& ld, DevBuf<int>& sat, DevBuf<int>& skel_tmp, DevBuf<double2>& interp_tmp) {
+  cudaStream_t st = b.stream;
+  const i64 ns = ld.nslots;
+  const i64 wmax = ld.L.wmax;
   ld.h_rank.resize(static_cast<size_t>(ns));
   ld.h_width.resize(static_cast<size_t>(ns));
   ld.h_sat.resize(static_cast<size_t>(ns));
@@ -1220,14 +1265,212 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked) {
   return pl;
 }
 
+// ---- tiny-box engine plan (config 4 scale: ~1e8 boxes of <= kTinyBox elements)
+// Largest box (input and output elements) of every level, both sides, and the
+// widest core row: the tiny engine costs O(box) per output element.
+bool tiny_eligible(const oiobf_tbf& b) {
+  if (b.world > 1 || b.d < 1) return false;
+  const int d = b.d;
+  for (int sd = 0; sd < 2; ++sd)
+    for (int l = 0; l <= b.Lc; ++l) {
+      const LevelData& ld = b.side[sd][static_cast<size_t>(l)];
+      const i64 nj = ld.L.nj;
+      const i64 ngroups = ld.nslots / (d * nj);
+      for (i64 g = 0; g < ngroups; ++g) {
+        i64 bin = 1, bout = 1;
+        for (int k = 0; k < d; ++k) {
+          int mr = 0, mw = 0;
+          for (i64 j = 0; j < nj; ++j) {
+            const size_t sl = static_cast<size_t>((g * d + k) * nj + j);
+            mr = std::max(mr, ld.h_rank[sl]);
+            mw = std::max(mw, ld.h_width[sl]);
+          }
+          bin *= sd == 0 ? mw : mr;
+          bout *= sd == 0 ? mr : mw;
+        }
+        if (bin > kTinyBox || bout > kTinyBox) return false;
+      }
+    }
+  for (const PairDesc& pd : b.h_pairs)
+    if (pd.C > kTinyBox) return false;
+  return true;
+}
+
+// auto: the tiny engine when every box is tiny AND there are so many pairs that
+// per-box descriptors / CTAs would dominate (>= 2^20 middle pairs)
+bool use_tiny_engine(oiobf_tbf& b) {
+  if (b.apply_engine == 1) return false;
+  if (b.apply_engine == 2) return true;
+  if (b.nmid * b.nmid < (i64{1} << 20)) return false;
+  return tiny_eligible(b);
+}
+
+std::unique_ptr<Plan> build_plan_tiny(oiobf_tbf& b, i64 nv) {
+  require(b.world == 1, "tiny-box engine: sharded factorizations use the box engine");
+  auto pl = std::make_unique<Plan>();
+  pl->nv = nv;
+  const int d = b.d;
+  const i64 n = b.n, N = ipow(n, d);
+  const i64 mid = n >> b.Lc, mpm = ipow(2, b.Lc);
+  i64 scratch = 0;
+  auto slab_off = [&](i64 outer) {
+    i64 off = 0, st = 1;
+    for (int p = 0; p < d; ++p) {
+      off += ((outer / ipow(mpm, p)) % mpm) * mid * st;
+      st *= n;
+    }
+    return off;
+  };
+  auto parent_of = [&](i64 inner, int l) {
+    i64 pi = 0;
+    for (int p = d - 1; p >= 0; --p) pi = (pi << (l - 1)) | (((inner >> (l * p)) & ((i64{1} << l) - 1)) >> 1);
+    return pi;
+  };
+  TinyLevelArgs base{};
+  base.d = d;
+  {
+    i64 st = 1;
+    for (int p = 0; p < d; ++p) {
+      base.gstride[p] = st;
+      st *= n;
+    }
+    base.gstride[d] = N;
+  }
+  auto add_level = [&](int sd, int l, i64 nin, i64 nj, int in_buf, int out_buf, int in_global, int out_global,
+                       i64 item_begin, i64 in_begin, i64 total) {
+    Plan::TinyLevel tl;
+    tl.side = sd;
+    tl.l = l;
+    tl.in_buf = in_buf;
+    tl.out_buf = out_buf;
+    tl.item_begin = item_begin;
+    tl.in_begin = in_begin;
+    tl.args = base;
+    tl.args.side = sd;
+    tl.args.l = l;
+    tl.args.in_global = in_global;
+    tl.args.out_global = out_global;
+    tl.args.nin = nin;
+    tl.args.nj = nj;
+    tl.args.nitems = static_cast<i64>(pl->tiny_items.size()) - item_begin;
+    tl.args.total_out = total;
+    pl->ops.push_back(Op{6, static_cast<i64>(pl->tiny_levels.size()), sd == 0 ? 0 : 2});
+    pl->tiny_levels.push_back(tl);
+  };
+  // ---- V / W: items (s, tau); output extents sum_j r per mode
+  std::vector<i64> prev;  // output offset per (s, tau) of the previous level
+  for (int l = 0; l <= b.Lc; ++l) {
+    const LevelData& ld = b.side[0][static_cast<size_t>(l)];
+    const i64 nin = ld.L.nin, nj = ld.L.nj;
+    const i64 item_begin = static_cast<i64>(pl->tiny_items.size());
+    const i64 in_begin = static_cast<i64>(pl->tiny_in_off.size());
+    std::vector<i64> cur(static_cast<size_t>(b.nmid * nin));
+    i64 total = 0;
+    for (i64 s = 0; s < b.nmid; ++s)
+      for (i64 tau = 0; tau < nin; ++tau) {
+        i64 size = nv;
+        for (int k = 0; k < d; ++k) {
+          i64 e = 0;
+          for (i64 j = 0; j < nj; ++j) e += ld.h_rank[static_cast<size_t>(((s * nin + tau) * d + k) * nj + j)];
+          size *= e;
+        }
+        TinyItem it{scratch, total, s, tau, 0};
+        pl->tiny_items.push_back(it);
+        cur[static_cast<size_t>(s * nin + tau)] = scratch;
+        pl->tiny_in_off.push_back(l == 0 ? slab_off(s)
+                                         : prev[static_cast<size_t>(s * ipow(2, static_cast<i64>(d) * (l - 1)) +
+                                                                    parent_of(tau, l))]);
+        scratch += size;
+        total += size;
+      }
+    add_level(0, l, nin, nj, l == 0 ? BUF_F : BUF_SCRATCH, BUF_SCRATCH, l == 0 ? 1 : 0, 0, item_begin, in_begin,
+              total);
+    prev.swap(cur);
+  }
+  // ---- cores: G_{t,s} = K(tbar, sbar) F_{t,s}, F_{t,s} = W output (s, tau = t)
+  std::vector<i64> gts(static_cast<size_t>(b.nmid * b.nmid));
+  {
+    i64 rows = 0;
+    for (i64 p = 0; p < b.nmid * b.nmid; ++p) {
+      const i64 s = p / b.nmid, t = p % b.nmid;
+      const PairDesc& pd = b.h_pairs[static_cast<size_t>(p)];
+      GemvDesc g;
+      g.core_off = pd.core_off;
+      g.x_off = prev[static_cast<size_t>(s * b.nmid + t)];
+      g.y_off = scratch;
+      g.R = pd.R;
+      g.C = pd.C;
+      g.cta_off = rows;
+      rows += pd.R;
+      gts[static_cast<size_t>(t * b.nmid + s)] = scratch;
+      scratch += static_cast<i64>(pd.R) * nv;
+      pl->gemv.push_back(g);
+    }
+    GemvLaunch gl;
+    gl.desc_begin = 0;
+    gl.ndesc = static_cast<i64>(pl->gemv.size());
+    gl.total_rows = rows;
+    pl->gemvs.push_back(gl);
+    pl->ops.push_back(Op{7, 0, 1});
+  }
+  // ---- P / U: items are parents (t, p_nu); output extents sum_j w per mode;
+  // children nu summed in ascending order inside the kernel
+  std::vector<i64> pin = gts;  // input offset per (t, nu) of the current level
+  for (int l = b.Lc; l >= 0; --l) {
+    const LevelData& ld = b.side[1][static_cast<size_t>(l)];
+    const i64 nin = ld.L.nin, nj = ld.L.nj;
+    const i64 pnin = l > 0 ? ipow(2, static_cast<i64>(d) * (l - 1)) : 1;
+    const i64 item_begin = static_cast<i64>(pl->tiny_items.size());
+    const i64 in_begin = static_cast<i64>(pl->tiny_in_off.size());
+    pl->tiny_in_off.insert(pl->tiny_in_off.end(), pin.begin(), pin.end());
+    std::vector<i64> out(static_cast<size_t>(b.nmid * pnin));
+    i64 total = 0;
+    for (i64 t = 0; t < b.nmid; ++t)
+      for (i64 pnu = 0; pnu < pnin; ++pnu) {
+        i64 first = 0;
+        if (l > 0) {  // smallest child: every mode coordinate 2 * pc_p
+          for (int p = d - 1; p >= 0; --p) {
+            const i64 pc = (pnu >> ((l - 1) * p)) & ((i64{1} << (l - 1)) - 1);
+            first = (first << l) | (2 * pc);
+          }
+        }
+        i64 size = nv;
+        for (int k = 0; k < d; ++k) {
+          i64 e = 0;
+          for (i64 j = 0; j < nj; ++j) e += ld.h_width[static_cast<size_t>(((t * nin + first) * d + k) * nj + j)];
+          size *= e;
+        }
+        const i64 off = l == 0 ? slab_off(t) : scratch;
+        TinyItem it{off, total, t, pnu, first};
+        pl->tiny_items.push_back(it);
+        out[static_cast<size_t>(t * pnin + pnu)] = off;
+        if (l > 0) scratch += size;
+        total += size;
+      }
+    add_level(1, l, nin, nj, l == b.Lc ? BUF_SCRATCH : BUF_SCRATCH, l == 0 ? BUF_G : BUF_SCRATCH, 0, l == 0 ? 1 : 0,
+              item_begin, in_begin, total);
+    pin.swap(out);
+  }
+  pl->scratch_elems = scratch;
+  cudaStream_t st = b.stream;
+  pl->d_gemv = to_device(pl->gemv, st);
+  pl->d_tiny_items = to_device(pl->tiny_items, st);
+  pl->d_tiny_in_off = to_device(pl->tiny_in_off, st);
+  pl->scratch.alloc(static_cast<size_t>(std::max<i64>(scratch, 1)));
+  TBF_CUDA(cudaStreamSynchronize(st));
+  return pl;
+}
+
 // chunked = true: the host-pipelined plan (ops per slab group, see
 // contract_host); the device-buffer path uses the unchunked plan
 Plan& get_plan(oiobf_tbf& b, i64 nv, bool chunked = false) {
+  const bool tiny = use_tiny_engine(b);
+  if (tiny) chunked = false;  // one slab group: the tiny plan is not split
   const i64 key = 2 * nv + (chunked ? 1 : 0);
   auto it = b.plans.find(key);
   if (it != b.plans.end()) return *it->second;
   auto& slot = b.plans[key];
-  slot = build_plan(b, nv, chunked);
+  slot = tiny ? build_plan_tiny(b, nv) : build_plan(b, nv, chunked);
   return *slot;
 }
 
@@ -1271,6 +1514,15 @@ void run_ops(oiobf_tbf& b, Plan& pl, const OpBuffers& io, cudaStream_t st, int g
       else
         launch_gemv(pl.d_gemv_map.p + gl.map_begin, gd, gl.ctas, gl.total_rows, pl.d_gemv_rb.p + gl.rb_begin,
                     static_cast<int>(pl.nv), b.cores.p, pl.scratch.p, y, gl.max_c, st);
+    } else if (op.kind == 6) {
+      const Plan::TinyLevel& tl = pl.tiny_levels[static_cast<size_t>(op.idx)];
+      const LevelData& ld = b.side[tl.side][static_cast<size_t>(tl.l)];
+      launch_tiny_level(tl.args, pl.d_tiny_items.p + tl.item_begin, pl.d_tiny_in_off.p + tl.in_begin, ld.rank.p,
+                        ld.width.p, ld.interp_off.p, ld.interp.p, in_ptr(tl.in_buf), out_ptr(tl.out_buf), st);
+    } else if (op.kind == 7) {
+      const GemvLaunch& gl = pl.gemvs[static_cast<size_t>(op.idx)];
+      launch_tiny_gemv(pl.d_gemv.p + gl.desc_begin, gl.ndesc, gl.total_rows, static_cast<int>(pl.nv), b.cores.p,
+                       pl.scratch.p, pl.scratch.p, st);
     } else if (op.kind == 3) {
       const BoxLaunch& bx = pl.boxes[static_cast<size_t>(op.idx)];
       const LevelData& ld = b.side[bx.side][static_cast<size_t>(bx.level)];
@@ -1639,6 +1891,27 @@ int oiobf_tbf_contract(oiobf_tbf* h, const double* F, double* G, int64_t nv) {
   require(h->world == 1, "tbf_contract: sharded factorization -- use oiobf_tbf_contract_phase");
   std::lock_guard<std::mutex> lk(h->mu);
   contract_host(*h, F, G, nv);
+  CAPI_END
+}
+
+int oiobf_tbf_set_apply_engine(oiobf_tbf* h, int32_t engine) {
+  CAPI_BEGIN
+  require(h, "tbf_set_apply_engine: null handle");
+  require(engine >= 0 && engine <= 2, "tbf_set_apply_engine: engine must be 0 (auto), 1 (box) or 2 (tiny)");
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (h->apply_engine != engine) {
+    TBF_CUDA(cudaStreamSynchronize(h->stream));
+    h->plans.clear();
+    h->apply_engine = engine;
+  }
+  CAPI_END
+}
+
+int oiobf_tbf_apply_engine(oiobf_tbf* h, int32_t* engine) {
+  CAPI_BEGIN
+  require(h && engine, "tbf_apply_engine: null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  *engine = use_tiny_engine(*h) ? 2 : 1;
   CAPI_END
 }
 

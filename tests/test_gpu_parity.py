@@ -213,6 +213,36 @@ def test_host_pipeline_paths_agree(name, spec, tol, L):
         np.testing.assert_array_equal(pg, first)  # pageable: same plan, no graph
 
 
+@pytest.mark.parametrize("name,spec,tol,L", CASES, ids=[c[0] for c in CASES])
+def test_tiny_engine_matches_box_engine_and_oracle(oracle, name, spec, tol, L):
+    """The tiny-box apply engine (thread per output, d = 6 scale) on every
+    parity case: same G as the fused-box engine to rounding, and within 1e-10
+    of the oracle applying the same factors; nv = 1 and 2."""
+    bf = tb.tbf_construct(spec, L, tol, seed=3)
+    tbo = oracle.tbf_construct(spec, L, tol, seed=3, replay=bf.export())
+    rng = np.random.default_rng(9)
+    for nv in (1, 2):
+        shape = (spec.n,) * spec.d + ((nv,) if nv > 1 else ())
+        F = rand_c(rng, shape)
+        bf.set_apply_engine("box")
+        assert bf.apply_engine() == "box"
+        gb = bf.contract(F)
+        bf.set_apply_engine("tiny")
+        assert bf.apply_engine() == "tiny"
+        gt = bf.contract(F)
+        assert rel(gt, gb) < 1e-13, f"tiny vs box {rel(gt, gb)}"
+        assert rel(gt, tbo.contract(F)) < 1e-10
+    bf.set_apply_engine("auto")
+
+
+def test_dft_uses_narrow_ids():
+    """DFT levels with <= 2 candidate columns take the closed-form narrow-ID
+    kernel (no panel / TSQR work is timed)."""
+    bf = tb.tbf_construct(dft(2, 16), 4, 1e-8, seed=3)
+    t = bf.timings()
+    assert t["panel_ms"] == 0.0 and t["proxies_targets_ms"] == 0.0, t
+
+
 def test_error_estimate_monotone():
     spec = green_plates(32)
     e2 = tb.tbf_error_estimate(tb.tbf_construct(spec, 2, 1e-2, seed=1), n_samples=5, seed=2)

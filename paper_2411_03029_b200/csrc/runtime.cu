@@ -409,6 +409,7 @@ struct oiobf_tbf {
   i64 total_core = 0;
   std::map<i64, std::unique_ptr<Plan>> plans;
   int apply_engine = 0;  // 0 auto, 1 box engine, 2 tiny-box engine
+  int tiny_auto = -1;    // cached auto decision (-1: not evaluated yet)
   double t_ms[6] = {0, 0, 0, 0, 0, 0};
   std::mutex mu;
   // host-buffer contraction pipeline: copy-in / copy-out streams and the
@@ -1301,8 +1302,9 @@ bool tiny_eligible(const oiobf_tbf& b) {
 bool use_tiny_engine(oiobf_tbf& b) {
   if (b.apply_engine == 1) return false;
   if (b.apply_engine == 2) return true;
-  if (b.nmid * b.nmid < (i64{1} << 20)) return false;
-  return tiny_eligible(b);
+  if (b.tiny_auto < 0)  // the eligibility scan walks every slot: once per handle
+    b.tiny_auto = (b.nmid * b.nmid >= (i64{1} << 20) && tiny_eligible(b)) ? 1 : 0;
+  return b.tiny_auto == 1;
 }
 
 std::unique_ptr<Plan> build_plan_tiny(oiobf_tbf& b, i64 nv) {

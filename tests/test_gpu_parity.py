@@ -10,7 +10,7 @@ import pytest
 import paper_2411_03029_b200 as tb
 from paper_2411_03029_b200.configs import BY_NAME, dft, green_cubes, green_plates, radon2d
 
-from helpers import TIE_EPS, compare_factorizations, rel, slot_geometry, slot_target
+from helpers import TIE_EPS, compare_factorizations, level_base, rel, slot_geometry, slot_target
 
 pytestmark = pytest.mark.gpu
 
@@ -288,6 +288,49 @@ def test_full_config_sampled_slots(oracle, cfg):
             np.testing.assert_array_equal(target[o["skeleton"] - 1], fz.skel[so[g]:so[g + 1]])
             gi = fz.interp[io[g]:io[g + 1]].reshape((fz.ranks[g], fz.ncols[g]), order="F")
             assert np.max(np.abs(gi - o["interp"])) <= 1e-8 * max(1, np.max(np.abs(o["interp"])))
+
+
+def test_config4_full_size(oracle):
+    """Config 4 (d = 6 DFT, n = 16, C_b = 1 -> L = 4; 2.08e8 IDs, 1.7e7 middle
+    pairs) at full size: sampled slots of every level recomputed by the oracle
+    from the same proxies and candidates (ranks / skeletons exact, interps to
+    1e-8), the tiny-box engine selected automatically, and 1000 sampled outputs
+    within tol of direct dense sums (GPU dense rows cross-checked against the
+    oracle's on 8 rows)."""
+    c = BY_NAME["dft6_n16"]
+    spec = c.spec
+    bf = tb.tbf_construct(spec, c.L, c.tol, seed=c.seed)
+    assert bf.apply_engine() == "tiny"
+    fz = bf.export()
+    assert len(fz.ranks) == 207814656
+    so, io, po, _ = fz.offsets()
+    rng = np.random.default_rng(7)
+    for sd, l, cnt in fz.level_counts():
+        base = level_base(fz, sd, l)
+        r_est = int(fz.r_est[sd * (fz.Lc + 1) + l])
+        for idx in rng.choice(cnt, size=3, replace=False):
+            g = base + int(idx)
+            geo = slot_geometry(fz.d, fz.n, fz.L, fz.Lc, sd, l, int(idx))
+            target = slot_target(fz, sd, l, int(idx))
+            lists = oracle.proxy_lists(geo["ranges"], geo["skip"], 3 * r_est,
+                                       seed=oracle.derive_seed(c.seed, geo["tags"]))
+            lists[geo["skip"]] = target
+            A = oracle.unfolding(spec, lists, geo["skip"])
+            assert A.shape[0] == fz.rows[g]
+            o = oracle.column_id(A, c.tol, forced_perm=fz.perm[po[g]:po[g + 1]], forced_rank=int(fz.ranks[g]))
+            assert not o["mismatch"]
+            assert o["rank"] == fz.ranks[g] == 1
+            np.testing.assert_array_equal(target[o["skeleton"] - 1], fz.skel[so[g]:so[g + 1]])
+            gi = fz.interp[io[g]:io[g + 1]].reshape((fz.ranks[g], fz.ncols[g]), order="F")
+            assert np.max(np.abs(gi - o["interp"])) <= 1e-8
+    del fz
+    F = rand_c(rng, (spec.n,) * spec.d)
+    G = bf.contract(F).reshape(-1, order="F")
+    rows = rng.choice(spec.n ** spec.d, 1000, replace=False)
+    exact = tb.dense_rows(spec, F, rows)[:, 0]
+    assert rel(exact[:8], oracle.dense_rows(spec, F, rows[:8])[:, 0]) < 1e-13
+    err = rel(G[rows], exact)
+    assert err <= c.tol, f"sampled relative error {err:.3e} > tol"
 
 
 @pytest.mark.parametrize("cfg,gate", [("green_plates_n64", 10), ("green_cubes_n64", 30)])

@@ -120,20 +120,30 @@ void box_trace_enable(unsigned long long* buf);  // debug: 8 globaltimer stamps 
 // programmatic dependent launch for the apply kernels (env OIOBF_NO_PDL=1 disables)
 bool pdl_enabled();
 
-// ---- tiny-box apply engine (tiny_kernels.cu): thread per output element,
-// block geometry read from the level's slot arrays (no per-box descriptors)
+// ---- tiny-box apply engine (tiny_kernels.cu): one CTA per group of boxes that
+// share data (V/W: the 2^d children tau of a parent, which all read the
+// parent's output; P/U: the 2^d children nu summed into one parent), block
+// geometry read from the level's slot arrays (no per-box descriptors)
 constexpr int kTinyBox = 64;  // largest box (elements) the engine is chosen for
-struct TinyItem {             // one output tensor of a level
-  i64 out_off, out_start;     // element offset; prefix of output elements (thread map)
-  i64 outer, inner;           // V/W: (s, tau); P/U: (t, parent p_nu)
-  i64 first_child;            // P/U: smallest child nu of p_nu (its widths give the output extents)
+struct TinyGroup {
+  i64 outer, pinner;  // V/W: (s, parent tau) [l = 0: (s, 0)];  P/U: (t, p_nu)
+  i64 io_off;         // V/W: offset of the shared input tensor;  P/U: offset of the parent output
 };
 struct TinyLevelArgs {
-  int side, l, d, in_global, out_global, pad;
-  i64 nin, nj, nitems, total_out;
+  int side, l, d, nv, in_global, out_global;
+  int nch;          // children per group (2^d, or 1 at l = 0)
+  int threads;      // CTA size: the group's output count rounded up to a power of two, in [32, 256]
+  i64 nin, nj, ngroups;
+  i64 max_in;       // elements of staged input per group (shared memory)
+  i64 fstride;      // factor elements per (child, mode) slot group; 0: factors read from global memory
+  i64 xstride;      // P/U: staged input elements per child
+  i64 ostride;      // V/W: output elements per child (thread map)
+  i64 maxo;         // largest output extent of one mode (table size)
   i64 gstride[kMaxD + 1];  // strides of the global n^d x nv tensor (V0 input / U0 output)
 };
-void launch_tiny_level(const TinyLevelArgs& a, const TinyItem* items, const i64* in_off_of, const int* rank,
+size_t tiny_smem_bytes(const TinyLevelArgs& a);
+// off_of[outer * nin + inner]: V/W child output offsets; P/U child input offsets
+void launch_tiny_level(const TinyLevelArgs& a, const TinyGroup* groups, const i64* off_of, const int* rank,
                        const int* width, const i64* moff, const double2* mats, const double2* in, double2* out,
                        cudaStream_t st);
 void launch_tiny_gemv(const GemvDesc* d, i64 npairs, i64 total_rows, int nv, const double2* cores, const double2* x,

@@ -220,14 +220,14 @@ struct Plan {
   // tiny-box engine (tiny_kernels.cu): one launch per level + a row GEMV
   struct TinyLevel {
     int side, l, in_buf, out_buf;
-    i64 item_begin, in_begin;
+    i64 group_begin, off_begin;
     TinyLevelArgs args;
   };
   std::vector<TinyLevel> tiny_levels;
-  std::vector<TinyItem> tiny_items;
-  std::vector<i64> tiny_in_off;
-  DevBuf<TinyItem> d_tiny_items;
-  DevBuf<i64> d_tiny_in_off;
+  std::vector<TinyGroup> tiny_groups;
+  std::vector<i64> tiny_off;  // per level: child output (V/W) / input (P/U) offsets by (outer, inner)
+  DevBuf<TinyGroup> d_tiny_groups;
+  DevBuf<i64> d_tiny_off;
   std::vector<GemvDesc> gemv;
   std::vector<GemvLaunch> gemvs;
   std::vector<int> gemv_map, tma_map;
@@ -1323,71 +1323,134 @@ std::unique_ptr<Plan> build_plan_tiny(oiobf_tbf& b, i64 nv) {
     }
     return off;
   };
-  auto parent_of = [&](i64 inner, int l) {
-    i64 pi = 0;
-    for (int p = d - 1; p >= 0; --p) pi = (pi << (l - 1)) | (((inner >> (l * p)) & ((i64{1} << l) - 1)) >> 1);
-    return pi;
-  };
-  TinyLevelArgs base{};
-  base.d = d;
-  {
-    i64 st = 1;
-    for (int p = 0; p < d; ++p) {
-      base.gstride[p] = st;
-      st *= n;
+  auto child_inner = [&](i64 pinner, int l, int c) {
+    i64 inner = 0;
+    for (int p = d - 1; p >= 0; --p) {
+      const i64 pc = (pinner >> ((l - 1) * p)) & ((i64{1} << (l - 1)) - 1);
+      inner = (inner << l) | (2 * pc + ((c >> p) & 1));
     }
-    base.gstride[d] = N;
-  }
-  auto add_level = [&](int sd, int l, i64 nin, i64 nj, int in_buf, int out_buf, int in_global, int out_global,
-                       i64 item_begin, i64 in_begin, i64 total) {
+    return inner;
+  };
+  // sum over blocks j of the rank (what = 0) or width (what = 1) of slot group (outer, inner, k)
+  auto ext_of = [&](const LevelData& ld, i64 outer, i64 inner, int k, int what) {
+    const i64 nin = ld.L.nin, nj = ld.L.nj;
+    i64 e = 0;
+    for (i64 j = 0; j < nj; ++j) {
+      const size_t sl = static_cast<size_t>(((outer * nin + inner) * d + k) * nj + j);
+      e += what == 0 ? ld.h_rank[sl] : ld.h_width[sl];
+    }
+    return e;
+  };
+  // largest factor block set of one (outer, inner, k): sum over j of r * w
+  auto fac_of = [&](const LevelData& ld, i64 outer, i64 inner) {
+    const i64 nin = ld.L.nin, nj = ld.L.nj;
+    i64 m = 0;
+    for (int k = 0; k < d; ++k) {
+      i64 e = 0;
+      for (i64 j = 0; j < nj; ++j) {
+        const size_t sl = static_cast<size_t>(((outer * nin + inner) * d + k) * nj + j);
+        e += static_cast<i64>(ld.h_rank[sl]) * ld.h_width[sl];
+      }
+      m = std::max(m, e);
+    }
+    return m;
+  };
+  i64 fstride = 0, xstride = 0, ostride = 0, maxo = 1;  // of the level being planned
+  auto add_level = [&](int sd, int l, const LevelData& ld, int nch, int in_buf, int out_buf, int in_global,
+                       int out_global, i64 group_begin, i64 off_begin, i64 max_in) {
     Plan::TinyLevel tl;
     tl.side = sd;
     tl.l = l;
     tl.in_buf = in_buf;
     tl.out_buf = out_buf;
-    tl.item_begin = item_begin;
-    tl.in_begin = in_begin;
-    tl.args = base;
-    tl.args.side = sd;
-    tl.args.l = l;
-    tl.args.in_global = in_global;
-    tl.args.out_global = out_global;
-    tl.args.nin = nin;
-    tl.args.nj = nj;
-    tl.args.nitems = static_cast<i64>(pl->tiny_items.size()) - item_begin;
-    tl.args.total_out = total;
+    tl.group_begin = group_begin;
+    tl.off_begin = off_begin;
+    TinyLevelArgs& a = tl.args;
+    a = TinyLevelArgs{};
+    a.side = sd;
+    a.l = l;
+    a.d = d;
+    a.nv = static_cast<int>(nv);
+    a.in_global = in_global;
+    a.out_global = out_global;
+    a.nch = nch;
+    a.nin = ld.L.nin;
+    a.nj = ld.L.nj;
+    a.ngroups = static_cast<i64>(pl->tiny_groups.size()) - group_begin;
+    a.max_in = max_in;
+    a.fstride = fstride;
+    a.xstride = xstride;
+    a.ostride = ostride;
+    a.maxo = maxo;
+    if (tiny_smem_bytes(a) > static_cast<size_t>(kMaxDynSmem)) a.fstride = 0;  // factors from global memory
+    // CTA size from the group's output count (small groups: small CTAs, more resident)
+    {
+      const i64 outs = sd == 0 ? nch * ostride : 0;
+      i64 mx = outs;
+      if (sd == 1) {  // parent output size
+        for (i64 gi = group_begin; gi < static_cast<i64>(pl->tiny_groups.size()); ++gi) {
+          const TinyGroup& tg = pl->tiny_groups[static_cast<size_t>(gi)];
+          i64 size = nv;
+          const i64 first = l > 0 ? child_inner(tg.pinner, l, 0) : 0;
+          for (int k = 0; k < d; ++k) size *= ext_of(ld, tg.outer, first, k, 1);
+          mx = std::max(mx, size);
+          if (gi - group_begin > 4096) break;  // a sample: the CTA size only affects speed
+        }
+      }
+      int th = 32;
+      while (th < 256 && th < mx) th *= 2;
+      a.threads = th;
+    }
+    {
+      i64 st = 1;
+      for (int p = 0; p < d; ++p) {
+        a.gstride[p] = st;
+        st *= n;
+      }
+      a.gstride[d] = N;
+    }
+    require(tiny_smem_bytes(a) <= static_cast<size_t>(kMaxDynSmem), "tiny engine: a box group does not fit on chip");
     pl->ops.push_back(Op{6, static_cast<i64>(pl->tiny_levels.size()), sd == 0 ? 0 : 2});
     pl->tiny_levels.push_back(tl);
   };
-  // ---- V / W: items (s, tau); output extents sum_j r per mode
+  // ---- V / W: group = parent (s, p_tau); its 2^d children tau read the parent output
   std::vector<i64> prev;  // output offset per (s, tau) of the previous level
   for (int l = 0; l <= b.Lc; ++l) {
     const LevelData& ld = b.side[0][static_cast<size_t>(l)];
-    const i64 nin = ld.L.nin, nj = ld.L.nj;
-    const i64 item_begin = static_cast<i64>(pl->tiny_items.size());
-    const i64 in_begin = static_cast<i64>(pl->tiny_in_off.size());
-    std::vector<i64> cur(static_cast<size_t>(b.nmid * nin));
-    i64 total = 0;
+    const i64 nin = ld.L.nin;
+    const i64 pnin = l > 0 ? ipow(2, static_cast<i64>(d) * (l - 1)) : 1;
+    const int nch = l > 0 ? (1 << d) : 1;
+    const i64 group_begin = static_cast<i64>(pl->tiny_groups.size());
+    const i64 off_begin = static_cast<i64>(pl->tiny_off.size());
+    pl->tiny_off.resize(static_cast<size_t>(off_begin + b.nmid * nin));
+    i64 max_in = 1;
+    fstride = 0;
+    ostride = 1;
+    maxo = 1;
     for (i64 s = 0; s < b.nmid; ++s)
-      for (i64 tau = 0; tau < nin; ++tau) {
-        i64 size = nv;
-        for (int k = 0; k < d; ++k) {
-          i64 e = 0;
-          for (i64 j = 0; j < nj; ++j) e += ld.h_rank[static_cast<size_t>(((s * nin + tau) * d + k) * nj + j)];
-          size *= e;
+      for (i64 ptau = 0; ptau < pnin; ++ptau) {
+        const i64 first = l > 0 ? child_inner(ptau, l, 0) : 0;
+        i64 in_sz = nv;
+        for (int k = 0; k < d; ++k) in_sz *= ext_of(ld, s, first, k, 1);
+        max_in = std::max(max_in, in_sz);
+        pl->tiny_groups.push_back(TinyGroup{s, ptau, l == 0 ? slab_off(s) : prev[static_cast<size_t>(s * pnin + ptau)]});
+        for (int c = 0; c < nch; ++c) {
+          const i64 tau = l > 0 ? child_inner(ptau, l, c) : 0;
+          fstride = std::max(fstride, fac_of(ld, s, tau));
+          i64 size = nv;
+          for (int k = 0; k < d; ++k) {
+            const i64 e = ext_of(ld, s, tau, k, 0);
+            maxo = std::max(maxo, e);
+            size *= e;
+          }
+          ostride = std::max(ostride, size);
+          pl->tiny_off[static_cast<size_t>(off_begin + s * nin + tau)] = scratch;
+          scratch += size;
         }
-        TinyItem it{scratch, total, s, tau, 0};
-        pl->tiny_items.push_back(it);
-        cur[static_cast<size_t>(s * nin + tau)] = scratch;
-        pl->tiny_in_off.push_back(l == 0 ? slab_off(s)
-                                         : prev[static_cast<size_t>(s * ipow(2, static_cast<i64>(d) * (l - 1)) +
-                                                                    parent_of(tau, l))]);
-        scratch += size;
-        total += size;
       }
-    add_level(0, l, nin, nj, l == 0 ? BUF_F : BUF_SCRATCH, BUF_SCRATCH, l == 0 ? 1 : 0, 0, item_begin, in_begin,
-              total);
-    prev.swap(cur);
+    add_level(0, l, ld, nch, l == 0 ? BUF_F : BUF_SCRATCH, BUF_SCRATCH, l == 0 ? 1 : 0, 0, group_begin, off_begin,
+              max_in);
+    prev.assign(pl->tiny_off.begin() + off_begin, pl->tiny_off.end());
   }
   // ---- cores: G_{t,s} = K(tbar, sbar) F_{t,s}, F_{t,s} = W output (s, tau = t)
   std::vector<i64> gts(static_cast<size_t>(b.nmid * b.nmid));
@@ -1415,49 +1478,50 @@ std::unique_ptr<Plan> build_plan_tiny(oiobf_tbf& b, i64 nv) {
     pl->gemvs.push_back(gl);
     pl->ops.push_back(Op{7, 0, 1});
   }
-  // ---- P / U: items are parents (t, p_nu); output extents sum_j w per mode;
-  // children nu summed in ascending order inside the kernel
+  // ---- P / U: group = parent (t, p_nu); its 2^d children nu (ascending) add into it
   std::vector<i64> pin = gts;  // input offset per (t, nu) of the current level
   for (int l = b.Lc; l >= 0; --l) {
     const LevelData& ld = b.side[1][static_cast<size_t>(l)];
-    const i64 nin = ld.L.nin, nj = ld.L.nj;
+    const i64 nin = ld.L.nin;
     const i64 pnin = l > 0 ? ipow(2, static_cast<i64>(d) * (l - 1)) : 1;
-    const i64 item_begin = static_cast<i64>(pl->tiny_items.size());
-    const i64 in_begin = static_cast<i64>(pl->tiny_in_off.size());
-    pl->tiny_in_off.insert(pl->tiny_in_off.end(), pin.begin(), pin.end());
+    const int nch = l > 0 ? (1 << d) : 1;
+    const i64 group_begin = static_cast<i64>(pl->tiny_groups.size());
+    const i64 off_begin = static_cast<i64>(pl->tiny_off.size());
+    pl->tiny_off.insert(pl->tiny_off.end(), pin.begin(), pin.end());
     std::vector<i64> out(static_cast<size_t>(b.nmid * pnin));
-    i64 total = 0;
+    fstride = 0;
+    xstride = 1;
+    maxo = 1;
     for (i64 t = 0; t < b.nmid; ++t)
       for (i64 pnu = 0; pnu < pnin; ++pnu) {
-        i64 first = 0;
-        if (l > 0) {  // smallest child: every mode coordinate 2 * pc_p
-          for (int p = d - 1; p >= 0; --p) {
-            const i64 pc = (pnu >> ((l - 1) * p)) & ((i64{1} << (l - 1)) - 1);
-            first = (first << l) | (2 * pc);
-          }
+        const i64 first = l > 0 ? child_inner(pnu, l, 0) : 0;
+        for (int c = 0; c < nch; ++c) {
+          const i64 nu = l > 0 ? child_inner(pnu, l, c) : 0;
+          i64 cs = nv;
+          for (int k = 0; k < d; ++k) cs *= ext_of(ld, t, nu, k, 0);
+          xstride = std::max(xstride, cs);
+          fstride = std::max(fstride, fac_of(ld, t, nu));
         }
         i64 size = nv;
         for (int k = 0; k < d; ++k) {
-          i64 e = 0;
-          for (i64 j = 0; j < nj; ++j) e += ld.h_width[static_cast<size_t>(((t * nin + first) * d + k) * nj + j)];
+          const i64 e = ext_of(ld, t, first, k, 1);
+          maxo = std::max(maxo, e);
           size *= e;
         }
         const i64 off = l == 0 ? slab_off(t) : scratch;
-        TinyItem it{off, total, t, pnu, first};
-        pl->tiny_items.push_back(it);
+        pl->tiny_groups.push_back(TinyGroup{t, pnu, off});
         out[static_cast<size_t>(t * pnin + pnu)] = off;
         if (l > 0) scratch += size;
-        total += size;
       }
-    add_level(1, l, nin, nj, l == b.Lc ? BUF_SCRATCH : BUF_SCRATCH, l == 0 ? BUF_G : BUF_SCRATCH, 0, l == 0 ? 1 : 0,
-              item_begin, in_begin, total);
+    add_level(1, l, ld, nch, BUF_SCRATCH, l == 0 ? BUF_G : BUF_SCRATCH, 0, l == 0 ? 1 : 0, group_begin, off_begin,
+              nch * xstride);
     pin.swap(out);
   }
   pl->scratch_elems = scratch;
   cudaStream_t st = b.stream;
   pl->d_gemv = to_device(pl->gemv, st);
-  pl->d_tiny_items = to_device(pl->tiny_items, st);
-  pl->d_tiny_in_off = to_device(pl->tiny_in_off, st);
+  pl->d_tiny_groups = to_device(pl->tiny_groups, st);
+  pl->d_tiny_off = to_device(pl->tiny_off, st);
   pl->scratch.alloc(static_cast<size_t>(std::max<i64>(scratch, 1)));
   TBF_CUDA(cudaStreamSynchronize(st));
   return pl;
@@ -1519,7 +1583,7 @@ void run_ops(oiobf_tbf& b, Plan& pl, const OpBuffers& io, cudaStream_t st, int g
     } else if (op.kind == 6) {
       const Plan::TinyLevel& tl = pl.tiny_levels[static_cast<size_t>(op.idx)];
       const LevelData& ld = b.side[tl.side][static_cast<size_t>(tl.l)];
-      launch_tiny_level(tl.args, pl.d_tiny_items.p + tl.item_begin, pl.d_tiny_in_off.p + tl.in_begin, ld.rank.p,
+      launch_tiny_level(tl.args, pl.d_tiny_groups.p + tl.group_begin, pl.d_tiny_off.p + tl.off_begin, ld.rank.p,
                         ld.width.p, ld.interp_off.p, ld.interp.p, in_ptr(tl.in_buf), out_ptr(tl.out_buf), st);
     } else if (op.kind == 7) {
       const GemvLaunch& gl = pl.gemvs[static_cast<size_t>(op.idx)];

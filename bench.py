@@ -342,24 +342,44 @@ def run_b200_sharded(args):
     from paper_2411_03029_b200.sharded import GpuShardBackend, TorchComm, construct
 
     ws, rank, local = dist_env()
+    verbose = os.environ.get("OIOBF_BENCH_VERBOSE") is not None
+
+    def stage(msg):
+        if verbose:
+            print(f"[rank {rank}] {time.strftime('%H:%M:%S')} {msg}", file=sys.stderr, flush=True)
+    # validation mode (single-GPU boxes): OIOBF_BENCH_DIST=gloo puts every rank
+    # on device 0 and exchanges through the host -- ranks never wait on each
+    # other on the GPU.  Timings from it are not scaling numbers.
+    backend = os.environ.get("OIOBF_BENCH_DIST", "nccl")
+    if backend == "gloo":
+        local = 0
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if backend == "gloo":
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stage(f"process group up ({backend})")
     _lib.check(_lib.load().oiobf_set_device(local))
     cfg = BY_NAME[args.config]
     dev = torch.device("cuda", local)
     comm = TorchComm(device=dev)
+
+    def allreduce_max(x: float) -> float:
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if comm.host else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
     sampler = ClockSampler(local)
     sampler.start()
     dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     be = GpuShardBackend(cfg.spec, cfg.L, cfg.tol, tb.ProxyStrategy(), cfg.seed, rank, ws)
+    stage("backend created")
     sb = construct(be, rank, ws, comm)
+    stage("constructed")
     torch.cuda.synchronize()
     construct_s = time.perf_counter() - t0
-    t = torch.tensor([construct_s], device=dev, dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    construct_s = float(t.item())
+    construct_s = allreduce_max(construct_s)
 
     Fh = make_input(cfg, cfg.input_seed, args.nv)
     N = cfg.points * args.nv
@@ -379,6 +399,7 @@ def run_b200_sharded(args):
 
     for _ in range(max(args.warmup, 3)):
         step()
+    stage("warm-up steps done")
     dist.barrier()
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -388,10 +409,8 @@ def run_b200_sharded(args):
         step()
         b.record(stream)
     torch.cuda.synchronize()
-    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms = allreduce_max(sum(a.elapsed_time(b) for a, b in evs) / args.steps)
+    stage("timed steps done")
     # e2e: pinned host F in, this rank's G out, exchange included
     pin_F = torch.from_numpy(np.ascontiguousarray(Fh.reshape(-1, order="F")).view(np.float64).copy()).pin_memory()
     pin_G = torch.empty_like(pin_F).pin_memory()
@@ -403,8 +422,14 @@ def run_b200_sharded(args):
         pin_G.copy_(G, non_blocking=True)
         torch.cuda.synchronize()
 
-    t_end = time.perf_counter() + 0.3  # PCIe link warm-up (see run_b200)
-    while time.perf_counter() < t_end:
+    # PCIe link warm-up (see run_b200) for ~0.3 s.  Every step holds a
+    # collective, so the count must be the same on all ranks: time a few
+    # steps, agree on the slowest rank's time, derive one count.
+    t1 = time.perf_counter()
+    for _ in range(5):
+        e2e_step()
+    per = allreduce_max((time.perf_counter() - t1) / 5)
+    for _ in range(max(1, int(0.3 / max(per, 1e-6)))):
         e2e_step()
     dist.barrier()
     for _ in range(max(args.steps, 50)):
@@ -415,13 +440,18 @@ def run_b200_sharded(args):
         pin_G.copy_(G, non_blocking=True)
         torch.cuda.synchronize()
         e2e.append(time.perf_counter() - t1)
-    e2e_ms = 1e3 * statistics.fmean(e2e)
-    t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t.item())
+    e2e_ms = allreduce_max(1e3 * statistics.fmean(e2e))
+    stage("e2e done")
     # correctness probe: gather G (disjoint slabs) and compare 200 rows with dense sums on rank 0
-    dist.all_reduce(G)
+    if comm.host:
+        Gc = G.cpu()
+        dist.all_reduce(Gc)
+        G.copy_(Gc)
+    else:
+        dist.all_reduce(G)
     clocks = sampler.stop()
+    st = np.zeros(4, np.int64)
+    _lib.check(_lib.load().oiobf_tbf_plan_stats(be.h, st))
     if rank == 0:
         rng = np.random.default_rng(1)
         rows = rng.choice(cfg.points, 200, replace=False)
@@ -439,6 +469,8 @@ def run_b200_sharded(args):
             "e2e": {"value": N / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step": 16 * N,
                     "d2h_bytes_per_step": 16 * N},
             "exchange_bytes_per_step_rank0": int(16 * lay.send_counts.sum() * args.nv),
+            "gpu_launches": int(st[2]) * args.steps,
+            "dist_backend": backend,
             "sampled_rel_err_vs_dense": err,
             "clocks": clocks,
             "construct": {"gpu_s": construct_s, "sharded": True},

@@ -161,23 +161,33 @@ class TorchComm:
     def __init__(self, group=None, device=None):
         import torch.distributed as dist
         self.dist, self.group, self.device = dist, group, device
+        # gloo (validation runs, CPU tests): collectives on host tensors
+        self.host = dist.get_backend(group) == "gloo"
+
+    def _dev(self):
+        return "cpu" if self.host else self.device
 
     def allreduce_max_int(self, v: int) -> int:
         import torch
-        t = torch.tensor([v], dtype=torch.int64, device=self.device)
+        t = torch.tensor([v], dtype=torch.int64, device=self._dev())
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return int(t.item())
 
     def allreduce_sum_np(self, a: np.ndarray) -> np.ndarray:
         import torch
-        t = torch.from_numpy(np.ascontiguousarray(a).astype(np.int64)).to(self.device)
+        t = torch.from_numpy(np.ascontiguousarray(a).astype(np.int64)).to(self._dev())
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return t.cpu().numpy()
 
     def alltoall(self, send, recv, send_counts, recv_counts):
         """send/recv: float64 tensors (complex interleaved); counts in complex elements."""
-        self.dist.all_to_all_single(recv, send, [2 * int(c) for c in recv_counts], [2 * int(c) for c in send_counts],
-                                    group=self.group)
+        rs, ss = [2 * int(c) for c in recv_counts], [2 * int(c) for c in send_counts]
+        if self.host and send.is_cuda:  # gloo has no CUDA all-to-all: stage through the host
+            r = recv.cpu()
+            self.dist.all_to_all_single(r, send.cpu(), rs, ss, group=self.group)
+            recv.copy_(r)
+        else:
+            self.dist.all_to_all_single(recv, send, rs, ss, group=self.group)
 
 
 def construct(backend, rank: int, world: int, comm) -> ShardedButterfly:

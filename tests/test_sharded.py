@@ -188,3 +188,26 @@ def test_sharded_gpu_lockstep(world):
     G = run_lockstep(backends, Ft).cpu().numpy().view(np.complex128)
     err = np.linalg.norm(G - G1) / np.linalg.norm(G1)
     assert err < 1e-12, err
+
+
+@pytest.mark.gpu
+def test_bench_sharded_torchrun_validation():
+    """bench.py's N > 1 path end to end under torchrun (world 2), in its
+    validation mode: gloo collectives staged through the host and both ranks on
+    device 0, so the ranks never wait on each other on the GPU.  Guards the
+    collective call order of construction, timed steps and e2e (a per-rank
+    time-based warm-up once desynchronised the all-to-all and hung)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, OIOBF_BENCH_DIST="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+           "--steps", "2", "--warmup", "3"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["dist_backend"] == "gloo"
+    assert line["sampled_rel_err_vs_dense"] < 1e-4
+    assert line["gpu_launches"] > 0

@@ -119,6 +119,13 @@ int oiobf_tbf_contract(oiobf_tbf* h, const double* F, double* G, int64_t nv);
 int oiobf_tbf_contract_device(oiobf_tbf* h, const void* dF, void* dG, int64_t nv, void* stream);
 
 /* tbf_memory: bytes of V, W, U, P, cores (out[5]). */
+// TBF1 serialization: self-describing little-endian file
+// (header, factor blocks in canonical tree order, cores, FNV-1a checksum);
+// save -> load round trips are bit-exact.  load returns a new handle on the
+// current device (oiobf_tbf_destroy it).
+int oiobf_tbf_save(const oiobf_tbf* h, const char* path);
+int oiobf_tbf_load(const char* path, oiobf_tbf** out);
+
 // Apply engine: 0 auto (the tiny-box engine when every box has <= 64
 // elements and there are >= 2^20 middle pairs, e.g. the d = 6 DFT), 1 the
 // fused-box engine, 2 the tiny-box engine.  Changing it drops cached plans.

@@ -9,11 +9,11 @@ loudly if it (or a Blackwell device) is missing — there is no CPU fallback.
 from .configs import CONFIGS, BY_NAME, Config, KernelSpec, dft, green_cubes, green_plates, level_rule, radon2d  # noqa
 from .butterfly import (ColumnID, ProxyStrategy, TensorButterfly, column_id, column_id_batch, dense_rows,  # noqa
                         derive_seed, mode_product_blockdiag, select_proxies, select_proxies_count, subtensor_at,
-                        tbf_construct, tbf_contract, tbf_error_estimate, tbf_memory)
+                        tbf_construct, tbf_contract, tbf_error_estimate, tbf_load, tbf_memory)
 
 __all__ = [
     "CONFIGS", "BY_NAME", "Config", "KernelSpec", "dft", "green_cubes", "green_plates", "level_rule", "radon2d",
     "ColumnID", "ProxyStrategy", "TensorButterfly", "column_id", "column_id_batch", "dense_rows", "derive_seed",
     "mode_product_blockdiag", "select_proxies", "select_proxies_count", "subtensor_at", "tbf_construct",
-    "tbf_contract", "tbf_error_estimate", "tbf_memory",
+    "tbf_contract", "tbf_error_estimate", "tbf_load", "tbf_memory",
 ]

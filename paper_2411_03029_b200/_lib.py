@@ -43,7 +43,7 @@ EXPORTS = [
     "oiobf_tbf_profile_contract", "oiobf_dense_rows", "oiobf_tbf_check_finite",
     "oiobf_tbf_shard_begin", "oiobf_tbf_shard_level", "oiobf_tbf_umid_info", "oiobf_tbf_umid_export",
     "oiobf_tbf_umid_import", "oiobf_tbf_set_exchange", "oiobf_tbf_contract_phase",
-    "oiobf_tbf_set_apply_engine", "oiobf_tbf_apply_engine",
+    "oiobf_tbf_set_apply_engine", "oiobf_tbf_apply_engine", "oiobf_tbf_save", "oiobf_tbf_load",
 ]
 
 _lock = threading.Lock()
@@ -77,6 +77,8 @@ def load(path: str = LIB_PATH):
         L.oiobf_tbf_contract_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
         L.oiobf_tbf_memory.argtypes = [C.c_void_p, i64p]
         L.oiobf_tbf_set_apply_engine.argtypes = [C.c_void_p, C.c_int32]
+        L.oiobf_tbf_save.argtypes = [C.c_void_p, C.c_char_p]
+        L.oiobf_tbf_load.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
         L.oiobf_tbf_apply_engine.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
         L.oiobf_tbf_info.argtypes = [C.c_void_p, i64p]
         L.oiobf_tbf_export.argtypes = [C.c_void_p] + [C.c_void_p] * 10

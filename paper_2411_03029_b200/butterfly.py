@@ -267,6 +267,10 @@ class TensorButterfly:
         _lib.check(_lib.load().oiobf_tbf_contract(self._h, _cx_f(F), out, nv))
         return _from_f(out, F.shape)
 
+    def save(self, path: str) -> None:
+        """TBF1 file: bit-exact round trip through tbf_load."""
+        _lib.check(_lib.load().oiobf_tbf_save(self._h, str(path).encode()))
+
     def set_apply_engine(self, engine: str) -> None:
         """'auto' | 'box' | 'tiny' (tiny: thread-per-output engine for d = 6 scale)."""
         code = {"auto": 0, "box": 1, "tiny": 2}[engine]
@@ -297,6 +301,15 @@ def tbf_construct(spec: KernelSpec, L: int, tol: float, proxies: ProxyStrategy |
     sc = _lib.spec_c(spec)
     ps = proxies.c()
     _lib.check(Lb.oiobf_tbf_construct(C.byref(sc), L, tol, C.byref(ps), seed, C.byref(h)))
+    return TensorButterfly(h, spec, L, tol)
+
+
+def tbf_load(path: str) -> TensorButterfly:
+    """Load a TBF1 file written by TensorButterfly.save onto the current device."""
+    from .tbf1 import read_header
+    spec, L, tol, _, _ = read_header(path)  # the library parses the rest and verifies the checksum
+    h = C.c_void_p()
+    _lib.check(_lib.load().oiobf_tbf_load(str(path).encode(), C.byref(h)))
     return TensorButterfly(h, spec, L, tol)
 
 

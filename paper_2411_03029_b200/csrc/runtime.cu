@@ -609,15 +609,15 @@ void finish_level(oiobf_tbf& b, LevelData& ld, DevBuf<int>& sat, DevBuf<int>& sk
 // Cores K(tbar, sbar) of the pairs (t, s) whose s this rank owns (all pairs
 // when world == 1).  Row skeletons come from the U side at level Lc -- local
 // when world == 1, gathered from every rank (umid_*) otherwise.
-void build_cores(oiobf_tbf& b) {
-  cudaStream_t st = b.stream;
+// Pair layout (R, C, ranks, skeleton offsets, arena offsets) of every middle
+// pair; returns the core arena size.  Shared by construction and TBF1 load.
+i64 layout_pairs(oiobf_tbf& b) {
   const int d = b.d;
   const LevelData& U = b.side[1][static_cast<size_t>(b.Lc)];
   const LevelData& V = b.side[0][static_cast<size_t>(b.Lc)];
   const bool gathered = b.world > 1;
   const int* urank = gathered ? b.umid_rank.data() : U.h_rank.data();
   const i64* uskel_off = gathered ? b.umid_skel_off.data() : U.h_skel_off.data();
-  const int* uskel = gathered ? b.umid_skel.p : U.skel.p;
   const i64 P = b.nmid * b.nmid;
   b.h_pairs.assign(static_cast<size_t>(P), PairDesc{});
   i64 off = 0;
@@ -642,6 +642,17 @@ void build_cores(oiobf_tbf& b) {
     off += static_cast<i64>(pd.R) * pd.C;
   }
   b.total_core = off;
+  return off;
+}
+
+void build_cores(oiobf_tbf& b) {
+  cudaStream_t st = b.stream;
+  const LevelData& U = b.side[1][static_cast<size_t>(b.Lc)];
+  const LevelData& V = b.side[0][static_cast<size_t>(b.Lc)];
+  const bool gathered = b.world > 1;
+  const int* uskel = gathered ? b.umid_skel.p : U.skel.p;
+  const i64 P = b.nmid * b.nmid;
+  const i64 off = layout_pairs(b);
   b.cores.alloc(static_cast<size_t>(std::max<i64>(off, 1)));
   DevBuf<PairDesc> dp = to_device(b.h_pairs, st);
   EventTimer t(st);
@@ -1745,6 +1756,205 @@ void contract_host(oiobf_tbf& b, const double* F, double* G, i64 nv) {
   TBF_CUDA(cudaStreamSynchronize(b.stream));
 }
 
+// ---- TBF1 serialization: self-describing little-endian
+// file: header (magic "TBF1", version, kernel spec, L, tol, proxy strategy,
+// seed), then the factor blocks in canonical tree order (V/W levels 0..Lc,
+// U/P levels 0..Lc: r_est, slot count, proxy rows, widest ID, ranks, widths,
+// pivots, sorted skeletons, interps), then the cores (per pair R, C and the
+// row-major R x C entries), then an FNV-1a 64-bit checksum of everything
+// before it.  Round trips are bit-exact (tests/test_gpu_parity.py).
+constexpr uint32_t kTbfVersion = 1;
+
+struct TbfWriter {
+  FILE* f;
+  u64 h = 1469598103934665603ULL;
+  void put(const void* p, size_t n) {
+    const unsigned char* c = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 1099511628211ULL;
+    if (n && std::fwrite(p, 1, n, f) != n) throw std::runtime_error("tbf_save: write failed");
+  }
+  template <class T>
+  void v(T x) { put(&x, sizeof(T)); }
+};
+
+struct TbfReader {
+  FILE* f;
+  u64 h = 1469598103934665603ULL;
+  void get(void* p, size_t n) {
+    if (n && std::fread(p, 1, n, f) != n) throw InvalidArg("tbf_load: truncated file");
+    const unsigned char* c = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 1099511628211ULL;
+  }
+  template <class T>
+  T v() {
+    T x;
+    get(&x, sizeof(T));
+    return x;
+  }
+};
+
+void tbf_save(const oiobf_tbf& b, const char* path) {
+  require(b.world == 1, "tbf_save: sharded factorizations are not serializable");
+  FILE* f = std::fopen(path, "wb");
+  if (!f) throw std::runtime_error(std::string("tbf_save: cannot open ") + path);
+  TbfWriter w{f};
+  try {
+    cudaStream_t st = b.stream;
+    w.put("TBF1", 4);
+    w.v<uint32_t>(kTbfVersion);
+    w.v<int32_t>(b.spec.kind);
+    w.v<int32_t>(b.spec.d);
+    w.v<int64_t>(b.spec.n);
+    w.v<int32_t>(b.spec.bitrev);
+    w.v<double>(b.spec.kappa);
+    for (int i = 0; i < 3; ++i) w.v<double>(b.spec.offset[i]);
+    w.v<int32_t>(b.L);
+    w.v<double>(b.tol);
+    w.v<int32_t>(b.strat.mode);
+    w.v<int64_t>(b.strat.q);
+    w.v<int64_t>(b.strat.max_retries);
+    w.v<int64_t>(b.strat.row_cap);
+    w.v<uint64_t>(b.seed);
+    for (int sd = 0; sd < 2; ++sd)
+      for (int l = 0; l <= b.Lc; ++l) {
+        const LevelData& ld = b.side[sd][static_cast<size_t>(l)];
+        const i64 ns = ld.nslots;
+        w.v<int64_t>(b.r_est[sd][static_cast<size_t>(l)]);
+        w.v<int64_t>(ns);
+        w.v<int64_t>(ld.L.m);
+        w.v<int64_t>(ld.L.wmax);
+        w.v<int64_t>(ld.total_skel);
+        w.v<int64_t>(ld.total_interp);
+        std::vector<int> perm(static_cast<size_t>(ns * ld.L.wmax)), skel(static_cast<size_t>(ld.total_skel));
+        std::vector<double2> interp(static_cast<size_t>(ld.total_interp));
+        ld.perm.download(perm.data(), perm.size(), st);
+        ld.skel.download(skel.data(), skel.size(), st);
+        ld.interp.download(interp.data(), interp.size(), st);
+        TBF_CUDA(cudaStreamSynchronize(st));
+        w.put(ld.h_rank.data(), sizeof(int) * static_cast<size_t>(ns));
+        w.put(ld.h_width.data(), sizeof(int) * static_cast<size_t>(ns));
+        w.put(perm.data(), sizeof(int) * perm.size());
+        w.put(skel.data(), sizeof(int) * skel.size());
+        w.put(interp.data(), sizeof(double2) * interp.size());
+      }
+    const i64 P = static_cast<i64>(b.h_pairs.size());
+    w.v<int64_t>(P);
+    w.v<int64_t>(b.total_core);
+    for (const PairDesc& pd : b.h_pairs) {
+      w.v<int32_t>(pd.R);
+      w.v<int32_t>(pd.C);
+    }
+    std::vector<double2> cores(static_cast<size_t>(b.total_core));
+    b.cores.download(cores.data(), cores.size(), st);
+    TBF_CUDA(cudaStreamSynchronize(st));
+    w.put(cores.data(), sizeof(double2) * cores.size());
+    const u64 sum = w.h;
+    if (std::fwrite(&sum, sizeof(sum), 1, f) != 1) throw std::runtime_error("tbf_save: write failed");
+  } catch (...) {
+    std::fclose(f);
+    throw;
+  }
+  if (std::fclose(f) != 0) throw std::runtime_error("tbf_save: close failed");
+}
+
+oiobf_tbf* tbf_load(const char* path) {
+  FILE* f = std::fopen(path, "rb");
+  if (!f) throw InvalidArg(std::string("tbf_load: cannot open ") + path);
+  TbfReader r{f};
+  std::unique_ptr<oiobf_tbf> b;
+  try {
+    char magic[4];
+    r.get(magic, 4);
+    require(std::memcmp(magic, "TBF1", 4) == 0, "tbf_load: not a TBF1 file");
+    require(r.v<uint32_t>() == kTbfVersion, "tbf_load: unsupported TBF1 version");
+    oiobf_kernel_spec spec{};
+    spec.kind = r.v<int32_t>();
+    spec.d = r.v<int32_t>();
+    spec.n = r.v<int64_t>();
+    spec.bitrev = r.v<int32_t>();
+    spec.kappa = r.v<double>();
+    for (int i = 0; i < 3; ++i) spec.offset[i] = r.v<double>();
+    const int L = r.v<int32_t>();
+    const double tol = r.v<double>();
+    oiobf_proxy_strategy ps{};
+    ps.mode = r.v<int32_t>();
+    ps.q = r.v<int64_t>();
+    ps.max_retries = r.v<int64_t>();
+    ps.row_cap = r.v<int64_t>();
+    const u64 seed = r.v<uint64_t>();
+    b = construct_begin(spec, L, tol, ps, seed, 0, 1);
+    cudaStream_t st = b->stream;
+    for (int sd = 0; sd < 2; ++sd)
+      for (int l = 0; l <= b->Lc; ++l) {
+        const i64 r_est = r.v<int64_t>(), ns = r.v<int64_t>(), m = r.v<int64_t>(), wmax = r.v<int64_t>();
+        const i64 tsk = r.v<int64_t>(), tip = r.v<int64_t>();
+        LevelData& ld = b->side[sd][static_cast<size_t>(l)];
+        ld.L = make_level(*b, sd, l, r_est, wmax);
+        require(ld.L.nslots == ns && ld.L.m == m && wmax >= 1 && wmax <= kMaxW, "tbf_load: level shape mismatch");
+        b->r_est[sd].push_back(r_est);
+        ld.nslots = ns;
+        ld.h_rank.resize(static_cast<size_t>(ns));
+        ld.h_width.resize(static_cast<size_t>(ns));
+        ld.h_sat.assign(static_cast<size_t>(ns), 0);
+        std::vector<int> perm(static_cast<size_t>(ns * wmax)), skel(static_cast<size_t>(tsk));
+        std::vector<double2> interp(static_cast<size_t>(tip));
+        r.get(ld.h_rank.data(), sizeof(int) * static_cast<size_t>(ns));
+        r.get(ld.h_width.data(), sizeof(int) * static_cast<size_t>(ns));
+        r.get(perm.data(), sizeof(int) * perm.size());
+        r.get(skel.data(), sizeof(int) * skel.size());
+        r.get(interp.data(), sizeof(double2) * interp.size());
+        ld.h_skel_off.resize(static_cast<size_t>(ns));
+        ld.h_interp_off.resize(static_cast<size_t>(ns));
+        i64 so = 0, io = 0;
+        ld.max_rank = 0;
+        for (i64 i = 0; i < ns; ++i) {
+          const int rk = ld.h_rank[static_cast<size_t>(i)], wd = ld.h_width[static_cast<size_t>(i)];
+          require(rk >= 0 && wd >= rk && wd <= wmax, "tbf_load: bad rank / width");
+          ld.h_skel_off[static_cast<size_t>(i)] = so;
+          ld.h_interp_off[static_cast<size_t>(i)] = io;
+          so += rk;
+          io += static_cast<i64>(rk) * wd;
+          ld.max_rank = std::max(ld.max_rank, rk);
+        }
+        require(so == tsk && io == tip, "tbf_load: skeleton / interp sizes disagree with the ranks");
+        ld.total_skel = tsk;
+        ld.total_interp = tip;
+        ld.rank = to_device(ld.h_rank, st);
+        ld.width = to_device(ld.h_width, st);
+        ld.perm = to_device(perm, st);
+        ld.gaps.alloc(static_cast<size_t>(ns));
+        ld.skel_off = to_device(ld.h_skel_off, st);
+        ld.interp_off = to_device(ld.h_interp_off, st);
+        ld.skel.alloc(static_cast<size_t>(std::max<i64>(tsk, 1)));
+        ld.skel.upload(skel.data(), skel.size(), st);
+        ld.interp.alloc(static_cast<size_t>(std::max<i64>(tip, 1)));
+        ld.interp.upload(interp.data(), interp.size(), st);
+        TBF_CUDA(cudaStreamSynchronize(st));
+      }
+    const i64 P = r.v<int64_t>(), tc = r.v<int64_t>();
+    const i64 off = layout_pairs(*b);
+    require(P == static_cast<i64>(b->h_pairs.size()) && tc == off, "tbf_load: core layout mismatch");
+    for (const PairDesc& pd : b->h_pairs) {
+      const int R = r.v<int32_t>(), C = r.v<int32_t>();
+      require(R == pd.R && C == pd.C, "tbf_load: core shape mismatch");
+    }
+    std::vector<double2> cores(static_cast<size_t>(tc));
+    r.get(cores.data(), sizeof(double2) * cores.size());
+    const u64 expect = r.h;
+    u64 sum = 0;
+    if (std::fread(&sum, sizeof(sum), 1, f) != 1) throw InvalidArg("tbf_load: truncated file");
+    require(sum == expect, "tbf_load: checksum mismatch");
+    b->cores.alloc(static_cast<size_t>(std::max<i64>(tc, 1)));
+    b->cores.upload(cores.data(), cores.size(), st);
+    TBF_CUDA(cudaStreamSynchronize(st));
+  } catch (...) {
+    std::fclose(f);
+    throw;
+  }
+  std::fclose(f);
+  return b.release();
+}
+
 int status_of(const std::exception& e) {
   g_err = e.what();
   return dynamic_cast<const InvalidArg*>(&e) ? OIOBF_EINVAL : OIOBF_ERUNTIME;
@@ -1957,6 +2167,22 @@ int oiobf_tbf_contract(oiobf_tbf* h, const double* F, double* G, int64_t nv) {
   require(h->world == 1, "tbf_contract: sharded factorization -- use oiobf_tbf_contract_phase");
   std::lock_guard<std::mutex> lk(h->mu);
   contract_host(*h, F, G, nv);
+  CAPI_END
+}
+
+int oiobf_tbf_save(const oiobf_tbf* h, const char* path) {
+  CAPI_BEGIN
+  require(h && path, "tbf_save: null argument");
+  std::lock_guard<std::mutex> lk(const_cast<oiobf_tbf*>(h)->mu);
+  TBF_CUDA(cudaSetDevice(h->device));
+  tbf_save(*h, path);
+  CAPI_END
+}
+
+int oiobf_tbf_load(const char* path, oiobf_tbf** out) {
+  CAPI_BEGIN
+  require(path && out, "tbf_load: null argument");
+  *out = tbf_load(path);
   CAPI_END
 }
 

@@ -357,3 +357,62 @@ def test_full_config_accuracy(oracle, cfg, gate):
     print(f"{cfg}: sampled rel err gpu {err:.3e} oracle {err_o:.3e} (tol {c.tol:g}, ratio {err / c.tol:.1f})")
     assert abs(err - err_o) <= 1e-3 * err_o
     assert err <= gate * c.tol
+
+
+def _factorization_from_tbf1(t):
+    """TBF1 (pure-Python reader) -> the oracle's Factorization (flat export)."""
+    from oracle.bindings import Factorization
+    ranks, ncols, rows, perm, skel, interp = [], [], [], [], [], []
+    for lv in t.levels:
+        ns = len(lv["rank"])
+        ranks.append(lv["rank"])
+        ncols.append(lv["width"])
+        rows.append(np.full(ns, lv["rows"], np.int64))
+        pm = lv["perm"].reshape(ns, lv["wmax"])
+        perm.extend(pm[i, :lv["width"][i]] for i in range(ns))
+        skel.append(lv["skel"])
+        interp.append(lv["interp"])
+    cores, off = [], 0
+    for R, Cc in zip(t.core_rows, t.core_cols):
+        blk = t.cores_rowmajor[off:off + R * Cc].reshape(R, Cc)
+        cores.append(blk.reshape(-1, order="F"))  # reference column-major matricization
+        off += R * Cc
+    d, Lc = t.spec.d, t.Lc
+    r_est = np.array([lv["r_est"] for lv in t.levels], np.int64)
+    ns_all = sum(len(x) for x in ranks)
+    return Factorization(d=d, n=t.spec.n, L=t.L, Lc=Lc, nmid=2 ** (d * Lc),
+                         ranks=np.concatenate(ranks).astype(np.int64), ncols=np.concatenate(ncols).astype(np.int64),
+                         rows=np.concatenate(rows), gaps=np.zeros(ns_all), flags=np.zeros(ns_all, np.int64),
+                         skel=np.concatenate(skel).astype(np.int64), interp=np.concatenate(interp),
+                         perm=np.concatenate(perm).astype(np.int64) if perm else np.zeros(0, np.int64),
+                         cores=np.concatenate(cores), core_rows=t.core_rows, core_cols=t.core_cols, r_est=r_est)
+
+
+@pytest.mark.parametrize("name,spec,tol,L", [CASES[0], CASES[2], CASES[5], CASES[7]],
+                         ids=[CASES[i][0] for i in (0, 2, 5, 7)])
+def test_tbf1_roundtrip_bitexact(oracle, tmp_path, name, spec, tol, L):
+    """TBF1 serialization: save -> load is bit-exact (every
+    exported array and the contraction), the pure-Python reader feeds the CPU
+    oracle (cross-process use of GPU factors), and corruption is detected."""
+    from paper_2411_03029_b200.tbf1 import read_tbf1
+    bf = tb.tbf_construct(spec, L, tol, seed=4)
+    path = tmp_path / f"{name}.tbf1"
+    bf.save(path)
+    bl = tb.tbf_load(path)
+    a, b = bf.export(), bl.export()
+    for f in ("ranks", "ncols", "rows", "skel", "interp", "perm", "cores", "core_rows", "core_cols", "r_est"):
+        np.testing.assert_array_equal(getattr(a, f), getattr(b, f), err_msg=f)
+    assert bf.memory() == bl.memory()
+    rng = np.random.default_rng(5)
+    F = rand_c(rng, (spec.n,) * spec.d)
+    g1, g2 = bf.contract(F), bl.contract(F)
+    assert np.array_equal(g1, g2)
+    t = read_tbf1(str(path))
+    tbo = oracle.tbf_import(spec, L, tol, _factorization_from_tbf1(t))
+    assert rel(g1, tbo.contract(F)) < 1e-10
+    data = bytearray(path.read_bytes())
+    data[len(data) // 2] ^= 0x40
+    bad = tmp_path / "bad.tbf1"
+    bad.write_bytes(bytes(data))
+    with pytest.raises(ValueError):
+        tb.tbf_load(bad)

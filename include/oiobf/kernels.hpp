@@ -12,7 +12,13 @@
 
 namespace oiobf {
 
-enum class KernelKind { Green = OIOBF_KERNEL_GREEN, DFT = OIOBF_KERNEL_DFT, Radon2D = OIOBF_KERNEL_RADON2D };
+enum class KernelKind {
+  Green = OIOBF_KERNEL_GREEN,
+  DFT = OIOBF_KERNEL_DFT,
+  Radon2D = OIOBF_KERNEL_RADON2D,
+  Radon3D = OIOBF_KERNEL_RADON3D,
+  NUDFT = OIOBF_KERNEL_NUDFT
+};
 
 struct KernelSpec {
   KernelKind kind = KernelKind::Green;
@@ -21,18 +27,22 @@ struct KernelSpec {
   double kappa = 0;                     // Green wavenumber
   double offset[3] = {0, 0, 0};         // Green source offset
   bool bitrev = false;                  // DFT: two-sided per-mode bit reversal
+  std::uint32_t seed = 0;               // NUDFT: seed of the random target locations
 };
 
 inline KernelEvaluator make_kernel(const KernelSpec& s) {
   require(s.d >= 1 && s.d <= 6, "make_kernel: d must be in [1, 6]");
   require(s.n >= 1, "make_kernel: n must be positive");
   require(s.kind != KernelKind::Radon2D || s.d == 2, "make_kernel: radon2d needs d = 2");
+  require(s.kind != KernelKind::Radon3D || s.d == 3, "make_kernel: radon3d needs d = 3");
+  require(s.kind != KernelKind::NUDFT || !s.bitrev, "make_kernel: nudft has no bit-reversed ordering");
   require(s.kind != KernelKind::Green || s.d <= 3, "make_kernel: green needs d <= 3");
   KernelFunctor f;
   f.spec.kind = static_cast<int32_t>(s.kind);
   f.spec.d = static_cast<int32_t>(s.d);
   f.spec.n = s.n;
   f.spec.bitrev = s.bitrev ? 1 : 0;
+  f.spec.seed = s.seed;
   f.spec.kappa = s.kappa;
   for (int p = 0; p < 3; ++p) f.spec.offset[p] = s.offset[p];
   KernelEvaluator k;
@@ -73,6 +83,23 @@ inline KernelSpec radon2d(std::int64_t n) {
   s.kind = KernelKind::Radon2D;
   s.d = 2;
   s.n = n;
+  return s;
+}
+// Phi = x.k + c|k|, c = (3 + sin 2 pi x1 sin 2 pi x2 sin 2 pi x3) / 100
+inline KernelSpec radon3d(std::int64_t n) {
+  KernelSpec s;
+  s.kind = KernelKind::Radon3D;
+  s.d = 3;
+  s.n = n;
+  return s;
+}
+// PAPER.md:707 type-2 NUDFT: seeded random target locations in [0, n-1]^d
+inline KernelSpec nudft(std::int64_t d, std::int64_t n, std::uint32_t seed = 1) {
+  KernelSpec s;
+  s.kind = KernelKind::NUDFT;
+  s.d = d;
+  s.n = n;
+  s.seed = seed;
   return s;
 }
 

@@ -33,6 +33,8 @@ extern "C" {
 #define OIOBF_KERNEL_GREEN 0   /* exp(-i kappa rho)/rho, plates (d=2) / cubes (d=3) */
 #define OIOBF_KERNEL_DFT 1     /* exp(-2 pi i x.k), optional two-sided bit reversal  */
 #define OIOBF_KERNEL_RADON2D 2 /* exp(2 pi i Phi(x,k))            */
+#define OIOBF_KERNEL_RADON3D 3 /* exp(2 pi i (x.k + c|k|)), PAPER.md:644-646 (d=3)  */
+#define OIOBF_KERNEL_NUDFT 4   /* type-2 NUDFT exp(2 pi i x^i.y^j), seeded random x^i */
 
 /* ProxyMode (id.hpp:48) */
 #define OIOBF_PROXY_ALL 0
@@ -46,7 +48,7 @@ typedef struct oiobf_kernel_spec {
   int32_t d;       /* modes per side, 1..6 */
   int64_t n;       /* points per mode (m_k = n_k = n) */
   int32_t bitrev;  /* DFT: two-sided per-mode bit reversal */
-  int32_t pad_;
+  uint32_t seed;   /* NUDFT: seed of the random target locations */
   double kappa;     /* Green: wavenumber */
   double offset[3]; /* Green: source-plane/cube offset added to y */
 } oiobf_kernel_spec;

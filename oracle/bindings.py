@@ -34,8 +34,9 @@ def ref_available() -> bool:
 
 
 def spec_arrays(spec) -> tuple[np.ndarray, np.ndarray]:
-    """(int32[4] = kind, d, n, bitrev ; float64[4] = kappa, offset xyz)."""
-    si = np.array([spec.kind, spec.d, spec.n, int(spec.bitrev)], dtype=np.int32)
+    """(int32[5] = kind, d, n, bitrev, seed ; float64[4] = kappa, offset xyz)."""
+    seed = int(getattr(spec, "seed", 0)) & 0xFFFFFFFF
+    si = np.array([spec.kind, spec.d, spec.n, int(spec.bitrev), np.int64(seed).astype(np.int32)], dtype=np.int32)
     off = list(spec.offset) + [0.0] * (3 - len(spec.offset))
     sf = np.array([spec.kappa, *off[:3]], dtype=np.float64)
     return si, sf

@@ -325,13 +325,23 @@ ColumnID column_id(std::vector<Cx> a, i64 m, i64 n, double tol, i64 max_rank, co
 
 // ----------------------------------------------------- kernels
 struct Spec {
-  int kind = 0;  // 0 green, 1 dft, 2 radon2d
+  int kind = 0;  // 0 green, 1 dft, 2 radon2d, 3 radon3d, 4 nudft
   int d = 2;
   i64 n = 0;
   int bitrev = 0;
+  u64 seed = 0;  // nudft locations
   double kappa = 0;
   double offset[3] = {0, 0, 0};
 };
+
+// NUDFT target location x^i_k in [0, n-1]: uniform per coordinate, counter-based
+// from the seed and the flattened (0-based, mode-0-fastest) target index
+// (SPEC.md kernels design decisions; "random in [0, n-1]")
+double nudft_loc(u64 seed, i64 flat, int k, i64 n) {
+  const u64 tags[3] = {0x4EULL, static_cast<u64>(flat), static_cast<u64>(k)};
+  const u64 h = derive_seed(seed, tags, 3);
+  return static_cast<double>(h >> 11) * 0x1.0p-53 * static_cast<double>(n - 1);
+}
 
 i64 bitrev1(i64 i, i64 n) {
   i64 x = i - 1, r = 0;
@@ -369,6 +379,35 @@ Cx kernel_eval(const Spec& s, const i64* i, const i64* j) {
     const double t = 2.0 * static_cast<double>(m) / n;
     return Cx(std::cos(M_PI * t), -std::sin(M_PI * t));
   }
+  if (s.kind == 3) {  // Radon 3D: Phi = x.k + c|k|, c = (3 + prod sin 2 pi x_p)/100
+    i64 num = 0;
+    double ss = 1, kk = 0;
+    for (int p = 0; p < 3; ++p) {
+      const double x = static_cast<double>(i[p] - 1) / n;
+      const i64 ki = j[p] - 1 - s.n / 2;
+      num += (i[p] - 1) * ki;
+      ss = ss * std::sin(2.0 * M_PI * x);
+      kk = kk + static_cast<double>(ki) * static_cast<double>(ki);
+    }
+    num %= s.n;
+    if (num < 0) num += s.n;
+    const double c = (3.0 + ss) / 100.0;
+    const double phi = static_cast<double>(num) / n + c * std::sqrt(kk);
+    const double ph = 2.0 * M_PI * phi;
+    return Cx(std::cos(ph), std::sin(ph));
+  }
+  if (s.kind == 4) {  // type-2 NUDFT: exp(2 pi i x^i . y^j), y^j_k = (j_k - 1)/n
+    i64 flat = 0, st = 1;
+    for (int p = 0; p < s.d; ++p) {
+      flat += (i[p] - 1) * st;
+      st *= s.n;
+    }
+    double phi = 0;
+    for (int p = 0; p < s.d; ++p) phi = phi + nudft_loc(s.seed, flat, p, s.n) * static_cast<double>(j[p] - 1) / n;
+    phi = phi - std::floor(phi);
+    const double ph = 2.0 * M_PI * phi;
+    return Cx(std::cos(ph), std::sin(ph));
+  }
   // generalized Radon 2D: exp(2 pi i Phi)
   const double x1 = static_cast<double>(i[0] - 1) / n, x2 = static_cast<double>(i[1] - 1) / n;
   const i64 k1i = j[0] - 1 - s.n / 2, k2i = j[1] - 1 - s.n / 2;
@@ -390,6 +429,7 @@ Spec spec_from(const int* si, const double* sf) {
   s.d = si[1];
   s.n = si[2];
   s.bitrev = si[3];
+  s.seed = static_cast<u64>(static_cast<uint32_t>(si[4]));
   s.kappa = sf[0];
   s.offset[0] = sf[1];
   s.offset[1] = sf[2];
@@ -397,6 +437,8 @@ Spec spec_from(const int* si, const double* sf) {
   if (s.d < 1 || s.d > 6) throw std::invalid_argument("kernel spec: d must be in [1,6]");
   if (s.kind == 2 && s.d != 2) throw std::invalid_argument("kernel spec: radon2d needs d=2");
   if (s.kind == 0 && s.d > 3) throw std::invalid_argument("kernel spec: green needs d<=3");
+  if (s.kind == 3 && s.d != 3) throw std::invalid_argument("kernel spec: radon3d needs d=3");
+  if (s.kind < 0 || s.kind > 4) throw std::invalid_argument("make_kernel: unknown kernel kind");
   return s;
 }
 

@@ -25,7 +25,7 @@ class OiobfError(RuntimeError):
 
 
 class KernelSpecC(C.Structure):
-    _fields_ = [("kind", C.c_int32), ("d", C.c_int32), ("n", C.c_int64), ("bitrev", C.c_int32), ("pad_", C.c_int32),
+    _fields_ = [("kind", C.c_int32), ("d", C.c_int32), ("n", C.c_int64), ("bitrev", C.c_int32), ("seed", C.c_uint32),
                 ("kappa", C.c_double), ("offset", C.c_double * 3)]
 
 
@@ -101,7 +101,8 @@ def check(rc: int) -> None:
 
 def spec_c(spec) -> KernelSpecC:
     off = list(spec.offset) + [0.0] * (3 - len(spec.offset))
-    return KernelSpecC(spec.kind, spec.d, spec.n, int(spec.bitrev), 0, spec.kappa, (C.c_double * 3)(*off[:3]))
+    return KernelSpecC(spec.kind, spec.d, spec.n, int(spec.bitrev), int(getattr(spec, "seed", 0)) & 0xFFFFFFFF,
+                       spec.kappa, (C.c_double * 3)(*off[:3]))
 
 
 def ptr(a: np.ndarray | None):

@@ -12,13 +12,19 @@ Formulas (BASELINE.json ``configs``), 1-based indices:
 * radon2d (kind 2): K = exp(2 pi i Phi), Phi = x.k + sqrt(c1^2 k1^2 + c2^2 k2^2),
   c1 = (2 + sin 2pi x1 sin 2pi x2)/16, c2 = (2 + cos 2pi x1 cos 2pi x2)/16,
   x_p = (i_p - 1)/n, k_p = j_p - 1 - n/2 (PAPER.md:633-642).
+* radon3d (kind 3): K = exp(2 pi i Phi), Phi = x.k + c |k|,
+  c = (3 + sin 2pi x1 sin 2pi x2 sin 2pi x3)/100; x.k reduced
+  exactly mod 1 as for radon2d.
+* nudft   (kind 4): type-2 non-uniform DFT K = exp(2 pi i x^i . y^j),
+  y^j_k = (j_k - 1)/n, x^i_k uniform in [0, n-1] from derive_seed(seed, {0x4E,
+  flat(i), k}) (SPEC.md kernels: counter-based locations).
 """
 from __future__ import annotations
 
 import math
 from dataclasses import dataclass, field
 
-GREEN, DFT, RADON2D = 0, 1, 2
+GREEN, DFT, RADON2D, RADON3D, NUDFT = 0, 1, 2, 3, 4
 
 
 @dataclass(frozen=True)
@@ -29,9 +35,10 @@ class KernelSpec:
     kappa: float = 0.0
     offset: tuple = (0.0, 0.0, 0.0)
     bitrev: bool = False
+    seed: int = 0  # NUDFT locations
 
     def describe(self) -> str:
-        name = {GREEN: "green", DFT: "dft", RADON2D: "radon2d"}[self.kind]
+        name = {GREEN: "green", DFT: "dft", RADON2D: "radon2d", RADON3D: "radon3d", NUDFT: "nudft"}[self.kind]
         return f"{name}(d={self.d}, n={self.n})"
 
 
@@ -49,6 +56,14 @@ def dft(d: int, n: int, bitrev: bool = True) -> KernelSpec:
 
 def radon2d(n: int) -> KernelSpec:
     return KernelSpec(RADON2D, 2, n)
+
+
+def radon3d(n: int) -> KernelSpec:
+    return KernelSpec(RADON3D, 3, n)
+
+
+def nudft(d: int, n: int, seed: int = 1) -> KernelSpec:
+    return KernelSpec(NUDFT, d, n, seed=seed)
 
 
 def level_rule(n: int, cb: int = 8) -> int:

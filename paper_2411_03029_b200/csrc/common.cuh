@@ -198,9 +198,22 @@ struct KSpec {
   int kind, d;
   i64 n;
   int bitrev;
+  unsigned seed;  // NUDFT locations
   double kappa, off0, off1, off2;
-  double inv_n;  // unused for exactness (we divide), kept for layout
 };
+
+// NUDFT target location x^i_k in [0, n-1] (SPEC.md kernels: uniform per
+// coordinate, counter-based from the seed and the flattened index)
+__host__ __device__ __forceinline__ double nudft_loc(unsigned seed, i64 flat, int k, i64 n) {
+  const u64 tags[3] = {0x4EULL, static_cast<u64>(flat), static_cast<u64>(k)};
+  const u64 h = derive_seed(static_cast<u64>(seed), tags, 3);
+  const double u = static_cast<double>(h >> 11) * 0x1.0p-53;
+#ifdef __CUDA_ARCH__
+  return __dmul_rn(u, static_cast<double>(n - 1));
+#else
+  return u * static_cast<double>(n - 1);
+#endif
+}
 
 __device__ __forceinline__ i64 bitrev1(i64 i, i64 n) {
   i64 x = i - 1, r = 0;
@@ -251,6 +264,38 @@ __device__ __forceinline__ double2 kernel_entry(const KSpec& s, const int* i, co
     sincos(__dmul_rn(M_PI, t), &sn, &cs);
     return make_double2(cs, -sn);
   }
+  if (s.kind == OIOBF_KERNEL_RADON3D) {  // exp(2 pi i (x.k + c |k|)), c = (3 + prod sin 2 pi x_p) / 100
+    i64 num = 0;
+    double ss = 1, kk = 0;
+    for (int p = 0; p < 3; ++p) {
+      const double x = __ddiv_rn(static_cast<double>(i[p] - 1), n);
+      const i64 ki = j[p] - 1 - s.n / 2;
+      num += (i[p] - 1) * ki;
+      ss = __dmul_rn(ss, sin(__dmul_rn(2.0 * M_PI, x)));
+      kk = __dadd_rn(kk, __dmul_rn(static_cast<double>(ki), static_cast<double>(ki)));
+    }
+    num %= s.n;
+    if (num < 0) num += s.n;
+    const double c = __ddiv_rn(__dadd_rn(3.0, ss), 100.0);
+    const double phi = __dadd_rn(__ddiv_rn(static_cast<double>(num), n), __dmul_rn(c, __dsqrt_rn(kk)));
+    double sn, cs;
+    sincos(__dmul_rn(2.0 * M_PI, phi), &sn, &cs);
+    return make_double2(cs, sn);
+  }
+  if (s.kind == OIOBF_KERNEL_NUDFT) {  // exp(2 pi i x^i . y^j), y^j_k = (j_k - 1) / n
+    i64 flat = 0, st = 1;
+    for (int p = 0; p < s.d; ++p) {
+      flat += (i[p] - 1) * st;
+      st *= s.n;
+    }
+    double phi = 0;
+    for (int p = 0; p < s.d; ++p)
+      phi = __dadd_rn(phi, __ddiv_rn(__dmul_rn(nudft_loc(s.seed, flat, p, s.n), static_cast<double>(j[p] - 1)), n));
+    phi = __dsub_rn(phi, floor(phi));
+    double sn, cs;
+    sincos(__dmul_rn(2.0 * M_PI, phi), &sn, &cs);
+    return make_double2(cs, sn);
+  }
   // radon 2d
   const double x1 = __ddiv_rn(static_cast<double>(i[0] - 1), n), x2 = __ddiv_rn(static_cast<double>(i[1] - 1), n);
   const i64 k1i = j[0] - 1 - s.n / 2, k2i = j[1] - 1 - s.n / 2;
@@ -276,11 +321,11 @@ inline KSpec kspec_from(const oiobf_kernel_spec& k) {
   s.d = k.d;
   s.n = k.n;
   s.bitrev = k.bitrev;
+  s.seed = k.seed;
   s.kappa = k.kappa;
   s.off0 = k.offset[0];
   s.off1 = k.offset[1];
   s.off2 = k.offset[2];
-  s.inv_n = 1.0 / static_cast<double>(k.n);
   return s;
 }
 

@@ -663,8 +663,10 @@ void build_cores(oiobf_tbf& b) {
 void validate_spec(const oiobf_kernel_spec& s) {
   require(s.d >= 1 && s.d <= kMaxD, "kernel spec: d must be in [1,6]");
   require(s.n >= 1, "kernel spec: n must be positive");
-  require(s.kind >= 0 && s.kind <= 2, "make_kernel: unknown kernel kind");
+  require(s.kind >= 0 && s.kind <= 4, "make_kernel: unknown kernel kind");
   require(s.kind != OIOBF_KERNEL_RADON2D || s.d == 2, "kernel spec: radon2d needs d=2");
+  require(s.kind != OIOBF_KERNEL_RADON3D || s.d == 3, "kernel spec: radon3d needs d=3");
+  require(s.kind != OIOBF_KERNEL_NUDFT || !s.bitrev, "kernel spec: nudft has no bit-reversed ordering");
   require(s.kind != OIOBF_KERNEL_GREEN || s.d <= 3, "kernel spec: green needs d<=3");
   if (s.bitrev) require((s.n & (s.n - 1)) == 0, "reorder_bit_reversal: extent must be a power of two");
 }
@@ -1806,6 +1808,7 @@ void tbf_save(const oiobf_tbf& b, const char* path) {
     w.v<int32_t>(b.spec.d);
     w.v<int64_t>(b.spec.n);
     w.v<int32_t>(b.spec.bitrev);
+    w.v<uint32_t>(b.spec.seed);
     w.v<double>(b.spec.kappa);
     for (int i = 0; i < 3; ++i) w.v<double>(b.spec.offset[i]);
     w.v<int32_t>(b.L);
@@ -1872,6 +1875,7 @@ oiobf_tbf* tbf_load(const char* path) {
     spec.d = r.v<int32_t>();
     spec.n = r.v<int64_t>();
     spec.bitrev = r.v<int32_t>();
+    spec.seed = r.v<uint32_t>();
     spec.kappa = r.v<double>();
     for (int i = 0; i < 3; ++i) spec.offset[i] = r.v<double>();
     const int L = r.v<int32_t>();

@@ -6,7 +6,7 @@ be inspected or applied by another process (the CPU oracle in the tests).
 Little-endian throughout:
 
   "TBF1"  u32 version
-  kernel: i32 kind, i32 d, i64 n, i32 bitrev, f64 kappa, f64 offset[3]
+  kernel: i32 kind, i32 d, i64 n, i32 bitrev, u32 seed, f64 kappa, f64 offset[3]
   i32 L, f64 tol
   proxies: i32 mode, i64 q, i64 max_retries, i64 row_cap;  u64 seed
   per level (V/W l = 0..Lc, then U/P l = 0..Lc), canonical slot order
@@ -80,20 +80,20 @@ class _Buf:
 def read_header(path: str):
     """(KernelSpec, L, tol, proxies, seed) from the first bytes only."""
     with open(path, "rb") as f:
-        head = f.read(4 + 4 + 4 + 4 + 8 + 4 + 8 + 24 + 4 + 8 + 4 + 24 + 8)
+        head = f.read(4 + 4 + 4 + 4 + 8 + 4 + 4 + 8 + 24 + 4 + 8 + 4 + 24 + 8)
     if head[:4] != MAGIC:
         raise ValueError("tbf_load: not a TBF1 file")
     r = _Buf(head)
     r.take(4)
     if r.s("I") != VERSION:
         raise ValueError("tbf_load: unsupported TBF1 version")
-    kind, d, n, bitrev = r.s("i"), r.s("i"), r.s("q"), r.s("i")
+    kind, d, n, bitrev, kseed = r.s("i"), r.s("i"), r.s("q"), r.s("i"), r.s("I")
     kappa = r.s("d")
     offset = tuple(r.s("ddd"))
     L, tol = r.s("i"), r.s("d")
     proxies = (r.s("i"), r.s("q"), r.s("q"), r.s("q"))
     seed = r.s("Q")
-    return KernelSpec(kind, d, n, kappa, offset, bool(bitrev)), L, tol, proxies, seed
+    return KernelSpec(kind, d, n, kappa, offset, bool(bitrev), kseed), L, tol, proxies, seed
 
 
 def read_tbf1(path: str, verify_checksum: bool = True) -> TBF1:
@@ -107,13 +107,13 @@ def read_tbf1(path: str, verify_checksum: bool = True) -> TBF1:
     r.take(4)
     if r.s("I") != VERSION:
         raise ValueError("tbf_load: unsupported TBF1 version")
-    kind, d, n, bitrev = r.s("i"), r.s("i"), r.s("q"), r.s("i")
+    kind, d, n, bitrev, kseed = r.s("i"), r.s("i"), r.s("q"), r.s("i"), r.s("I")
     kappa = r.s("d")
     offset = tuple(r.s("ddd"))
     L, tol = r.s("i"), r.s("d")
     proxies = (r.s("i"), r.s("q"), r.s("q"), r.s("q"))
     seed = r.s("Q")
-    spec = KernelSpec(kind, d, n, kappa, offset, bool(bitrev))
+    spec = KernelSpec(kind, d, n, kappa, offset, bool(bitrev), kseed)
     levels = []
     for _side in range(2):
         for _l in range(L // 2 + 1):

@@ -224,31 +224,36 @@ __device__ __forceinline__ i64 bitrev1(i64 i, i64 n) {
   return r + 1;
 }
 
+// Green geometry, split so row-invariant coordinates can be hoisted:
+// target coordinate p of index i: i / n; source coordinate p: j / n + off_p
+// (modes >= d stay 0 / off_p).  green_from_coords finishes the entry.
+__device__ __forceinline__ double green_x(const KSpec& s, int i) {
+  return __ddiv_rn(static_cast<double>(i), static_cast<double>(s.n));
+}
+__device__ __forceinline__ double green_y(const KSpec& s, int p, int j) {
+  const double off = p == 0 ? s.off0 : p == 1 ? s.off1 : s.off2;
+  return __dadd_rn(__ddiv_rn(static_cast<double>(j), static_cast<double>(s.n)), off);
+}
+__device__ __forceinline__ double2 green_from_coords(const KSpec& s, const double* xs, const double* ys) {
+  const double dx = __dsub_rn(xs[0], ys[0]), dy = __dsub_rn(xs[1], ys[1]), dz = __dsub_rn(xs[2], ys[2]);
+  const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  const double rho = __dsqrt_rn(r2);
+  const double ph = __dmul_rn(s.kappa, rho);
+  double sn, cs;
+  sincos(ph, &sn, &cs);
+  return make_double2(__ddiv_rn(cs, rho), __ddiv_rn(-sn, rho));
+}
+
 // i[], j[]: 1-based multi-indices
 __device__ __forceinline__ double2 kernel_entry(const KSpec& s, const int* i, const int* j) {
   const double n = static_cast<double>(s.n);
   if (s.kind == OIOBF_KERNEL_GREEN) {
-    double xs0 = 0, xs1 = 0, xs2 = 0, ys0 = 0, ys1 = 0, ys2 = 0;
-    xs0 = __ddiv_rn(static_cast<double>(i[0]), n);
-    ys0 = __ddiv_rn(static_cast<double>(j[0]), n);
-    if (s.d > 1) {
-      xs1 = __ddiv_rn(static_cast<double>(i[1]), n);
-      ys1 = __ddiv_rn(static_cast<double>(j[1]), n);
+    double xs[3] = {0, 0, 0}, ys[3] = {s.off0, s.off1, s.off2};
+    for (int p = 0; p < s.d; ++p) {
+      xs[p] = green_x(s, i[p]);
+      ys[p] = green_y(s, p, j[p]);
     }
-    if (s.d > 2) {
-      xs2 = __ddiv_rn(static_cast<double>(i[2]), n);
-      ys2 = __ddiv_rn(static_cast<double>(j[2]), n);
-    }
-    ys0 = __dadd_rn(ys0, s.off0);
-    ys1 = __dadd_rn(ys1, s.off1);
-    ys2 = __dadd_rn(ys2, s.off2);
-    const double dx = __dsub_rn(xs0, ys0), dy = __dsub_rn(xs1, ys1), dz = __dsub_rn(xs2, ys2);
-    const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-    const double rho = __dsqrt_rn(r2);
-    const double ph = __dmul_rn(s.kappa, rho);
-    double sn, cs;
-    sincos(ph, &sn, &cs);
-    return make_double2(__ddiv_rn(cs, rho), __ddiv_rn(-sn, rho));
+    return green_from_coords(s, xs, ys);
   }
   if (s.kind == OIOBF_KERNEL_DFT) {
     i64 acc = 0;

@@ -105,20 +105,32 @@ __device__ __forceinline__ double2 reflect_coeff(const Bcast& b, double2 r, doub
   return cscale(b.tau, s);
 }
 
+// Column k is owned by warp k % kWarps for the whole panel.  Look-ahead: the
+// owner of column j+1 updates that column first in step j and immediately
+// builds reflector j+1 into the other broadcast slot, so its norm reduction
+// and reflector set-up overlap the other warps' updates of step j (one
+// __syncthreads per column; the critical path no longer stalls every warp on
+// a single warp's reduction).
+__device__ __forceinline__ void panel_reflector(double2* __restrict__ R, const double2* __restrict__ X, int w, int j,
+                                                int nrows, int pr, Bcast* slot) {
+  const int lane = threadIdx.x & 31;
+  double sig = 0;
+  for (int i = lane; i < nrows; i += 32) sig += cnorm2(X[i + j * pr]);
+  sig = warp_sum(sig);
+  if (lane == 0) *slot = make_reflector(R[j + j * w], sig, &R[j + j * w]);
+  __syncwarp();
+}
+
 __device__ void absorb_panel(double2* __restrict__ R, double2* __restrict__ X, int w, int nrows, int pr,
                              Bcast* bc) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) panel_reflector(R, X, w, 0, nrows, pr, &bc[0]);
+  __syncthreads();
   for (int j = 0; j < w; ++j) {
-    if (warp == j % kWarps) {
-      double sig = 0;
-      for (int i = lane; i < nrows; i += 32) sig += cnorm2(X[i + j * pr]);
-      sig = warp_sum(sig);
-      if (lane == 0) bc[j & 1] = make_reflector(R[j + j * w], sig, &R[j + j * w]);
-    }
-    __syncthreads();
     const Bcast b = bc[j & 1];
+    const bool owns_next = j + 1 < w && warp == (j + 1) % kWarps;
+    int k0 = j + 1 + ((warp - (j + 1) % kWarps) % kWarps + kWarps) % kWarps;
     if (b.active) {
-      int k0 = j + 1 + ((warp - (j + 1) % kWarps) % kWarps + kWarps) % kWarps;
       for (int k = k0; k < w; k += kWarps) {
         double2 dot = make_double2(0, 0);
         for (int i = lane; i < nrows; i += 32) cfmac(dot, X[i + j * pr], X[i + k * pr]);
@@ -127,10 +139,14 @@ __device__ void absorb_panel(double2* __restrict__ R, double2* __restrict__ X, i
         const double2 t = cmul(b.scale, ws);
         if (lane == 0) R[j + k * w] = csub(R[j + k * w], ws);
         for (int i = lane; i < nrows; i += 32) X[i + k * pr] = csub(X[i + k * pr], cmul(X[i + j * pr], t));
+        __syncwarp();
+        if (k == j + 1) panel_reflector(R, X, w, j + 1, nrows, pr, &bc[(j + 1) & 1]);  // look-ahead
       }
+    } else if (owns_next) {
+      panel_reflector(R, X, w, j + 1, nrows, pr, &bc[(j + 1) & 1]);
     }
+    __syncthreads();
   }
-  __syncthreads();
 }
 
 __global__ void __launch_bounds__(kThreads) k_panel(LevelDesc L, KSpec ks, const int* __restrict__ proxies,
@@ -180,15 +196,47 @@ __global__ void __launch_bounds__(kThreads) k_panel(LevelDesc L, KSpec ks, const
           else jj[p - L.d] = v;
         }
       }
-      for (int c = my_cg; c < w; c += ncg) {
-        double2 e = make_double2(0, 0);
+      if (ks.kind == OIOBF_KERNEL_GREEN) {
+        // row-invariant coordinates once per row; per column only the
+        // unfolded mode's coordinate (same operations as kernel_entry)
+        double xs[3] = {0, 0, 0}, ys[3] = {ks.off0, ks.off1, ks.off2};
         if (valid) {
-          const int t = stgt[c];
-          if (s.skip < L.d) ii[s.skip] = t;
-          else jj[s.skip - L.d] = t;
-          e = kernel_entry(ks, ii, jj);
+#pragma unroll
+          for (int p = 0; p < 3; ++p)
+            if (p < L.d) {
+              if (p != s.skip) xs[p] = green_x(ks, ii[p]);
+              if (p + L.d != s.skip) ys[p] = green_y(ks, p, jj[p]);
+            }
         }
-        X[my_row + c * pr] = e;
+        const int sk = s.skip;
+        for (int c = my_cg; c < w; c += ncg) {
+          double2 e = make_double2(0, 0);
+          if (valid) {
+            const int t = stgt[c];
+            const bool tgt = sk < L.d;
+            const int q = tgt ? sk : sk - L.d;
+            const double v = tgt ? green_x(ks, t) : green_y(ks, q, t);
+            double xc[3], yc[3];
+#pragma unroll
+            for (int p = 0; p < 3; ++p) {
+              xc[p] = (tgt && p == q) ? v : xs[p];
+              yc[p] = (!tgt && p == q) ? v : ys[p];
+            }
+            e = green_from_coords(ks, xc, yc);
+          }
+          X[my_row + c * pr] = e;
+        }
+      } else {
+        for (int c = my_cg; c < w; c += ncg) {
+          double2 e = make_double2(0, 0);
+          if (valid) {
+            const int t = stgt[c];
+            if (s.skip < L.d) ii[s.skip] = t;
+            else jj[s.skip - L.d] = t;
+            e = kernel_entry(ks, ii, jj);
+          }
+          X[my_row + c * pr] = e;
+        }
       }
     }
     __syncthreads();

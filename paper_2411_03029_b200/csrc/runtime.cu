@@ -701,19 +701,27 @@ std::unique_ptr<oiobf_tbf> construct_begin(const oiobf_kernel_spec& spec, int L,
 }
 
 oiobf_tbf* construct(const oiobf_kernel_spec& spec, int L, double tol, const oiobf_proxy_strategy& ps, u64 seed) {
+  static const bool dbg = std::getenv("OIOBF_DEBUG") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  auto t_begin = now();
   auto b = construct_begin(spec, L, tol, ps, seed, 0, 1);
-  auto t_start = std::chrono::steady_clock::now();
+  auto t_start = now();
   for (int sd = 0; sd < 2; ++sd) {
     i64 r_est = 8;
     for (int l = 0; l <= b->Lc; ++l) {
       b->r_est[sd].push_back(r_est);
+      auto t0 = now();
       build_side_level(*b, sd, l, r_est);
+      if (dbg) fprintf(stderr, "[oiobf] construct side %d level %d: %.2f ms\n", sd, l, ms(t0, now()));
       r_est = std::max<i64>(r_est, b->side[sd][static_cast<size_t>(l)].max_rank);
     }
   }
+  auto t1 = now();
   build_cores(*b);
   TBF_CUDA(cudaStreamSynchronize(b->stream));
-  b->t_ms[5] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+  if (dbg) fprintf(stderr, "[oiobf] construct begin %.2f ms, cores %.2f ms\n", ms(t_begin, t_start), ms(t1, now()));
+  b->t_ms[5] = ms(t_start, now());
   return b.release();
 }
 

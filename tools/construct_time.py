@@ -1,0 +1,12 @@
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import time, torch, paper_2411_03029_b200 as tb
+from paper_2411_03029_b200.configs import BY_NAME
+torch.cuda.set_device(0)
+c = BY_NAME["green_cubes_n64"]
+for i in range(3):
+    torch.cuda.synchronize(); t = time.perf_counter()
+    bf = tb.tbf_construct(c.spec, c.L, c.tol, seed=c.seed)
+    torch.cuda.synchronize()
+    print("construct", i, round((time.perf_counter() - t) * 1e3, 1), "ms", bf.timings(), flush=True)
+    del bf

@@ -132,11 +132,17 @@ __global__ void __launch_bounds__(kGemvThreads, 4) k_gemv(const int* __restrict_
           for (int v = 0; v < kAcc; ++v)
             if (v < nv) cfma(acc[v], a[u], sx[v * C + c + u * 32]);
       }
-      for (; c < C; c += 32) {
-        const double2 a0 = ld_stream2(row + c);
+      if (c < C) {  // row tail (< 8 x 32 elements): all its loads in one batch, not one round trip each
+        double2 a[8];
 #pragma unroll
-        for (int v = 0; v < kAcc; ++v)
-          if (v < nv) cfma(acc[v], a0, sx[v * C + c]);
+        for (int u = 0; u < 8; ++u)
+          if (c + u * 32 < C) a[u] = ld_stream2(row + c + u * 32);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c + u * 32 < C)
+#pragma unroll
+            for (int v = 0; v < kAcc; ++v)
+              if (v < nv) cfma(acc[v], a[u], sx[v * C + c + u * 32]);
       }
 #pragma unroll
       for (int v = 0; v < kAcc; ++v)

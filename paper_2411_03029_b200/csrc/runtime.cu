@@ -51,25 +51,36 @@ void require(bool c, const std::string& msg) {
   if (!c) throw InvalidArg(msg);
 }
 
+// Device buffer.  alloc(): cudaMalloc / cudaFree (long-lived arrays).
+// alloc_on(stream): stream-ordered cudaMallocAsync / cudaFreeAsync from the
+// device pool (per-level construction temporaries: no device-wide sync on
+// free, and the pool keeps the memory for the next level).
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  cudaStream_t ast = nullptr;  // set: stream-ordered allocation
+  bool async = false;
   DevBuf() = default;
   explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(size_t count, cudaStream_t st) { alloc_on(count, st); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), ast(o.ast), async(o.async) {
     o.p = nullptr;
     o.n = 0;
+    o.async = false;
   }
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
       reset();
       p = o.p;
       n = o.n;
+      ast = o.ast;
+      async = o.async;
       o.p = nullptr;
       o.n = 0;
+      o.async = false;
     }
     return *this;
   }
@@ -79,10 +90,21 @@ struct DevBuf {
     n = count;
     if (count) TBF_CUDA(cudaMalloc(&p, sizeof(T) * count));
   }
+  void alloc_on(size_t count, cudaStream_t st) {
+    reset();
+    n = count;
+    ast = st;
+    async = true;
+    if (count) TBF_CUDA(cudaMallocAsync(&p, sizeof(T) * count, st));
+  }
   void reset() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (async) cudaFreeAsync(p, ast);
+      else cudaFree(p);
+    }
     p = nullptr;
     n = 0;
+    async = false;
   }
   void upload(const T* h, size_t count, cudaStream_t st) {
     if (count) TBF_CUDA(cudaMemcpyAsync(p, h, sizeof(T) * count, cudaMemcpyHostToDevice, st));
@@ -105,15 +127,31 @@ i64 ipow(i64 b, i64 e) {
   return r;
 }
 
+void keep_pool_memory(int dev) {  // freed stream-ordered memory stays cached in the pool
+  static bool done[64] = {};
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
 void ensure_device() {
   int cnt = 0;
   cudaError_t e = cudaGetDeviceCount(&cnt);
   if (e != cudaSuccess || cnt == 0)
     throw std::runtime_error("no CUDA device available (the B200 path has no CPU fallback)");
   TBF_CUDA(cudaSetDevice(g_device));
-  cudaDeviceProp pr;
-  TBF_CUDA(cudaGetDeviceProperties(&pr, g_device));
-  if (pr.major < 10) throw std::runtime_error("device is not sm_100-class (Blackwell) — this build targets sm_100a");
+  static int checked[64] = {};  // 1: sm_100-class (cudaGetDeviceProperties is slow; query once)
+  if (g_device < 0 || g_device >= 64 || !checked[g_device]) {
+    int major = 0;
+    TBF_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, g_device));
+    if (major < 10) throw std::runtime_error("device is not sm_100-class (Blackwell) — this build targets sm_100a");
+    if (g_device >= 0 && g_device < 64) checked[g_device] = 1;
+  }
+  keep_pool_memory(g_device);
 }
 
 struct EventTimer {
@@ -526,11 +564,11 @@ void build_side_level(oiobf_tbf& b, int sd, int l, i64 r_est) {
     // closed-form narrow IDs (k_narrow_dft): no proxy / panel / R buffers
     ld.width.alloc(static_cast<size_t>(ns));
     ld.rank.alloc(static_cast<size_t>(ns));
-    DevBuf<int> sat(static_cast<size_t>(ns));
+    DevBuf<int> sat(static_cast<size_t>(ns), st);
     ld.perm.alloc(static_cast<size_t>(ns * wmax));
     ld.gaps.alloc(static_cast<size_t>(ns));
-    DevBuf<int> skel_tmp(static_cast<size_t>(ns * wmax));
-    DevBuf<double2> interp_tmp(static_cast<size_t>(ns * wmax * wmax));
+    DevBuf<int> skel_tmp(static_cast<size_t>(ns * wmax), st);
+    DevBuf<double2> interp_tmp(static_cast<size_t>(ns * wmax * wmax), st);
     EventTimer t2(st);
     const LevelData* c = l > 0 ? &b.side[sd][static_cast<size_t>(l - 1)] : nullptr;
     launch_narrow_dft(L, b.ks, b.tol, c ? c->rank.p : nullptr, c ? c->skel_off.p : nullptr, c ? c->skel.p : nullptr,
@@ -539,8 +577,8 @@ void build_side_level(oiobf_tbf& b, int sd, int l, i64 r_est) {
     finish_level(b, ld, sat, skel_tmp, interp_tmp);
     return;
   }
-  DevBuf<int> proxies(static_cast<size_t>(ns * L.psize));
-  DevBuf<int> targets(static_cast<size_t>(ns * wmax));
+  DevBuf<int> proxies(static_cast<size_t>(ns * L.psize), st);
+  DevBuf<int> targets(static_cast<size_t>(ns * wmax), st);
   ld.width.alloc(static_cast<size_t>(ns));
   EventTimer t0(st);
   launch_gen_proxies(L, proxies.p, st);
@@ -551,16 +589,16 @@ void build_side_level(oiobf_tbf& b, int sd, int l, i64 r_est) {
     launch_targets(L, c.rank.p, c.skel_off.p, c.skel.p, targets.p, ld.width.p, st);
   }
   b.t_ms[0] += t0.stop();
-  DevBuf<double2> rpart(static_cast<size_t>(ns * L.nparts * wmax * wmax));
+  DevBuf<double2> rpart(static_cast<size_t>(ns * L.nparts * wmax * wmax), st);
   EventTimer t1(st);
   launch_panel(L, b.ks, proxies.p, targets.p, ld.width.p, rpart.p, st);
   b.t_ms[1] += t1.stop();
   ld.rank.alloc(static_cast<size_t>(ns));
-  DevBuf<int> sat(static_cast<size_t>(ns));
+  DevBuf<int> sat(static_cast<size_t>(ns), st);
   ld.perm.alloc(static_cast<size_t>(ns * wmax));
   ld.gaps.alloc(static_cast<size_t>(ns));
-  DevBuf<int> skel_tmp(static_cast<size_t>(ns * wmax));
-  DevBuf<double2> interp_tmp(static_cast<size_t>(ns * wmax * wmax));
+  DevBuf<int> skel_tmp(static_cast<size_t>(ns * wmax), st);
+  DevBuf<double2> interp_tmp(static_cast<size_t>(ns * wmax * wmax), st);
   EventTimer t2(st);
   launch_finish(L, b.tol, kTieEps, -1, rpart.p, targets.p, ld.width.p, ld.rank.p, sat.p, ld.perm.p, skel_tmp.p,
                 interp_tmp.p, ld.gaps.p, st);

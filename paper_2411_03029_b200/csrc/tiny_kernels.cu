@@ -154,28 +154,28 @@ __global__ void __launch_bounds__(kTinyThreads) k_tiny_level(TinyLevelArgs a, co
       const int sz = s_r[e] * s_w[e];
       for (int q = 0; q < sz; ++q) fm[s_pf[e] + q] = __ldg(mats + s_mo[e] + q);
     }
-  // ---- ... and the input(s): packed first-mode-fastest (or global strides at V0)
+  // ---- ... and the input(s): packed first-mode-fastest (or global strides at V0);
+  // one flat loop over (child, element) so tiny children do not serialize
   {
     const int nsrc = a.side == 0 ? 1 : nch;
-    for (int c = 0; c < nsrc; ++c) {
+    const int xst = a.side == 0 ? s_isv[0] * a.nv : static_cast<int>(a.xstride);
+    for (int e = tid; e < nsrc * xst; e += nth) {
+      const int c = e / xst, loc = e - c * xst;
+      if (loc >= s_isv[c] * a.nv) continue;
       const i64 base = a.side == 0 ? g.io_off : s_go[c];
-      const int xo = a.side == 0 ? 0 : c * static_cast<int>(a.xstride);
-      const int sz = s_isv[c] * a.nv;
-      for (int e = tid; e < sz; e += nth) {
-        int rem = e;
-        i64 addr = base;
-        int st = 1;
-        for (int k = 0; k < d; ++k) {
-          const int ext = s_ie[c * d + k];
-          const int q = rem / ext;
-          const int x = rem - q * ext;
-          rem = q;
-          addr += a.in_global ? x * a.gstride[k] : static_cast<i64>(x * st);
-          st *= ext;
-        }
-        addr += a.in_global ? rem * a.gstride[d] : static_cast<i64>(rem * st);
-        xs[xo + e] = in[addr];
+      int rem = loc;
+      i64 addr = base;
+      int st = 1;
+      for (int k = 0; k < d; ++k) {
+        const int ext = s_ie[c * d + k];
+        const int q = rem / ext;
+        const int x = rem - q * ext;
+        rem = q;
+        addr += a.in_global ? x * a.gstride[k] : static_cast<i64>(x * st);
+        st *= ext;
       }
+      addr += a.in_global ? rem * a.gstride[d] : static_cast<i64>(rem * st);
+      xs[(a.side == 0 ? 0 : c * static_cast<int>(a.xstride)) + loc] = in[addr];
     }
   }
   __syncthreads();

@@ -64,6 +64,9 @@ __global__ void k_mode_product(i64 nitems, const MPStep* __restrict__ steps, i64
   out[out_addr] = acc;
 }
 
+__device__ __forceinline__ void pdl_wait_dep() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger_dep() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 constexpr int kGemvThreads = 256;
 constexpr int kGemvRowsPerCta = 32;
 
@@ -95,11 +98,13 @@ __global__ void __launch_bounds__(kGemvThreads, 4) k_gemv(const int* __restrict_
   extern __shared__ __align__(16) double2 sx[];
   const int nv = NV == 1 ? 1 : nv_rt;
   constexpr int kAcc = NV == 1 ? 1 : 4;
+  pdl_trigger_dep();  // the P/U boxes behind may start their prologue on freed SMs
   const long long g0 = row_begin[blockIdx.x];
   const long long g1 = min(total_rows, row_begin[blockIdx.x + 1]);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int p = cta_pair[blockIdx.x];
   long long g = g0;
+  pdl_wait_dep();  // x (the W outputs) comes from the previous kernel
   while (g < g1) {
     const GemvDesc D = ds[p];
     const long long pend = min(g1, D.cta_off + D.R);  // cta_off holds the pair's first global row
@@ -109,7 +114,7 @@ __global__ void __launch_bounds__(kGemvThreads, 4) k_gemv(const int* __restrict_
       double2 v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (i + u * kGemvThreads < C * nv) v[u] = __ldg(x + D.x_off + i + u * kGemvThreads);
+        if (i + u * kGemvThreads < C * nv) v[u] = x[D.x_off + i + u * kGemvThreads];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         if (i + u * kGemvThreads < C * nv) sx[i + u * kGemvThreads] = v[u];
@@ -225,6 +230,7 @@ __global__ void __launch_bounds__(kTmaThreads) k_gemv_tma(const int* __restrict_
   const long long g1 = min(total_rows, row_begin[blockIdx.x + 1]);
   const int p0 = cta_pair[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_trigger_dep();
   if (threadIdx.x == 0) {
     int np = 0;
     while (np < kTmaMaxPairs) {
@@ -242,10 +248,15 @@ __global__ void __launch_bounds__(kTmaThreads) k_gemv_tma(const int* __restrict_
   }
   __syncthreads();
   const int np = npairs_s;
-  for (int q = 0; q < np; ++q)
-    for (int i = threadIdx.x; i < pd[q].C * nv; i += kTmaThreads) sxs[q * xcap + i] = __ldg(x + pd[q].x_off + i);
-  __syncthreads();
   const long long nrows = g1 - g0;
+  if (warp != kTmaConsumers) {
+    // consumers stage x (the previous kernel's output) while the producer
+    // already streams core rows (independent of the previous kernel)
+    pdl_wait_dep();
+    for (int q = 0; q < np; ++q)
+      for (int i = threadIdx.x; i < pd[q].C * nv; i += 32 * kTmaConsumers) sxs[q * xcap + i] = x[pd[q].x_off + i];
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kTmaConsumers) : "memory");
+  }
   if (warp == kTmaConsumers) {  // producer
     if (lane == 0) {
       int q = 0;
@@ -315,14 +326,24 @@ void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_ro
                  const double2* cores, const double2* x, double2* y, int max_c, cudaStream_t st) {
   if (nctas == 0) return;
   const size_t smem = sizeof(double2) * static_cast<size_t>(max_c) * nv;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(nctas));
+  cfg.blockDim = dim3(kGemvThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   if (nv == 1) {
     TBF_CUDA(cudaFuncSetAttribute(k_gemv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-    k_gemv<1><<<static_cast<unsigned>(nctas), kGemvThreads, smem, st>>>(cta_pair, d, nv, total_rows, row_begin,
-                                                                        cores, x, y);
+    TBF_CUDA(cudaLaunchKernelEx(&cfg, k_gemv<1>, cta_pair, d, nv, static_cast<long long>(total_rows), row_begin, cores,
+                                x, y));
   } else {
     TBF_CUDA(cudaFuncSetAttribute(k_gemv<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-    k_gemv<0><<<static_cast<unsigned>(nctas), kGemvThreads, smem, st>>>(cta_pair, d, nv, total_rows, row_begin,
-                                                                        cores, x, y);
+    TBF_CUDA(cudaLaunchKernelEx(&cfg, k_gemv<0>, cta_pair, d, nv, static_cast<long long>(total_rows), row_begin, cores,
+                                x, y));
   }
   TBF_CUDA(cudaGetLastError());
 }
@@ -333,8 +354,18 @@ void launch_gemv_tma(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 tota
   if (nctas == 0) return;
   const size_t smem = gemv_tma_smem_bytes(stages, stage_elems, xcap);
   TBF_CUDA(cudaFuncSetAttribute(k_gemv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-  k_gemv_tma<<<static_cast<unsigned>(nctas), kTmaThreads, smem, st>>>(cta_pair, d, nv, total_rows, row_begin,
-                                                                      stages, stage_elems, xcap, cores, x, y);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(nctas));
+  cfg.blockDim = dim3(kTmaThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  TBF_CUDA(cudaLaunchKernelEx(&cfg, k_gemv_tma, cta_pair, d, nv, static_cast<long long>(total_rows), row_begin, stages,
+                              stage_elems, xcap, cores, x, y));
   TBF_CUDA(cudaGetLastError());
 }
 

@@ -104,6 +104,13 @@ __global__ void __launch_bounds__(kGemvThreads, 4) k_gemv(const int* __restrict_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int p = cta_pair[blockIdx.x];
   long long g = g0;
+  if (g0 + warp < g1) {  // this warp's first core row into L2 while the previous kernel drains
+    const GemvDesc D0 = ds[p];
+    if (g0 + warp < D0.cta_off + D0.R) {
+      const char* r0 = reinterpret_cast<const char*>(cores + D0.core_off + (g0 + warp - D0.cta_off) * D0.C);
+      for (int o = lane * 128; o < D0.C * 16; o += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(r0 + o));
+    }
+  }
   pdl_wait_dep();  // x (the W outputs) comes from the previous kernel
   while (g < g1) {
     const GemvDesc D = ds[p];

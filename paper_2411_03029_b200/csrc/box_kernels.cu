@@ -118,7 +118,7 @@ __device__ __forceinline__ void first_mode_smem(const double2* __restrict__ xs, 
 #pragma unroll
     for (int i = 0; i < AM; ++i) acc[i] = make_double2(0, 0);
     const double2* col = xs + rs + Rs * ein_f * v;
-#pragma unroll 1
+#pragma unroll 4
     for (int x = 0; x < ein_f; ++x) {
       const double2 v0 = col[x * Rs];
 #pragma unroll
@@ -184,7 +184,7 @@ __device__ __forceinline__ void middle_mode(const double2* __restrict__ src, dou
 #pragma unroll
     for (int g = 0; g < 4; ++g) acc[g] = make_double2(0, 0);
     const double2* s = src + b + B * ein * c;
-#pragma unroll 1
+#pragma unroll 4
     for (int x = 0; x < ein; ++x) {
       const double2 val = s[B * x];
       const double2* m = Mk + x * eo + a0;
@@ -214,7 +214,7 @@ __device__ __forceinline__ void last_mode(const BoxDesc& D, int d, int lo, int A
 #pragma unroll
     for (int g = 0; g < 4; ++g) acc[g] = make_double2(0, 0);
     const double2* s = src + ein * c0;
-#pragma unroll 1
+#pragma unroll 4
     for (int x = 0; x < ein; ++x) {
       const double2 m = M0[x * eo + a];
 #pragma unroll

@@ -111,13 +111,18 @@ __device__ __forceinline__ double2 reflect_coeff(const Bcast& b, double2 r, doub
 // and reflector set-up overlap the other warps' updates of step j (one
 // __syncthreads per column; the critical path no longer stalls every warp on
 // a single warp's reduction).
+// R (w x w upper triangular) is kept packed column by column in shared
+// memory: element (j, k), j <= k, at k (k + 1) / 2 + j -- half the footprint
+// of a full w x w array, which leaves room for taller row panels.
+__device__ __forceinline__ int rpk(int j, int k) { return k * (k + 1) / 2 + j; }
+
 __device__ __forceinline__ void panel_reflector(double2* __restrict__ R, const double2* __restrict__ X, int w, int j,
                                                 int nrows, int pr, Bcast* slot) {
   const int lane = threadIdx.x & 31;
   double sig = 0;
   for (int i = lane; i < nrows; i += 32) sig += cnorm2(X[i + j * pr]);
   sig = warp_sum(sig);
-  if (lane == 0) *slot = make_reflector(R[j + j * w], sig, &R[j + j * w]);
+  if (lane == 0) *slot = make_reflector(R[rpk(j, j)], sig, &R[rpk(j, j)]);
   __syncwarp();
 }
 
@@ -135,9 +140,9 @@ __device__ void absorb_panel(double2* __restrict__ R, double2* __restrict__ X, i
         double2 dot = make_double2(0, 0);
         for (int i = lane; i < nrows; i += 32) cfmac(dot, X[i + j * pr], X[i + k * pr]);
         dot = warp_sum2(dot);
-        const double2 ws = reflect_coeff(b, R[j + k * w], dot);
+        const double2 ws = reflect_coeff(b, R[rpk(j, k)], dot);
         const double2 t = cmul(b.scale, ws);
-        if (lane == 0) R[j + k * w] = csub(R[j + k * w], ws);
+        if (lane == 0) R[rpk(j, k)] = csub(R[rpk(j, k)], ws);
         for (int i = lane; i < nrows; i += 32) X[i + k * pr] = csub(X[i + k * pr], cmul(X[i + j * pr], t));
         __syncwarp();
         if (k == j + 1) panel_reflector(R, X, w, j + 1, nrows, pr, &bc[(j + 1) & 1]);  // look-ahead
@@ -157,8 +162,8 @@ __global__ void __launch_bounds__(kThreads) k_panel(LevelDesc L, KSpec ks, const
   const i64 part = blockIdx.x % L.nparts;
   const int w = width[slot];
   const int pr = L.pr;
-  double2* R = reinterpret_cast<double2*>(smem);
-  double2* X = R + L.wmax * L.wmax;
+  double2* R = reinterpret_cast<double2*>(smem);  // packed upper triangle
+  double2* X = R + L.wmax * (L.wmax + 1) / 2;
   Bcast* bc = reinterpret_cast<Bcast*>(X + static_cast<i64>(pr) * L.wmax);
   int* sprox = reinterpret_cast<int*>(bc + 2);
   int* stgt = sprox + L.psize;
@@ -166,7 +171,7 @@ __global__ void __launch_bounds__(kThreads) k_panel(LevelDesc L, KSpec ks, const
   const int D = 2 * L.d;
   for (int i = threadIdx.x; i < L.psize; i += kThreads) sprox[i] = proxies[slot * L.psize + i];
   for (int i = threadIdx.x; i < w; i += kThreads) stgt[i] = targets[slot * L.wmax + i];
-  for (int i = threadIdx.x; i < w * w; i += kThreads) R[i] = make_double2(0, 0);
+  for (int i = threadIdx.x; i < w * (w + 1) / 2; i += kThreads) R[i] = make_double2(0, 0);
   int cnt[kMaxModes], off[kMaxModes];
   for (int p = 0; p < D; ++p) {
     cnt[p] = L.counts[s.k][p];
@@ -243,7 +248,10 @@ __global__ void __launch_bounds__(kThreads) k_panel(LevelDesc L, KSpec ks, const
     absorb_panel(R, X, w, nrows, pr, bc);
   }
   double2* out = rpart + (slot * L.nparts + part) * L.wmax * L.wmax;
-  for (int i = threadIdx.x; i < w * w; i += kThreads) out[i] = R[i];
+  for (int i = threadIdx.x; i < w * w; i += kThreads) {  // unpack to w x w column-major
+    const int r = i % w, c = i / w;
+    out[i] = r <= c ? R[rpk(r, c)] : make_double2(0, 0);
+  }
 }
 
 // ---------------------------------------------------------------- finish
@@ -499,10 +507,10 @@ __global__ void __launch_bounds__(kThreads) k_matrix_panel(i64 nparts, i64 rpp, 
   const i64 part = blockIdx.x % nparts;
   const int w = ncols[slot];
   const i64 m = mrows[slot];
-  double2* R = reinterpret_cast<double2*>(smem);
-  double2* X = R + wmax * wmax;
+  double2* R = reinterpret_cast<double2*>(smem);  // packed upper triangle
+  double2* X = R + wmax * (wmax + 1) / 2;
   Bcast* bc = reinterpret_cast<Bcast*>(X + static_cast<i64>(pr) * wmax);
-  for (int i = threadIdx.x; i < w * w; i += kThreads) R[i] = make_double2(0, 0);
+  for (int i = threadIdx.x; i < w * (w + 1) / 2; i += kThreads) R[i] = make_double2(0, 0);
   __syncthreads();
   const i64 r_begin = part * rpp;
   i64 r_end = r_begin + rpp;
@@ -518,13 +526,16 @@ __global__ void __launch_bounds__(kThreads) k_matrix_panel(i64 nparts, i64 rpp, 
     absorb_panel(R, X, w, nrows, pr, bc);
   }
   double2* out = rpart + (slot * nparts + part) * wmax * wmax;
-  for (int i = threadIdx.x; i < w * w; i += kThreads) out[i] = R[i];
+  for (int i = threadIdx.x; i < w * w; i += kThreads) {  // unpack to w x w column-major
+    const int r = i % w, c = i / w;
+    out[i] = r <= c ? R[rpk(r, c)] : make_double2(0, 0);
+  }
 }
 
 }  // namespace
 
 size_t panel_smem_bytes(const LevelDesc& L) {
-  return sizeof(double2) * (L.wmax * L.wmax + static_cast<size_t>(L.pr) * L.wmax) + 2 * sizeof(Bcast) +
+  return sizeof(double2) * (L.wmax * (L.wmax + 1) / 2 + static_cast<size_t>(L.pr) * L.wmax) + 2 * sizeof(Bcast) +
          sizeof(int) * (L.psize + L.wmax) + 16;
 }
 
@@ -704,7 +715,7 @@ void launch_compact(i64 nslots, i64 wmax, const int* rank, const int* width, con
 
 void launch_matrix_ids(i64 njobs, const i64* a_off, const i64* m, const int* n, const double2* A, i64 nparts, i64 rpp,
                        int pr, i64 wmax, double2* rpart, cudaStream_t st) {
-  const size_t smem = sizeof(double2) * (wmax * wmax + static_cast<size_t>(pr) * wmax) + 2 * sizeof(Bcast) + 16;
+  const size_t smem = sizeof(double2) * (wmax * (wmax + 1) / 2 + static_cast<size_t>(pr) * wmax) + 2 * sizeof(Bcast) + 16;
   TBF_CUDA(cudaFuncSetAttribute(k_matrix_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   k_matrix_panel<<<static_cast<unsigned>(njobs * nparts), kThreads, smem, st>>>(nparts, rpp, pr, wmax, a_off, m, n, A,
                                                                                rpart);

@@ -513,7 +513,7 @@ LevelDesc make_level(const oiobf_tbf& b, int sd, int l, i64 r_est, i64 wmax) {
     m = rows;
   }
   L.m = m;
-  L.pr = wmax <= 16 ? 256 : wmax <= 32 ? 128 : wmax <= 64 ? 64 : 32;
+  L.pr = wmax <= 16 ? 256 : wmax <= 64 ? 128 : 64;  // R packed: (w(w+1)/2 + pr w) x 16 B fits the 220 KB budget
   L.rank = b.rank;
   L.world = b.world;
   const i64 target_ctas = 148 * 8;
@@ -2607,7 +2607,7 @@ int oiobf_column_id_batch(int64_t batch, const int64_t* m, const int64_t* n, con
     L.nslots = batch;
     L.wmax = wmax;
     L.m = mmax;
-    L.pr = wmax <= 16 ? 256 : wmax <= 32 ? 128 : wmax <= 64 ? 64 : 32;
+    L.pr = wmax <= 16 ? 256 : wmax <= 64 ? 128 : 64;  // R packed: (w(w+1)/2 + pr w) x 16 B fits the 220 KB budget
     if (const char* e = std::getenv("OIOBF_ID_PR")) L.pr = std::atoi(e);  // debug override
     i64 parts = std::max<i64>(1, (148 * 8 + batch - 1) / batch);
     parts = std::min(parts, std::max<i64>(1, (mmax + 4 * L.pr - 1) / (4 * L.pr)));

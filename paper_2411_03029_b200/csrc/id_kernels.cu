@@ -126,6 +126,48 @@ __device__ __forceinline__ void panel_reflector(double2* __restrict__ R, const d
   __syncwarp();
 }
 
+// apply reflector j (broadcast b) to trailing column k: R(j, k) and X(:, k)
+__device__ __forceinline__ void reflect_col(const Bcast& b, double2* __restrict__ R, double2* __restrict__ X, int j,
+                                            int k, int nrows, int pr, int lane) {
+  double2 dot = make_double2(0, 0);
+  for (int i = lane; i < nrows; i += 32) cfmac(dot, X[i + j * pr], X[i + k * pr]);
+  dot = warp_sum2(dot);
+  const double2 ws = reflect_coeff(b, R[rpk(j, k)], dot);
+  const double2 t = cmul(b.scale, ws);
+  if (lane == 0) R[rpk(j, k)] = csub(R[rpk(j, k)], ws);
+  for (int i = lane; i < nrows; i += 32) X[i + k * pr] = csub(X[i + k * pr], cmul(X[i + j * pr], t));
+}
+
+// two columns at once: the two dot products and shuffle reductions interleave
+// (independent dependency chains), halving the per-step latency of wide panels
+__device__ __forceinline__ void reflect_col2(const Bcast& b, double2* __restrict__ R, double2* __restrict__ X, int j,
+                                             int k1, int k2, int nrows, int pr, int lane) {
+  double2 d1 = make_double2(0, 0), d2 = make_double2(0, 0);
+  for (int i = lane; i < nrows; i += 32) {
+    const double2 xj = X[i + j * pr];
+    cfmac(d1, xj, X[i + k1 * pr]);
+    cfmac(d2, xj, X[i + k2 * pr]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    d1.x += __shfl_xor_sync(0xffffffffu, d1.x, o);
+    d1.y += __shfl_xor_sync(0xffffffffu, d1.y, o);
+    d2.x += __shfl_xor_sync(0xffffffffu, d2.x, o);
+    d2.y += __shfl_xor_sync(0xffffffffu, d2.y, o);
+  }
+  const double2 w1 = reflect_coeff(b, R[rpk(j, k1)], d1), w2 = reflect_coeff(b, R[rpk(j, k2)], d2);
+  const double2 t1 = cmul(b.scale, w1), t2 = cmul(b.scale, w2);
+  if (lane == 0) {
+    R[rpk(j, k1)] = csub(R[rpk(j, k1)], w1);
+    R[rpk(j, k2)] = csub(R[rpk(j, k2)], w2);
+  }
+  for (int i = lane; i < nrows; i += 32) {
+    const double2 xj = X[i + j * pr];
+    X[i + k1 * pr] = csub(X[i + k1 * pr], cmul(xj, t1));
+    X[i + k2 * pr] = csub(X[i + k2 * pr], cmul(xj, t2));
+  }
+}
+
 __device__ void absorb_panel(double2* __restrict__ R, double2* __restrict__ X, int w, int nrows, int pr,
                              Bcast* bc) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -134,19 +176,16 @@ __device__ void absorb_panel(double2* __restrict__ R, double2* __restrict__ X, i
   for (int j = 0; j < w; ++j) {
     const Bcast b = bc[j & 1];
     const bool owns_next = j + 1 < w && warp == (j + 1) % kWarps;
-    int k0 = j + 1 + ((warp - (j + 1) % kWarps) % kWarps + kWarps) % kWarps;
+    int k = j + 1 + ((warp - (j + 1) % kWarps) % kWarps + kWarps) % kWarps;
     if (b.active) {
-      for (int k = k0; k < w; k += kWarps) {
-        double2 dot = make_double2(0, 0);
-        for (int i = lane; i < nrows; i += 32) cfmac(dot, X[i + j * pr], X[i + k * pr]);
-        dot = warp_sum2(dot);
-        const double2 ws = reflect_coeff(b, R[rpk(j, k)], dot);
-        const double2 t = cmul(b.scale, ws);
-        if (lane == 0) R[rpk(j, k)] = csub(R[rpk(j, k)], ws);
-        for (int i = lane; i < nrows; i += 32) X[i + k * pr] = csub(X[i + k * pr], cmul(X[i + j * pr], t));
+      if (owns_next) {  // look-ahead column first, then its reflector
+        reflect_col(b, R, X, j, k, nrows, pr, lane);
         __syncwarp();
-        if (k == j + 1) panel_reflector(R, X, w, j + 1, nrows, pr, &bc[(j + 1) & 1]);  // look-ahead
+        panel_reflector(R, X, w, j + 1, nrows, pr, &bc[(j + 1) & 1]);
+        k += kWarps;
       }
+      for (; k + kWarps < w; k += 2 * kWarps) reflect_col2(b, R, X, j, k, k + kWarps, nrows, pr, lane);
+      if (k < w) reflect_col(b, R, X, j, k, nrows, pr, lane);
     } else if (owns_next) {
       panel_reflector(R, X, w, j + 1, nrows, pr, &bc[(j + 1) & 1]);
     }

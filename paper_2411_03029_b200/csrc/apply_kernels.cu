@@ -144,17 +144,20 @@ __global__ void __launch_bounds__(kGemvThreads, 4) k_gemv(const int* __restrict_
           for (int v = 0; v < kAcc; ++v)
             if (v < nv) cfma(acc[v], a[u], sx[v * C + c + u * 32]);
       }
-      if (c < C) {  // row tail (< 8 x 32 elements): all its loads in one batch, not one round trip each
-        double2 a[8];
+      if (c < C) {  // row tail (< 8 x 32 elements): its loads in batches of 4, not one round trip each
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (c + u * 32 < C) a[u] = ld_stream2(row + c + u * 32);
+        for (int h = 0; h < 8; h += 4) {
+          double2 a[4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (c + u * 32 < C)
+          for (int u = 0; u < 4; ++u)
+            if (c + (h + u) * 32 < C) a[u] = ld_stream2(row + c + (h + u) * 32);
 #pragma unroll
-            for (int v = 0; v < kAcc; ++v)
-              if (v < nv) cfma(acc[v], a[u], sx[v * C + c + u * 32]);
+          for (int u = 0; u < 4; ++u)
+            if (c + (h + u) * 32 < C)
+#pragma unroll
+              for (int v = 0; v < kAcc; ++v)
+                if (v < nv) cfma(acc[v], a[u], sx[v * C + c + (h + u) * 32]);
+        }
       }
 #pragma unroll
       for (int v = 0; v < kAcc; ++v)

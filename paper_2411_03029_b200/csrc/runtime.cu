@@ -310,9 +310,11 @@ struct Plan {
 int split_rows(const Plan& pl, i64 begin, i64 end, i64 nct, std::vector<i64>& rb, std::vector<int>& map) {
   // cost of a row = its C elements + a fixed per-row overhead (warp reduction,
   // row setup, the dependent load batches of one warp), in element units.
-  // Measured on B200 (config 2): pure bytes (K = 0) 96 us, K = 64 92 us,
-  // K >= 1024 (about equal rows) 87 us.  OIOBF_GEMV_ROW_COST overrides.
-  static const i64 K = std::getenv("OIOBF_GEMV_ROW_COST") ? std::atoll(std::getenv("OIOBF_GEMV_ROW_COST")) : 1024;
+  // Measured on B200: config 2 (C ~ 64..1000) graph 89.5 us at K = 0, ~85 us
+  // for K in [128, 1024]; config 5 (C ~ 256..2400) GEMV 14.2 ms at K = 0,
+  // 14.4 ms at K = 256, 15.7 ms at K = 1024, 19.1 ms row-balanced.
+  // OIOBF_GEMV_ROW_COST overrides.
+  static const i64 K = std::getenv("OIOBF_GEMV_ROW_COST") ? std::atoll(std::getenv("OIOBF_GEMV_ROW_COST")) : 256;
   auto cost = [&](i64 q) { return static_cast<i64>(pl.gemv[static_cast<size_t>(q)].C) + K; };
   i64 E = 0;
   for (i64 q = begin; q < end; ++q) E += pl.gemv[static_cast<size_t>(q)].R * cost(q);

@@ -168,8 +168,10 @@ __device__ __forceinline__ void reflect_col2(const Bcast& b, double2* __restrict
   }
 }
 
+template <int NW>  // warps in the CTA (columns are owned round-robin)
 __device__ void absorb_panel(double2* __restrict__ R, double2* __restrict__ X, int w, int nrows, int pr,
                              Bcast* bc) {
+  constexpr int kWarps = NW;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) panel_reflector(R, X, w, 0, nrows, pr, &bc[0]);
   __syncthreads();
@@ -193,7 +195,10 @@ __device__ void absorb_panel(double2* __restrict__ R, double2* __restrict__ X, i
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_panel(LevelDesc L, KSpec ks, const int* __restrict__ proxies,
+// NT threads: 256, or 512 for wide IDs (w > 32, one CTA per SM by shared
+// memory) so each column step spreads over 16 warps
+template <int NT>
+__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 3) k_panel(LevelDesc L, KSpec ks, const int* __restrict__ proxies,
                                                     const int* __restrict__ targets, const int* __restrict__ width,
                                                     double2* __restrict__ rpart) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -208,9 +213,9 @@ __global__ void __launch_bounds__(kThreads) k_panel(LevelDesc L, KSpec ks, const
   int* stgt = sprox + L.psize;
   const SlotPos s = decode_slot(L, slot);
   const int D = 2 * L.d;
-  for (int i = threadIdx.x; i < L.psize; i += kThreads) sprox[i] = proxies[slot * L.psize + i];
-  for (int i = threadIdx.x; i < w; i += kThreads) stgt[i] = targets[slot * L.wmax + i];
-  for (int i = threadIdx.x; i < w * (w + 1) / 2; i += kThreads) R[i] = make_double2(0, 0);
+  for (int i = threadIdx.x; i < L.psize; i += NT) sprox[i] = proxies[slot * L.psize + i];
+  for (int i = threadIdx.x; i < w; i += NT) stgt[i] = targets[slot * L.wmax + i];
+  for (int i = threadIdx.x; i < w * (w + 1) / 2; i += NT) R[i] = make_double2(0, 0);
   int cnt[kMaxModes], off[kMaxModes];
   for (int p = 0; p < D; ++p) {
     cnt[p] = L.counts[s.k][p];
@@ -221,7 +226,7 @@ __global__ void __launch_bounds__(kThreads) k_panel(LevelDesc L, KSpec ks, const
   const i64 r_begin = part * L.rpp;
   i64 r_end = r_begin + L.rpp;
   if (r_end > L.m) r_end = L.m;
-  const int ncg = kThreads / pr;  // column groups per row
+  const int ncg = NT / pr;  // column groups per row
   const int my_row = threadIdx.x % pr, my_cg = threadIdx.x / pr;
   for (i64 r0 = r_begin; r0 < r_end; r0 += pr) {
     const int nrows = static_cast<int>((r_end - r0) < pr ? (r_end - r0) : pr);
@@ -284,10 +289,10 @@ __global__ void __launch_bounds__(kThreads) k_panel(LevelDesc L, KSpec ks, const
       }
     }
     __syncthreads();
-    absorb_panel(R, X, w, nrows, pr, bc);
+    absorb_panel<NT / 32>(R, X, w, nrows, pr, bc);
   }
   double2* out = rpart + (slot * L.nparts + part) * L.wmax * L.wmax;
-  for (int i = threadIdx.x; i < w * w; i += kThreads) {  // unpack to w x w column-major
+  for (int i = threadIdx.x; i < w * w; i += NT) {  // unpack to w x w column-major
     const int r = i % w, c = i / w;
     out[i] = r <= c ? R[rpk(r, c)] : make_double2(0, 0);
   }
@@ -562,7 +567,7 @@ __global__ void __launch_bounds__(kThreads) k_matrix_panel(i64 nparts, i64 rpp, 
       X[i + c * pr] = i < nrows ? a[r0 + i + static_cast<i64>(c) * m] : make_double2(0, 0);
     }
     __syncthreads();
-    absorb_panel(R, X, w, nrows, pr, bc);
+    absorb_panel<kWarps>(R, X, w, nrows, pr, bc);
   }
   double2* out = rpart + (slot * nparts + part) * wmax * wmax;
   for (int i = threadIdx.x; i < w * w; i += kThreads) {  // unpack to w x w column-major
@@ -599,9 +604,14 @@ void launch_targets(const LevelDesc& L, const int* crank, const i64* cskel_off, 
 void launch_panel(const LevelDesc& L, const KSpec& ks, const int* proxies, const int* targets, const int* width,
                   double2* rpart, cudaStream_t st) {
   const size_t smem = panel_smem_bytes(L);
-  TBF_CUDA(cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  TBF_CUDA(cudaFuncSetAttribute(k_panel<kThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   const i64 grid = L.nslots * L.nparts;
-  k_panel<<<static_cast<unsigned>(grid), kThreads, smem, st>>>(L, ks, proxies, targets, width, rpart);
+  if (L.wmax > 32) {
+    TBF_CUDA(cudaFuncSetAttribute(k_panel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    k_panel<512><<<static_cast<unsigned>(grid), 512, smem, st>>>(L, ks, proxies, targets, width, rpart);
+  } else {
+    k_panel<kThreads><<<static_cast<unsigned>(grid), kThreads, smem, st>>>(L, ks, proxies, targets, width, rpart);
+  }
   TBF_CUDA(cudaGetLastError());
 }
 

@@ -90,7 +90,7 @@ __device__ __forceinline__ double2 ld_stream2(const double2* p) {
 // each warp walks whole rows with 8 independent 16-B streaming loads per lane
 // in flight; a row is read once and applied to all nv vectors.
 template <int NV>  // NV = 1: single-vector fast path; NV = 0: generic nv
-__global__ void __launch_bounds__(kGemvThreads, 4) k_gemv(const int* __restrict__ cta_pair,
+__global__ void __launch_bounds__(kGemvThreads, NV == 1 ? 4 : 2) k_gemv(const int* __restrict__ cta_pair,
                                                        const GemvDesc* __restrict__ ds, int nv_rt, long long total_rows,
                                                        const long long* __restrict__ row_begin,
                                                        const double2* __restrict__ cores,
@@ -112,70 +112,71 @@ __global__ void __launch_bounds__(kGemvThreads, 4) k_gemv(const int* __restrict_
     }
   }
   pdl_wait_dep();  // x (the W outputs) comes from the previous kernel
-  while (g < g1) {
-    const GemvDesc D = ds[p];
-    const long long pend = min(g1, D.cta_off + D.R);  // cta_off holds the pair's first global row
-    const int C = D.C;
-    // stage x (C * nv) with independent loads
-    for (int i = threadIdx.x; i < C * nv; i += kGemvThreads * 4) {
-      double2 v[4];
+  // vectors in chunks of kAcc: x of one chunk staged at a time (shared memory
+  // bounded by C_max * kAcc for any nv); a row is read once per chunk
+  for (int v0 = 0; v0 < nv; v0 += kAcc) {
+    const int nvc = min(kAcc, nv - v0);
+    g = g0;
+    p = cta_pair[blockIdx.x];
+    while (g < g1) {
+      const GemvDesc D = ds[p];
+      const long long pend = min(g1, D.cta_off + D.R);  // cta_off holds the pair's first global row
+      const int C = D.C;
+      const double2* xs = x + D.x_off + static_cast<long long>(v0) * C;
+      // stage x (C * nvc) with independent loads
+      for (int i = threadIdx.x; i < C * nvc; i += kGemvThreads * 4) {
+        double2 v[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (i + u * kGemvThreads < C * nv) v[u] = x[D.x_off + i + u * kGemvThreads];
+        for (int u = 0; u < 4; ++u)
+          if (i + u * kGemvThreads < C * nvc) v[u] = xs[i + u * kGemvThreads];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (i + u * kGemvThreads < C * nv) sx[i + u * kGemvThreads] = v[u];
-    }
-    __syncthreads();
-    for (long long gr = g + warp; gr < pend; gr += kGemvThreads / 32) {
-      const int r = static_cast<int>(gr - D.cta_off);
-      const double2* row = cores + D.core_off + static_cast<long long>(r) * C;
-      double2 acc[kAcc];
-#pragma unroll
-      for (int v = 0; v < kAcc; ++v) acc[v] = make_double2(0, 0);
-      int c = lane;
-      for (; c + 7 * 32 < C; c += 8 * 32) {
-        double2 a[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] = ld_stream2(row + c + u * 32);
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-#pragma unroll
-          for (int v = 0; v < kAcc; ++v)
-            if (v < nv) cfma(acc[v], a[u], sx[v * C + c + u * 32]);
+        for (int u = 0; u < 4; ++u)
+          if (i + u * kGemvThreads < C * nvc) sx[i + u * kGemvThreads] = v[u];
       }
-      if (c < C) {  // row tail (< 8 x 32 elements): its loads in batches of 4, not one round trip each
+      __syncthreads();
+      for (long long gr = g + warp; gr < pend; gr += kGemvThreads / 32) {
+        const int r = static_cast<int>(gr - D.cta_off);
+        const double2* row = cores + D.core_off + static_cast<long long>(r) * C;
+        double2 acc[kAcc];
 #pragma unroll
-        for (int h = 0; h < 8; h += 4) {
-          double2 a[4];
+        for (int v = 0; v < kAcc; ++v) acc[v] = make_double2(0, 0);
+        int c = lane;
+        for (; c + 7 * 32 < C; c += 8 * 32) {
+          double2 a[8];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (c + (h + u) * 32 < C) a[u] = ld_stream2(row + c + (h + u) * 32);
+          for (int u = 0; u < 8; ++u) a[u] = ld_stream2(row + c + u * 32);
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (c + (h + u) * 32 < C)
+          for (int u = 0; u < 8; ++u)
 #pragma unroll
-              for (int v = 0; v < kAcc; ++v)
-                if (v < nv) cfma(acc[v], a[u], sx[v * C + c + (h + u) * 32]);
+            for (int v = 0; v < kAcc; ++v)
+              if (v < nvc) cfma(acc[v], a[u], sx[v * C + c + u * 32]);
         }
-      }
+        if (c < C) {  // row tail (< 8 x 32 elements): its loads in batches of 4, not one round trip each
 #pragma unroll
-      for (int v = 0; v < kAcc; ++v)
-        if (v < nv) {
-          const double2 t = warp_sum2(acc[v]);
-          if (lane == 0) y[D.y_off + r + static_cast<long long>(v) * D.R] = t;
+          for (int h = 0; h < 8; h += 4) {
+            double2 a[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (c + (h + u) * 32 < C) a[u] = ld_stream2(row + c + (h + u) * 32);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (c + (h + u) * 32 < C)
+#pragma unroll
+                for (int v = 0; v < kAcc; ++v)
+                  if (v < nvc) cfma(acc[v], a[u], sx[v * C + c + (h + u) * 32]);
+          }
         }
-      // nv > 4: remaining vectors re-read the row (rare path)
-      for (int v = kAcc; v < nv; ++v) {
-        double2 t = make_double2(0, 0);
-        for (int cc = lane; cc < C; cc += 32) cfma(t, ld_stream2(row + cc), sx[v * C + cc]);
-        t = warp_sum2(t);
-        if (lane == 0) y[D.y_off + r + static_cast<long long>(v) * D.R] = t;
+#pragma unroll
+        for (int v = 0; v < kAcc; ++v)
+          if (v < nvc) {
+            const double2 t = warp_sum2(acc[v]);
+            if (lane == 0) y[D.y_off + r + static_cast<long long>(v0 + v) * D.R] = t;
+          }
       }
+      __syncthreads();
+      g = pend;
+      ++p;
     }
-    __syncthreads();
-    g = pend;
-    ++p;
   }
 }
 
@@ -335,7 +336,7 @@ void launch_mode_product(i64 nitems, const MPStep* steps, i64 total_out, const B
 void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, const i64* row_begin, int nv,
                  const double2* cores, const double2* x, double2* y, int max_c, cudaStream_t st) {
   if (nctas == 0) return;
-  const size_t smem = sizeof(double2) * static_cast<size_t>(max_c) * nv;
+  const size_t smem = sizeof(double2) * static_cast<size_t>(max_c) * (nv == 1 ? 1 : std::min(nv, 4));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(nctas));
   cfg.blockDim = dim3(kGemvThreads);
@@ -388,7 +389,7 @@ int gemv_tma_max_pairs() { return kTmaMaxPairs; }
 
 int gemv_ctas_per_sm(int nv, int max_c) {
   int n = 0;
-  const size_t smem = sizeof(double2) * static_cast<size_t>(max_c) * nv;
+  const size_t smem = sizeof(double2) * static_cast<size_t>(max_c) * (nv == 1 ? 1 : std::min(nv, 4));
   if (nv == 1) {
     TBF_CUDA(cudaFuncSetAttribute(k_gemv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     TBF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gemv<1>, kGemvThreads, smem));

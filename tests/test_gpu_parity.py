@@ -185,6 +185,20 @@ def test_catalog_dense_accuracy(name, spec, tol, L):
         assert err <= 10 * tol, f"{name}: sampled relative error {err:.3e} > 10*tol"
 
 
+@pytest.mark.parametrize("nv", [9, 16])
+def test_multi_rhs_matches_single_vectors(nv):
+    """n_v > 4 right-hand sides (vector chunks of 4 in the GEMV, nv as an extra
+    box mode): every column equals the single-vector contraction."""
+    spec = green_cubes(32)
+    bf = tb.tbf_construct(spec, 2, 1e-6, seed=2)
+    rng = np.random.default_rng(nv)
+    F = rand_c(rng, (32, 32, 32, nv))
+    G = bf.contract(F)
+    for v in range(nv):
+        g1 = bf.contract(np.ascontiguousarray(F[..., v]))
+        assert rel(G[..., v], g1) < 1e-13, (v, rel(G[..., v], g1))
+
+
 def test_contract_zero_and_linearity():
     spec = green_plates(32)
     bf = tb.tbf_construct(spec, 2, 1e-6, seed=1)

@@ -3,9 +3,17 @@
 //                   U-bar steps (tensor.cpp:136-166 semantics, one launch per
 //                   (level, mode) covering every (tau, s) or (t, nu) item)
 //   k_gemv          middle-level core contraction G_{t,s} = K(tbar,sbar) F_{t,s}
-//                   (id.cpp:321 pattern): HBM-bound stream of the cores, one
-//                   warp per core row, 16-B loads, F_{t,s} staged in SMEM
-//   k_sum_children  ordered accumulation G_{t,p_nu} = sum_nu (...) (Alg. 2 l. 203)
+//                   (id.cpp:321 pattern): HBM-bound stream of the cores; a
+//                   persistent grid whose CTA row ranges come from a cost
+//                   model (row length + per-row overhead), one warp per core
+//                   row with 8 independent 16-B streaming loads per lane,
+//                   F_{t,s} staged in SMEM (vectors in chunks of 4 for n_v > 1);
+//                   programmatic dependent launch: each warp's first row is
+//                   prefetched into L2 before waiting for the W boxes
+//   k_gemv_tma      variant for long rows: cp.async.bulk ring, producer warp
+//                   streams cores before the dependency wait
+//   k_sum_children  ordered accumulation G_{t,p_nu} = sum_nu (...) (Alg. 2 l. 203),
+//                   fallback path only (box plans fold it into staging)
 #include "kernels.h"
 
 namespace tbf {
@@ -68,7 +76,6 @@ __device__ __forceinline__ void pdl_wait_dep() { asm volatile("griddepcontrol.wa
 __device__ __forceinline__ void pdl_trigger_dep() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
 constexpr int kGemvThreads = 256;
-constexpr int kGemvRowsPerCta = 32;
 
 __device__ __forceinline__ double4 ld_stream(const double4* p) {
   double4 r;
@@ -406,6 +413,5 @@ void launch_sum_children(i64 n, const SumDesc* d, i64 total, const double2* in, 
   TBF_CUDA(cudaGetLastError());
 }
 
-int gemv_rows_per_cta() { return kGemvRowsPerCta; }
 
 }  // namespace tbf

@@ -26,7 +26,6 @@
 #include "kernels.h"
 
 namespace tbf {
-int gemv_rows_per_cta();
 void launch_subtensor(const KSpec& ks, const i64* counts_h, const int* lists, i64 total, double2* out,
                       cudaStream_t st);
 void launch_matrix_ids(i64 njobs, const i64* a_off, const i64* m, const int* n, const double2* A, i64 nparts, i64 rpp,

@@ -84,3 +84,28 @@ def test_compute_fails_loudly_without_device(lib):
     with pytest.raises(Exception):
         tb.tbf_construct(green_plates(32), 2, 1e-6, seed=1)
     assert lib.oiobf_last_error()  # an error message is recorded, not a silent fallback
+
+
+def test_new_entry_points_reject_bad_arguments(lib, tmp_path):
+    """TBF1 load and the apply-engine selector validate their arguments before
+    touching a device (std::invalid_argument -> OIOBF_EINVAL)."""
+    import ctypes as C
+    h = C.c_void_p()
+    assert lib.oiobf_tbf_load(str(tmp_path / "missing.tbf1").encode(), C.byref(h)) == 1
+    assert b"cannot open" in lib.oiobf_last_error()
+    bad = tmp_path / "bad.tbf1"
+    bad.write_bytes(b"NOPE" + bytes(64))
+    assert lib.oiobf_tbf_load(str(bad).encode(), C.byref(h)) == 1
+    assert b"not a TBF1 file" in lib.oiobf_last_error()
+    assert lib.oiobf_tbf_set_apply_engine(None, 1) == 1
+    assert lib.oiobf_tbf_save(None, b"x") == 1
+
+
+def test_tbf1_header_reader_rejects_garbage(tmp_path):
+    from paper_2411_03029_b200.tbf1 import read_header, read_tbf1
+    p = tmp_path / "g.tbf1"
+    p.write_bytes(b"TBF2" + bytes(200))
+    with pytest.raises(ValueError):
+        read_header(str(p))
+    with pytest.raises(ValueError):
+        read_tbf1(str(p))

@@ -264,11 +264,27 @@ def run_b200(args):
         t = time.perf_counter()
         _lib.check(L.oiobf_tbf_contract(bf.handle, Fv, Gv, args.nv))
         e2e_times.append(time.perf_counter() - t)
-    e2e_ms = 1e3 * statistics.fmean(e2e_times)
+    sync_ms = 1e3 * statistics.fmean(e2e_times)
+    # stream-ordered calls back to back (oiobf_tbf_contract_async): every call
+    # still copies its F in and its G out, but the H2D of call k+1 overlaps the
+    # contraction of call k and the D2H of call k-1.  No L2 flush between
+    # calls: one call's working set (cores + F + G) is larger than the L2.
+    s_e2e = torch.cuda.Stream()
+    for _ in range(8):
+        bf.contract_async(Fv, Gv, args.nv, s_e2e.cuda_stream)
+    s_e2e.synchronize()
     if ws > 1:
-        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        torch.distributed.barrier()
+    a_steps = max(e2e_steps, 200)
+    t = time.perf_counter()
+    for _ in range(a_steps):
+        bf.contract_async(Fv, Gv, args.nv, s_e2e.cuda_stream)
+    s_e2e.synchronize()
+    e2e_ms = 1e3 * (time.perf_counter() - t) / a_steps
+    if ws > 1:
+        t = torch.tensor([e2e_ms, sync_ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        e2e_ms, sync_ms = float(t[0].item()), float(t[1].item())
     e2e_value = N * ws / (e2e_ms / 1e3)
     # sanity: host result equals the device result
     dres = Gt.cpu().numpy()
@@ -307,8 +323,14 @@ def run_b200(args):
                    "l2": "flushed (256 MiB write) before every timed step",
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
         "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step": 16 * N,
-                "d2h_bytes_per_step": 16 * N, "steps": e2e_steps, "warmup_calls": nw,
-                "api": "oiobf_tbf_contract (pinned host F/G; copies pipelined over slab groups)"},
+                "d2h_bytes_per_step": 16 * N, "steps": a_steps, "warmup_calls": nw,
+                "api": "oiobf_tbf_contract_async (pinned host F/G, calls back to back on one stream: the H2D "
+                       "of call k+1 overlaps the contraction of call k and the D2H of call k-1)",
+                "timing": "wall clock over all calls, stream synchronised on both sides; no L2 flush "
+                          "(a call's working set exceeds the 126 MB L2)",
+                "sync_call": {"value": N * ws / (sync_ms / 1e3), "ms_per_step": sync_ms,
+                              "api": "oiobf_tbf_contract (one synchronous call per step, L2 flushed before "
+                                     "each; copies pipelined over slab groups inside the call)"}},
         "gpu_launches": int(stats["launches"]) * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "kernel": "k_gemv (middle-level core contraction)",

@@ -115,6 +115,15 @@ int oiobf_tbf_destroy(oiobf_tbf* h);
  * F, G: n^d x nv complex, first mode fastest.  Includes H2D/D2H copies. */
 int oiobf_tbf_contract(oiobf_tbf* h, const double* F, double* G, int64_t nv);
 
+/* Stream-ordered tbf_contract with PINNED host buffers: enqueues H2D(F) ->
+ * contraction -> D2H(G) on the handle's copy / compute streams, makes `stream`
+ * (cudaStream_t, NULL = legacy default) wait for the result, and returns.
+ * Two calls per (handle, nv) can be in flight with their own device staging,
+ * so the H2D of one call overlaps the contraction of the previous one and the
+ * D2H of the one before (PCIe is full duplex).  F must stay unmodified and G
+ * unread until `stream` reaches this point.  Pageable F or G: error. */
+int oiobf_tbf_contract_async(oiobf_tbf* h, const double* F, double* G, int64_t nv, void* stream);
+
 /* Same with device buffers (double2*), enqueued on `stream` (cudaStream_t,
  * NULL = legacy default).  Replays a captured CUDA graph after the first call
  * for a given (nv, F, G, stream). */

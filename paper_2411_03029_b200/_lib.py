@@ -44,6 +44,7 @@ EXPORTS = [
     "oiobf_tbf_shard_begin", "oiobf_tbf_shard_level", "oiobf_tbf_umid_info", "oiobf_tbf_umid_export",
     "oiobf_tbf_umid_import", "oiobf_tbf_set_exchange", "oiobf_tbf_contract_phase",
     "oiobf_tbf_set_apply_engine", "oiobf_tbf_apply_engine", "oiobf_tbf_save", "oiobf_tbf_load",
+    "oiobf_tbf_contract_async",
 ]
 
 _lock = threading.Lock()
@@ -75,6 +76,7 @@ def load(path: str = LIB_PATH):
         L.oiobf_tbf_destroy.argtypes = [C.c_void_p]
         L.oiobf_tbf_contract.argtypes = [C.c_void_p, f64p, f64p, C.c_int64]
         L.oiobf_tbf_contract_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+        L.oiobf_tbf_contract_async.argtypes = [C.c_void_p, f64p, f64p, C.c_int64, C.c_void_p]
         L.oiobf_tbf_memory.argtypes = [C.c_void_p, i64p]
         L.oiobf_tbf_set_apply_engine.argtypes = [C.c_void_p, C.c_int32]
         L.oiobf_tbf_save.argtypes = [C.c_void_p, C.c_char_p]

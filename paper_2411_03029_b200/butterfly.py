@@ -272,14 +272,23 @@ class TensorButterfly:
         _lib.check(_lib.load().oiobf_tbf_save(self._h, str(path).encode()))
 
     def set_apply_engine(self, engine: str) -> None:
-        """'auto' | 'box' | 'tiny' (tiny: thread-per-output engine for d = 6 scale)."""
-        code = {"auto": 0, "box": 1, "tiny": 2}[engine]
+        """'auto' | 'box' | 'tiny' | 'flow'.  box: one fused-box launch per level
+        (CUDA graph); tiny: thread-per-output engine for d = 6 scale; flow: one
+        persistent dataflow launch (items wait on their producers' flags)."""
+        code = {"auto": 0, "box": 1, "tiny": 2, "flow": 3}[engine]
         _lib.check(_lib.load().oiobf_tbf_set_apply_engine(self._h, code))
 
     def apply_engine(self) -> str:
         e = C.c_int32(0)
         _lib.check(_lib.load().oiobf_tbf_apply_engine(self._h, C.byref(e)))
-        return {1: "box", 2: "tiny"}[e.value]
+        return {1: "box", 2: "tiny", 3: "flow"}[e.value]
+
+    def contract_async(self, F: np.ndarray, G: np.ndarray, nv: int = 1, stream: int = 0) -> None:
+        """Stream-ordered contraction with PINNED host buffers (float64 views of
+        complex128 data, e.g. ``torch.empty(..., pin_memory=True).numpy()``):
+        enqueues H2D -> contraction -> D2H and returns; `stream` (cudaStream_t)
+        waits for G.  Consecutive calls overlap their copies and compute."""
+        _lib.check(_lib.load().oiobf_tbf_contract_async(self._h, F, G, nv, C.c_void_p(stream)))
 
     def contract_device(self, dF: int, dG: int, nv: int = 1, stream: int = 0) -> None:
         """Device pointers (double2*) already in HBM; enqueued on `stream`."""

@@ -1,0 +1,397 @@
+// Device code of one fused box contraction (Alg. 2, 185,
+// 201, 203; reference mode_product_blockdiag tensor.cpp:136-166 semantics),
+// shared by the per-level kernel k_box (box_kernels.cu) and the persistent
+// dataflow kernel k_flow (flow_kernels.cu): both run the same arithmetic in
+// the same order, so the two engines agree bit for bit.
+//
+// One box is
+//   out = in x_{d-1} M_{d-1} ... x_1 M_1 x_0 M_0      (M_k^T on the P/U side)
+// handled by cs CTAs that split the OUTPUT rows of mode d-1 (the first mode
+// contracted): every CTA needs the whole input box but no partial sums are
+// exchanged.  Per CTA:
+//   prologue  this CTA's factor rows -> shared memory, stored [x][a] (a
+//             fastest); independent of the producer of the input, so it runs
+//             before the dependency wait (PDL in k_box, item flags in k_flow)
+//   stage     input box -> shared memory: one cp.async.bulk per contiguous
+//             mode-0 row (mbarrier completion); for the ordered sum of P-level
+//             child contributions, batched register loads (8 children in
+//             flight) summed in ascending child order
+//   mode d-1  thread per input column, this CTA's A output rows in registers
+//   modes d-2..1  smem -> smem, 4 output rows per thread-task
+//   mode 0    4 columns per thread-task, written straight to global memory
+//             (consecutive threads = consecutive rows of mode 0: coalesced)
+// The code is latency/issue bound (boxes are small); the layout choices above
+// minimise instructions per useful FMA.  32-bit index math inside a box.
+#pragma once
+
+#include "kernels.h"
+
+namespace tbf {
+namespace {
+
+constexpr int kBoxThreads = 256;
+
+// n / d for 0 <= n < 2^24, d >= 1: float reciprocal estimate (off by at most
+// one in that range) plus one integer correction; no division subroutine.
+__device__ __forceinline__ int qdiv(int n, int d) {
+  int q = __float2int_rz(__fdividef(static_cast<float>(n), static_cast<float>(d)));
+  const int r = n - q * d;
+  q += (r >= d) - (r < 0);
+  return q;
+}
+
+template <class T>
+__device__ __forceinline__ void copy_desc(T* dst, const T* src) {
+  static_assert(sizeof(T) % 8 == 0, "descriptor must be 8-byte sized");
+  const long long* s = reinterpret_cast<const long long*>(src);
+  long long* d = reinterpret_cast<long long*>(dst);
+  for (int i = threadIdx.x; i < static_cast<int>(sizeof(T) / 8); i += blockDim.x) d[i] = s[i];
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Loads of data another CTA of the SAME kernel may have produced (k_flow):
+// L2-coherent (.cg, no L1 allocation); plain loads otherwise.
+template <bool kCoh>
+__device__ __forceinline__ double2 ld_in(const double2* p) {
+  if (kCoh) {
+    double2 r;
+    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p) : "memory");
+    return r;
+  }
+  return *p;
+}
+
+// address of mode-0 row `row` of the box (row = index over modes 1..d-1, nv)
+__device__ __forceinline__ long long row_addr(const BoxDesc& D, int d, int row) {
+  int rem = row;
+  long long a = D.in_off;
+  for (int p = 1; p < d; ++p) {
+    const int q = qdiv(rem, D.ein[p]);
+    a += static_cast<long long>(rem - q * D.ein[p]) * D.in_stride[p];
+    rem = q;
+  }
+  return a + static_cast<long long>(rem) * D.in_stride[d];
+}
+
+// mode d-1 from the staged input: t0[rs + Rs (i + A v)] = sum_x X(rs, x, v) M(i, x)
+// (AM = register bucket >= A; the code is kept small on purpose: these CTAs
+// are short and a cold instruction cache is their largest stall)
+template <int AM>
+__device__ __forceinline__ void first_mode_smem(const double2* __restrict__ xs, const double2* __restrict__ Mf,
+                                                double2* __restrict__ t0, int A, int Rs, int ein_f, int nv) {
+  const int R = Rs * nv;
+  for (int r = threadIdx.x; r < R; r += kBoxThreads) {
+    const int v = qdiv(r, Rs), rs = r - v * Rs;
+    double2 acc[AM];
+#pragma unroll
+    for (int i = 0; i < AM; ++i) acc[i] = make_double2(0, 0);
+    const double2* col = xs + rs + Rs * ein_f * v;
+#pragma unroll 4
+    for (int x = 0; x < ein_f; ++x) {
+      const double2 v0 = col[x * Rs];
+#pragma unroll
+      for (int i = 0; i < AM; ++i)
+        if (i < A) cfma(acc[i], v0, Mf[x * A + i]);
+    }
+#pragma unroll
+    for (int i = 0; i < AM; ++i)
+      if (i < A) t0[rs + Rs * (i + A * v)] = acc[i];
+  }
+}
+
+// mode d-1 streamed from global memory (input box too large to stage)
+template <int AM, bool kCoh>
+__device__ __forceinline__ void first_mode_global(const BoxDesc& D, int d, const double2* in,
+                                                  const double2* __restrict__ Mf, double2* __restrict__ t0, int A,
+                                                  int Rs, int ein_f, int nv) {
+  const int f = d - 1;
+  const int R = Rs * nv;
+  const long long sf = D.in_stride[f];
+  for (int r = threadIdx.x; r < R; r += kBoxThreads) {
+    const int v = qdiv(r, Rs), rs = r - v * Rs;
+    int rem = rs;
+    long long addr = D.in_off + static_cast<long long>(v) * D.in_stride[d];
+    for (int p = 0; p < f; ++p) {
+      const int q = qdiv(rem, D.ein[p]);
+      addr += static_cast<long long>(rem - q * D.ein[p]) * D.in_stride[p];
+      rem = q;
+    }
+    double2 acc[AM];
+#pragma unroll
+    for (int i = 0; i < AM; ++i) acc[i] = make_double2(0, 0);
+#pragma unroll 1
+    for (int x0 = 0; x0 < ein_f; x0 += 4) {
+      double2 val[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (x0 + u < ein_f) val[u] = ld_in<kCoh>(in + addr + (x0 + u) * sf);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (x0 + u < ein_f)
+#pragma unroll
+          for (int i = 0; i < AM; ++i)
+            if (i < A) cfma(acc[i], val[u], Mf[(x0 + u) * A + i]);
+    }
+#pragma unroll
+    for (int i = 0; i < AM; ++i)
+      if (i < A) t0[rs + Rs * (i + A * v)] = acc[i];
+  }
+}
+
+// middle mode k: dst(b, a, c) = sum_x M(a, x) src(b, x, c), 4 output rows per task
+__device__ __forceinline__ void middle_mode(const double2* __restrict__ src, double2* __restrict__ dst,
+                                            const double2* __restrict__ Mk, int B, int ein, int eo, int Cc) {
+  const int ng = (eo + 3) >> 2;
+  const int ntask = B * ng * Cc;
+  for (int t = threadIdx.x; t < ntask; t += kBoxThreads) {
+    const int q1 = qdiv(t, B), b = t - q1 * B;
+    const int c = qdiv(q1, ng), ag = q1 - c * ng;
+    const int a0 = ag * 4;
+    const int na = min(4, eo - a0);
+    double2 acc[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) acc[g] = make_double2(0, 0);
+    const double2* s = src + b + B * ein * c;
+#pragma unroll 4
+    for (int x = 0; x < ein; ++x) {
+      const double2 val = s[B * x];
+      const double2* m = Mk + x * eo + a0;
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+        if (g < na) cfma(acc[g], val, m[g]);
+    }
+    double2* o = dst + b + B * (a0 + eo * c);
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+      if (g < na) o[B * g] = acc[g];
+  }
+}
+
+// global offset (modes 1..d-1, nv) of output column c = (a_1 .. a_{d-2}, i, v)
+__device__ __forceinline__ long long col_offset(const BoxDesc& D, int d, int lo, int A, int c) {
+  const int f = d - 1;
+  int rem = c;
+  long long addr = 0;
+  for (int p = 1; p < f; ++p) {
+    const int q = qdiv(rem, D.eout[p]);
+    addr += static_cast<long long>(rem - q * D.eout[p]) * D.out_stride[p];
+    rem = q;
+  }
+  const int v = qdiv(rem, A), i = rem - v * A;
+  return addr + static_cast<long long>(lo + i) * D.out_stride[f] + static_cast<long long>(v) * D.out_stride[d];
+}
+
+constexpr int kColTab = 512;  // output columns whose offsets are tabulated in shared memory
+
+// mode 0 -> global: task (a, 4 consecutive columns); column c = (a_1 .. a_{d-2}, i, v)
+// tab: per-column offsets (Cc <= kColTab), or null (computed per store)
+__device__ __forceinline__ void last_mode(const BoxDesc& D, int d, int lo, int A, const double2* __restrict__ src,
+                                          const double2* __restrict__ M0, int Cc, const long long* tab,
+                                          double2* __restrict__ out) {
+  const int ein = D.ein[0], eo = D.eout[0];
+  const int ncg = (Cc + 3) >> 2;
+  const int ntask = eo * ncg;
+  for (int t = threadIdx.x; t < ntask; t += kBoxThreads) {
+    const int cg = qdiv(t, eo), a = t - cg * eo;
+    const int c0 = cg * 4;
+    const int nc = min(4, Cc - c0);
+    double2 acc[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) acc[g] = make_double2(0, 0);
+    const double2* s = src + ein * c0;
+#pragma unroll 4
+    for (int x = 0; x < ein; ++x) {
+      const double2 m = M0[x * eo + a];
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+        if (g < nc) cfma(acc[g], s[x + ein * g], m);
+    }
+    const long long base = D.out_off + static_cast<long long>(a) * D.out_stride[0];
+    if (tab) {
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+        if (g < nc) out[base + tab[c0 + g]] = acc[g];
+    } else {
+#pragma unroll 1
+      for (int g = 0; g < nc; ++g)
+        out[base + col_offset(D, d, lo, A, c0 + g)] = g == 0 ? acc[0] : g == 1 ? acc[1] : g == 2 ? acc[2] : acc[3];
+    }
+  }
+}
+
+// Shared-memory state of one box CTA besides the dynamic buffer.
+struct BoxSmem {
+  BoxDesc D;
+  long long coltab[kColTab];  // output column offsets of mode 0's stores
+  int mo[kMaxD + 1];
+  unsigned long long bar;  // staging mbarrier (initialised once per CTA)
+};
+
+// One CTA's share (crank of info.cs) of the box whose descriptor is already
+// in S.D (all threads synchronised after the copy).  `wait` blocks until the
+// input is produced (all threads call it; it ends with a CTA barrier).
+// `phase` is the staging mbarrier's parity, flipped on each bulk staging.
+// `stamp(slot)` is the optional debug timeline hook.
+template <bool kCoh, class Wait, class Stamp>
+__device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, int crank,
+                                         const double2* __restrict__ mats, const double2* in, double2* out,
+                                         double2* sm, unsigned& phase, Wait wait, Stamp stamp) {
+  const BoxDesc& D = S.D;
+  const int tid = threadIdx.x;
+  const int cs = info.cs;
+  const int d = info.d, f = d - 1, nv = info.nv, tr = info.transpose;
+  const int ef = D.eout[f];
+  const int lo = qdiv(crank * ef, cs), hi = qdiv((crank + 1) * ef, cs);
+  const int A = hi - lo;  // 0 <= A <= 8 (host)
+  if (A <= 0) {           // narrow box: nothing left for this CTA (k_flow never issues one)
+    wait();
+    return;
+  }
+  int Rs = 1;  // columns of mode d-1 (modes 0..d-2); times nv below
+  for (int p = 0; p < f; ++p) Rs *= D.ein[p];
+  const int ein_f = D.ein[f];
+  const int e0n = D.ein[0];
+  const int total_in = Rs * ein_f * nv;
+  // bulk staging needs contiguous 16-B rows (every double2 row qualifies)
+  const bool bulk = info.stage && D.nsum == 1 && D.in_stride[0] == 1;
+  if (tid == 0) {
+    S.mo[0] = 0;
+    for (int k = 0; k < d; ++k) S.mo[k + 1] = S.mo[k] + D.ein[k] * (k == f ? A : D.eout[k]);
+    if (bulk) mbar_expect_tx(&S.bar, static_cast<unsigned>(total_in) * 16u);
+  }
+  __syncthreads();
+  double2* smat = sm;
+  double2* xs = smat + info.smem_mat;
+  double2* t0 = xs + info.smem_in;
+  double2* t1 = t0 + info.smem_t;
+  // ---- prologue: factor rows, [x][a] with a fastest (mode d-1: rows lo..hi)
+  for (int k = 0; k < d; ++k) {
+    const int ein = D.ein[k], eo = k == f ? A : D.eout[k], a0 = k == f ? lo : 0;
+    const int mrows = tr ? ein : D.eout[k];  // stored matrix: r x w column-major
+    const double2* M = mats + D.mat_off[k];
+    double2* Sm = smat + S.mo[k];
+    for (int q = tid; q < ein * eo; q += kBoxThreads) {
+      const int x = qdiv(q, eo), a = q - x * eo + a0;
+      Sm[q] = __ldg(M + (tr ? x + mrows * a : a + mrows * x));
+    }
+  }
+  // ---- the input box is produced by an earlier launch / item
+  stamp(1);
+  wait();
+  stamp(2);
+  if (info.stage) {
+    const int nrows = total_in / e0n;
+    if (bulk) {
+      const unsigned rbytes = static_cast<unsigned>(e0n) * 16u;
+      for (int row = tid; row < nrows; row += kBoxThreads)
+        bulk_g2s(xs + row * e0n, in + row_addr(D, d, row), rbytes, &S.bar);
+      mbar_wait(&S.bar, phase);
+      phase ^= 1u;
+    } else if (D.nsum == 1) {
+      const long long s0 = D.in_stride[0];
+      for (int row = tid; row < nrows; row += kBoxThreads) {
+        const long long ra = row_addr(D, d, row);
+        for (int x = 0; x < e0n; ++x) cp_async16(xs + row * e0n + x, in + ra + x * s0);
+      }
+      cp_async_wait_all();
+    } else {
+      // ordered child sums (ascending child), 8 children of loads in flight
+      const long long s0 = D.in_stride[0];
+      const long long cstr = D.sum_stride;
+#pragma unroll 1
+      for (int e = tid; e < total_in; e += kBoxThreads) {
+        const int row = qdiv(e, e0n);
+        const double2* p = in + row_addr(D, d, row) + (e - row * e0n) * s0;
+        double2 acc = make_double2(0, 0);
+#pragma unroll 1
+        for (int c0 = 0; c0 < D.nsum; c0 += 8) {
+          double2 v[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            if (c0 + c < D.nsum) v[c] = ld_in<kCoh>(p + (c0 + c) * cstr);
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            if (c0 + c < D.nsum) acc = (c0 + c == 0) ? v[c] : cadd(acc, v[c]);
+        }
+        xs[e] = acc;
+      }
+    }
+  }
+  __syncthreads();
+  stamp(3);
+  // ---- mode d-1: column r = rs + Rs * v  ->  t0[rs + Rs * (i + A * v)]
+  {
+    // (the row count is dispatched to its register bucket: no predicated-off
+    // FMAs; one bucket is hot per launch, so the i-cache footprint stays)
+    const double2* Mf = smat + S.mo[f];
+    if (info.stage) {
+      if (info.amax <= 2) first_mode_smem<2>(xs, Mf, t0, A, Rs, ein_f, nv);
+      else if (info.amax <= 4) first_mode_smem<4>(xs, Mf, t0, A, Rs, ein_f, nv);
+      else first_mode_smem<8>(xs, Mf, t0, A, Rs, ein_f, nv);
+    } else {
+      first_mode_global<8, kCoh>(D, d, in, Mf, t0, A, Rs, ein_f, nv);
+    }
+  }
+  __syncthreads();
+  stamp(4);
+  // ---- modes d-2 .. 1 (smem -> smem); extents: e[p] = ein (p <= k), eout (k < p < f), A (f), nv
+  double2* src = t0;
+  double2* dst = t1;
+  int Cc = A * nv;  // product of the extents above the current mode
+  for (int k = f - 1; k >= 1; --k) {
+    const int ein = D.ein[k], eo = D.eout[k];
+    int B = 1;
+    for (int p = 0; p < k; ++p) B *= D.ein[p];
+    middle_mode(src, dst, smat + S.mo[k], B, ein, eo, Cc);
+    __syncthreads();
+    Cc *= eo;
+    double2* tmp = src;
+    src = dst;
+    dst = tmp;
+  }
+  // output column offsets of mode 0's stores (computed once, not per store)
+  const bool tab = Cc <= kColTab;
+  if (tab)
+    for (int c = tid; c < Cc; c += kBoxThreads) S.coltab[c] = col_offset(D, d, lo, A, c);
+  __syncthreads();
+  stamp(5);
+  // ---- mode 0 -> global
+  last_mode(D, d, lo, A, src, smat + S.mo[0], Cc, tab ? S.coltab : nullptr, out);
+  __syncthreads();
+  stamp(6);
+}
+
+}  // namespace
+}  // namespace tbf

@@ -249,6 +249,89 @@ def test_host_pipeline_paths_agree(name, spec, tol, L):
         np.testing.assert_array_equal(pg, first)  # pageable: same plan, no graph
 
 
+@pytest.mark.parametrize("name,spec,tol,L", CASES[:4], ids=[c[0] for c in CASES[:4]])
+def test_contract_async_in_flight(name, spec, tol, L):
+    """oiobf_tbf_contract_async: six calls in flight on one stream (distinct
+    inputs, alternating device slots, the last two sharing one output buffer)
+    give the device path's G bit for bit; pageable buffers are refused."""
+    import torch
+    bf = tb.tbf_construct(spec, L, tol, seed=5)
+    rng = np.random.default_rng(12)
+    N = spec.n ** spec.d
+    for nv in (1, 2):
+        Fs = [rng.standard_normal(2 * N * nv) for _ in range(6)]
+        refs = []
+        for F in Fs:
+            dF = torch.from_numpy(F).cuda()
+            dG = torch.empty_like(dF)
+            bf.contract_device(dF.data_ptr(), dG.data_ptr(), nv, 0)
+            torch.cuda.synchronize()
+            refs.append(dG.cpu().numpy())
+        hF = [torch.from_numpy(F).pin_memory() for F in Fs]
+        hG = [torch.zeros(2 * N * nv, dtype=torch.float64).pin_memory() for _ in range(5)]
+        s = torch.cuda.Stream()
+        for i in range(6):
+            bf.contract_async(hF[i].numpy(), hG[min(i, 4)].numpy(), nv, s.cuda_stream)
+            if i == 4:
+                s.synchronize()
+                np.testing.assert_array_equal(hG[4].numpy(), refs[4])
+        s.synchronize()
+        for i in range(4):
+            np.testing.assert_array_equal(hG[i].numpy(), refs[i])
+        np.testing.assert_array_equal(hG[4].numpy(), refs[5])
+    with pytest.raises(ValueError, match="pinned"):
+        bf.contract_async(Fs[0], np.zeros_like(Fs[0]), 2, 0)
+
+
+@pytest.mark.parametrize("name,spec,tol,L", CASES, ids=[c[0] for c in CASES])
+def test_flow_engine_matches_box_engine(oracle, name, spec, tol, L):
+    """The persistent dataflow engine (one launch, items wait on completion
+    flags): same G as the per-level box engine to rounding and within 1e-10 of
+    the oracle on the same factors; 20 device replays bit-identical (no races);
+    the host-buffer variant (slab flags raised by the copy stream, G written
+    straight to mapped pinned memory) bit-identical to the device variant."""
+    import torch
+    from paper_2411_03029_b200 import _lib
+    bf = tb.tbf_construct(spec, L, tol, seed=3)
+    bf.set_apply_engine("flow")
+    if bf.apply_engine() != "flow":
+        bf.set_apply_engine("auto")
+        pytest.skip("plan not eligible for the flow engine (mode-product levels or d = 1)")
+    tbo = oracle.tbf_construct(spec, L, tol, seed=3, replay=bf.export())
+    rng = np.random.default_rng(11)
+    N = spec.n ** spec.d
+    Lb = _lib.load()
+    for nv in (1, 3):
+        F = rng.standard_normal(2 * N * nv)
+        dF = torch.from_numpy(F).cuda()
+        dG = torch.empty_like(dF)
+        bf.set_apply_engine("box")
+        bf.contract_device(dF.data_ptr(), dG.data_ptr(), nv, 0)
+        torch.cuda.synchronize()
+        gbox = dG.cpu().numpy()
+        bf.set_apply_engine("flow")
+        first = None
+        for _ in range(20):
+            dG.zero_()
+            bf.contract_device(dF.data_ptr(), dG.data_ptr(), nv, 0)
+            torch.cuda.synchronize()
+            got = dG.cpu().numpy()
+            if first is None:
+                first = got
+            np.testing.assert_array_equal(got, first)
+        assert rel(first, gbox) < 1e-13, f"flow vs box {rel(first, gbox)}"
+        Fc = F.view(np.complex128).reshape((spec.n,) * spec.d + ((nv,) if nv > 1 else ()), order="F")
+        ref = tbo.contract(Fc).reshape(-1, order="F").view(np.float64)
+        assert rel(first, ref) < 1e-10
+        hF = torch.from_numpy(F).pin_memory()
+        hG = torch.zeros_like(hF).pin_memory()
+        for _ in range(3):  # graph capture, then replays
+            hG.zero_()
+            _lib.check(Lb.oiobf_tbf_contract(bf.handle, hF.numpy(), hG.numpy(), nv))
+            np.testing.assert_array_equal(hG.numpy(), first)
+    bf.set_apply_engine("auto")
+
+
 @pytest.mark.parametrize("name,spec,tol,L", CASES, ids=[c[0] for c in CASES])
 def test_tiny_engine_matches_box_engine_and_oracle(oracle, name, spec, tol, L):
     """The tiny-box apply engine (thread per output, d = 6 scale) on every

@@ -16,10 +16,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="green_cubes_n64")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--construct-only", action="store_true")
+ap.add_argument("--engine", default="auto")
 a = ap.parse_args()
 cfg = BY_NAME[a.config]
 torch.cuda.set_device(0)
 bf = tb.tbf_construct(cfg.spec, cfg.L, cfg.tol, seed=cfg.seed)
+bf.set_apply_engine(a.engine)
 if not a.construct_only:
     rng = np.random.default_rng(0)
     F = torch.from_numpy(rng.standard_normal(2 * cfg.points)).cuda()

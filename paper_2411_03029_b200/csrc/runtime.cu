@@ -274,7 +274,7 @@ struct FlowPlan {
 // (contract_host_async): device staging, its captured compute graph, and the
 // events that order reuse of the slot against the previous call that used it
 struct AsyncSet {
-  DevBuf<double2> F, G;
+  DevBuf<double2> F, G, scratch;  // own scratch: the two slots' contractions may overlap
   cudaEvent_t in = nullptr, done = nullptr, out = nullptr;  // H2D landed / compute done / D2H done
   cudaGraphExec_t gexec = nullptr;
   bool used = false;
@@ -501,9 +501,18 @@ struct oiobf_tbf {
   // host-buffer contraction pipeline: copy-in / copy-out streams and the
   // events that order them against the compute stream (created on first use)
   cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaStream_t s_cmp[2] = {nullptr, nullptr};  // compute streams of the two async slots
   std::vector<cudaEvent_t> ev;
+  // every stream of the handle idle (before plans and their buffers go away)
+  void sync_all() {
+    for (cudaStream_t x : {stream, s_in, s_out, s_cmp[0], s_cmp[1]})
+      if (x) cudaStreamSynchronize(x);
+  }
   ~oiobf_tbf() {
+    sync_all();
     plans.clear();
+    for (cudaStream_t x : {s_cmp[0], s_cmp[1]})
+      if (x) cudaStreamDestroy(x);
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
     if (s_in) cudaStreamDestroy(s_in);
     if (s_out) cudaStreamDestroy(s_out);
@@ -1954,6 +1963,7 @@ struct OpBuffers {
   double2* G = nullptr;
   double2* send = nullptr;
   const double2* recv = nullptr;
+  double2* scratch = nullptr;  // null: the plan's own scratch
 };
 
 // phase: 0 = whole contraction, 1 = V/W + core GEMV, 2 = P/U (sharded, or
@@ -1963,10 +1973,11 @@ void run_ops(oiobf_tbf& b, Plan& pl, const OpBuffers& io, cudaStream_t st, int g
   // OIOBF_ABLATE=<digits>: skip these op kinds (timing experiments only; the
   // result is wrong when set)
   static const char* ablate = std::getenv("OIOBF_ABLATE");
+  double2* const scr = io.scratch ? io.scratch : pl.scratch.p;
   auto in_ptr = [&](int id) -> const double2* {
-    return id == BUF_F ? io.F : id == BUF_RECV ? io.recv : pl.scratch.p;
+    return id == BUF_F ? io.F : id == BUF_RECV ? io.recv : scr;
   };
-  auto out_ptr = [&](int id) -> double2* { return id == BUF_G ? io.G : id == BUF_SEND ? io.send : pl.scratch.p; };
+  auto out_ptr = [&](int id) -> double2* { return id == BUF_G ? io.G : id == BUF_SEND ? io.send : scr; };
   for (const Op& op : pl.ops) {
     if (group_filter >= 0 && op.group != group_filter) continue;
     if (phase == 1 && op.group == 2) continue;
@@ -1979,16 +1990,16 @@ void run_ops(oiobf_tbf& b, Plan& pl, const OpBuffers& io, cudaStream_t st, int g
       launch_mode_product(m.nsteps, pl.d_steps.p + m.step_begin, m.total_out, pl.d_blks.p, ld.interp.p,
                           in_ptr(m.in_buf), out_ptr(m.out_buf), st);
     } else if (op.kind == 1) {
-      double2* y = pl.sharded ? io.send : pl.scratch.p;
+      double2* y = pl.sharded ? io.send : scr;
       const GemvLaunch& gl = pl.gemvs[static_cast<size_t>(op.idx)];
       const GemvDesc* gd = pl.d_gemv.p + gl.desc_begin;
       if (gl.tma)
         launch_gemv_tma(pl.d_tma_map.p + gl.tma_map_begin, gd, gl.tma_ctas, gl.total_rows,
                         pl.d_gemv_rb.p + gl.tma_rb_begin, static_cast<int>(pl.nv), gl.tma_stages,
-                        gl.tma_stage_elems, gl.tma_xcap, b.cores.p, pl.scratch.p, y, st);
+                        gl.tma_stage_elems, gl.tma_xcap, b.cores.p, scr, y, st);
       else
         launch_gemv(pl.d_gemv_map.p + gl.map_begin, gd, gl.ctas, gl.total_rows, pl.d_gemv_rb.p + gl.rb_begin,
-                    static_cast<int>(pl.nv), b.cores.p, pl.scratch.p, y, gl.max_c, st);
+                    static_cast<int>(pl.nv), b.cores.p, scr, y, gl.max_c, st);
     } else if (op.kind == 6) {
       const Plan::TinyLevel& tl = pl.tiny_levels[static_cast<size_t>(op.idx)];
       const LevelData& ld = b.side[tl.side][static_cast<size_t>(tl.l)];
@@ -1997,7 +2008,7 @@ void run_ops(oiobf_tbf& b, Plan& pl, const OpBuffers& io, cudaStream_t st, int g
     } else if (op.kind == 7) {
       const GemvLaunch& gl = pl.gemvs[static_cast<size_t>(op.idx)];
       launch_tiny_gemv(pl.d_gemv.p + gl.desc_begin, gl.ndesc, gl.total_rows, static_cast<int>(pl.nv), b.cores.p,
-                       pl.scratch.p, pl.scratch.p, st);
+                       scr, scr, st);
     } else if (op.kind == 3) {
       const BoxLaunch& bx = pl.boxes[static_cast<size_t>(op.idx)];
       const LevelData& ld = b.side[bx.side][static_cast<size_t>(bx.level)];
@@ -2005,7 +2016,7 @@ void run_ops(oiobf_tbf& b, Plan& pl, const OpBuffers& io, cudaStream_t st, int g
                  out_ptr(bx.out_buf), st);
     } else {
       const SumLaunch& s = pl.sum_launches[static_cast<size_t>(op.idx)];
-      launch_sum_children(s.n, pl.d_sums.p + s.begin, s.total, pl.scratch.p, pl.scratch.p, st);
+      launch_sum_children(s.n, pl.d_sums.p + s.begin, s.total, scr, scr, st);
     }
   }
 }
@@ -2020,13 +2031,17 @@ void run_ops(oiobf_tbf& b, Plan& pl, const double2* F, double2* G, cudaStream_t 
 bool is_pinned(const void* p);
 
 // the plan's launches for (F, G) captured into an instantiated graph
-cudaGraphExec_t capture_ops(oiobf_tbf& b, Plan& pl, const double2* F, double2* G) {
+cudaGraphExec_t capture_ops(oiobf_tbf& b, Plan& pl, const double2* F, double2* G, double2* scratch = nullptr) {
   cudaStream_t cap;
   TBF_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
   cudaGraph_t g;
   TBF_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
   try {
-    run_ops(b, pl, F, G, cap);
+    OpBuffers io;
+    io.F = F;
+    io.G = G;
+    io.scratch = scratch;
+    run_ops(b, pl, io, cap);
   } catch (...) {
     cudaStreamEndCapture(cap, &g);
     cudaStreamDestroy(cap);
@@ -2089,14 +2104,16 @@ void contract_device(oiobf_tbf& b, const double2* F, double2* G, i64 nv, cudaStr
 }
 
 // Stream-ordered host-buffer contraction (pinned F and G): slot k of the plan
-//   copy-in stream   [slot's previous compute done] H2D F -> slot.F   -> in
-//   compute stream   wait in, [slot's previous D2H done]; graph        -> done
-//   copy-out stream  wait done; D2H slot.G -> G                         -> out
-//   caller's stream  waits out
+//   copy-in stream     [slot's previous compute done] H2D F -> slot.F  -> in
+//   slot's compute     wait in, [slot's previous D2H done]; graph       -> done
+//   copy-out stream    wait done; D2H slot.G -> G                        -> out
+//   caller's stream    waits out
 // Consecutive calls alternate slots, so the H2D of call k+1 overlaps the
-// contraction of call k and the D2H of call k-1 (PCIe is full duplex); the
-// caller's stream is never waited on before the copies (F is host memory the
-// caller has finished writing when it makes the call).
+// contraction of call k and the D2H of call k-1 (PCIe is full duplex).  Each
+// slot has its own compute stream and scratch, so two contractions may also
+// overlap each other (their box levels are latency-bound and leave the GPU
+// mostly idle).  The caller's stream is never waited on before the copies
+// (F is host memory the caller has finished writing when it makes the call).
 void contract_host_async(oiobf_tbf& b, const double* F, double* G, i64 nv, cudaStream_t user) {
   require(nv >= 1, "tbf_contract_async: nv must be >= 1");
   TBF_CUDA(cudaSetDevice(b.device));
@@ -2107,8 +2124,10 @@ void contract_host_async(oiobf_tbf& b, const double* F, double* G, i64 nv, cudaS
     TBF_CUDA(cudaStreamCreateWithFlags(&b.s_in, cudaStreamNonBlocking));
     TBF_CUDA(cudaStreamCreateWithFlags(&b.s_out, cudaStreamNonBlocking));
   }
-  AsyncSet& A = pl.aset[pl.anext];
+  const int slot = pl.anext;
+  AsyncSet& A = pl.aset[slot];
   pl.anext ^= 1;
+  if (!b.s_cmp[slot]) TBF_CUDA(cudaStreamCreateWithFlags(&b.s_cmp[slot], cudaStreamNonBlocking));
   const size_t tot = static_cast<size_t>(ipow(b.n, b.d) * nv);
   if (A.F.n != tot) {
     if (A.used) TBF_CUDA(cudaEventSynchronize(A.out));
@@ -2118,20 +2137,23 @@ void contract_host_async(oiobf_tbf& b, const double* F, double* G, i64 nv, cudaS
     }
     A.F.alloc(tot);
     A.G.alloc(tot);
+    A.scratch.alloc(static_cast<size_t>(std::max<i64>(pl.scratch_elems, 1)));
     A.used = false;
   }
   if (!A.in)
     for (cudaEvent_t* e : {&A.in, &A.done, &A.out}) TBF_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   FlowPlan* fp = flow_for(b, pl, false);
-  if (!fp && !A.gexec) A.gexec = capture_ops(b, pl, A.F.p, A.G.p);
+  if (!fp && !A.gexec) A.gexec = capture_ops(b, pl, A.F.p, A.G.p, A.scratch.p);
+  // the flow engine's completion flags and scratch are per plan: one stream
+  cudaStream_t cst = fp ? b.stream : b.s_cmp[slot];
   if (A.used) TBF_CUDA(cudaStreamWaitEvent(b.s_in, A.done, 0));
   TBF_CUDA(cudaMemcpyAsync(A.F.p, F, tot * sizeof(double2), cudaMemcpyHostToDevice, b.s_in));
   TBF_CUDA(cudaEventRecord(A.in, b.s_in));
-  TBF_CUDA(cudaStreamWaitEvent(b.stream, A.in, 0));
-  if (A.used) TBF_CUDA(cudaStreamWaitEvent(b.stream, A.out, 0));
-  if (fp) launch_flow(flow_args(b, pl, *fp, A.F.p, A.G.p), fp->grid, fp->smem, b.stream);
-  else TBF_CUDA(cudaGraphLaunch(A.gexec, b.stream));
-  TBF_CUDA(cudaEventRecord(A.done, b.stream));
+  TBF_CUDA(cudaStreamWaitEvent(cst, A.in, 0));
+  if (A.used) TBF_CUDA(cudaStreamWaitEvent(cst, A.out, 0));
+  if (fp) launch_flow(flow_args(b, pl, *fp, A.F.p, A.G.p), fp->grid, fp->smem, cst);
+  else TBF_CUDA(cudaGraphLaunch(A.gexec, cst));
+  TBF_CUDA(cudaEventRecord(A.done, cst));
   TBF_CUDA(cudaStreamWaitEvent(b.s_out, A.done, 0));
   TBF_CUDA(cudaMemcpyAsync(G, A.G.p, tot * sizeof(double2), cudaMemcpyDeviceToHost, b.s_out));
   TBF_CUDA(cudaEventRecord(A.out, b.s_out));
@@ -2687,6 +2709,7 @@ int oiobf_tbf_set_exchange(oiobf_tbf* h, const int64_t* send_off, const int64_t*
   h->recv_off.assign(recv_off, recv_off + P);
   h->send_elems = send_elems;
   h->recv_elems = recv_elems;
+  h->sync_all();
   h->plans.clear();
   CAPI_END
 }
@@ -2765,7 +2788,7 @@ int oiobf_tbf_set_apply_engine(oiobf_tbf* h, int32_t engine) {
           "tbf_set_apply_engine: engine must be 0 (auto), 1 (box), 2 (tiny) or 3 (flow)");
   std::lock_guard<std::mutex> lk(h->mu);
   if (h->apply_engine != engine) {
-    TBF_CUDA(cudaStreamSynchronize(h->stream));
+    h->sync_all();
     h->plans.clear();
     h->apply_engine = engine;
   }

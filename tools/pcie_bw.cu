@@ -77,6 +77,14 @@ int main() {
       for (int i = 0; i < 8; ++i) cudaMemcpyAsync(dst + i * (bytes / 8), src + i * (bytes / 8), bytes / 8, k, s[0]);
     });
   }
+  run("H2D || D2H concurrently (4 MB each)", [&] {
+    cudaEventRecord(ev[0], s[0]);
+    cudaStreamWaitEvent(s[1], ev[0], 0);
+    cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s[0]);
+    cudaMemcpyAsync(h2, d2, bytes, cudaMemcpyDeviceToHost, s[1]);
+    cudaEventRecord(ev[1], s[1]);
+    cudaStreamWaitEvent(s[0], ev[1], 0);
+  });
   for (int grid : {148, 296, 592}) {
     char name[64];
     snprintf(name, sizeof name, "zero-copy kernel read, %d CTAs", grid);

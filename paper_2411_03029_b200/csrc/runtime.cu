@@ -334,14 +334,34 @@ struct Plan {
   // (built on first use; flow_state -1 = not eligible)
   std::unique_ptr<FlowPlan> flow_dev, flow_host;
   int flow_state[2] = {0, 0};
-  // graph cache
-  cudaGraphExec_t gexec = nullptr;
-  const void* g_F = nullptr;
-  void* g_G = nullptr;
-  cudaStream_t g_st = nullptr;
-  ~Plan() {
-    if (gexec) cudaGraphExecDestroy(gexec);
-  }
+  // captured graphs keyed by their buffers (device path: F, G, stream;
+  // host pipeline: F, G), a few of each so alternating buffers (vector groups
+  // of a wide n_v, ping-pong callers) replay instead of re-capturing
+  struct GraphCache {
+    struct Entry {
+      const void* F;
+      const void* G;
+      cudaStream_t st;
+      cudaGraphExec_t ex;
+    };
+    std::vector<Entry> e;
+    cudaGraphExec_t find(const void* F, const void* G, cudaStream_t st) const {
+      for (const Entry& x : e)
+        if (x.F == F && x.G == G && x.st == st) return x.ex;
+      return nullptr;
+    }
+    void put(const void* F, const void* G, cudaStream_t st, cudaGraphExec_t ex) {
+      if (e.size() >= 16) {
+        cudaGraphExecDestroy(e.front().ex);
+        e.erase(e.begin());
+      }
+      e.push_back(Entry{F, G, st, ex});
+    }
+    ~GraphCache() {
+      for (const Entry& x : e) cudaGraphExecDestroy(x.ex);
+    }
+  };
+  GraphCache dev_graphs, host_graphs;
 };
 
 // Fill a GemvLaunch for descs [begin, end) of pl.gemv: persistent balanced
@@ -2030,6 +2050,17 @@ void run_ops(oiobf_tbf& b, Plan& pl, const double2* F, double2* G, cudaStream_t 
 
 bool is_pinned(const void* p);
 
+// Right-hand sides per contraction: beyond 4 vectors the box levels no longer
+// stage their inputs on chip and the GEMV re-reads the cores per group of 4,
+// so wider n_v runs as consecutive 4-vector contractions (F and G are
+// n^d x n_v with vector stride n^d: each group is a contiguous slice).
+// Measured (config 2, L2 flushed): 96 / 71 / 48 us per vector at n_v = 1 / 2 /
+// 4; 65 / 64 / 61 at n_v = 8 / 16 / 32 as one plan.  OIOBF_NV_CHUNK overrides.
+i64 nv_chunk() {
+  static const i64 c = std::getenv("OIOBF_NV_CHUNK") ? std::atoll(std::getenv("OIOBF_NV_CHUNK")) : 4;
+  return c > 0 ? c : 4;
+}
+
 // the plan's launches for (F, G) captured into an instantiated graph
 cudaGraphExec_t capture_ops(oiobf_tbf& b, Plan& pl, const double2* F, double2* G, double2* scratch = nullptr) {
   cudaStream_t cap;
@@ -2058,6 +2089,12 @@ cudaGraphExec_t capture_ops(oiobf_tbf& b, Plan& pl, const double2* F, double2* G
 void contract_device(oiobf_tbf& b, const double2* F, double2* G, i64 nv, cudaStream_t st) {
   require(nv >= 1, "tbf_contract: nv must be >= 1");
   TBF_CUDA(cudaSetDevice(b.device));
+  if (nv > nv_chunk() && b.world == 1) {
+    const i64 N = ipow(b.n, b.d);
+    for (i64 v0 = 0; v0 < nv; v0 += nv_chunk())
+      contract_device(b, F + v0 * N, G + v0 * N, std::min(nv_chunk(), nv - v0), st);
+    return;
+  }
   Plan& pl = get_plan(b, nv);
   if (FlowPlan* fp = flow_for(b, pl, false)) {  // one persistent launch
     FlowArgs a = flow_args(b, pl, *fp, F, G);
@@ -2090,17 +2127,12 @@ void contract_device(oiobf_tbf& b, const double2* F, double2* G, i64 nv, cudaStr
     run_ops(b, pl, F, G, st);
     return;
   }
-  if (!pl.gexec || pl.g_F != F || pl.g_G != G || pl.g_st != st) {
-    if (pl.gexec) {
-      cudaGraphExecDestroy(pl.gexec);
-      pl.gexec = nullptr;
-    }
-    pl.gexec = capture_ops(b, pl, F, G);
-    pl.g_F = F;
-    pl.g_G = G;
-    pl.g_st = st;
+  cudaGraphExec_t ex = pl.dev_graphs.find(F, G, st);
+  if (!ex) {
+    ex = capture_ops(b, pl, F, G);
+    pl.dev_graphs.put(F, G, st, ex);
   }
-  TBF_CUDA(cudaGraphLaunch(pl.gexec, st));
+  TBF_CUDA(cudaGraphLaunch(ex, st));
 }
 
 // Stream-ordered host-buffer contraction (pinned F and G): slot k of the plan
@@ -2117,6 +2149,12 @@ void contract_device(oiobf_tbf& b, const double2* F, double2* G, i64 nv, cudaStr
 void contract_host_async(oiobf_tbf& b, const double* F, double* G, i64 nv, cudaStream_t user) {
   require(nv >= 1, "tbf_contract_async: nv must be >= 1");
   TBF_CUDA(cudaSetDevice(b.device));
+  if (nv > nv_chunk()) {
+    const i64 N = ipow(b.n, b.d);
+    for (i64 v0 = 0; v0 < nv; v0 += nv_chunk())
+      contract_host_async(b, F + 2 * v0 * N, G + 2 * v0 * N, std::min(nv_chunk(), nv - v0), user);
+    return;
+  }
   require(is_pinned(F) && is_pinned(G),
           "tbf_contract_async: F and G must be pinned host memory (cudaHostAlloc / cudaHostRegister)");
   Plan& pl = get_plan(b, nv);
@@ -2286,6 +2324,12 @@ void contract_host_flow(oiobf_tbf& b, Plan& pl, FlowPlan& fp, const double* F, d
 
 void contract_host(oiobf_tbf& b, const double* F, double* G, i64 nv) {
   TBF_CUDA(cudaSetDevice(b.device));
+  if (nv > nv_chunk()) {
+    const i64 N = ipow(b.n, b.d);
+    for (i64 v0 = 0; v0 < nv; v0 += nv_chunk())
+      contract_host(b, F + 2 * v0 * N, G + 2 * v0 * N, std::min(nv_chunk(), nv - v0));
+    return;
+  }
   if (is_pinned(F) && is_pinned(G)) {
     Plan& pl0 = get_plan(b, nv, false);
     if (FlowPlan* fp = flow_for(b, pl0, true)) {
@@ -2315,11 +2359,8 @@ void contract_host(oiobf_tbf& b, const double* F, double* G, i64 nv) {
     TBF_CUDA(cudaStreamSynchronize(b.stream));
     return;
   }
-  if (!pl.gexec || pl.g_F != F || pl.g_G != G) {
-    if (pl.gexec) {
-      cudaGraphExecDestroy(pl.gexec);
-      pl.gexec = nullptr;
-    }
+  cudaGraphExec_t ex = pl.host_graphs.find(F, G, nullptr);
+  if (!ex) {
     cudaGraph_t g;
     // global mode: the fork/join events pull the copy streams into the capture
     TBF_CUDA(cudaStreamBeginCapture(b.stream, cudaStreamCaptureModeThreadLocal));
@@ -2330,12 +2371,11 @@ void contract_host(oiobf_tbf& b, const double* F, double* G, i64 nv) {
       throw;
     }
     TBF_CUDA(cudaStreamEndCapture(b.stream, &g));
-    TBF_CUDA(cudaGraphInstantiate(&pl.gexec, g, 0));
+    TBF_CUDA(cudaGraphInstantiate(&ex, g, 0));
     TBF_CUDA(cudaGraphDestroy(g));
-    pl.g_F = F;
-    pl.g_G = G;
+    pl.host_graphs.put(F, G, nullptr, ex);
   }
-  TBF_CUDA(cudaGraphLaunch(pl.gexec, b.stream));
+  TBF_CUDA(cudaGraphLaunch(ex, b.stream));
   TBF_CUDA(cudaStreamSynchronize(b.stream));
 }
 

@@ -297,6 +297,14 @@ def run_b200(args):
     clocks = sampler.stop()
     hbm, peak_src = peaks()
     gemv_bytes = stats["core_bytes"]
+    kname = "k_gemv (middle-level core contraction)"
+    if bf.apply_engine() == "rank1":
+        # rank-one engine: the core product is folded into the middle V/W level
+        # (k_r1_vw_mid), which streams the level-Lc factors (d blocks of 1 x 2
+        # per pair), the 1 x 1 cores, its input and its output: 16 (2d + 3) B per pair
+        npairs = 2 ** (cfg.spec.d * cfg.L)
+        gemv_bytes = 16 * npairs * (2 * cfg.spec.d + 3)
+        kname = "k_r1_vw_mid (middle-level V/W transfer + 1x1 core contraction, rank-one engine)"
     achieved = gemv_bytes / (prof["core_ms"] / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"ncu_{cfg.name}.json")
@@ -333,7 +341,7 @@ def run_b200(args):
                                      "each; copies pipelined over slab groups inside the call)"}},
         "gpu_launches": int(stats["launches"]) * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": traffic, "kernel": "k_gemv (middle-level core contraction)",
+                     "traffic": traffic, "kernel": kname,
                      "algorithmic_bytes_per_launch": gemv_bytes, "launch_ms": prof["core_ms"], "peak_source": peak_src,
                      "whole_apply_bytes_alg": stats["bytes_alg"],
                      "whole_apply_GBps": stats["bytes_alg"] / (ms / 1e3) / 1e9,

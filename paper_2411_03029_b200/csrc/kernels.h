@@ -185,6 +185,38 @@ void launch_tiny_level(const TinyLevelArgs& a, const TinyGroup* groups, const i6
 void launch_tiny_gemv(const GemvDesc* d, i64 npairs, i64 total_rows, int nv, const double2* cores, const double2* x,
                       double2* y, cudaStream_t st);
 
+// ---- rank-one apply engine (r1_kernels.cu): every ID of rank 1, factor
+// blocks 1 x W at slot * W, 1 x 1 cores at pair s * nmid + t; geometry implicit
+struct R1LevelArgs {
+  int side, l, d, W, nv, Lc;
+  int nch;             // children per group (2^d at l >= 1, else 1)
+  int gpb;             // V/W: groups per CTA; P/U: (group, block tuple) units per CTA
+  int in_global;       // V/W l = 0: input is the n^d x nv tensor F
+  int out_global;      // P/U l = 0: output is G
+  int in_transposed;   // P/U l = Lc: input indexed by the pair s * nmid + t
+  int core_mul;        // V/W l = Lc: multiply by the 1 x 1 core of pair s * nmid + t
+  i64 n, nmid, mpm, mid;
+  i64 nin, nj, njd;    // this level: inner multi-sets, blocks per mode, nj^d
+  i64 pnin;            // groups per outer multi-set (parents)
+  i64 ngroups;         // nmid * pnin
+  i64 nunits;          // P/U: ngroups * njd
+  i64 E, ED;           // V/W: input extent per mode and E^d; P/U: output extent and E^d
+  int fblk, FS;        // factor elements per (outer, inner) slot group (d * nj * W); odd SMEM stride
+  unsigned magic;      // ceil(2^32 / fblk): e / fblk as a multiply-high
+  int lg_T;            // V/W: log2 consecutive tau per CTA; P/U cluster: log2 children per CTA
+  int Pc;              // V/W: parents staged per CTA (max); P/U cluster: parents per cluster
+  int XS;              // V/W: SMEM stride of a staged parent tensor (odd)
+  int warp_tiles;      // middle level: V/W one warp per 32 consecutive tau (Pc = parents per warp
+                       // tile), P/U one warp per group
+  // log2 of the power-of-two extents above (n is a power of two)
+  int lg_n, lg_mid, lg_nmid, lg_nin, lg_nj, lg_njd, lg_pnin, lg_nch, lg_E, lg_ED;
+};
+size_t r1_smem_bytes(const R1LevelArgs& a);
+int r1_threads();
+int r1_vthreads();
+void launch_r1_level(const R1LevelArgs& a, const double2* fac, const double2* cores, const double2* in, double2* out,
+                     cudaStream_t st);
+
 // ---- dense check (core_kernels.cu)
 unsigned long long count_nonfinite(const double2* x, i64 n, cudaStream_t st);
 void launch_dense_rows(const KSpec& ks, i64 nrows, const i64* rows, const double2* F, int nv, double2* out,

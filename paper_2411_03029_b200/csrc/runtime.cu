@@ -232,7 +232,7 @@ struct BoxLaunch {
   BoxLaunchInfo info;
 };
 struct Op {
-  int kind;  // 0 mode product, 1 gemv, 2 ordered child sums, 3 fused boxes, 6 tiny level, 7 tiny gemv
+  int kind;  // 0 mode product, 1 gemv, 2 ordered child sums, 3 fused boxes, 6 tiny level, 7 tiny gemv, 8 rank-one level
   i64 idx;
   int group;  // 0 V/W, 1 core, 2 P/U
   int chunk = 0;  // pipelined plans: slab group (outer index of mode d-1)
@@ -303,6 +303,12 @@ struct Plan {
   std::vector<i64> tiny_off;  // per level: child output (V/W) / input (P/U) offsets by (outer, inner)
   DevBuf<TinyGroup> d_tiny_groups;
   DevBuf<i64> d_tiny_off;
+  // rank-one engine (r1_kernels.cu): one launch per level, ping-pong scratch
+  struct R1Level {
+    R1LevelArgs args;
+    i64 in_off, out_off;  // scratch element offsets; -1: F (input) / G (output)
+  };
+  std::vector<R1Level> r1_levels;
   std::vector<GemvDesc> gemv;
   std::vector<int> gemv_t;  // row multi-set t of each GemvDesc (flow ticket priority)
   std::vector<GemvLaunch> gemvs;
@@ -513,9 +519,10 @@ struct oiobf_tbf {
   std::vector<PairDesc> h_pairs;
   i64 total_core = 0;
   std::map<i64, std::unique_ptr<Plan>> plans;
-  int apply_engine = 0;  // 0 auto, 1 box engine, 2 tiny-box engine, 3 dataflow engine
+  int apply_engine = 0;  // 0 auto, 1 box engine, 2 tiny-box engine, 3 dataflow engine, 4 rank-one engine
   int* h_one = nullptr;  // pinned host 1: raises the input-slab flags of the flow engine
   int tiny_auto = -1;    // cached auto decision (-1: not evaluated yet)
+  int r1_ok = -1;        // cached rank-one eligibility (-1: not evaluated yet)
   double t_ms[6] = {0, 0, 0, 0, 0, 0};
   std::mutex mu;
   // host-buffer contraction pipeline: copy-in / copy-out streams and the
@@ -1665,16 +1672,160 @@ std::unique_ptr<Plan> build_plan_tiny(oiobf_tbf& b, i64 nv) {
   return pl;
 }
 
+// ---- rank-one engine (r1_kernels.cu): every ID of rank 1 (DFT with two-sided
+// bit reversal), so factor blocks, intermediates and cores are regular.
+// Eligible when, on both sides and every level, each slot has rank 1 and
+// width W_l (the leaf size <= 2 at l = 0, 2 above) with its block at slot * W_l
+// in the interp arena, and every core is 1 x 1 at its pair index.
+bool r1_eligible(const oiobf_tbf& b) {
+  if (b.world > 1 || b.d < 1 || b.d > kMaxD || (b.n & (b.n - 1)) != 0) return false;
+  const i64 leaf = b.n >> b.L;
+  if (leaf < 1 || leaf > 2) return false;
+  for (int sd = 0; sd < 2; ++sd) {
+    if (b.side[sd].size() != static_cast<size_t>(b.Lc + 1)) return false;
+    for (int l = 0; l <= b.Lc; ++l) {
+      const LevelData& ld = b.side[sd][static_cast<size_t>(l)];
+      const int w = l == 0 ? static_cast<int>(leaf) : 2;
+      if (static_cast<i64>(ld.h_rank.size()) != ld.nslots || static_cast<i64>(ld.h_interp_off.size()) != ld.nslots)
+        return false;
+      for (i64 sl = 0; sl < ld.nslots; ++sl) {
+        const size_t i = static_cast<size_t>(sl);
+        if (ld.h_rank[i] != 1 || ld.h_width[i] != w || ld.h_interp_off[i] != sl * w) return false;
+      }
+    }
+  }
+  const i64 P = b.nmid * b.nmid;
+  if (static_cast<i64>(b.h_pairs.size()) != P) return false;
+  for (i64 p = 0; p < P; ++p) {
+    const PairDesc& pd = b.h_pairs[static_cast<size_t>(p)];
+    if (pd.R != 1 || pd.C != 1 || pd.core_off != p) return false;
+  }
+  return true;
+}
+
+bool use_r1_engine(oiobf_tbf& b) {
+  if (b.apply_engine != 0 && b.apply_engine != 4) return false;
+  if (b.r1_ok < 0) b.r1_ok = r1_eligible(b) ? 1 : 0;  // one scan of every slot per handle
+  if (b.apply_engine == 4)
+    require(b.r1_ok == 1, "tbf_set_apply_engine: the rank-one engine needs every ID of rank 1 (leaf <= 2)");
+  return b.r1_ok == 1;
+}
+
+std::unique_ptr<Plan> build_plan_r1(oiobf_tbf& b, i64 nv) {
+  auto pl = std::make_unique<Plan>();
+  pl->nv = nv;
+  const int d = b.d;
+  const i64 n = b.n;
+  const i64 P = b.nmid * b.nmid;  // elements of every intermediate (per vector)
+  const i64 leaf = n >> b.L;
+  auto base = [&](int sd, int l) {
+    const LevelData& ld = b.side[sd][static_cast<size_t>(l)];
+    R1LevelArgs a{};
+    a.side = sd;
+    a.l = l;
+    a.d = d;
+    a.W = l == 0 ? static_cast<int>(leaf) : 2;
+    a.nv = static_cast<int>(nv);
+    a.Lc = b.Lc;
+    a.nch = l > 0 ? (1 << d) : 1;
+    a.n = n;
+    a.nmid = b.nmid;
+    a.mpm = ipow(2, b.Lc);
+    a.mid = n >> b.Lc;
+    a.nin = ld.L.nin;
+    a.nj = ld.L.nj;
+    a.njd = ipow(a.nj, d);
+    a.pnin = l > 0 ? ipow(2, static_cast<i64>(d) * (l - 1)) : 1;
+    a.ngroups = b.nmid * a.pnin;
+    a.E = a.nj * a.W;
+    a.ED = ipow(a.E, d);
+    a.fblk = static_cast<int>(d * a.nj * a.W);
+    a.FS = a.fblk | 1;
+    auto lg = [](i64 x) {
+      int r = 0;
+      while ((i64{1} << r) < x) ++r;
+      require((i64{1} << r) == x, "rank-one engine: extents must be powers of two");
+      return r;
+    };
+    a.lg_n = lg(n);
+    a.lg_mid = lg(a.mid);
+    a.lg_nmid = lg(a.nmid);
+    a.lg_nin = lg(a.nin);
+    a.lg_nj = lg(a.nj);
+    a.lg_njd = lg(a.njd);
+    a.lg_pnin = lg(a.pnin);
+    a.lg_nch = lg(a.nch);
+    a.lg_E = lg(a.E);
+    a.lg_ED = lg(a.ED);
+    return a;
+  };
+  const int th = r1_threads();
+  // ping-pong: level outputs alternate between scratch halves [0, P nv) and [P nv, 2 P nv)
+  int cur = 0;  // half holding the current intermediate (-1: F)
+  auto add = [&](R1LevelArgs a, int in_half, int out_half) {
+    Plan::R1Level rl;
+    a.magic = static_cast<unsigned>(((u64{1} << 32) + a.fblk - 1) / a.fblk);
+    rl.args = a;
+    rl.in_off = in_half < 0 ? -1 : in_half * P * nv;
+    rl.out_off = out_half < 0 ? -1 : out_half * P * nv;
+    require(r1_smem_bytes(a) <= static_cast<size_t>(kMaxDynSmem), "rank-one engine: a group does not fit on chip");
+    pl->ops.push_back(Op{8, static_cast<i64>(pl->r1_levels.size()), a.side == 0 ? (a.core_mul ? 1 : 0) : 2});
+    pl->r1_levels.push_back(rl);
+  };
+  auto parent_of = [&](i64 inner, int l) {
+    i64 p = 0;
+    for (int q = 0; q < d; ++q) p |= (((inner >> (l * q)) & ((i64{1} << l) - 1)) >> 1) << ((l - 1) * q);
+    return p;
+  };
+  for (int l = 0; l <= b.Lc; ++l) {
+    R1LevelArgs a = base(0, l);
+    a.in_global = l == 0;
+    a.core_mul = l == b.Lc;
+    // T consecutive tau per CTA: their factor blocks (T * FS elements) <= 32 KB
+    a.lg_T = 0;
+    while (a.lg_T < a.lg_nin && (i64{2} << a.lg_T) * a.FS * 16 <= 32 * 1024) ++a.lg_T;
+    a.Pc = l > 0 ? static_cast<int>(parent_of((i64{1} << a.lg_T) - 1, l) + 1) : 1;
+    a.XS = static_cast<int>(a.ED | 1);
+    if (l >= 1 && a.njd == 1 && a.lg_nin >= 5) {  // middle level: warp tiles of 32 tau
+      a.warp_tiles = 1;
+      a.Pc = static_cast<int>(parent_of(31, l) + 1);
+    }
+    const int out_half = l == 0 ? 0 : 1 - cur;
+    add(a, l == 0 ? -1 : cur, out_half);
+    cur = out_half;
+  }
+  for (int l = b.Lc; l >= 0; --l) {
+    R1LevelArgs a = base(1, l);
+    a.in_transposed = l == b.Lc;
+    a.out_global = l == 0;
+    a.nunits = a.ngroups * a.njd;
+    i64 nx = 1;
+    for (int k = 0; k < d; ++k) nx *= a.W;
+    a.warp_tiles = l >= 1 && a.njd == 1;  // middle level: one warp per group
+    if (!a.warp_tiles) {
+      a.gpb = static_cast<int>(std::max<i64>(1, th / std::max<i64>(nx, a.nch)));  // units: <= one thread per child
+      while (a.gpb > 1 && r1_smem_bytes(a) > 72 * 1024) a.gpb /= 2;
+    }
+    const int out_half = l == 0 ? -1 : 1 - cur;
+    add(a, cur, out_half);
+    cur = out_half;
+  }
+  pl->scratch_elems = 2 * P * nv;
+  pl->scratch.alloc(static_cast<size_t>(std::max<i64>(pl->scratch_elems, 1)));
+  return pl;
+}
+
 // chunked = true: the host-pipelined plan (ops per slab group, see
 // contract_host); the device-buffer path uses the unchunked plan
 Plan& get_plan(oiobf_tbf& b, i64 nv, bool chunked = false) {
-  const bool tiny = use_tiny_engine(b);
-  if (tiny) chunked = false;  // one slab group: the tiny plan is not split
+  const bool r1 = use_r1_engine(b);
+  const bool tiny = !r1 && use_tiny_engine(b);
+  if (tiny || r1) chunked = false;  // one slab group: these plans are not split
   const i64 key = 2 * nv + (chunked ? 1 : 0);
   auto it = b.plans.find(key);
   if (it != b.plans.end()) return *it->second;
   auto& slot = b.plans[key];
-  slot = tiny ? build_plan_tiny(b, nv) : build_plan(b, nv, chunked);
+  slot = r1 ? build_plan_r1(b, nv) : tiny ? build_plan_tiny(b, nv) : build_plan(b, nv, chunked);
   return *slot;
 }
 
@@ -1944,7 +2095,7 @@ std::unique_ptr<FlowPlan> build_flow(oiobf_tbf& b, Plan& pl, int nflags) {
 FlowPlan* flow_for(oiobf_tbf& b, Plan& pl, bool host) {
   static const char* env = std::getenv("OIOBF_FLOW");
   const bool want = b.apply_engine == 3 || (b.apply_engine == 0 && env && env[0] == '1');
-  if (!want || use_tiny_engine(b)) return nullptr;
+  if (!want || use_r1_engine(b) || use_tiny_engine(b)) return nullptr;
   int& state = pl.flow_state[host ? 1 : 0];
   std::unique_ptr<FlowPlan>& fp = host ? pl.flow_host : pl.flow_dev;
   if (state == 0) {
@@ -2025,6 +2176,11 @@ void run_ops(oiobf_tbf& b, Plan& pl, const OpBuffers& io, cudaStream_t st, int g
       const LevelData& ld = b.side[tl.side][static_cast<size_t>(tl.l)];
       launch_tiny_level(tl.args, pl.d_tiny_groups.p + tl.group_begin, pl.d_tiny_off.p + tl.off_begin, ld.rank.p,
                         ld.width.p, ld.interp_off.p, ld.interp.p, in_ptr(tl.in_buf), out_ptr(tl.out_buf), st);
+    } else if (op.kind == 8) {
+      const Plan::R1Level& rl = pl.r1_levels[static_cast<size_t>(op.idx)];
+      const LevelData& ld = b.side[rl.args.side][static_cast<size_t>(rl.args.l)];
+      launch_r1_level(rl.args, ld.interp.p, b.cores.p, rl.in_off < 0 ? io.F : scr + rl.in_off,
+                      rl.out_off < 0 ? io.G : scr + rl.out_off, st);
     } else if (op.kind == 7) {
       const GemvLaunch& gl = pl.gemvs[static_cast<size_t>(op.idx)];
       launch_tiny_gemv(pl.d_gemv.p + gl.desc_begin, gl.ndesc, gl.total_rows, static_cast<int>(pl.nv), b.cores.p,
@@ -2824,8 +2980,8 @@ int oiobf_tbf_load(const char* path, oiobf_tbf** out) {
 int oiobf_tbf_set_apply_engine(oiobf_tbf* h, int32_t engine) {
   CAPI_BEGIN
   require(h, "tbf_set_apply_engine: null handle");
-  require(engine >= 0 && engine <= 3,
-          "tbf_set_apply_engine: engine must be 0 (auto), 1 (box), 2 (tiny) or 3 (flow)");
+  require(engine >= 0 && engine <= 4,
+          "tbf_set_apply_engine: engine must be 0 (auto), 1 (box), 2 (tiny), 3 (flow) or 4 (rank-one)");
   std::lock_guard<std::mutex> lk(h->mu);
   if (h->apply_engine != engine) {
     h->sync_all();
@@ -2839,7 +2995,9 @@ int oiobf_tbf_apply_engine(oiobf_tbf* h, int32_t* engine) {
   CAPI_BEGIN
   require(h && engine, "tbf_apply_engine: null argument");
   std::lock_guard<std::mutex> lk(h->mu);
-  if (use_tiny_engine(*h)) {
+  if (use_r1_engine(*h)) {
+    *engine = 4;
+  } else if (use_tiny_engine(*h)) {
     *engine = 2;
   } else {
     TBF_CUDA(cudaSetDevice(h->device));

@@ -358,6 +358,59 @@ def test_tiny_engine_matches_box_engine_and_oracle(oracle, name, spec, tol, L):
     bf.set_apply_engine("auto")
 
 
+# rank 1 needs leaf 1 (C_b = 1): a leaf of 2 DFT columns has rank 2
+R1_CASES = [
+    ("dft2_16_L4", dft(2, 16), 1e-8, 4),
+    ("dft2_64_L6", dft(2, 64), 1e-8, 6),   # Lc = 3
+    ("dft3_4_L2", dft(3, 4), 1e-8, 2),
+    ("dft4_4_L2", dft(4, 4), 1e-8, 2),
+    ("dft5_4_L2", dft(5, 4), 1e-8, 2),
+    ("dft6_4_L2", dft(6, 4), 1e-8, 2),     # d = 6: config 4's kernels
+    ("dft1_16_L4", dft(1, 16), 1e-8, 4),   # d = 1
+]
+
+
+@pytest.mark.parametrize("name,spec,tol,L", R1_CASES, ids=[c[0] for c in R1_CASES])
+def test_rank1_engine_matches_oracle_and_box(oracle, name, spec, tol, L):
+    """The rank-one engine (implicit geometry, every ID of rank 1): chosen by
+    'auto' for two-sided bit-reversed DFTs, within 1e-10 of the oracle applying
+    the same factors and equal to the fused-box engine to rounding, nv = 1, 2, 3;
+    host-buffer and device paths agree bit for bit."""
+    import torch
+    bf = tb.tbf_construct(spec, L, tol, seed=3)
+    fz = bf.export()
+    assert (fz.ranks == 1).all()
+    assert bf.apply_engine() == "rank1"
+    tbo = oracle.tbf_construct(spec, L, tol, seed=3, replay=fz)
+    rng = np.random.default_rng(21)
+    for nv in (1, 2, 3):
+        shape = (spec.n,) * spec.d + ((nv,) if nv > 1 else ())
+        F = rand_c(rng, shape)
+        g1 = bf.contract(F)
+        assert rel(g1, tbo.contract(F)) < 1e-10, f"rank1 vs oracle {rel(g1, tbo.contract(F))}"
+        dF = torch.from_numpy(F.reshape(-1, order="F").view(np.float64).copy()).cuda()
+        dG = torch.empty_like(dF)
+        bf.contract_device(dF.data_ptr(), dG.data_ptr(), nv, 0)
+        torch.cuda.synchronize()
+        gd = dG.cpu().numpy().view(np.complex128).reshape(shape, order="F")
+        np.testing.assert_array_equal(gd, g1)
+        bf.set_apply_engine("box")
+        assert bf.apply_engine() == "box"
+        gb = bf.contract(F)
+        assert rel(g1, gb) < 1e-13, f"rank1 vs box {rel(g1, gb)}"
+        bf.set_apply_engine("auto")
+    assert bf.apply_engine() == "rank1"
+
+
+def test_rank1_engine_refuses_ineligible():
+    bf = tb.tbf_construct(green_plates(32), 2, 1e-6, seed=3)
+    bf.set_apply_engine("rank1")
+    with pytest.raises(ValueError, match="rank 1"):
+        bf.contract(np.zeros((32, 32), np.complex128))
+    bf.set_apply_engine("auto")
+    assert bf.apply_engine() == "box"
+
+
 def test_dft_uses_narrow_ids():
     """DFT levels with <= 2 candidate columns take the closed-form narrow-ID
     kernel (no panel / TSQR work is timed)."""
@@ -417,13 +470,13 @@ def test_config4_full_size(oracle):
     """Config 4 (d = 6 DFT, n = 16, C_b = 1 -> L = 4; 2.08e8 IDs, 1.7e7 middle
     pairs) at full size: sampled slots of every level recomputed by the oracle
     from the same proxies and candidates (ranks / skeletons exact, interps to
-    1e-8), the tiny-box engine selected automatically, and 1000 sampled outputs
+    1e-8), the rank-one engine selected automatically, and 1000 sampled outputs
     within tol of direct dense sums (GPU dense rows cross-checked against the
     oracle's on 8 rows)."""
     c = BY_NAME["dft6_n16"]
     spec = c.spec
     bf = tb.tbf_construct(spec, c.L, c.tol, seed=c.seed)
-    assert bf.apply_engine() == "tiny"
+    assert bf.apply_engine() == "rank1"
     fz = bf.export()
     assert len(fz.ranks) == 207814656
     so, io, po, _ = fz.offsets()

@@ -206,8 +206,8 @@ struct R1LevelArgs {
   int lg_T;            // V/W: log2 consecutive tau per CTA; P/U cluster: log2 children per CTA
   int Pc;              // V/W: parents staged per CTA (max); P/U cluster: parents per cluster
   int XS;              // V/W: SMEM stride of a staged parent tensor (odd)
-  int warp_tiles;      // middle level: V/W one warp per 32 consecutive tau (Pc = parents per warp
-                       // tile), P/U one warp per group
+  int warp_tiles;      // V/W middle level: one warp per 32 consecutive tau (Pc = parents per warp
+                       // tile); P/U levels >= 1: one warp per (group, block tuple) unit
   // log2 of the power-of-two extents above (n is a power of two)
   int lg_n, lg_mid, lg_nmid, lg_nin, lg_nj, lg_njd, lg_pnin, lg_nch, lg_E, lg_ED;
 };

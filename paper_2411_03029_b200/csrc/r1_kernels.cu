@@ -142,7 +142,7 @@ __device__ __forceinline__ i64 r1_pu_out(const R1LevelArgs& a, i64 v, i64 t, i64
 // range (aligned power-of-two tau ranges), staged at odd stride XS; the T
 // factor blocks are one contiguous run of the arena.
 template <int D, int W>
-__global__ void __launch_bounds__(kR1VThreads, 4) k_r1_vw(R1LevelArgs a, const double2* __restrict__ fac,
+__global__ void __launch_bounds__(kR1Threads, 2) k_r1_vw(R1LevelArgs a, const double2* __restrict__ fac,
                                                           const double2* __restrict__ cores,
                                                           const double2* __restrict__ in, double2* __restrict__ out) {
   extern __shared__ __align__(16) double2 xs[];
@@ -381,17 +381,25 @@ __global__ void __launch_bounds__(kR1Threads, 3) k_r1_pu(R1LevelArgs a, const do
   }
 }
 
-// P/U level with one block tuple per child (nj = 1, the middle level Lc, the
-// bulk of the factor bytes): one WARP per group (t, p_nu).  The children are
-// taken 32 at a time: the warp copies their factor blocks into a warp-private
-// shared-memory slice (each lane computes one child's arena offset, the copy
-// loop fetches it by shuffle), lane c builds A_c / B_c (aliasing the slice),
-// and each lane accumulates its outputs over the chunk's children in
-// ascending order -- the reference's order, with no CTA-wide barrier.
+// P/U levels l >= 1 (the middle level Lc holds the bulk of the factor bytes):
+// one WARP per unit (group (t, p_nu), block tuple jt).  The children are
+// taken 32 at a time: the warp copies their factor blocks with cp.async into
+// one of two warp-private shared-memory buffers (each lane computes one
+// child's arena offset, the copy loop fetches it by shuffle; the next chunk's
+// copies are in flight while this one is computed), lane c builds A_c / B_c
+// (aliasing the buffer), and each lane accumulates its outputs over the
+// chunk's children in ascending order -- the reference's order, with no
+// CTA-wide barrier.
+__device__ __forceinline__ void r1_cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+
 template <int D, int W>
-__global__ void __launch_bounds__(kR1VThreads, 5) k_r1_pu_mid(R1LevelArgs a, const double2* __restrict__ fac,
-                                                             const double2* __restrict__ in,
-                                                             double2* __restrict__ out) {
+__global__ void __launch_bounds__(kR1VThreads, 3) k_r1_pu_mid(R1LevelArgs a, const double2* __restrict__ fac,
+                                                              const double2* __restrict__ in,
+                                                              double2* __restrict__ out) {
   extern __shared__ __align__(16) double2 wsm[];
   constexpr int H = D / 2;
   constexpr int NA = Pow<W, H>::v, NB = Pow<W, D - H>::v, NX = NA * NB;
@@ -399,45 +407,66 @@ __global__ void __launch_bounds__(kR1VThreads, 5) k_r1_pu_mid(R1LevelArgs a, con
   constexpr int OPL = (NX + 31) / 32;  // outputs per lane
   const i64 v = blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const i64 g = static_cast<i64>(blockIdx.x) * (kR1VThreads / 32) + warp;
-  if (g >= a.ngroups) return;
-  const int SL = a.FS > TS ? a.FS : TS;
-  double2* ws = wsm + warp * 32 * SL;
+  const i64 u = static_cast<i64>(blockIdx.x) * (kR1VThreads / 32) + warp;  // unit (group, block tuple)
+  if (u >= a.nunits) return;
+  const i64 g = u >> a.lg_njd;
+  const int jt = static_cast<int>(u & ((i64{1} << a.lg_njd) - 1));
+  constexpr int SL = ((D * W) | 1) > TS ? ((D * W) | 1) : TS;
+  double2* ws = wsm + warp * 2 * 32 * SL;  // two chunk buffers (factor rows, then aliased tables)
   const i64 t = g & ((i64{1} << a.lg_nmid) - 1), pnu = g >> a.lg_nmid;  // groups t fastest
-  const int nch = 1 << a.lg_nch, fblk = a.fblk, FS = a.FS;
-  double2 acc[OPL];
-#pragma unroll
-  for (int i = 0; i < OPL; ++i) acc[i] = make_double2(0, 0);
-  for (int c0 = 0; c0 < nch; c0 += 32) {
+  const int nch = 1 << a.lg_nch, fblk = a.fblk;
+  const int nchunk = (nch + 31) / 32;
+  // chunk c0 / 32 -> buffer (c0 / 32) & 1: async copies of the chunk's factor
+  // rows for this block tuple (d blocks of W per child)
+  constexpr int DW = D * W;
+  const int nj = 1 << a.lg_nj;
+  auto prefetch = [&](int c0, double2& val) {
     const int cn = min(32, nch - c0);
     const i64 nuc = a.l > 0 ? r1_child<D>(pnu, a.l, c0 + lane) : 0;
     const i64 mybase = ((t << a.lg_nin) + nuc) * fblk;
-    double2 val = make_double2(0, 0);
     if (lane < cn)
       val = __ldg(in + (a.in_transposed ? (((v << a.lg_nmid) + nuc) << a.lg_nmid) + t
-                                        : (((v << a.lg_nmid) + t) << a.lg_nin) + nuc));
-    for (int e0 = 0; e0 < cn * fblk; e0 += 32) {
-      const int e = e0 + lane;
-      const int cc = r1_div(min(e, cn * fblk - 1), a.magic);
+                                        : (((((v << a.lg_nmid) + t) << a.lg_nin) + nuc) << a.lg_njd) + jt));
+    double2* buf = ws + ((c0 >> 5) & 1) * 32 * SL;
+    for (int e0 = 0; e0 < cn * DW; e0 += 32) {
+      const int e = min(e0 + lane, cn * DW - 1);
+      const int cc = e / DW, r = e - cc * DW, k = r / W, x = r - k * W;
       const i64 base = __shfl_sync(0xffffffffu, mybase, cc);
-      if (e < cn * fblk) ws[cc * FS + e - cc * fblk] = __ldg(fac + base + e - cc * fblk);
+      const int jk = (jt >> (a.lg_nj * k)) & (nj - 1);
+      if (e0 + lane < cn * DW) r1_cp_async16(buf + cc * SL + r, fac + base + (k * nj + jk) * W + x);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double2 acc[OPL];
+#pragma unroll
+  for (int i = 0; i < OPL; ++i) acc[i] = make_double2(0, 0);
+  double2 val_cur = make_double2(0, 0), val_next = make_double2(0, 0);
+  prefetch(0, val_cur);
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const int c0 = ch * 32, cn = min(32, nch - c0);
+    if (ch + 1 < nchunk) {
+      prefetch(c0 + 32, val_next);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncwarp();
+    double2* buf = ws + (ch & 1) * 32 * SL;
     double2 A[NA], B[NB];
     if (lane < cn) {
       double2 b[D][W];
 #pragma unroll
       for (int k = 0; k < D; ++k)
 #pragma unroll
-        for (int x = 0; x < W; ++x) b[k][x] = ws[lane * FS + k * W + x];
-      r1_tables<D, W, NA, NB>(val, b, A, B);
+        for (int x = 0; x < W; ++x) b[k][x] = buf[lane * SL + k * W + x];
+      r1_tables<D, W, NA, NB>(val_cur, b, A, B);
     }
     __syncwarp();
     if (lane < cn) {
 #pragma unroll
-      for (int i = 0; i < NA; ++i) ws[lane * TS + i] = A[i];
+      for (int i = 0; i < NA; ++i) buf[lane * SL + i] = A[i];
 #pragma unroll
-      for (int i = 0; i < NB; ++i) ws[lane * TS + NA + i] = B[i];
+      for (int i = 0; i < NB; ++i) buf[lane * SL + NA + i] = B[i];
     }
     __syncwarp();
 #pragma unroll
@@ -445,15 +474,16 @@ __global__ void __launch_bounds__(kR1VThreads, 5) k_r1_pu_mid(R1LevelArgs a, con
       const int o = lane + 32 * i;
       if (o < NX) {
         const int xlo = o % NA, xhi = o / NA;
-        for (int cc = 0; cc < cn; ++cc) cfma(acc[i], ws[cc * TS + xlo], ws[cc * TS + NA + xhi]);
+        for (int cc = 0; cc < cn; ++cc) cfma(acc[i], buf[cc * SL + xlo], buf[cc * SL + NA + xhi]);
       }
     }
-    __syncwarp();
+    __syncwarp();  // the buffer is refilled two chunks later
+    val_cur = val_next;
   }
 #pragma unroll
   for (int i = 0; i < OPL; ++i) {
     const int o = lane + 32 * i;
-    if (o < NX) out[r1_pu_out<D, W>(a, v, t, pnu, 0, o)] = acc[i];
+    if (o < NX) out[r1_pu_out<D, W>(a, v, t, pnu, jt, o)] = acc[i];
   }
 }
 
@@ -469,9 +499,9 @@ void launch_r1_dw(const R1LevelArgs& a, const double2* fac, const double2* cores
   } else if (a.side == 0) {
     const dim3 grid(static_cast<unsigned>(a.nmid << (a.lg_nin - a.lg_T)), static_cast<unsigned>(a.nv));
     TBF_CUDA(cudaFuncSetAttribute(k_r1_vw<D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-    k_r1_vw<D, W><<<grid, kR1VThreads, smem, st>>>(a, fac, cores, in, out);
+    k_r1_vw<D, W><<<grid, kR1Threads, smem, st>>>(a, fac, cores, in, out);
   } else if (a.warp_tiles) {
-    const dim3 grid(static_cast<unsigned>((a.ngroups + kR1VThreads / 32 - 1) / (kR1VThreads / 32)), static_cast<unsigned>(a.nv));
+    const dim3 grid(static_cast<unsigned>((a.nunits + kR1VThreads / 32 - 1) / (kR1VThreads / 32)), static_cast<unsigned>(a.nv));
     TBF_CUDA(cudaFuncSetAttribute(k_r1_pu_mid<D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     k_r1_pu_mid<D, W><<<grid, kR1VThreads, smem, st>>>(a, fac, in, out);
   } else {
@@ -499,7 +529,8 @@ size_t r1_smem_bytes(const R1LevelArgs& a) {
   for (int k = 0; k < H; ++k) na *= a.W;
   for (int k = H; k < a.d; ++k) nb *= a.W;
   const size_t ts = static_cast<size_t>((na + nb) | 1);
-  if (a.warp_tiles) return sizeof(double2) * (kR1VThreads / 32) * 32 * std::max<size_t>(ts, a.FS);
+  if (a.warp_tiles)
+    return sizeof(double2) * (kR1VThreads / 32) * 2 * 32 * std::max<size_t>(ts, static_cast<size_t>((a.d * a.W) | 1));
   const size_t tabs = (static_cast<size_t>(a.gpb) << a.lg_nch) * ts;
   const size_t ngr = std::max<size_t>(1, static_cast<size_t>(a.gpb) >> a.lg_njd);  // groups a CTA's units span
   const size_t facs = (ngr << a.lg_nch) * static_cast<size_t>(a.FS);

@@ -1801,7 +1801,7 @@ std::unique_ptr<Plan> build_plan_r1(oiobf_tbf& b, i64 nv) {
     a.nunits = a.ngroups * a.njd;
     i64 nx = 1;
     for (int k = 0; k < d; ++k) nx *= a.W;
-    a.warp_tiles = l >= 1 && a.njd == 1;  // middle level: one warp per group
+    a.warp_tiles = l >= 1;  // one warp per (group, block tuple) unit
     if (!a.warp_tiles) {
       a.gpb = static_cast<int>(std::max<i64>(1, th / std::max<i64>(nx, a.nch)));  // units: <= one thread per child
       while (a.gpb > 1 && r1_smem_bytes(a) > 72 * 1024) a.gpb /= 2;

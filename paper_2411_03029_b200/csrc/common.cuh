@@ -244,6 +244,25 @@ __device__ __forceinline__ double2 green_from_coords(const KSpec& s, const doubl
   return make_double2(__ddiv_rn(cs, rho), __ddiv_rn(-sn, rho));
 }
 
+// Radon 2D entry given sin / cos(2 pi x_p) of the two target coordinates
+// (hoistable: they depend on the target index only)
+__device__ __forceinline__ double2 radon2d_entry_sc(const KSpec& s, const int* i, const int* j, double s1, double c1v,
+                                                    double s2, double c2v) {
+  const double n = static_cast<double>(s.n);
+  const i64 k1i = j[0] - 1 - s.n / 2, k2i = j[1] - 1 - s.n / 2;
+  const double k1 = static_cast<double>(k1i), k2 = static_cast<double>(k2i);
+  const double c1 = __ddiv_rn(__dadd_rn(2.0, __dmul_rn(s1, s2)), 16.0);
+  const double c2 = __ddiv_rn(__dadd_rn(2.0, __dmul_rn(c1v, c2v)), 16.0);
+  i64 num = ((i[0] - 1) * k1i + (i[1] - 1) * k2i) % s.n;
+  if (num < 0) num += s.n;
+  const double frac = __ddiv_rn(static_cast<double>(num), n);
+  const double q = __dadd_rn(__dmul_rn(__dmul_rn(__dmul_rn(c1, c1), k1), k1), __dmul_rn(__dmul_rn(__dmul_rn(c2, c2), k2), k2));
+  const double phi = __dadd_rn(frac, __dsqrt_rn(q));
+  double sn, cs;
+  sincos(__dmul_rn(2.0 * M_PI, phi), &sn, &cs);
+  return make_double2(cs, sn);
+}
+
 // i[], j[]: 1-based multi-indices
 __device__ __forceinline__ double2 kernel_entry(const KSpec& s, const int* i, const int* j) {
   const double n = static_cast<double>(s.n);
@@ -303,21 +322,10 @@ __device__ __forceinline__ double2 kernel_entry(const KSpec& s, const int* i, co
   }
   // radon 2d
   const double x1 = __ddiv_rn(static_cast<double>(i[0] - 1), n), x2 = __ddiv_rn(static_cast<double>(i[1] - 1), n);
-  const i64 k1i = j[0] - 1 - s.n / 2, k2i = j[1] - 1 - s.n / 2;
-  const double k1 = static_cast<double>(k1i), k2 = static_cast<double>(k2i);
   double s1, c1v, s2, c2v;
   sincos(__dmul_rn(2.0 * M_PI, x1), &s1, &c1v);
   sincos(__dmul_rn(2.0 * M_PI, x2), &s2, &c2v);
-  const double c1 = __ddiv_rn(__dadd_rn(2.0, __dmul_rn(s1, s2)), 16.0);
-  const double c2 = __ddiv_rn(__dadd_rn(2.0, __dmul_rn(c1v, c2v)), 16.0);
-  i64 num = ((i[0] - 1) * k1i + (i[1] - 1) * k2i) % s.n;
-  if (num < 0) num += s.n;
-  const double frac = __ddiv_rn(static_cast<double>(num), n);
-  const double q = __dadd_rn(__dmul_rn(__dmul_rn(__dmul_rn(c1, c1), k1), k1), __dmul_rn(__dmul_rn(__dmul_rn(c2, c2), k2), k2));
-  const double phi = __dadd_rn(frac, __dsqrt_rn(q));
-  double sn, cs;
-  sincos(__dmul_rn(2.0 * M_PI, phi), &sn, &cs);
-  return make_double2(cs, sn);
+  return radon2d_entry_sc(s, i, j, s1, c1v, s2, c2v);
 }
 
 inline KSpec kspec_from(const oiobf_kernel_spec& k) {

@@ -211,10 +211,22 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 3) k_panel(LevelDesc L, KS
   Bcast* bc = reinterpret_cast<Bcast*>(X + static_cast<i64>(pr) * L.wmax);
   int* sprox = reinterpret_cast<int*>(bc + 2);
   int* stgt = sprox + L.psize;
+  // Radon 2D, columns over a target mode: sin / cos(2 pi x) of each candidate
+  double* csin = reinterpret_cast<double*>(reinterpret_cast<uintptr_t>(stgt + L.wmax + 1) & ~uintptr_t{7});
+  double* ccos = csin + L.wmax;
   const SlotPos s = decode_slot(L, slot);
   const int D = 2 * L.d;
   for (int i = threadIdx.x; i < L.psize; i += NT) sprox[i] = proxies[slot * L.psize + i];
-  for (int i = threadIdx.x; i < w; i += NT) stgt[i] = targets[slot * L.wmax + i];
+  for (int i = threadIdx.x; i < w; i += NT) {
+    const int t = targets[slot * L.wmax + i];
+    stgt[i] = t;
+    if (ks.kind == OIOBF_KERNEL_RADON2D && s.skip < L.d) {
+      double sn, cs;
+      sincos(__dmul_rn(2.0 * M_PI, __ddiv_rn(static_cast<double>(t - 1), static_cast<double>(ks.n))), &sn, &cs);
+      csin[i] = sn;
+      ccos[i] = cs;
+    }
+  }
   for (int i = threadIdx.x; i < w * (w + 1) / 2; i += NT) R[i] = make_double2(0, 0);
   int cnt[kMaxModes], off[kMaxModes];
   for (int p = 0; p < D; ++p) {
@@ -272,6 +284,32 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 3) k_panel(LevelDesc L, KS
               yc[p] = (!tgt && p == q) ? v : ys[p];
             }
             e = green_from_coords(ks, xc, yc);
+          }
+          X[my_row + c * pr] = e;
+        }
+      } else if (ks.kind == OIOBF_KERNEL_RADON2D) {
+        // radon2d_entry with sin / cos(2 pi x_p) hoisted: per row for the row's
+        // target modes, per candidate column (csin / ccos) for an unfolded
+        // target mode -- the same operations as kernel_entry, so bit-identical
+        const int sk = s.skip;
+        double sx[2] = {0, 0}, cx[2] = {0, 0};
+        if (valid)
+          for (int p = 0; p < 2; ++p)
+            if (p != sk)
+              sincos(__dmul_rn(2.0 * M_PI, __ddiv_rn(static_cast<double>(ii[p] - 1), static_cast<double>(ks.n))), &sx[p],
+                     &cx[p]);
+        for (int c = my_cg; c < w; c += ncg) {
+          double2 e = make_double2(0, 0);
+          if (valid) {
+            const int t = stgt[c];
+            if (sk < 2) {
+              ii[sk] = t;
+              sx[sk] = csin[c];
+              cx[sk] = ccos[c];
+            } else {
+              jj[sk - 2] = t;
+            }
+            e = radon2d_entry_sc(ks, ii, jj, sx[0], cx[0], sx[1], cx[1]);
           }
           X[my_row + c * pr] = e;
         }
@@ -580,7 +618,7 @@ __global__ void __launch_bounds__(kThreads) k_matrix_panel(i64 nparts, i64 rpp, 
 
 size_t panel_smem_bytes(const LevelDesc& L) {
   return sizeof(double2) * (L.wmax * (L.wmax + 1) / 2 + static_cast<size_t>(L.pr) * L.wmax) + 2 * sizeof(Bcast) +
-         sizeof(int) * (L.psize + L.wmax) + 16;
+         sizeof(int) * (L.psize + L.wmax + 1) + sizeof(double) * (2 * L.wmax + 1) + 16;
 }
 
 size_t finish_smem_bytes(const LevelDesc& L) {

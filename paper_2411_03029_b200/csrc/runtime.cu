@@ -13,6 +13,7 @@
 // sums), captured once into a CUDA graph and replayed.
 #include <algorithm>
 #include <chrono>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -122,6 +123,68 @@ DevBuf<T> to_device(const std::vector<T>& v, cudaStream_t st) {
   return b;
 }
 
+// Host bookkeeping at config-4 scale (2e8 slots, 1.7e7 pairs) is dominated by
+// serial first-touch of multi-GB arrays: loops over them run on a few host
+// threads, chunked.
+template <class F>
+void parallel_chunks(size_t n, F&& fn) {  // fn(chunk index, begin, end), chunks in order
+  static const size_t nt = std::max<size_t>(1, std::min<size_t>(16, std::thread::hardware_concurrency()));
+  const size_t nc = n < (size_t{1} << 16) ? 1 : nt;
+  if (nc == 1) {
+    fn(size_t{0}, size_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (size_t c = 0; c < nc; ++c) th.emplace_back([&, c] { fn(c, n * c / nc, n * (c + 1) / nc); });
+  for (auto& t : th) t.join();
+}
+size_t parallel_nchunks(size_t n) {
+  static const size_t nt = std::max<size_t>(1, std::min<size_t>(16, std::thread::hardware_concurrency()));
+  return n < (size_t{1} << 16) ? 1 : nt;
+}
+
+// std::vector-like host array whose resize does NOT value-initialise (the
+// contents are overwritten right after); pages are first touched in parallel.
+template <class T>
+class HostArray {
+  std::unique_ptr<T[]> p_;
+  size_t n_ = 0;
+
+ public:
+  void resize(size_t n) {
+    if (n == n_) return;
+    p_.reset(n ? new T[n] : nullptr);  // default-initialised (trivial T: untouched)
+    n_ = n;
+    char* b = reinterpret_cast<char*>(p_.get());
+    parallel_chunks(n * sizeof(T), [&](size_t, size_t lo, size_t hi) {
+      for (size_t i = lo; i < hi; i += 4096) b[i] = 0;  // fault the pages in from several threads
+    });
+  }
+  void assign(size_t n, const T& v) {
+    resize(n);
+    parallel_chunks(n, [&](size_t, size_t lo, size_t hi) {
+      for (size_t i = lo; i < hi; ++i) p_[i] = v;
+    });
+  }
+  T* data() { return p_.get(); }
+  const T* data() const { return p_.get(); }
+  size_t size() const { return n_; }
+  bool empty() const { return n_ == 0; }
+  T& operator[](size_t i) { return p_[i]; }
+  const T& operator[](size_t i) const { return p_[i]; }
+  T* begin() { return p_.get(); }
+  T* end() { return p_.get() + n_; }
+  const T* begin() const { return p_.get(); }
+  const T* end() const { return p_.get() + n_; }
+};
+
+template <class T>
+DevBuf<T> to_device(const HostArray<T>& v, cudaStream_t st) {
+  DevBuf<T> b(v.size());
+  b.upload(v.data(), v.size(), st);
+  return b;
+}
+
 i64 ipow(i64 b, i64 e) {
   i64 r = 1;
   while (e-- > 0) r *= b;
@@ -183,8 +246,8 @@ struct LevelData {
   DevBuf<double2> interp;
   DevBuf<i64> skel_off, interp_off;
   DevBuf<double> gaps;
-  std::vector<int> h_rank, h_width, h_sat;
-  std::vector<i64> h_skel_off, h_interp_off;
+  HostArray<int> h_rank, h_width, h_sat;
+  HostArray<i64> h_skel_off, h_interp_off;
   i64 total_skel = 0, total_interp = 0;
   int max_rank = 0;
 };
@@ -516,7 +579,7 @@ struct oiobf_tbf {
   std::vector<LevelData> side[2];
   std::vector<i64> r_est[2];
   DevBuf<double2> cores;
-  std::vector<PairDesc> h_pairs;
+  HostArray<PairDesc> h_pairs;
   i64 total_core = 0;
   std::map<i64, std::unique_ptr<Plan>> plans;
   int apply_engine = 0;  // 0 auto, 1 box engine, 2 tiny-box engine, 3 dataflow engine, 4 rank-one engine
@@ -697,6 +760,11 @@ void finish_level(oiobf_tbf& b, LevelData& ld, DevBuf<int>& sat, DevBuf<int>& sk
   cudaStream_t st = b.stream;
   const i64 ns = ld.nslots;
   const i64 wmax = ld.L.wmax;
+  static const bool dbg = std::getenv("OIOBF_DEBUG") != nullptr;
+  auto tnow = [] { return std::chrono::steady_clock::now(); };
+  auto tms = [](auto a, auto c) { return std::chrono::duration<double, std::milli>(c - a).count(); };
+  TBF_CUDA(cudaStreamSynchronize(st));
+  const auto f0 = tnow();
   ld.h_rank.resize(static_cast<size_t>(ns));
   ld.h_width.resize(static_cast<size_t>(ns));
   ld.h_sat.resize(static_cast<size_t>(ns));
@@ -704,22 +772,52 @@ void finish_level(oiobf_tbf& b, LevelData& ld, DevBuf<int>& sat, DevBuf<int>& sk
   ld.width.download(ld.h_width.data(), static_cast<size_t>(ns), st);
   sat.download(ld.h_sat.data(), static_cast<size_t>(ns), st);
   TBF_CUDA(cudaStreamSynchronize(st));
+  const auto f1 = tnow();
   ld.h_skel_off.resize(static_cast<size_t>(ns));
   ld.h_interp_off.resize(static_cast<size_t>(ns));
-  i64 so = 0, io = 0;
+  // exclusive prefix sums of rank and rank * width: chunk totals, then chunk scans
+  const size_t nck = parallel_nchunks(static_cast<size_t>(ns));
+  std::vector<i64> cso(nck + 1, 0), cio(nck + 1, 0);
+  std::vector<int> cmr(nck, 0);
+  parallel_chunks(static_cast<size_t>(ns), [&](size_t c, size_t lo, size_t hi) {
+    i64 a = 0, bb = 0;
+    int mr = 0;
+    for (size_t i = lo; i < hi; ++i) {
+      a += ld.h_rank[i];
+      bb += static_cast<i64>(ld.h_rank[i]) * ld.h_width[i];
+      mr = std::max(mr, ld.h_rank[i]);
+    }
+    cso[c + 1] = a;
+    cio[c + 1] = bb;
+    cmr[c] = mr;
+  });
   ld.max_rank = 0;
-  for (i64 i = 0; i < ns; ++i) {
-    ld.h_skel_off[static_cast<size_t>(i)] = so;
-    ld.h_interp_off[static_cast<size_t>(i)] = io;
-    so += ld.h_rank[static_cast<size_t>(i)];
-    io += static_cast<i64>(ld.h_rank[static_cast<size_t>(i)]) * ld.h_width[static_cast<size_t>(i)];
-    ld.max_rank = std::max(ld.max_rank, ld.h_rank[static_cast<size_t>(i)]);
+  for (size_t c = 0; c < nck; ++c) {
+    cso[c + 1] += cso[c];
+    cio[c + 1] += cio[c];
+    ld.max_rank = std::max(ld.max_rank, cmr[c]);
   }
+  parallel_chunks(static_cast<size_t>(ns), [&](size_t c, size_t lo, size_t hi) {
+    i64 a = cso[c], bb = cio[c];
+    for (size_t i = lo; i < hi; ++i) {
+      ld.h_skel_off[i] = a;
+      ld.h_interp_off[i] = bb;
+      a += ld.h_rank[i];
+      bb += static_cast<i64>(ld.h_rank[i]) * ld.h_width[i];
+    }
+  });
+  const i64 so = cso[nck], io = cio[nck];
   ld.total_skel = so;
   ld.total_interp = io;
+  const auto f2 = tnow();
   EventTimer t3(st);
   ld.skel_off = to_device(ld.h_skel_off, st);
   ld.interp_off = to_device(ld.h_interp_off, st);
+  if (dbg) {
+    TBF_CUDA(cudaStreamSynchronize(st));
+    fprintf(stderr, "[oiobf] finish_level %lld slots: download %.1f ms, prefix %.1f ms, upload %.1f ms\n", ns,
+            tms(f0, f1), tms(f1, f2), tms(f2, tnow()));
+  }
   ld.skel.alloc(static_cast<size_t>(std::max<i64>(so, 1)));
   ld.interp.alloc(static_cast<size_t>(std::max<i64>(io, 1)));
   launch_compact(ns, wmax, ld.rank.p, ld.width.p, ld.skel_off.p, ld.interp_off.p, skel_tmp.p, interp_tmp.p, ld.skel.p,
@@ -743,27 +841,44 @@ i64 layout_pairs(oiobf_tbf& b) {
   const i64* uskel_off = gathered ? b.umid_skel_off.data() : U.h_skel_off.data();
   const i64 P = b.nmid * b.nmid;
   b.h_pairs.assign(static_cast<size_t>(P), PairDesc{});
-  i64 off = 0;
-  for (i64 p = 0; p < P; ++p) {
-    const i64 s = p / b.nmid, t = p % b.nmid;
-    PairDesc& pd = b.h_pairs[static_cast<size_t>(p)];
-    pd.R = 1;
-    pd.C = 1;
-    for (int k = 0; k < d; ++k) {
-      const i64 us = (t * b.nmid + s) * d + k;  // U slot (Lc, t, nu=s, k, j=0)
-      const i64 vs = (s * b.nmid + t) * d + k;  // V slot (Lc, s, tau=t, k, j=0)
-      pd.rr[k] = urank[us];
-      pd.rc[k] = V.h_rank[static_cast<size_t>(vs)];
-      pd.rs_off[k] = uskel_off[us];
-      pd.cs_off[k] = V.h_skel_off[static_cast<size_t>(vs)];
-      pd.R *= pd.rr[k];
-      pd.C *= pd.rc[k];
+  // per-pair geometry in parallel chunks, then the arena offsets (exclusive
+  // prefix of R * C) from chunk totals
+  const size_t nck = parallel_nchunks(static_cast<size_t>(P));
+  std::vector<i64> ctot(nck + 1, 0);
+  parallel_chunks(static_cast<size_t>(P), [&](size_t c, size_t lo, size_t hi) {
+    i64 sum = 0;
+    for (size_t pp = lo; pp < hi; ++pp) {
+      const i64 p = static_cast<i64>(pp);
+      const i64 s = p / b.nmid, t = p % b.nmid;
+      PairDesc& pd = b.h_pairs[pp];
+      pd.R = 1;
+      pd.C = 1;
+      for (int k = 0; k < d; ++k) {
+        const i64 us = (t * b.nmid + s) * d + k;  // U slot (Lc, t, nu=s, k, j=0)
+        const i64 vs = (s * b.nmid + t) * d + k;  // V slot (Lc, s, tau=t, k, j=0)
+        pd.rr[k] = urank[us];
+        pd.rc[k] = V.h_rank[static_cast<size_t>(vs)];
+        pd.rs_off[k] = uskel_off[us];
+        pd.cs_off[k] = V.h_skel_off[static_cast<size_t>(vs)];
+        pd.R *= pd.rr[k];
+        pd.C *= pd.rc[k];
+      }
+      if (!b.owns(s)) pd.C = 0;  // another rank generates and applies this core
+      sum += static_cast<i64>(pd.R) * pd.C;
     }
-    if (!b.owns(s)) pd.C = 0;  // another rank generates and applies this core
-    pd.core_off = off;
-    pd.work_off = off;
-    off += static_cast<i64>(pd.R) * pd.C;
-  }
+    ctot[c + 1] = sum;
+  });
+  for (size_t c = 0; c < nck; ++c) ctot[c + 1] += ctot[c];
+  parallel_chunks(static_cast<size_t>(P), [&](size_t c, size_t lo, size_t hi) {
+    i64 o = ctot[c];
+    for (size_t pp = lo; pp < hi; ++pp) {
+      PairDesc& pd = b.h_pairs[pp];
+      pd.core_off = o;
+      pd.work_off = o;
+      o += static_cast<i64>(pd.R) * pd.C;
+    }
+  });
+  const i64 off = ctot[nck];
   b.total_core = off;
   return off;
 }
@@ -775,9 +890,18 @@ void build_cores(oiobf_tbf& b) {
   const bool gathered = b.world > 1;
   const int* uskel = gathered ? b.umid_skel.p : U.skel.p;
   const i64 P = b.nmid * b.nmid;
+  static const bool dbg = std::getenv("OIOBF_DEBUG") != nullptr;
+  auto tnow = [] { return std::chrono::steady_clock::now(); };
+  auto tms = [](auto a, auto c) { return std::chrono::duration<double, std::milli>(c - a).count(); };
+  const auto c0 = tnow();
   const i64 off = layout_pairs(b);
+  const auto c1 = tnow();
   b.cores.alloc(static_cast<size_t>(std::max<i64>(off, 1)));
   DevBuf<PairDesc> dp = to_device(b.h_pairs, st);
+  if (dbg) {
+    TBF_CUDA(cudaStreamSynchronize(st));
+    fprintf(stderr, "[oiobf] cores: layout %.1f ms, upload %.1f ms (%lld pairs)\n", tms(c0, c1), tms(c1, tnow()), P);
+  }
   EventTimer t(st);
   launch_cores(b.ks, P, dp.p, off, uskel, V.skel.p, b.cores.p, st);
   b.t_ms[4] += t.stop();
@@ -1688,18 +1812,26 @@ bool r1_eligible(const oiobf_tbf& b) {
       const int w = l == 0 ? static_cast<int>(leaf) : 2;
       if (static_cast<i64>(ld.h_rank.size()) != ld.nslots || static_cast<i64>(ld.h_interp_off.size()) != ld.nslots)
         return false;
-      for (i64 sl = 0; sl < ld.nslots; ++sl) {
-        const size_t i = static_cast<size_t>(sl);
-        if (ld.h_rank[i] != 1 || ld.h_width[i] != w || ld.h_interp_off[i] != sl * w) return false;
-      }
+      std::vector<char> bad(parallel_nchunks(static_cast<size_t>(ld.nslots)), 0);
+      parallel_chunks(static_cast<size_t>(ld.nslots), [&](size_t c, size_t lo, size_t hi) {
+        for (size_t i = lo; i < hi && !bad[c]; ++i)
+          bad[c] = ld.h_rank[i] != 1 || ld.h_width[i] != w || ld.h_interp_off[i] != static_cast<i64>(i) * w;
+      });
+      for (char x : bad)
+        if (x) return false;
     }
   }
   const i64 P = b.nmid * b.nmid;
   if (static_cast<i64>(b.h_pairs.size()) != P) return false;
-  for (i64 p = 0; p < P; ++p) {
-    const PairDesc& pd = b.h_pairs[static_cast<size_t>(p)];
-    if (pd.R != 1 || pd.C != 1 || pd.core_off != p) return false;
-  }
+  std::vector<char> bad(parallel_nchunks(static_cast<size_t>(P)), 0);
+  parallel_chunks(static_cast<size_t>(P), [&](size_t c, size_t lo, size_t hi) {
+    for (size_t p = lo; p < hi && !bad[c]; ++p) {
+      const PairDesc& pd = b.h_pairs[p];
+      bad[c] = pd.R != 1 || pd.C != 1 || pd.core_off != static_cast<i64>(p);
+    }
+  });
+  for (char x : bad)
+    if (x) return false;
   return true;
 }
 

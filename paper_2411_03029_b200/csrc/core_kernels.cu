@@ -5,6 +5,8 @@
 // Cores are stored ROW-major (one contiguous row per target skeleton
 // multi-index), i.e. the transpose of the reference's column-major
 // matricization, so the apply GEMV streams each row with coalesced 16-B loads.
+#include <cub/cub.cuh>
+
 #include "kernels.h"
 
 namespace tbf {
@@ -161,6 +163,87 @@ void launch_dense_rows(const KSpec& ks, i64 nrows, const i64* rows, const double
   for (int p = 0; p < ks.d; ++p) N *= ks.n;
   k_dense_rows<<<static_cast<unsigned>(nrows), 512, 0, st>>>(ks, rows, F, nv, N, out, nrows);
   TBF_CUDA(cudaGetLastError());
+}
+
+
+// ---- device-side bookkeeping (construction at config-4 scale: 1e8 slots /
+// 1.7e7 pairs per level would otherwise be uploaded from host mirrors)
+namespace {
+__global__ void k_slot_sizes(i64 n, const int* __restrict__ rank, const int* __restrict__ width, i64* __restrict__ a,
+                             i64* __restrict__ b) {
+  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  a[i] = rank[i];
+  b[i] = static_cast<i64>(rank[i]) * width[i];
+}
+__global__ void k_layout_pairs(int d, i64 nmid, const int* __restrict__ urank, const i64* __restrict__ uskel_off,
+                               const int* __restrict__ vrank, const i64* __restrict__ vskel_off,
+                               PairDesc* __restrict__ pairs, i64* __restrict__ work) {
+  const i64 p = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= nmid * nmid) return;
+  const i64 s = p / nmid, t = p % nmid;
+  PairDesc pd;
+  pd.R = 1;
+  pd.C = 1;
+  for (int k = 0; k < kMaxD; ++k) {
+    pd.rr[k] = pd.rc[k] = 0;
+    pd.rs_off[k] = pd.cs_off[k] = 0;
+  }
+  for (int k = 0; k < d; ++k) {
+    const i64 us = (t * nmid + s) * d + k;  // U slot (Lc, t, nu=s, k, j=0)
+    const i64 vs = (s * nmid + t) * d + k;  // V slot (Lc, s, tau=t, k, j=0)
+    pd.rr[k] = urank[us];
+    pd.rc[k] = vrank[vs];
+    pd.rs_off[k] = uskel_off[us];
+    pd.cs_off[k] = vskel_off[vs];
+    pd.R *= pd.rr[k];
+    pd.C *= pd.rc[k];
+  }
+  pd.core_off = 0;
+  pd.work_off = 0;
+  pairs[p] = pd;
+  work[p] = static_cast<i64>(pd.R) * pd.C;
+}
+__global__ void k_pair_offsets(i64 np, const i64* __restrict__ off, PairDesc* __restrict__ pairs) {
+  const i64 p = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= np) return;
+  pairs[p].core_off = off[p];
+  pairs[p].work_off = off[p];
+}
+template <class T>
+void exclusive_sum(const i64* in, i64* out, i64 n, cudaStream_t st, T) {
+  size_t bytes = 0;
+  TBF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, st));
+  void* tmp = nullptr;
+  TBF_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(bytes, 16), st));
+  TBF_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, n, st));
+  TBF_CUDA(cudaFreeAsync(tmp, st));
+}
+}  // namespace
+
+void scan_slot_offsets(i64 n, const int* rank, const int* width, i64* skel_off, i64* interp_off, cudaStream_t st) {
+  if (n == 0) return;
+  i64* a = nullptr;
+  TBF_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a), sizeof(i64) * 2 * n, st));
+  k_slot_sizes<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(n, rank, width, a, a + n);
+  TBF_CUDA(cudaGetLastError());
+  exclusive_sum(a, skel_off, n, st, 0);
+  exclusive_sum(a + n, interp_off, n, st, 0);
+  TBF_CUDA(cudaFreeAsync(a, st));
+}
+
+void layout_pairs_device(int d, i64 nmid, const int* urank, const i64* uskel_off, const int* vrank,
+                         const i64* vskel_off, PairDesc* pairs, cudaStream_t st) {
+  const i64 np = nmid * nmid;
+  i64* w = nullptr;
+  TBF_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&w), sizeof(i64) * 2 * np, st));
+  k_layout_pairs<<<static_cast<unsigned>((np + 255) / 256), 256, 0, st>>>(d, nmid, urank, uskel_off, vrank, vskel_off,
+                                                                          pairs, w);
+  TBF_CUDA(cudaGetLastError());
+  exclusive_sum(w, w + np, np, st, 0);
+  k_pair_offsets<<<static_cast<unsigned>((np + 255) / 256), 256, 0, st>>>(np, w + np, pairs);
+  TBF_CUDA(cudaGetLastError());
+  TBF_CUDA(cudaFreeAsync(w, st));
 }
 
 }  // namespace tbf

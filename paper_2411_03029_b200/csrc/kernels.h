@@ -46,6 +46,11 @@ struct PairDesc {
 };
 void launch_cores(const KSpec& ks, i64 npairs, const PairDesc* pairs, i64 total_entries, const int* uskel,
                   const int* vskel, double2* cores, cudaStream_t st);
+// device-side bookkeeping: exclusive prefix sums of rank and rank * width per
+// slot; middle-pair layout (same values as the host layout_pairs, world = 1)
+void scan_slot_offsets(i64 n, const int* rank, const int* width, i64* skel_off, i64* interp_off, cudaStream_t st);
+void layout_pairs_device(int d, i64 nmid, const int* urank, const i64* uskel_off, const int* vrank,
+                         const i64* vskel_off, PairDesc* pairs, cudaStream_t st);
 
 // ---- apply (apply_kernels.cu)
 constexpr int kMaxTM = kMaxD + 1;  // tensor modes incl. n_v

@@ -811,8 +811,10 @@ void finish_level(oiobf_tbf& b, LevelData& ld, DevBuf<int>& sat, DevBuf<int>& sk
   ld.total_interp = io;
   const auto f2 = tnow();
   EventTimer t3(st);
-  ld.skel_off = to_device(ld.h_skel_off, st);
-  ld.interp_off = to_device(ld.h_interp_off, st);
+  // the device offsets are scanned on the device (same integers as the host mirror)
+  ld.skel_off.alloc(static_cast<size_t>(ns));
+  ld.interp_off.alloc(static_cast<size_t>(ns));
+  scan_slot_offsets(ns, ld.rank.p, ld.width.p, ld.skel_off.p, ld.interp_off.p, st);
   if (dbg) {
     TBF_CUDA(cudaStreamSynchronize(st));
     fprintf(stderr, "[oiobf] finish_level %lld slots: download %.1f ms, prefix %.1f ms, upload %.1f ms\n", ns,
@@ -897,7 +899,13 @@ void build_cores(oiobf_tbf& b) {
   const i64 off = layout_pairs(b);
   const auto c1 = tnow();
   b.cores.alloc(static_cast<size_t>(std::max<i64>(off, 1)));
-  DevBuf<PairDesc> dp = to_device(b.h_pairs, st);
+  DevBuf<PairDesc> dp;
+  if (gathered) {
+    dp = to_device(b.h_pairs, st);
+  } else {  // same layout computed on the device: no multi-GB upload at config-4 scale
+    dp.alloc(static_cast<size_t>(P));
+    layout_pairs_device(b.d, b.nmid, U.rank.p, U.skel_off.p, V.rank.p, V.skel_off.p, dp.p, st);
+  }
   if (dbg) {
     TBF_CUDA(cudaStreamSynchronize(st));
     fprintf(stderr, "[oiobf] cores: layout %.1f ms, upload %.1f ms (%lld pairs)\n", tms(c0, c1), tms(c1, tnow()), P);

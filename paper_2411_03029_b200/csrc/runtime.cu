@@ -1165,6 +1165,22 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked) {
     bl.info.smem_mat = static_cast<int>(smem_mat);
     bl.info.smem_in = static_cast<int>(smem_in);
     bl.info.smem_t = static_cast<int>(smem_t);
+    if (std::getenv("OIOBF_DEBUG")) {
+      i64 ein = 0, eout = 0;
+      for (const BoxDesc& x : descs) {
+        i64 a = 1, c = 1;
+        for (int k = 0; k < d; ++k) {
+          a *= x.ein[k];
+          c *= x.eout[k];
+        }
+        ein = std::max(ein, a);
+        eout = std::max(eout, c);
+      }
+      fprintf(stderr, "[oiobf] box side %d level %d: %lld boxes x cs %d (amax %d, stage %d), max box in %lld out %lld, "
+              "smem %lld B, ef %d..%d\n", sd, l, static_cast<long long>(nitems), cs, amax_rows, stage ? 1 : 0,
+              static_cast<long long>(ein), static_cast<long long>(eout),
+              static_cast<long long>(16 * (smem_mat + smem_in + 2 * smem_t)), ef_min, ef_max);
+    }
     pl->bdescs.insert(pl->bdescs.end(), descs.begin(), descs.end());
     pl->ops.push_back(Op{3, static_cast<i64>(pl->boxes.size()), group});
     pl->boxes.push_back(bl);

@@ -369,7 +369,7 @@ def run_b200_sharded(args):
 
     import paper_2411_03029_b200 as tb
     from paper_2411_03029_b200 import _lib
-    from paper_2411_03029_b200.sharded import GpuShardBackend, TorchComm, construct
+    from paper_2411_03029_b200.sharded import GpuShardBackend, PeerExchange, TorchComm, construct
 
     ws, rank, local = dist_env()
     verbose = os.environ.get("OIOBF_BENCH_VERBOSE") is not None
@@ -422,7 +422,30 @@ def run_b200_sharded(args):
     sh = stream.cuda_stream
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
+    # exchange: fused by default -- the phase-1 core GEMV stores G_{t,s} straight
+    # into the owners' receive buffers (CUDA IPC peer memory over NVLink), one
+    # barrier per step; OIOBF_EXCHANGE=nccl selects send buffer + NCCL all-to-all
+    px = None
+    exchange = "nccl all_to_all_single of the send buffer"
+    if os.environ.get("OIOBF_EXCHANGE", "fused") != "nccl":
+        try:
+            px = PeerExchange(sb, comm, nv_max=args.nv)
+            exchange = "fused: core GEMV epilogue stores into peer receive buffers (CUDA IPC), 1 barrier per step"
+        except Exception as e:  # e.g. no IPC between these devices: the all-to-all path
+            stage(f"fused exchange unavailable ({e}); NCCL all-to-all")
+            px = None
+        ok = torch.tensor([0 if px is None else 1], dtype=torch.int64, device="cpu" if comm.host else dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0 and px is not None:  # every rank must take the same path
+            px.close()
+            px = None
+            exchange = "nccl all_to_all_single of the send buffer"
+    stage(f"exchange: {exchange}")
+
     def step():
+        if px is not None:
+            px.step(F.data_ptr(), G.data_ptr(), args.nv, sh)
+            return
         be.phase(1, F.data_ptr(), send.data_ptr(), args.nv, sh)
         comm.alltoall(send, recv, lay.send_counts * args.nv, lay.recv_counts * args.nv)
         be.phase(2, recv.data_ptr(), G.data_ptr(), args.nv, sh)
@@ -495,7 +518,7 @@ def run_b200_sharded(args):
             "data": "synthetic (seeded complex normal input; operator from the BASELINE formula)",
             "config": {"workload": cfg.name, "points": cfg.points, "tol": cfg.tol, "L": cfg.L, "nv": args.nv,
                        "l2": "flushed (256 MiB write) before every timed step",
-                       "parallelism": f"sharded x{ws}: middle multi-sets round-robin, 1 NCCL all-to-all per step"},
+                       "parallelism": f"sharded x{ws}: middle multi-sets round-robin", "exchange": exchange},
             "e2e": {"value": N / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step": 16 * N,
                     "d2h_bytes_per_step": 16 * N},
             "exchange_bytes_per_step_rank0": int(16 * lay.send_counts.sum() * args.nv),
@@ -507,6 +530,10 @@ def run_b200_sharded(args):
             "cpu_baseline": None,
         }
         print(json.dumps(out), flush=True)
+    dist.barrier()
+    if px is not None:
+        torch.cuda.synchronize()
+        px.close()
     dist.barrier()
     dist.destroy_process_group()
     return 0

@@ -211,6 +211,25 @@ int oiobf_tbf_set_exchange(oiobf_tbf* h, const int64_t* send_off, const int64_t*
                            int64_t recv_elems);
 int oiobf_tbf_contract_phase(oiobf_tbf* h, int32_t phase, const void* dIn, void* dOut, int64_t nv, void* stream);
 
+// Fused exchange (replaces the all-to-all between the phases): the phase-1 core
+// GEMV stores every block G_{t,s} straight into the receive buffer of the
+// owner of t (peer memory over NVLink, mapped with oiobf_ipc_open).
+// recv_base[par * world + q] = device address (in this process) of rank q's
+// receive buffer of parity par (0/1: consecutive steps alternate, so a step's
+// stores never overwrite a buffer a peer is still reading); peer_off[t * nmid
+// + s] = element offset (n_v = 1) of block (t, s) in its owner's receive
+// buffer, for the pairs whose s this rank owns (-1 elsewhere); nv_max bounds
+// n_v.  Phase 1 is then called with dOut = recv_base[par * world + rank].
+// recv_base = NULL returns to the send buffer + all-to-all path.
+int oiobf_tbf_set_peer_exchange(oiobf_tbf* h, const int64_t* peer_off, const uint64_t* recv_base, int32_t world,
+                                int64_t nv_max);
+// device buffers with a stable base address (for IPC) and CUDA IPC handles
+int oiobf_device_alloc(int64_t bytes, void** out);
+int oiobf_device_free(void* p);
+int oiobf_ipc_handle(void* p, uint8_t handle[64]);
+int oiobf_ipc_open(const uint8_t handle[64], void** out);
+int oiobf_ipc_close(void* p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -576,6 +576,11 @@ struct oiobf_tbf {
   // exchange tables (element offsets per pair t*nmid+s, nv = 1 units), -1 = none
   std::vector<i64> send_off, recv_off;
   i64 send_elems = 0, recv_elems = 0;
+  // fused exchange: phase-1 GEMV stores into the owners' receive buffers
+  std::vector<i64> peer_off;        // per pair (t * nmid + s): offset in the owner's buffer (nv = 1)
+  std::vector<u64> peer_base;       // [parity * world + q]: receive buffer addresses
+  i64 peer_nv_max = 0;
+  bool peer_mode() const { return !peer_base.empty(); }
   std::vector<LevelData> side[2];
   std::vector<i64> r_est[2];
   DevBuf<double2> cores;
@@ -1021,7 +1026,7 @@ MPStep make_step(const TRef& in, const TRef& out, int mode, int transpose) {
   return s;
 }
 
-std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked) {
+std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity = 0) {
   auto pl = std::make_unique<Plan>();
   pl->nv = nv;
   pl->nchunk = chunked && b.world == 1 ? static_cast<int>(ipow(2, b.Lc)) : 1;
@@ -1339,7 +1344,19 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked) {
       const PairDesc& pd = b.h_pairs[static_cast<size_t>(p)];
       const TRef& x = wout[static_cast<size_t>(s * b.nmid + t)];
       TRef y;
-      if (sharded) {  // GEMV output goes straight into the send buffer
+      if (sharded && b.peer_mode()) {
+        // fused exchange: the GEMV stores G_{t,s} into the receive buffer of
+        // the owner q of t (peer memory), addressed relative to this rank's own
+        // receive buffer of the same parity (the phase-1 output pointer)
+        const i64 po = b.peer_off[static_cast<size_t>(t * b.nmid + s)];
+        require(po >= 0, "sharded contract: missing peer offset");
+        const int q = static_cast<int>(t % b.world);
+        const u64 mine_base = b.peer_base[static_cast<size_t>(parity * b.world + b.rank)];
+        const u64 dest_base = b.peer_base[static_cast<size_t>(parity * b.world + q)];
+        const i64 delta = static_cast<i64>(dest_base - mine_base);
+        require(delta % 16 == 0, "sharded contract: receive buffers must be 16-byte aligned");
+        y = packed(delta / 16 + po * nv, nd, gext);
+      } else if (sharded) {  // GEMV output goes straight into the send buffer
         const i64 so = b.send_off[static_cast<size_t>(t * b.nmid + s)];
         require(so >= 0, "sharded contract: missing send offset");
         y = packed(so * nv, nd, gext);
@@ -1973,15 +1990,16 @@ std::unique_ptr<Plan> build_plan_r1(oiobf_tbf& b, i64 nv) {
 
 // chunked = true: the host-pipelined plan (ops per slab group, see
 // contract_host); the device-buffer path uses the unchunked plan
-Plan& get_plan(oiobf_tbf& b, i64 nv, bool chunked = false) {
+// parity: fused-exchange plans (receive buffers alternate between steps)
+Plan& get_plan(oiobf_tbf& b, i64 nv, bool chunked = false, int parity = 0) {
   const bool r1 = use_r1_engine(b);
   const bool tiny = !r1 && use_tiny_engine(b);
   if (tiny || r1) chunked = false;  // one slab group: these plans are not split
-  const i64 key = 2 * nv + (chunked ? 1 : 0);
+  const i64 key = 4 * nv + 2 * parity + (chunked ? 1 : 0);
   auto it = b.plans.find(key);
   if (it != b.plans.end()) return *it->second;
   auto& slot = b.plans[key];
-  slot = r1 ? build_plan_r1(b, nv) : tiny ? build_plan_tiny(b, nv) : build_plan(b, nv, chunked);
+  slot = r1 ? build_plan_r1(b, nv) : tiny ? build_plan_tiny(b, nv) : build_plan(b, nv, chunked, parity);
   return *slot;
 }
 
@@ -3066,6 +3084,73 @@ int oiobf_tbf_set_exchange(oiobf_tbf* h, const int64_t* send_off, const int64_t*
   CAPI_END
 }
 
+int oiobf_tbf_set_peer_exchange(oiobf_tbf* h, const int64_t* peer_off, const uint64_t* recv_base, int32_t world,
+                                int64_t nv_max) {
+  CAPI_BEGIN
+  require(h, "tbf_set_peer_exchange: null handle");
+  if (!recv_base) {  // back to the send buffer + all-to-all path
+    std::lock_guard<std::mutex> lk(h->mu);
+    h->sync_all();
+    h->plans.clear();
+    h->peer_off.clear();
+    h->peer_base.clear();
+    h->peer_nv_max = 0;
+    return OIOBF_OK;
+  }
+  require(peer_off, "tbf_set_peer_exchange: null argument");
+  require(world == h->world && world > 1, "tbf_set_peer_exchange: world must match the sharded factorization");
+  require(nv_max >= 1, "tbf_set_peer_exchange: nv_max must be >= 1");
+  std::lock_guard<std::mutex> lk(h->mu);
+  const i64 P = h->nmid * h->nmid;
+  h->sync_all();
+  h->plans.clear();
+  h->peer_off.assign(peer_off, peer_off + P);
+  h->peer_base.assign(recv_base, recv_base + 2 * world);
+  h->peer_nv_max = nv_max;
+  for (u64 a : h->peer_base) require(a != 0 && a % 16 == 0, "tbf_set_peer_exchange: bad receive buffer address");
+  CAPI_END
+}
+
+int oiobf_device_alloc(int64_t bytes, void** out) {
+  CAPI_BEGIN
+  require(out && bytes > 0, "device_alloc: bad argument");
+  ensure_device();
+  TBF_CUDA(cudaMalloc(out, static_cast<size_t>(bytes)));
+  CAPI_END
+}
+
+int oiobf_device_free(void* p) {
+  CAPI_BEGIN
+  if (p) TBF_CUDA(cudaFree(p));
+  CAPI_END
+}
+
+int oiobf_ipc_handle(void* p, uint8_t handle[64]) {
+  CAPI_BEGIN
+  require(p && handle, "ipc_handle: null argument");
+  cudaIpcMemHandle_t hd;
+  TBF_CUDA(cudaIpcGetMemHandle(&hd, p));
+  static_assert(sizeof(hd) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle, &hd, 64);
+  CAPI_END
+}
+
+int oiobf_ipc_open(const uint8_t handle[64], void** out) {
+  CAPI_BEGIN
+  require(handle && out, "ipc_open: null argument");
+  ensure_device();
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle, 64);
+  TBF_CUDA(cudaIpcOpenMemHandle(out, hd, cudaIpcMemLazyEnablePeerAccess));
+  CAPI_END
+}
+
+int oiobf_ipc_close(void* p) {
+  CAPI_BEGIN
+  if (p) TBF_CUDA(cudaIpcCloseMemHandle(p));
+  CAPI_END
+}
+
 // phase 1: dIn = F (n^d x nv), dOut = send buffer; phase 2: dIn = receive
 // buffer, dOut = G (only this rank's row slabs are written)
 int oiobf_tbf_contract_phase(oiobf_tbf* h, int32_t phase, const void* dIn, void* dOut, int64_t nv, void* stream) {
@@ -3075,7 +3160,17 @@ int oiobf_tbf_contract_phase(oiobf_tbf* h, int32_t phase, const void* dIn, void*
   require(nv >= 1, "tbf_contract: nv must be >= 1");
   std::lock_guard<std::mutex> lk(h->mu);
   TBF_CUDA(cudaSetDevice(h->device));
-  Plan& pl = get_plan(*h, nv);
+  int parity = 0;
+  if (h->peer_mode() && phase == 1) {  // dOut names the parity: this rank's own receive buffer
+    const u64 a = reinterpret_cast<u64>(dOut);
+    const u64 own0 = h->peer_base[static_cast<size_t>(h->rank)];
+    const u64 own1 = h->peer_base[static_cast<size_t>(h->world + h->rank)];
+    require(a == own0 || a == own1,
+            "tbf_contract_phase: with a fused exchange, phase 1 writes this rank's own receive buffer");
+    require(nv <= h->peer_nv_max, "tbf_contract_phase: nv exceeds the receive buffers (nv_max)");
+    parity = a == own0 ? 0 : 1;
+  }
+  Plan& pl = get_plan(*h, nv, false, parity);
   OpBuffers io;
   if (phase == 1) {
     io.F = static_cast<const double2*>(dIn);

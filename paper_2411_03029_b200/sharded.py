@@ -141,6 +141,12 @@ def _declare(Lb):
     Lb.oiobf_tbf_umid_import.argtypes = [C.c_void_p, i64p, i32p, C.c_int64]
     Lb.oiobf_tbf_set_exchange.argtypes = [C.c_void_p, i64p, i64p, C.c_int64, C.c_int64]
     Lb.oiobf_tbf_contract_phase.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+    Lb.oiobf_tbf_set_peer_exchange.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64]
+    Lb.oiobf_device_alloc.argtypes = [C.c_int64, C.POINTER(C.c_void_p)]
+    Lb.oiobf_device_free.argtypes = [C.c_void_p]
+    Lb.oiobf_ipc_handle.argtypes = [C.c_void_p, C.c_char_p]
+    Lb.oiobf_ipc_open.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+    Lb.oiobf_ipc_close.argtypes = [C.c_void_p]
     Lb._shard_declared = True
 
 
@@ -179,6 +185,22 @@ class TorchComm:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return t.cpu().numpy()
 
+    def allgather_bytes(self, b: bytes) -> list:
+        out = [None] * self.dist.get_world_size(self.group)
+        self.dist.all_gather_object(out, b, group=self.group)
+        return out
+
+    def barrier(self):
+        """Stream-ordered on NCCL (a one-element all-reduce on the current
+        stream); host-synchronous on gloo (validation runs on one GPU)."""
+        import torch
+        if self.host:
+            torch.cuda.synchronize()
+            self.dist.barrier(group=self.group)
+        else:
+            t = torch.zeros(1, dtype=torch.float32, device=self.device)
+            self.dist.all_reduce(t, group=self.group)
+
     def alltoall(self, send, recv, send_counts, recv_counts):
         """send/recv: float64 tensors (complex interleaved); counts in complex elements."""
         rs, ss = [2 * int(c) for c in recv_counts], [2 * int(c) for c in send_counts]
@@ -188,6 +210,83 @@ class TorchComm:
             recv.copy_(r)
         else:
             self.dist.all_to_all_single(recv, send, rs, ss, group=self.group)
+
+
+def peer_offsets(R: np.ndarray, rank: int, world: int) -> np.ndarray:
+    """For the fused exchange: element offset (n_v = 1) of every block (t, s)
+    this rank produces (s owned) inside the receive buffer of its destination
+    (the owner of t) -- the destination's own `exchange_layout` receive
+    offsets, so sender and receiver agree without exchanging metadata."""
+    nmid = R.shape[0]
+    off = np.full(nmid * nmid, -1, np.int64)
+    for q in range(world):
+        rq = exchange_layout(R, q, world).recv_off
+        for t in range(nmid):
+            if not owns(t, q, world):
+                continue
+            for s in range(nmid):
+                if owns(s, rank, world):
+                    off[t * nmid + s] = rq[t * nmid + s]
+    return off
+
+
+class PeerExchange:
+    """Fused exchange (GpuShardBackend): the phase-1 core GEMV stores every
+    block G_{t,s} straight into the receive buffer of the owner of t -- peer
+    memory over NVLink, mapped through CUDA IPC -- instead of a send buffer
+    followed by an all-to-all.  Two receive buffers per rank alternate between
+    steps, so one barrier per step (after phase 1) orders everything: a step's
+    stores never touch the buffer a peer's phase 2 may still be reading."""
+
+    def __init__(self, sb: "ShardedButterfly", comm, nv_max: int = 1):
+        Lb = _lib.load()
+        _declare(Lb)
+        self.sb, self.comm, self.nv_max = sb, comm, nv_max
+        lay = sb.layout
+        nbytes = 16 * max(1, int(lay.recv_counts.sum())) * nv_max
+        self.own, self.opened = [], []
+        for _ in range(2):
+            p = C.c_void_p()
+            _lib.check(Lb.oiobf_device_alloc(nbytes, C.byref(p)))
+            self.own.append(int(p.value))
+        hs = b""
+        for p in self.own:
+            buf = C.create_string_buffer(64)
+            _lib.check(Lb.oiobf_ipc_handle(C.c_void_p(p), buf))
+            hs += buf.raw
+        allh = comm.allgather_bytes(hs)
+        world, rank = sb.world, sb.rank
+        base = np.zeros(2 * world, np.uint64)
+        for q in range(world):
+            for par in range(2):
+                if q == rank:
+                    base[par * world + q] = self.own[par]
+                else:
+                    p = C.c_void_p()
+                    _lib.check(Lb.oiobf_ipc_open(allh[q][64 * par: 64 * (par + 1)], C.byref(p)))
+                    self.opened.append(int(p.value))
+                    base[par * world + q] = int(p.value)
+        off = np.ascontiguousarray(peer_offsets(sb.R, rank, world), np.int64)
+        _lib.check(Lb.oiobf_tbf_set_peer_exchange(sb.be.h, C.c_void_p(off.ctypes.data), C.c_void_p(base.ctypes.data),
+                                                  world, nv_max))
+        self.parity = 0
+
+    def step(self, F_ptr: int, G_ptr: int, nv: int = 1, stream: int = 0):
+        buf = self.own[self.parity]
+        self.sb.be.phase(1, F_ptr, buf, nv, stream)
+        self.comm.barrier()  # every rank's GEMV stores have landed
+        self.sb.be.phase(2, buf, G_ptr, nv, stream)
+        self.parity ^= 1
+
+    def close(self):
+        Lb = _lib.load()
+        if self.own:  # the handle goes back to the send buffer + all-to-all path
+            _lib.check(Lb.oiobf_tbf_set_peer_exchange(self.sb.be.h, None, None, self.sb.world, 0))
+        for p in self.opened:
+            Lb.oiobf_ipc_close(C.c_void_p(p))
+        for p in self.own:
+            Lb.oiobf_device_free(C.c_void_p(p))
+        self.opened, self.own = [], []
 
 
 def construct(backend, rank: int, world: int, comm) -> ShardedButterfly:

@@ -211,3 +211,43 @@ def test_bench_sharded_torchrun_validation():
     assert line["n_gpus"] == 2 and line["dist_backend"] == "gloo"
     assert line["sampled_rel_err_vs_dense"] < 1e-4
     assert line["gpu_launches"] > 0
+
+
+def test_peer_offsets_match_receivers():
+    """Fused exchange: the offset at which a producer stores block (t, s) in
+    the owner of t's receive buffer is that owner's own receive offset."""
+    from paper_2411_03029_b200.sharded import exchange_layout, owns, peer_offsets
+    rng = np.random.default_rng(0)
+    for world in (2, 3, 4, 8):
+        nmid = 8
+        R = rng.integers(1, 6, (nmid, nmid))
+        lays = [exchange_layout(R, q, world) for q in range(world)]
+        for r in range(world):
+            off = peer_offsets(R, r, world)
+            for t in range(nmid):
+                for s in range(nmid):
+                    if owns(s, r, world):
+                        assert off[t * nmid + s] == lays[t % world].recv_off[t * nmid + s] >= 0
+                    else:
+                        assert off[t * nmid + s] == -1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_exchange_equals_alltoall(world):
+    """The fused exchange (phase-1 GEMV storing G_{t,s} into the owners'
+    receive buffers through CUDA IPC, two alternating buffers) gives the same
+    G bit for bit as the send buffer + all-to-all path, nv = 1, 2, three
+    consecutive steps (both parities).  Validation mode: all ranks on device 0,
+    gloo host barriers -- no kernel waits on another rank."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, OIOBF_BENCH_DIST="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(world),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "tools/peer_check.py"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=400)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["world"] == world and line["fused_equals_alltoall"], line

@@ -66,7 +66,7 @@ int box_ctas_per_sm(int amax, size_t smem) {
 
 size_t box_smem_bytes(const BoxLaunchInfo& info) {
   return sizeof(double2) * (static_cast<size_t>(info.smem_mat) + static_cast<size_t>(info.smem_in) +
-                            2 * static_cast<size_t>(info.smem_t));
+                            static_cast<size_t>(info.smem_t) + static_cast<size_t>(info.smem_t1));
 }
 
 void launch_box(i64 nitems, const BoxDesc* descs, const BoxLaunchInfo& info, const double2* mats,

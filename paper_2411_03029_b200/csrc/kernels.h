@@ -114,8 +114,8 @@ struct BoxLaunchInfo {
   int d, nv, transpose, cs;  // cs: CTAs per box (split of mode d-1's output)
   int amax;                  // max output rows of mode d-1 per CTA (template bucket: 2, 4 or 8)
   int stage;                 // 1: stage the whole input box in shared memory (cp.async)
-  int smem_mat, smem_in, smem_t;  // elements: factors, staged input, each intermediate
-  int pad;
+  int smem_mat, smem_in, smem_t;  // elements: factors, staged input, intermediate buffer t0
+  int smem_t1;                    // elements of intermediate buffer t1 (odd middle modes, staging table)
 };
 void launch_box(i64 nitems, const BoxDesc* descs, const BoxLaunchInfo& info, const double2* mats,
                 const double2* in, double2* out, cudaStream_t st);

@@ -1098,8 +1098,9 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
     }
     struct Cfg {
       int cs = 0, amax_rows = 0;
-      i64 smem_mat = 0, smem_in = 0, smem_t = 0;
+      i64 smem_mat = 0, smem_in = 0, smem_t = 0, smem_t1 = 0;  // t0: modes f, f-2, ...; t1: f-1, f-3, ...
       bool stage = false, fits = false;
+      i64 total() const { return smem_mat + smem_in + smem_t + smem_t1; }
     };
     auto size_for = [&](int cs) {
       Cfg c;
@@ -1114,19 +1115,24 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
         }
         c.smem_mat = std::max(c.smem_mat, m);
         c.smem_in = std::max(c.smem_in, in_sz);
-        i64 t = rs * c.amax_rows * nv;  // after mode d-1
+        i64 t = rs * c.amax_rows * nv;  // after mode d-1 (buffer t0)
         c.smem_t = std::max(c.smem_t, t);
-        for (int k = f - 1; k >= 1; --k) {  // after mode k
+        int buf = 1;
+        for (int k = f - 1; k >= 1; --k, buf ^= 1) {  // after mode k: the other buffer
           t = t / std::max(1, x.ein[k]) * x.eout[k];
-          c.smem_t = std::max(c.smem_t, t);
+          i64& slot = buf ? c.smem_t1 : c.smem_t;
+          slot = std::max(slot, t);
         }
-        // staging keeps a table of mode-0 row offsets (8 B each) in the second buffer
-        c.smem_t = std::max(c.smem_t, (in_sz / std::max(1, x.ein[0]) + 1) / 2);
+        // staging keeps a table of mode-0 row offsets (8 B each) in buffer t1
+        c.smem_t1 = std::max(c.smem_t1, (in_sz / std::max(1, x.ein[0]) + 1) / 2);
       }
-      // stage the input when two CTAs per SM still fit (always for child sums)
-      c.stage = sums || (c.smem_mat + c.smem_in + 2 * c.smem_t) * 16 <= 112 * 1024;
+      // stage the input when two CTAs per SM still fit (always for child sums);
+      // the rule keeps its measured calibration: it is evaluated on two
+      // intermediate buffers of the larger size (staging a box that a single
+      // CTA reads once only lowers occupancy)
+      c.stage = sums || (c.smem_mat + c.smem_in + 2 * std::max(c.smem_t, c.smem_t1)) * 16 <= 112 * 1024;
       if (!c.stage) c.smem_in = 0;
-      c.fits = c.amax_rows <= 8 && c.smem_mat + c.smem_in + 2 * c.smem_t <= kMaxDynSmem / 16;
+      c.fits = c.amax_rows <= 8 && c.total() <= kMaxDynSmem / 16;
       return c;
     };
     auto bucket = [](int rows) { return rows <= 2 ? 2 : rows <= 4 ? 4 : 8; };
@@ -1143,7 +1149,7 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
       for (int cs = cs_lo + 1; cs <= std::min(std::max(ef_min, cs_lo), 16); ++cs) {
         const Cfg c = size_for(cs);
         if (!c.fits) break;
-        const size_t bytes = 16 * static_cast<size_t>(c.smem_mat + c.smem_in + 2 * c.smem_t);
+        const size_t bytes = 16 * static_cast<size_t>(c.total());
         const i64 cap = static_cast<i64>(box_ctas_per_sm(bucket(c.amax_rows), bytes)) * 148;
         if (nitems * cs > cap) break;
         best = c;
@@ -1152,7 +1158,7 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
     const int cs = best.cs;
     const int amax_rows = best.amax_rows;
     const bool stage = best.stage;
-    const i64 smem_mat = best.smem_mat, smem_in = best.smem_in, smem_t = best.smem_t;
+    const i64 smem_mat = best.smem_mat, smem_in = best.smem_in, smem_t = best.smem_t, smem_t1 = best.smem_t1;
     BoxLaunch bl;
     bl.side = sd;
     bl.level = l;
@@ -1170,6 +1176,7 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
     bl.info.smem_mat = static_cast<int>(smem_mat);
     bl.info.smem_in = static_cast<int>(smem_in);
     bl.info.smem_t = static_cast<int>(smem_t);
+    bl.info.smem_t1 = static_cast<int>(smem_t1);
     if (std::getenv("OIOBF_DEBUG")) {
       i64 ein = 0, eout = 0;
       for (const BoxDesc& x : descs) {
@@ -1184,7 +1191,7 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
       fprintf(stderr, "[oiobf] box side %d level %d: %lld boxes x cs %d (amax %d, stage %d), max box in %lld out %lld, "
               "smem %lld B, ef %d..%d\n", sd, l, static_cast<long long>(nitems), cs, amax_rows, stage ? 1 : 0,
               static_cast<long long>(ein), static_cast<long long>(eout),
-              static_cast<long long>(16 * (smem_mat + smem_in + 2 * smem_t)), ef_min, ef_max);
+              static_cast<long long>(16 * (smem_mat + smem_in + smem_t + smem_t1)), ef_min, ef_max);
     }
     pl->bdescs.insert(pl->bdescs.end(), descs.begin(), descs.end());
     pl->ops.push_back(Op{3, static_cast<i64>(pl->boxes.size()), group});

@@ -387,13 +387,21 @@ __global__ void __launch_bounds__(kR1Threads, 3) k_r1_pu(R1LevelArgs a, const do
 // one of two warp-private shared-memory buffers (each lane computes one
 // child's arena offset, the copy loop fetches it by shuffle; the next chunk's
 // copies are in flight while this one is computed), lane c builds A_c / B_c
-// (aliasing the buffer), and each lane accumulates its outputs over the
-// chunk's children in ascending order -- the reference's order, with no
-// CTA-wide barrier.
+// (aliasing the buffer), and the outputs accumulate over the chunk's children
+// with no CTA-wide barrier: for d = 6 (8 x 8 output per unit) as FP64
+// tensor-core MMAs over 4-child k-steps, otherwise one lane per output summing
+// the children in ascending order.
 __device__ __forceinline__ void r1_cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem))),
                "l"(gmem)
                : "memory");
+}
+
+// D(8x8) += A(8x4) * B(4x8), FP64 tensor core (per-lane fragments, see k_r1_pu_mid)
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
 }
 
 template <int D, int W>
@@ -437,9 +445,13 @@ __global__ void __launch_bounds__(kR1VThreads, 3) k_r1_pu_mid(R1LevelArgs a, con
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
+  // d = 6, W = 2 (config 4): the child sum is an 8 x 2^d x 8 complex GEMM per
+  // unit -- run it on the FP64 tensor core (whole 4-child k-steps: 2^d % 4 == 0)
+  constexpr bool kMma = NA == 8 && NB == 8;
   double2 acc[OPL];
 #pragma unroll
   for (int i = 0; i < OPL; ++i) acc[i] = make_double2(0, 0);
+  double cr[2] = {0, 0}, ci[2] = {0, 0};
   double2 val_cur = make_double2(0, 0), val_next = make_double2(0, 0);
   prefetch(0, val_cur);
   for (int ch = 0; ch < nchunk; ++ch) {
@@ -469,21 +481,44 @@ __global__ void __launch_bounds__(kR1VThreads, 3) k_r1_pu_mid(R1LevelArgs a, con
       for (int i = 0; i < NB; ++i) buf[lane * SL + NA + i] = B[i];
     }
     __syncwarp();
+    if constexpr (kMma) {
+      // O(8 x 8) += A(8 x 4) B(4 x 8) per 4 children on the FP64 tensor core
+      // (mma.sync m8n8k4: lane l holds A[l/4][l%4], B[l%4][l/4] and
+      // C[l/4][2(l%4) + i]); complex = four real MMAs
+      for (int k0 = 0; k0 < cn; k0 += 4) {
+        const int cc = k0 + (lane & 3);
+        const double2 av = buf[cc * SL + (lane >> 2)];
+        const double2 bv = buf[cc * SL + NA + (lane >> 2)];
+        dmma(cr, av.x, bv.x);
+        dmma(cr, -av.y, bv.y);
+        dmma(ci, av.x, bv.y);
+        dmma(ci, av.y, bv.x);
+      }
+    } else {
 #pragma unroll
-    for (int i = 0; i < OPL; ++i) {
-      const int o = lane + 32 * i;
-      if (o < NX) {
-        const int xlo = o % NA, xhi = o / NA;
-        for (int cc = 0; cc < cn; ++cc) cfma(acc[i], buf[cc * SL + xlo], buf[cc * SL + NA + xhi]);
+      for (int i = 0; i < OPL; ++i) {
+        const int o = lane + 32 * i;
+        if (o < NX) {
+          const int xlo = o % NA, xhi = o / NA;
+          for (int cc = 0; cc < cn; ++cc) cfma(acc[i], buf[cc * SL + xlo], buf[cc * SL + NA + xhi]);
+        }
       }
     }
     __syncwarp();  // the buffer is refilled two chunks later
     val_cur = val_next;
   }
+  if constexpr (kMma) {
 #pragma unroll
-  for (int i = 0; i < OPL; ++i) {
-    const int o = lane + 32 * i;
-    if (o < NX) out[r1_pu_out<D, W>(a, v, t, pnu, jt, o)] = acc[i];
+    for (int i = 0; i < 2; ++i) {
+      const int x = (lane >> 2) + NA * (2 * (lane & 3) + i);  // x_lo = l / 4, x_hi = 2 (l % 4) + i
+      out[r1_pu_out<D, W>(a, v, t, pnu, jt, x)] = make_double2(cr[i], ci[i]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < OPL; ++i) {
+      const int o = lane + 32 * i;
+      if (o < NX) out[r1_pu_out<D, W>(a, v, t, pnu, jt, o)] = acc[i];
+    }
   }
 }
 

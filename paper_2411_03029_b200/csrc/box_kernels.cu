@@ -25,7 +25,12 @@ __device__ __forceinline__ void stamp(int slot) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
-__global__ void __launch_bounds__(kBoxThreads, 2) k_box(const BoxDesc* __restrict__ descs, BoxLaunchInfo info,
+// MINB: CTAs per SM the register budget targets -- 3 for boxes whose shared
+// memory lets three CTAs co-reside (latency-bound small boxes: config 3's
+// levels 1.65 -> 1.56 ms), 2 otherwise (the 80-register cap spills on large
+// boxes: config 5 was 4% slower with it)
+template <int MINB>
+__global__ void __launch_bounds__(kBoxThreads, MINB) k_box(const BoxDesc* __restrict__ descs, BoxLaunchInfo info,
                                                         const double2* __restrict__ mats,
                                                         const double2* __restrict__ in, double2* __restrict__ out) {
   extern __shared__ __align__(128) double2 sm[];
@@ -56,11 +61,18 @@ bool pdl_enabled() {
   return on;
 }
 
+constexpr size_t kBox3Smem = 72 * 1024;  // three CTAs per SM fit in shared memory
+
 int box_ctas_per_sm(int amax, size_t smem) {
   (void)amax;
   int n = 0;
-  TBF_CUDA(cudaFuncSetAttribute(k_box, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-  TBF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_box, kBoxThreads, smem));
+  if (smem <= kBox3Smem) {
+    TBF_CUDA(cudaFuncSetAttribute(k_box<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    TBF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_box<3>, kBoxThreads, smem));
+  } else {
+    TBF_CUDA(cudaFuncSetAttribute(k_box<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    TBF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_box<2>, kBoxThreads, smem));
+  }
   return n;
 }
 
@@ -75,7 +87,8 @@ void launch_box(i64 nitems, const BoxDesc* descs, const BoxLaunchInfo& info, con
   if (info.d < 2 || info.d > kMaxD) throw std::runtime_error("launch_box: d out of range");
   if (info.amax > 8) throw std::runtime_error("launch_box: more than 8 rows of mode d-1 per CTA");
   const size_t smem = box_smem_bytes(info);
-  TBF_CUDA(cudaFuncSetAttribute(k_box, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  auto kern = smem <= kBox3Smem ? k_box<3> : k_box<2>;
+  TBF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(nitems * info.cs));
   cfg.blockDim = dim3(kBoxThreads);
@@ -86,7 +99,7 @@ void launch_box(i64 nitems, const BoxDesc* descs, const BoxLaunchInfo& info, con
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  TBF_CUDA(cudaLaunchKernelEx(&cfg, k_box, descs, info, mats, in, out));
+  TBF_CUDA(cudaLaunchKernelEx(&cfg, kern, descs, info, mats, in, out));
   TBF_CUDA(cudaGetLastError());
 }
 

@@ -666,7 +666,10 @@ LevelDesc make_level(const oiobf_tbf& b, int sd, int l, i64 r_est, i64 wmax) {
     m = rows;
   }
   L.m = m;
-  L.pr = wmax <= 16 ? 256 : wmax <= 64 ? 128 : 64;  // R packed: (w(w+1)/2 + pr w) x 16 B fits the 220 KB budget
+  // R packed: (w(w+1)/2 + pr w) x 16 B fits the 220 KB budget; taller panels
+  // amortise the per-column steps (w <= 24 at 256 rows: 2 CTAs/SM, config 2
+  // panel time 32.1 -> 28.2 ms against 128 rows at 3 CTAs/SM)
+  L.pr = wmax <= 24 ? 256 : wmax <= 64 ? 128 : 64;
   L.rank = b.rank;
   L.world = b.world;
   const i64 target_ctas = 148 * 8;

@@ -64,8 +64,14 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / den)
 
 
-def compare_factorizations(gpu, ora, interp_tol=1e-9, core_tol=1e-12):
-    """Slot-by-slot: ranks and skeletons bit-exact, interps within tol, cores."""
+def compare_factorizations(gpu, ora, interp_tol=4e-9, core_tol=1e-12):
+    """Slot-by-slot: ranks and skeletons bit-exact, interps within tol, cores.
+
+    The interps T = R11^-1 R12 are only determined to ~eps * cond(R11) (cond up
+    to ~1/tol for these IDs), so two QR orders (the GPU's TSQR panels vs the
+    oracle's Householder) differ by up to ~1e-9 here (1.06e-9 on plates64 with
+    256-row panels); the BASELINE gates are the exact skeletons and the apply
+    within 1e-10 of the oracle on the same factors, both checked by the callers."""
     assert gpu.d == ora.d and gpu.L == ora.L
     np.testing.assert_array_equal(gpu.ranks, ora.ranks)
     np.testing.assert_array_equal(gpu.ncols, ora.ncols)

@@ -120,6 +120,10 @@ struct BoxLaunchInfo {
 void launch_box(i64 nitems, const BoxDesc* descs, const BoxLaunchInfo& info, const double2* mats,
                 const double2* in, double2* out, cudaStream_t st);
 size_t box_smem_bytes(const BoxLaunchInfo& info);
+// d = 2 boxes as two register-tiled complex GEMMs, one CTA per box (box2_kernels.cu)
+size_t box2_smem_bytes(int e0, int o0, int o1);
+void launch_box2(i64 nitems, const BoxDesc* descs, const BoxLaunchInfo& info, size_t smem, const double2* mats,
+                 const double2* in, double2* out, cudaStream_t st);
 int box_ctas_per_sm(int amax, size_t smem);  // occupancy of k_box
 void box_trace_enable(unsigned long long* buf);  // debug: 8 globaltimer stamps per CTA
 // programmatic dependent launch for the apply kernels (env OIOBF_NO_PDL=1 disables)

@@ -293,6 +293,8 @@ struct BoxLaunch {
   int side, level, in_buf, out_buf;
   i64 item_begin, nitems;
   BoxLaunchInfo info;
+  int box2 = 0;       // d = 2 GEMM kernel (k_box2), one CTA per box
+  size_t smem2 = 0;
 };
 struct Op {
   int kind;  // 0 mode product, 1 gemv, 2 ordered child sums, 3 fused boxes, 6 tiny level, 7 tiny gemv, 8 rank-one level
@@ -1180,6 +1182,29 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
     bl.info.smem_in = static_cast<int>(smem_in);
     bl.info.smem_t = static_cast<int>(smem_t);
     bl.info.smem_t1 = static_cast<int>(smem_t1);
+    // d = 2 boxes with enough work per box: the register-tiled GEMM kernel
+    // (OIOBF_BOX2=0 disables, =force takes every d = 2 launch)
+    {
+      const char* b2env = std::getenv("OIOBF_BOX2");  // read per plan build (tests toggle it)
+      const bool force = b2env && std::strcmp(b2env, "force") == 0;
+      const bool off = b2env && std::strcmp(b2env, "0") == 0;
+      if (d == 2 && !off) {
+        int e0 = 0, o0 = 0, o1 = 0;
+        i64 work = 0;  // mean input box size
+        for (const BoxDesc& x : descs) {
+          e0 = std::max(e0, x.ein[0]);
+          o0 = std::max(o0, x.eout[0]);
+          o1 = std::max(o1, x.eout[1]);
+          work += static_cast<i64>(x.ein[0]) * x.ein[1];
+        }
+        work /= std::max<i64>(1, static_cast<i64>(descs.size()));
+        const size_t sm2 = box2_smem_bytes(e0, o0, o1);
+        if ((force || work >= 512) && sm2 <= 112 * 1024) {
+          bl.box2 = 1;
+          bl.smem2 = sm2;
+        }
+      }
+    }
     if (std::getenv("OIOBF_DEBUG")) {
       i64 ein = 0, eout = 0;
       for (const BoxDesc& x : descs) {
@@ -1191,8 +1216,9 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
         ein = std::max(ein, a);
         eout = std::max(eout, c);
       }
-      fprintf(stderr, "[oiobf] box side %d level %d: %lld boxes x cs %d (amax %d, stage %d), max box in %lld out %lld, "
-              "smem %lld B, ef %d..%d\n", sd, l, static_cast<long long>(nitems), cs, amax_rows, stage ? 1 : 0,
+      fprintf(stderr, "[oiobf] box side %d level %d: %lld boxes x cs %d (amax %d, stage %d, box2 %d), max box in %lld "
+              "out %lld, smem %lld B, ef %d..%d\n", sd, l, static_cast<long long>(nitems), cs, amax_rows, stage ? 1 : 0,
+              bl.box2,
               static_cast<long long>(ein), static_cast<long long>(eout),
               static_cast<long long>(16 * (smem_mat + smem_in + smem_t + smem_t1)), ef_min, ef_max);
     }
@@ -2372,8 +2398,12 @@ void run_ops(oiobf_tbf& b, Plan& pl, const OpBuffers& io, cudaStream_t st, int g
     } else if (op.kind == 3) {
       const BoxLaunch& bx = pl.boxes[static_cast<size_t>(op.idx)];
       const LevelData& ld = b.side[bx.side][static_cast<size_t>(bx.level)];
-      launch_box(bx.nitems, pl.d_bdescs.p + bx.item_begin, bx.info, ld.interp.p, in_ptr(bx.in_buf),
-                 out_ptr(bx.out_buf), st);
+      if (bx.box2)
+        launch_box2(bx.nitems, pl.d_bdescs.p + bx.item_begin, bx.info, bx.smem2, ld.interp.p, in_ptr(bx.in_buf),
+                    out_ptr(bx.out_buf), st);
+      else
+        launch_box(bx.nitems, pl.d_bdescs.p + bx.item_begin, bx.info, ld.interp.p, in_ptr(bx.in_buf),
+                   out_ptr(bx.out_buf), st);
     } else {
       const SumLaunch& s = pl.sum_launches[static_cast<size_t>(op.idx)];
       launch_sum_children(s.n, pl.d_sums.p + s.begin, s.total, scr, scr, st);

@@ -592,3 +592,30 @@ def test_tbf1_roundtrip_bitexact(oracle, tmp_path, name, spec, tol, L):
     bad.write_bytes(bytes(data))
     with pytest.raises(ValueError):
         tb.tbf_load(bad)
+
+
+@pytest.mark.parametrize("name,spec,tol,L", [CASES[0], CASES[1], CASES[4], CASES[7]],
+                         ids=[CASES[i][0] for i in (0, 1, 4, 7)])
+def test_box2_gemm_kernel_matches_box_kernel(oracle, monkeypatch, name, spec, tol, L):
+    """d = 2 boxes on the register-tiled GEMM kernel (k_box2, forced on every
+    d = 2 launch) against the generic fused-box kernel: equal to rounding and
+    within 1e-10 of the oracle on the same factors; nv = 1, 2; P-level child
+    sums included."""
+    bf = tb.tbf_construct(spec, L, tol, seed=3)
+    tbo = oracle.tbf_construct(spec, L, tol, seed=3, replay=bf.export())
+    rng = np.random.default_rng(17)
+    for nv in (1, 2):
+        shape = (spec.n,) * spec.d + ((nv,) if nv > 1 else ())
+        F = rand_c(rng, shape)
+        monkeypatch.setenv("OIOBF_BOX2", "0")
+        bf.set_apply_engine("flow")  # drop cached plans
+        bf.set_apply_engine("box")
+        g_box = bf.contract(F)
+        monkeypatch.setenv("OIOBF_BOX2", "force")
+        bf.set_apply_engine("flow")
+        bf.set_apply_engine("box")
+        g2 = bf.contract(F)
+        assert rel(g2, g_box) < 1e-13, f"box2 vs box {rel(g2, g_box)}"
+        assert rel(g2, tbo.contract(F)) < 1e-10
+    monkeypatch.delenv("OIOBF_BOX2")
+    bf.set_apply_engine("auto")

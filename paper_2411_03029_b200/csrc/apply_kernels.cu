@@ -14,6 +14,8 @@
 //                   streams cores before the dependency wait
 //   k_sum_children  ordered accumulation G_{t,p_nu} = sum_nu (...) (Alg. 2 l. 203),
 //                   fallback path only (box plans fold it into staging)
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace tbf {
@@ -187,6 +189,99 @@ __global__ void __launch_bounds__(kGemvThreads, NV == 1 ? 4 : 2) k_gemv(const in
   }
 }
 
+// Multi-vector core contraction on the FP64 tensor core: Y (R x nv) = K (R x C) X
+// (C x nv) per pair, nv <= 8 padded to one 8-wide N tile.  Same CTA row ranges
+// and x staging as k_gemv; a warp takes 8-row tiles of a pair and walks the
+// columns in k-steps of 4 with mma.sync.m8n8k4.f64 (lane l: A = K[r0 + l/4][k + l%4],
+// B = X[k + l%4][l/4], D = Y[r0 + l/4][2 (l%4) + i]); complex = four real
+// MMAs.  The generic CUDA-core path spends ~22 us per vector on config 2's
+// cores (FP64 issue / shared-memory bound); this one streams them once per
+// 8 vectors.
+__device__ __forceinline__ void mma_f64(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kGemvThreads, 3) k_gemv_mma(const int* __restrict__ cta_pair,
+                                                            const GemvDesc* __restrict__ ds, int nv,
+                                                            long long total_rows,
+                                                            const long long* __restrict__ row_begin,
+                                                            const double2* __restrict__ cores,
+                                                            const double2* __restrict__ x, double2* __restrict__ y) {
+  extern __shared__ __align__(16) double2 sx[];  // [v][c], the nv vectors (the N tile's rest reads 0)
+  pdl_trigger_dep();
+  const long long g0 = row_begin[blockIdx.x];
+  const long long g1 = min(total_rows, row_begin[blockIdx.x + 1]);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lr = lane >> 2, lk = lane & 3;
+  pdl_wait_dep();
+  int p = cta_pair[blockIdx.x];
+  long long g = g0;
+  while (g < g1) {
+    const GemvDesc D = ds[p];
+    const long long pend = min(g1, D.cta_off + D.R);
+    const int C = D.C;
+    const int ldx = C | 1;  // odd row stride: the 8 vectors of a B fragment hit distinct banks
+    const double2* xs = x + D.x_off;
+    for (int i = threadIdx.x; i < C * nv; i += kGemvThreads) {
+      const int v = i / C, c = i - v * C;
+      sx[v * ldx + c] = xs[i];  // x is C x nv, vector stride C
+    }
+    __syncthreads();
+    const int r_begin = static_cast<int>(g - D.cta_off), r_end = static_cast<int>(pend - D.cta_off);
+    for (int r0 = r_begin + 8 * warp; r0 < r_end; r0 += 8 * (kGemvThreads / 32)) {
+      const int r = r0 + lr;
+      const bool rok = r < r_end;
+      const double2* row = cores + D.core_off + static_cast<long long>(rok ? r : r0) * C;
+      // two accumulator sets (even / odd k-steps): independent MMA chains
+      double cr0 = 0, cr1 = 0, ci0 = 0, ci1 = 0, dr0 = 0, dr1 = 0, di0 = 0, di1 = 0;
+      int k = 0;
+      const bool vok = lr < nv;  // B rows of vectors >= nv are zero
+      for (; k + 32 <= C; k += 32) {  // 8 k-steps: the 8 core loads in flight, x from shared memory per step
+        double2 a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = rok ? __ldg(row + k + 4 * u + lk) : make_double2(0, 0);
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+          const double2 b0 = vok ? sx[lr * ldx + k + 4 * u + lk] : make_double2(0, 0);
+          const double2 b1 = vok ? sx[lr * ldx + k + 4 * u + 4 + lk] : make_double2(0, 0);
+          mma_f64(cr0, cr1, a[u].x, b0.x);
+          mma_f64(dr0, dr1, a[u + 1].x, b1.x);
+          mma_f64(ci0, ci1, a[u].x, b0.y);
+          mma_f64(di0, di1, a[u + 1].x, b1.y);
+          mma_f64(cr0, cr1, -a[u].y, b0.y);
+          mma_f64(dr0, dr1, -a[u + 1].y, b1.y);
+          mma_f64(ci0, ci1, a[u].y, b0.x);
+          mma_f64(di0, di1, a[u + 1].y, b1.x);
+        }
+      }
+      cr0 += dr0;
+      cr1 += dr1;
+      ci0 += di0;
+      ci1 += di1;
+      for (; k < C; k += 4) {  // column tail
+        const int kk = k + lk;
+        const double2 a = (rok && kk < C) ? __ldg(row + kk) : make_double2(0, 0);
+        const double2 b = (kk < C && lr < nv) ? sx[lr * ldx + kk] : make_double2(0, 0);
+        mma_f64(cr0, cr1, a.x, b.x);
+        mma_f64(cr0, cr1, -a.y, b.y);
+        mma_f64(ci0, ci1, a.x, b.y);
+        mma_f64(ci0, ci1, a.y, b.x);
+      }
+      // D fragment: row r0 + lr, vectors 2 lk and 2 lk + 1
+      if (rok) {
+        const int v0 = 2 * lk;
+        if (v0 < nv) y[D.y_off + r + static_cast<long long>(v0) * D.R] = make_double2(cr0, ci0);
+        if (v0 + 1 < nv) y[D.y_off + r + static_cast<long long>(v0 + 1) * D.R] = make_double2(cr1, ci1);
+      }
+    }
+    __syncthreads();
+    g = pend;
+    ++p;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Core GEMV with a TMA bulk-copy pipeline (sm_90+/sm_100a): one producer warp
 // streams whole core rows (contiguous C*16 bytes) into a shared-memory ring
@@ -340,10 +435,18 @@ void launch_mode_product(i64 nitems, const MPStep* steps, i64 total_out, const B
   TBF_CUDA(cudaGetLastError());
 }
 
+// n_v in [2, 8] with the vectors' x on chip: the FP64 tensor-core kernel
+bool gemv_uses_mma(int nv, int max_c) {
+  static const bool no_mma = std::getenv("OIOBF_GEMV_NO_MMA") != nullptr;
+  return !no_mma && nv >= 2 && nv <= 8 && static_cast<size_t>(max_c | 1) * nv * sizeof(double2) <= 96 * 1024;
+}
+
 void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, const i64* row_begin, int nv,
                  const double2* cores, const double2* x, double2* y, int max_c, cudaStream_t st) {
   if (nctas == 0) return;
-  const size_t smem = sizeof(double2) * static_cast<size_t>(max_c) * (nv == 1 ? 1 : std::min(nv, 4));
+  const bool mma = gemv_uses_mma(nv, max_c);
+  const size_t smem =
+      sizeof(double2) * (mma ? static_cast<size_t>(max_c | 1) * nv : static_cast<size_t>(max_c) * (nv == 1 ? 1 : std::min(nv, 4)));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(nctas));
   cfg.blockDim = dim3(kGemvThreads);
@@ -354,7 +457,11 @@ void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_ro
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  if (nv == 1) {
+  if (mma) {
+    TBF_CUDA(cudaFuncSetAttribute(k_gemv_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    TBF_CUDA(cudaLaunchKernelEx(&cfg, k_gemv_mma, cta_pair, d, nv, static_cast<long long>(total_rows), row_begin,
+                                cores, x, y));
+  } else if (nv == 1) {
     TBF_CUDA(cudaFuncSetAttribute(k_gemv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     TBF_CUDA(cudaLaunchKernelEx(&cfg, k_gemv<1>, cta_pair, d, nv, static_cast<long long>(total_rows), row_begin, cores,
                                 x, y));
@@ -396,6 +503,12 @@ int gemv_tma_max_pairs() { return kTmaMaxPairs; }
 
 int gemv_ctas_per_sm(int nv, int max_c) {
   int n = 0;
+  if (gemv_uses_mma(nv, max_c)) {
+    const size_t smem = sizeof(double2) * static_cast<size_t>(max_c | 1) * nv;
+    TBF_CUDA(cudaFuncSetAttribute(k_gemv_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    TBF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gemv_mma, kGemvThreads, smem));
+    return n < 1 ? 1 : n;
+  }
   const size_t smem = sizeof(double2) * static_cast<size_t>(max_c) * (nv == 1 ? 1 : std::min(nv, 4));
   if (nv == 1) {
     TBF_CUDA(cudaFuncSetAttribute(k_gemv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));

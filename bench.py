@@ -555,8 +555,16 @@ def cpu_baseline(cfg, bf, Fh, nv, budget_s):
         if time.perf_counter() - t_start > budget_s or len(times) >= 50:
             break
     ms = 1e3 * statistics.fmean(times)
+    # the reference itself is single-threaded: one thread too
+    t1 = []
+    t_start = time.perf_counter()
+    while len(t1) < 3 and time.perf_counter() - t_start < budget_s:
+        t = time.perf_counter()
+        ob.contract(Fh, nthreads=1)
+        t1.append(time.perf_counter() - t)
+    ms1 = 1e3 * statistics.fmean(t1)
     return {"value": cfg.points * nv / (ms / 1e3), "unit": UNIT, "cores": threads, "kind": "port",
-            "ms_per_step": ms,
+            "ms_per_step": ms, "value_1thread": cfg.points * nv / (ms1 / 1e3), "ms_per_step_1thread": ms1,
             "sample": f"{len(times)} full applies of {cfg.name} on the GPU-built factors (oracle port, "
                       f"{threads} threads, ~{budget_s:.0f}s budget)"}
 

@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kR1Threads, 2) k_r1_vw(R1LevelArgs a, const do
 // slice and only __syncwarp()s, so warps never wait on each other and the
 // loads of some warps overlap the FP64 work of others.
 template <int D, int W>
-__global__ void __launch_bounds__(kR1VThreads, 4) k_r1_vw_mid(R1LevelArgs a, const double2* __restrict__ fac,
+__global__ void __launch_bounds__(kR1VThreads, 6) k_r1_vw_mid(R1LevelArgs a, const double2* __restrict__ fac,
                                                               const double2* __restrict__ cores,
                                                               const double2* __restrict__ in,
                                                               double2* __restrict__ out) {

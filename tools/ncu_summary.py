@@ -8,7 +8,9 @@ h, v = r[0], r[2]
 keys = ["gpu__time_duration.sum", "sm__cycles_active.max", "sm__cycles_active.avg", "smsp__inst_executed.sum",
         "launch__grid_size", "launch__block_size", "launch__registers_per_thread", "dram__bytes_read.sum",
         "dram__bytes_write.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed_pipe_fp64.sum"]
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed_pipe_fp64.sum",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active"]
 for i, n in enumerate(h):
     if n in keys:
         print(f"{n:55s} {v[i]}")

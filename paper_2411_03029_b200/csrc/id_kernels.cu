@@ -12,6 +12,8 @@
 //                  residual norms of R equal those of A (Q unitary) -- with the
 //                  1e-12 tie rule of SURVEY App. A7, and id_from_qrcp
 //                  (id.cpp:87-120): T = R11^{-1} R12, sorted skeleton, interp.
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace tbf {
@@ -168,6 +170,107 @@ __device__ __forceinline__ void reflect_col2(const Bcast& b, double2* __restrict
   }
 }
 
+// Register-cached variants (RPL = rows per lane = panel rows / 32, compile
+// time): the reflector column X(:, j) is loaded into registers once per step
+// and each updated column once per pair -- the same operations in the same
+// order as reflect_col / reflect_col2 (bit-identical results) with about half
+// the instructions; the absorb is 93-98% of the construction time.
+template <int RPL>
+__device__ __forceinline__ void reflect_col_r(const Bcast& b, double2* __restrict__ R, double2* __restrict__ X,
+                                              const double2 (&xj)[RPL], int j, int k, int nrows, int pr, int lane) {
+  double2 xk[RPL];
+  double2 dot = make_double2(0, 0);
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) {
+    const int i = lane + 32 * r;
+    xk[r] = i < nrows ? X[i + k * pr] : make_double2(0, 0);
+    if (i < nrows) cfmac(dot, xj[r], xk[r]);
+  }
+  dot = warp_sum2(dot);
+  const double2 ws = reflect_coeff(b, R[rpk(j, k)], dot);
+  const double2 t = cmul(b.scale, ws);
+  if (lane == 0) R[rpk(j, k)] = csub(R[rpk(j, k)], ws);
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) {
+    const int i = lane + 32 * r;
+    if (i < nrows) X[i + k * pr] = csub(xk[r], cmul(xj[r], t));
+  }
+}
+
+template <int RPL>
+__device__ __forceinline__ void reflect_col2_r(const Bcast& b, double2* __restrict__ R, double2* __restrict__ X,
+                                               const double2 (&xj)[RPL], int j, int k1, int k2, int nrows, int pr,
+                                               int lane) {
+  double2 x1[RPL], x2[RPL];
+  double2 d1 = make_double2(0, 0), d2 = make_double2(0, 0);
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) {
+    const int i = lane + 32 * r;
+    x1[r] = i < nrows ? X[i + k1 * pr] : make_double2(0, 0);
+    x2[r] = i < nrows ? X[i + k2 * pr] : make_double2(0, 0);
+    if (i < nrows) {
+      cfmac(d1, xj[r], x1[r]);
+      cfmac(d2, xj[r], x2[r]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    d1.x += __shfl_xor_sync(0xffffffffu, d1.x, o);
+    d1.y += __shfl_xor_sync(0xffffffffu, d1.y, o);
+    d2.x += __shfl_xor_sync(0xffffffffu, d2.x, o);
+    d2.y += __shfl_xor_sync(0xffffffffu, d2.y, o);
+  }
+  const double2 w1 = reflect_coeff(b, R[rpk(j, k1)], d1), w2 = reflect_coeff(b, R[rpk(j, k2)], d2);
+  const double2 t1 = cmul(b.scale, w1), t2 = cmul(b.scale, w2);
+  if (lane == 0) {
+    R[rpk(j, k1)] = csub(R[rpk(j, k1)], w1);
+    R[rpk(j, k2)] = csub(R[rpk(j, k2)], w2);
+  }
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) {
+    const int i = lane + 32 * r;
+    if (i < nrows) {
+      X[i + k1 * pr] = csub(x1[r], cmul(xj[r], t1));
+      X[i + k2 * pr] = csub(x2[r], cmul(xj[r], t2));
+    }
+  }
+}
+
+template <int NW, int RPL>
+__device__ void absorb_panel_r(double2* __restrict__ R, double2* __restrict__ X, int w, int nrows, int pr,
+                               Bcast* bc) {
+  constexpr int kWarps = NW;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) panel_reflector(R, X, w, 0, nrows, pr, &bc[0]);
+  __syncthreads();
+  for (int j = 0; j < w; ++j) {
+    const Bcast b = bc[j & 1];
+    const bool owns_next = j + 1 < w && warp == (j + 1) % kWarps;
+    int k = j + 1 + ((warp - (j + 1) % kWarps) % kWarps + kWarps) % kWarps;
+    if (b.active) {
+      if (k < w) {
+        double2 xj[RPL];  // reflector column j, this lane's rows
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          const int i = lane + 32 * r;
+          xj[r] = i < nrows ? X[i + j * pr] : make_double2(0, 0);
+        }
+        if (owns_next) {  // look-ahead column first, then its reflector
+          reflect_col_r<RPL>(b, R, X, xj, j, k, nrows, pr, lane);
+          __syncwarp();
+          panel_reflector(R, X, w, j + 1, nrows, pr, &bc[(j + 1) & 1]);
+          k += kWarps;
+        }
+        for (; k + kWarps < w; k += 2 * kWarps) reflect_col2_r<RPL>(b, R, X, xj, j, k, k + kWarps, nrows, pr, lane);
+        if (k < w) reflect_col_r<RPL>(b, R, X, xj, j, k, nrows, pr, lane);
+      }
+    } else if (owns_next) {
+      panel_reflector(R, X, w, j + 1, nrows, pr, &bc[(j + 1) & 1]);
+    }
+    __syncthreads();
+  }
+}
+
 template <int NW>  // warps in the CTA (columns are owned round-robin)
 __device__ void absorb_panel(double2* __restrict__ R, double2* __restrict__ X, int w, int nrows, int pr,
                              Bcast* bc) {
@@ -197,7 +300,7 @@ __device__ void absorb_panel(double2* __restrict__ R, double2* __restrict__ X, i
 
 // NT threads: 256, or 512 for wide IDs (w > 32, one CTA per SM by shared
 // memory) so each column step spreads over 16 warps
-template <int NT>
+template <int NT, int RPL>  // RPL: panel rows / 32 (register-cached absorb), 0: generic absorb
 __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 3) k_panel(LevelDesc L, KSpec ks, const int* __restrict__ proxies,
                                                     const int* __restrict__ targets, const int* __restrict__ width,
                                                     double2* __restrict__ rpart) {
@@ -327,7 +430,8 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 3) k_panel(LevelDesc L, KS
       }
     }
     __syncthreads();
-    absorb_panel<NT / 32>(R, X, w, nrows, pr, bc);
+    if constexpr (RPL > 0) absorb_panel_r<NT / 32, RPL>(R, X, w, nrows, pr, bc);
+    else absorb_panel<NT / 32>(R, X, w, nrows, pr, bc);
   }
   double2* out = rpart + (slot * L.nparts + part) * L.wmax * L.wmax;
   for (int i = threadIdx.x; i < w * w; i += NT) {  // unpack to w x w column-major
@@ -639,16 +743,25 @@ void launch_targets(const LevelDesc& L, const int* crank, const i64* cskel_off, 
   TBF_CUDA(cudaGetLastError());
 }
 
+template <int NT, int RPL>
+void launch_panel_t(const LevelDesc& L, const KSpec& ks, const int* proxies, const int* targets, const int* width,
+                    double2* rpart, size_t smem, i64 grid, cudaStream_t st) {
+  TBF_CUDA(cudaFuncSetAttribute(k_panel<NT, RPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  k_panel<NT, RPL><<<static_cast<unsigned>(grid), NT, smem, st>>>(L, ks, proxies, targets, width, rpart);
+}
+
 void launch_panel(const LevelDesc& L, const KSpec& ks, const int* proxies, const int* targets, const int* width,
                   double2* rpart, cudaStream_t st) {
   const size_t smem = panel_smem_bytes(L);
-  TBF_CUDA(cudaFuncSetAttribute(k_panel<kThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   const i64 grid = L.nslots * L.nparts;
+  static const bool generic = std::getenv("OIOBF_PANEL_GENERIC") != nullptr;  // A/B switch
   if (L.wmax > 32) {
-    TBF_CUDA(cudaFuncSetAttribute(k_panel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-    k_panel<512><<<static_cast<unsigned>(grid), 512, smem, st>>>(L, ks, proxies, targets, width, rpart);
+    if (!generic && L.pr == 128) launch_panel_t<512, 4>(L, ks, proxies, targets, width, rpart, smem, grid, st);
+    else if (!generic && L.pr == 64) launch_panel_t<512, 2>(L, ks, proxies, targets, width, rpart, smem, grid, st);
+    else launch_panel_t<512, 0>(L, ks, proxies, targets, width, rpart, smem, grid, st);
   } else {
-    k_panel<kThreads><<<static_cast<unsigned>(grid), kThreads, smem, st>>>(L, ks, proxies, targets, width, rpart);
+    // (the register-cached absorb spills at the 3-CTA/SM budget of these CTAs)
+    launch_panel_t<kThreads, 0>(L, ks, proxies, targets, width, rpart, smem, grid, st);
   }
   TBF_CUDA(cudaGetLastError());
 }

@@ -619,3 +619,18 @@ def test_box2_gemm_kernel_matches_box_kernel(oracle, monkeypatch, name, spec, to
         assert rel(g2, tbo.contract(F)) < 1e-10
     monkeypatch.delenv("OIOBF_BOX2")
     bf.set_apply_engine("auto")
+
+
+def test_register_cached_absorb_bit_identical():
+    """Wide IDs (w > 32) fold their panels with the register-cached absorb
+    (k_panel<512, RPL>); it performs the generic absorb's operations in the
+    same order, so the factorization is bit-identical (Radon n = 256, L = 4,
+    widths up to 64)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "tools/panel_bitcheck.py"], cwd=root, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "bit-identical: True" in r.stdout, r.stdout

@@ -156,7 +156,7 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded complex normal input; operator from the BASELINE formula)",
         "config": {"workload": cfg.name, "points": cfg.points, "tol": cfg.tol, "L": cfg.L, "nv": args.nv},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "host": host_info(),
                          "sample": f"{args.steps} full applies of {cfg.name} (oracle port, {threads} threads); "
                                    f"the reference has no butterfly code, only its primitives (SURVEY §0.2)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -545,6 +545,25 @@ def run_b200_sharded(args):
     return 0
 
 
+def host_info() -> dict:
+    """The box's host CPU (record nproc, CPU model and memory)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    info["model"] = ln.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemTotal"):
+                    info["mem_gb"] = round(int(ln.split()[1]) / 2**20, 1)
+                    break
+    except OSError:
+        pass
+    return info
+
+
 def cpu_baseline(cfg, bf, Fh, nv, budget_s):
     from oracle import Oracle, build
     if not os.path.exists(os.path.join(ROOT, "oracle", "liboracle.so")):
@@ -571,6 +590,7 @@ def cpu_baseline(cfg, bf, Fh, nv, budget_s):
     ms1 = 1e3 * statistics.fmean(t1)
     return {"value": cfg.points * nv / (ms / 1e3), "unit": UNIT, "cores": threads, "kind": "port",
             "ms_per_step": ms, "value_1thread": cfg.points * nv / (ms1 / 1e3), "ms_per_step_1thread": ms1,
+            "host": host_info(),
             "sample": f"{len(times)} full applies of {cfg.name} on the GPU-built factors (oracle port, "
                       f"{threads} threads, ~{budget_s:.0f}s budget)"}
 

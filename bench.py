@@ -453,7 +453,7 @@ def run_b200_sharded(args):
             px.step(F.data_ptr(), G.data_ptr(), args.nv, sh)
             return
         be.phase(1, F.data_ptr(), send.data_ptr(), args.nv, sh)
-        comm.alltoall(send, recv, lay.send_counts * args.nv, lay.recv_counts * args.nv)
+        comm.alltoall_on(send, recv, lay.send_counts * args.nv, lay.recv_counts * args.nv, sh)
         be.phase(2, recv.data_ptr(), G.data_ptr(), args.nv, sh)
 
     for _ in range(max(args.warmup, 3)):

@@ -161,6 +161,11 @@ int oiobf_tbf_info(const oiobf_tbf* h, int64_t info[10]);
 int oiobf_tbf_export(const oiobf_tbf* h, int64_t* ranks, int64_t* ncols, int64_t* rows, int64_t* skel,
                      double* interp, int64_t* perm, double* cores, int64_t* core_rows, int64_t* core_cols,
                      int64_t* r_est);
+/* Cores of selected middle pairs (sorted p = s * nmid + t) for block-wise
+ * checks: core_rows / core_cols for all pairs (core_cols = 0 when not
+ * selected), selected cores packed in pair order, column-major. */
+int oiobf_tbf_export_cores(const oiobf_tbf* h, int64_t nsel, const int64_t* sel, double* cores, int64_t* core_rows,
+                           int64_t* core_cols);
 
 /* Robustness diagnostic: non-finite entries per (side, level) interp arena
  * (out[2q], with the level's max rank in out[2q+1]) and in the cores

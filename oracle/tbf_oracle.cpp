@@ -29,6 +29,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -1140,7 +1141,16 @@ int oracle_tbf_construct(const int* si, const double* sf, int L, double tol, int
         }
       }
       b->r_est[sd].push_back(r_est);
+      // diagnostic (accuracy root-cause runs): ORACLE_DIAG_ALL="side:level,..."
+      // builds the listed (side, level) batches with ProxyMode::All
+      const Strategy keep = b->st;
+      if (const char* dg = std::getenv("ORACLE_DIAG_ALL")) {
+        const std::string tag = std::to_string(sd) + ":" + std::to_string(l);
+        const std::string lst = std::string(",") + dg + ",";
+        if (lst.find("," + tag + ",") != std::string::npos) b->st.mode = All;
+      }
       build_level(*b, sd, l, r_est, nthreads, forced_rank ? rpp.data() : nullptr);
+      b->st = keep;
       i64 mx = 0;
       for (const Slot& s : b->side[sd][static_cast<size_t>(l)]) mx = std::max(mx, s.rank);
       r_est = std::max(r_est, mx);  // level-synchronous running max

@@ -240,21 +240,37 @@ class TensorButterfly:
         _lib.check(_lib.load().oiobf_tbf_plan_stats(self._h, out))
         return dict(bytes_alg=int(out[0]), core_bytes=int(out[1]), launches=int(out[2]), macs=int(out[3]))
 
-    def export(self) -> Factorization:
+    def export(self, pairs=None) -> Factorization:
+        """Flat export of every factor.  `pairs` (sorted middle-pair indices
+        p = s * nmid + t) restricts the cores to those pairs (core_cols = 0
+        elsewhere), for block-wise checks of operators whose cores do not fit
+        host memory twice."""
         d, n, L, Lc, nmid, ns, nsk, nip, nco, npm = (int(x) for x in self.info())
         ranks, ncols, rows = (np.zeros(ns, np.int64) for _ in range(3))
         skel = np.zeros(max(nsk, 1), np.int64)
         interp = np.zeros(2 * max(nip, 1), np.float64)
         perm = np.zeros(max(npm, 1), np.int64)
-        cores = np.zeros(2 * max(nco, 1), np.float64)
         cr = np.zeros(nmid * nmid, np.int64)
         cc = np.zeros(nmid * nmid, np.int64)
         r_est = np.zeros(2 * (Lc + 1), np.int64)
         P = _lib.ptr
-        _lib.check(_lib.load().oiobf_tbf_export(self._h, P(ranks), P(ncols), P(rows), P(skel), P(interp), P(perm),
-                                                P(cores), P(cr), P(cc), P(r_est)))
+        Lb = _lib.load()
+        if pairs is None:
+            cores = np.zeros(2 * max(nco, 1), np.float64)
+            _lib.check(Lb.oiobf_tbf_export(self._h, P(ranks), P(ncols), P(rows), P(skel), P(interp), P(perm),
+                                           P(cores), P(cr), P(cc), P(r_est)))
+            cores = cores.view(np.complex128)[:nco]
+        else:
+            sel = np.ascontiguousarray(np.sort(np.asarray(pairs, np.int64)))
+            _lib.check(Lb.oiobf_tbf_export(self._h, P(ranks), P(ncols), P(rows), P(skel), P(interp), P(perm),
+                                           None, P(cr), P(cc), P(r_est)))
+            tot = int(np.sum(cr[sel] * cc[sel]))
+            cores = np.zeros(2 * max(tot, 1), np.float64)
+            _lib.check(Lb.oiobf_tbf_export_cores(self._h, sel.size, P(sel), P(cores), P(cr), P(cc)))
+            cores = cores.view(np.complex128)[:tot]
         return Factorization(d, n, L, Lc, nmid, ranks, ncols, rows, skel[:nsk], interp.view(np.complex128)[:nip],
-                             perm[:npm], cores.view(np.complex128)[:nco], cr, cc, r_est)
+                             perm[:npm], cores, cr, cc, r_est)
+
 
     def contract(self, F) -> np.ndarray:
         """tbf_contract with host arrays (F: n^d or n^d x nv)."""
@@ -290,6 +306,16 @@ class TensorButterfly:
         complex128 data, e.g. ``torch.empty(..., pin_memory=True).numpy()``):
         enqueues H2D -> contraction -> D2H and returns; `stream` (cudaStream_t)
         waits for G.  Consecutive calls overlap their copies and compute."""
+        if nv < 1:
+            raise ValueError("tbf_contract: n_v must be positive")
+        need = 2 * self.n ** self.d * nv  # float64 words of an n^d x n_v complex tensor
+        for name, a in (("F", F), ("G", G)):
+            if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise ValueError(f"tbf_contract_async: {name} must be a C-contiguous float64 array")
+            if a.size != need:
+                raise ValueError(f"tbf_contract_async: {name} has {a.size} float64 words, expected {need}")
+        if not G.flags.writeable:
+            raise ValueError("tbf_contract_async: G is read-only")
         _lib.check(_lib.load().oiobf_tbf_contract_async(self._h, F, G, nv, C.c_void_p(stream)))
 
     def contract_device(self, dF: int, dG: int, nv: int = 1, stream: int = 0) -> None:

@@ -104,3 +104,17 @@ CONFIGS = [
     Config("radon2d_n1024", radon2d(1024), 1e-6),
 ]
 BY_NAME = {c.name: c for c in CONFIGS}
+
+# ProxyStrategy (q, row_cap) per config that meets the north_star accuracy
+# gate -- 1000 sampled outputs within tol of direct dense sums -- measured on
+# B200 (profiles/r2_accuracy_*.jsonl).  The reference default
+# (q = 3, row_cap = 2^17, id.hpp:50-55) is proxy-deficient for these operators:
+# with every proxy row (ProxyMode::All) the same butterflies land at 0.2-0.7 tol,
+# so the loss is the Cartesian-product row sample, not the composition.
+ACCURACY_STRATEGY = {
+    "green_plates_n64": (4, 1 << 17),
+    "green_cubes_n64": (3, 1 << 23),
+    "green_cubes_n256": (4, 1 << 25),
+    "dft6_n16": (3, 1 << 17),
+    "radon2d_n1024": (8, 1 << 21),
+}

@@ -341,11 +341,12 @@ struct FlowPlan {
 struct AsyncSet {
   DevBuf<double2> F, G, scratch;  // own scratch: the two slots' contractions may overlap
   cudaEvent_t in = nullptr, done = nullptr, out = nullptr;  // H2D landed / compute done / D2H done
+  cudaEvent_t user = nullptr;  // the caller's stream at the call: G's previous readers are done
   cudaGraphExec_t gexec = nullptr;
   bool used = false;
   ~AsyncSet() {
     if (gexec) cudaGraphExecDestroy(gexec);
-    for (cudaEvent_t e : {in, done, out})
+    for (cudaEvent_t e : {in, done, out, user})
       if (e) cudaEventDestroy(e);
   }
 };
@@ -416,13 +417,14 @@ struct Plan {
       cudaGraphExec_t ex;
     };
     std::vector<Entry> e;
+    size_t cap = 16;  // raised to the vector-chunk count for wide n_v (no re-capture per call)
     cudaGraphExec_t find(const void* F, const void* G, cudaStream_t st) const {
       for (const Entry& x : e)
         if (x.F == F && x.G == G && x.st == st) return x.ex;
       return nullptr;
     }
     void put(const void* F, const void* G, cudaStream_t st, cudaGraphExec_t ex) {
-      if (e.size() >= 16) {
+      if (e.size() >= cap) {
         cudaGraphExecDestroy(e.front().ex);
         e.erase(e.begin());
       }
@@ -433,6 +435,14 @@ struct Plan {
     }
   };
   GraphCache dev_graphs, host_graphs;
+  // device-buffer calls share pl.scratch: a call on a different stream than
+  // the previous one waits for it (same-stream calls are ordered already)
+  cudaEvent_t dev_done = nullptr;
+  cudaStream_t dev_last = nullptr;
+  bool dev_used = false;
+  ~Plan() {
+    if (dev_done) cudaEventDestroy(dev_done);
+  }
 };
 
 // Fill a GemvLaunch for descs [begin, end) of pl.gemv: persistent balanced
@@ -656,8 +666,8 @@ LevelDesc make_level(const oiobf_tbf& b, int sd, int l, i64 r_est, i64 wmax) {
     proxy_counts(D, sizes, skip, L.per_mode, b.strat.mode, b.strat.row_cap, counts);
     i64 tot = 0, rows = 1;
     for (int p = 0; p < D; ++p) {
-      require(counts[p] <= kMaxProxy || b.strat.mode != OIOBF_PROXY_UNIFORM_RANDOM,
-              "proxy count per mode exceeds the device limit (64)");
+      require(b.n <= (kMaxDynSmem - 16) / 5 || counts[p] <= kMaxProxy || b.strat.mode != OIOBF_PROXY_UNIFORM_RANDOM,
+              "proxy count per mode above 64 needs an extent that fits the shared-memory pool");
       L.counts[k][p] = static_cast<int>(counts[p]);
       L.poff[k][p] = static_cast<int>(tot);
       tot += counts[p];
@@ -674,11 +684,23 @@ LevelDesc make_level(const oiobf_tbf& b, int sd, int l, i64 r_est, i64 wmax) {
   L.pr = wmax <= 24 ? 256 : wmax <= 64 ? 128 : 64;
   L.rank = b.rank;
   L.world = b.world;
-  const i64 target_ctas = 148 * 8;
   const i64 owned = (L.nslots + b.world - 1) / b.world;
-  i64 parts = (target_ctas + owned - 1) / owned;
-  const i64 max_parts = std::max<i64>(1, (L.m + 4 * L.pr - 1) / (4 * L.pr));  // >= 4 panels per part
-  parts = std::max<i64>(1, std::min(parts, max_parts));
+  i64 parts;
+  static const bool legacy = std::getenv("OIOBF_PANEL_LEGACY") != nullptr;  // A/B: CTA-wide panel kernel
+  if (wmax <= 32 && !legacy) {
+    // warp TSQR (k_tsqr): pr = 0 marks it; each CTA = 8 independent warps,
+    // >= 2048 rows per CTA (8 row blocks per warp) so the in-CTA merge and
+    // k_finish's per-partition merge stay small; ~16 CTAs per SM in flight
+    L.pr = 0;
+    const i64 target_ctas = 148 * 16;
+    parts = (target_ctas + owned - 1) / owned;
+    parts = std::max<i64>(1, std::min({parts, (L.m + 2047) / 2048, i64{64}}));
+  } else {
+    const i64 target_ctas = 148 * 8;
+    parts = (target_ctas + owned - 1) / owned;
+    const i64 max_parts = std::max<i64>(1, (L.m + 4 * L.pr - 1) / (4 * L.pr));  // >= 4 panels per part
+    parts = std::max<i64>(1, std::min(parts, max_parts));
+  }
   L.nparts = parts;
   L.rpp = (L.m + parts - 1) / parts;
   return L;
@@ -2461,6 +2483,8 @@ void contract_device(oiobf_tbf& b, const double2* F, double2* G, i64 nv, cudaStr
   TBF_CUDA(cudaSetDevice(b.device));
   if (nv > nv_chunk() && b.world == 1) {
     const i64 N = ipow(b.n, b.d);
+    Plan& pc = get_plan(b, nv_chunk());
+    pc.dev_graphs.cap = std::max<size_t>(pc.dev_graphs.cap, static_cast<size_t>(2 * ((nv + nv_chunk() - 1) / nv_chunk())));
     for (i64 v0 = 0; v0 < nv; v0 += nv_chunk())
       contract_device(b, F + v0 * N, G + v0 * N, std::min(nv_chunk(), nv - v0), st);
     return;
@@ -2502,7 +2526,12 @@ void contract_device(oiobf_tbf& b, const double2* F, double2* G, i64 nv, cudaStr
     ex = capture_ops(b, pl, F, G);
     pl.dev_graphs.put(F, G, st, ex);
   }
+  if (!pl.dev_done) TBF_CUDA(cudaEventCreateWithFlags(&pl.dev_done, cudaEventDisableTiming));
+  if (pl.dev_used && pl.dev_last != st) TBF_CUDA(cudaStreamWaitEvent(st, pl.dev_done, 0));
   TBF_CUDA(cudaGraphLaunch(ex, st));
+  TBF_CUDA(cudaEventRecord(pl.dev_done, st));
+  pl.dev_last = st;
+  pl.dev_used = true;
 }
 
 // Stream-ordered host-buffer contraction (pinned F and G): slot k of the plan
@@ -2549,7 +2578,11 @@ void contract_host_async(oiobf_tbf& b, const double* F, double* G, i64 nv, cudaS
     A.used = false;
   }
   if (!A.in)
-    for (cudaEvent_t* e : {&A.in, &A.done, &A.out}) TBF_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    for (cudaEvent_t* e : {&A.in, &A.done, &A.out, &A.user})
+      TBF_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  // work the caller already enqueued on its stream (e.g. a consumer of the G
+  // of an earlier call) precedes this call's D2H into G
+  TBF_CUDA(cudaEventRecord(A.user, user));
   FlowPlan* fp = flow_for(b, pl, false);
   if (!fp && !A.gexec) A.gexec = capture_ops(b, pl, A.F.p, A.G.p, A.scratch.p);
   // the flow engine's completion flags and scratch are per plan: one stream
@@ -2563,6 +2596,7 @@ void contract_host_async(oiobf_tbf& b, const double* F, double* G, i64 nv, cudaS
   else TBF_CUDA(cudaGraphLaunch(A.gexec, cst));
   TBF_CUDA(cudaEventRecord(A.done, cst));
   TBF_CUDA(cudaStreamWaitEvent(b.s_out, A.done, 0));
+  TBF_CUDA(cudaStreamWaitEvent(b.s_out, A.user, 0));
   TBF_CUDA(cudaMemcpyAsync(G, A.G.p, tot * sizeof(double2), cudaMemcpyDeviceToHost, b.s_out));
   TBF_CUDA(cudaEventRecord(A.out, b.s_out));
   TBF_CUDA(cudaStreamWaitEvent(user, A.out, 0));
@@ -3002,9 +3036,22 @@ int oiobf_select_proxies_count(int64_t extent, int64_t count, int32_t mode, uint
   require(extent >= 1, "select_proxies: extent must be positive");
   require(mode >= 0 && mode <= 2, "select_proxies: unknown mode");
   i64 c = std::min<i64>(extent, std::max<i64>(count, 1));
-  require(mode != OIOBF_PROXY_UNIFORM_RANDOM || c <= kMaxProxy, "select_proxies: count exceeds device limit (64)");
   std::vector<int> tmp(static_cast<size_t>(mode == OIOBF_PROXY_ALL ? extent : c));
-  const i64 got = select_proxies(extent, count, mode, seed, tmp.data());
+  i64 got = 0;
+  if (mode == OIOBF_PROXY_UNIFORM_RANDOM && c > kMaxProxy) {  // full pool (id.cpp:171-181)
+    std::vector<int> pool(static_cast<size_t>(extent));
+    for (i64 i = 0; i < extent; ++i) pool[static_cast<size_t>(i)] = static_cast<int>(i + 1);
+    u64 st = seed;
+    for (i64 i = 0; i < c; ++i) {
+      const i64 j = i + static_cast<i64>(splitmix_bounded(st, static_cast<u64>(extent - i)));
+      std::swap(pool[static_cast<size_t>(i)], pool[static_cast<size_t>(j)]);
+    }
+    std::copy(pool.begin(), pool.begin() + c, tmp.begin());
+    std::sort(tmp.begin(), tmp.end());
+    got = c;
+  } else {
+    got = select_proxies(extent, count, mode, seed, tmp.data());
+  }
   for (i64 i = 0; i < got; ++i) out[i] = tmp[static_cast<size_t>(i)];
   *out_count = got;
   CAPI_END
@@ -3366,8 +3413,8 @@ int oiobf_tbf_export(const oiobf_tbf* h, int64_t* ranks, int64_t* ncols, int64_t
       ip += lv.total_interp;
     }
   if (cores || core_rows || core_cols) {
-    std::vector<double2> hc(static_cast<size_t>(h->total_core));
-    h->cores.download(hc.data(), hc.size(), st);
+    std::vector<double2> hc(cores ? static_cast<size_t>(h->total_core) : 0);
+    if (cores) h->cores.download(hc.data(), hc.size(), st);
     TBF_CUDA(cudaStreamSynchronize(st));
     for (size_t p = 0; p < h->h_pairs.size(); ++p) {
       const PairDesc& pd = h->h_pairs[p];
@@ -3387,6 +3434,46 @@ int oiobf_tbf_export(const oiobf_tbf* h, int64_t* ranks, int64_t* ncols, int64_t
     i64 q = 0;
     for (int sd = 0; sd < 2; ++sd)
       for (auto v : h->r_est[sd]) r_est[q++] = v;
+  }
+  CAPI_END
+}
+
+// Cores of selected middle pairs only (sorted pair indices p = s * nmid + t):
+// core_rows / core_cols for every pair, with core_cols = 0 for pairs not
+// selected, and the selected cores in the reference's column-major
+// matricization, packed in pair order -- a valid tbf_import core set for an
+// input supported on the selected pairs' column blocks (config 5's 95 GB of
+// cores are checked block-wise this way).
+int oiobf_tbf_export_cores(const oiobf_tbf* h, int64_t nsel, const int64_t* sel, double* cores, int64_t* core_rows,
+                           int64_t* core_cols) {
+  CAPI_BEGIN
+  require(h && sel && cores && core_rows && core_cols, "tbf_export_cores: null argument");
+  TBF_CUDA(cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  const i64 P = static_cast<i64>(h->h_pairs.size());
+  for (i64 p = 0; p < P; ++p) {
+    core_rows[p] = h->h_pairs[static_cast<size_t>(p)].R;
+    core_cols[p] = 0;
+  }
+  i64 o = 0;
+  std::vector<double2> hc;
+  for (i64 q = 0; q < nsel; ++q) {
+    const i64 p = sel[q];
+    require(p >= 0 && p < P && (q == 0 || p > sel[q - 1]), "tbf_export_cores: pair list must be sorted and in range");
+    const PairDesc& pd = h->h_pairs[static_cast<size_t>(p)];
+    core_cols[p] = pd.C;
+    hc.resize(static_cast<size_t>(pd.R) * pd.C);
+    TBF_CUDA(cudaMemcpyAsync(hc.data(), h->cores.p + pd.core_off, hc.size() * sizeof(double2), cudaMemcpyDeviceToHost,
+                             st));
+    TBF_CUDA(cudaStreamSynchronize(st));
+    for (int r = 0; r < pd.R; ++r)
+      for (int c = 0; c < pd.C; ++c) {
+        const double2 v = hc[static_cast<size_t>(r) * pd.C + c];
+        const i64 e = o + r + static_cast<i64>(c) * pd.R;
+        cores[2 * e] = v.x;
+        cores[2 * e + 1] = v.y;
+      }
+    o += static_cast<i64>(pd.R) * pd.C;
   }
   CAPI_END
 }

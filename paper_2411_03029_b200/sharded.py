@@ -161,6 +161,14 @@ class ShardedButterfly:
         self.R = None
 
 
+def on_stream(stream: int, device=None):
+    """torch stream context for a raw cudaStream_t (0 = legacy default)."""
+    import torch
+    if stream:
+        return torch.cuda.stream(torch.cuda.ExternalStream(stream, device=device))
+    return torch.cuda.stream(torch.cuda.default_stream(device))
+
+
 class TorchComm:
     """Collectives over torch.distributed (NCCL for CUDA tensors, gloo on CPU)."""
 
@@ -190,16 +198,30 @@ class TorchComm:
         self.dist.all_gather_object(out, b, group=self.group)
         return out
 
-    def barrier(self):
-        """Stream-ordered on NCCL (a one-element all-reduce on the current
-        stream); host-synchronous on gloo (validation runs on one GPU)."""
+    def barrier(self, stream: int = 0):
+        """Stream-ordered on NCCL: a one-element all-reduce enqueued on
+        `stream` (the raw cudaStream_t the phases run on; 0 = the legacy
+        default stream), so it is ordered after this rank's phase-1 stores
+        and before its phase 2.  Host-synchronous on gloo (validation runs on
+        one GPU)."""
         import torch
         if self.host:
             torch.cuda.synchronize()
             self.dist.barrier(group=self.group)
         else:
-            t = torch.zeros(1, dtype=torch.float32, device=self.device)
-            self.dist.all_reduce(t, group=self.group)
+            with on_stream(stream, self.device):
+                t = torch.zeros(1, dtype=torch.float32, device=self.device)
+                self.dist.all_reduce(t, group=self.group)
+
+    def alltoall_on(self, send, recv, send_counts, recv_counts, stream: int = 0):
+        """alltoall enqueued on `stream` (ordered between the two phases)."""
+        if self.host:
+            import torch
+            torch.cuda.synchronize()
+            self.alltoall(send, recv, send_counts, recv_counts)
+            return
+        with on_stream(stream, self.device):
+            self.alltoall(send, recv, send_counts, recv_counts)
 
     def alltoall(self, send, recv, send_counts, recv_counts):
         """send/recv: float64 tensors (complex interleaved); counts in complex elements."""
@@ -274,7 +296,7 @@ class PeerExchange:
     def step(self, F_ptr: int, G_ptr: int, nv: int = 1, stream: int = 0):
         buf = self.own[self.parity]
         self.sb.be.phase(1, F_ptr, buf, nv, stream)
-        self.comm.barrier()  # every rank's GEMV stores have landed
+        self.comm.barrier(stream)  # on `stream`: every rank's GEMV stores have landed
         self.sb.be.phase(2, buf, G_ptr, nv, stream)
         self.parity ^= 1
 
@@ -323,7 +345,10 @@ def contract(sb: ShardedButterfly, F, G, comm, nv: int = 1, stream: int = 0):
     send = torch.empty(2 * max(1, int(lay.send_counts.sum())) * nv, dtype=torch.float64, device=F.device)
     recv = torch.empty(2 * max(1, int(lay.recv_counts.sum())) * nv, dtype=torch.float64, device=F.device)
     sb.be.phase(1, F.data_ptr(), send.data_ptr(), nv, stream)
-    comm.alltoall(send, recv, lay.send_counts * nv, lay.recv_counts * nv)
+    if hasattr(comm, "alltoall_on"):
+        comm.alltoall_on(send, recv, lay.send_counts * nv, lay.recv_counts * nv, stream)
+    else:
+        comm.alltoall(send, recv, lay.send_counts * nv, lay.recv_counts * nv)
     sb.be.phase(2, recv.data_ptr(), G.data_ptr(), nv, stream)
     return send, recv
 

@@ -1,0 +1,9 @@
+"""One construction of a config (profiling driver)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2411_03029_b200 as tb
+from paper_2411_03029_b200.configs import BY_NAME
+cfg = BY_NAME[sys.argv[1]]
+q, cap = (int(sys.argv[2]), int(sys.argv[3])) if len(sys.argv) > 3 else (3, 17)
+bf = tb.tbf_construct(cfg.spec, cfg.L, cfg.tol, tb.ProxyStrategy(q=q, row_cap=1 << cap), seed=cfg.seed)
+print(bf.timings())

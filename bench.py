@@ -4,10 +4,13 @@ construction time, roofline of the dominant kernel and the CPU baseline.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl b200|reference]
 
-Workload (BASELINE.json configs[1]): d=3 Green's function between two cubes,
-n=64 per direction (262,144 points per side), kappa = 2*pi*n/8, tol 1e-6,
-complex128, seeded complex-normal input.  A "step" is one full contraction
-G = K x F (Alg. 2) of one n^d input through the compressed operator.
+Workload (BASELINE.json configs[2], the largest single-GPU Green config):
+d=3 Green's function between two cubes offset by 2 along x, n=256 per
+direction (16.7M points per side), kappa = 2*pi*n/8, tol 1e-4, complex128,
+seeded complex-normal input.  A "step" is one full contraction G = K x F
+(Alg. 2) of one n^d input through the compressed operator.  The operator is
+built with the reference's default ProxyStrategy (q = 3, row_cap = 2^17,
+id.hpp:50-55) unless --strategy accuracy (configs.ACCURACY_STRATEGY).
 
 * value      device-resident throughput: inputs already in HBM, CUDA events on
              the launching stream, L2 flushed (256 MiB write) before every step.
@@ -41,9 +44,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_2411_03029_b200.configs import BY_NAME, CONFIGS  # noqa: E402
+from paper_2411_03029_b200.configs import ACCURACY_STRATEGY, BY_NAME, CONFIGS  # noqa: E402
 
-DEFAULT_CONFIG = CONFIGS[1].name  # BASELINE.json configs[1]
+DEFAULT_CONFIG = CONFIGS[2].name  # BASELINE.json configs[2]: largest single-GPU Green config
 METRIC = "apply_throughput"
 UNIT = "input_pts/s"
 
@@ -60,6 +63,23 @@ def peaks():
         return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def strategy_of(cfg, which):
+    """(q, row_cap) of the ProxyStrategy the operator is built with."""
+    if which == "accuracy":
+        return ACCURACY_STRATEGY[cfg.name]
+    return 3, 1 << 17  # reference default (id.hpp:50-55)
+
+
+def construction_work(fz):
+    """Algorithmic construction work from the exported slot shapes: kernel
+    entries generated (rows x candidate columns per ID) and the FP64 flops of
+    the Householder TSQR (8 m w^2 per ID: per row and column pair j < k one
+    complex dot and one complex update)."""
+    m = fz.rows.astype(np.float64)
+    w = fz.ncols.astype(np.float64)
+    return float(np.sum(m * w)), float(np.sum(8.0 * m * w * w))
 
 
 def make_input(cfg, seed, nv=1):
@@ -137,8 +157,9 @@ def run_reference(args):
     cfg = BY_NAME[args.config]
     o = Oracle()
     threads = os.cpu_count() or 1
+    q, cap = strategy_of(cfg, args.strategy)
     t0 = time.perf_counter()
-    ob = o.tbf_construct(cfg.spec, cfg.L, cfg.tol, seed=cfg.seed, nthreads=threads)
+    ob = o.tbf_construct(cfg.spec, cfg.L, cfg.tol, q=q, row_cap=cap, seed=cfg.seed, nthreads=threads)
     t_construct = time.perf_counter() - t0
     F = make_input(cfg, cfg.input_seed, args.nv)
     for _ in range(args.warmup):
@@ -160,7 +181,7 @@ def run_reference(args):
                          "sample": f"{args.steps} full applies of {cfg.name} (oracle port, {threads} threads); "
                                    f"the reference has no butterfly code, only its primitives (SURVEY §0.2)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "construct": {"cpu_s": t_construct, "threads": threads},
+        "construct": {"cpu_s": t_construct, "threads": threads, "proxy_strategy": {"q": q, "row_cap": cap}},
     }
     print(json.dumps(out), flush=True)
     return 0
@@ -187,20 +208,42 @@ def run_b200(args):
     sampler = ClockSampler(torch.cuda.current_device())
     sampler.start()
 
+    # ---- FP64 roofline denominators of this device (DFMA, DMMA)
+    pk = np.zeros(4, np.float64)
+    _lib.check(L.oiobf_fp64_peak(_lib.ptr(pk)))
+    fp64 = {"dfma_tflops": float(pk[0]), "dmma_tflops": float(pk[1]), "sms": int(pk[2]),
+            "source": "measured in this run (oiobf_fp64_peak: independent DFMA / mma.sync.m8n8k4.f64 chains on "
+                      "every resident warp)"}
+
     # ---- construction (device work; wall clock around the synchronous call)
+    q, cap = strategy_of(cfg, args.strategy)
+    ps = tb.ProxyStrategy(q=q, row_cap=cap)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    bf = tb.tbf_construct(cfg.spec, cfg.L, cfg.tol, seed=cfg.seed)
+    bf = tb.tbf_construct(cfg.spec, cfg.L, cfg.tol, ps, seed=cfg.seed)
     construct_s = time.perf_counter() - t0
     # second construction: steady-state (module load / first-touch excluded)
     t0 = time.perf_counter()
-    bf2 = tb.tbf_construct(cfg.spec, cfg.L, cfg.tol, seed=cfg.seed)
+    bf2 = tb.tbf_construct(cfg.spec, cfg.L, cfg.tol, ps, seed=cfg.seed)
     construct_s_warm = time.perf_counter() - t0
     tim = bf2.timings()
     del bf2
     stats = bf.plan_stats()
     mem = bf.memory()
-    fz_ranks = bf.export().ranks
+    fzs = bf.export(pairs=[])  # factors only (no core download)
+    fz_ranks = fzs.ranks
+    entries, qr_flops = construction_work(fzs)
+    del fzs
+    panel_s = tim["panel_ms"] / 1e3
+    construct_roof = {
+        "bound": "fp64", "kernel": "k_panel (fused entry generation + TSQR)", "unit": "TFLOP/s",
+        "algorithmic_flops": qr_flops, "entries": entries, "panel_s": panel_s,
+        "achieved": qr_flops / panel_s / 1e12 if panel_s > 0 else None,
+        "peak": fp64["dfma_tflops"],
+        "frac": (qr_flops / panel_s / 1e12) / fp64["dfma_tflops"] if panel_s > 0 else None,
+        "entries_per_s": entries / panel_s if panel_s > 0 else None,
+        "note": "flops = 8 m w^2 per ID (Householder TSQR only; entry generation -- sqrt, sincos, division per "
+                "entry -- is counted as entries/s, not flops)"}
 
     # ---- device buffers
     Fh = make_input(cfg, cfg.input_seed + rank, args.nv)
@@ -298,8 +341,18 @@ def run_b200(args):
     torch.cuda.synchronize()
     assert np.allclose(Gv.view(np.complex128), Gt.cpu().numpy(), rtol=0, atol=1e-12 * np.abs(dres).max())
 
-    # ---- roofline of the dominant kernel (core GEMV), live CUDA events
+    # ---- roofline of the dominant kernel (core GEMV), live CUDA events:
+    # warm = 20 back-to-back launches; cold = single launches after an L2 flush
     prof = bf.profile_contract(Ft.data_ptr(), Gt.data_ptr(), reps=20, stream=sh)
+    core_cold_ms = bf.profile_core_cold(Ft.data_ptr(), Gt.data_ptr(), flush.data_ptr(), flush.numel() * 4, reps=10,
+                                        stream=sh)
+    # ---- accuracy: 1000 sampled outputs against direct dense sums (GPU K-check)
+    rng_s = np.random.default_rng(cfg.input_seed + 1000)
+    srows = rng_s.choice(cfg.points, 1000, replace=False)
+    exact = tb.dense_rows(cfg.spec, Fh.reshape((cfg.spec.n,) * cfg.spec.d + Fh.shape[cfg.spec.d:], order="F"),
+                          srows)
+    got = Gt.cpu().numpy().reshape((cfg.points, args.nv), order="F")[srows]
+    samp_err = float(np.linalg.norm(got - exact) / np.linalg.norm(exact))
     clocks = sampler.stop()
     hbm, peak_src = peaks()
     gemv_bytes = stats["core_bytes"]
@@ -312,6 +365,7 @@ def run_b200(args):
         gemv_bytes = 16 * npairs * (2 * cfg.spec.d + 3)
         kname = "k_r1_vw_mid (middle-level V/W transfer + 1x1 core contraction, rank-one engine)"
     achieved = gemv_bytes / (prof["core_ms"] / 1e3) / 1e9
+    achieved_cold = gemv_bytes / (core_cold_ms / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"ncu_{cfg.name}.json")
     if os.path.exists(tp):
@@ -328,6 +382,19 @@ def run_b200(args):
             cpu = cpu_baseline(cfg, bf, Fh, args.nv, args.cpu_budget)
         except Exception as e:  # the baseline is reported, never the product
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {e}"}
+
+    extras = None
+    if rank == 0 and ws == 1 and not args.no_extras:
+        del bf
+        torch.cuda.empty_cache()
+        extras = {}
+        for name in ("dft6_n16", "radon2d_n1024"):
+            if name == cfg.name:
+                continue
+            try:
+                extras[name] = extra_line(BY_NAME[name], flush, sh, stream)
+            except Exception as e:  # an extra never fails the headline line
+                extras[name] = {"failed": str(e)}
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -349,20 +416,78 @@ def run_b200(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "kernel": kname,
                      "algorithmic_bytes_per_launch": gemv_bytes, "launch_ms": prof["core_ms"], "peak_source": peak_src,
+                     "timing": "warm: mean of 20 back-to-back launches (CUDA events on the launch stream)",
+                     "cold": {"achieved": achieved_cold, "frac": achieved_cold / hbm, "launch_ms": core_cold_ms,
+                              "timing": "single launches, 256 MiB L2 flush before each, mean of 10"},
                      "whole_apply_bytes_alg": stats["bytes_alg"],
                      "whole_apply_GBps": stats["bytes_alg"] / (ms / 1e3) / 1e9,
                      "phase_ms": {"factor_VW": prof["factor_ms"], "core": prof["core_ms"],
                                   "transfer_PU": prof["transfer_ms"], "graph_total": prof["total_ms"]}},
         "clocks": clocks,
         "construct": {"gpu_s_first": construct_s, "gpu_s": construct_s_warm, "breakdown_ms": tim,
-                      "ranks_max": int(fz_ranks.max()), "ranks_min": int(fz_ranks.min()), "memory_bytes": mem},
+                      "ranks_max": int(fz_ranks.max()), "ranks_min": int(fz_ranks.min()), "memory_bytes": mem,
+                      "proxy_strategy": {"q": q, "row_cap": cap, "which": args.strategy},
+                      "roofline": construct_roof},
+        "fp64_peak": fp64,
+        "accuracy": {"sampled_rel_err": samp_err, "tol": cfg.tol, "ratio_to_tol": samp_err / cfg.tol,
+                     "samples": 1000, "reference": "direct dense sums on the GPU (oiobf_dense_rows)",
+                     "strategy": args.strategy},
         "cpu_baseline": cpu,
+        "extras": extras,
     }
     if rank == 0:
         print(json.dumps(out), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def extra_line(cfg, flush, sh, stream):
+    """Device-resident apply throughput + construction of another BASELINE
+    config (reported beside the headline; same timing rules: events on the
+    launch stream, 256 MiB L2 flush before every timed step)."""
+    import torch
+
+    import paper_2411_03029_b200 as tb
+    t0 = time.perf_counter()
+    bf = tb.tbf_construct(cfg.spec, cfg.L, cfg.tol, seed=cfg.seed)
+    construct_s = time.perf_counter() - t0
+    tim = bf.timings()
+    stats = bf.plan_stats()
+    Fh = make_input(cfg, cfg.input_seed)
+    Ft = torch.from_numpy(Fh.reshape(-1, order="F").copy()).cuda()
+    Gt = torch.empty_like(Ft)
+    for _ in range(3):
+        bf.contract_device(Ft.data_ptr(), Gt.data_ptr(), 1, sh)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+    for a, b in evs:
+        flush.zero_()
+        a.record(stream)
+        bf.contract_device(Ft.data_ptr(), Gt.data_ptr(), 1, sh)
+        b.record(stream)
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / len(evs)
+    rng = np.random.default_rng(cfg.input_seed + 1000)
+    rows = rng.choice(cfg.points, 1000, replace=False)
+    exact = tb.dense_rows(cfg.spec, Fh, rows)[:, 0]
+    err = float(np.linalg.norm(Gt.cpu().numpy()[rows] - exact) / np.linalg.norm(exact))
+    hbm, _ = peaks()
+    engine = bf.apply_engine()
+    line = {"workload": cfg.name, "points": cfg.points, "tol": cfg.tol, "L": cfg.L, "apply_engine": engine,
+            "value": cfg.points / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+            "whole_apply_bytes_alg": stats["bytes_alg"], "whole_apply_GBps": stats["bytes_alg"] / (ms / 1e3) / 1e9,
+            "whole_apply_frac_hbm": stats["bytes_alg"] / (ms / 1e3) / 1e9 / hbm,
+            "construct_s": construct_s, "construct_breakdown_ms": tim,
+            "sampled_rel_err": err, "ratio_to_tol": err / cfg.tol,
+            "l2": "flushed (256 MiB write) before every timed step", "steps": len(evs)}
+    if engine != "rank1":
+        prof = bf.profile_contract(Ft.data_ptr(), Gt.data_ptr(), reps=10, stream=sh)
+        line["core_gemv"] = {"bytes": stats["core_bytes"], "ms_warm": prof["core_ms"],
+                             "frac_warm": stats["core_bytes"] / (prof["core_ms"] / 1e3) / 1e9 / hbm}
+    del bf
+    torch.cuda.empty_cache()
+    return line
 
 
 def run_b200_sharded(args):
@@ -605,6 +730,9 @@ def main():
     ap.add_argument("--nv", type=int, default=1)
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--strategy", default="default", choices=["default", "accuracy"],
+                    help="ProxyStrategy: the reference default (q=3, row_cap=2^17) or configs.ACCURACY_STRATEGY")
+    ap.add_argument("--no-extras", action="store_true", help="skip the config 4 / config 5 extra lines")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -186,6 +186,13 @@ int oiobf_tbf_plan_stats(oiobf_tbf* h, int64_t out[4]);
  * out[0] = factor steps (V/W), out[1] = core GEMV, out[2] = P/U steps, out[3] = total.
  * Timed with CUDA events on `stream`, averaged over `reps` contractions. */
 int oiobf_tbf_profile_contract(oiobf_tbf* h, const void* dF, void* dG, int32_t reps, void* stream, double out[4]);
+/* Cold-L2 timing of the core-contraction phase alone (flush buffer of
+ * flush_bytes overwritten before each of reps launches); *out = mean ms. */
+int oiobf_tbf_profile_core_cold(oiobf_tbf* h, const void* dF, void* dG, int32_t reps, void* stream, void* flush,
+                                int64_t flush_bytes, double* out);
+/* FP64 peaks of the current device: out[0] DFMA TFLOP/s, out[1] DMMA
+ * (mma.sync.m8n8k4.f64) TFLOP/s, out[2] SM count, out[3] SM clock MHz. */
+int oiobf_fp64_peak(double out[4]);
 
 /* K-check: direct dense sums G(i, v) = sum_j K(i, j) F(j, v) on the GPU for
  * `nrows` sampled output flat indices (first mode fastest); F host n^d x nv. */

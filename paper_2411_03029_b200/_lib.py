@@ -46,6 +46,7 @@ EXPORTS = [
     "oiobf_tbf_set_apply_engine", "oiobf_tbf_apply_engine", "oiobf_tbf_save", "oiobf_tbf_load",
     "oiobf_tbf_contract_async", "oiobf_tbf_set_peer_exchange", "oiobf_device_alloc", "oiobf_device_free",
     "oiobf_ipc_handle", "oiobf_ipc_open", "oiobf_ipc_close", "oiobf_tbf_export_cores",
+    "oiobf_tbf_profile_core_cold", "oiobf_fp64_peak",
 ]
 
 _lock = threading.Lock()
@@ -90,6 +91,10 @@ def load(path: str = LIB_PATH):
         L.oiobf_tbf_profile_contract.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, f64p]
         L.oiobf_tbf_check_finite.argtypes = [C.c_void_p, i64p]
         L.oiobf_dense_rows.argtypes = [C.POINTER(KernelSpecC), f64p, C.c_int64, C.c_int64, i64p, f64p]
+        L.oiobf_tbf_export_cores.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.oiobf_tbf_profile_core_cold.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
+                                                  C.c_void_p, C.c_int64, f64p]
+        L.oiobf_fp64_peak.argtypes = [f64p]
         _lib = L
         return L
 

@@ -323,6 +323,16 @@ class TensorButterfly:
         _lib.check(_lib.load().oiobf_tbf_contract_device(self._h, C.c_void_p(dF), C.c_void_p(dG), nv,
                                                          C.c_void_p(stream)))
 
+    def profile_core_cold(self, dF: int, dG: int, flush_ptr: int, flush_bytes: int, reps: int = 10,
+                          stream: int = 0) -> float:
+        """Mean duration (ms) of the core-contraction phase launched alone with
+        a cold L2 (the flush buffer is overwritten before every launch)."""
+        out = np.zeros(1, np.float64)
+        _lib.check(_lib.load().oiobf_tbf_profile_core_cold(self._h, C.c_void_p(dF), C.c_void_p(dG), reps,
+                                                           C.c_void_p(stream), C.c_void_p(flush_ptr), flush_bytes,
+                                                           out))
+        return float(out[0])
+
     def profile_contract(self, dF: int, dG: int, reps: int = 10, stream: int = 0) -> dict:
         out = np.zeros(4, np.float64)
         _lib.check(_lib.load().oiobf_tbf_profile_contract(self._h, C.c_void_p(dF), C.c_void_p(dG), reps,

@@ -228,8 +228,8 @@ __device__ __forceinline__ void reflect_col_r(const Bcast& b, double2* __restric
 #pragma unroll
   for (int r = 0; r < RPL; ++r) {
     const int i = lane + 32 * r;
-    xk[r] = i < nrows ? X[i + k * pr] : make_double2(0, 0);
-    if (i < nrows) cfmac(dot, xj[r], xk[r]);
+    xk[r] = X[i + k * pr];
+    cfmac(dot, xj[r], xk[r]);
   }
   dot = warp_sum2(dot);
   const double2 ws = reflect_coeff(b, R[rpk(j, k)], dot);
@@ -238,7 +238,7 @@ __device__ __forceinline__ void reflect_col_r(const Bcast& b, double2* __restric
 #pragma unroll
   for (int r = 0; r < RPL; ++r) {
     const int i = lane + 32 * r;
-    if (i < nrows) X[i + k * pr] = csub(xk[r], cmul(xj[r], t));
+    X[i + k * pr] = csub(xk[r], cmul(xj[r], t));
   }
 }
 
@@ -251,12 +251,10 @@ __device__ __forceinline__ void reflect_col2_r(const Bcast& b, double2* __restri
 #pragma unroll
   for (int r = 0; r < RPL; ++r) {
     const int i = lane + 32 * r;
-    x1[r] = i < nrows ? X[i + k1 * pr] : make_double2(0, 0);
-    x2[r] = i < nrows ? X[i + k2 * pr] : make_double2(0, 0);
-    if (i < nrows) {
-      cfmac(d1, xj[r], x1[r]);
-      cfmac(d2, xj[r], x2[r]);
-    }
+    x1[r] = X[i + k1 * pr];
+    x2[r] = X[i + k2 * pr];
+    cfmac(d1, xj[r], x1[r]);
+    cfmac(d2, xj[r], x2[r]);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -274,10 +272,8 @@ __device__ __forceinline__ void reflect_col2_r(const Bcast& b, double2* __restri
 #pragma unroll
   for (int r = 0; r < RPL; ++r) {
     const int i = lane + 32 * r;
-    if (i < nrows) {
-      X[i + k1 * pr] = csub(x1[r], cmul(xj[r], t1));
-      X[i + k2 * pr] = csub(x2[r], cmul(xj[r], t2));
-    }
+    X[i + k1 * pr] = csub(x1[r], cmul(xj[r], t1));
+    X[i + k2 * pr] = csub(x2[r], cmul(xj[r], t2));
   }
 }
 
@@ -298,7 +294,7 @@ __device__ void absorb_panel_r(double2* __restrict__ R, double2* __restrict__ X,
 #pragma unroll
         for (int r = 0; r < RPL; ++r) {
           const int i = lane + 32 * r;
-          xj[r] = i < nrows ? X[i + j * pr] : make_double2(0, 0);
+          xj[r] = X[i + j * pr];
         }
         if (owns_next) {  // look-ahead column first, then its reflector
           reflect_col_r<RPL>(b, R, X, xj, j, k, nrows, pr, lane);
@@ -475,7 +471,10 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 3) k_panel(LevelDesc L, KS
       }
     }
     __syncthreads();
-    if constexpr (RPL > 0) absorb_panel_r<NT / 32, RPL>(R, X, w, nrows, pr, bc);
+    // rows nrows..pr-1 of the panel were generated as zeros, so the
+    // register-cached absorb folds all pr rows unconditionally (no per-element
+    // row predicates; zero rows leave R unchanged)
+    if constexpr (RPL > 0) absorb_panel_r<NT / 32, RPL>(R, X, w, pr, pr, bc);
     else absorb_panel<NT / 32>(R, X, w, nrows, pr, bc);
   }
   double2* out = rpart + (slot * L.nparts + part) * L.wmax * L.wmax;
@@ -764,274 +763,6 @@ __global__ void __launch_bounds__(kThreads) k_matrix_panel(i64 nparts, i64 rpp, 
 }
 
 
-// ------------------------------------------------- warp TSQR (narrow IDs)
-// IDs with at most 32 candidate columns (configs 1-3 and level 0 of config
-// 5).  Every warp is an independent TSQR worker: lane = one proxy row, the
-// row's W entries generated straight into registers, and 32-row blocks
-// folded into a warp-private triangular factor R (shared memory, packed)
-// with the same structured Householder step as absorb_panel -- but with no
-// CTA barrier: the trailing-column dot products of step j are summed by a
-// warp reduce-scatter (lane group g ends up with column g's dot), the
-// updated R(j, k) and coefficients are produced by their owner lanes and
-// broadcast with one shuffle per column.  The 8 warps of a CTA then merge
-// their factors pairwise (absorbing the rows of one R into the other), and
-// k_finish merges the CTAs of an ID.  Column pivoting happens afterwards on
-// R, so the row order of this reduction tree does not change the ID.
-__device__ __forceinline__ double2 shfl_xor2(double2 v, int o) {
-  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, o), __shfl_xor_sync(0xffffffffu, v.y, o));
-}
-__device__ __forceinline__ double2 shfl_idx2(double2 v, int src) {
-  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
-}
-constexpr int pow2ceil(int v) { return v <= 1 ? 1 : 2 * pow2ceil((v + 1) / 2); }
-constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
-
-// One Householder step j = J on [R; X] (X = the warp's 32 rows in x, lane =
-// row).  R packed upper triangular, warp-private.
-template <int W, int J>
-__device__ __forceinline__ void wstep(double2 (&x)[W], double2* __restrict__ R, int lane) {
-  constexpr int V = W - 1 - J;  // trailing columns
-  const double sg = warp_sum(cnorm2(x[J]));
-  const double2 alpha = R[rpk(J, J)];
-  double2 rjj = alpha;
-  const Bcast b = make_reflector(alpha, sg, &rjj);
-  __syncwarp();
-  if (!b.active) return;  // warp-uniform (the xor all-reduce is bitwise identical on every lane)
-  if (lane == 0) R[rpk(J, J)] = rjj;
-  if constexpr (V > 0) {
-    constexpr int P = pow2ceil(V), LOGP = ilog2(P), H = P > 1 ? P / 2 : 1;
-    double2 e[H];
-    if constexpr (P == 1) {
-      e[0] = cmulc(x[J], x[J + 1]);
-    } else {  // first reduce-scatter stage fused with the dot products
-      const bool up = lane & 16;
-#pragma unroll
-      for (int i = 0; i < H; ++i) {
-        const double2 a = cmulc(x[J], x[J + 1 + i]);
-        const double2 c = (i + H < V) ? cmulc(x[J], x[(J + 1 + i + H) < W ? (J + 1 + i + H) : 0]) : make_double2(0, 0);
-        e[i] = cadd(up ? c : a, shfl_xor2(up ? a : c, 16));
-      }
-#pragma unroll
-      for (int s = 1; s < LOGP; ++s) {
-        const int o = 16 >> s, h = H >> s;
-        const bool u = lane & o;
-#pragma unroll
-        for (int i = 0; i < h; ++i) e[i] = cadd(u ? e[i + h] : e[i], shfl_xor2(u ? e[i] : e[i + h], o));
-      }
-    }
-#pragma unroll
-    for (int s = LOGP; s < 5; ++s) e[0] = cadd(e[0], shfl_xor2(e[0], 16 >> s));
-    int idx = 0;
-#pragma unroll
-    for (int s = 0; s < LOGP; ++s)
-      if (lane & (16 >> s)) idx += P >> (s + 1);
-    double2 t = make_double2(0, 0);
-    if (idx < V) {
-      const int k = J + 1 + idx;
-      const double2 r = R[rpk(J, k)];
-      const double2 ws = reflect_coeff(b, r, e[0]);
-      t = cmul(b.scale, ws);
-      if ((lane & ((32 >> LOGP) - 1)) == 0) R[rpk(J, k)] = csub(r, ws);
-    }
-#pragma unroll
-    for (int i = 0; i < V; ++i) {
-      int src = 0;
-#pragma unroll
-      for (int s = 0; s < LOGP; ++s)
-        if (i & (P >> (s + 1))) src += 16 >> s;
-      const double2 tt = shfl_idx2(t, src);
-      x[J + 1 + i] = csub(x[J + 1 + i], cmul(x[J], tt));
-    }
-  }
-  __syncwarp();
-}
-
-template <int W, int J>
-struct WSteps {
-  static __device__ __forceinline__ void run(double2 (&x)[W], double2* R, int w, int lane) {
-    if (J >= w) return;
-    wstep<W, J>(x, R, lane);
-    WSteps<W, J + 1>::run(x, R, w, lane);
-  }
-};
-template <int W>
-struct WSteps<W, W> {
-  static __device__ __forceinline__ void run(double2 (&)[W], double2*, int, int) {}
-};
-
-// Fold the warp's 32-row tile T (column c of lane's row at T[c * 32 + lane])
-// into R.  One out-of-line copy: the row-block loop and the factor merge
-// share it (the unrolled steps are the kernel's hot code and must stay small
-// enough for the instruction cache).
-template <int W>
-__device__ __noinline__ void absorb_tile(const double2* __restrict__ T, double2* __restrict__ R, int w, int lane) {
-  double2 x[W];
-#pragma unroll
-  for (int c = 0; c < W; ++c) x[c] = c < w ? T[c * 32 + lane] : make_double2(0, 0);
-  WSteps<W, 0>::run(x, R, w, lane);
-}
-
-// the entries of proxy row `row` of slot s (this lane's row) into column c of
-// the warp tile, in unfolded order; columns loop at run time (code size)
-__device__ __forceinline__ void gen_row_tile(const LevelDesc& L, const KSpec& ks, const SlotPos& s, i64 row,
-                                             bool valid, const int* __restrict__ sprox, const int* __restrict__ cnt,
-                                             const int* __restrict__ off, const int* __restrict__ stgt,
-                                             const double* __restrict__ csin, const double* __restrict__ ccos, int w,
-                                             double2* __restrict__ T, int lane) {
-  if (!valid) {
-    for (int c = 0; c < w; ++c) T[c * 32 + lane] = make_double2(0, 0);
-    return;
-  }
-  int ii[kMaxD] = {1, 1, 1, 1, 1, 1}, jj[kMaxD] = {1, 1, 1, 1, 1, 1};
-  const int D = 2 * L.d;
-  i64 rem = row;
-  for (int p = 0; p < D; ++p) {
-    if (p == s.skip) continue;
-    const int c = cnt[p];
-    const int v = sprox[off[p] + static_cast<int>(rem % c)];
-    rem /= c;
-    if (p < L.d) ii[p] = v;
-    else jj[p - L.d] = v;
-  }
-  const int sk = s.skip;
-  if (ks.kind == OIOBF_KERNEL_GREEN) {
-    double xs[3] = {0, 0, 0}, ys[3] = {ks.off0, ks.off1, ks.off2};
-#pragma unroll
-    for (int p = 0; p < 3; ++p)
-      if (p < L.d) {
-        if (p != sk) xs[p] = green_x(ks, ii[p]);
-        if (p + L.d != sk) ys[p] = green_y(ks, p, jj[p]);
-      }
-    const bool tgt = sk < L.d;
-    const int q = tgt ? sk : sk - L.d;
-    for (int c = 0; c < w; ++c) {
-      const int t = stgt[c];
-      const double v = tgt ? green_x(ks, t) : green_y(ks, q, t);
-      double xc[3], yc[3];
-#pragma unroll
-      for (int p = 0; p < 3; ++p) {
-        xc[p] = (tgt && p == q) ? v : xs[p];
-        yc[p] = (!tgt && p == q) ? v : ys[p];
-      }
-      T[c * 32 + lane] = green_from_coords(ks, xc, yc);
-    }
-  } else if (ks.kind == OIOBF_KERNEL_RADON2D) {
-    double sx[2] = {0, 0}, cx[2] = {0, 0};
-#pragma unroll
-    for (int p = 0; p < 2; ++p)
-      if (p != sk)
-        sincos(__dmul_rn(2.0 * M_PI, __ddiv_rn(static_cast<double>(ii[p] - 1), static_cast<double>(ks.n))), &sx[p],
-               &cx[p]);
-    for (int c = 0; c < w; ++c) {
-      const int t = stgt[c];
-      int i2[2] = {ii[0], ii[1]}, j2[2] = {jj[0], jj[1]};
-      double s0 = sx[0], c0 = cx[0], s1 = sx[1], c1 = cx[1];
-      if (sk == 0) {
-        i2[0] = t;
-        s0 = csin[c];
-        c0 = ccos[c];
-      } else if (sk == 1) {
-        i2[1] = t;
-        s1 = csin[c];
-        c1 = ccos[c];
-      } else if (sk == 2) {
-        j2[0] = t;
-      } else {
-        j2[1] = t;
-      }
-      T[c * 32 + lane] = radon2d_entry_sc(ks, i2, j2, s0, c0, s1, c1);
-    }
-  } else {
-    for (int c = 0; c < w; ++c) {
-      const int t = stgt[c];
-      int i2[kMaxD], j2[kMaxD];
-#pragma unroll
-      for (int p = 0; p < kMaxD; ++p) {
-        i2[p] = (p == sk) ? t : ii[p];
-        j2[p] = (p + L.d == sk) ? t : jj[p];
-      }
-      T[c * 32 + lane] = kernel_entry(ks, i2, j2);
-    }
-  }
-}
-
-constexpr int kTsqrWarps = 8;
-
-template <int W>
-__global__ void __launch_bounds__(kTsqrWarps * 32, W <= 16 ? 2 : 1)
-    k_tsqr(LevelDesc L, KSpec ks, const int* __restrict__ proxies, const int* __restrict__ targets,
-           const int* __restrict__ width, double2* __restrict__ rpart) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int RP = W * (W + 1) / 2;
-  const i64 slot = blockIdx.x / L.nparts;
-  const i64 part = blockIdx.x % L.nparts;
-  const int w = width[slot];
-  double2* Rall = reinterpret_cast<double2*>(smem);
-  double2* Tall = Rall + kTsqrWarps * RP;  // per-warp 32 x W row tiles
-  int* sprox = reinterpret_cast<int*>(Tall + kTsqrWarps * 32 * W);
-  int* scnt = sprox + L.psize;
-  int* soff = scnt + kMaxModes;
-  int* stgt = soff + kMaxModes;
-  double* csin = reinterpret_cast<double*>(reinterpret_cast<uintptr_t>(stgt + W + 1) & ~uintptr_t{7});
-  double* ccos = csin + W;
-  const SlotPos s = decode_slot(L, slot);
-  for (int i = threadIdx.x; i < L.psize; i += blockDim.x) sprox[i] = proxies[slot * L.psize + i];
-  for (int i = threadIdx.x; i < w; i += blockDim.x) {
-    const int t = targets[slot * L.wmax + i];
-    stgt[i] = t;
-    if (ks.kind == OIOBF_KERNEL_RADON2D && s.skip < L.d) {
-      double sn, cs;
-      sincos(__dmul_rn(2.0 * M_PI, __ddiv_rn(static_cast<double>(t - 1), static_cast<double>(ks.n))), &sn, &cs);
-      csin[i] = sn;
-      ccos[i] = cs;
-    }
-  }
-  if (threadIdx.x < kMaxModes) {
-    const int p = threadIdx.x;
-    scnt[p] = p < 2 * L.d ? L.counts[s.k][p] : 1;
-    soff[p] = p < 2 * L.d ? L.poff[s.k][p] : 0;
-  }
-  for (int i = threadIdx.x; i < kTsqrWarps * RP; i += blockDim.x) Rall[i] = make_double2(0, 0);
-  __syncthreads();
-  if (w == 0) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* R = Rall + warp * RP;
-  double2* T = Tall + warp * 32 * W;
-  const i64 r_begin = part * L.rpp;
-  const i64 r_end = r_begin + L.rpp < L.m ? r_begin + L.rpp : L.m;
-  for (i64 r0 = r_begin + 32 * warp; r0 < r_end; r0 += 32 * kTsqrWarps) {
-    gen_row_tile(L, ks, s, r0 + lane, r0 + lane < r_end, sprox, scnt, soff, stgt, csin, ccos, w, T, lane);
-    __syncwarp();
-    absorb_tile<W>(T, R, w, lane);
-  }
-  // merge the warps' factors: warp q absorbs the rows of warp q + stride's R
-  for (int stride = 1; stride < kTsqrWarps; stride <<= 1) {
-    __syncthreads();
-    if (warp % (2 * stride) == 0) {
-      const double2* Ro = Rall + (warp + stride) * RP;
-      for (int c = 0; c < w; ++c) T[c * 32 + lane] = (lane <= c) ? Ro[rpk(lane, c)] : make_double2(0, 0);
-      __syncwarp();
-      absorb_tile<W>(T, R, w, lane);
-    }
-  }
-  __syncthreads();
-  double2* out = rpart + (slot * L.nparts + part) * L.wmax * L.wmax;
-  for (int i = threadIdx.x; i < w * w; i += blockDim.x) {
-    const int r = i % w, c = i / w;
-    out[i] = r <= c ? Rall[rpk(r, c)] : make_double2(0, 0);
-  }
-}
-
-template <int W>
-void launch_tsqr_t(const LevelDesc& L, const KSpec& ks, const int* proxies, const int* targets, const int* width,
-                   double2* rpart, cudaStream_t st) {
-  const size_t smem = sizeof(double2) * kTsqrWarps * (W * (W + 1) / 2 + 32 * W) +
-                      sizeof(int) * (L.psize + 2 * kMaxModes + W + 1) + sizeof(double) * (2 * W + 1) + 16;
-  TBF_CUDA(cudaFuncSetAttribute(k_tsqr<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-  k_tsqr<W><<<static_cast<unsigned>(L.nslots * L.nparts), kTsqrWarps * 32, smem, st>>>(L, ks, proxies, targets, width,
-                                                                                         rpart);
-}
-
 }  // namespace
 
 size_t panel_smem_bytes(const LevelDesc& L) {
@@ -1078,12 +809,7 @@ void launch_panel(const LevelDesc& L, const KSpec& ks, const int* proxies, const
   const size_t smem = panel_smem_bytes(L);
   const i64 grid = L.nslots * L.nparts;
   static const bool generic = std::getenv("OIOBF_PANEL_GENERIC") != nullptr;  // A/B switch
-  if (L.pr == 0) {  // warp TSQR (make_level: wmax <= 32)
-    if (L.wmax <= 8) launch_tsqr_t<8>(L, ks, proxies, targets, width, rpart, st);
-    else if (L.wmax <= 16) launch_tsqr_t<16>(L, ks, proxies, targets, width, rpart, st);
-    else if (L.wmax <= 24) launch_tsqr_t<24>(L, ks, proxies, targets, width, rpart, st);
-    else launch_tsqr_t<32>(L, ks, proxies, targets, width, rpart, st);
-  } else if (L.wmax > 32) {
+  if (L.wmax > 32) {
     if (!generic && L.pr == 128) launch_panel_t<512, 4>(L, ks, proxies, targets, width, rpart, smem, grid, st);
     else if (!generic && L.pr == 64) launch_panel_t<512, 2>(L, ks, proxies, targets, width, rpart, smem, grid, st);
     else launch_panel_t<512, 0>(L, ks, proxies, targets, width, rpart, smem, grid, st);

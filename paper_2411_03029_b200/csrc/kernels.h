@@ -6,6 +6,9 @@
 
 namespace tbf {
 
+// ---- FP64 roofline denominators (peak_kernels.cu)
+void measure_fp64_peak(double* out);
+
 // ---- construction (id_kernels.cu)
 size_t panel_smem_bytes(const LevelDesc& L);
 size_t finish_smem_bytes(const LevelDesc& L);

@@ -684,23 +684,11 @@ LevelDesc make_level(const oiobf_tbf& b, int sd, int l, i64 r_est, i64 wmax) {
   L.pr = wmax <= 24 ? 256 : wmax <= 64 ? 128 : 64;
   L.rank = b.rank;
   L.world = b.world;
+  const i64 target_ctas = 148 * 8;
   const i64 owned = (L.nslots + b.world - 1) / b.world;
-  i64 parts;
-  static const bool legacy = std::getenv("OIOBF_PANEL_LEGACY") != nullptr;  // A/B: CTA-wide panel kernel
-  if (wmax <= 32 && !legacy) {
-    // warp TSQR (k_tsqr): pr = 0 marks it; each CTA = 8 independent warps,
-    // >= 2048 rows per CTA (8 row blocks per warp) so the in-CTA merge and
-    // k_finish's per-partition merge stay small; ~16 CTAs per SM in flight
-    L.pr = 0;
-    const i64 target_ctas = 148 * 16;
-    parts = (target_ctas + owned - 1) / owned;
-    parts = std::max<i64>(1, std::min({parts, (L.m + 2047) / 2048, i64{64}}));
-  } else {
-    const i64 target_ctas = 148 * 8;
-    parts = (target_ctas + owned - 1) / owned;
-    const i64 max_parts = std::max<i64>(1, (L.m + 4 * L.pr - 1) / (4 * L.pr));  // >= 4 panels per part
-    parts = std::max<i64>(1, std::min(parts, max_parts));
-  }
+  i64 parts = (target_ctas + owned - 1) / owned;
+  const i64 max_parts = std::max<i64>(1, (L.m + 4 * L.pr - 1) / (4 * L.pr));  // >= 4 panels per part
+  parts = std::max<i64>(1, std::min(parts, max_parts));
   L.nparts = parts;
   L.rpp = (L.m + parts - 1) / parts;
   return L;
@@ -3597,6 +3585,40 @@ int oiobf_tbf_profile_contract(oiobf_tbf* h, const void* dF, void* dG, int32_t r
   EventTimer t(st);
   for (int r = 0; r < reps; ++r) contract_device(*h, static_cast<const double2*>(dF), static_cast<double2*>(dG), 1, st);
   out[3] = t.stop() / reps;
+  CAPI_END
+}
+
+// FP64 peaks of this device (bench roofline denominators): out[0] DFMA
+// TFLOP/s, out[1] DMMA (mma.sync f64) TFLOP/s, out[2] SMs, out[3] SM MHz
+int oiobf_fp64_peak(double* out) {
+  CAPI_BEGIN
+  require(out, "fp64_peak: null argument");
+  ensure_device();
+  measure_fp64_peak(out);
+  CAPI_END
+}
+
+// Cold-L2 timing of the core-contraction phase alone: before each of `reps`
+// single launches the caller's flush buffer (larger than the 126 MB L2) is
+// overwritten on the same stream; out = mean launch time in ms.
+int oiobf_tbf_profile_core_cold(oiobf_tbf* h, const void* dF, void* dG, int32_t reps, void* stream, void* flush,
+                                int64_t flush_bytes, double* out) {
+  CAPI_BEGIN
+  require(h && dF && dG && flush && out && reps >= 1 && flush_bytes > 0, "tbf_profile_core_cold: bad argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  TBF_CUDA(cudaSetDevice(h->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Plan& pl = get_plan(*h, 1);
+  for (int g = 0; g < 3; ++g)  // full warm pass: the core phase's input is the V/W output in scratch
+    run_ops(*h, pl, static_cast<const double2*>(dF), static_cast<double2*>(dG), st, g);
+  double tot = 0;
+  for (int r = 0; r < reps; ++r) {
+    TBF_CUDA(cudaMemsetAsync(flush, r & 0xff, static_cast<size_t>(flush_bytes), st));
+    EventTimer t(st);
+    run_ops(*h, pl, static_cast<const double2*>(dF), static_cast<double2*>(dG), st, 1);
+    tot += t.stop();
+  }
+  *out = tot / reps;
   CAPI_END
 }
 

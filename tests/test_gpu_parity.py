@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import paper_2411_03029_b200 as tb
-from paper_2411_03029_b200.configs import BY_NAME, dft, green_cubes, green_plates, nudft, radon2d, radon3d
+from paper_2411_03029_b200.configs import ACCURACY_STRATEGY, BY_NAME, dft, green_cubes, green_plates, nudft, radon2d, radon3d
 
 from helpers import TIE_EPS, compare_factorizations, level_base, rel, slot_geometry, slot_target
 
@@ -436,34 +436,102 @@ def test_invalid_arguments():
 
 
 # ------------------------------------------------- full-size configs (sampled)
-@pytest.mark.parametrize("cfg", ["green_plates_n64", "green_cubes_n64"])
-def test_full_config_sampled_slots(oracle, cfg):
-    """At BASELINE sizes: every rank/skeleton of a random sample of slots is
-    recomputed by the oracle from the same proxies and candidate columns."""
-    c = BY_NAME[cfg]
-    spec = c.spec
-    bf = tb.tbf_construct(spec, c.L, c.tol, seed=c.seed)
-    fz = bf.export()
+def check_sampled_slots(oracle, c, fz, nper, q=3, cap=1 << 17, seed=7):
+    """Recompute `nper` random slots of every (side, level) with the oracle from
+    the same proxies and candidate columns (id.cpp:199-231 + 24-130): ranks and
+    skeletons exact (ties replayed), interps to 1e-8."""
     so, io, po, _ = fz.offsets()
-    rng = np.random.default_rng(7)
+    rng = np.random.default_rng(seed)
     for sd, l, cnt in fz.level_counts():
-        base = sum(x for s2, l2, x in fz.level_counts() if (s2, l2) < (sd, l))
+        base = level_base(fz, sd, l)
         r_est = int(fz.r_est[sd * (fz.Lc + 1) + l])
-        for idx in rng.choice(cnt, size=min(cnt, 4), replace=False):
+        for idx in rng.choice(cnt, size=min(cnt, nper), replace=False):
             g = base + int(idx)
             geo = slot_geometry(fz.d, fz.n, fz.L, fz.Lc, sd, l, int(idx))
             target = slot_target(fz, sd, l, int(idx))
-            lists = oracle.proxy_lists(geo["ranges"], geo["skip"], 3 * r_est,
+            lists = oracle.proxy_lists(geo["ranges"], geo["skip"], q * r_est, q=q, row_cap=cap,
                                        seed=oracle.derive_seed(c.seed, geo["tags"]))
             lists[geo["skip"]] = target
-            A = oracle.unfolding(spec, lists, geo["skip"])
+            A = oracle.unfolding(c.spec, lists, geo["skip"])
             assert A.shape[0] == fz.rows[g]
             o = oracle.column_id(A, c.tol, forced_perm=fz.perm[po[g]:po[g + 1]], forced_rank=int(fz.ranks[g]))
-            assert not o["mismatch"]
+            assert not o["mismatch"], (sd, l, int(idx))
             assert o["rank"] == fz.ranks[g]
             np.testing.assert_array_equal(target[o["skeleton"] - 1], fz.skel[so[g]:so[g + 1]])
             gi = fz.interp[io[g]:io[g + 1]].reshape((fz.ranks[g], fz.ncols[g]), order="F")
             assert np.max(np.abs(gi - o["interp"])) <= 1e-8 * max(1, np.max(np.abs(o["interp"])))
+
+
+@pytest.mark.parametrize("cfg,nper", [("green_plates_n64", 4), ("green_cubes_n64", 4), ("green_cubes_n256", 3),
+                                      ("radon2d_n1024", 2)])
+def test_full_config_sampled_slots(oracle, cfg, nper):
+    """At BASELINE sizes (configs 1, 2, 3, 5; config 4 below): every rank /
+    skeleton of a random sample of slots of every (side, level) is recomputed
+    by the oracle from the same proxies and candidate columns."""
+    c = BY_NAME[cfg]
+    bf = tb.tbf_construct(c.spec, c.L, c.tol, seed=c.seed)
+    check_sampled_slots(oracle, c, bf.export(pairs=[]), nper)
+
+
+def test_config2_accuracy_strategy_sampled_slots(oracle):
+    """The accuracy strategy's proxy lists (q = 3, row_cap = 2^23: 8e6 rows per
+    ID, no halving) through the same oracle recomputation."""
+    c = BY_NAME["green_cubes_n64"]
+    q, cap = ACCURACY_STRATEGY[c.name]
+    bf = tb.tbf_construct(c.spec, c.L, c.tol, tb.ProxyStrategy(q=q, row_cap=cap), seed=c.seed)
+    check_sampled_slots(oracle, c, bf.export(pairs=[]), 1, q=q, cap=cap)
+
+
+def test_config3_apply_matches_oracle(oracle):
+    """Config 3 (green cubes n = 256, 16.7M points, 2.9 GB of cores) at full
+    size: the GPU contraction equals the oracle's contraction on the SAME
+    factors to 1e-10 (Alg. 2, tensor.cpp:136-166, id.cpp:305-329), and
+    1000 sampled outputs are compared with direct dense sums (reported)."""
+    c = BY_NAME["green_cubes_n256"]
+    spec = c.spec
+    bf = tb.tbf_construct(spec, c.L, c.tol, seed=c.seed)
+    rng = np.random.default_rng(9)
+    F = rand_c(rng, (spec.n,) * spec.d)
+    G = bf.contract(F)
+    ob = oracle.tbf_import(spec, c.L, c.tol, bf.export())
+    Go = ob.contract(F)
+    assert rel(G, Go) < 1e-10, rel(G, Go)
+    rows = rng.choice(spec.n ** spec.d, 1000, replace=False)
+    exact = tb.dense_rows(spec, F, rows)[:, 0]
+    err = rel(G.reshape(-1, order="F")[rows], exact)
+    err_o = rel(Go.reshape(-1, order="F")[rows], exact)
+    print(f"config 3 default strategy: sampled rel err {err:.3e} (oracle {err_o:.3e}, tol {c.tol:g})")
+    assert abs(err - err_o) <= 1e-6 * err_o
+
+
+def test_config5_blockwise_apply_matches_oracle(oracle):
+    """Config 5 (Radon 2D n = 1024, 95 GB of cores: too large to hold twice on
+    the host) block-wise: F supported on two middle column blocks s; the GPU
+    contraction of the full operator equals the oracle's contraction on the
+    same factors with the cores of exactly those pairs (t, s) (every other
+    pair's input is zero, so the two agree to rounding), to 1e-10.  Plus 1000
+    sampled outputs of a full random input against direct dense sums."""
+    c = BY_NAME["radon2d_n1024"]
+    spec = c.spec
+    bf = tb.tbf_construct(spec, c.L, c.tol, seed=c.seed)
+    nmid, mpm, msz = 2 ** (spec.d * (c.L // 2)), 2 ** (c.L // 2), spec.n >> (c.L // 2)
+    S = [5, 42]
+    pairs = sorted(s * nmid + t for s in S for t in range(nmid))
+    rng = np.random.default_rng(12)
+    F = np.zeros((spec.n, spec.n), np.complex128)
+    for s in S:
+        s1, s2 = s % mpm, s // mpm
+        F[s1 * msz:(s1 + 1) * msz, s2 * msz:(s2 + 1) * msz] = rand_c(rng, (msz, msz))
+    G = bf.contract(F)
+    ob = oracle.tbf_import(spec, c.L, c.tol, bf.export(pairs=pairs))
+    Go = ob.contract(F)
+    assert rel(G, Go) < 1e-10, rel(G, Go)
+    del ob
+    Ff = rand_c(rng, (spec.n, spec.n))
+    Gf = bf.contract(Ff).reshape(-1, order="F")
+    rows = rng.choice(spec.n ** spec.d, 1000, replace=False)
+    exact = tb.dense_rows(spec, Ff, rows)[:, 0]
+    print(f"config 5 default strategy: sampled rel err {rel(Gf[rows], exact):.3e} (tol {c.tol:g})")
 
 
 def test_config4_full_size(oracle):
@@ -509,12 +577,13 @@ def test_config4_full_size(oracle):
     assert err <= c.tol, f"sampled relative error {err:.3e} > tol"
 
 
-@pytest.mark.parametrize("cfg,gate", [("green_plates_n64", 10), ("green_cubes_n64", 30)])
-def test_full_config_accuracy(oracle, cfg, gate):
-    """1000 sampled outputs vs direct dense sums (BASELINE check).  The error is
-    a property of the reference's proxy strategy: the GPU must
-    reproduce the oracle's error on the same factors; the ratio to tol is
-    reported and gated loosely."""
+@pytest.mark.parametrize("cfg", ["green_plates_n64", "green_cubes_n64"])
+def test_full_config_default_strategy_error_matches_oracle(oracle, cfg):
+    """Reference default ProxyStrategy (q = 3, row_cap = 2^17): 1000 sampled
+    outputs vs direct dense sums.  The default strategy is proxy-deficient for
+    these operators (7.6-17x tol, every proxy row gives 0.2-0.7x),
+    so this test gates parity, not tol: the GPU's error equals the oracle's on
+    the same factors, and GPU dense sums equal the oracle's."""
     c = BY_NAME[cfg]
     spec = c.spec
     bf = tb.tbf_construct(spec, c.L, c.tol, seed=c.seed)
@@ -530,9 +599,32 @@ def test_full_config_accuracy(oracle, cfg, gate):
     Go = ob.contract(F).reshape(-1, order="F")
     assert rel(G, Go) < 1e-10
     err_o = rel(Go[rows], exact)
-    print(f"{cfg}: sampled rel err gpu {err:.3e} oracle {err_o:.3e} (tol {c.tol:g}, ratio {err / c.tol:.1f})")
+    print(f"{cfg} default strategy: sampled rel err gpu {err:.3e} oracle {err_o:.3e} (ratio {err / c.tol:.1f})")
     assert abs(err - err_o) <= 1e-3 * err_o
-    assert err <= gate * c.tol
+
+
+@pytest.mark.parametrize("cfg", ["green_plates_n64", "green_cubes_n64"])
+def test_full_config_accuracy_gate(oracle, cfg):
+    """north_star accuracy gate at 1 x tol: 1000 sampled outputs within the
+    stated ID tolerance of direct dense sums, with the config's accuracy
+    ProxyStrategy (configs.ACCURACY_STRATEGY), the GPU apply equal to the
+    oracle's on the same factors.  (Configs 3 and 5 are measured with their
+    accuracy strategies by tools/accuracy_configs.py: profiles/r2_accuracy_*.)"""
+    c = BY_NAME[cfg]
+    spec = c.spec
+    q, cap = ACCURACY_STRATEGY[cfg]
+    bf = tb.tbf_construct(spec, c.L, c.tol, tb.ProxyStrategy(q=q, row_cap=cap), seed=c.seed)
+    rng = np.random.default_rng(8)
+    F = rand_c(rng, (spec.n,) * spec.d)
+    G = bf.contract(F).reshape(-1, order="F")
+    rows = rng.choice(spec.n ** spec.d, 1000, replace=False)
+    exact = tb.dense_rows(spec, F, rows)[:, 0]
+    err = rel(G[rows], exact)
+    ob = oracle.tbf_import(spec, c.L, c.tol, bf.export())
+    assert rel(G, ob.contract(F).reshape(-1, order="F")) < 1e-10
+    print(f"{cfg} accuracy strategy q={q} row_cap=2^{cap.bit_length() - 1}: sampled rel err {err:.3e} "
+          f"(ratio {err / c.tol:.2f})")
+    assert err <= c.tol, f"sampled relative error {err:.3e} > tol {c.tol:g}"
 
 
 def _factorization_from_tbf1(t):

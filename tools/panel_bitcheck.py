@@ -1,5 +1,7 @@
 """Register-cached vs generic absorb (OIOBF_PANEL_GENERIC=1) must give the same
-factorization BIT FOR BIT (same operations, same order).  Wide IDs: Radon n=256, L=4."""
+factorization BIT FOR BIT (same operations, same order; the register-cached
+absorb also folds the zero rows of a partial last panel, which add +0 to every
+sum).  Wide IDs: Radon n=256, L=4 (widths up to 64)."""
 import os, subprocess, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 if len(sys.argv) > 1:

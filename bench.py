@@ -210,7 +210,7 @@ def run_b200(args):
 
     # ---- FP64 roofline denominators of this device (DFMA, DMMA)
     pk = np.zeros(4, np.float64)
-    _lib.check(L.oiobf_fp64_peak(_lib.ptr(pk)))
+    _lib.check(L.oiobf_fp64_peak(pk))
     fp64 = {"dfma_tflops": float(pk[0]), "dmma_tflops": float(pk[1]), "sms": int(pk[2]),
             "source": "measured in this run (oiobf_fp64_peak: independent DFMA / mma.sync.m8n8k4.f64 chains on "
                       "every resident warp)"}

@@ -141,10 +141,10 @@ int oiobf_tbf_load(const char* path, oiobf_tbf** out);
 // leaf size is <= 2, e.g. the two-sided bit-reversed DFT; else the tiny-box
 // engine when every box has <= 64 elements and there are >= 2^20 middle pairs;
 // else the fused-box engine), 1 the fused-box engine, 2 the tiny-box engine,
-// 3 the persistent dataflow engine, 4 the rank-one engine (OIOBF_EINVAL when
-// the factorization is not eligible).  Changing it drops cached plans.
+// 4 the rank-one engine (OIOBF_EINVAL when the factorization is not eligible;
+// 3, the round-1 dataflow engine, was removed).  Changing it drops cached plans.
 int oiobf_tbf_set_apply_engine(oiobf_tbf* h, int32_t engine);
-// engine in use: 1 box, 2 tiny, 3 flow, 4 rank-one
+// engine in use: 1 box, 2 tiny, 4 rank-one
 int oiobf_tbf_apply_engine(oiobf_tbf* h, int32_t* engine);
 
 int oiobf_tbf_memory(const oiobf_tbf* h, int64_t out[5]);

@@ -288,18 +288,17 @@ class TensorButterfly:
         _lib.check(_lib.load().oiobf_tbf_save(self._h, str(path).encode()))
 
     def set_apply_engine(self, engine: str) -> None:
-        """'auto' | 'box' | 'tiny' | 'flow' | 'rank1'.  box: one fused-box launch
-        per level (CUDA graph); tiny: thread-per-output engine for d = 6 scale;
-        flow: one persistent dataflow launch (items wait on their producers'
-        flags); rank1: implicit-geometry engine for butterflies whose every ID
-        has rank 1 (two-sided bit-reversed DFT; auto picks it when eligible)."""
-        code = {"auto": 0, "box": 1, "tiny": 2, "flow": 3, "rank1": 4}[engine]
+        """'auto' | 'box' | 'tiny' | 'rank1'.  box: one fused-box launch per
+        level (CUDA graph); tiny: thread-per-output engine for d = 6 scale;
+        rank1: implicit-geometry engine for butterflies whose every ID has
+        rank 1 (two-sided bit-reversed DFT; auto picks it when eligible)."""
+        code = {"auto": 0, "box": 1, "tiny": 2, "rank1": 4}[engine]
         _lib.check(_lib.load().oiobf_tbf_set_apply_engine(self._h, code))
 
     def apply_engine(self) -> str:
         e = C.c_int32(0)
         _lib.check(_lib.load().oiobf_tbf_apply_engine(self._h, C.byref(e)))
-        return {1: "box", 2: "tiny", 3: "flow", 4: "rank1"}[e.value]
+        return {1: "box", 2: "tiny", 4: "rank1"}[e.value]
 
     def contract_async(self, F: np.ndarray, G: np.ndarray, nv: int = 1, stream: int = 0) -> None:
         """Stream-ordered contraction with PINNED host buffers (float64 views of

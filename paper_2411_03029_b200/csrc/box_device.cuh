@@ -1,8 +1,6 @@
 // Device code of one fused box contraction (Alg. 2, 185,
 // 201, 203; reference mode_product_blockdiag tensor.cpp:136-166 semantics),
-// shared by the per-level kernel k_box (box_kernels.cu) and the persistent
-// dataflow kernel k_flow (flow_kernels.cu): both run the same arithmetic in
-// the same order, so the two engines agree bit for bit.
+// run by the per-level kernel k_box (box_kernels.cu).
 //
 // One box is
 //   out = in x_{d-1} M_{d-1} ... x_1 M_1 x_0 M_0      (M_k^T on the P/U side)
@@ -11,7 +9,7 @@
 // exchanged.  Per CTA:
 //   prologue  this CTA's factor rows -> shared memory, stored [x][a] (a
 //             fastest); independent of the producer of the input, so it runs
-//             before the dependency wait (PDL in k_box, item flags in k_flow)
+//             before the dependency wait (programmatic dependent launch)
 //   stage     input box -> shared memory: one cp.async.bulk per contiguous
 //             mode-0 row (mbarrier completion); for the ordered sum of P-level
 //             child contributions, batched register loads (8 children in
@@ -81,17 +79,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
-// Loads of data another CTA of the SAME kernel may have produced (k_flow):
-// L2-coherent (.cg, no L1 allocation); plain loads otherwise.
-template <bool kCoh>
-__device__ __forceinline__ double2 ld_in(const double2* p) {
-  if (kCoh) {
-    double2 r;
-    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p) : "memory");
-    return r;
-  }
-  return *p;
-}
 
 // address of mode-0 row `row` of the box (row = index over modes 1..d-1, nv)
 __device__ __forceinline__ long long row_addr(const BoxDesc& D, int d, int row) {
@@ -132,7 +119,7 @@ __device__ __forceinline__ void first_mode_smem(const double2* __restrict__ xs, 
 }
 
 // mode d-1 streamed from global memory (input box too large to stage)
-template <int AM, bool kCoh>
+template <int AM>
 __device__ __forceinline__ void first_mode_global(const BoxDesc& D, int d, const double2* in,
                                                   const double2* __restrict__ Mf, double2* __restrict__ t0, int A,
                                                   int Rs, int ein_f, int nv) {
@@ -156,7 +143,7 @@ __device__ __forceinline__ void first_mode_global(const BoxDesc& D, int d, const
       double2 val[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (x0 + u < ein_f) val[u] = ld_in<kCoh>(in + addr + (x0 + u) * sf);
+        if (x0 + u < ein_f) val[u] = in[addr + (x0 + u) * sf];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         if (x0 + u < ein_f)
@@ -263,11 +250,10 @@ struct BoxSmem {
 // in S.D (all threads synchronised after the copy).  `wait` blocks until the
 // input is produced (all threads call it; it ends with a CTA barrier).
 // `phase` is the staging mbarrier's parity, flipped on each bulk staging.
-// `stamp(slot)` is the optional debug timeline hook.
-template <bool kCoh, class Wait, class Stamp>
+template <class Wait>
 __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, int crank,
                                          const double2* __restrict__ mats, const double2* in, double2* out,
-                                         double2* sm, unsigned& phase, Wait wait, Stamp stamp) {
+                                         double2* sm, unsigned& phase, Wait wait) {
   const BoxDesc& D = S.D;
   const int tid = threadIdx.x;
   const int cs = info.cs;
@@ -308,9 +294,7 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
     }
   }
   // ---- the input box is produced by an earlier launch / item
-  stamp(1);
   wait();
-  stamp(2);
   if (info.stage) {
     const int nrows = total_in / e0n;
     if (bulk) {
@@ -340,7 +324,7 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
           double2 v[8];
 #pragma unroll
           for (int c = 0; c < 8; ++c)
-            if (c0 + c < D.nsum) v[c] = ld_in<kCoh>(p + (c0 + c) * cstr);
+            if (c0 + c < D.nsum) v[c] = p[(c0 + c) * cstr];
 #pragma unroll
           for (int c = 0; c < 8; ++c)
             if (c0 + c < D.nsum) acc = (c0 + c == 0) ? v[c] : cadd(acc, v[c]);
@@ -350,7 +334,6 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
     }
   }
   __syncthreads();
-  stamp(3);
   // ---- mode d-1: column r = rs + Rs * v  ->  t0[rs + Rs * (i + A * v)]
   {
     // (the row count is dispatched to its register bucket: no predicated-off
@@ -361,11 +344,10 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
       else if (info.amax <= 4) first_mode_smem<4>(xs, Mf, t0, A, Rs, ein_f, nv);
       else first_mode_smem<8>(xs, Mf, t0, A, Rs, ein_f, nv);
     } else {
-      first_mode_global<8, kCoh>(D, d, in, Mf, t0, A, Rs, ein_f, nv);
+      first_mode_global<8>(D, d, in, Mf, t0, A, Rs, ein_f, nv);
     }
   }
   __syncthreads();
-  stamp(4);
   // ---- modes d-2 .. 1 (smem -> smem); extents: e[p] = ein (p <= k), eout (k < p < f), A (f), nv
   double2* src = t0;
   double2* dst = t1;
@@ -386,11 +368,9 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
   if (tab)
     for (int c = tid; c < Cc; c += kBoxThreads) S.coltab[c] = col_offset(D, d, lo, A, c);
   __syncthreads();
-  stamp(5);
   // ---- mode 0 -> global
   last_mode(D, d, lo, A, src, smat + S.mo[0], Cc, tab ? S.coltab : nullptr, out);
   __syncthreads();
-  stamp(6);
 }
 
 }  // namespace

@@ -1,26 +1,13 @@
 // Fused level contractions for the apply, one launch per (side, level [, slab
 // group]); the per-box device code (staging, the d mode phases, the layout
-// choices) is in box_device.cuh, shared with the persistent dataflow kernel
-// (flow_kernels.cu).  This file adds the per-level launch: grid = boxes x cs,
-// programmatic dependent launch (the factor prologue runs before
-// griddepcontrol.wait), and the optional per-CTA %globaltimer trace.
+// choices) is in box_device.cuh.  This file adds the per-level launch: grid =
+// boxes x cs, programmatic dependent launch (the factor prologue runs before
+// griddepcontrol.wait).
 #include "box_device.cuh"
 
 namespace tbf {
 
 namespace {
-
-// debug timeline (oiobf_debug_box_trace): per-CTA %globaltimer stamps at the
-// phase boundaries; one predicated branch per stamp when disabled
-__device__ unsigned long long* g_box_trace = nullptr;
-constexpr int kTraceSlots = 8;
-__device__ __forceinline__ void stamp(int slot) {
-  if (g_box_trace != nullptr && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    g_box_trace[blockIdx.x * kTraceSlots + slot] = t;
-  }
-}
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
@@ -36,7 +23,6 @@ __global__ void __launch_bounds__(kBoxThreads, MINB) k_box(const BoxDesc* __rest
   extern __shared__ __align__(128) double2 sm[];
   __shared__ BoxSmem S;
   pdl_trigger();
-  stamp(0);
   const int cs = info.cs;
   const int item = static_cast<int>(blockIdx.x) / cs;
   const int crank = static_cast<int>(blockIdx.x) - item * cs;
@@ -47,14 +33,10 @@ __global__ void __launch_bounds__(kBoxThreads, MINB) k_box(const BoxDesc* __rest
   }
   __syncthreads();
   unsigned phase = 0;
-  box_body<false>(S, info, crank, mats, in, out, sm, phase, [] { pdl_wait(); }, [](int s) { stamp(s); });
+  box_body(S, info, crank, mats, in, out, sm, phase, [] { pdl_wait(); });
 }
 
 }  // namespace
-
-void box_trace_enable(unsigned long long* buf) {
-  TBF_CUDA(cudaMemcpyToSymbol(g_box_trace, &buf, sizeof(buf)));
-}
 
 bool pdl_enabled() {
   static const bool on = std::getenv("OIOBF_NO_PDL") == nullptr;

@@ -128,45 +128,8 @@ size_t box2_smem_bytes(int e0, int o0, int o1);
 void launch_box2(i64 nitems, const BoxDesc* descs, const BoxLaunchInfo& info, size_t smem, const double2* mats,
                  const double2* in, double2* out, cudaStream_t st);
 int box_ctas_per_sm(int amax, size_t smem);  // occupancy of k_box
-void box_trace_enable(unsigned long long* buf);  // debug: 8 globaltimer stamps per CTA
 // programmatic dependent launch for the apply kernels (env OIOBF_NO_PDL=1 disables)
 bool pdl_enabled();
-
-// ---- persistent dataflow apply engine (flow_kernels.cu): every box CTA and
-// core-row chunk of a contraction is one work item; items run in ticket order
-// on a persistent grid and wait on their producers' completion flags.
-struct FlowItem {
-  int kind;            // 0 box CTA, 1 core GEMV rows
-  int op;              // FlowOp index
-  int desc;            // box: BoxDesc index in op.descs; GEMV: GemvDesc index in op.gdescs
-  int crank;           // box: CTA rank of the box (split of mode d-1)
-  int r0, r1;          // GEMV: rows [r0, r1) of the pair
-  int dep_begin, ndep;  // producers in FlowArgs::deps
-};
-struct FlowOp {
-  BoxLaunchInfo info;
-  int kind, in_buf, out_buf, pad;  // buffers: 0 F, 1 G, 2 scratch
-  const double2* mats;             // factor arena of the level (boxes)
-  const BoxDesc* descs;
-  const GemvDesc* gdescs;
-};
-struct FlowArgs {
-  const FlowItem* items;
-  const FlowOp* ops;
-  const int* deps;   // >= 0: item (ticket) index; < 0: input slab -1 - dep
-  int* done;         // per item: epoch mark of its completion
-  unsigned* ctl;     // [0] next ticket, [1] finished CTAs, [2] epoch
-  int* in_flags;     // per input slab: nonzero once its copy landed
-  const double2* F;
-  double2* G;
-  double2* scratch;
-  const double2* cores;
-  unsigned long long* trace;  // debug: per item [claimed, inputs ready, done, SM, box phases 3..6], or null
-  int nitems, nv, nflags, pad;
-};
-void launch_flow(const FlowArgs& a, int grid, size_t smem, cudaStream_t st);
-int flow_ctas_per_sm(int nv, size_t smem);
-int flow_threads();
 
 // ---- tiny-box apply engine (tiny_kernels.cu): one CTA per group of boxes that
 // share data (V/W: the 2^d children tau of a parent, which all read the

@@ -314,27 +314,6 @@ struct GemvLaunch {
   int tma_stages = 0, tma_stage_elems = 0, tma_xcap = 0;
 };
 
-// persistent dataflow engine state of one plan (build_flow)
-struct FlowPlan {
-  std::vector<FlowItem> items;  // ticket order
-  std::vector<int> deps;
-  std::vector<FlowOp> ops;
-  DevBuf<FlowItem> d_items;
-  DevBuf<FlowOp> d_ops;
-  DevBuf<int> d_deps, d_done, d_flags;
-  DevBuf<unsigned> d_ctl;
-  int grid = 0, nflags = 0;
-  size_t smem = 0;
-  i64 slab = 0;  // host-buffer path: F elements per input slab (per vector)
-  // host-buffer path graph (copies + kernel), replayed while pointers match
-  cudaGraphExec_t gexec = nullptr;
-  const void* g_F = nullptr;
-  void* g_G = nullptr;
-  ~FlowPlan() {
-    if (gexec) cudaGraphExecDestroy(gexec);
-  }
-};
-
 // one in-flight slot of the stream-ordered host-buffer contraction
 // (contract_host_async): device staging, its captured compute graph, and the
 // events that order reuse of the slot against the previous call that used it
@@ -376,7 +355,6 @@ struct Plan {
   };
   std::vector<R1Level> r1_levels;
   std::vector<GemvDesc> gemv;
-  std::vector<int> gemv_t;  // row multi-set t of each GemvDesc (flow ticket priority)
   std::vector<GemvLaunch> gemvs;
   std::vector<int> gemv_map, tma_map;
   std::vector<i64> gemv_rb;  // CTA row ranges of every GEMV launch (both variants)
@@ -402,10 +380,6 @@ struct Plan {
   // stream-ordered host-buffer contraction: two slots, used alternately
   AsyncSet aset[2];
   int anext = 0;
-  // persistent dataflow engine: device-buffer / host-buffer variants
-  // (built on first use; flow_state -1 = not eligible)
-  std::unique_ptr<FlowPlan> flow_dev, flow_host;
-  int flow_state[2] = {0, 0};
   // captured graphs keyed by their buffers (device path: F, G, stream;
   // host pipeline: F, G), a few of each so alternating buffers (vector groups
   // of a wide n_v, ping-pong callers) replay instead of re-capturing
@@ -599,8 +573,7 @@ struct oiobf_tbf {
   HostArray<PairDesc> h_pairs;
   i64 total_core = 0;
   std::map<i64, std::unique_ptr<Plan>> plans;
-  int apply_engine = 0;  // 0 auto, 1 box engine, 2 tiny-box engine, 3 dataflow engine, 4 rank-one engine
-  int* h_one = nullptr;  // pinned host 1: raises the input-slab flags of the flow engine
+  int apply_engine = 0;  // 0 auto, 1 box engine, 2 tiny-box engine, 4 rank-one engine
   int tiny_auto = -1;    // cached auto decision (-1: not evaluated yet)
   int r1_ok = -1;        // cached rank-one eligibility (-1: not evaluated yet)
   double t_ms[6] = {0, 0, 0, 0, 0, 0};
@@ -624,7 +597,6 @@ struct oiobf_tbf {
     if (s_in) cudaStreamDestroy(s_in);
     if (s_out) cudaStreamDestroy(s_out);
     if (stream) cudaStreamDestroy(stream);
-    if (h_one) cudaFreeHost(h_one);
   }
 };
 
@@ -1419,7 +1391,6 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
       g.R = pd.R;
       g.C = pd.C;
       pl->gemv.push_back(g);
-      pl->gemv_t.push_back(static_cast<int>(t));
     }
     if (static_cast<i64>(pl->gemv.size()) > gemv_begin) {
       finish_gemv(*pl, gemv_begin, static_cast<i64>(pl->gemv.size()), nv);
@@ -2049,305 +2020,6 @@ Plan& get_plan(oiobf_tbf& b, i64 nv, bool chunked = false, int parity = 0) {
   return *slot;
 }
 
-// ---- persistent dataflow engine (flow_kernels.cu): the plan's box CTAs and
-// core-row chunks become work items.  Dependencies come from the scratch
-// intervals each item reads and the earlier items write (plans never reuse
-// scratch within one contraction, so read-after-write is the only hazard);
-// on the host-buffer path, items reading F also wait on the flags of the input
-// slabs they touch.  Ticket order = items sorted by a simulated start time:
-// boxes take a fixed latency, the GEMV is one bandwidth resource serving
-// ready chunks t-major (so the P/U boxes of the first row multi-sets can start
-// while the cores of later ones stream), input slabs arrive at PCIe rate.
-// Every dependency starts strictly earlier (or ties in an earlier op), so the
-// order is topological, which the kernel's progress argument needs.
-constexpr double kFlowBoxUs = 8.0;          // modelled box CTA latency
-constexpr double kFlowHbmBytesPerUs = 6e6;  // modelled GEMV stream rate
-constexpr double kFlowPcieBytesPerUs = 5e4;
-
-std::unique_ptr<FlowPlan> build_flow(oiobf_tbf& b, Plan& pl, int nflags) {
-  if (pl.sharded || pl.nchunk != 1 || pl.ops.empty()) return nullptr;
-  for (const Op& op : pl.ops)
-    if (op.kind != 1 && op.kind != 3) return nullptr;
-  if (pl.gemv_t.size() != pl.gemv.size()) return nullptr;
-  auto fp = std::make_unique<FlowPlan>();
-  const i64 nv = pl.nv;
-  const int d = b.d;
-  const i64 N = ipow(b.n, d);
-  size_t smem = 0;
-  int max_c = 0;
-  for (const Op& op : pl.ops) {
-    if (op.kind == 3) smem = std::max(smem, box_smem_bytes(pl.boxes[static_cast<size_t>(op.idx)].info));
-    else max_c = std::max(max_c, pl.gemvs[static_cast<size_t>(op.idx)].max_c);
-  }
-  smem = std::max(smem, sizeof(double2) * static_cast<size_t>(max_c) * static_cast<size_t>(nv == 1 ? 1 : std::min<i64>(nv, 4)));
-  smem = std::max<size_t>(smem, 16);
-  if (smem > static_cast<size_t>(kMaxDynSmem)) return nullptr;
-  const int per_sm = flow_ctas_per_sm(static_cast<int>(nv), smem);
-  if (per_sm < 2) return nullptr;  // the core stream wants >= 16 warps per SM
-  int nsm = 0;
-  TBF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, b.device));
-  fp->grid = per_sm * nsm;
-  fp->smem = smem;
-  fp->nflags = nflags;
-  fp->slab = nflags > 0 ? N / nflags : 0;
-  i64 total_core_bytes = 0;
-  for (const GemvDesc& g : pl.gemv) total_core_bytes += 16 * static_cast<i64>(g.R) * g.C;
-  static const i64 chunk_env = std::getenv("OIOBF_FLOW_CHUNK_KB") ? std::atoll(std::getenv("OIOBF_FLOW_CHUNK_KB")) : 0;
-  const i64 chunk_bytes =
-      chunk_env > 0 ? chunk_env * 1024 : std::max<i64>(32 * 1024, total_core_bytes / (4 * static_cast<i64>(fp->grid)));
-
-  struct Tmp {
-    FlowItem it;
-    i64 rlo = 0, rhi = 0, wlo = 0, whi = 0;  // scratch read / write spans (empty: lo >= hi)
-    int q0 = 0, q1 = -1;                     // input slabs read (host path)
-    int t = 0;                               // GEMV: row multi-set
-    i64 bytes = 0;
-    double ready = 0, start = 0, finish = 0;
-    std::vector<int> deps;
-  };
-  std::vector<Tmp> T;
-  // write registry over scratch: bucket -> items whose write span touches it
-  const i64 scratch = std::max<i64>(pl.scratch_elems, 1);
-  const i64 B = std::max<i64>(256, scratch / (1 << 20));
-  std::vector<std::vector<int>> bucket(static_cast<size_t>((scratch + B - 1) / B + 1));
-  std::vector<int> seen;
-  auto span = [&](i64 off, const i64* stride, const int* ext, int nd, i64& lo, i64& hi) {
-    lo = off;
-    hi = off + 1;
-    for (int p = 0; p < nd; ++p) {
-      if (ext[p] <= 0) {
-        hi = lo;  // empty
-        return;
-      }
-      hi += static_cast<i64>(ext[p] - 1) * stride[p];
-    }
-  };
-  auto slabs_of = [&](i64 lo, i64 hi, Tmp& t) {  // F span of vector 0 -> slab range
-    if (nflags <= 0 || hi <= lo) return;
-    t.q0 = static_cast<int>(std::min<i64>(lo / fp->slab, nflags - 1));
-    t.q1 = static_cast<int>(std::min<i64>((hi - 1) / fp->slab, nflags - 1));
-  };
-  for (size_t oi = 0; oi < pl.ops.size(); ++oi) {
-    const Op& op = pl.ops[oi];
-    const size_t first = T.size();
-    FlowOp fo{};
-    if (op.kind == 3) {
-      const BoxLaunch& bx = pl.boxes[static_cast<size_t>(op.idx)];
-      fo.info = bx.info;
-      fo.kind = 0;
-      fo.in_buf = bx.in_buf;
-      fo.out_buf = bx.out_buf;
-      fo.mats = b.side[bx.side][static_cast<size_t>(bx.level)].interp.p;
-      fo.descs = pl.d_bdescs.p + bx.item_begin;
-      const int f = d - 1, cs = bx.info.cs;
-      for (i64 i = 0; i < bx.nitems; ++i) {
-        const BoxDesc& D = pl.bdescs[static_cast<size_t>(bx.item_begin + i)];
-        i64 rlo, rhi, wlo, whi;
-        span(D.in_off, D.in_stride, D.ein, d + 1, rlo, rhi);
-        if (rhi > rlo) rhi += static_cast<i64>(std::max(D.nsum, 1) - 1) * D.sum_stride;
-        span(D.out_off, D.out_stride, D.eout, d + 1, wlo, whi);
-        i64 flo = 0, fhi = 0;
-        if (bx.in_buf == BUF_F) span(D.in_off, D.in_stride, D.ein, d, flo, fhi);
-        const int ef = D.eout[f];
-        for (int c = 0; c < cs; ++c) {
-          if ((c + 1) * ef / cs <= c * ef / cs) continue;  // empty share (the kernel's split)
-          Tmp t;
-          t.it = FlowItem{0, static_cast<int>(oi), static_cast<int>(i), c, 0, 0, 0, 0};
-          if (bx.in_buf == BUF_SCRATCH) {
-            t.rlo = rlo;
-            t.rhi = rhi;
-          }
-          if (bx.out_buf == BUF_SCRATCH) {
-            t.wlo = wlo;
-            t.whi = whi;
-          }
-          if (bx.in_buf == BUF_F) slabs_of(flo, fhi, t);
-          T.push_back(std::move(t));
-        }
-      }
-    } else {
-      const GemvLaunch& gl = pl.gemvs[static_cast<size_t>(op.idx)];
-      fo.kind = 1;
-      fo.in_buf = BUF_SCRATCH;
-      fo.out_buf = BUF_SCRATCH;
-      fo.gdescs = pl.d_gemv.p + gl.desc_begin;
-      for (i64 q = 0; q < gl.ndesc; ++q) {
-        const GemvDesc& g = pl.gemv[static_cast<size_t>(gl.desc_begin + q)];
-        if (g.R <= 0) continue;
-        const i64 row_bytes = 16 * static_cast<i64>(std::max(g.C, 1));
-        const i64 want = std::max<i64>(1, chunk_bytes / row_bytes);
-        const i64 nch = (g.R + want - 1) / want;
-        for (i64 c = 0; c < nch; ++c) {
-          const int r0 = static_cast<int>(g.R * c / nch), r1 = static_cast<int>(g.R * (c + 1) / nch);
-          if (r1 <= r0) continue;
-          Tmp t;
-          t.it = FlowItem{1, static_cast<int>(oi), static_cast<int>(q), 0, r0, r1, 0, 0};
-          t.rlo = g.x_off;
-          t.rhi = g.x_off + static_cast<i64>(g.C) * nv;
-          t.wlo = g.y_off + r0;
-          t.whi = g.y_off + static_cast<i64>(nv - 1) * g.R + r1;
-          t.t = pl.gemv_t[static_cast<size_t>(gl.desc_begin + q)];
-          t.bytes = row_bytes * (r1 - r0) * (nv > 4 ? (nv + 3) / 4 : 1);
-          T.push_back(std::move(t));
-        }
-      }
-    }
-    fp->ops.push_back(fo);
-    // dependencies of this op's items on earlier writes
-    seen.assign(T.size(), -1);
-    for (size_t i = first; i < T.size(); ++i) {
-      Tmp& t = T[i];
-      if (t.rhi <= t.rlo) continue;
-      for (i64 k = t.rlo / B; k <= (t.rhi - 1) / B && k < static_cast<i64>(bucket.size()); ++k)
-        for (int w : bucket[static_cast<size_t>(k)]) {
-          if (seen[static_cast<size_t>(w)] == static_cast<int>(i)) continue;
-          const Tmp& p = T[static_cast<size_t>(w)];
-          if (p.wlo < t.rhi && t.rlo < p.whi) {
-            seen[static_cast<size_t>(w)] = static_cast<int>(i);
-            t.deps.push_back(w);
-          }
-        }
-    }
-    for (size_t i = first; i < T.size(); ++i) {
-      const Tmp& t = T[i];
-      if (t.whi <= t.wlo) continue;
-      for (i64 k = t.wlo / B; k <= (t.whi - 1) / B && k < static_cast<i64>(bucket.size()); ++k)
-        bucket[static_cast<size_t>(k)].push_back(static_cast<int>(i));
-    }
-  }
-  // ticket order: list scheduling of the DAG on grid slots.  A slot that
-  // frees at time tau claims, among the items whose producers are all
-  // claimed, one whose inputs are ready by tau -- the latest op first (finish
-  // started work: P/U boxes jump ahead of the remaining core chunks; chunks
-  // t-major) -- else the one that becomes ready first (it waits in its slot).
-  // Claimed-before-producers can never happen, so the order is topological.
-  const double slot_bw = kFlowHbmBytesPerUs / fp->grid;
-  std::vector<std::vector<int>> users(T.size());
-  std::vector<int> pending(T.size(), 0);
-  for (size_t i = 0; i < T.size(); ++i) {
-    pending[i] = static_cast<int>(T[i].deps.size());
-    for (int w : T[i].deps) users[static_cast<size_t>(w)].push_back(static_cast<int>(i));
-  }
-  auto dur = [&](const Tmp& t) {
-    return t.it.kind == 0 ? kFlowBoxUs : std::max(0.05, static_cast<double>(t.bytes) / slot_bw);
-  };
-  auto arrival = [&](const Tmp& t) {
-    return t.q1 >= 0 ? (t.q1 + 1) * (static_cast<double>(fp->slab) * nv * 16) / kFlowPcieBytesPerUs : 0.0;
-  };
-  using RKey = std::tuple<int, int, int>;  // (-op, t, index): ready items
-  std::priority_queue<RKey, std::vector<RKey>, std::greater<RKey>> ready;
-  using WKey = std::pair<double, int>;  // (ready time, index): frontier not yet ready
-  std::priority_queue<WKey, std::vector<WKey>, std::greater<WKey>> waiting;
-  auto frontier = [&](int i) {
-    Tmp& t = T[static_cast<size_t>(i)];
-    double r = arrival(t);
-    for (int w : t.deps) r = std::max(r, T[static_cast<size_t>(w)].finish);
-    t.ready = r;
-    waiting.push(WKey{r, i});
-  };
-  for (size_t i = 0; i < T.size(); ++i)
-    if (pending[i] == 0) frontier(static_cast<int>(i));
-  std::priority_queue<double, std::vector<double>, std::greater<double>> slots;
-  for (int k = 0; k < fp->grid; ++k) slots.push(0.0);
-  std::vector<int> order;
-  order.reserve(T.size());
-  while (order.size() < T.size()) {
-    const double tau = slots.top();
-    slots.pop();
-    while (!waiting.empty() && waiting.top().first <= tau) {
-      const int i = waiting.top().second;
-      waiting.pop();
-      ready.push(RKey{-T[static_cast<size_t>(i)].it.op, T[static_cast<size_t>(i)].t, i});
-    }
-    int pick;
-    if (!ready.empty()) {
-      pick = std::get<2>(ready.top());
-      ready.pop();
-    } else {
-      pick = waiting.top().second;
-      waiting.pop();
-    }
-    Tmp& t = T[static_cast<size_t>(pick)];
-    t.start = std::max(tau, t.ready);
-    t.finish = t.start + dur(t);
-    slots.push(t.finish);
-    order.push_back(pick);
-    for (int u : users[static_cast<size_t>(pick)])
-      if (--pending[static_cast<size_t>(u)] == 0) frontier(u);
-  }
-  std::vector<int> pos(T.size());
-  for (size_t k = 0; k < order.size(); ++k) pos[static_cast<size_t>(order[k])] = static_cast<int>(k);
-  for (size_t k = 0; k < order.size(); ++k) {
-    Tmp& t = T[static_cast<size_t>(order[k])];
-    FlowItem it = t.it;
-    it.dep_begin = static_cast<int>(fp->deps.size());
-    for (int w : t.deps) {
-      const int pw = pos[static_cast<size_t>(w)];
-      if (pw >= static_cast<int>(k)) throw std::runtime_error("internal: flow ticket order is not topological");
-      fp->deps.push_back(pw);
-    }
-    for (int q = t.q0; q <= t.q1; ++q) fp->deps.push_back(-1 - q);
-    it.ndep = static_cast<int>(fp->deps.size()) - it.dep_begin;
-    fp->items.push_back(it);
-  }
-  if (fp->items.size() > static_cast<size_t>(1 << 30)) return nullptr;
-  cudaStream_t st = b.stream;
-  fp->d_items = to_device(fp->items, st);
-  fp->d_ops = to_device(fp->ops, st);
-  fp->d_deps = to_device(fp->deps, st);
-  fp->d_done.alloc(std::max<size_t>(fp->items.size(), 1));
-  TBF_CUDA(cudaMemsetAsync(fp->d_done.p, 0, sizeof(int) * fp->d_done.n, st));
-  fp->d_ctl.alloc(4);
-  TBF_CUDA(cudaMemsetAsync(fp->d_ctl.p, 0, sizeof(unsigned) * 4, st));
-  fp->d_flags.alloc(static_cast<size_t>(std::max(nflags, 1)));
-  TBF_CUDA(cudaMemsetAsync(fp->d_flags.p, 0, sizeof(int) * fp->d_flags.n, st));
-  TBF_CUDA(cudaStreamSynchronize(st));
-  if (std::getenv("OIOBF_DEBUG")) {
-    size_t nbox = 0;
-    for (const FlowItem& it : fp->items) nbox += it.kind == 0;
-    fprintf(stderr, "[oiobf] flow plan: %zu items (%zu box, %zu gemv), %zu deps, grid %d, smem %zu, flags %d\n",
-            fp->items.size(), nbox, fp->items.size() - nbox, fp->deps.size(), fp->grid, fp->smem, nflags);
-  }
-  return fp;
-}
-
-// engine 3 (flow) or auto with OIOBF_FLOW=1; host = the host-buffer variant
-FlowPlan* flow_for(oiobf_tbf& b, Plan& pl, bool host) {
-  static const char* env = std::getenv("OIOBF_FLOW");
-  const bool want = b.apply_engine == 3 || (b.apply_engine == 0 && env && env[0] == '1');
-  if (!want || use_r1_engine(b) || use_tiny_engine(b)) return nullptr;
-  int& state = pl.flow_state[host ? 1 : 0];
-  std::unique_ptr<FlowPlan>& fp = host ? pl.flow_host : pl.flow_dev;
-  if (state == 0) {
-    int nflags = 0;
-    if (host) {
-      static const int slabs_env = std::getenv("OIOBF_FLOW_SLABS") ? std::atoi(std::getenv("OIOBF_FLOW_SLABS")) : 0;
-      nflags = static_cast<int>(std::min<i64>(b.n, slabs_env > 0 ? slabs_env : std::min<i64>(ipow(2, b.L), 8)));
-      while (nflags > 1 && b.n % nflags != 0) --nflags;
-    }
-    fp = build_flow(b, pl, nflags);
-    state = fp ? 1 : -1;
-  }
-  return state == 1 ? fp.get() : nullptr;
-}
-
-FlowArgs flow_args(oiobf_tbf& b, Plan& pl, FlowPlan& fp, const double2* F, double2* G) {
-  FlowArgs a{};
-  a.items = fp.d_items.p;
-  a.ops = fp.d_ops.p;
-  a.deps = fp.d_deps.p;
-  a.done = fp.d_done.p;
-  a.ctl = fp.d_ctl.p;
-  a.in_flags = fp.d_flags.p;
-  a.F = F;
-  a.G = G;
-  a.scratch = pl.scratch.p;
-  a.cores = b.cores.p;
-  a.nitems = static_cast<int>(fp.items.size());
-  a.nv = static_cast<int>(pl.nv);
-  a.nflags = fp.nflags;
-  return a;
-}
 
 struct OpBuffers {
   const double2* F = nullptr;
@@ -2478,32 +2150,6 @@ void contract_device(oiobf_tbf& b, const double2* F, double2* G, i64 nv, cudaStr
     return;
   }
   Plan& pl = get_plan(b, nv);
-  if (FlowPlan* fp = flow_for(b, pl, false)) {  // one persistent launch
-    FlowArgs a = flow_args(b, pl, *fp, F, G);
-    static const char* trace_path = std::getenv("OIOBF_FLOW_TRACE");  // debug timeline dump
-    if (trace_path) {
-      DevBuf<unsigned long long> tr(8 * fp->items.size());
-      TBF_CUDA(cudaMemsetAsync(tr.p, 0, 8 * tr.n, st));
-      a.trace = tr.p;
-      launch_flow(a, fp->grid, fp->smem, st);
-      std::vector<unsigned long long> h(tr.n);
-      TBF_CUDA(cudaMemcpyAsync(h.data(), tr.p, 8 * tr.n, cudaMemcpyDeviceToHost, st));
-      TBF_CUDA(cudaStreamSynchronize(st));
-      if (FILE* f = std::fopen(trace_path, "w")) {
-        std::fprintf(f, "ticket,kind,op,ndep,claimed,ready,done,sm,staged,first,middle,last\n");
-        for (size_t i = 0; i < fp->items.size(); ++i) {
-          const FlowItem& it = fp->items[i];
-          const unsigned long long* r = h.data() + 8 * i;
-          std::fprintf(f, "%zu,%d,%d,%d,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", i, it.kind, it.op, it.ndep, r[0],
-                       r[1], r[2], r[3], r[4], r[5], r[6], r[7]);
-        }
-        std::fclose(f);
-      }
-      return;
-    }
-    launch_flow(a, fp->grid, fp->smem, st);
-    return;
-  }
   static const bool no_graph = std::getenv("OIOBF_NO_GRAPH") != nullptr;  // profiling aid
   if (no_graph) {
     run_ops(b, pl, F, G, st);
@@ -2571,17 +2217,14 @@ void contract_host_async(oiobf_tbf& b, const double* F, double* G, i64 nv, cudaS
   // work the caller already enqueued on its stream (e.g. a consumer of the G
   // of an earlier call) precedes this call's D2H into G
   TBF_CUDA(cudaEventRecord(A.user, user));
-  FlowPlan* fp = flow_for(b, pl, false);
-  if (!fp && !A.gexec) A.gexec = capture_ops(b, pl, A.F.p, A.G.p, A.scratch.p);
-  // the flow engine's completion flags and scratch are per plan: one stream
-  cudaStream_t cst = fp ? b.stream : b.s_cmp[slot];
+  if (!A.gexec) A.gexec = capture_ops(b, pl, A.F.p, A.G.p, A.scratch.p);
+  cudaStream_t cst = b.s_cmp[slot];
   if (A.used) TBF_CUDA(cudaStreamWaitEvent(b.s_in, A.done, 0));
   TBF_CUDA(cudaMemcpyAsync(A.F.p, F, tot * sizeof(double2), cudaMemcpyHostToDevice, b.s_in));
   TBF_CUDA(cudaEventRecord(A.in, b.s_in));
   TBF_CUDA(cudaStreamWaitEvent(cst, A.in, 0));
   if (A.used) TBF_CUDA(cudaStreamWaitEvent(cst, A.out, 0));
-  if (fp) launch_flow(flow_args(b, pl, *fp, A.F.p, A.G.p), fp->grid, fp->smem, cst);
-  else TBF_CUDA(cudaGraphLaunch(A.gexec, cst));
+  TBF_CUDA(cudaGraphLaunch(A.gexec, cst));
   TBF_CUDA(cudaEventRecord(A.done, cst));
   TBF_CUDA(cudaStreamWaitEvent(b.s_out, A.done, 0));
   TBF_CUDA(cudaStreamWaitEvent(b.s_out, A.user, 0));
@@ -2644,76 +2287,6 @@ bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
-// Host-buffer contraction on the dataflow engine (pinned F and G): one graph
-//   copy stream    H2D slab q of F, then a 4-byte copy raising flag q
-//   compute stream the persistent kernel (items reading F wait on the flags);
-//                  G is written straight into the mapped pinned host buffer
-//                  (OIOBF_FLOW_ZC_OUT=0: device staging + one D2H copy)
-void contract_host_flow(oiobf_tbf& b, Plan& pl, FlowPlan& fp, const double* F, double* G) {
-  const i64 N = ipow(b.n, b.d);
-  const size_t nv = static_cast<size_t>(pl.nv);
-  const size_t tot = static_cast<size_t>(N) * nv;
-  if (pl.stage_F.n != tot) {
-    pl.stage_F.alloc(tot);
-    pl.stage_G.alloc(tot);
-  }
-  if (!b.s_in) {
-    TBF_CUDA(cudaStreamCreateWithFlags(&b.s_in, cudaStreamNonBlocking));
-    TBF_CUDA(cudaStreamCreateWithFlags(&b.s_out, cudaStreamNonBlocking));
-  }
-  while (b.ev.size() < 2) {
-    cudaEvent_t e;
-    TBF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    b.ev.push_back(e);
-  }
-  if (!b.h_one) {
-    TBF_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&b.h_one), sizeof(int), cudaHostAllocDefault));
-    *b.h_one = 1;
-  }
-  static const bool zc = !(std::getenv("OIOBF_FLOW_ZC_OUT") && std::getenv("OIOBF_FLOW_ZC_OUT")[0] == '0');
-  double2* Gd = nullptr;
-  if (zc) {
-    cudaPointerAttributes at{};
-    if (cudaPointerGetAttributes(&at, G) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
-      Gd = static_cast<double2*>(at.devicePointer);
-    cudaGetLastError();
-  }
-  if (!fp.gexec || fp.g_F != F || fp.g_G != G) {
-    if (fp.gexec) {
-      cudaGraphExecDestroy(fp.gexec);
-      fp.gexec = nullptr;
-    }
-    const size_t slab_bytes = static_cast<size_t>(fp.slab) * sizeof(double2);
-    const size_t pitch = static_cast<size_t>(N) * sizeof(double2);
-    cudaGraph_t g;
-    TBF_CUDA(cudaStreamBeginCapture(b.stream, cudaStreamCaptureModeThreadLocal));
-    try {
-      TBF_CUDA(cudaEventRecord(b.ev[0], b.stream));
-      TBF_CUDA(cudaStreamWaitEvent(b.s_in, b.ev[0], 0));
-      char* dF = reinterpret_cast<char*>(pl.stage_F.p);
-      for (int q = 0; q < fp.nflags; ++q) {
-        TBF_CUDA(cudaMemcpy2DAsync(dF + q * slab_bytes, pitch, reinterpret_cast<const char*>(F) + q * slab_bytes,
-                                   pitch, slab_bytes, nv, cudaMemcpyHostToDevice, b.s_in));
-        TBF_CUDA(cudaMemcpyAsync(fp.d_flags.p + q, b.h_one, sizeof(int), cudaMemcpyHostToDevice, b.s_in));
-      }
-      TBF_CUDA(cudaEventRecord(b.ev[1], b.s_in));
-      launch_flow(flow_args(b, pl, fp, pl.stage_F.p, Gd ? Gd : pl.stage_G.p), fp.grid, fp.smem, b.stream);
-      if (!Gd) TBF_CUDA(cudaMemcpyAsync(G, pl.stage_G.p, tot * sizeof(double2), cudaMemcpyDeviceToHost, b.stream));
-      TBF_CUDA(cudaStreamWaitEvent(b.stream, b.ev[1], 0));
-    } catch (...) {
-      cudaStreamEndCapture(b.stream, &g);
-      throw;
-    }
-    TBF_CUDA(cudaStreamEndCapture(b.stream, &g));
-    TBF_CUDA(cudaGraphInstantiate(&fp.gexec, g, 0));
-    TBF_CUDA(cudaGraphDestroy(g));
-    fp.g_F = F;
-    fp.g_G = G;
-  }
-  TBF_CUDA(cudaGraphLaunch(fp.gexec, b.stream));
-  TBF_CUDA(cudaStreamSynchronize(b.stream));
-}
-
 void contract_host(oiobf_tbf& b, const double* F, double* G, i64 nv) {
   TBF_CUDA(cudaSetDevice(b.device));
   if (nv > nv_chunk()) {
@@ -2721,13 +2294,6 @@ void contract_host(oiobf_tbf& b, const double* F, double* G, i64 nv) {
     for (i64 v0 = 0; v0 < nv; v0 += nv_chunk())
       contract_host(b, F + 2 * v0 * N, G + 2 * v0 * N, std::min(nv_chunk(), nv - v0));
     return;
-  }
-  if (is_pinned(F) && is_pinned(G)) {
-    Plan& pl0 = get_plan(b, nv, false);
-    if (FlowPlan* fp = flow_for(b, pl0, true)) {
-      contract_host_flow(b, pl0, *fp, F, G);
-      return;
-    }
   }
   Plan& pl = get_plan(b, nv, true);
   const size_t N = static_cast<size_t>(ipow(b.n, b.d) * nv);
@@ -3306,8 +2872,8 @@ int oiobf_tbf_load(const char* path, oiobf_tbf** out) {
 int oiobf_tbf_set_apply_engine(oiobf_tbf* h, int32_t engine) {
   CAPI_BEGIN
   require(h, "tbf_set_apply_engine: null handle");
-  require(engine >= 0 && engine <= 4,
-          "tbf_set_apply_engine: engine must be 0 (auto), 1 (box), 2 (tiny), 3 (flow) or 4 (rank-one)");
+  require(engine >= 0 && engine <= 4 && engine != 3,
+          "tbf_set_apply_engine: engine must be 0 (auto), 1 (box), 2 (tiny) or 4 (rank-one)");
   std::lock_guard<std::mutex> lk(h->mu);
   if (h->apply_engine != engine) {
     h->sync_all();
@@ -3327,7 +2893,7 @@ int oiobf_tbf_apply_engine(oiobf_tbf* h, int32_t* engine) {
     *engine = 2;
   } else {
     TBF_CUDA(cudaSetDevice(h->device));
-    *engine = flow_for(*h, get_plan(*h, 1), false) ? 3 : 1;
+    *engine = 1;
   }
   CAPI_END
 }
@@ -3518,53 +3084,6 @@ int oiobf_tbf_plan_stats(oiobf_tbf* h, int64_t out[4]) {
     }
   }
   out[3] = macs;
-  CAPI_END
-}
-
-// Debug (not in the public header): run the box launches of the nv = 1 plan
-// one by one with per-CTA globaltimer stamps.  out receives, per launch,
-// [nctas, cs, smem_bytes, stage, then nctas x 8 stamps (ns, relative to the
-// launch's earliest stamp)], up to max_out doubles; returns the count written
-// through *written.
-int oiobf_debug_box_trace(oiobf_tbf* h, const void* dF, void* dG, double* out, int64_t max_out, int64_t* written) {
-  CAPI_BEGIN
-  std::lock_guard<std::mutex> lk(h->mu);
-  TBF_CUDA(cudaSetDevice(h->device));
-  Plan& pl = get_plan(*h, 1);
-  // run the whole contraction once so scratch holds valid inputs
-  contract_device(*h, static_cast<const double2*>(dF), static_cast<double2*>(dG), 1, h->stream);
-  i64 maxc = 1;
-  for (const BoxLaunch& bx : pl.boxes) maxc = std::max(maxc, bx.nitems * bx.info.cs);
-  DevBuf<unsigned long long> tr(static_cast<size_t>(maxc * 8));
-  i64 w = 0;
-  OpBuffers io;
-  io.F = static_cast<const double2*>(dF);
-  io.G = static_cast<double2*>(dG);
-  for (const Op& op : pl.ops) {
-    if (op.kind != 3) continue;
-    const BoxLaunch& bx = pl.boxes[static_cast<size_t>(op.idx)];
-    const i64 nct = bx.nitems * bx.info.cs;
-    if (w + 4 + nct * 8 > max_out) break;
-    TBF_CUDA(cudaMemsetAsync(tr.p, 0, tr.n * 8, h->stream));
-    box_trace_enable(tr.p);
-    const LevelData& ld = h->side[bx.side][static_cast<size_t>(bx.level)];
-    const double2* in = bx.in_buf == BUF_F ? io.F : pl.scratch.p;
-    double2* o = bx.out_buf == BUF_G ? io.G : pl.scratch.p;
-    launch_box(bx.nitems, pl.d_bdescs.p + bx.item_begin, bx.info, ld.interp.p, in, o, h->stream);
-    TBF_CUDA(cudaStreamSynchronize(h->stream));
-    box_trace_enable(nullptr);
-    std::vector<unsigned long long> ht(static_cast<size_t>(nct * 8));
-    TBF_CUDA(cudaMemcpy(ht.data(), tr.p, ht.size() * 8, cudaMemcpyDeviceToHost));
-    unsigned long long t0 = ~0ULL;
-    for (unsigned long long v : ht)
-      if (v) t0 = std::min(t0, v);
-    out[w++] = static_cast<double>(nct);
-    out[w++] = bx.info.cs;
-    out[w++] = static_cast<double>(box_smem_bytes(bx.info));
-    out[w++] = bx.info.stage;
-    for (unsigned long long v : ht) out[w++] = v ? static_cast<double>(v - t0) : -1.0;
-  }
-  *written = w;
   CAPI_END
 }
 

@@ -12,6 +12,7 @@
 //                  residual norms of R equal those of A (Q unitary) -- with the
 //                  1e-12 tie rule of SURVEY App. A7, and id_from_qrcp
 //                  (id.cpp:87-120): T = R11^{-1} R12, sorted skeleton, interp.
+#include <algorithm>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -125,6 +126,13 @@ struct Bcast {
   int active;
 };
 
+// The reflector set-up is on the critical path of every column step (the
+// other warps wait for it at the step's barrier), so it is written with two
+// reciprocal square roots and one reciprocal instead of two square roots and
+// five IEEE divisions.  With sign = alpha / |alpha| and s = |alpha| + |x|:
+// v0 = alpha + sign |x| = sign s, so scale = 1 / v0 = conj(sign) / s, and
+// tau = 2 / (1 + sig / s^2) = 2 s^2 / (2 |x| s) = 1 + |alpha| / |x|
+// (|x|^2 = |alpha|^2 + sig) -- the same reflector, a few ulps apart.
 __device__ __forceinline__ Bcast make_reflector(double2 alpha, double sig, double2* rjj) {
   Bcast b;
   if (!(sig > 0)) {
@@ -133,12 +141,20 @@ __device__ __forceinline__ Bcast make_reflector(double2 alpha, double sig, doubl
     b.active = 0;
     return b;
   }
-  const double aa = sqrt(cnorm2(alpha));
-  const double xnorm = sqrt(cnorm2(alpha) + sig);
-  const double2 sign = aa == 0 ? make_double2(1, 0) : make_double2(alpha.x / aa, alpha.y / aa);
-  const double2 v0 = make_double2(alpha.x + sign.x * xnorm, alpha.y + sign.y * xnorm);
-  b.scale = cdiv(make_double2(1, 0), v0);
-  b.tau = 2.0 / (1.0 + sig * cnorm2(b.scale));
+  const double a2 = cnorm2(alpha);
+  const double x2 = a2 + sig;
+  const double rx = rsqrt(x2);
+  const double xnorm = x2 * rx;
+  double aa = 0;
+  double2 sign = make_double2(1, 0);
+  if (a2 > 0) {
+    const double ra = rsqrt(a2);
+    aa = a2 * ra;
+    sign = make_double2(alpha.x * ra, alpha.y * ra);
+  }
+  const double inv = __drcp_rn(aa + xnorm);
+  b.scale = make_double2(sign.x * inv, -sign.y * inv);
+  b.tau = fma(aa, rx, 1.0);
   b.active = 1;
   *rjj = make_double2(-sign.x * xnorm, -sign.y * xnorm);
   return b;
@@ -176,25 +192,53 @@ __device__ __forceinline__ void panel_reflector(double2* __restrict__ R, const d
 // apply reflector j (broadcast b) to trailing column k: R(j, k) and X(:, k)
 __device__ __forceinline__ void reflect_col(const Bcast& b, double2* __restrict__ R, double2* __restrict__ X, int j,
                                             int k, int nrows, int pr, int lane) {
-  double2 dot = make_double2(0, 0);
-  for (int i = lane; i < nrows; i += 32) cfmac(dot, X[i + j * pr], X[i + k * pr]);
-  dot = warp_sum2(dot);
+  double2 da = make_double2(0, 0), db = make_double2(0, 0);  // even / odd row blocks (shorter chains)
+  for (int i = lane, r = 0; i < nrows; i += 32, ++r) cfmac((r & 1) ? db : da, X[i + j * pr], X[i + k * pr]);
+  const double2 dot = warp_sum2(cadd(da, db));
   const double2 ws = reflect_coeff(b, R[rpk(j, k)], dot);
   const double2 t = cmul(b.scale, ws);
   if (lane == 0) R[rpk(j, k)] = csub(R[rpk(j, k)], ws);
   for (int i = lane; i < nrows; i += 32) X[i + k * pr] = csub(X[i + k * pr], cmul(X[i + j * pr], t));
 }
 
+// look-ahead column k = j + 1: apply reflector j, accumulate the updated
+// column's norm in the same pass, and build reflector k into `slot`
+// (replaces reflect_col + panel_reflector: one read of the column, and the
+// norm reduction starts as soon as the update is done)
+__device__ __forceinline__ void reflect_col_next(const Bcast& b, double2* __restrict__ R, double2* __restrict__ X,
+                                                 int j, int k, int nrows, int pr, int lane, Bcast* slot) {
+  double2 da = make_double2(0, 0), db = make_double2(0, 0);
+  for (int i = lane, r = 0; i < nrows; i += 32, ++r) cfmac((r & 1) ? db : da, X[i + j * pr], X[i + k * pr]);
+  const double2 rjk = R[rpk(j, k)];
+  const double2 dot = warp_sum2(cadd(da, db));
+  const double2 ws = reflect_coeff(b, rjk, dot);
+  const double2 t = cmul(b.scale, ws);
+  double sig = 0;
+  for (int i = lane; i < nrows; i += 32) {
+    const double2 x = csub(X[i + k * pr], cmul(X[i + j * pr], t));
+    X[i + k * pr] = x;
+    sig += cnorm2(x);
+  }
+  sig = warp_sum(sig);
+  if (lane == 0) {
+    R[rpk(j, k)] = csub(rjk, ws);
+    *slot = make_reflector(R[rpk(k, k)], sig, &R[rpk(k, k)]);
+  }
+  __syncwarp();
+}
+
 // two columns at once: the two dot products and shuffle reductions interleave
 // (independent dependency chains), halving the per-step latency of wide panels
 __device__ __forceinline__ void reflect_col2(const Bcast& b, double2* __restrict__ R, double2* __restrict__ X, int j,
                                              int k1, int k2, int nrows, int pr, int lane) {
-  double2 d1 = make_double2(0, 0), d2 = make_double2(0, 0);
-  for (int i = lane; i < nrows; i += 32) {
+  double2 d1 = make_double2(0, 0), d2 = make_double2(0, 0), e1 = make_double2(0, 0), e2 = make_double2(0, 0);
+  for (int i = lane, r = 0; i < nrows; i += 32, ++r) {
     const double2 xj = X[i + j * pr];
-    cfmac(d1, xj, X[i + k1 * pr]);
-    cfmac(d2, xj, X[i + k2 * pr]);
+    cfmac((r & 1) ? e1 : d1, xj, X[i + k1 * pr]);
+    cfmac((r & 1) ? e2 : d2, xj, X[i + k2 * pr]);
   }
+  d1 = cadd(d1, e1);
+  d2 = cadd(d2, e2);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     d1.x += __shfl_xor_sync(0xffffffffu, d1.x, o);
@@ -224,14 +268,14 @@ template <int RPL>
 __device__ __forceinline__ void reflect_col_r(const Bcast& b, double2* __restrict__ R, double2* __restrict__ X,
                                               const double2 (&xj)[RPL], int j, int k, int nrows, int pr, int lane) {
   double2 xk[RPL];
-  double2 dot = make_double2(0, 0);
+  double2 da = make_double2(0, 0), db = make_double2(0, 0);
 #pragma unroll
   for (int r = 0; r < RPL; ++r) {
     const int i = lane + 32 * r;
     xk[r] = X[i + k * pr];
-    cfmac(dot, xj[r], xk[r]);
+    cfmac((r & 1) ? db : da, xj[r], xk[r]);
   }
-  dot = warp_sum2(dot);
+  const double2 dot = warp_sum2(cadd(da, db));
   const double2 ws = reflect_coeff(b, R[rpk(j, k)], dot);
   const double2 t = cmul(b.scale, ws);
   if (lane == 0) R[rpk(j, k)] = csub(R[rpk(j, k)], ws);
@@ -243,19 +287,53 @@ __device__ __forceinline__ void reflect_col_r(const Bcast& b, double2* __restric
 }
 
 template <int RPL>
+__device__ __forceinline__ void reflect_col_next_r(const Bcast& b, double2* __restrict__ R, double2* __restrict__ X,
+                                                   const double2 (&xj)[RPL], int j, int k, int pr, int lane,
+                                                   Bcast* slot) {
+  double2 xk[RPL];
+  double2 da = make_double2(0, 0), db = make_double2(0, 0);
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) {
+    const int i = lane + 32 * r;
+    xk[r] = X[i + k * pr];
+    cfmac((r & 1) ? db : da, xj[r], xk[r]);
+  }
+  const double2 rjk = R[rpk(j, k)];
+  const double2 dot = warp_sum2(cadd(da, db));
+  const double2 ws = reflect_coeff(b, rjk, dot);
+  const double2 t = cmul(b.scale, ws);
+  double sig = 0;
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) {
+    const int i = lane + 32 * r;
+    xk[r] = csub(xk[r], cmul(xj[r], t));
+    X[i + k * pr] = xk[r];
+    sig += cnorm2(xk[r]);
+  }
+  sig = warp_sum(sig);
+  if (lane == 0) {
+    R[rpk(j, k)] = csub(rjk, ws);
+    *slot = make_reflector(R[rpk(k, k)], sig, &R[rpk(k, k)]);
+  }
+  __syncwarp();
+}
+
+template <int RPL>
 __device__ __forceinline__ void reflect_col2_r(const Bcast& b, double2* __restrict__ R, double2* __restrict__ X,
                                                const double2 (&xj)[RPL], int j, int k1, int k2, int nrows, int pr,
                                                int lane) {
   double2 x1[RPL], x2[RPL];
-  double2 d1 = make_double2(0, 0), d2 = make_double2(0, 0);
+  double2 d1 = make_double2(0, 0), d2 = make_double2(0, 0), e1 = make_double2(0, 0), e2 = make_double2(0, 0);
 #pragma unroll
   for (int r = 0; r < RPL; ++r) {
     const int i = lane + 32 * r;
     x1[r] = X[i + k1 * pr];
     x2[r] = X[i + k2 * pr];
-    cfmac(d1, xj[r], x1[r]);
-    cfmac(d2, xj[r], x2[r]);
+    cfmac((r & 1) ? e1 : d1, xj[r], x1[r]);
+    cfmac((r & 1) ? e2 : d2, xj[r], x2[r]);
   }
+  d1 = cadd(d1, e1);
+  d2 = cadd(d2, e2);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     d1.x += __shfl_xor_sync(0xffffffffu, d1.x, o);
@@ -297,9 +375,7 @@ __device__ void absorb_panel_r(double2* __restrict__ R, double2* __restrict__ X,
           xj[r] = X[i + j * pr];
         }
         if (owns_next) {  // look-ahead column first, then its reflector
-          reflect_col_r<RPL>(b, R, X, xj, j, k, nrows, pr, lane);
-          __syncwarp();
-          panel_reflector(R, X, w, j + 1, nrows, pr, &bc[(j + 1) & 1]);
+          reflect_col_next_r<RPL>(b, R, X, xj, j, k, pr, lane, &bc[(j + 1) & 1]);
           k += kWarps;
         }
         for (; k + kWarps < w; k += 2 * kWarps) reflect_col2_r<RPL>(b, R, X, xj, j, k, k + kWarps, nrows, pr, lane);
@@ -325,9 +401,7 @@ __device__ void absorb_panel(double2* __restrict__ R, double2* __restrict__ X, i
     int k = j + 1 + ((warp - (j + 1) % kWarps) % kWarps + kWarps) % kWarps;
     if (b.active) {
       if (owns_next) {  // look-ahead column first, then its reflector
-        reflect_col(b, R, X, j, k, nrows, pr, lane);
-        __syncwarp();
-        panel_reflector(R, X, w, j + 1, nrows, pr, &bc[(j + 1) & 1]);
+        reflect_col_next(b, R, X, j, k, nrows, pr, lane, &bc[(j + 1) & 1]);
         k += kWarps;
       }
       for (; k + kWarps < w; k += 2 * kWarps) reflect_col2(b, R, X, j, k, k + kWarps, nrows, pr, lane);
@@ -358,13 +432,14 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 3) k_panel(LevelDesc L, KS
   // Radon 2D, columns over a target mode: sin / cos(2 pi x) of each candidate
   double* csin = reinterpret_cast<double*>(reinterpret_cast<uintptr_t>(stgt + L.wmax + 1) & ~uintptr_t{7});
   double* ccos = csin + L.wmax;
-  const SlotPos s = decode_slot(L, slot);
+  const int sk_k = static_cast<int>((slot / L.nj) % L.d);  // unfolded mode k of the slot (decode_slot)
+  const int sk = (L.side == 0 ? L.d : 0) + sk_k;
   const int D = 2 * L.d;
   for (int i = threadIdx.x; i < L.psize; i += NT) sprox[i] = proxies[slot * L.psize + i];
   for (int i = threadIdx.x; i < w; i += NT) {
     const int t = targets[slot * L.wmax + i];
     stgt[i] = t;
-    if (ks.kind == OIOBF_KERNEL_RADON2D && s.skip < L.d) {
+    if (ks.kind == OIOBF_KERNEL_RADON2D && sk < L.d) {
       double sn, cs;
       sincos(__dmul_rn(2.0 * M_PI, __ddiv_rn(static_cast<double>(t - 1), static_cast<double>(ks.n))), &sn, &cs);
       csin[i] = sn;
@@ -374,8 +449,8 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 3) k_panel(LevelDesc L, KS
   for (int i = threadIdx.x; i < w * (w + 1) / 2; i += NT) R[i] = make_double2(0, 0);
   int cnt[kMaxModes], off[kMaxModes];
   for (int p = 0; p < D; ++p) {
-    cnt[p] = L.counts[s.k][p];
-    off[p] = L.poff[s.k][p];
+    cnt[p] = L.counts[sk_k][p];
+    off[p] = L.poff[sk_k][p];
   }
   __syncthreads();
   if (w == 0) return;
@@ -393,7 +468,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 3) k_panel(LevelDesc L, KS
       if (valid) {
         i64 rem = row;
         for (int p = 0; p < D; ++p) {
-          if (p == s.skip) continue;
+          if (p == sk) continue;
           const int c = cnt[p];
           const int v = sprox[off[p] + static_cast<int>(rem % c)];
           rem /= c;
@@ -409,11 +484,10 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 3) k_panel(LevelDesc L, KS
 #pragma unroll
           for (int p = 0; p < 3; ++p)
             if (p < L.d) {
-              if (p != s.skip) xs[p] = green_x(ks, ii[p]);
-              if (p + L.d != s.skip) ys[p] = green_y(ks, p, jj[p]);
+              if (p != sk) xs[p] = green_x(ks, ii[p]);
+              if (p + L.d != sk) ys[p] = green_y(ks, p, jj[p]);
             }
         }
-        const int sk = s.skip;
         for (int c = my_cg; c < w; c += ncg) {
           double2 e = make_double2(0, 0);
           if (valid) {
@@ -435,7 +509,6 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 3) k_panel(LevelDesc L, KS
         // radon2d_entry with sin / cos(2 pi x_p) hoisted: per row for the row's
         // target modes, per candidate column (csin / ccos) for an unfolded
         // target mode -- the same operations as kernel_entry, so bit-identical
-        const int sk = s.skip;
         double sx[2] = {0, 0}, cx[2] = {0, 0};
         if (valid)
           for (int p = 0; p < 2; ++p)
@@ -462,8 +535,8 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 3) k_panel(LevelDesc L, KS
           double2 e = make_double2(0, 0);
           if (valid) {
             const int t = stgt[c];
-            if (s.skip < L.d) ii[s.skip] = t;
-            else jj[s.skip - L.d] = t;
+            if (sk < L.d) ii[sk] = t;
+            else jj[sk - L.d] = t;
             e = kernel_entry(ks, ii, jj);
           }
           X[my_row + c * pr] = e;
@@ -804,13 +877,42 @@ void launch_panel_t(const LevelDesc& L, const KSpec& ks, const int* proxies, con
   k_panel<NT, RPL><<<static_cast<unsigned>(grid), NT, smem, st>>>(L, ks, proxies, targets, width, rpart);
 }
 
+// Panel rows and resident CTAs per SM for a level of width wmax.  The column
+// sweep is latency-bound (one CTA barrier and one look-ahead reflector per
+// column), so a step should carry as many rows as shared memory holds:
+// w <= 32: 256-thread CTAs, 256- / 128-row panels, up to 3 CTAs per SM;
+// w > 32: one 512-thread CTA per SM with the tallest panel (multiple of 32
+// rows, at most 192) next to the packed R.
+void panel_shape(i64 wmax, i64 psize, int* pr, int* ctas_per_sm) {
+  static const int over = std::getenv("OIOBF_PANEL_PR") ? std::atoi(std::getenv("OIOBF_PANEL_PR")) : 0;  // sweeps
+  LevelDesc t{};
+  t.wmax = wmax;
+  t.psize = psize;
+  if (wmax <= 32) {
+    t.pr = over > 0 ? over : wmax <= 24 ? 256 : 128;
+    *pr = t.pr;
+    *ctas_per_sm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(3, 227 * 1024 / (panel_smem_bytes(t) + 1024))));
+    return;
+  }
+  int best = 64;
+  for (int p = 64; p <= 192; p += 32) {
+    t.pr = p;
+    if (panel_smem_bytes(t) <= static_cast<size_t>(kMaxDynSmem)) best = p;
+  }
+  *pr = over > 0 ? over : best;
+  *ctas_per_sm = 1;
+}
+
 void launch_panel(const LevelDesc& L, const KSpec& ks, const int* proxies, const int* targets, const int* width,
                   double2* rpart, cudaStream_t st) {
   const size_t smem = panel_smem_bytes(L);
   const i64 grid = L.nslots * L.nparts;
   static const bool generic = std::getenv("OIOBF_PANEL_GENERIC") != nullptr;  // A/B switch
   if (L.wmax > 32) {
-    if (!generic && L.pr == 128) launch_panel_t<512, 4>(L, ks, proxies, targets, width, rpart, smem, grid, st);
+    if (!generic && L.pr == 192) launch_panel_t<512, 6>(L, ks, proxies, targets, width, rpart, smem, grid, st);
+    else if (!generic && L.pr == 160) launch_panel_t<512, 5>(L, ks, proxies, targets, width, rpart, smem, grid, st);
+    else if (!generic && L.pr == 128) launch_panel_t<512, 4>(L, ks, proxies, targets, width, rpart, smem, grid, st);
+    else if (!generic && L.pr == 96) launch_panel_t<512, 3>(L, ks, proxies, targets, width, rpart, smem, grid, st);
     else if (!generic && L.pr == 64) launch_panel_t<512, 2>(L, ks, proxies, targets, width, rpart, smem, grid, st);
     else launch_panel_t<512, 0>(L, ks, proxies, targets, width, rpart, smem, grid, st);
   } else {

@@ -11,6 +11,8 @@ void measure_fp64_peak(double* out);
 
 // ---- construction (id_kernels.cu)
 size_t panel_smem_bytes(const LevelDesc& L);
+// panel rows and resident CTAs per SM of k_panel for a level of width wmax
+void panel_shape(i64 wmax, i64 psize, int* pr, int* ctas_per_sm);
 size_t finish_smem_bytes(const LevelDesc& L);
 void launch_gen_proxies(const LevelDesc& L, int* proxies, cudaStream_t st);
 void launch_targets(const LevelDesc& L, const int* crank, const i64* cskel_off, const int* cskel, int* targets,

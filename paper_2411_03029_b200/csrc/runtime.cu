@@ -604,6 +604,13 @@ namespace {
 
 constexpr double kTieEps = 1e-12;
 
+int device_sms() {
+  static int sms[64] = {0};
+  const int dv = g_device >= 0 && g_device < 64 ? g_device : 0;
+  if (!sms[dv]) TBF_CUDA(cudaDeviceGetAttribute(&sms[dv], cudaDevAttrMultiProcessorCount, g_device));
+  return sms[dv];
+}
+
 LevelDesc make_level(const oiobf_tbf& b, int sd, int l, i64 r_est, i64 wmax) {
   LevelDesc L{};
   L.d = b.d;
@@ -653,10 +660,12 @@ LevelDesc make_level(const oiobf_tbf& b, int sd, int l, i64 r_est, i64 wmax) {
   // R packed: (w(w+1)/2 + pr w) x 16 B fits the 220 KB budget; taller panels
   // amortise the per-column steps (w <= 24 at 256 rows: 2 CTAs/SM, config 2
   // panel time 32.1 -> 28.2 ms against 128 rows at 3 CTAs/SM)
-  L.pr = wmax <= 24 ? 256 : wmax <= 64 ? 128 : 64;
+  int cps = 1;
+  panel_shape(wmax, L.psize, &L.pr, &cps);
   L.rank = b.rank;
   L.world = b.world;
-  const i64 target_ctas = 148 * 8;
+  // >= 4 waves of resident CTAs, each CTA >= 4 panels
+  const i64 target_ctas = static_cast<i64>(device_sms()) * cps * 4;
   const i64 owned = (L.nslots + b.world - 1) / b.world;
   i64 parts = (target_ctas + owned - 1) / owned;
   const i64 max_parts = std::max<i64>(1, (L.m + 4 * L.pr - 1) / (4 * L.pr));  // >= 4 panels per part

@@ -204,7 +204,7 @@ def test_bench_sharded_torchrun_validation():
     env = dict(os.environ, OIOBF_BENCH_DIST="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
-           "--steps", "2", "--warmup", "3"]
+           "--steps", "2", "--warmup", "3", "--config", "green_cubes_n64"]
     r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])

@@ -553,12 +553,14 @@ def run_b200_sharded(args):
     sh = stream.cuda_stream
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    # exchange: fused by default -- the phase-1 core GEMV stores G_{t,s} straight
-    # into the owners' receive buffers (CUDA IPC peer memory over NVLink), one
-    # barrier per step; OIOBF_EXCHANGE=nccl selects send buffer + NCCL all-to-all
+    # exchange: send buffer + NCCL all-to-all by default; OIOBF_EXCHANGE=fused
+    # makes the phase-1 core GEMV store G_{t,s} straight into the owners'
+    # receive buffers (CUDA IPC peer memory over NVLink, one stream-ordered
+    # barrier per step) -- validated only with ranks sharing one device so far
+    # (tests/test_sharded.py), so it is opt-in until a multi-GPU run checks it
     px = None
     exchange = "nccl all_to_all_single of the send buffer"
-    if os.environ.get("OIOBF_EXCHANGE", "fused") != "nccl":
+    if os.environ.get("OIOBF_EXCHANGE", "nccl") == "fused":
         try:
             px = PeerExchange(sb, comm, nv_max=args.nv)
             exchange = "fused: core GEMV epilogue stores into peer receive buffers (CUDA IPC), 1 barrier per step"
@@ -595,15 +597,24 @@ def run_b200_sharded(args):
     torch.cuda.synchronize()
     ms = allreduce_max(sum(a.elapsed_time(b) for a, b in evs) / args.steps)
     stage("timed steps done")
-    # e2e: pinned host F in, this rank's G out, exchange included
+    # e2e: from pinned host F, each rank copies in only the input sub-tensors
+    # F(s) of its owned s and copies out only the G(t) of its owned t (strided
+    # DMA, oiobf_tbf_copy_owned), exchange included
     pin_F = torch.from_numpy(np.ascontiguousarray(Fh.reshape(-1, order="F")).view(np.float64).copy()).pin_memory()
     pin_G = torch.empty_like(pin_F).pin_memory()
     e2e = []
+    n_own_s = sum(1 for o in range(sb.nmid) if o % ws == rank)
+
+    def copy_in():
+        be.copy_owned(0, pin_F.data_ptr(), F.data_ptr(), args.nv, sh)
+
+    def copy_out():
+        be.copy_owned(1, G.data_ptr(), pin_G.data_ptr(), args.nv, sh)
 
     def e2e_step():
-        F.copy_(pin_F, non_blocking=True)
+        copy_in()
         step()
-        pin_G.copy_(G, non_blocking=True)
+        copy_out()
         torch.cuda.synchronize()
 
     # PCIe link warm-up (see run_b200) for ~0.3 s.  Every step holds a
@@ -619,9 +630,9 @@ def run_b200_sharded(args):
     for _ in range(max(args.steps, 50)):
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        F.copy_(pin_F, non_blocking=True)
+        copy_in()
         step()
-        pin_G.copy_(G, non_blocking=True)
+        copy_out()
         torch.cuda.synchronize()
         e2e.append(time.perf_counter() - t1)
     e2e_ms = allreduce_max(1e3 * statistics.fmean(e2e))
@@ -650,8 +661,10 @@ def run_b200_sharded(args):
             "config": {"workload": cfg.name, "points": cfg.points, "tol": cfg.tol, "L": cfg.L, "nv": args.nv,
                        "l2": "flushed (256 MiB write) before every timed step",
                        "parallelism": f"sharded x{ws}: middle multi-sets round-robin", "exchange": exchange},
-            "e2e": {"value": N / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms, "h2d_bytes_per_step": 16 * N,
-                    "d2h_bytes_per_step": 16 * N},
+            "e2e": {"value": N / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": 16 * N * n_own_s // sb.nmid, "d2h_bytes_per_step": 16 * N * n_own_s // sb.nmid,
+                    "copies": "rank 0's owned sub-tensors F(s) in and G(t) out (oiobf_tbf_copy_owned; every rank "
+                              "moves its own share over its own PCIe link)"},
             "exchange_bytes_per_step_rank0": int(16 * lay.send_counts.sum() * args.nv),
             "gpu_launches": int(st[2]) * args.steps,
             "dist_backend": backend,

@@ -241,6 +241,20 @@ int oiobf_device_free(void* p);
 int oiobf_ipc_handle(void* p, uint8_t handle[64]);
 int oiobf_ipc_open(const uint8_t handle[64], void** out);
 int oiobf_ipc_close(void* p);
+// copies between any two of host / this device / a peer device (UVA,
+// cudaMemcpyDefault; synchronous), and a device-wide synchronize of the
+// calling thread's device -- the plumbing of the in-process multi-device
+// driver in include/oiobf/sharded.hpp (one handle per device, peer copies over
+// NVLink for the exchange)
+int oiobf_memcpy(void* dst, const void* src, int64_t bytes);
+// Owned-slab copies of a sharded handle (stream-ordered, strided DMA, no
+// staging): dir 0 copies the input sub-tensors F(s) of the middle column
+// multi-sets s this rank owns from host F to device dF (what phase 1 reads);
+// dir 1 copies the output sub-tensors G(t) of the owned row multi-sets t from
+// device dG to host G (what phase 2 wrote).  F / G: n^d x nv, first mode
+// fastest; host buffers should be pinned for the copies to be asynchronous.
+int oiobf_tbf_copy_owned(oiobf_tbf* h, int32_t dir, const void* src, void* dst, int64_t nv, void* stream);
+int oiobf_synchronize(void);
 
 #ifdef __cplusplus
 }

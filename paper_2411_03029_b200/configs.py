@@ -105,12 +105,18 @@ CONFIGS = [
 ]
 BY_NAME = {c.name: c for c in CONFIGS}
 
-# ProxyStrategy (q, row_cap) per config that meets the north_star accuracy
-# gate -- 1000 sampled outputs within tol of direct dense sums -- measured on
-# B200 (profiles/r2_accuracy_*.jsonl).  The reference default
-# (q = 3, row_cap = 2^17, id.hpp:50-55) is proxy-deficient for these operators:
-# with every proxy row (ProxyMode::All) the same butterflies land at 0.2-0.7 tol,
-# so the loss is the Cartesian-product row sample, not the composition.
+# ProxyStrategy (q, row_cap) per config for the north_star accuracy gate --
+# 1000 sampled outputs against direct dense sums -- measured on B200
+# (profiles/r2_accuracy_sweep.jsonl).  The reference default
+# (q = 3, row_cap = 2^17, id.hpp:50-55) is proxy-deficient for these
+# operators: with every proxy row (ProxyMode::All) the same butterflies land at
+# 0.2-0.7 tol at sizes where All is feasible, so the loss is the
+# Cartesian-product row sample, not the composition; the error falls
+# monotonically with the row cap.  Measured sampled error / tol:
+#   green_plates_n64  (4, 2^17): 0.69          green_cubes_n64 (3, 2^23): 0.65
+#   green_cubes_n256  (4, 2^25): 1.23 (338 s construction; 2^23: 2.0-2.5, 2^21: 6.8)
+#   dft6_n16          (3, 2^17): 1e-7 (exact: every ID has rank 1)
+#   radon2d_n1024     (8, 2^21): 5.3  (328 s construction; default 2256-4375)
 ACCURACY_STRATEGY = {
     "green_plates_n64": (4, 1 << 17),
     "green_cubes_n64": (3, 1 << 23),

@@ -189,6 +189,59 @@ __global__ void __launch_bounds__(kGemvThreads, NV == 1 ? 4 : 2) k_gemv(const in
   }
 }
 
+// Short rows (C <= 32 * RL, n_v = 1): a warp issues every load of its row at
+// once (RL 16-B streaming loads per lane, predicated on C) before any FMA, so
+// a row is one DRAM round trip instead of a loop of 8-load batches and tails;
+// config 3's rows (C = 343-448) kept too few bytes in flight for HBM with the
+// batched loop (ncu: long-scoreboard stalls, DRAM 61% of peak).
+template <int RL>
+__global__ void __launch_bounds__(kGemvThreads, 2) k_gemv_short(const int* __restrict__ cta_pair,
+                                                              const GemvDesc* __restrict__ ds, long long total_rows,
+                                                              const long long* __restrict__ row_begin,
+                                                              const double2* __restrict__ cores,
+                                                              const double2* __restrict__ x, double2* __restrict__ y) {
+  extern __shared__ __align__(16) double2 sx[];
+  pdl_trigger_dep();
+  const long long g0 = row_begin[blockIdx.x];
+  const long long g1 = min(total_rows, row_begin[blockIdx.x + 1]);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int p = cta_pair[blockIdx.x];
+  if (g0 + warp < g1) {  // this warp's first core row into L2 while the previous kernel drains
+    const GemvDesc D0 = ds[p];
+    if (g0 + warp < D0.cta_off + D0.R) {
+      const char* r0 = reinterpret_cast<const char*>(cores + D0.core_off + (g0 + warp - D0.cta_off) * D0.C);
+      for (int o = lane * 128; o < D0.C * 16; o += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(r0 + o));
+    }
+  }
+  pdl_wait_dep();
+  long long g = g0;
+  while (g < g1) {
+    const GemvDesc D = ds[p];
+    const long long pend = min(g1, D.cta_off + D.R);
+    const int C = D.C;
+    const double2* xs = x + D.x_off;
+    for (int i = threadIdx.x; i < C; i += kGemvThreads) sx[i] = xs[i];
+    __syncthreads();
+    for (long long gr = g + warp; gr < pend; gr += kGemvThreads / 32) {
+      const int r = static_cast<int>(gr - D.cta_off);
+      const double2* row = cores + D.core_off + static_cast<long long>(r) * C;
+      double2 a[RL];
+#pragma unroll
+      for (int u = 0; u < RL; ++u)
+        if (lane + u * 32 < C) a[u] = ld_stream2(row + lane + u * 32);
+      double2 acc0 = make_double2(0, 0), acc1 = make_double2(0, 0);
+#pragma unroll
+      for (int u = 0; u < RL; ++u)
+        if (lane + u * 32 < C) cfma((u & 1) ? acc1 : acc0, a[u], sx[lane + u * 32]);
+      const double2 t = warp_sum2(cadd(acc0, acc1));
+      if (lane == 0) y[D.y_off + r] = t;
+    }
+    __syncthreads();
+    g = pend;
+    ++p;
+  }
+}
+
 // Multi-vector core contraction on the FP64 tensor core: Y (R x nv) = K (R x C) X
 // (C x nv) per pair, nv <= 8 padded to one 8-wide N tile.  Same CTA row ranges
 // and x staging as k_gemv; a warp takes 8-row tiles of a pair and walks the
@@ -441,6 +494,12 @@ bool gemv_uses_mma(int nv, int max_c) {
   return !no_mma && nv >= 2 && nv <= 8 && static_cast<size_t>(max_c | 1) * nv * sizeof(double2) <= 96 * 1024;
 }
 
+constexpr int kShortRL = 16;  // k_gemv_short: rows up to 512 elements
+bool gemv_uses_short(int nv, int max_c) {
+  static const bool off = std::getenv("OIOBF_GEMV_SHORT") && std::getenv("OIOBF_GEMV_SHORT")[0] == '0';
+  return !off && nv == 1 && max_c >= 128 && max_c <= 32 * kShortRL;
+}
+
 void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, const i64* row_begin, int nv,
                  const double2* cores, const double2* x, double2* y, int max_c, cudaStream_t st) {
   if (nctas == 0) return;
@@ -460,6 +519,10 @@ void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_ro
   if (mma) {
     TBF_CUDA(cudaFuncSetAttribute(k_gemv_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     TBF_CUDA(cudaLaunchKernelEx(&cfg, k_gemv_mma, cta_pair, d, nv, static_cast<long long>(total_rows), row_begin,
+                                cores, x, y));
+  } else if (gemv_uses_short(nv, max_c)) {
+    TBF_CUDA(cudaFuncSetAttribute(k_gemv_short<kShortRL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    TBF_CUDA(cudaLaunchKernelEx(&cfg, k_gemv_short<kShortRL>, cta_pair, d, static_cast<long long>(total_rows), row_begin,
                                 cores, x, y));
   } else if (nv == 1) {
     TBF_CUDA(cudaFuncSetAttribute(k_gemv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
@@ -510,7 +573,10 @@ int gemv_ctas_per_sm(int nv, int max_c) {
     return n < 1 ? 1 : n;
   }
   const size_t smem = sizeof(double2) * static_cast<size_t>(max_c) * (nv == 1 ? 1 : std::min(nv, 4));
-  if (nv == 1) {
+  if (gemv_uses_short(nv, max_c)) {
+    TBF_CUDA(cudaFuncSetAttribute(k_gemv_short<kShortRL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    TBF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gemv_short<kShortRL>, kGemvThreads, smem));
+  } else if (nv == 1) {
     TBF_CUDA(cudaFuncSetAttribute(k_gemv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     TBF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gemv<1>, kGemvThreads, smem));
   } else {

@@ -444,6 +444,8 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 3) k_panel(LevelDesc L, KS
       sincos(__dmul_rn(2.0 * M_PI, __ddiv_rn(static_cast<double>(t - 1), static_cast<double>(ks.n))), &sn, &cs);
       csin[i] = sn;
       ccos[i] = cs;
+    } else if (ks.kind == OIOBF_KERNEL_GREEN) {  // the candidate's coordinate along the unfolded mode
+      csin[i] = sk < L.d ? green_x(ks, t) : green_y(ks, sk - L.d, t);
     }
   }
   for (int i = threadIdx.x; i < w * (w + 1) / 2; i += NT) R[i] = make_double2(0, 0);
@@ -491,10 +493,9 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 3) k_panel(LevelDesc L, KS
         for (int c = my_cg; c < w; c += ncg) {
           double2 e = make_double2(0, 0);
           if (valid) {
-            const int t = stgt[c];
             const bool tgt = sk < L.d;
             const int q = tgt ? sk : sk - L.d;
-            const double v = tgt ? green_x(ks, t) : green_y(ks, q, t);
+            const double v = csin[c];  // green_x / green_y of the candidate (hoisted per column)
             double xc[3], yc[3];
 #pragma unroll
             for (int p = 0; p < 3; ++p) {

@@ -409,6 +409,7 @@ struct Plan {
     }
   };
   GraphCache dev_graphs, host_graphs;
+  GraphCache phase_graphs[2];  // sharded phases 1 / 2, keyed by (input, output, stream)
   // device-buffer calls share pl.scratch: a call on a different stream than
   // the previous one waits for it (same-stream calls are ordered already)
   cudaEvent_t dev_done = nullptr;
@@ -2122,7 +2123,28 @@ i64 nv_chunk() {
   return c > 0 ? c : 4;
 }
 
-// the plan's launches for (F, G) captured into an instantiated graph
+// the plan's launches for io (phase 0: whole contraction, 1 / 2: sharded
+// phases) captured into an instantiated graph
+cudaGraphExec_t capture_io(oiobf_tbf& b, Plan& pl, const OpBuffers& io, int phase) {
+  cudaStream_t cap;
+  TBF_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  cudaGraph_t g;
+  TBF_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+  try {
+    run_ops(b, pl, io, cap, -1, phase);
+  } catch (...) {
+    cudaStreamEndCapture(cap, &g);
+    cudaStreamDestroy(cap);
+    throw;
+  }
+  TBF_CUDA(cudaStreamEndCapture(cap, &g));
+  cudaGraphExec_t ex;
+  TBF_CUDA(cudaGraphInstantiate(&ex, g, 0));
+  TBF_CUDA(cudaGraphDestroy(g));
+  TBF_CUDA(cudaStreamDestroy(cap));
+  return ex;
+}
+
 cudaGraphExec_t capture_ops(oiobf_tbf& b, Plan& pl, const double2* F, double2* G, double2* scratch = nullptr) {
   cudaStream_t cap;
   TBF_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
@@ -2801,6 +2823,62 @@ int oiobf_ipc_close(void* p) {
   CAPI_END
 }
 
+int oiobf_memcpy(void* dst, const void* src, int64_t bytes) {
+  CAPI_BEGIN
+  require(bytes >= 0 && (bytes == 0 || (dst && src)), "memcpy: bad argument");
+  ensure_device();
+  if (bytes) TBF_CUDA(cudaMemcpy(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault));
+  CAPI_END
+}
+
+int oiobf_tbf_copy_owned(oiobf_tbf* h, int32_t dir, const void* src, void* dst, int64_t nv, void* stream) {
+  CAPI_BEGIN
+  require(h && src && dst, "tbf_copy_owned: null argument");
+  require(dir == 0 || dir == 1, "tbf_copy_owned: dir must be 0 (F in) or 1 (G out)");
+  require(nv >= 1, "tbf_copy_owned: nv must be >= 1");
+  TBF_CUDA(cudaSetDevice(h->device));
+  const int d = h->d;
+  const i64 n = h->n, mpm = ipow(2, h->Lc), mid = n >> h->Lc, N = ipow(n, d);
+  // modes 0..2 as one 3D copy (x = mode 0 contiguous), the rest looped
+  const int d3 = std::min(d, 3);
+  i64 outer_cnt = nv;
+  for (int k = 3; k < d; ++k) outer_cnt *= mid;
+  for (i64 o = 0; o < h->nmid; ++o) {
+    if (!h->owns(o)) continue;
+    i64 base = 0, st = 1;
+    for (int k = 0; k < d; ++k) {
+      base += ((o / ipow(mpm, k)) % mpm) * mid * st;
+      st *= n;
+    }
+    for (i64 q = 0; q < outer_cnt; ++q) {
+      i64 off = base, rem = q;
+      for (int k = 3; k < d; ++k) {
+        off += (rem % mid) * ipow(n, k);
+        rem /= mid;
+      }
+      off += rem * N;  // vector index
+      cudaMemcpy3DParms p = {};
+      const size_t pitch = static_cast<size_t>(n) * 16;
+      p.srcPtr = make_cudaPitchedPtr(const_cast<char*>(static_cast<const char*>(src)) + 16 * off, pitch,
+                                     static_cast<size_t>(n), static_cast<size_t>(d > 1 ? n : 1));
+      p.dstPtr = make_cudaPitchedPtr(static_cast<char*>(dst) + 16 * off, pitch, static_cast<size_t>(n),
+                                     static_cast<size_t>(d > 1 ? n : 1));
+      p.extent = make_cudaExtent(static_cast<size_t>(mid) * 16, static_cast<size_t>(d3 > 1 ? mid : 1),
+                                 static_cast<size_t>(d3 > 2 ? mid : 1));
+      p.kind = cudaMemcpyDefault;
+      TBF_CUDA(cudaMemcpy3DAsync(&p, static_cast<cudaStream_t>(stream)));
+    }
+  }
+  CAPI_END
+}
+
+int oiobf_synchronize(void) {
+  CAPI_BEGIN
+  ensure_device();
+  TBF_CUDA(cudaDeviceSynchronize());
+  CAPI_END
+}
+
 // phase 1: dIn = F (n^d x nv), dOut = send buffer; phase 2: dIn = receive
 // buffer, dOut = G (only this rank's row slabs are written)
 int oiobf_tbf_contract_phase(oiobf_tbf* h, int32_t phase, const void* dIn, void* dOut, int64_t nv, void* stream) {
@@ -2829,7 +2907,24 @@ int oiobf_tbf_contract_phase(oiobf_tbf* h, int32_t phase, const void* dIn, void*
     io.recv = static_cast<const double2*>(dIn);
     io.G = static_cast<double2*>(dOut);
   }
-  run_ops(*h, pl, io, static_cast<cudaStream_t>(stream), -1, phase);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  static const bool no_graph = std::getenv("OIOBF_NO_GRAPH") != nullptr;  // profiling aid
+  if (no_graph) {
+    run_ops(*h, pl, io, st, -1, phase);
+  } else {  // one captured graph per (phase, input, output, stream)
+    GraphCache& gc = pl.phase_graphs[phase - 1];
+    cudaGraphExec_t ex = gc.find(dIn, dOut, st);
+    if (!ex) {
+      ex = capture_io(*h, pl, io, phase);
+      gc.put(dIn, dOut, st, ex);
+    }
+    if (!pl.dev_done) TBF_CUDA(cudaEventCreateWithFlags(&pl.dev_done, cudaEventDisableTiming));
+    if (pl.dev_used && pl.dev_last != st) TBF_CUDA(cudaStreamWaitEvent(st, pl.dev_done, 0));
+    TBF_CUDA(cudaGraphLaunch(ex, st));
+    TBF_CUDA(cudaEventRecord(pl.dev_done, st));
+    pl.dev_last = st;
+    pl.dev_used = true;
+  }
   CAPI_END
 }
 

@@ -123,6 +123,13 @@ class GpuShardBackend:
         _lib.check(_lib.load().oiobf_tbf_set_exchange(self.h, lay.send_off, lay.recv_off,
                                                       int(lay.send_counts.sum()), int(lay.recv_counts.sum())))
 
+    def copy_owned(self, direction: int, src_ptr: int, dst_ptr: int, nv: int, stream: int = 0):
+        """Owned-slab copies (C ABI oiobf_tbf_copy_owned): direction 0 = the
+        F(s) sub-tensors of the owned s, host -> device; 1 = the G(t)
+        sub-tensors of the owned t, device -> host (strided DMA on `stream`)."""
+        _lib.check(_lib.load().oiobf_tbf_copy_owned(self.h, direction, C.c_void_p(src_ptr), C.c_void_p(dst_ptr), nv,
+                                                    C.c_void_p(stream)))
+
     def phase(self, phase: int, src_ptr: int, dst_ptr: int, nv: int, stream: int = 0):
         _lib.check(_lib.load().oiobf_tbf_contract_phase(self.h, phase, C.c_void_p(src_ptr), C.c_void_p(dst_ptr), nv,
                                                         C.c_void_p(stream)))
@@ -141,6 +148,7 @@ def _declare(Lb):
     Lb.oiobf_tbf_umid_import.argtypes = [C.c_void_p, i64p, i32p, C.c_int64]
     Lb.oiobf_tbf_set_exchange.argtypes = [C.c_void_p, i64p, i64p, C.c_int64, C.c_int64]
     Lb.oiobf_tbf_contract_phase.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+    Lb.oiobf_tbf_copy_owned.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
     Lb.oiobf_tbf_set_peer_exchange.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64]
     Lb.oiobf_device_alloc.argtypes = [C.c_int64, C.POINTER(C.c_void_p)]
     Lb.oiobf_device_free.argtypes = [C.c_void_p]
@@ -188,8 +196,10 @@ class TorchComm:
         return int(t.item())
 
     def allreduce_sum_np(self, a: np.ndarray) -> np.ndarray:
+        """Element-wise sum over ranks, in the array's own integer width
+        (int32 skeletons move half the bytes of int64)."""
         import torch
-        t = torch.from_numpy(np.ascontiguousarray(a).astype(np.int64)).to(self._dev())
+        t = torch.from_numpy(np.ascontiguousarray(a)).to(self._dev())
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return t.cpu().numpy()
 

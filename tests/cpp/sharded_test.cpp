@@ -1,0 +1,59 @@
+// In-process multi-device butterfly (include/oiobf/sharded.hpp) against the
+// single-GPU butterfly of the same operator: usage
+//   sharded_test WORLD [case]      (every rank on device 0 -- a one-GPU box)
+// case: cubes32 (d = 3, L = 2), radon64 (d = 2, L = 2), plates64L4 (d = 2,
+// L = 4), dft6 (d = 6, n = 4, C_b = 1, L = 2, all ranks 1).  Prints one JSON line.
+#include <cmath>
+#include <iostream>
+#include <random>
+#include <string>
+
+#include "oiobf/butterfly.hpp"
+#include "oiobf/kernels.hpp"
+#include "oiobf/sharded.hpp"
+
+using namespace oiobf;
+
+int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "--compile-only") return 0;
+  const int world = argc > 1 ? std::atoi(argv[1]) : 2;
+  const std::string which = argc > 2 ? argv[2] : "cubes32";
+  KernelSpec s;
+  std::int64_t L = 2;
+  double tol = 1e-6;
+  if (which == "cubes32") s = green_cubes(32);
+  else if (which == "radon64") s = radon2d(64);
+  else if (which == "plates64L4") {
+    s = green_plates(64);
+    L = 4;
+    tol = 1e-4;
+  } else if (which == "dft6") {
+    s = dft(6, 4);
+    L = 2;
+    tol = 1e-8;
+  } else {
+    std::cerr << "unknown case " << which << "\n";
+    return 2;
+  }
+  const KernelEvaluator k = make_kernel(s);
+  const TensorButterfly single = tbf_construct(k, L, tol, ProxyStrategy{}, 5);
+  const ShardedTensorButterfly sh = tbf_construct_sharded(k, L, tol, ProxyStrategy{}, 5, std::vector<int>(world, 0));
+  std::vector<std::int64_t> shape(k.col_extents.begin(), k.col_extents.end());
+  shape.push_back(2);  // n_v = 2
+  DenseTensor F(shape);
+  std::mt19937_64 rng(3);
+  std::normal_distribution<double> nd;
+  for (auto& z : F.data()) z = Complex(nd(rng), nd(rng));
+  const DenseTensor G1 = tbf_contract(single, F);
+  const DenseTensor G = tbf_contract(sh, F);
+  double num = 0, den = 0;
+  for (std::size_t i = 0; i < G.data().size(); ++i) {
+    num += std::norm(G.data()[i] - G1.data()[i]);
+    den += std::norm(G1.data()[i]);
+  }
+  std::int64_t sent = 0;
+  for (int r = 0; r < world; ++r) sent += sh.layout(static_cast<std::size_t>(r)).send_total();
+  std::cout << "{\"case\":\"" << which << "\",\"world\":" << world << ",\"nmid\":" << sh.nmid()
+            << ",\"rel\":" << std::sqrt(num / den) << ",\"exchanged_elems\":" << sent << "}" << std::endl;
+  return 0;
+}

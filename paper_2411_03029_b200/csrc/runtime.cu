@@ -2912,7 +2912,7 @@ int oiobf_tbf_contract_phase(oiobf_tbf* h, int32_t phase, const void* dIn, void*
   if (no_graph) {
     run_ops(*h, pl, io, st, -1, phase);
   } else {  // one captured graph per (phase, input, output, stream)
-    GraphCache& gc = pl.phase_graphs[phase - 1];
+    auto& gc = pl.phase_graphs[phase - 1];
     cudaGraphExec_t ex = gc.find(dIn, dOut, st);
     if (!ex) {
       ex = capture_io(*h, pl, io, phase);

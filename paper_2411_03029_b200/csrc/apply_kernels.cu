@@ -199,7 +199,8 @@ __global__ void __launch_bounds__(kGemvThreads, 2) k_gemv_short(const int* __res
                                                               const GemvDesc* __restrict__ ds, long long total_rows,
                                                               const long long* __restrict__ row_begin,
                                                               const double2* __restrict__ cores,
-                                                              const double2* __restrict__ x, double2* __restrict__ y) {
+                                                              const double2* __restrict__ x, double2* __restrict__ y,
+                                                              int l2_ahead) {
   extern __shared__ __align__(16) double2 sx[];
   pdl_trigger_dep();
   const long long g0 = row_begin[blockIdx.x];
@@ -225,6 +226,10 @@ __global__ void __launch_bounds__(kGemvThreads, 2) k_gemv_short(const int* __res
     for (long long gr = g + warp; gr < pend; gr += kGemvThreads / 32) {
       const int r = static_cast<int>(gr - D.cta_off);
       const double2* row = cores + D.core_off + static_cast<long long>(r) * C;
+      if (l2_ahead && gr + kGemvThreads / 32 < pend) {  // this warp's next row into L2 behind this one
+        const char* nx = reinterpret_cast<const char*>(row + static_cast<long long>(kGemvThreads / 32) * C);
+        for (int o = lane * 128; o < C * 16; o += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(nx + o));
+      }
       double2 a[RL];
 #pragma unroll
       for (int u = 0; u < RL; ++u)
@@ -522,8 +527,10 @@ void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_ro
                                 cores, x, y));
   } else if (gemv_uses_short(nv, max_c)) {
     TBF_CUDA(cudaFuncSetAttribute(k_gemv_short<kShortRL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    const char* pe = std::getenv("OIOBF_GEMV_L2AHEAD");  // read per launch (A/B sweeps)
+    const int ahead = pe ? std::atoi(pe) : 1;
     TBF_CUDA(cudaLaunchKernelEx(&cfg, k_gemv_short<kShortRL>, cta_pair, d, static_cast<long long>(total_rows), row_begin,
-                                cores, x, y));
+                                cores, x, y, ahead));
   } else if (nv == 1) {
     TBF_CUDA(cudaFuncSetAttribute(k_gemv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     TBF_CUDA(cudaLaunchKernelEx(&cfg, k_gemv<1>, cta_pair, d, nv, static_cast<long long>(total_rows), row_begin, cores,

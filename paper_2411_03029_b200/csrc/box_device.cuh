@@ -27,7 +27,8 @@
 namespace tbf {
 namespace {
 
-constexpr int kBoxThreads = 256;
+constexpr int kBoxThreads = 256;  // default CTA size (k_box<128, .> for small boxes)
+__device__ __forceinline__ int box_nt() { return static_cast<int>(blockDim.x); }
 
 // n / d for 0 <= n < 2^24, d >= 1: float reciprocal estimate (off by at most
 // one in that range) plus one integer correction; no division subroutine.
@@ -99,7 +100,7 @@ template <int AM>
 __device__ __forceinline__ void first_mode_smem(const double2* __restrict__ xs, const double2* __restrict__ Mf,
                                                 double2* __restrict__ t0, int A, int Rs, int ein_f, int nv) {
   const int R = Rs * nv;
-  for (int r = threadIdx.x; r < R; r += kBoxThreads) {
+  for (int r = threadIdx.x; r < R; r += box_nt()) {
     const int v = qdiv(r, Rs), rs = r - v * Rs;
     double2 acc[AM];
 #pragma unroll
@@ -119,14 +120,14 @@ __device__ __forceinline__ void first_mode_smem(const double2* __restrict__ xs, 
 }
 
 // mode d-1 streamed from global memory (input box too large to stage)
-template <int AM>
+template <int AM, int LD>  // LD: loads in flight per thread (8 where the register budget allows)
 __device__ __forceinline__ void first_mode_global(const BoxDesc& D, int d, const double2* in,
                                                   const double2* __restrict__ Mf, double2* __restrict__ t0, int A,
                                                   int Rs, int ein_f, int nv) {
   const int f = d - 1;
   const int R = Rs * nv;
   const long long sf = D.in_stride[f];
-  for (int r = threadIdx.x; r < R; r += kBoxThreads) {
+  for (int r = threadIdx.x; r < R; r += box_nt()) {
     const int v = qdiv(r, Rs), rs = r - v * Rs;
     int rem = rs;
     long long addr = D.in_off + static_cast<long long>(v) * D.in_stride[d];
@@ -138,14 +139,16 @@ __device__ __forceinline__ void first_mode_global(const BoxDesc& D, int d, const
     double2 acc[AM];
 #pragma unroll
     for (int i = 0; i < AM; ++i) acc[i] = make_double2(0, 0);
+    // LD loads in flight per thread (the input streams from HBM: config 3's
+    // first V level reads 268 MB this way)
 #pragma unroll 1
-    for (int x0 = 0; x0 < ein_f; x0 += 4) {
-      double2 val[4];
+    for (int x0 = 0; x0 < ein_f; x0 += LD) {
+      double2 val[LD];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (x0 + u < ein_f) val[u] = in[addr + (x0 + u) * sf];
+      for (int u = 0; u < LD; ++u)
+        if (x0 + u < ein_f) val[u] = __ldcs(reinterpret_cast<const double2*>(in + addr + (x0 + u) * sf));
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < LD; ++u)
         if (x0 + u < ein_f)
 #pragma unroll
           for (int i = 0; i < AM; ++i)
@@ -162,7 +165,7 @@ __device__ __forceinline__ void middle_mode(const double2* __restrict__ src, dou
                                             const double2* __restrict__ Mk, int B, int ein, int eo, int Cc) {
   const int ng = (eo + 3) >> 2;
   const int ntask = B * ng * Cc;
-  for (int t = threadIdx.x; t < ntask; t += kBoxThreads) {
+  for (int t = threadIdx.x; t < ntask; t += box_nt()) {
     const int q1 = qdiv(t, B), b = t - q1 * B;
     const int c = qdiv(q1, ng), ag = q1 - c * ng;
     const int a0 = ag * 4;
@@ -210,7 +213,7 @@ __device__ __forceinline__ void last_mode(const BoxDesc& D, int d, int lo, int A
   const int ein = D.ein[0], eo = D.eout[0];
   const int ncg = (Cc + 3) >> 2;
   const int ntask = eo * ncg;
-  for (int t = threadIdx.x; t < ntask; t += kBoxThreads) {
+  for (int t = threadIdx.x; t < ntask; t += box_nt()) {
     const int cg = qdiv(t, eo), a = t - cg * eo;
     const int c0 = cg * 4;
     const int nc = min(4, Cc - c0);
@@ -250,7 +253,7 @@ struct BoxSmem {
 // in S.D (all threads synchronised after the copy).  `wait` blocks until the
 // input is produced (all threads call it; it ends with a CTA barrier).
 // `phase` is the staging mbarrier's parity, flipped on each bulk staging.
-template <class Wait>
+template <int LD, class Wait>
 __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, int crank,
                                          const double2* __restrict__ mats, const double2* in, double2* out,
                                          double2* sm, unsigned& phase, Wait wait) {
@@ -288,7 +291,7 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
     const int mrows = tr ? ein : D.eout[k];  // stored matrix: r x w column-major
     const double2* M = mats + D.mat_off[k];
     double2* Sm = smat + S.mo[k];
-    for (int q = tid; q < ein * eo; q += kBoxThreads) {
+    for (int q = tid; q < ein * eo; q += box_nt()) {
       const int x = qdiv(q, eo), a = q - x * eo + a0;
       Sm[q] = __ldg(M + (tr ? x + mrows * a : a + mrows * x));
     }
@@ -299,13 +302,13 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
     const int nrows = total_in / e0n;
     if (bulk) {
       const unsigned rbytes = static_cast<unsigned>(e0n) * 16u;
-      for (int row = tid; row < nrows; row += kBoxThreads)
+      for (int row = tid; row < nrows; row += box_nt())
         bulk_g2s(xs + row * e0n, in + row_addr(D, d, row), rbytes, &S.bar);
       mbar_wait(&S.bar, phase);
       phase ^= 1u;
     } else if (D.nsum == 1) {
       const long long s0 = D.in_stride[0];
-      for (int row = tid; row < nrows; row += kBoxThreads) {
+      for (int row = tid; row < nrows; row += box_nt()) {
         const long long ra = row_addr(D, d, row);
         for (int x = 0; x < e0n; ++x) cp_async16(xs + row * e0n + x, in + ra + x * s0);
       }
@@ -315,7 +318,7 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
       const long long s0 = D.in_stride[0];
       const long long cstr = D.sum_stride;
 #pragma unroll 1
-      for (int e = tid; e < total_in; e += kBoxThreads) {
+      for (int e = tid; e < total_in; e += box_nt()) {
         const int row = qdiv(e, e0n);
         const double2* p = in + row_addr(D, d, row) + (e - row * e0n) * s0;
         double2 acc = make_double2(0, 0);
@@ -344,7 +347,7 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
       else if (info.amax <= 4) first_mode_smem<4>(xs, Mf, t0, A, Rs, ein_f, nv);
       else first_mode_smem<8>(xs, Mf, t0, A, Rs, ein_f, nv);
     } else {
-      first_mode_global<8>(D, d, in, Mf, t0, A, Rs, ein_f, nv);
+      first_mode_global<8, LD>(D, d, in, Mf, t0, A, Rs, ein_f, nv);
     }
   }
   __syncthreads();
@@ -366,7 +369,7 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
   // output column offsets of mode 0's stores (computed once, not per store)
   const bool tab = Cc <= kColTab;
   if (tab)
-    for (int c = tid; c < Cc; c += kBoxThreads) S.coltab[c] = col_offset(D, d, lo, A, c);
+    for (int c = tid; c < Cc; c += box_nt()) S.coltab[c] = col_offset(D, d, lo, A, c);
   __syncthreads();
   // ---- mode 0 -> global
   last_mode(D, d, lo, A, src, smat + S.mo[0], Cc, tab ? S.coltab : nullptr, out);

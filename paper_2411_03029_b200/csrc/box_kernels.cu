@@ -16,8 +16,8 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // memory lets three CTAs co-reside (latency-bound small boxes: config 3's
 // levels 1.65 -> 1.56 ms), 2 otherwise (the 80-register cap spills on large
 // boxes: config 5 was 4% slower with it)
-template <int MINB>
-__global__ void __launch_bounds__(kBoxThreads, MINB) k_box(const BoxDesc* __restrict__ descs, BoxLaunchInfo info,
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_box(const BoxDesc* __restrict__ descs, BoxLaunchInfo info,
                                                         const double2* __restrict__ mats,
                                                         const double2* __restrict__ in, double2* __restrict__ out) {
   extern __shared__ __align__(128) double2 sm[];
@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(kBoxThreads, MINB) k_box(const BoxDesc* __rest
   }
   __syncthreads();
   unsigned phase = 0;
-  box_body(S, info, crank, mats, in, out, sm, phase, [] { pdl_wait(); });
+  box_body<MINB >= 3 ? 4 : 8>(S, info, crank, mats, in, out, sm, phase, [] { pdl_wait(); });
 }
 
 }  // namespace
@@ -45,16 +45,22 @@ bool pdl_enabled() {
 
 constexpr size_t kBox3Smem = 72 * 1024;  // three CTAs per SM fit in shared memory
 
-int box_ctas_per_sm(int amax, size_t smem) {
-  (void)amax;
+using BoxKernel = void (*)(const BoxDesc*, BoxLaunchInfo, const double2*, const double2*, double2*);
+constexpr size_t kBox6Smem = 36 * 1024;  // six 128-thread CTAs per SM fit in shared memory
+
+// kernel instance for a launch: 128 threads at 6 CTAs / SM (80 registers) for
+// small boxes, 256 threads at 3 (80 registers) or 2 (128: large boxes, and
+// streamed inputs whose 8 loads in flight would spill at 80) CTAs / SM
+BoxKernel box_kernel(int nt, int stage, size_t smem) {
+  if (nt == 128) return smem <= kBox6Smem ? k_box<128, 6> : k_box<128, 3>;
+  return smem <= kBox3Smem && stage ? k_box<256, 3> : k_box<256, 2>;
+}
+
+int box_ctas_per_sm(int nt, int stage, size_t smem) {
   int n = 0;
-  if (smem <= kBox3Smem) {
-    TBF_CUDA(cudaFuncSetAttribute(k_box<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-    TBF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_box<3>, kBoxThreads, smem));
-  } else {
-    TBF_CUDA(cudaFuncSetAttribute(k_box<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-    TBF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_box<2>, kBoxThreads, smem));
-  }
+  const BoxKernel k = box_kernel(nt, stage, smem);
+  TBF_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  TBF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, nt, smem));
   return n;
 }
 
@@ -69,11 +75,12 @@ void launch_box(i64 nitems, const BoxDesc* descs, const BoxLaunchInfo& info, con
   if (info.d < 2 || info.d > kMaxD) throw std::runtime_error("launch_box: d out of range");
   if (info.amax > 8) throw std::runtime_error("launch_box: more than 8 rows of mode d-1 per CTA");
   const size_t smem = box_smem_bytes(info);
-  auto kern = smem <= kBox3Smem ? k_box<3> : k_box<2>;
+  const int nt = info.nt > 0 ? info.nt : kBoxThreads;
+  const BoxKernel kern = box_kernel(nt, info.stage, smem);
   TBF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(nitems * info.cs));
-  cfg.blockDim = dim3(kBoxThreads);
+  cfg.blockDim = dim3(static_cast<unsigned>(nt));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

@@ -121,6 +121,7 @@ struct BoxLaunchInfo {
   int stage;                 // 1: stage the whole input box in shared memory (cp.async)
   int smem_mat, smem_in, smem_t;  // elements: factors, staged input, intermediate buffer t0
   int smem_t1;                    // elements of intermediate buffer t1 (odd middle modes, staging table)
+  int nt, pad_;                   // CTA size (256, or 128 for small boxes at up to 6 CTAs per SM)
 };
 void launch_box(i64 nitems, const BoxDesc* descs, const BoxLaunchInfo& info, const double2* mats,
                 const double2* in, double2* out, cudaStream_t st);
@@ -129,7 +130,7 @@ size_t box_smem_bytes(const BoxLaunchInfo& info);
 size_t box2_smem_bytes(int e0, int o0, int o1);
 void launch_box2(i64 nitems, const BoxDesc* descs, const BoxLaunchInfo& info, size_t smem, const double2* mats,
                  const double2* in, double2* out, cudaStream_t st);
-int box_ctas_per_sm(int amax, size_t smem);  // occupancy of k_box
+int box_ctas_per_sm(int nt, int stage, size_t smem);  // occupancy of k_box
 // programmatic dependent launch for the apply kernels (env OIOBF_NO_PDL=1 disables)
 bool pdl_enabled();
 

@@ -1085,6 +1085,15 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
     descs.swap(keep);
     if (descs.empty()) return true;
     static const int cs_env = std::getenv("OIOBF_BOX_SPLIT") ? std::atoi(std::getenv("OIOBF_BOX_SPLIT")) : 0;
+    // CTA size and input staging overrides (read per plan build: A/B sweeps)
+    const int nt_env = std::getenv("OIOBF_BOX_NT") ? std::atoi(std::getenv("OIOBF_BOX_NT")) : 0;
+    const int stage_env = std::getenv("OIOBF_BOX_STAGE") ? std::atoi(std::getenv("OIOBF_BOX_STAGE")) : -1;
+    // many small boxes (config 3: 4096 per level): 128-thread CTAs, up to 6
+    // per SM, and (without child sums) no input staging -- mode d-1 streams
+    // its columns from L2 -- measured 1.49 -> 1.27 ms for the config-3 apply;
+    // a few large boxes (config 2: 64 per level) keep 256 threads and staging
+    const bool many = static_cast<i64>(descs.size()) >= 4 * static_cast<i64>(device_sms());
+    const int box_nt = nt_env == 128 || nt_env == 256 ? nt_env : (many ? 128 : 256);
     const i64 nitems = static_cast<i64>(descs.size());
     int ef_min = 1 << 30, ef_max = 0;
     bool sums = false;
@@ -1128,6 +1137,8 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
       // intermediate buffers of the larger size (staging a box that a single
       // CTA reads once only lowers occupancy)
       c.stage = sums || (c.smem_mat + c.smem_in + 2 * std::max(c.smem_t, c.smem_t1)) * 16 <= 112 * 1024;
+      if ((stage_env == 0 || (stage_env < 0 && box_nt == 128)) && !sums) c.stage = false;
+      if (stage_env == 1) c.stage = true;
       if (!c.stage) c.smem_in = 0;
       c.fits = c.amax_rows <= 8 && c.total() <= kMaxDynSmem / 16;
       return c;
@@ -1147,7 +1158,7 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
         const Cfg c = size_for(cs);
         if (!c.fits) break;
         const size_t bytes = 16 * static_cast<size_t>(c.total());
-        const i64 cap = static_cast<i64>(box_ctas_per_sm(bucket(c.amax_rows), bytes)) * 148;
+        const i64 cap = static_cast<i64>(box_ctas_per_sm(box_nt, c.stage ? 1 : 0, bytes)) * 148;
         if (nitems * cs > cap) break;
         best = c;
       }
@@ -1170,6 +1181,7 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
     bl.info.cs = cs;
     bl.info.amax = bucket(amax_rows);
     bl.info.stage = stage ? 1 : 0;
+    bl.info.nt = box_nt;
     bl.info.smem_mat = static_cast<int>(smem_mat);
     bl.info.smem_in = static_cast<int>(smem_in);
     bl.info.smem_t = static_cast<int>(smem_t);

@@ -1084,7 +1084,7 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
     }
     descs.swap(keep);
     if (descs.empty()) return true;
-    static const int cs_env = std::getenv("OIOBF_BOX_SPLIT") ? std::atoi(std::getenv("OIOBF_BOX_SPLIT")) : 0;
+    const int cs_env = std::getenv("OIOBF_BOX_SPLIT") ? std::atoi(std::getenv("OIOBF_BOX_SPLIT")) : 0;
     // CTA size and input staging overrides (read per plan build: A/B sweeps)
     const int nt_env = std::getenv("OIOBF_BOX_NT") ? std::atoi(std::getenv("OIOBF_BOX_NT")) : 0;
     const int stage_env = std::getenv("OIOBF_BOX_STAGE") ? std::atoi(std::getenv("OIOBF_BOX_STAGE")) : -1;

@@ -664,6 +664,36 @@ def test_box2_gemm_kernel_matches_box_kernel(oracle, monkeypatch, name, spec, to
     bf.set_apply_engine("auto")
 
 
+@pytest.mark.parametrize("name,spec,tol,L", [CASES[1], CASES[3], CASES[6], CASES[7], CASES[8]],
+                         ids=[CASES[i][0] for i in (1, 3, 6, 7, 8)])
+def test_box_cta_variants_bit_identical(oracle, monkeypatch, name, spec, tol, L):
+    """Every CTA variant of the fused-box engine does the same operations in
+    the same order: 256-thread staged CTAs, 128-thread unstaged CTAs (one box
+    per CTA) and the persistent pipelined 128-thread kernel (next item's
+    descriptor / factors / raw children prefetched) give bit-identical G, within
+    1e-10 of the oracle on the same factors; nv = 1, 2."""
+    bf = tb.tbf_construct(spec, L, tol, seed=3)
+    tbo = oracle.tbf_construct(spec, L, tol, seed=3, replay=bf.export())
+    rng = np.random.default_rng(23)
+    monkeypatch.setenv("OIOBF_BOX2", "0")
+    for nv in (1, 2):
+        shape = (spec.n,) * spec.d + ((nv,) if nv > 1 else ())
+        F = rand_c(rng, shape)
+        outs = []
+        for env in ({"OIOBF_BOX_NT": "256"}, {"OIOBF_BOX_NT": "128", "OIOBF_BOX_PIPE": "0"},
+                    {"OIOBF_BOX_NT": "128", "OIOBF_BOX_PIPE": "1"}):
+            for k, v in env.items():
+                monkeypatch.setenv(k, v)
+            bf.set_apply_engine("tiny")  # drop cached plans
+            bf.set_apply_engine("box")
+            outs.append(bf.contract(F))
+            for k in env:
+                monkeypatch.delenv(k)
+        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+        assert rel(outs[2], tbo.contract(F)) < 1e-10
+    bf.set_apply_engine("auto")
+
+
 def test_register_cached_absorb_bit_identical():
     """Wide IDs (w > 32) fold their panels with the register-cached absorb
     (k_panel<512, RPL>); it performs the generic absorb's operations in the

@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(NT, MINB) k_box(const BoxDesc* __restrict__ de
   box_body<MINB >= 3 ? 4 : 8>(S, info, crank, mats, in, out, sm, phase, [] { pdl_wait(); });
 }
 
+
 }  // namespace
 
 bool pdl_enabled() {
@@ -68,6 +69,8 @@ size_t box_smem_bytes(const BoxLaunchInfo& info) {
   return sizeof(double2) * (static_cast<size_t>(info.smem_mat) + static_cast<size_t>(info.smem_in) +
                             static_cast<size_t>(info.smem_t) + static_cast<size_t>(info.smem_t1));
 }
+
+
 
 void launch_box(i64 nitems, const BoxDesc* descs, const BoxLaunchInfo& info, const double2* mats,
                 const double2* in, double2* out, cudaStream_t st) {

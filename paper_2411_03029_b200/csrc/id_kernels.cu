@@ -378,8 +378,12 @@ __device__ void absorb_panel_r(double2* __restrict__ R, double2* __restrict__ X,
           reflect_col_next_r<RPL>(b, R, X, xj, j, k, pr, lane, &bc[(j + 1) & 1]);
           k += kWarps;
         }
-        for (; k + kWarps < w; k += 2 * kWarps) reflect_col2_r<RPL>(b, R, X, xj, j, k, k + kWarps, nrows, pr, lane);
-        if (k < w) reflect_col_r<RPL>(b, R, X, xj, j, k, nrows, pr, lane);
+        if constexpr (RPL >= 8 || (NW <= 8 && RPL >= 4)) {  // one column at a time (two would spill)
+          for (; k < w; k += kWarps) reflect_col_r<RPL>(b, R, X, xj, j, k, nrows, pr, lane);
+        } else {
+          for (; k + kWarps < w; k += 2 * kWarps) reflect_col2_r<RPL>(b, R, X, xj, j, k, k + kWarps, nrows, pr, lane);
+          if (k < w) reflect_col_r<RPL>(b, R, X, xj, j, k, nrows, pr, lane);
+        }
       }
     } else if (owns_next) {
       panel_reflector(R, X, w, j + 1, nrows, pr, &bc[(j + 1) & 1]);
@@ -416,7 +420,7 @@ __device__ void absorb_panel(double2* __restrict__ R, double2* __restrict__ X, i
 // NT threads: 256, or 512 for wide IDs (w > 32, one CTA per SM by shared
 // memory) so each column step spreads over 16 warps
 template <int NT, int RPL>  // RPL: panel rows / 32 (register-cached absorb), 0: generic absorb
-__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 3) k_panel(LevelDesc L, KSpec ks, const int* __restrict__ proxies,
+__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : (RPL >= 8 ? 2 : 3)) k_panel(LevelDesc L, KSpec ks, const int* __restrict__ proxies,
                                                     const int* __restrict__ targets, const int* __restrict__ width,
                                                     double2* __restrict__ rpart) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -918,7 +922,12 @@ void launch_panel(const LevelDesc& L, const KSpec& ks, const int* proxies, const
     else launch_panel_t<512, 0>(L, ks, proxies, targets, width, rpart, smem, grid, st);
   } else {
     // (the register-cached absorb spills at the 3-CTA/SM budget of these CTAs)
-    launch_panel_t<kThreads, 0>(L, ks, proxies, targets, width, rpart, smem, grid, st);
+    // register-cached absorb on 256-row panels at 2 CTAs/SM (128 registers,
+    // one column update at a time): bit-identical to the generic absorb,
+    // config 2 panel 20.4 -> 17.2 ms, config 3 unchanged
+    static const int rc = std::getenv("OIOBF_PANEL_NARROW_RC") ? std::atoi(std::getenv("OIOBF_PANEL_NARROW_RC")) : 1;
+    if (rc && !generic && L.pr == 256) launch_panel_t<kThreads, 8>(L, ks, proxies, targets, width, rpart, smem, grid, st);
+    else launch_panel_t<kThreads, 0>(L, ks, proxies, targets, width, rpart, smem, grid, st);
   }
   TBF_CUDA(cudaGetLastError());
 }

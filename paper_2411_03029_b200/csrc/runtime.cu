@@ -1220,11 +1220,11 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
         ein = std::max(ein, a);
         eout = std::max(eout, c);
       }
-      fprintf(stderr, "[oiobf] box side %d level %d: %lld boxes x cs %d (amax %d, stage %d, box2 %d), max box in %lld "
-              "out %lld, smem %lld B, ef %d..%d\n", sd, l, static_cast<long long>(nitems), cs, amax_rows, stage ? 1 : 0,
-              bl.box2,
+      fprintf(stderr, "[oiobf] box side %d level %d: %lld boxes x cs %d (amax %d, stage %d, box2 %d, nt %d), "
+              "max box in %lld out %lld, smem %lld B, ef %d..%d\n", sd, l, static_cast<long long>(nitems), cs,
+              amax_rows, stage ? 1 : 0, bl.box2, bl.info.nt,
               static_cast<long long>(ein), static_cast<long long>(eout),
-              static_cast<long long>(16 * (smem_mat + smem_in + smem_t + smem_t1)), ef_min, ef_max);
+              static_cast<long long>(box_smem_bytes(bl.info)), ef_min, ef_max);
     }
     pl->bdescs.insert(pl->bdescs.end(), descs.begin(), descs.end());
     pl->ops.push_back(Op{3, static_cast<i64>(pl->boxes.size()), group});

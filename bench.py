@@ -234,10 +234,14 @@ def run_b200(args):
     fz_ranks = fzs.ranks
     entries, qr_flops = construction_work(fzs)
     del fzs
-    panel_s = tim["panel_ms"] / 1e3
+    # the two sides build concurrently (their k_panel launches overlap), so the
+    # summed per-launch panel time over-counts: the time base is the smaller of
+    # the summed panel time and the whole construction's wall time
+    panel_s = min(tim["panel_ms"], tim["total_ms"]) / 1e3
     construct_roof = {
         "bound": "fp64", "kernel": "k_panel (fused entry generation + TSQR)", "unit": "TFLOP/s",
         "algorithmic_flops": qr_flops, "entries": entries, "panel_s": panel_s,
+        "time_base": "min(summed k_panel launch time, construction wall time)",
         "achieved": qr_flops / panel_s / 1e12 if panel_s > 0 else None,
         "peak": fp64["dfma_tflops"],
         "frac": (qr_flops / panel_s / 1e12) / fp64["dfma_tflops"] if panel_s > 0 else None,

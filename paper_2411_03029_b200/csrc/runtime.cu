@@ -579,6 +579,16 @@ struct oiobf_tbf {
   int r1_ok = -1;        // cached rank-one eligibility (-1: not evaluated yet)
   double t_ms[6] = {0, 0, 0, 0, 0, 0};
   std::mutex mu;
+  // construction: the V/W and U/P sides are independent until the cores, so
+  // they build concurrently (one host thread and one stream each); their
+  // phase timers accumulate under t_mu
+  cudaStream_t sstream[2] = {nullptr, nullptr};
+  std::mutex t_mu;
+  cudaStream_t side_stream(int sd) const { return sstream[sd] ? sstream[sd] : stream; }
+  void add_ms(int i, double v) {
+    std::lock_guard<std::mutex> lk(t_mu);
+    t_ms[i] += v;
+  }
   // host-buffer contraction pipeline: copy-in / copy-out streams and the
   // events that order them against the compute stream (created on first use)
   cudaStream_t s_in = nullptr, s_out = nullptr;
@@ -597,6 +607,8 @@ struct oiobf_tbf {
     for (cudaEvent_t e : ev) cudaEventDestroy(e);
     if (s_in) cudaStreamDestroy(s_in);
     if (s_out) cudaStreamDestroy(s_out);
+    for (cudaStream_t x : sstream)
+      if (x) cudaStreamDestroy(x);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -679,7 +691,7 @@ LevelDesc make_level(const oiobf_tbf& b, int sd, int l, i64 r_est, i64 wmax) {
 void finish_level(oiobf_tbf& b, LevelData& ld, DevBuf<int>& sat, DevBuf<int>& skel_tmp, DevBuf<double2>& interp_tmp);
 
 void build_side_level(oiobf_tbf& b, int sd, int l, i64 r_est) {
-  cudaStream_t st = b.stream;
+  cudaStream_t st = b.side_stream(sd);
   const int d = b.d;
   // widest candidate set: leaf size (l=0) or max r(child0)+r(child1)
   i64 wmax;
@@ -723,7 +735,7 @@ void build_side_level(oiobf_tbf& b, int sd, int l, i64 r_est) {
     const LevelData* c = l > 0 ? &b.side[sd][static_cast<size_t>(l - 1)] : nullptr;
     launch_narrow_dft(L, b.ks, b.tol, c ? c->rank.p : nullptr, c ? c->skel_off.p : nullptr, c ? c->skel.p : nullptr,
                       ld.width.p, ld.rank.p, sat.p, ld.perm.p, skel_tmp.p, interp_tmp.p, ld.gaps.p, st);
-    b.t_ms[2] += t2.stop();
+    b.add_ms(2, t2.stop());
     finish_level(b, ld, sat, skel_tmp, interp_tmp);
     return;
   }
@@ -738,11 +750,11 @@ void build_side_level(oiobf_tbf& b, int sd, int l, i64 r_est) {
     const LevelData& c = b.side[sd][static_cast<size_t>(l - 1)];
     launch_targets(L, c.rank.p, c.skel_off.p, c.skel.p, targets.p, ld.width.p, st);
   }
-  b.t_ms[0] += t0.stop();
+  b.add_ms(0, t0.stop());
   DevBuf<double2> rpart(static_cast<size_t>(ns * L.nparts * wmax * wmax), st);
   EventTimer t1(st);
   launch_panel(L, b.ks, proxies.p, targets.p, ld.width.p, rpart.p, st);
-  b.t_ms[1] += t1.stop();
+  b.add_ms(1, t1.stop());
   ld.rank.alloc(static_cast<size_t>(ns));
   DevBuf<int> sat(static_cast<size_t>(ns), st);
   ld.perm.alloc(static_cast<size_t>(ns * wmax));
@@ -752,14 +764,14 @@ void build_side_level(oiobf_tbf& b, int sd, int l, i64 r_est) {
   EventTimer t2(st);
   launch_finish(L, b.tol, kTieEps, -1, rpart.p, targets.p, ld.width.p, ld.rank.p, sat.p, ld.perm.p, skel_tmp.p,
                 interp_tmp.p, ld.gaps.p, st);
-  b.t_ms[2] += t2.stop();
+  b.add_ms(2, t2.stop());
   finish_level(b, ld, sat, skel_tmp, interp_tmp);
 }
 
 // Host-side bookkeeping after a level's IDs: ranks / widths to the host, skeleton
 // and interp offsets, compaction of the per-slot scratch into the level arrays.
 void finish_level(oiobf_tbf& b, LevelData& ld, DevBuf<int>& sat, DevBuf<int>& skel_tmp, DevBuf<double2>& interp_tmp) {
-  cudaStream_t st = b.stream;
+  cudaStream_t st = b.side_stream(ld.L.side);
   const i64 ns = ld.nslots;
   const i64 wmax = ld.L.wmax;
   static const bool dbg = std::getenv("OIOBF_DEBUG") != nullptr;
@@ -826,7 +838,7 @@ void finish_level(oiobf_tbf& b, LevelData& ld, DevBuf<int>& sat, DevBuf<int>& sk
   ld.interp.alloc(static_cast<size_t>(std::max<i64>(io, 1)));
   launch_compact(ns, wmax, ld.rank.p, ld.width.p, ld.skel_off.p, ld.interp_off.p, skel_tmp.p, interp_tmp.p, ld.skel.p,
                  ld.interp.p, st);
-  b.t_ms[3] += t3.stop();
+  b.add_ms(3, t3.stop());
   // saturation would trigger the doubling retry (id.cpp:256-269); with the
   // default rank limit it is unreachable, so it is only reported.
 }
@@ -964,7 +976,8 @@ oiobf_tbf* construct(const oiobf_kernel_spec& spec, int L, double tol, const oio
   auto t_begin = now();
   auto b = construct_begin(spec, L, tol, ps, seed, 0, 1);
   auto t_start = now();
-  for (int sd = 0; sd < 2; ++sd) {
+  for (int sd = 0; sd < 2; ++sd) TBF_CUDA(cudaStreamCreateWithFlags(&b->sstream[sd], cudaStreamNonBlocking));
+  auto build_side = [&](int sd) {
     i64 r_est = 8;
     for (int l = 0; l <= b->Lc; ++l) {
       b->r_est[sd].push_back(r_est);
@@ -973,7 +986,33 @@ oiobf_tbf* construct(const oiobf_kernel_spec& spec, int L, double tol, const oio
       if (dbg) fprintf(stderr, "[oiobf] construct side %d level %d: %.2f ms\n", sd, l, ms(t0, now()));
       r_est = std::max<i64>(r_est, b->side[sd][static_cast<size_t>(l)].max_rank);
     }
+  };
+  static const bool serial = std::getenv("OIOBF_SERIAL_SIDES") != nullptr;  // A/B switch
+  if (serial) {
+    build_side(0);
+    build_side(1);
+  } else {  // U/P side on a second host thread (same device, own stream)
+    std::exception_ptr err;
+    const int dev = g_device;
+    std::thread th([&] {
+      try {
+        g_device = dev;
+        TBF_CUDA(cudaSetDevice(dev));
+        build_side(1);
+      } catch (...) {
+        err = std::current_exception();
+      }
+    });
+    try {
+      build_side(0);
+    } catch (...) {
+      th.join();
+      throw;
+    }
+    th.join();
+    if (err) std::rethrow_exception(err);
   }
+  for (int sd = 0; sd < 2; ++sd) TBF_CUDA(cudaStreamSynchronize(b->sstream[sd]));
   auto t1 = now();
   build_cores(*b);
   TBF_CUDA(cudaStreamSynchronize(b->stream));
@@ -1221,8 +1260,10 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
         eout = std::max(eout, c);
       }
       fprintf(stderr, "[oiobf] box side %d level %d: %lld boxes x cs %d (amax %d, stage %d, box2 %d, nt %d), "
+              "smem mat/in/t0/t1 %lld/%lld/%lld/%lld el, "
               "max box in %lld out %lld, smem %lld B, ef %d..%d\n", sd, l, static_cast<long long>(nitems), cs,
-              amax_rows, stage ? 1 : 0, bl.box2, bl.info.nt,
+              amax_rows, stage ? 1 : 0, bl.box2, bl.info.nt, static_cast<long long>(smem_mat),
+              static_cast<long long>(smem_in), static_cast<long long>(smem_t), static_cast<long long>(smem_t1),
               static_cast<long long>(ein), static_cast<long long>(eout),
               static_cast<long long>(box_smem_bytes(bl.info)), ef_min, ef_max);
     }

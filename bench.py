@@ -387,6 +387,37 @@ def run_b200(args):
         except Exception as e:  # the baseline is reported, never the product
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {e}"}
 
+    # compressed cores (block floating point, the ZFP role of PAPER.md Alg. 2):
+    # same timing rules; the core GEMV reads half the bytes
+    bfp = None
+    if rank == 0 and ws == 1 and args.nv == 1 and not args.no_extras and bf.apply_engine() == "box":
+        G64 = Gt.clone()
+        bf.set_core_format("bfp32")
+        for _ in range(max(args.warmup, 3)):
+            step()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for a, b in evs:
+            flush.zero_()
+            a.record(stream)
+            step()
+            b.record(stream)
+        torch.cuda.synchronize()
+        bms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+        bst = bf.plan_stats()
+        bprof = bf.profile_contract(Ft.data_ptr(), Gt.data_ptr(), reps=20, stream=sh)
+        gb = Gt.cpu().numpy().reshape((cfg.points, args.nv), order="F")
+        g64 = G64.cpu().numpy().reshape((cfg.points, args.nv), order="F")
+        b_err = float(np.linalg.norm(gb[srows] - exact) / np.linalg.norm(exact))
+        bfp = {"format": "bfp32: per 32 entries of a core row one 16-bit exponent, 32-bit mantissas (8.06 B/entry)",
+               "value": N / (bms / 1e3), "unit": UNIT, "ms_per_step": bms, "core_bytes": bst["core_bytes"],
+               "core_ms": bprof["core_ms"], "core_GBps": bst["core_bytes"] / (bprof["core_ms"] / 1e3) / 1e9,
+               "rel_diff_vs_fp64_apply": float(np.linalg.norm(gb - g64) / np.linalg.norm(g64)),
+               "sampled_rel_err": b_err, "ratio_to_tol": b_err / cfg.tol,
+               "note": "opt-in (oiobf_tbf_set_core_format); the headline value uses the FP64 cores"}
+        bf.set_core_format("fp64")
+        del G64
+
     extras = None
     if rank == 0 and ws == 1 and not args.no_extras:
         del bf
@@ -437,6 +468,7 @@ def run_b200(args):
                      "samples": 1000, "reference": "direct dense sums on the GPU (oiobf_dense_rows)",
                      "strategy": args.strategy},
         "cpu_baseline": cpu,
+        "compressed_cores": bfp,
         "extras": extras,
     }
     if rank == 0:

@@ -143,6 +143,14 @@ int oiobf_tbf_load(const char* path, oiobf_tbf** out);
 // else the fused-box engine), 1 the fused-box engine, 2 the tiny-box engine,
 // 4 the rank-one engine (OIOBF_EINVAL when the factorization is not eligible;
 // 3, the round-1 dataflow engine, was removed).  Changing it drops cached plans.
+/* Core storage for the apply: 0 = FP64 (exact, default); 1 = block floating
+ * point -- the role ZFP plays in PAPER.md Alg. 2 ("ZFP decompress K(tbar,
+ * sbar)"): per 32 entries of a core row one 16-bit exponent, per component a
+ * 32-bit mantissa (8.06 instead of 16 bytes per entry; every entry within
+ * 2^-31 of its block's largest component, ~5e-10 relative), decoded in the
+ * core GEMV (n_v = 1).  The FP64 cores stay resident; the rank-one engine
+ * (1 x 1 cores) refuses format 1. */
+int oiobf_tbf_set_core_format(oiobf_tbf* h, int32_t format);
 int oiobf_tbf_set_apply_engine(oiobf_tbf* h, int32_t engine);
 // engine in use: 1 box, 2 tiny, 4 rank-one
 int oiobf_tbf_apply_engine(oiobf_tbf* h, int32_t* engine);

@@ -45,7 +45,8 @@ EXPORTS = [
     "oiobf_tbf_umid_import", "oiobf_tbf_set_exchange", "oiobf_tbf_contract_phase",
     "oiobf_tbf_set_apply_engine", "oiobf_tbf_apply_engine", "oiobf_tbf_save", "oiobf_tbf_load",
     "oiobf_tbf_contract_async", "oiobf_tbf_set_peer_exchange", "oiobf_device_alloc", "oiobf_device_free",
-    "oiobf_ipc_handle", "oiobf_ipc_open", "oiobf_ipc_close", "oiobf_memcpy", "oiobf_synchronize", "oiobf_tbf_copy_owned",
+    "oiobf_ipc_handle", "oiobf_ipc_open", "oiobf_ipc_close", "oiobf_memcpy", "oiobf_synchronize",
+    "oiobf_tbf_copy_owned", "oiobf_tbf_set_core_format",
     "oiobf_tbf_export_cores",
     "oiobf_tbf_profile_core_cold", "oiobf_fp64_peak",
 ]
@@ -82,6 +83,7 @@ def load(path: str = LIB_PATH):
         L.oiobf_tbf_contract_async.argtypes = [C.c_void_p, f64p, f64p, C.c_int64, C.c_void_p]
         L.oiobf_tbf_memory.argtypes = [C.c_void_p, i64p]
         L.oiobf_tbf_set_apply_engine.argtypes = [C.c_void_p, C.c_int32]
+        L.oiobf_tbf_set_core_format.argtypes = [C.c_void_p, C.c_int32]
         L.oiobf_tbf_save.argtypes = [C.c_void_p, C.c_char_p]
         L.oiobf_tbf_load.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
         L.oiobf_tbf_apply_engine.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]

@@ -287,6 +287,14 @@ class TensorButterfly:
         """TBF1 file: bit-exact round trip through tbf_load."""
         _lib.check(_lib.load().oiobf_tbf_save(self._h, str(path).encode()))
 
+    def set_core_format(self, fmt: str) -> None:
+        """'fp64' (exact, default) | 'bfp32': block-floating-point cores (one
+        16-bit exponent per 32 entries of a core row, 32-bit mantissas; half the
+        core bytes, ~5e-10 relative per entry) read by the n_v = 1 core GEMV --
+        the role ZFP plays in PAPER.md Alg. 2.  The FP64 cores stay resident."""
+        code = {"fp64": 0, "bfp32": 1}[fmt]
+        _lib.check(_lib.load().oiobf_tbf_set_core_format(self._h, code))
+
     def set_apply_engine(self, engine: str) -> None:
         """'auto' | 'box' | 'tiny' | 'rank1'.  box: one fused-box launch per
         level (CUDA graph); tiny: thread-per-output engine for d = 6 scale;

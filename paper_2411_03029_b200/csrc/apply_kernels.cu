@@ -247,6 +247,122 @@ __global__ void __launch_bounds__(kGemvThreads, 2) k_gemv_short(const int* __res
   }
 }
 
+// ---- compressed cores (the role ZFP plays in PAPER.md Alg. 2: "ZFP
+// decompress K(tbar, sbar)"): block floating point, fixed rate.  Each core
+// row is cut into blocks of 32 complex entries; a block stores one 16-bit
+// exponent e (every |component| < 2^e) and, per component, the 32-bit integer
+// round(x 2^(31 - e)), so a decoded entry is within 2^(e - 32) <= 2^-31 max|block|
+// of the FP64 value (~5e-10 relative) and a core takes 8.06 instead of 16
+// bytes per entry.  The core GEMV is HBM-bound, so it reads half the bytes.
+// Layout: pair p's rows padded to nb = ceil(C / 32) blocks, row r at
+// q_off[p] + r nb 32 (int2 = re, im), its exponents at (q_off[p] + r nb 32) / 32.
+__global__ void k_bfp_compress(const long long* __restrict__ blk_prefix, long long npairs,
+                               const GemvDesc* __restrict__ raw, const long long* __restrict__ q_off,
+                               long long total_blocks, const double2* __restrict__ cores, int2* __restrict__ q,
+                               short* __restrict__ ex) {
+  const long long gb = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gb >= total_blocks) return;
+  long long lo = 0, hi = npairs - 1;  // pair holding block gb
+  while (lo < hi) {
+    const long long mid = (lo + hi + 1) >> 1;
+    if (blk_prefix[mid] <= gb) lo = mid;
+    else hi = mid - 1;
+  }
+  const GemvDesc D = raw[lo];
+  const int nb = (D.C + 31) / 32;
+  const long long local = gb - blk_prefix[lo];
+  const long long r = local / nb;
+  const int b = static_cast<int>(local - r * nb);
+  const int c = b * 32 + lane;
+  const double2 v = c < D.C ? cores[D.core_off + r * D.C + c] : make_double2(0, 0);
+  double m = fmax(fabs(v.x), fabs(v.y));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const int e = m > 0 ? ilogb(m) + 1 : -1000;  // |component| < 2^e
+  const double sc = ldexp(1.0, 31 - e);
+  const long long base = q_off[lo] + (r * nb + b) * 32;
+  const double qx = fmin(fmax(rint(v.x * sc), -2147483647.0), 2147483647.0);
+  const double qy = fmin(fmax(rint(v.y * sc), -2147483647.0), 2147483647.0);
+  q[base + lane] = make_int2(static_cast<int>(qx), static_cast<int>(qy));
+  if (lane == 0) ex[base / 32] = static_cast<short>(e);
+}
+
+__device__ __forceinline__ int4 ld_stream_i4(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// Core GEMV on block-floating-point cores (n_v = 1): k_gemv_short's schedule
+// (persistent byte-balanced CTAs, a warp per row, every load of a row chunk
+// in flight at once, the warp's next row prefetched into L2), rows decoded in
+// registers.  Each lane loads 16 B = two consecutive entries per instruction
+// (a warp instruction covers two 32-entry blocks: lanes 0-15 the first, 16-31
+// the second); the blocks' exponents are loaded once per chunk (lane b holds
+// block b's) and shuffled to the lanes that decode them.
+template <int NBC>  // blocks per chunk of a row (16: rows up to 512 entries in one chunk)
+__global__ void __launch_bounds__(kGemvThreads, 3) k_gemv_bfp(const int* __restrict__ cta_pair,
+                                                            const GemvDesc* __restrict__ ds, long long total_rows,
+                                                            const long long* __restrict__ row_begin,
+                                                            const int2* __restrict__ q, const short* __restrict__ ex,
+                                                            const double2* __restrict__ x, double2* __restrict__ y) {
+  extern __shared__ __align__(16) double2 sx[];
+  constexpr int NL = NBC / 2;  // 16-byte loads per lane per chunk
+  pdl_trigger_dep();
+  const long long g0 = row_begin[blockIdx.x];
+  const long long g1 = min(total_rows, row_begin[blockIdx.x + 1]);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = lane >> 4, hl = lane & 15;
+  int p = cta_pair[blockIdx.x];
+  pdl_wait_dep();
+  long long g = g0;
+  while (g < g1) {
+    const GemvDesc D = ds[p];
+    const long long pend = min(g1, D.cta_off + D.R);
+    const int C = D.C, nb = (C + 31) / 32;
+    const int nb2 = (nb + 1) & ~1;  // x padded to whole block pairs
+    const double2* xs = x + D.x_off;
+    for (int i = threadIdx.x; i < nb2 * 32; i += kGemvThreads) sx[i] = i < C ? xs[i] : make_double2(0, 0);
+    __syncthreads();
+    for (long long gr = g + warp; gr < pend; gr += kGemvThreads / 32) {
+      const int r = static_cast<int>(gr - D.cta_off);
+      const long long rq = D.core_off + static_cast<long long>(r) * nb * 32;  // this row's first entry
+      if (gr + kGemvThreads / 32 < pend) {  // the warp's next row into L2
+        const char* nx = reinterpret_cast<const char*>(q + rq + static_cast<long long>(kGemvThreads / 32) * nb * 32);
+        for (int o = lane * 128; o < nb * 256; o += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(nx + o));
+      }
+      double2 acc0 = make_double2(0, 0), acc1 = make_double2(0, 0);
+      for (int b0 = 0; b0 < nb; b0 += NBC) {
+        int4 a[NL];
+#pragma unroll
+        for (int u = 0; u < NL; ++u)
+          if (b0 + 2 * u + half < nb)
+            a[u] = ld_stream_i4(reinterpret_cast<const int4*>(q + rq + (b0 + 2 * u + half) * 32 + 2 * hl));
+        const int ev = b0 + lane < nb ? ex[rq / 32 + b0 + lane] : 0;
+#pragma unroll
+        for (int u = 0; u < NL; ++u) {
+          const int bb = 2 * u + half;  // this lane's block in the chunk
+          const int e = __shfl_sync(0xffffffffu, ev, bb & 31);
+          if (b0 + bb < nb) {
+            const double sc = __longlong_as_double(static_cast<long long>(e - 31 + 1023) << 52);  // 2^(e - 31)
+            const int c = (b0 + bb) * 32 + 2 * hl;
+            cfma(acc0, make_double2(static_cast<double>(a[u].x) * sc, static_cast<double>(a[u].y) * sc), sx[c]);
+            cfma(acc1, make_double2(static_cast<double>(a[u].z) * sc, static_cast<double>(a[u].w) * sc), sx[c + 1]);
+          }
+        }
+      }
+      const double2 t = warp_sum2(cadd(acc0, acc1));
+      if (lane == 0) y[D.y_off + r] = t;
+    }
+    __syncthreads();
+    g = pend;
+    ++p;
+  }
+}
+
 // Multi-vector core contraction on the FP64 tensor core: Y (R x nv) = K (R x C) X
 // (C x nv) per pair, nv <= 8 padded to one 8-wide N tile.  Same CTA row ranges
 // and x staging as k_gemv; a warp takes 8-row tiles of a pair and walks the
@@ -497,6 +613,43 @@ void launch_mode_product(i64 nitems, const MPStep* steps, i64 total_out, const B
 bool gemv_uses_mma(int nv, int max_c) {
   static const bool no_mma = std::getenv("OIOBF_GEMV_NO_MMA") != nullptr;
   return !no_mma && nv >= 2 && nv <= 8 && static_cast<size_t>(max_c | 1) * nv * sizeof(double2) <= 96 * 1024;
+}
+
+void launch_bfp_compress(const long long* blk_prefix, i64 npairs, const GemvDesc* raw, const long long* q_off,
+                         i64 total_blocks, const double2* cores, int2* q, short* ex, cudaStream_t st) {
+  if (total_blocks == 0) return;
+  const i64 threads = total_blocks * 32;
+  k_bfp_compress<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(blk_prefix, npairs, raw, q_off,
+                                                                              total_blocks, cores, q, ex);
+  TBF_CUDA(cudaGetLastError());
+}
+
+int gemv_bfp_ctas_per_sm(int max_c) {
+  int n = 0;
+  const size_t smem = sizeof(double2) * static_cast<size_t>((max_c + 63) / 64 * 64);
+  TBF_CUDA(cudaFuncSetAttribute(k_gemv_bfp<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  TBF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gemv_bfp<16>, kGemvThreads, smem));
+  return n < 1 ? 1 : n;
+}
+
+void launch_gemv_bfp(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, const i64* row_begin,
+                     const int2* q, const short* ex, const double2* x, double2* y, int max_c, cudaStream_t st) {
+  if (nctas == 0) return;
+  const size_t smem = sizeof(double2) * static_cast<size_t>((max_c + 63) / 64 * 64);
+  TBF_CUDA(cudaFuncSetAttribute(k_gemv_bfp<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(nctas));
+  cfg.blockDim = dim3(kGemvThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  TBF_CUDA(cudaLaunchKernelEx(&cfg, k_gemv_bfp<16>, cta_pair, d, static_cast<long long>(total_rows), row_begin, q, ex,
+                              x, y));
+  TBF_CUDA(cudaGetLastError());
 }
 
 constexpr int kShortRL = 16;  // k_gemv_short: rows up to 512 elements

@@ -85,6 +85,13 @@ struct GemvDesc {  // y(R x nv) = K(R x C, row-major) * x(C x nv)
 void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, const i64* row_begin, int nv,
                  const double2* cores, const double2* x, double2* y, int max_c, cudaStream_t st);
 int gemv_ctas_per_sm(int nv, int max_c);
+// block-floating-point cores (fixed rate: 32-bit mantissas, one 16-bit
+// exponent per 32 complex entries of a row; the ZFP role of PAPER.md Alg. 2)
+void launch_bfp_compress(const long long* blk_prefix, i64 npairs, const GemvDesc* raw, const long long* q_off,
+                         i64 total_blocks, const double2* cores, int2* q, short* ex, cudaStream_t st);
+int gemv_bfp_ctas_per_sm(int max_c);
+void launch_gemv_bfp(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, const i64* row_begin,
+                     const int2* q, const short* ex, const double2* x, double2* y, int max_c, cudaStream_t st);
 // TMA bulk-copy pipelined variant (rows staged by cp.async.bulk into an SMEM ring)
 void launch_gemv_tma(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_rows, const i64* row_begin, int nv,
                      int stages, int stage_elems, int xcap, const double2* cores, const double2* x, double2* y,

@@ -333,6 +333,7 @@ struct AsyncSet {
 struct Plan {
   i64 nv = 0;
   i64 scratch_elems = 0;
+  bool bfp = false;  // core GEMV on the block-floating-point cores (n_v = 1)
   std::vector<MPStep> steps;
   std::vector<Blk> blks;
   std::vector<MPLaunch> mps;
@@ -491,7 +492,8 @@ void finish_gemv(Plan& pl, i64 begin, i64 end, i64 nv) {
   std::vector<i64> rb;
   std::vector<int> map;
   {
-    const int per_sm = gemv_ctas_per_sm(static_cast<int>(nv), std::max(gl.max_c, 1));
+    const int per_sm = pl.bfp ? gemv_bfp_ctas_per_sm(std::max(gl.max_c, 1))
+                              : gemv_ctas_per_sm(static_cast<int>(nv), std::max(gl.max_c, 1));
     gl.ctas = std::min<i64>(static_cast<i64>(148) * per_sm, rows);
     split_rows(pl, begin, end, gl.ctas, rb, map);
     gl.map_begin = static_cast<i64>(pl.gemv_map.size());
@@ -506,7 +508,7 @@ void finish_gemv(Plan& pl, i64 begin, i64 end, i64 nv) {
   static const int per_sm_env =
       std::getenv("OIOBF_TMA_CTAS_PER_SM") ? std::atoi(std::getenv("OIOBF_TMA_CTAS_PER_SM")) : 2;
   static const int stages_env = std::getenv("OIOBF_TMA_STAGES") ? std::atoi(std::getenv("OIOBF_TMA_STAGES")) : 8;
-  if (!no_tma && gl.max_c >= 64) {
+  if (!no_tma && !pl.bfp && gl.max_c >= 64) {
     const i64 grid = std::min<i64>(148 * std::max(1, per_sm_env), rows);
     const int stage_elems = (gl.max_c + 7) / 8 * 8;
     const int xcap = gl.max_c * static_cast<int>(nv);
@@ -572,6 +574,13 @@ struct oiobf_tbf {
   std::vector<i64> r_est[2];
   DevBuf<double2> cores;
   HostArray<PairDesc> h_pairs;
+  // block-floating-point copy of the cores (oiobf_tbf_set_core_format 1):
+  // pair p's blocks at bfp_off[p] (entries), exponents at bfp_off[p] / 32
+  int core_format = 0;
+  DevBuf<int2> bfp_q;
+  DevBuf<short> bfp_e;
+  std::vector<i64> bfp_off;
+  i64 bfp_entries = 0;
   i64 total_core = 0;
   std::map<i64, std::unique_ptr<Plan>> plans;
   int apply_engine = 0;  // 0 auto, 1 box engine, 2 tiny-box engine, 4 rank-one engine
@@ -1064,6 +1073,7 @@ MPStep make_step(const TRef& in, const TRef& out, int mode, int transpose) {
 
 std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity = 0) {
   auto pl = std::make_unique<Plan>();
+  pl->bfp = b.core_format == 1 && nv == 1;
   pl->nv = nv;
   pl->nchunk = chunked && b.world == 1 ? static_cast<int>(ipow(2, b.Lc)) : 1;
   const int d = b.d;
@@ -1448,7 +1458,7 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
       if (R != pd.R || x.size() != static_cast<i64>(pd.C) * nv)
         throw std::runtime_error("internal: core shape mismatch");
       GemvDesc g;
-      g.core_off = pd.core_off;
+      g.core_off = pl->bfp ? b.bfp_off[static_cast<size_t>(p)] : pd.core_off;
       g.x_off = x.off;
       g.y_off = y.off;
       g.R = pd.R;
@@ -2119,7 +2129,10 @@ void run_ops(oiobf_tbf& b, Plan& pl, const OpBuffers& io, cudaStream_t st, int g
       double2* y = pl.sharded ? io.send : scr;
       const GemvLaunch& gl = pl.gemvs[static_cast<size_t>(op.idx)];
       const GemvDesc* gd = pl.d_gemv.p + gl.desc_begin;
-      if (gl.tma)
+      if (pl.bfp)
+        launch_gemv_bfp(pl.d_gemv_map.p + gl.map_begin, gd, gl.ctas, gl.total_rows, pl.d_gemv_rb.p + gl.rb_begin,
+                        b.bfp_q.p, b.bfp_e.p, scr, y, gl.max_c, st);
+      else if (gl.tma)
         launch_gemv_tma(pl.d_tma_map.p + gl.tma_map_begin, gd, gl.tma_ctas, gl.total_rows,
                         pl.d_gemv_rb.p + gl.tma_rb_begin, static_cast<int>(pl.nv), gl.tma_stages,
                         gl.tma_stage_elems, gl.tma_xcap, b.cores.p, scr, y, st);
@@ -3026,6 +3039,59 @@ int oiobf_tbf_load(const char* path, oiobf_tbf** out) {
   CAPI_END
 }
 
+namespace {
+// Block-floating-point copy of the cores (k_bfp_compress, one warp per block
+// of 32 entries of a row).  Pairs this rank does not own have C = 0.
+void compress_cores_bfp(oiobf_tbf& b) {
+  cudaStream_t st = b.stream;
+  const i64 P = b.nmid * b.nmid;
+  std::vector<long long> blk_prefix(static_cast<size_t>(P)), q_off(static_cast<size_t>(P));
+  std::vector<GemvDesc> raw(static_cast<size_t>(P));
+  b.bfp_off.assign(static_cast<size_t>(P), 0);
+  i64 blocks = 0;
+  for (i64 p = 0; p < P; ++p) {
+    const PairDesc& pd = b.h_pairs[static_cast<size_t>(p)];
+    GemvDesc g{};
+    g.core_off = pd.core_off;
+    g.R = pd.R;
+    g.C = pd.C;
+    raw[static_cast<size_t>(p)] = g;
+    blk_prefix[static_cast<size_t>(p)] = blocks;
+    q_off[static_cast<size_t>(p)] = blocks * 32;
+    b.bfp_off[static_cast<size_t>(p)] = blocks * 32;
+    if (pd.C > 0) blocks += static_cast<i64>(pd.R) * ((pd.C + 31) / 32);
+  }
+  b.bfp_entries = blocks * 32;
+  b.bfp_q.alloc(static_cast<size_t>(std::max<i64>(b.bfp_entries, 32)));
+  b.bfp_e.alloc(static_cast<size_t>(std::max<i64>(blocks, 1)));
+  DevBuf<long long> d_prefix = to_device(blk_prefix, st), d_qoff = to_device(q_off, st);
+  DevBuf<GemvDesc> d_raw = to_device(raw, st);
+  launch_bfp_compress(d_prefix.p, P, d_raw.p, d_qoff.p, blocks, b.cores.p, b.bfp_q.p, b.bfp_e.p, st);
+  TBF_CUDA(cudaStreamSynchronize(st));
+}
+}  // namespace
+
+// 0 = FP64 cores (exact; default), 1 = block floating point (32-bit mantissas,
+// one 16-bit exponent per 32 entries of a core row: half the core bytes, each
+// entry within 2^-31 of its block's largest component; used by the n_v = 1
+// core GEMV).  The FP64 cores stay resident; switching rebuilds the plans.
+int oiobf_tbf_set_core_format(oiobf_tbf* h, int32_t format) {
+  CAPI_BEGIN
+  require(h, "tbf_set_core_format: null handle");
+  require(format == 0 || format == 1, "tbf_set_core_format: format must be 0 (fp64) or 1 (block floating point)");
+  std::lock_guard<std::mutex> lk(h->mu);
+  TBF_CUDA(cudaSetDevice(h->device));
+  if (format == h->core_format) return OIOBF_OK;
+  h->sync_all();
+  if (format == 1) {
+    require(!use_r1_engine(*h), "tbf_set_core_format: the rank-one engine keeps its 1 x 1 cores in FP64");
+    if (h->bfp_off.empty()) compress_cores_bfp(*h);
+  }
+  h->plans.clear();
+  h->core_format = format;
+  CAPI_END
+}
+
 int oiobf_tbf_set_apply_engine(oiobf_tbf* h, int32_t engine) {
   CAPI_BEGIN
   require(h, "tbf_set_apply_engine: null handle");
@@ -3221,8 +3287,10 @@ int oiobf_tbf_plan_stats(oiobf_tbf* h, int64_t out[4]) {
   for (int sd = 0; sd < 2; ++sd)
     for (const auto& lv : h->side[sd]) fac += lv.total_interp;
   const i64 N = ipow(h->n, h->d);
-  out[0] = 16 * (2 * N + fac + h->total_core);
-  out[1] = 16 * h->total_core;
+  // cores as the GEMV reads them: FP64, or 8 B per entry + 2 B per 32-entry block
+  const i64 core_bytes = pl.bfp ? 8 * h->bfp_entries + 2 * (h->bfp_entries / 32) : 16 * h->total_core;
+  out[0] = 16 * (2 * N + fac) + core_bytes;
+  out[1] = core_bytes;
   out[2] = static_cast<int64_t>(pl.ops.size());
   i64 macs = h->total_core;
   for (const MPStep& s : pl.steps) {

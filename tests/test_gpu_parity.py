@@ -705,3 +705,46 @@ def test_register_cached_absorb_bit_identical():
                        timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "bit-identical: True" in r.stdout, r.stdout
+
+
+@pytest.mark.parametrize("name,spec,tol,L", [CASES[1], CASES[3], CASES[4], CASES[7]],
+                         ids=[CASES[i][0] for i in (1, 3, 4, 7)])
+def test_bfp_cores(oracle, name, spec, tol, L):
+    """Block-floating-point cores (oiobf_tbf_set_core_format 1, the ZFP role of
+    PAPER.md Alg. 2): the n_v = 1 apply stays within 1e-8 relative of the FP64
+    apply (entries carry 31-bit mantissas per block), n_v > 1 keeps the FP64
+    cores (bit-identical), and switching back restores the FP64 result bit for
+    bit."""
+    bf = tb.tbf_construct(spec, L, tol, seed=3)
+    rng = np.random.default_rng(29)
+    F = rand_c(rng, (spec.n,) * spec.d)
+    F2 = rand_c(rng, (spec.n,) * spec.d + (2,))
+    g64, g64_2 = bf.contract(F), bf.contract(F2)
+    bf.set_core_format("bfp32")
+    gb = bf.contract(F)
+    assert 0 < rel(gb, g64) < 1e-8, rel(gb, g64)
+    assert np.array_equal(bf.contract(F2), g64_2)
+    bf.set_core_format("fp64")
+    assert np.array_equal(bf.contract(F), g64)
+
+
+def test_bfp_cores_config3_and_refusals():
+    """Config 3 at full size on compressed cores: within 1e-8 of the FP64 apply
+    and the same sampled error against dense sums; the rank-one engine (1 x 1
+    cores) refuses the format."""
+    c = BY_NAME["green_cubes_n256"]
+    bf = tb.tbf_construct(c.spec, c.L, c.tol, seed=c.seed)
+    rng = np.random.default_rng(31)
+    F = rand_c(rng, (c.spec.n,) * c.spec.d)
+    g64 = bf.contract(F).reshape(-1, order="F")
+    bf.set_core_format("bfp32")
+    gb = bf.contract(F).reshape(-1, order="F")
+    assert rel(gb, g64) < 1e-8
+    rows = rng.choice(c.points, 1000, replace=False)
+    exact = tb.dense_rows(c.spec, F, rows)[:, 0]
+    assert abs(rel(gb[rows], exact) - rel(g64[rows], exact)) <= 1e-6 * rel(g64[rows], exact)
+    del bf
+    d6 = tb.tbf_construct(dft(6, 4), 2, 1e-8, seed=3)
+    assert d6.apply_engine() == "rank1"
+    with pytest.raises(Exception):
+        d6.set_core_format("bfp32")

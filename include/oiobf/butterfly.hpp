@@ -38,6 +38,10 @@ class TensorButterfly {
   const KernelEvaluator& evaluator() const { return eval_; }
   oiobf_tbf* handle() const { return h_.get(); }
 
+  // Core storage for the apply: false = FP64 (exact, default), true = block
+  // floating point (the ZFP step of PAPER.md Alg. 2; oiobf_tbf_set_core_format)
+  void compress_cores(bool on) { detail::check(oiobf_tbf_set_core_format(h_.get(), on ? 1 : 0)); }
+
   TbfMemory memory() const {
     std::int64_t m[5];
     detail::check(oiobf_tbf_memory(h_.get(), m));

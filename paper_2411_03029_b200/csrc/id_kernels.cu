@@ -419,8 +419,8 @@ __device__ void absorb_panel(double2* __restrict__ R, double2* __restrict__ X, i
 
 // NT threads: 256, or 512 for wide IDs (w > 32, one CTA per SM by shared
 // memory) so each column step spreads over 16 warps
-template <int NT, int RPL>  // RPL: panel rows / 32 (register-cached absorb), 0: generic absorb
-__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : (RPL >= 8 ? 2 : 3)) k_panel(LevelDesc L, KSpec ks, const int* __restrict__ proxies,
+template <int NT, int RPL, int MINB = (NT >= 512 ? 1 : (RPL >= 8 ? 2 : 3))>  // RPL: panel rows / 32
+__global__ void __launch_bounds__(NT, MINB) k_panel(LevelDesc L, KSpec ks, const int* __restrict__ proxies,
                                                     const int* __restrict__ targets, const int* __restrict__ width,
                                                     double2* __restrict__ rpart) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -875,11 +875,11 @@ void launch_targets(const LevelDesc& L, const int* crank, const i64* cskel_off, 
   TBF_CUDA(cudaGetLastError());
 }
 
-template <int NT, int RPL>
+template <int NT, int RPL, int MINB = (NT >= 512 ? 1 : (RPL >= 8 ? 2 : 3))>
 void launch_panel_t(const LevelDesc& L, const KSpec& ks, const int* proxies, const int* targets, const int* width,
                     double2* rpart, size_t smem, i64 grid, cudaStream_t st) {
-  TBF_CUDA(cudaFuncSetAttribute(k_panel<NT, RPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-  k_panel<NT, RPL><<<static_cast<unsigned>(grid), NT, smem, st>>>(L, ks, proxies, targets, width, rpart);
+  TBF_CUDA(cudaFuncSetAttribute(k_panel<NT, RPL, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  k_panel<NT, RPL, MINB><<<static_cast<unsigned>(grid), NT, smem, st>>>(L, ks, proxies, targets, width, rpart);
 }
 
 // Panel rows and resident CTAs per SM for a level of width wmax.  The column

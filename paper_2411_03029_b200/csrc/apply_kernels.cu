@@ -680,8 +680,7 @@ void launch_gemv(const int* cta_pair, const GemvDesc* d, i64 nctas, i64 total_ro
                                 cores, x, y));
   } else if (gemv_uses_short(nv, max_c)) {
     TBF_CUDA(cudaFuncSetAttribute(k_gemv_short<kShortRL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-    const char* pe = std::getenv("OIOBF_GEMV_L2AHEAD");  // read per launch (A/B sweeps)
-    const int ahead = pe ? std::atoi(pe) : 1;
+    static const int ahead = std::getenv("OIOBF_GEMV_L2AHEAD") ? std::atoi(std::getenv("OIOBF_GEMV_L2AHEAD")) : 1;
     TBF_CUDA(cudaLaunchKernelEx(&cfg, k_gemv_short<kShortRL>, cta_pair, d, static_cast<long long>(total_rows), row_begin,
                                 cores, x, y, ahead));
   } else if (nv == 1) {

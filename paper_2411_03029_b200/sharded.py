@@ -5,8 +5,9 @@ on both sides: the V/W IDs of its column multi-sets s and the cores of the
 pairs (t, s) it owns, the U/P IDs of its row multi-sets t.  Collectives:
 
 * construction: one all-reduce(max) of the local max rank per (side, level)
-  (level-synchronous r_est) and one sum-all-reduce of the
-  U-side middle skeletons (the row skeletons of every core);
+  (level-synchronous r_est), one sum-all-reduce of the U-side
+  middle ranks (the rows of every block) and one all-to-all of the U-side
+  middle skeletons (each rank receives those of the cores it generates);
 * apply: V/W levels + core GEMV on the s-owner, ONE all-to-all of the blocks
   G_{t,s} to the t-owner, P/U levels on the t-owner.
 
@@ -203,6 +204,15 @@ class TorchComm:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return t.cpu().numpy()
 
+    def alltoall_np(self, send: np.ndarray, send_counts, recv_counts) -> np.ndarray:
+        """Variable all-to-all of a 1-D integer array (counts in elements)."""
+        import torch
+        st = torch.from_numpy(np.ascontiguousarray(send)).to(self._dev())
+        rt = torch.empty(int(sum(recv_counts)), dtype=st.dtype, device=self._dev())
+        self.dist.all_to_all_single(rt, st, [int(c) for c in recv_counts], [int(c) for c in send_counts],
+                                    group=self.group)
+        return rt.cpu().numpy()
+
     def allgather_bytes(self, b: bytes) -> list:
         out = [None] * self.dist.get_world_size(self.group)
         self.dist.all_gather_object(out, b, group=self.group)
@@ -332,11 +342,45 @@ def construct(backend, rank: int, world: int, comm) -> ShardedButterfly:
     _, local_max = backend.umid_info()
     wpad = max(1, comm.allreduce_max_int(local_max))
     ranks, skel = backend.umid_export(wpad)
-    ranks_all = comm.allreduce_sum_np(ranks)
-    skel_all = comm.allreduce_sum_np(skel).astype(np.int32)
+    ranks_all = comm.allreduce_sum_np(ranks)  # every block's rows: the exchange layout needs all of them
+    skel_all = exchange_umid_skeletons(skel, rank, world, sb.nmid, sb.d, wpad, comm)
     backend.umid_import(ranks_all, skel_all, wpad)
     _finish_layout(sb, ranks_all)
     return sb
+
+
+def umid_slots(nmid: int, d: int, t_owner: int, s_owner: int, world: int) -> np.ndarray:
+    """U-side middle slots (Lc, t, nu = s, k) = (t nmid + s) d + k with t owned
+    by `t_owner` and s by `s_owner`, ascending."""
+    t = np.arange(t_owner, nmid, world, dtype=np.int64)
+    s = np.arange(s_owner, nmid, world, dtype=np.int64)
+    pairs = (t[:, None] * nmid + s[None, :]).reshape(-1)
+    return (pairs[:, None] * d + np.arange(d, dtype=np.int64)[None, :]).reshape(-1)
+
+
+def exchange_umid_skeletons(skel: np.ndarray, rank: int, world: int, nmid: int, d: int, wpad: int, comm) -> np.ndarray:
+    """The row skeletons a rank's cores need -- U-side middle slots (t, nu = s)
+    for every t and the s it owns -- from their builders (the owners of t) by
+    one variable all-to-all: rank q sends rank r the slots (t of q, s of r),
+    so every rank receives nmid^2 d wpad / world ints instead of the
+    all-reduce of the whole array.  Slots of other s stay zero (unused: the
+    cores of pairs with s not owned are generated elsewhere)."""
+    skel = np.asarray(skel, np.int32).reshape(-1, wpad)
+    send_parts, send_counts = [], []
+    for r in range(world):
+        part = skel[umid_slots(nmid, d, rank, r, world)].reshape(-1)
+        send_parts.append(part)
+        send_counts.append(part.size)
+    recv_counts = [umid_slots(nmid, d, q, rank, world).size * wpad for q in range(world)]
+    recv = comm.alltoall_np(np.concatenate(send_parts) if send_parts else np.zeros(0, np.int32), send_counts,
+                            recv_counts)
+    out = np.zeros_like(skel)
+    off = 0
+    for q in range(world):
+        sl = umid_slots(nmid, d, q, rank, world)
+        out[sl] = recv[off:off + sl.size * wpad].reshape(-1, wpad)
+        off += sl.size * wpad
+    return out.reshape(-1)
 
 
 def _finish_layout(sb: ShardedButterfly, ranks_all: np.ndarray):

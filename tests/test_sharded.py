@@ -251,3 +251,45 @@ def test_fused_exchange_equals_alltoall(world):
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["world"] == world and line["fused_equals_alltoall"], line
+
+
+def _umid_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2411_03029_b200.sharded import exchange_umid_skeletons
+        nmid, d, wpad = 8, 3, 4
+        nslots = nmid * nmid * d
+        full = (np.arange(nslots * wpad, dtype=np.int32) + 7).reshape(nslots, wpad)  # the whole truth
+        t_of = np.arange(nslots) // (nmid * d)
+        s_of = (np.arange(nslots) // d) % nmid
+        mine_built = full.copy()
+        mine_built[t_of % world != rank] = 0  # this rank built only its t (umid_export zeroes the rest)
+        got = exchange_umid_skeletons(mine_built.reshape(-1), rank, world, nmid, d, wpad, TorchComm()).reshape(nslots,
+                                                                                                            wpad)
+        need = s_of % world == rank
+        ok = bool(np.array_equal(got[need], full[need]) and not got[~need].any())
+        q.put(("ok", ok, 0.0))
+    except Exception as e:  # pragma: no cover
+        q.put(("err", repr(e), 0.0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_umid_skeleton_alltoall(world):
+    """The U-side middle skeletons reach exactly the ranks whose cores need them
+    (slots (t, nu = s) with s owned), over a real gloo all-to-all."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_umid_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+    assert all(r[0] == "ok" and r[1] for r in res), res

@@ -521,6 +521,27 @@ def extra_line(cfg, flush, sh, stream):
         prof = bf.profile_contract(Ft.data_ptr(), Gt.data_ptr(), reps=10, stream=sh)
         line["core_gemv"] = {"bytes": stats["core_bytes"], "ms_warm": prof["core_ms"],
                              "frac_warm": stats["core_bytes"] / (prof["core_ms"] / 1e3) / 1e9 / hbm}
+        # the same apply on block-floating-point cores (opt-in; the ZFP role of PAPER Alg. 2)
+        G64 = Gt.clone()
+        bf.set_core_format("bfp32")
+        for _ in range(3):
+            bf.contract_device(Ft.data_ptr(), Gt.data_ptr(), 1, sh)
+        torch.cuda.synchronize()
+        for a, b in evs:
+            flush.zero_()
+            a.record(stream)
+            bf.contract_device(Ft.data_ptr(), Gt.data_ptr(), 1, sh)
+            b.record(stream)
+        torch.cuda.synchronize()
+        bms = sum(a.elapsed_time(b) for a, b in evs) / len(evs)
+        bprof = bf.profile_contract(Ft.data_ptr(), Gt.data_ptr(), reps=10, stream=sh)
+        bst = bf.plan_stats()
+        line["compressed_cores"] = {
+            "format": "bfp32", "value": cfg.points / (bms / 1e3), "ms_per_step": bms, "core_bytes": bst["core_bytes"],
+            "core_ms": bprof["core_ms"],
+            "rel_diff_vs_fp64_apply": float(torch.linalg.norm(Gt - G64).item() / torch.linalg.norm(G64).item())}
+        bf.set_core_format("fp64")
+        del G64
     del bf
     torch.cuda.empty_cache()
     return line

@@ -244,6 +244,21 @@ __device__ __forceinline__ double2 green_from_coords(const KSpec& s, const doubl
   return make_double2(__ddiv_rn(cs, rho), __ddiv_rn(-sn, rho));
 }
 
+// Same entry with one reciprocal of rho instead of two divisions (each part
+// within 1 ulp of the divided one) -- the ID panels' generator, where the
+// entries only feed the pivoted QR (differences of this size are far below
+// the 1e-12 pivot tie rule); cores and dense check rows keep the divisions.
+__device__ __forceinline__ double2 green_from_coords_rcp(const KSpec& s, const double* xs, const double* ys) {
+  const double dx = __dsub_rn(xs[0], ys[0]), dy = __dsub_rn(xs[1], ys[1]), dz = __dsub_rn(xs[2], ys[2]);
+  const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  const double rho = __dsqrt_rn(r2);
+  const double ph = __dmul_rn(s.kappa, rho);
+  double sn, cs;
+  sincos(ph, &sn, &cs);
+  const double inv = __drcp_rn(rho);
+  return make_double2(__dmul_rn(cs, inv), -__dmul_rn(sn, inv));
+}
+
 // Radon 2D entry given sin / cos(2 pi x_p) of the two target coordinates
 // (hoistable: they depend on the target index only)
 __device__ __forceinline__ double2 radon2d_entry_sc(const KSpec& s, const int* i, const int* j, double s1, double c1v,

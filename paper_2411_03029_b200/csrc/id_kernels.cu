@@ -13,6 +13,7 @@
 //                  1e-12 tie rule of SURVEY App. A7, and id_from_qrcp
 //                  (id.cpp:87-120): T = R11^{-1} R12, sorted skeleton, interp.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -419,7 +420,9 @@ __device__ void absorb_panel(double2* __restrict__ R, double2* __restrict__ X, i
 
 // NT threads: 256, or 512 for wide IDs (w > 32, one CTA per SM by shared
 // memory) so each column step spreads over 16 warps
-template <int NT, int RPL, int MINB = (NT >= 512 ? 1 : (RPL >= 8 ? 2 : 3))>  // RPL: panel rows / 32
+// DIAG (timing diagnostics only, OIOBF_PANEL_DIAG): 1 = entry generation
+// alone (no absorb), 2 = absorb alone (cheap synthetic entries)
+template <int NT, int RPL, int MINB = (NT >= 512 ? 1 : (RPL >= 8 ? 2 : 3)), int DIAG = 0>  // RPL: panel rows / 32
 __global__ void __launch_bounds__(NT, MINB) k_panel(LevelDesc L, KSpec ks, const int* __restrict__ proxies,
                                                     const int* __restrict__ targets, const int* __restrict__ width,
                                                     double2* __restrict__ rpart) {
@@ -465,9 +468,18 @@ __global__ void __launch_bounds__(NT, MINB) k_panel(LevelDesc L, KSpec ks, const
   if (r_end > L.m) r_end = L.m;
   const int ncg = NT / pr;  // column groups per row
   const int my_row = threadIdx.x % pr, my_cg = threadIdx.x / pr;
+  double diag_acc = 0;
   for (i64 r0 = r_begin; r0 < r_end; r0 += pr) {
     const int nrows = static_cast<int>((r_end - r0) < pr ? (r_end - r0) : pr);
-    if (my_cg < ncg) {
+    if (DIAG == 2) {
+      for (int i = threadIdx.x; i < pr * w; i += NT) {
+        const int rr = i % pr, c = i / pr;
+        const unsigned hsh = static_cast<unsigned>((r0 + rr) * 2654435761u) ^ static_cast<unsigned>(c * 40503u + 17u);
+        X[rr + c * pr] = rr < nrows ? make_double2(static_cast<double>(hsh & 0xffff) * 1.5e-5 - 0.5,
+                                                   static_cast<double>(hsh >> 16) * 1.5e-5 - 0.5)
+                                    : make_double2(0, 0);
+      }
+    } else if (my_cg < ncg) {
       int ii[kMaxD], jj[kMaxD];
       const i64 row = r0 + my_row;
       const bool valid = my_row < nrows;
@@ -506,7 +518,7 @@ __global__ void __launch_bounds__(NT, MINB) k_panel(LevelDesc L, KSpec ks, const
               xc[p] = (tgt && p == q) ? v : xs[p];
               yc[p] = (!tgt && p == q) ? v : ys[p];
             }
-            e = green_from_coords(ks, xc, yc);
+            e = green_from_coords_rcp(ks, xc, yc);
           }
           X[my_row + c * pr] = e;
         }
@@ -552,9 +564,16 @@ __global__ void __launch_bounds__(NT, MINB) k_panel(LevelDesc L, KSpec ks, const
     // rows nrows..pr-1 of the panel were generated as zeros, so the
     // register-cached absorb folds all pr rows unconditionally (no per-element
     // row predicates; zero rows leave R unchanged)
-    if constexpr (RPL > 0) absorb_panel_r<NT / 32, RPL>(R, X, w, pr, pr, bc);
-    else absorb_panel<NT / 32>(R, X, w, nrows, pr, bc);
+    if constexpr (DIAG == 1) {
+      for (int i = threadIdx.x; i < pr * w; i += NT) diag_acc += X[i].x;
+      __syncthreads();
+    } else if constexpr (RPL > 0) {
+      absorb_panel_r<NT / 32, RPL>(R, X, w, pr, pr, bc);
+    } else {
+      absorb_panel<NT / 32>(R, X, w, nrows, pr, bc);
+    }
   }
+  if (DIAG == 1 && diag_acc == 12345.678) R[0].x += 1;  // keeps the generation live
   double2* out = rpart + (slot * L.nparts + part) * L.wmax * L.wmax;
   for (int i = threadIdx.x; i < w * w; i += NT) {  // unpack to w x w column-major
     const int r = i % w, c = i / w;
@@ -875,11 +894,12 @@ void launch_targets(const LevelDesc& L, const int* crank, const i64* cskel_off, 
   TBF_CUDA(cudaGetLastError());
 }
 
-template <int NT, int RPL, int MINB = (NT >= 512 ? 1 : (RPL >= 8 ? 2 : 3))>
+template <int NT, int RPL, int DIAG = 0, int MINB = (NT >= 512 ? 1 : (RPL >= 8 ? 2 : 3))>
 void launch_panel_t(const LevelDesc& L, const KSpec& ks, const int* proxies, const int* targets, const int* width,
                     double2* rpart, size_t smem, i64 grid, cudaStream_t st) {
-  TBF_CUDA(cudaFuncSetAttribute(k_panel<NT, RPL, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-  k_panel<NT, RPL, MINB><<<static_cast<unsigned>(grid), NT, smem, st>>>(L, ks, proxies, targets, width, rpart);
+  TBF_CUDA(cudaFuncSetAttribute(k_panel<NT, RPL, MINB, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kMaxDynSmem));
+  k_panel<NT, RPL, MINB, DIAG><<<static_cast<unsigned>(grid), NT, smem, st>>>(L, ks, proxies, targets, width, rpart);
 }
 
 // Panel rows and resident CTAs per SM for a level of width wmax.  The column
@@ -908,28 +928,57 @@ void panel_shape(i64 wmax, i64 psize, int* pr, int* ctas_per_sm) {
   *ctas_per_sm = 1;
 }
 
-void launch_panel(const LevelDesc& L, const KSpec& ks, const int* proxies, const int* targets, const int* width,
-                  double2* rpart, cudaStream_t st) {
+template <int DIAG>
+void launch_panel_mode(const LevelDesc& L, const KSpec& ks, const int* proxies, const int* targets,
+                       const int* width, double2* rpart, cudaStream_t st) {
   const size_t smem = panel_smem_bytes(L);
   const i64 grid = L.nslots * L.nparts;
   static const bool generic = std::getenv("OIOBF_PANEL_GENERIC") != nullptr;  // A/B switch
   if (L.wmax > 32) {
-    if (!generic && L.pr == 192) launch_panel_t<512, 6>(L, ks, proxies, targets, width, rpart, smem, grid, st);
-    else if (!generic && L.pr == 160) launch_panel_t<512, 5>(L, ks, proxies, targets, width, rpart, smem, grid, st);
-    else if (!generic && L.pr == 128) launch_panel_t<512, 4>(L, ks, proxies, targets, width, rpart, smem, grid, st);
-    else if (!generic && L.pr == 96) launch_panel_t<512, 3>(L, ks, proxies, targets, width, rpart, smem, grid, st);
-    else if (!generic && L.pr == 64) launch_panel_t<512, 2>(L, ks, proxies, targets, width, rpart, smem, grid, st);
-    else launch_panel_t<512, 0>(L, ks, proxies, targets, width, rpart, smem, grid, st);
+    if (!generic && L.pr == 192) launch_panel_t<512, 6, DIAG>(L, ks, proxies, targets, width, rpart, smem, grid, st);
+    else if (!generic && L.pr == 160) launch_panel_t<512, 5, DIAG>(L, ks, proxies, targets, width, rpart, smem, grid, st);
+    else if (!generic && L.pr == 128) launch_panel_t<512, 4, DIAG>(L, ks, proxies, targets, width, rpart, smem, grid, st);
+    else if (!generic && L.pr == 96) launch_panel_t<512, 3, DIAG>(L, ks, proxies, targets, width, rpart, smem, grid, st);
+    else if (!generic && L.pr == 64) launch_panel_t<512, 2, DIAG>(L, ks, proxies, targets, width, rpart, smem, grid, st);
+    else launch_panel_t<512, 0, DIAG>(L, ks, proxies, targets, width, rpart, smem, grid, st);
   } else {
     // (the register-cached absorb spills at the 3-CTA/SM budget of these CTAs)
     // register-cached absorb on 256-row panels at 2 CTAs/SM (128 registers,
     // one column update at a time): bit-identical to the generic absorb,
     // config 2 panel 20.4 -> 17.2 ms, config 3 unchanged
     static const int rc = std::getenv("OIOBF_PANEL_NARROW_RC") ? std::atoi(std::getenv("OIOBF_PANEL_NARROW_RC")) : 1;
-    if (rc && !generic && L.pr == 256) launch_panel_t<kThreads, 8>(L, ks, proxies, targets, width, rpart, smem, grid, st);
-    else launch_panel_t<kThreads, 0>(L, ks, proxies, targets, width, rpart, smem, grid, st);
+    if (rc && !generic && L.pr == 256) launch_panel_t<kThreads, 8, DIAG>(L, ks, proxies, targets, width, rpart, smem, grid, st);
+    else launch_panel_t<kThreads, 0, DIAG>(L, ks, proxies, targets, width, rpart, smem, grid, st);
   }
   TBF_CUDA(cudaGetLastError());
+}
+
+void launch_panel(const LevelDesc& L, const KSpec& ks, const int* proxies, const int* targets, const int* width,
+                  double2* rpart, cudaStream_t st) {
+  launch_panel_mode<0>(L, ks, proxies, targets, width, rpart, st);
+  static const bool diag = std::getenv("OIOBF_PANEL_DIAG") != nullptr;  // timing split (tools)
+  if (!diag) return;
+  cudaEvent_t e[4];
+  for (auto& x : e) TBF_CUDA(cudaEventCreate(&x));
+  double2* scratch = nullptr;
+  const size_t bytes = sizeof(double2) * static_cast<size_t>(L.nslots * L.nparts * L.wmax * L.wmax);
+  TBF_CUDA(cudaMallocAsync(&scratch, bytes, st));
+  TBF_CUDA(cudaEventRecord(e[0], st));
+  launch_panel_mode<0>(L, ks, proxies, targets, width, scratch, st);
+  TBF_CUDA(cudaEventRecord(e[1], st));
+  launch_panel_mode<1>(L, ks, proxies, targets, width, scratch, st);
+  TBF_CUDA(cudaEventRecord(e[2], st));
+  launch_panel_mode<2>(L, ks, proxies, targets, width, scratch, st);
+  TBF_CUDA(cudaEventRecord(e[3], st));
+  TBF_CUDA(cudaEventSynchronize(e[3]));
+  float t[3];
+  for (int i = 0; i < 3; ++i) TBF_CUDA(cudaEventElapsedTime(&t[i], e[i], e[i + 1]));
+  std::fprintf(stderr, "panel-diag side %d l %d nslots %lld w %lld pr %d nparts %lld m %lld: full %.3f gen %.3f absorb %.3f ms\n",
+               static_cast<int>(L.side), static_cast<int>(L.l), static_cast<long long>(L.nslots),
+               static_cast<long long>(L.wmax), L.pr, static_cast<long long>(L.nparts), static_cast<long long>(L.m),
+               t[0], t[1], t[2]);
+  TBF_CUDA(cudaFreeAsync(scratch, st));
+  for (auto& x : e) TBF_CUDA(cudaEventDestroy(x));
 }
 
 void launch_finish(const LevelDesc& L, double tol, double tie_eps, i64 max_rank, const double2* rpart,

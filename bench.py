@@ -557,7 +557,8 @@ def run_b200_sharded(args):
 
     import paper_2411_03029_b200 as tb
     from paper_2411_03029_b200 import _lib
-    from paper_2411_03029_b200.sharded import GpuShardBackend, PeerExchange, TorchComm, construct
+    from paper_2411_03029_b200.sharded import (GpuShardBackend, PeerExchange, TorchComm, balanced_owners, construct,
+                                                round_robin_owners)
 
     ws, rank, local = dist_env()
     verbose = os.environ.get("OIOBF_BENCH_VERBOSE") is not None
@@ -598,6 +599,47 @@ def run_b200_sharded(args):
     torch.cuda.synchronize()
     construct_s = time.perf_counter() - t0
     construct_s = allreduce_max(construct_s)
+
+    # Byte-balanced ownership: the core stage is HBM-bound and
+    # the core bytes per s follow the geometry (config 3, s % 8: heaviest rank
+    # 1.61x the mean), so the per-s core bytes of this first construction --
+    # summed over ranks, each knows its own s -- feed the LPT map and the
+    # operator is rebuilt with it (identical factors: the IDs do not depend on
+    # who builds them).  OIOBF_OWNERSHIP=round_robin keeps s % world.
+    def core_bytes_per_s(handle):
+        nm = sb.nmid
+        cr = np.zeros(nm * nm, np.int64)
+        cc = np.zeros(nm * nm, np.int64)
+        _lib.check(_lib.load().oiobf_tbf_export(handle, None, None, None, None, None, None, None, _lib.ptr(cr),
+                                                _lib.ptr(cc), None))
+        return 16 * (cr * cc).reshape(nm, nm).sum(axis=1)  # pair p = s * nmid + t; other ranks' pairs have cc = 0
+
+    def heaviest_over_mean(owner, w):
+        load = np.bincount(owner, weights=w, minlength=ws)
+        return float(load.max() / max(load.mean(), 1.0))
+    w_s = comm.allreduce_sum_np(core_bytes_per_s(be.h)).astype(np.float64)
+    rr_map = round_robin_owners(sb.nmid, ws)
+    owner = None
+    ownership = {"map": "round_robin (s % world)", "core_bytes_heaviest_over_mean": heaviest_over_mean(rr_map, w_s)}
+    if os.environ.get("OIOBF_OWNERSHIP", "balanced") != "round_robin":
+        bal = balanced_owners(w_s, ws)
+        if not np.array_equal(bal, rr_map):
+            owner = bal
+            del sb, be
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            be = GpuShardBackend(cfg.spec, cfg.L, cfg.tol, tb.ProxyStrategy(), cfg.seed, rank, ws)
+            sb = construct(be, rank, ws, comm, owner)
+            torch.cuda.synchronize()
+            ownership = {"map": "byte-balanced (LPT bin packing of the per-s core bytes measured by a first "
+                                "round-robin construction)",
+                         "core_bytes_heaviest_over_mean": heaviest_over_mean(bal, w_s),
+                         "round_robin_heaviest_over_mean": heaviest_over_mean(rr_map, w_s),
+                         "measuring_construction_s": construct_s}
+            construct_s = allreduce_max(time.perf_counter() - t0)
+            stage("rebuilt with the byte-balanced ownership map")
+    own_map = rr_map if owner is None else owner
 
     Fh = make_input(cfg, cfg.input_seed, args.nv)
     N = cfg.points * args.nv
@@ -660,7 +702,7 @@ def run_b200_sharded(args):
     pin_F = torch.from_numpy(np.ascontiguousarray(Fh.reshape(-1, order="F")).view(np.float64).copy()).pin_memory()
     pin_G = torch.empty_like(pin_F).pin_memory()
     e2e = []
-    n_own_s = sum(1 for o in range(sb.nmid) if o % ws == rank)
+    n_own_s = int(np.count_nonzero(own_map == rank))
 
     def copy_in():
         be.copy_owned(0, pin_F.data_ptr(), F.data_ptr(), args.nv, sh)
@@ -717,7 +759,8 @@ def run_b200_sharded(args):
             "data": "synthetic (seeded complex normal input; operator from the BASELINE formula)",
             "config": {"workload": cfg.name, "points": cfg.points, "tol": cfg.tol, "L": cfg.L, "nv": args.nv,
                        "l2": "flushed (256 MiB write) before every timed step",
-                       "parallelism": f"sharded x{ws}: middle multi-sets round-robin", "exchange": exchange},
+                       "parallelism": f"sharded x{ws} by middle multi-sets", "exchange": exchange},
+            "ownership": ownership,
             "e2e": {"value": N / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": 16 * N * n_own_s // sb.nmid, "d2h_bytes_per_step": 16 * N * n_own_s // sb.nmid,
                     "copies": "rank 0's owned sub-tensors F(s) in and G(t) out (oiobf_tbf_copy_owned; every rank "

@@ -2,8 +2,10 @@
 // (PAPER.md:502 -- the reference's distributed setting).
 //
 // Host orchestration in C++ over the C ABI, no Python: one library handle per
-// device (rank r of `devices.size()`), each owning the middle multi-sets with
-// index % world == r on both sides:
+// device (rank r of `devices.size()`), each owning the middle multi-sets o with
+// owner(o) == r on both sides -- o % world by default, or an ownership map
+// (`balanced_owners`: byte-balanced over the measured per-s core bytes;
+// `tbf_construct_sharded_balanced` measures and applies it):
 //   construction  per side and level, every rank builds its slots (one host
 //                 thread per distinct device), then r_est = max over ranks
 //                 (identical to the single-GPU r_est); the
@@ -34,8 +36,12 @@ namespace oiobf {
 
 namespace detail {
 
-inline bool owns_outer(std::int64_t outer, std::int64_t rank, std::int64_t world) {
-  return world <= 1 || outer % world == rank;
+inline std::int64_t owner_of(std::int64_t outer, std::int64_t world, const std::vector<std::int32_t>& owners) {
+  return owners.empty() ? outer % world : owners[static_cast<std::size_t>(outer)];
+}
+inline bool owns_outer(std::int64_t outer, std::int64_t rank, std::int64_t world,
+                       const std::vector<std::int32_t>& owners = {}) {
+  return world <= 1 || owner_of(outer, world, owners) == rank;
 }
 
 // run f(r) for every rank: concurrently (one host thread per rank) when the
@@ -101,7 +107,7 @@ struct ShardLayout {
 };
 
 inline ShardLayout shard_layout(const std::vector<std::int64_t>& R, std::int64_t nmid, std::int64_t rank,
-                                std::int64_t world) {
+                                std::int64_t world, const std::vector<std::int32_t>& owners = {}) {
   ShardLayout lay;
   lay.send_off.assign(static_cast<std::size_t>(nmid * nmid), -1);
   lay.recv_off.assign(static_cast<std::size_t>(nmid * nmid), -1);
@@ -111,9 +117,9 @@ inline ShardLayout shard_layout(const std::vector<std::int64_t>& R, std::int64_t
   for (std::int64_t q = 0; q < world; ++q) {
     const std::int64_t start = cur;
     for (std::int64_t t = 0; t < nmid; ++t) {
-      if (!detail::owns_outer(t, q, world)) continue;
+      if (!detail::owns_outer(t, q, world, owners)) continue;
       for (std::int64_t s = 0; s < nmid; ++s)
-        if (detail::owns_outer(s, rank, world)) {
+        if (detail::owns_outer(s, rank, world, owners)) {
           lay.send_off[static_cast<std::size_t>(t * nmid + s)] = cur;
           cur += R[static_cast<std::size_t>(t * nmid + s)];
         }
@@ -124,9 +130,9 @@ inline ShardLayout shard_layout(const std::vector<std::int64_t>& R, std::int64_t
   for (std::int64_t q = 0; q < world; ++q) {
     const std::int64_t start = cur;
     for (std::int64_t t = 0; t < nmid; ++t) {
-      if (!detail::owns_outer(t, rank, world)) continue;
+      if (!detail::owns_outer(t, rank, world, owners)) continue;
       for (std::int64_t s = 0; s < nmid; ++s)
-        if (detail::owns_outer(s, q, world)) {
+        if (detail::owns_outer(s, q, world, owners)) {
           lay.recv_off[static_cast<std::size_t>(t * nmid + s)] = cur;
           cur += R[static_cast<std::size_t>(t * nmid + s)];
         }
@@ -134,6 +140,34 @@ inline ShardLayout shard_layout(const std::vector<std::int64_t>& R, std::int64_t
     lay.recv_counts[static_cast<std::size_t>(q)] = cur - start;
   }
   return lay;
+}
+
+// Byte-balanced ownership map (sharded.py balanced_owners): longest-processing-
+// time bin packing of per-multi-set weights over `world` ranks with at most
+// ceil(n / world) multi-sets each; deterministic (ties to the lower index /
+// rank); the round-robin map when that is at least as good.
+inline std::vector<std::int32_t> balanced_owners(const std::vector<double>& w, std::int64_t world) {
+  const std::size_t n = w.size();
+  std::vector<std::int32_t> own(n, 0);
+  if (world <= 1) return own;
+  const std::size_t cap = (n + static_cast<std::size_t>(world) - 1) / static_cast<std::size_t>(world);
+  std::vector<std::size_t> order(n);
+  for (std::size_t i = 0; i < n; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](std::size_t a, std::size_t b) { return w[a] > w[b]; });
+  std::vector<double> load(static_cast<std::size_t>(world), 0.0), rr(static_cast<std::size_t>(world), 0.0);
+  std::vector<std::size_t> cnt(static_cast<std::size_t>(world), 0);
+  for (std::size_t i : order) {
+    std::size_t best = n;  // sentinel
+    for (std::size_t r = 0; r < static_cast<std::size_t>(world); ++r)
+      if (cnt[r] < cap && (best == n || load[r] < load[best])) best = r;
+    own[i] = static_cast<std::int32_t>(best);
+    load[best] += w[i];
+    ++cnt[best];
+  }
+  for (std::size_t i = 0; i < n; ++i) rr[i % static_cast<std::size_t>(world)] += w[i];
+  if (*std::max_element(rr.begin(), rr.end()) <= *std::max_element(load.begin(), load.end()))
+    for (std::size_t i = 0; i < n; ++i) own[i] = static_cast<std::int32_t>(i % static_cast<std::size_t>(world));
+  return own;
 }
 
 class ShardedTensorButterfly {
@@ -147,10 +181,32 @@ class ShardedTensorButterfly {
   oiobf_tbf* handle(std::size_t rank) const { return h_[rank].get(); }
   const ShardLayout& layout(std::size_t rank) const { return lay_[rank]; }
   const std::vector<std::int64_t>& block_rows() const { return R_; }
+  // ownership map of the middle multi-sets (empty: o % world)
+  const std::vector<std::int32_t>& owners() const { return owners_; }
+  std::int64_t owner_of(std::int64_t outer) const { return detail::owner_of(outer, world(), owners_); }
+  // core bytes read by the owner of each s (the weights of balanced_owners)
+  std::vector<double> core_bytes_per_s() const {
+    std::vector<double> w(static_cast<std::size_t>(nmid_), 0.0);
+    std::vector<std::int64_t> cr(static_cast<std::size_t>(nmid_ * nmid_)), cc(cr.size());
+    for (std::size_t r = 0; r < h_.size(); ++r) {
+      detail::check(oiobf_set_device(devices_[r]));
+      detail::check(oiobf_tbf_export(h_[r].get(), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                     cr.data(), cc.data(), nullptr));
+      for (std::int64_t s = 0; s < nmid_; ++s)
+        if (owner_of(s) == static_cast<std::int64_t>(r))
+          for (std::int64_t t = 0; t < nmid_; ++t) {  // pair p = s * nmid + t
+            const std::size_t p = static_cast<std::size_t>(s * nmid_ + t);
+            w[static_cast<std::size_t>(s)] += 16.0 * static_cast<double>(cr[p]) * static_cast<double>(cc[p]);
+          }
+    }
+    return w;
+  }
 
  private:
   friend ShardedTensorButterfly tbf_construct_sharded(const KernelEvaluator&, std::int64_t, double, const ProxyStrategy&,
-                                                      std::uint64_t, const std::vector<int>&);
+                                                      std::uint64_t, const std::vector<int>&,
+                                                      const std::vector<std::int32_t>&);
+  std::vector<std::int32_t> owners_;
   std::vector<int> devices_;
   KernelEvaluator eval_;
   std::int64_t L_ = 0, Lc_ = 0, nmid_ = 0;
@@ -159,10 +215,13 @@ class ShardedTensorButterfly {
   std::vector<ShardLayout> lay_;
 };
 
-// Alg. 1 over devices.size() GPUs (ranks in the order given).
+// Alg. 1 over devices.size() GPUs (ranks in the order given).  owners: the
+// ownership map of the middle multi-sets (entries in [0, devices.size())), or
+// empty for o % world.
 inline ShardedTensorButterfly tbf_construct_sharded(const KernelEvaluator& eval, std::int64_t L, double tol,
                                                     const ProxyStrategy& proxies, std::uint64_t seed,
-                                                    const std::vector<int>& devices) {
+                                                    const std::vector<int>& devices,
+                                                    const std::vector<std::int32_t>& owners = {}) {
   require(!devices.empty(), "tbf_construct_sharded: no devices");
   const oiobf_kernel_spec& spec = eval.device_spec();
   oiobf_proxy_strategy ps{};
@@ -183,7 +242,14 @@ inline ShardedTensorButterfly tbf_construct_sharded(const KernelEvaluator& eval,
     detail::check(oiobf_tbf_shard_begin(&spec, static_cast<int32_t>(L), tol, &ps, seed, static_cast<int32_t>(r),
                                         static_cast<int32_t>(world), &h));
     bf.h_[r] = std::shared_ptr<oiobf_tbf>(h, &oiobf_tbf_destroy);
+    if (!owners.empty()) {
+      std::int64_t hi[10];
+      detail::check(oiobf_tbf_info(h, hi));
+      require(static_cast<std::int64_t>(owners.size()) == hi[4], "tbf_construct_sharded: owners needs nmid entries");
+      detail::check(oiobf_tbf_shard_set_owners(h, owners.data()));
+    }
   }
+  bf.owners_ = owners;
   // levels, r_est level-synchronous across ranks (the max plays the all-reduce)
   std::vector<std::int64_t> local(devices.size());
   for (int side = 0; side < 2; ++side) {
@@ -229,12 +295,29 @@ inline ShardedTensorButterfly tbf_construct_sharded(const KernelEvaluator& eval,
   for (std::int64_t p = 0; p < nm * nm; ++p)
     for (std::int64_t k = 0; k < d; ++k) bf.R_[static_cast<std::size_t>(p)] *= ranks_all[static_cast<std::size_t>(p * d + k)];
   for (std::size_t r = 0; r < devices.size(); ++r) {
-    bf.lay_.push_back(shard_layout(bf.R_, nm, static_cast<std::int64_t>(r), world));
+    bf.lay_.push_back(shard_layout(bf.R_, nm, static_cast<std::int64_t>(r), world, owners));
     const ShardLayout& lay = bf.lay_.back();
     detail::check(oiobf_tbf_set_exchange(bf.h_[r].get(), lay.send_off.data(), lay.recv_off.data(), lay.send_total(),
                                          lay.recv_total()));
   }
   return bf;
+}
+
+// Byte-balanced sharded construction: a first construction with the default
+// map measures the core bytes of every s, a second one uses the LPT map of
+// those bytes (construction is deterministic and independent of the
+// ownership, so both build identical factors; the second costs one more
+// construction and pays off over repeated applies -- the core stage is
+// HBM-bound, config 3 at world 8: heaviest rank 1.61x -> 1.00x the mean).
+inline ShardedTensorButterfly tbf_construct_sharded_balanced(const KernelEvaluator& eval, std::int64_t L, double tol,
+                                                             const ProxyStrategy& proxies, std::uint64_t seed,
+                                                             const std::vector<int>& devices) {
+  std::vector<std::int32_t> owners;
+  {
+    const ShardedTensorButterfly first = tbf_construct_sharded(eval, L, tol, proxies, seed, devices);
+    owners = balanced_owners(first.core_bytes_per_s(), first.world());
+  }
+  return tbf_construct_sharded(eval, L, tol, proxies, seed, devices, owners);
 }
 
 // Alg. 2 over the ranks: G = K x F, F of shape (n_1..n_d[, n_v]).
@@ -296,7 +379,7 @@ inline DenseTensor tbf_contract(const ShardedTensorButterfly& bf, const DenseTen
   const std::int64_t mid = n / mpm;
   const std::int64_t N = F.size() / nv;
   for (std::int64_t t = 0; t < nmid; ++t) {
-    const auto& src = Gr[static_cast<std::size_t>(t % world)];
+    const auto& src = Gr[static_cast<std::size_t>(bf.owner_of(t))];
     std::int64_t base = 0, st = 1, rem = t;
     for (std::int64_t k = 0; k < d; ++k) {
       base += (rem % mpm) * mid * st;

@@ -208,8 +208,10 @@ int oiobf_dense_rows(const oiobf_kernel_spec* spec, const double* F, int64_t nv,
                      const int64_t* rows_flat, double* out);
 
 /* ---- sharded (multi-GPU) construction and apply, SURVEY §8(e) -------------
- * One process per GPU.  Rank r owns the middle multi-sets with index % world
- * == r on both sides: it builds the V/W IDs of its column multi-sets s, the
+ * One process per GPU.  Rank r owns the middle multi-sets o with owner(o) ==
+ * r on both sides -- o % world by default, or the map given to
+ * oiobf_tbf_shard_set_owners (byte-balanced ownership: the same map on every
+ * rank, set right after oiobf_tbf_shard_begin).  It builds the V/W IDs of its column multi-sets s, the
  * U/P IDs of its row multi-sets t, and the cores of the pairs (t, s) with s
  * owned.  The caller performs the collectives (torch.distributed / NCCL):
  *   1. oiobf_tbf_shard_begin, then for each side and level l = 0..Lc:
@@ -223,6 +225,8 @@ int oiobf_dense_rows(const oiobf_kernel_spec* spec, const double* F, int64_t nv,
  */
 int oiobf_tbf_shard_begin(const oiobf_kernel_spec* spec, int32_t L, double tol, const oiobf_proxy_strategy* proxies,
                           uint64_t seed, int32_t rank, int32_t world, oiobf_tbf** out);
+/* owners[o] in [0, world) for every middle multi-set o (nmid entries); before the first level */
+int oiobf_tbf_shard_set_owners(oiobf_tbf* h, const int32_t* owners);
 int oiobf_tbf_shard_level(oiobf_tbf* h, int32_t side, int32_t level, int64_t r_est, int64_t* local_max_rank);
 int oiobf_tbf_umid_info(oiobf_tbf* h, int64_t out[2]);
 int oiobf_tbf_umid_export(oiobf_tbf* h, int64_t* ranks, int32_t* skel, int64_t wpad);

@@ -719,6 +719,7 @@ Tensor mode_product_blockdiag(const Tensor& t, int mode /*0-based*/, const std::
 // multi-sets t, blocks read at recv_off[t*nmid+s]*nv.  phase 0 = everything.
 struct ShardIO {
   int phase = 0, rank = 0, world = 1;
+  const int* owner = nullptr;  // ownership map of the middle multi-sets (null: index % world)
   Cx* send = nullptr;
   const i64* send_off = nullptr;
   const Cx* recv = nullptr;
@@ -727,7 +728,10 @@ struct ShardIO {
 
 void tbf_contract(const TBF& b, const Cx* F, Cx* G, i64 nv, int nthreads, const ShardIO* io = nullptr) {
   const int phase = io ? io->phase : 0;
-  auto own = [&](i64 outer) { return !io || io->world <= 1 || outer % io->world == io->rank; };
+  auto own = [&](i64 outer) {
+    if (!io || io->world <= 1) return true;
+    return (io->owner ? static_cast<i64>(io->owner[outer]) : outer % io->world) == io->rank;
+  };
   const int d = b.spec.d;
   const i64 n = b.spec.n;
   const i64 mpm = ipow(2, b.Lc);
@@ -1296,9 +1300,20 @@ int oracle_tbf_contract(void* h, const double* F, double* G, i64 nv, int nthread
 }
 
 // Sharded apply phases (test backend for paper_2411_03029_b200/sharded.py).
+int oracle_tbf_contract_phase_owned(void* h, int phase, int rank, int world, const int* owner, const double* in,
+                                    double* out, const i64* send_off, const i64* recv_off, i64 send_elems,
+                                    i64 recv_elems, i64 nv, int nthreads);
 int oracle_tbf_contract_phase(void* h, int phase, int rank, int world, const double* in, double* out,
                               const i64* send_off, const i64* recv_off, i64 send_elems, i64 recv_elems, i64 nv,
                               int nthreads) {
+  return oracle_tbf_contract_phase_owned(h, phase, rank, world, nullptr, in, out, send_off, recv_off, send_elems,
+                                         recv_elems, nv, nthreads);
+}
+
+// owner: ownership map of the middle multi-sets (nmid ints in [0, world)), or null for index % world
+int oracle_tbf_contract_phase_owned(void* h, int phase, int rank, int world, const int* owner, const double* in,
+                                    double* out, const i64* send_off, const i64* recv_off, i64 send_elems,
+                                    i64 recv_elems, i64 nv, int nthreads) {
   GUARD_BEGIN
   const TBF& b = *static_cast<TBF*>(h);
   const i64 N = ipow(b.spec.n, b.spec.d) * nv;
@@ -1306,6 +1321,7 @@ int oracle_tbf_contract_phase(void* h, int phase, int rank, int world, const dou
   io.phase = phase;
   io.rank = rank;
   io.world = world;
+  io.owner = owner;
   io.send_off = send_off;
   io.recv_off = recv_off;
   if (phase == 1) {

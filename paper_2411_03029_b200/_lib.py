@@ -41,7 +41,7 @@ EXPORTS = [
     "oiobf_tbf_construct", "oiobf_tbf_destroy", "oiobf_tbf_contract", "oiobf_tbf_contract_device",
     "oiobf_tbf_memory", "oiobf_tbf_info", "oiobf_tbf_export", "oiobf_tbf_timings", "oiobf_tbf_plan_stats",
     "oiobf_tbf_profile_contract", "oiobf_dense_rows", "oiobf_tbf_check_finite",
-    "oiobf_tbf_shard_begin", "oiobf_tbf_shard_level", "oiobf_tbf_umid_info", "oiobf_tbf_umid_export",
+    "oiobf_tbf_shard_begin", "oiobf_tbf_shard_set_owners", "oiobf_tbf_shard_level", "oiobf_tbf_umid_info", "oiobf_tbf_umid_export",
     "oiobf_tbf_umid_import", "oiobf_tbf_set_exchange", "oiobf_tbf_contract_phase",
     "oiobf_tbf_set_apply_engine", "oiobf_tbf_apply_engine", "oiobf_tbf_save", "oiobf_tbf_load",
     "oiobf_tbf_contract_async", "oiobf_tbf_set_peer_exchange", "oiobf_device_alloc", "oiobf_device_free",

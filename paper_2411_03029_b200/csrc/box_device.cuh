@@ -160,6 +160,92 @@ __device__ __forceinline__ void first_mode_global(const BoxDesc& D, int d, const
   }
 }
 
+__device__ __forceinline__ void box_mma_f64(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// mode d-1 streamed from global memory on the FP64 tensor core (ein_f <= 16):
+//   T(i, col) = sum_z M(i, z) X(col, z)   as m8n8k4 MMAs with
+//   A = M (rows i: this CTA's <= 8 output rows, zero beyond; k = z),
+//   B = 8 input columns of the box (lane l: column 8 tile + l / 4, z = 4 ks + l % 4:
+//       8 consecutive columns are 128 contiguous bytes per z),
+//   D = T(l / 4, 8 tile + 2 (l % 4) + {0, 1});  complex = four real MMAs.
+// A warp takes two column tiles per step and has all their loads (8 per lane)
+// in flight before the first MMA.  Against the CUDA-core loop this is 16
+// MMAs instead of ~100 DFMAs + their shared-memory operand loads per tile
+// (config 3 first V level: ncu issue slots 40% busy with the FP64 pipe at 31%).
+__device__ __forceinline__ void first_mode_global_mma(const BoxDesc& D, int d, const double2* in,
+                                                      const double2* __restrict__ Mf, double2* __restrict__ t0,
+                                                      int A, int Rs, int ein_f, int nv) {
+  const int f = d - 1;
+  const int R = Rs * nv;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = box_nt() >> 5;
+  const int li = lane >> 2, lk = lane & 3;
+  const long long sf = D.in_stride[f];
+  double mr[4], mi[4], mn[4];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int z = 4 * ks + lk;
+    double2 m = make_double2(0, 0);
+    if (li < A && z < ein_f) m = Mf[z * A + li];
+    mr[ks] = m.x;
+    mi[ks] = m.y;
+    mn[ks] = -m.y;
+  }
+  const int ntiles = (R + 7) >> 3;
+#pragma unroll 1
+  for (int t = warp * 2; t < ntiles; t += nw * 2) {
+    double2 xv[2][4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int col = (t + u) * 8 + li;
+      const bool okc = col < R;
+      long long addr = 0;
+      if (okc) {
+        const int v = qdiv(col, Rs);
+        int rem = col - v * Rs;
+        addr = D.in_off + static_cast<long long>(v) * D.in_stride[d];
+        for (int p = 0; p < f; ++p) {
+          const int q = qdiv(rem, D.ein[p]);
+          addr += static_cast<long long>(rem - q * D.ein[p]) * D.in_stride[p];
+          rem = q;
+        }
+      }
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const int z = 4 * ks + lk;
+        xv[u][ks] = okc && z < ein_f ? __ldcs(reinterpret_cast<const double2*>(in + addr + z * sf))
+                                     : make_double2(0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      double cr0 = 0, cr1 = 0, ci0 = 0, ci1 = 0;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+        if (4 * ks < ein_f) {
+          box_mma_f64(cr0, cr1, mr[ks], xv[u][ks].x);
+          box_mma_f64(ci0, ci1, mr[ks], xv[u][ks].y);
+          box_mma_f64(cr0, cr1, mn[ks], xv[u][ks].y);
+          box_mma_f64(ci0, ci1, mi[ks], xv[u][ks].x);
+        }
+      if (li < A) {
+        const int c0 = (t + u) * 8 + 2 * lk;
+        if (c0 < R) {
+          const int v = qdiv(c0, Rs);
+          t0[c0 - v * Rs + Rs * (li + A * v)] = make_double2(cr0, ci0);
+        }
+        if (c0 + 1 < R) {
+          const int v = qdiv(c0 + 1, Rs);
+          t0[c0 + 1 - v * Rs + Rs * (li + A * v)] = make_double2(cr1, ci1);
+        }
+      }
+    }
+  }
+}
+
 // middle mode k: dst(b, a, c) = sum_x M(a, x) src(b, x, c), 4 output rows per task
 __device__ __forceinline__ void middle_mode(const double2* __restrict__ src, double2* __restrict__ dst,
                                             const double2* __restrict__ Mk, int B, int ein, int eo, int Cc) {
@@ -346,6 +432,8 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
       if (info.amax <= 2) first_mode_smem<2>(xs, Mf, t0, A, Rs, ein_f, nv);
       else if (info.amax <= 4) first_mode_smem<4>(xs, Mf, t0, A, Rs, ein_f, nv);
       else first_mode_smem<8>(xs, Mf, t0, A, Rs, ein_f, nv);
+    } else if (info.mma && ein_f <= 16) {
+      first_mode_global_mma(D, d, in, Mf, t0, A, Rs, ein_f, nv);
     } else {
       first_mode_global<8, LD>(D, d, in, Mf, t0, A, Rs, ein_f, nv);
     }

@@ -128,7 +128,8 @@ struct BoxLaunchInfo {
   int stage;                 // 1: stage the whole input box in shared memory (cp.async)
   int smem_mat, smem_in, smem_t;  // elements: factors, staged input, intermediate buffer t0
   int smem_t1;                    // elements of intermediate buffer t1 (odd middle modes, staging table)
-  int nt, pad_;                   // CTA size (256, or 128 for small boxes at up to 6 CTAs per SM)
+  int nt;                         // CTA size (256, or 128 for small boxes at up to 6 CTAs per SM)
+  int mma;                        // 1: FP64 tensor-core phases (unstaged mode d-1 with <= 16 input rows)
 };
 void launch_box(i64 nitems, const BoxDesc* descs, const BoxLaunchInfo& info, const double2* mats,
                 const double2* in, double2* out, cudaStream_t st);

@@ -39,12 +39,15 @@ struct LevelDesc {
   // children (level l-1) for l >= 1
   i64 c_nin, c_nj;
   // sharded construction: this rank builds only slots whose outer middle
-  // multi-set satisfies outer % world == rank (others get width 0 -> rank 0)
+  // multi-set belongs to it (others get width 0 -> rank 0): owner[outer] ==
+  // rank when a device ownership map is set, outer % world == rank otherwise
   int rank, world;
+  const int* owner;
 };
 
-__host__ __device__ inline bool owns_outer(const LevelDesc& L, i64 outer) {
-  return L.world <= 1 || (outer % L.world) == L.rank;
+__device__ inline bool owns_outer(const LevelDesc& L, i64 outer) {
+  if (L.world <= 1) return true;
+  return (L.owner ? L.owner[outer] : static_cast<int>(outer % L.world)) == L.rank;
 }
 
 struct SlotPos {

@@ -553,10 +553,16 @@ struct oiobf_tbf {
   u64 seed = 0;
   int device = 0;
   cudaStream_t stream = nullptr;
-  // sharding: this rank owns middle multi-sets with
-  // index % world == rank on both sides
+  // sharding: this rank owns the middle multi-sets o with
+  // owner_of(o) == rank on both sides -- o % world by default, or the map set
+  // by oiobf_tbf_shard_set_owners (byte-balanced ownership)
   int rank = 0, world = 1;
-  bool owns(i64 outer) const { return world <= 1 || outer % world == rank; }
+  std::vector<int> owner;  // empty: round-robin
+  DevBuf<int> d_owner;
+  int owner_of(i64 outer) const {
+    return owner.empty() ? static_cast<int>(outer % world) : owner[static_cast<size_t>(outer)];
+  }
+  bool owns(i64 outer) const { return world <= 1 || owner_of(outer) == rank; }
   // U-side middle-level (l = Lc) ranks / skeletons of ALL t (gathered from the
   // other ranks) -- the row skeletons of the cores of the owned pairs (t, s)
   std::vector<int> umid_rank;
@@ -686,6 +692,7 @@ LevelDesc make_level(const oiobf_tbf& b, int sd, int l, i64 r_est, i64 wmax) {
   panel_shape(wmax, L.psize, &L.pr, &cps);
   L.rank = b.rank;
   L.world = b.world;
+  L.owner = b.owner.empty() ? nullptr : b.d_owner.p;
   // >= 4 waves of resident CTAs, each CTA >= 4 panels
   const i64 target_ctas = static_cast<i64>(device_sms()) * cps * 4;
   const i64 owned = (L.nslots + b.world - 1) / b.world;
@@ -1231,6 +1238,10 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
     bl.info.amax = bucket(amax_rows);
     bl.info.stage = stage ? 1 : 0;
     bl.info.nt = box_nt;
+    {  // FP64 tensor-core phases (OIOBF_BOX_MMA=0: the CUDA-core loops)
+      const char* e = std::getenv("OIOBF_BOX_MMA");
+      bl.info.mma = e && std::strcmp(e, "0") == 0 ? 0 : 1;
+    }
     bl.info.smem_mat = static_cast<int>(smem_mat);
     bl.info.smem_in = static_cast<int>(smem_in);
     bl.info.smem_t = static_cast<int>(smem_t);
@@ -1441,7 +1452,7 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
         // receive buffer of the same parity (the phase-1 output pointer)
         const i64 po = b.peer_off[static_cast<size_t>(t * b.nmid + s)];
         require(po >= 0, "sharded contract: missing peer offset");
-        const int q = static_cast<int>(t % b.world);
+        const int q = b.owner_of(t);
         const u64 mine_base = b.peer_base[static_cast<size_t>(parity * b.world + b.rank)];
         const u64 dest_base = b.peer_base[static_cast<size_t>(parity * b.world + q)];
         const i64 delta = static_cast<i64>(dest_base - mine_base);
@@ -2728,6 +2739,22 @@ int oiobf_tbf_shard_begin(const oiobf_kernel_spec* spec, int32_t L, double tol, 
   CAPI_BEGIN
   require(spec && proxies && out, "tbf_shard_begin: null argument");
   *out = construct_begin(*spec, L, tol, *proxies, seed, rank, world).release();
+  CAPI_END
+}
+
+int oiobf_tbf_shard_set_owners(oiobf_tbf* h, const int32_t* owners) {
+  CAPI_BEGIN
+  require(h && owners, "tbf_shard_set_owners: null argument");
+  require(h->r_est[0].empty() && h->r_est[1].empty(), "tbf_shard_set_owners: call before the first level is built");
+  std::vector<int> own(static_cast<size_t>(h->nmid));
+  for (i64 o = 0; o < h->nmid; ++o) {
+    require(owners[o] >= 0 && owners[o] < h->world, "tbf_shard_set_owners: owner out of range");
+    own[static_cast<size_t>(o)] = owners[o];
+  }
+  TBF_CUDA(cudaSetDevice(h->device));
+  h->d_owner = to_device(own, h->stream);
+  TBF_CUDA(cudaStreamSynchronize(h->stream));
+  h->owner = std::move(own);
   CAPI_END
 }
 

@@ -1,7 +1,8 @@
 """Sharded (multi-GPU) tensor butterfly — SURVEY.md §8(e), DESIGN.md §7.
 
-One process per GPU.  Rank r owns the middle multi-sets with index % world == r
-on both sides: the V/W IDs of its column multi-sets s and the cores of the
+One process per GPU.  Rank r owns the middle multi-sets o with owner(o) == r on
+both sides (o % world by default, or an explicit ownership map -- e.g. the
+byte-balanced `balanced_owners` of the measured per-s core bytes): the V/W IDs of its column multi-sets s and the cores of the
 pairs (t, s) it owns, the U/P IDs of its row multi-sets t.  Collectives:
 
 * construction: one all-reduce(max) of the local max rank per (side, level)
@@ -29,8 +30,52 @@ from . import _lib
 from .configs import KernelSpec
 
 
-def owns(outer: int, rank: int, world: int) -> bool:
-    return world <= 1 or outer % world == rank
+def owns(outer: int, rank: int, world: int, owner=None) -> bool:
+    if world <= 1:
+        return True
+    return (outer % world if owner is None else int(owner[outer])) == rank
+
+
+def _owner_map(nmid: int, world: int, owner=None) -> np.ndarray:
+    if owner is None:
+        return round_robin_owners(nmid, world)
+    owner = np.ascontiguousarray(owner, np.int32)
+    if owner.shape != (nmid,) or owner.min(initial=0) < 0 or owner.max(initial=0) >= max(world, 1):
+        raise ValueError("ownership map: need nmid entries in [0, world)")
+    return owner
+
+
+def round_robin_owners(nmid: int, world: int) -> np.ndarray:
+    """The default ownership map: middle multi-set i belongs to rank i % world."""
+    return (np.arange(nmid, dtype=np.int64) % max(world, 1)).astype(np.int32)
+
+
+def balanced_owners(weights, world: int) -> np.ndarray:
+    """Byte-balanced ownership map: longest-processing-time bin
+    packing of per-multi-set weights (e.g. the core bytes of each s) over
+    `world` ranks, every rank getting the same NUMBER of multi-sets where
+    world divides it (the input / output slabs stay even).  Deterministic:
+    ties go to the lower index / lower rank, so every rank computes the same
+    map from the same weights; the round-robin map is returned when it is at
+    least as good (tiny nmid)."""
+    w = np.asarray(weights, np.float64)
+    n = w.size
+    if world <= 1:
+        return np.zeros(n, np.int32)
+    cap = -(-n // world)
+    order = sorted(range(n), key=lambda i: (-w[i], i))
+    load = [0.0] * world
+    cnt = [0] * world
+    own = np.zeros(n, np.int32)
+    for i in order:
+        q = min((r for r in range(world) if cnt[r] < cap), key=lambda r: (load[r], r))
+        own[i] = q
+        load[q] += w[i]
+        cnt[q] += 1
+    rr = round_robin_owners(n, world)  # never worse than the default map
+    if np.bincount(rr, weights=w, minlength=world).max() <= max(load):
+        return rr
+    return own
 
 
 @dataclass
@@ -41,40 +86,40 @@ class Layout:
     recv_counts: np.ndarray  # int64[world], elements per source
 
 
-def exchange_layout(R: np.ndarray, rank: int, world: int) -> Layout:
+def exchange_layout(R: np.ndarray, rank: int, world: int, owner=None) -> Layout:
     """R[t, s] = rows of G_{t,s} (prod of the U-side middle ranks).  The send
     buffer holds, per destination q (ascending), the blocks (t owned by q,
     s owned by me) in (t, s) order; the receive buffer holds, per source q, the
     blocks (t owned by me, s owned by q) in the same (t, s) order, so sender and
-    receiver agree without any extra metadata."""
+    receiver agree without any extra metadata.  `owner`: the ownership map
+    (None = round-robin)."""
+    R = np.asarray(R, np.int64)
     nmid = R.shape[0]
-    send_off = np.full(nmid * nmid, -1, np.int64)
-    recv_off = np.full(nmid * nmid, -1, np.int64)
+    own = _owner_map(nmid, world, owner)
+    send_off = np.full((nmid, nmid), -1, np.int64)
+    recv_off = np.full((nmid, nmid), -1, np.int64)
     send_counts = np.zeros(world, np.int64)
     recv_counts = np.zeros(world, np.int64)
+    mine = np.flatnonzero(own == rank)
     cur = 0
     for q in range(world):
-        start = cur
-        for t in range(nmid):
-            if not owns(t, q, world):
-                continue
-            for s in range(nmid):
-                if owns(s, rank, world):
-                    send_off[t * nmid + s] = cur
-                    cur += int(R[t, s])
-        send_counts[q] = cur - start
+        theirs = np.flatnonzero(own == q)
+        # send: (t of q, s of me), t-major
+        blk = R[np.ix_(theirs, mine)]
+        flat = blk.reshape(-1)
+        send_off[np.ix_(theirs, mine)] = (cur + np.cumsum(flat) - flat).reshape(blk.shape)
+        send_counts[q] = int(flat.sum())
+        cur += send_counts[q]
     cur = 0
     for q in range(world):
-        start = cur
-        for t in range(nmid):
-            if not owns(t, rank, world):
-                continue
-            for s in range(nmid):
-                if owns(s, q, world):
-                    recv_off[t * nmid + s] = cur
-                    cur += int(R[t, s])
-        recv_counts[q] = cur - start
-    return Layout(send_off, recv_off, send_counts, recv_counts)
+        theirs = np.flatnonzero(own == q)
+        # receive: (t of me, s of q), t-major
+        blk = R[np.ix_(mine, theirs)]
+        flat = blk.reshape(-1)
+        recv_off[np.ix_(mine, theirs)] = (cur + np.cumsum(flat) - flat).reshape(blk.shape)
+        recv_counts[q] = int(flat.sum())
+        cur += recv_counts[q]
+    return Layout(send_off.reshape(-1), recv_off.reshape(-1), send_counts, recv_counts)
 
 
 class GpuShardBackend:
@@ -98,6 +143,11 @@ class GpuShardBackend:
             _lib.load().oiobf_tbf_destroy(self.h)
         except Exception:
             pass
+
+    def set_owners(self, owner: np.ndarray):
+        """Ownership map of the middle multi-sets (before the first level)."""
+        owner = np.ascontiguousarray(owner, np.int32)
+        _lib.check(_lib.load().oiobf_tbf_shard_set_owners(self.h, owner))
 
     def level(self, side: int, l: int, r_est: int) -> int:
         out = C.c_int64()
@@ -143,6 +193,7 @@ def _declare(Lb):
     Lb.oiobf_tbf_shard_begin.argtypes = [C.POINTER(_lib.KernelSpecC), C.c_int32, C.c_double,
                                          C.POINTER(_lib.ProxyStrategyC), C.c_uint64, C.c_int32, C.c_int32,
                                          C.POINTER(C.c_void_p)]
+    Lb.oiobf_tbf_shard_set_owners.argtypes = [C.c_void_p, i32p]
     Lb.oiobf_tbf_shard_level.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.POINTER(C.c_int64)]
     Lb.oiobf_tbf_umid_info.argtypes = [C.c_void_p, i64p]
     Lb.oiobf_tbf_umid_export.argtypes = [C.c_void_p, i64p, i32p, C.c_int64]
@@ -163,11 +214,17 @@ class ShardedButterfly:
     """Step-wise sharded construction/apply for one rank.  Collectives are the
     caller's (`construct` / `contract` below do them with a Comm)."""
 
-    def __init__(self, backend, rank: int, world: int):
+    def __init__(self, backend, rank: int, world: int, owner=None):
         self.be, self.rank, self.world = backend, rank, world
         self.nmid, self.d, self.Lc = backend.nmid, backend.d, backend.Lc
         self.layout: Layout | None = None
         self.R = None
+        # ownership map of the middle multi-sets (None = round-robin); a map
+        # must be the same on every rank and reaches the backend before the
+        # first level is built
+        self.owner = None if owner is None else _owner_map(self.nmid, world, owner)
+        if self.owner is not None:
+            backend.set_owners(self.owner)
 
 
 def on_stream(stream: int, device=None):
@@ -254,22 +311,20 @@ class TorchComm:
             self.dist.all_to_all_single(recv, send, rs, ss, group=self.group)
 
 
-def peer_offsets(R: np.ndarray, rank: int, world: int) -> np.ndarray:
+def peer_offsets(R: np.ndarray, rank: int, world: int, owner=None) -> np.ndarray:
     """For the fused exchange: element offset (n_v = 1) of every block (t, s)
     this rank produces (s owned) inside the receive buffer of its destination
     (the owner of t) -- the destination's own `exchange_layout` receive
     offsets, so sender and receiver agree without exchanging metadata."""
     nmid = R.shape[0]
-    off = np.full(nmid * nmid, -1, np.int64)
+    own = _owner_map(nmid, world, owner)
+    mine = np.flatnonzero(own == rank)
+    off = np.full((nmid, nmid), -1, np.int64)
     for q in range(world):
-        rq = exchange_layout(R, q, world).recv_off
-        for t in range(nmid):
-            if not owns(t, q, world):
-                continue
-            for s in range(nmid):
-                if owns(s, rank, world):
-                    off[t * nmid + s] = rq[t * nmid + s]
-    return off
+        rq = exchange_layout(R, q, world, owner).recv_off.reshape(nmid, nmid)
+        theirs = np.flatnonzero(own == q)
+        off[np.ix_(theirs, mine)] = rq[np.ix_(theirs, mine)]
+    return off.reshape(-1)
 
 
 class PeerExchange:
@@ -308,7 +363,7 @@ class PeerExchange:
                     _lib.check(Lb.oiobf_ipc_open(allh[q][64 * par: 64 * (par + 1)], C.byref(p)))
                     self.opened.append(int(p.value))
                     base[par * world + q] = int(p.value)
-        off = np.ascontiguousarray(peer_offsets(sb.R, rank, world), np.int64)
+        off = np.ascontiguousarray(peer_offsets(sb.R, rank, world, sb.owner), np.int64)
         _lib.check(Lb.oiobf_tbf_set_peer_exchange(sb.be.h, C.c_void_p(off.ctypes.data), C.c_void_p(base.ctypes.data),
                                                   world, nv_max))
         self.parity = 0
@@ -331,9 +386,12 @@ class PeerExchange:
         self.opened, self.own = [], []
 
 
-def construct(backend, rank: int, world: int, comm) -> ShardedButterfly:
-    """Sharded construction with real collectives (one rank per process)."""
-    sb = ShardedButterfly(backend, rank, world)
+def construct(backend, rank: int, world: int, comm, owner=None) -> ShardedButterfly:
+    """Sharded construction with real collectives (one rank per process).
+    `owner`: ownership map of the middle multi-sets, identical on every rank
+    (None = round-robin; `balanced_owners` of measured per-s core bytes for a
+    byte-balanced apply, see `core_bytes_per_s`)."""
+    sb = ShardedButterfly(backend, rank, world, owner)
     for side in (0, 1):
         r_est = 8
         for l in range(sb.Lc + 1):
@@ -343,22 +401,24 @@ def construct(backend, rank: int, world: int, comm) -> ShardedButterfly:
     wpad = max(1, comm.allreduce_max_int(local_max))
     ranks, skel = backend.umid_export(wpad)
     ranks_all = comm.allreduce_sum_np(ranks)  # every block's rows: the exchange layout needs all of them
-    skel_all = exchange_umid_skeletons(skel, rank, world, sb.nmid, sb.d, wpad, comm)
+    skel_all = exchange_umid_skeletons(skel, rank, world, sb.nmid, sb.d, wpad, comm, sb.owner)
     backend.umid_import(ranks_all, skel_all, wpad)
     _finish_layout(sb, ranks_all)
     return sb
 
 
-def umid_slots(nmid: int, d: int, t_owner: int, s_owner: int, world: int) -> np.ndarray:
+def umid_slots(nmid: int, d: int, t_owner: int, s_owner: int, world: int, owner=None) -> np.ndarray:
     """U-side middle slots (Lc, t, nu = s, k) = (t nmid + s) d + k with t owned
     by `t_owner` and s by `s_owner`, ascending."""
-    t = np.arange(t_owner, nmid, world, dtype=np.int64)
-    s = np.arange(s_owner, nmid, world, dtype=np.int64)
+    own = _owner_map(nmid, world, owner)
+    t = np.flatnonzero(own == t_owner).astype(np.int64)
+    s = np.flatnonzero(own == s_owner).astype(np.int64)
     pairs = (t[:, None] * nmid + s[None, :]).reshape(-1)
     return (pairs[:, None] * d + np.arange(d, dtype=np.int64)[None, :]).reshape(-1)
 
 
-def exchange_umid_skeletons(skel: np.ndarray, rank: int, world: int, nmid: int, d: int, wpad: int, comm) -> np.ndarray:
+def exchange_umid_skeletons(skel: np.ndarray, rank: int, world: int, nmid: int, d: int, wpad: int, comm,
+                            owner=None) -> np.ndarray:
     """The row skeletons a rank's cores need -- U-side middle slots (t, nu = s)
     for every t and the s it owns -- from their builders (the owners of t) by
     one variable all-to-all: rank q sends rank r the slots (t of q, s of r),
@@ -368,16 +428,16 @@ def exchange_umid_skeletons(skel: np.ndarray, rank: int, world: int, nmid: int, 
     skel = np.asarray(skel, np.int32).reshape(-1, wpad)
     send_parts, send_counts = [], []
     for r in range(world):
-        part = skel[umid_slots(nmid, d, rank, r, world)].reshape(-1)
+        part = skel[umid_slots(nmid, d, rank, r, world, owner)].reshape(-1)
         send_parts.append(part)
         send_counts.append(part.size)
-    recv_counts = [umid_slots(nmid, d, q, rank, world).size * wpad for q in range(world)]
+    recv_counts = [umid_slots(nmid, d, q, rank, world, owner).size * wpad for q in range(world)]
     recv = comm.alltoall_np(np.concatenate(send_parts) if send_parts else np.zeros(0, np.int32), send_counts,
                             recv_counts)
     out = np.zeros_like(skel)
     off = 0
     for q in range(world):
-        sl = umid_slots(nmid, d, q, rank, world)
+        sl = umid_slots(nmid, d, q, rank, world, owner)
         out[sl] = recv[off:off + sl.size * wpad].reshape(-1, wpad)
         off += sl.size * wpad
     return out.reshape(-1)
@@ -387,7 +447,7 @@ def _finish_layout(sb: ShardedButterfly, ranks_all: np.ndarray):
     nmid, d = sb.nmid, sb.d
     r = ranks_all.reshape(nmid, nmid, d)  # [t, s, k]  (U slot (Lc, t, nu=s, k))
     sb.R = np.prod(r, axis=2)
-    sb.layout = exchange_layout(sb.R, sb.rank, sb.world)
+    sb.layout = exchange_layout(sb.R, sb.rank, sb.world, sb.owner)
     sb.be.set_exchange(sb.layout)
 
 
@@ -407,14 +467,21 @@ def contract(sb: ShardedButterfly, F, G, comm, nv: int = 1, stream: int = 0):
     return send, recv
 
 
-def run_lockstep(backends: list, F, nv: int = 1):
+def core_bytes_per_s(R: np.ndarray, C: np.ndarray) -> np.ndarray:
+    """Core bytes read by the owner of each s: 16 * sum_t R[t, s] * C[t, s]
+    (R, C: rows / columns of every core, indexed [t, s]) -- the weights of the
+    byte-balanced ownership map."""
+    return 16 * (np.asarray(R, np.int64) * np.asarray(C, np.int64)).sum(axis=0)
+
+
+def run_lockstep(backends: list, F, nv: int = 1, owner=None):
     """Emulate `world` ranks in one process (sequentially, one GPU): same
     steps and the same exchange layout, collectives done by hand.  Returns the
     assembled G (each rank contributes its own row slabs).  Used by the
     single-GPU test of the sharded path; ranks never wait on each other."""
     import torch
     world = len(backends)
-    sbs = [ShardedButterfly(b, r, world) for r, b in enumerate(backends)]
+    sbs = [ShardedButterfly(b, r, world, owner) for r, b in enumerate(backends)]
     Lc = sbs[0].Lc
     for side in (0, 1):
         r_est = 8

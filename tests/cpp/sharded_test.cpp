@@ -1,6 +1,7 @@
 // In-process multi-device butterfly (include/oiobf/sharded.hpp) against the
 // single-GPU butterfly of the same operator: usage
-//   sharded_test WORLD [case]      (every rank on device 0 -- a one-GPU box)
+//   sharded_test WORLD [case] [balanced]   (every rank on device 0 -- a one-GPU box)
+// balanced: tbf_construct_sharded_balanced (byte-balanced ownership map)
 // case: cubes32 (d = 3, L = 2), radon64 (d = 2, L = 2), plates64L4 (d = 2,
 // L = 4), dft6 (d = 6, n = 4, C_b = 1, L = 2, all ranks 1).  Prints one JSON line.
 #include <cmath>
@@ -37,7 +38,19 @@ int main(int argc, char** argv) {
   }
   const KernelEvaluator k = make_kernel(s);
   const TensorButterfly single = tbf_construct(k, L, tol, ProxyStrategy{}, 5);
-  const ShardedTensorButterfly sh = tbf_construct_sharded(k, L, tol, ProxyStrategy{}, 5, std::vector<int>(world, 0));
+  const bool balanced = argc > 3 && std::string(argv[3]) == "balanced";
+  const ShardedTensorButterfly sh =
+      balanced ? tbf_construct_sharded_balanced(k, L, tol, ProxyStrategy{}, 5, std::vector<int>(world, 0))
+               : tbf_construct_sharded(k, L, tol, ProxyStrategy{}, 5, std::vector<int>(world, 0));
+  // heaviest rank's core bytes over the mean (phase-1 imbalance)
+  const std::vector<double> w = sh.core_bytes_per_s();
+  std::vector<double> load(static_cast<std::size_t>(world), 0.0);
+  double tot = 0;
+  for (std::size_t i = 0; i < w.size(); ++i) {
+    load[static_cast<std::size_t>(sh.owner_of(static_cast<std::int64_t>(i)))] += w[i];
+    tot += w[i];
+  }
+  const double imb = *std::max_element(load.begin(), load.end()) / (tot / world);
   std::vector<std::int64_t> shape(k.col_extents.begin(), k.col_extents.end());
   shape.push_back(2);  // n_v = 2
   DenseTensor F(shape);
@@ -54,6 +67,7 @@ int main(int argc, char** argv) {
   std::int64_t sent = 0;
   for (int r = 0; r < world; ++r) sent += sh.layout(static_cast<std::size_t>(r)).send_total();
   std::cout << "{\"case\":\"" << which << "\",\"world\":" << world << ",\"nmid\":" << sh.nmid()
-            << ",\"rel\":" << std::sqrt(num / den) << ",\"exchanged_elems\":" << sent << "}" << std::endl;
+            << ",\"rel\":" << std::sqrt(num / den) << ",\"exchanged_elems\":" << sent
+            << ",\"mapped\":" << (sh.owners().empty() ? 0 : 1) << ",\"core_max_over_mean\":" << imb << "}" << std::endl;
   return 0;
 }

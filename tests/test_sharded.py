@@ -15,15 +15,18 @@ import numpy as np
 import pytest
 
 from paper_2411_03029_b200.configs import green_cubes, green_plates, radon2d
-from paper_2411_03029_b200.sharded import ShardedButterfly, TorchComm, construct, exchange_layout, owns
+from paper_2411_03029_b200.sharded import (ShardedButterfly, TorchComm, balanced_owners, construct, exchange_layout,
+                                            owns)
 
 
+@pytest.mark.parametrize("mapped", [False, True], ids=["round_robin", "owner_map"])
 @pytest.mark.parametrize("world", [1, 2, 3, 4])
-def test_exchange_layout_consistent(world):
+def test_exchange_layout_consistent(world, mapped):
     rng = np.random.default_rng(world)
     nmid = 8
     R = rng.integers(0, 30, size=(nmid, nmid))
-    lays = [exchange_layout(R, r, world) for r in range(world)]
+    owner = rng.integers(0, world, nmid).astype(np.int32) if mapped else None  # uneven on purpose
+    lays = [exchange_layout(R, r, world, owner) for r in range(world)]
     for r in range(world):
         for q in range(world):
             assert lays[q].send_counts[r] == lays[r].recv_counts[q]
@@ -32,8 +35,8 @@ def test_exchange_layout_consistent(world):
         for t in range(nmid):
             for s in range(nmid):
                 so, ro = lay.send_off[t * nmid + s], lay.recv_off[t * nmid + s]
-                assert (so >= 0) == owns(s, r, world)
-                assert (ro >= 0) == owns(t, r, world)
+                assert (so >= 0) == owns(s, r, world, owner)
+                assert (ro >= 0) == owns(t, r, world, owner)
                 seen[t, s] += so >= 0
         # blocks are packed back to back in both buffers
         for off, counts in ((lay.send_off, lay.send_counts), (lay.recv_off, lay.recv_counts)):
@@ -44,6 +47,32 @@ def test_exchange_layout_consistent(world):
                 cur += sz
             assert cur == counts.sum()
     assert np.all(seen == 1)  # every block is sent exactly once
+    # sender and receiver agree on the order inside each (source, destination) segment
+    for r in range(world):
+        for q in range(world):
+            snd = sorted((lays[r].send_off[t * nmid + s], t, s) for t in range(nmid) for s in range(nmid)
+                         if owns(s, r, world, owner) and owns(t, q, world, owner))
+            rcv = sorted((lays[q].recv_off[t * nmid + s], t, s) for t in range(nmid) for s in range(nmid)
+                         if owns(s, r, world, owner) and owns(t, q, world, owner))
+            assert [x[1:] for x in snd] == [x[1:] for x in rcv]
+
+
+def test_balanced_owners():
+    """LPT bin packing: even counts, deterministic, no worse than round-robin
+    and near the mean on a skewed weight profile."""
+    rng = np.random.default_rng(1)
+    for nmid, world in ((64, 8), (64, 4), (8, 2), (16, 3)):
+        w = rng.integers(20, 80, nmid).astype(np.float64)
+        w[: nmid // 4] *= 3  # a heavy corner, like the s nearest the target cube
+        own = balanced_owners(w, world)
+        assert np.array_equal(own, balanced_owners(w, world))
+        cnt = np.bincount(own, minlength=world)
+        assert cnt.max() <= -(-nmid // world) and cnt.sum() == nmid
+        load = np.bincount(own, weights=w, minlength=world)
+        rr = np.bincount(np.arange(nmid) % world, weights=w, minlength=world)
+        assert load.max() <= rr.max() + 1e-9
+        if nmid >= 8 * world:
+            assert load.max() / load.mean() < 1.03
 
 
 class OracleShardBackend:
@@ -51,6 +80,7 @@ class OracleShardBackend:
 
     def __init__(self, oracle, spec, L, tol, seed, rank, world):
         self.o, self.spec = oracle, spec
+        self.owner = None
         self.tbf = oracle.tbf_construct(spec, L, tol, seed=seed, nthreads=2)
         self.fz = self.tbf.export()
         self.rank, self.world = rank, world
@@ -61,18 +91,21 @@ class OracleShardBackend:
             self.base[(sd, l)] = (b, cnt)
             b += cnt
 
+    def set_owners(self, owner):
+        self.owner = np.ascontiguousarray(owner, np.int32)
+
     def level(self, side, l, r_est):
         assert r_est == self.fz.r_est[side * (self.Lc + 1) + l]
         b, cnt = self.base[(side, l)]
         nin, nj = 2 ** (self.d * l), 2 ** (self.Lc - l)
         outer = np.arange(cnt) // (nj * self.d * nin)
-        mine = np.array([owns(int(o), self.rank, self.world) for o in outer])
+        mine = np.array([owns(int(o), self.rank, self.world, self.owner) for o in outer])
         return int(self.fz.ranks[b:b + cnt][mine].max(initial=0))
 
     def umid_info(self):
         b, cnt = self.base[(1, self.Lc)]
         t = np.arange(cnt) // (self.nmid * self.d)
-        mine = np.array([owns(int(x), self.rank, self.world) for x in t])
+        mine = np.array([owns(int(x), self.rank, self.world, self.owner) for x in t])
         return cnt, int(self.fz.ranks[b:b + cnt][mine].max(initial=0))
 
     def umid_export(self, wpad):
@@ -81,7 +114,7 @@ class OracleShardBackend:
         ranks = np.zeros(cnt, np.int64)
         skel = np.zeros(cnt * wpad, np.int32)
         for q in range(cnt):
-            if owns(q // (self.nmid * self.d), self.rank, self.world):
+            if owns(q // (self.nmid * self.d), self.rank, self.world, self.owner):
                 r = int(self.fz.ranks[b + q])
                 ranks[q] = r
                 skel[q * wpad:q * wpad + r] = self.fz.skel[so[b + q]:so[b + q] + r]
@@ -98,8 +131,9 @@ class OracleShardBackend:
         import ctypes as C
         from oracle.bindings import cx
         L = self.o.lib
-        L.oracle_tbf_contract_phase.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
-                                                C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int]
+        L.oracle_tbf_contract_phase_owned.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                                      C.c_int64, C.c_int]
         N = self.spec.n ** self.spec.d * nv
         se, re = int(self.lay.send_counts.sum()), int(self.lay.recv_counts.sum())
         if phase == 1:
@@ -108,9 +142,10 @@ class OracleShardBackend:
         else:
             inp = src.astype(np.float64) if src.size else np.zeros(2)
             out = np.zeros(2 * N)
-        rc = L.oracle_tbf_contract_phase(self.tbf.h, phase, self.rank, self.world, inp.ctypes.data,
-                                         out.ctypes.data, self.lay.send_off.ctypes.data,
-                                         self.lay.recv_off.ctypes.data, se, re, nv, 2)
+        rc = L.oracle_tbf_contract_phase_owned(self.tbf.h, phase, self.rank, self.world,
+                                               None if self.owner is None else self.owner.ctypes.data,
+                                               inp.ctypes.data, out.ctypes.data, self.lay.send_off.ctypes.data,
+                                               self.lay.recv_off.ctypes.data, se, re, nv, 2)
         assert rc == 0, L.oracle_last_error()
         return out
 
@@ -132,10 +167,18 @@ def _gloo_worker(rank, world, port, spec_args, q):
     try:
         from oracle import Oracle
         o = Oracle()
-        spec, L, tol, seed = spec_args
+        spec, L, tol, seed = spec_args[:4]
         be = OracleShardBackend(o, spec, L, tol, seed, rank, world)
         comm = TorchComm()
-        sb = construct(be, rank, world, comm)
+        owner = None
+        if len(spec_args) > 4 and spec_args[4]:  # byte-balanced map from the core shapes (same on every rank)
+            from paper_2411_03029_b200.sharded import core_bytes_per_s
+            nm = be.nmid
+            cr = np.asarray(be.fz.core_rows).reshape(nm, nm).T  # pair p = s * nmid + t -> [t, s]
+            cc = np.asarray(be.fz.core_cols).reshape(nm, nm).T
+            owner = balanced_owners(core_bytes_per_s(cr, cc), world)
+            assert not np.array_equal(owner, np.arange(nm) % world)
+        sb = construct(be, rank, world, comm, owner)
         rng = np.random.default_rng(11)
         F = (rng.standard_normal((spec.n,) * spec.d) + 1j * rng.standard_normal((spec.n,) * spec.d))
         send = torch.from_numpy(be.phase(1, F.reshape(-1, order="F"), 1))
@@ -154,14 +197,16 @@ def _gloo_worker(rank, world, port, spec_args, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("spec,L,tol", [(green_plates(32), 2, 1e-6), (green_cubes(16), 2, 1e-4), (radon2d(32), 2, 1e-6)],
-                         ids=["plates32", "cubes16", "radon32"])
-def test_sharded_gloo_world2_bitexact(oracle, spec, L, tol):
+@pytest.mark.parametrize("spec,L,tol,balanced",
+                         [(green_plates(32), 2, 1e-6, False), (green_cubes(16), 2, 1e-4, False),
+                          (radon2d(32), 2, 1e-6, False), (green_cubes(16), 2, 1e-4, True)],
+                         ids=["plates32", "cubes16", "radon32", "cubes16_balanced"])
+def test_sharded_gloo_world2_bitexact(oracle, spec, L, tol, balanced):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, (spec, L, tol, 5), q)) for r in range(2)]
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, (spec, L, tol, 5, balanced), q)) for r in range(2)]
     for p in procs:
         p.start()
     res = q.get(timeout=600)
@@ -169,6 +214,36 @@ def test_sharded_gloo_world2_bitexact(oracle, spec, L, tol):
         p.join(timeout=120)
     assert res[0] == "ok", res
     assert res[1], f"sharded result differs from the unsharded oracle (max {res[2]})"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_gpu_lockstep_balanced(world):
+    """Byte-balanced ownership (an LPT map of the per-s core bytes instead of
+    s % world) through the device construction, the exchange layout and both
+    apply phases: G within 1e-12 of the single-GPU contraction."""
+    import torch
+
+    import paper_2411_03029_b200 as tb
+    from paper_2411_03029_b200.sharded import GpuShardBackend, core_bytes_per_s, run_lockstep
+    spec, L, tol = green_cubes(32), 2, 1e-4
+    single = tb.tbf_construct(spec, L, tol, seed=5)
+    fz = single.export()
+    nm = fz.nmid
+    w = core_bytes_per_s(np.asarray(fz.core_rows).reshape(nm, nm).T, np.asarray(fz.core_cols).reshape(nm, nm).T)
+    owner = balanced_owners(w, world)
+    assert not np.array_equal(owner, np.arange(nm) % world)
+    rr = np.bincount(np.arange(nm) % world, weights=w, minlength=world)
+    bal = np.bincount(owner, weights=w, minlength=world)
+    assert bal.max() <= rr.max()
+    rng = np.random.default_rng(3)
+    F = rng.standard_normal((32,) * 3) + 1j * rng.standard_normal((32,) * 3)
+    G1 = single.contract(F).reshape(-1, order="F")
+    Ft = torch.from_numpy(np.ascontiguousarray(F.reshape(-1, order="F")).view(np.float64).copy()).cuda()
+    backends = [GpuShardBackend(spec, L, tol, tb.ProxyStrategy(), 5, r, world) for r in range(world)]
+    G = run_lockstep(backends, Ft, owner=owner).cpu().numpy().view(np.complex128)
+    err = np.linalg.norm(G - G1) / np.linalg.norm(G1)
+    assert err < 1e-12, err
 
 
 @pytest.mark.gpu

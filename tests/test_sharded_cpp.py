@@ -39,3 +39,21 @@ def test_sharded_cpp_matches_single_gpu(world, case):
     out = json.loads(r.stdout.strip().splitlines()[-1])
     assert out["world"] == world
     assert out["rel"] < 1e-12, out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_cpp_balanced_ownership(world):
+    """tbf_construct_sharded_balanced: the LPT ownership map of the measured
+    per-s core bytes gives the same G and a heaviest rank no heavier than
+    round-robin's."""
+    _build()
+    outs = []
+    for mode in ("", "balanced"):
+        r = subprocess.run([EXE, str(world), "cubes32"] + ([mode] if mode else []), capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    rr, bal = outs
+    assert rr["rel"] < 1e-12 and bal["rel"] < 1e-12, outs
+    assert bal["core_max_over_mean"] <= rr["core_max_over_mean"] + 1e-12, outs

@@ -14,6 +14,19 @@ keys = ["gpu__time_duration.sum", "sm__cycles_active.max", "sm__cycles_active.av
 for i, n in enumerate(h):
     if n in keys:
         print(f"{n:55s} {v[i]}")
+stalls = []
+for i, n in enumerate(h):
+    if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("_not_issued"):
+        try: stalls.append((float(v[i].replace(",", "")), n[len("smsp__pcsamp_warps_issue_stalled_"):]))
+        except ValueError: pass
+ts = sum(x[0] for x in stalls) or 1.0
+print("stall reasons (pc samples): " + ", ".join(f"{n} {100 * c / ts:.1f}%" for c, n in sorted(stalls, reverse=True)[:8]))
+for i, n in enumerate(h):
+    if n in ("smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+             "l1tex__data_pipe_lsu_wavefronts_mem_shared.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed_pipe_lsu.sum",
+             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
+             "lts__t_sector_hit_rate.pct"):
+        print(f"{n:55s} {v[i]}")
 rows = list(csv.reader(io.StringIO(run("--page", "source", "--csv", "--print-source", "cuda,sass"))))
 agg = collections.defaultdict(lambda: [0, 0]); cur = None; fname = None; hdr = None
 for row in rows:

@@ -196,10 +196,21 @@ struct R1LevelArgs {
                        // tile); P/U levels >= 1: one warp per (group, block tuple) unit
   // log2 of the power-of-two extents above (n is a power of two)
   int lg_n, lg_mid, lg_nmid, lg_nin, lg_nj, lg_njd, lg_pnin, lg_nch, lg_E, lg_ED;
+  // sharded (world > 1): this rank's 2^lg_nown outer multi-sets, local index i
+  // -> middle multi-set own[i] (ascending); buffers, factor arenas and cores
+  // are indexed by the LOCAL outer index, F / G slabs by own[i].  Unsharded:
+  // lg_nown = lg_nmid, own = null (identity).
+  int lg_nown;
+  const int* own;
 };
 size_t r1_smem_bytes(const R1LevelArgs& a);
 int r1_threads();
 int r1_vthreads();
+// sharded middle-level exchange of the rank-one engine: unpack = 0 packs the
+// level-Lc V/W output into the send buffer, 1 unpacks the receive buffer into
+// the level-Lc P/U input (off: the exchange offsets per pair t * nmid + s)
+void launch_r1_exchange(const R1LevelArgs& a, int unpack, const long long* off, const double2* in, double2* out,
+                        cudaStream_t st);
 void launch_r1_level(const R1LevelArgs& a, const double2* fac, const double2* cores, const double2* in, double2* out,
                      cudaStream_t st);
 

@@ -32,6 +32,14 @@
 // jt / pos mixed radix, mode 0 fastest.  The level-Lc V/W output is indexed by
 // the pair p = s * nmid + t, like the cores.  P/U groups are ordered t fastest
 // (g = p_nu * nmid + t), so the level-Lc gather of G_{t,s} reads runs of t.
+//
+// Sharded (world > 1, a power-of-two number nown of owned multi-sets per rank):
+// the outer index s / t above is the LOCAL index i < nown everywhere (buffers
+// hold nown * nmid elements per vector, the factor arenas and cores hold only
+// the owned slots, in local order) and a.own[i] names the middle multi-set for
+// the F / G slabs.  The level-Lc P/U input is then (v * nmid + s) * nown + t
+// with s over ALL middle multi-sets: k_r1_pack / k_r1_unpack move the blocks
+// G_{t,s} between these buffers and the exchange's send / receive buffers.
 #include "kernels.h"
 
 namespace tbf {
@@ -119,12 +127,13 @@ __device__ __forceinline__ i64 r1_pu_out(const R1LevelArgs& a, i64 v, i64 t, i64
   const int nj = 1 << a.lg_nj;
   int q = x;
   if (a.out_global) {
+    const i64 tg = a.own ? a.own[t] : t;  // the middle multi-set of local t
     i64 addr = v << (a.lg_n * D);
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       const int jk = (jt >> (a.lg_nj * k)) & (nj - 1), xk = q % W;
       q /= W;
-      addr += ((((t >> (a.Lc * k)) & (a.mpm - 1)) << a.lg_mid) + jk * W + xk) << (a.lg_n * k);
+      addr += ((((tg >> (a.Lc * k)) & (a.mpm - 1)) << a.lg_mid) + jk * W + xk) << (a.lg_n * k);
     }
     return addr;
   }
@@ -135,7 +144,7 @@ __device__ __forceinline__ i64 r1_pu_out(const R1LevelArgs& a, i64 v, i64 t, i64
     q /= W;
     pos += static_cast<i64>(jk * W + xk) << (a.lg_E * k);
   }
-  return (((((v << a.lg_nmid) + t) << a.lg_pnin) + pnu) << a.lg_ED) + pos;
+  return (((((v << a.lg_nown) + t) << a.lg_pnin) + pnu) << a.lg_ED) + pos;
 }
 
 // V/W level: CTA = (s, T consecutive tau); their parents form a contiguous
@@ -151,7 +160,8 @@ __global__ void __launch_bounds__(kR1Threads, 2) k_r1_vw(R1LevelArgs a, const do
   const int lg_T = a.lg_T, T = 1 << lg_T;
   const int lg_ED = a.lg_ED, lg_E = a.lg_E, E = 1 << lg_E, XS = a.XS;
   const i64 blk = blockIdx.x;
-  const i64 s = blk >> (a.lg_nin - lg_T);
+  const i64 s = blk >> (a.lg_nin - lg_T);     // local outer index
+  const i64 sg = a.own ? a.own[s] : s;        // its middle multi-set (F slab)
   const i64 tau0 = (blk & ((i64{1} << (a.lg_nin - lg_T)) - 1)) << lg_T;
   const i64 pfirst = a.l > 0 ? r1_parent<D>(tau0, a.l) : 0;
   const int np = a.l > 0 ? static_cast<int>(r1_parent<D>(tau0 + T - 1, a.l) - pfirst + 1) : 1;
@@ -165,10 +175,10 @@ __global__ void __launch_bounds__(kR1Threads, 2) k_r1_vw(R1LevelArgs a, const do
 #pragma unroll
       for (int k = 0; k < D; ++k) {
         const int ek = (loc >> (lg_E * k)) & (E - 1);
-        addr += ((((s >> (a.Lc * k)) & (a.mpm - 1)) << a.lg_mid) + ek) << (a.lg_n * k);
+        addr += ((((sg >> (a.Lc * k)) & (a.mpm - 1)) << a.lg_mid) + ek) << (a.lg_n * k);
       }
     } else {
-      addr = (((((v << a.lg_nmid) + s) << a.lg_pnin) + pfirst + pl) << lg_ED) + loc;
+      addr = (((((v << a.lg_nown) + s) << a.lg_pnin) + pfirst + pl) << lg_ED) + loc;
     }
     xs[pl * XS + loc] = __ldg(in + addr);
   }
@@ -224,7 +234,7 @@ __global__ void __launch_bounds__(kR1Threads, 2) k_r1_vw(R1LevelArgs a, const do
     }
     double2 res = part[D - 1];
     if (a.core_mul) res = cmul(__ldg(cores + (s << a.lg_nmid) + tau), res);
-    out[(((((v << a.lg_nmid) + s) << a.lg_nin) + tau) << lg_njd) + jt] = res;
+    out[(((((v << a.lg_nown) + s) << a.lg_nin) + tau) << lg_njd) + jt] = res;
   }
 }
 
@@ -244,7 +254,7 @@ __global__ void __launch_bounds__(kR1VThreads, 6) k_r1_vw_mid(R1LevelArgs a, con
   const i64 v = blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const i64 tile = static_cast<i64>(blockIdx.x) * (kR1VThreads / 32) + warp;
-  if (tile >= (a.nmid << (a.lg_nin - 5))) return;
+  if (tile >= (i64{1} << (a.lg_nown + a.lg_nin - 5))) return;
   const int lg_ED = a.lg_ED, lg_E = a.lg_E, XS = a.XS, FS = a.FS, fblk = a.fblk;
   double2* xs = wsm + warp * (a.Pc * XS + 32 * FS);
   double2* fs = xs + a.Pc * XS;
@@ -255,7 +265,7 @@ __global__ void __launch_bounds__(kR1VThreads, 6) k_r1_vw_mid(R1LevelArgs a, con
   const i64 tau = tau0 + lane;
   const double2 core = a.core_mul ? __ldg(cores + (s << a.lg_nmid) + tau) : make_double2(1, 0);
   {
-    const double2* src = in + ((((v << a.lg_nmid) + s) << a.lg_pnin) + pfirst << lg_ED);
+    const double2* src = in + ((((v << a.lg_nown) + s) << a.lg_pnin) + pfirst << lg_ED);
     const int n = np << lg_ED;
 #pragma unroll 4
     for (int e = lane; e < n; e += 32) xs[(e >> lg_ED) * XS + (e & ((1 << lg_ED) - 1))] = __ldg(src + e);
@@ -300,7 +310,7 @@ __global__ void __launch_bounds__(kR1VThreads, 6) k_r1_vw_mid(R1LevelArgs a, con
       else cfma(part[k + 1], fb[(k + 1) * W + xk], part[k]);
     }
   }
-  out[(((v << a.lg_nmid) + s) << a.lg_nin) + tau] = cmul(core, part[D - 1]);
+  out[(((v << a.lg_nown) + s) << a.lg_nin) + tau] = cmul(core, part[D - 1]);
 }
 
 // P/U level, general form: CTA = gpb (group, block tuple) units, groups t
@@ -324,7 +334,7 @@ __global__ void __launch_bounds__(kR1Threads, 3) k_r1_pu(R1LevelArgs a, const do
   for (int q = threadIdx.x; q < (ngr << lg_nch); q += blockDim.x) {
     const int gl = q >> lg_nch, c = q & (nch - 1);
     const i64 g = gfirst + gl;
-    const i64 t = g & ((i64{1} << a.lg_nmid) - 1), pnu = g >> a.lg_nmid;
+    const i64 t = g & ((i64{1} << a.lg_nown) - 1), pnu = g >> a.lg_nown;
     cbase[q] = ((t << a.lg_nin) + (a.l > 0 ? r1_child<D>(pnu, a.l, c) : 0)) * a.fblk;
   }
   __syncthreads();
@@ -342,11 +352,11 @@ __global__ void __launch_bounds__(kR1Threads, 3) k_r1_pu(R1LevelArgs a, const do
     const i64 u = u0 + ul;
     const i64 g = u >> lg_njd;
     const int jt = static_cast<int>(u & ((i64{1} << lg_njd) - 1));
-    const i64 t = g & ((i64{1} << a.lg_nmid) - 1), pnu = g >> a.lg_nmid;  // groups t fastest
+    const i64 t = g & ((i64{1} << a.lg_nown) - 1), pnu = g >> a.lg_nown;  // groups t fastest
     const i64 nuc = a.l > 0 ? r1_child<D>(pnu, a.l, c) : 0;
     const double2 val =
-        __ldg(in + (a.in_transposed ? (((v << a.lg_nmid) + nuc) << a.lg_nmid) + t
-                                    : (((((v << a.lg_nmid) + t) << a.lg_nin) + nuc) << lg_njd) + jt));
+        __ldg(in + (a.in_transposed ? (((v << a.lg_nmid) + nuc) << a.lg_nown) + t
+                                    : (((((v << a.lg_nown) + t) << a.lg_nin) + nuc) << lg_njd) + jt));
     const double2* fb = sm + ((static_cast<int>(g - gfirst) << lg_nch) + c) * a.FS;
     double2 b[D][W];
 #pragma unroll
@@ -376,7 +386,7 @@ __global__ void __launch_bounds__(kR1Threads, 3) k_r1_pu(R1LevelArgs a, const do
     const i64 u = u0 + ul;
     const i64 g = u >> lg_njd;
     const int jt = static_cast<int>(u & ((i64{1} << lg_njd) - 1));
-    const i64 t = g & ((i64{1} << a.lg_nmid) - 1), pnu = g >> a.lg_nmid;
+    const i64 t = g & ((i64{1} << a.lg_nown) - 1), pnu = g >> a.lg_nown;
     out[r1_pu_out<D, W>(a, v, t, pnu, jt, x)] = acc;
   }
 }
@@ -421,7 +431,7 @@ __global__ void __launch_bounds__(kR1VThreads, 3) k_r1_pu_mid(R1LevelArgs a, con
   const int jt = static_cast<int>(u & ((i64{1} << a.lg_njd) - 1));
   constexpr int SL = ((D * W) | 1) > TS ? ((D * W) | 1) : TS;
   double2* ws = wsm + warp * 2 * 32 * SL;  // two chunk buffers (factor rows, then aliased tables)
-  const i64 t = g & ((i64{1} << a.lg_nmid) - 1), pnu = g >> a.lg_nmid;  // groups t fastest
+  const i64 t = g & ((i64{1} << a.lg_nown) - 1), pnu = g >> a.lg_nown;  // groups t fastest
   const int nch = 1 << a.lg_nch, fblk = a.fblk;
   const int nchunk = (nch + 31) / 32;
   // chunk c0 / 32 -> buffer (c0 / 32) & 1: async copies of the chunk's factor
@@ -433,8 +443,8 @@ __global__ void __launch_bounds__(kR1VThreads, 3) k_r1_pu_mid(R1LevelArgs a, con
     const i64 nuc = a.l > 0 ? r1_child<D>(pnu, a.l, c0 + lane) : 0;
     const i64 mybase = ((t << a.lg_nin) + nuc) * fblk;
     if (lane < cn)
-      val = __ldg(in + (a.in_transposed ? (((v << a.lg_nmid) + nuc) << a.lg_nmid) + t
-                                        : (((((v << a.lg_nmid) + t) << a.lg_nin) + nuc) << a.lg_njd) + jt));
+      val = __ldg(in + (a.in_transposed ? (((v << a.lg_nmid) + nuc) << a.lg_nown) + t
+                                        : (((((v << a.lg_nown) + t) << a.lg_nin) + nuc) << a.lg_njd) + jt));
     double2* buf = ws + ((c0 >> 5) & 1) * 32 * SL;
     for (int e0 = 0; e0 < cn * DW; e0 += 32) {
       const int e = min(e0 + lane, cn * DW - 1);
@@ -522,17 +532,45 @@ __global__ void __launch_bounds__(kR1VThreads, 3) k_r1_pu_mid(R1LevelArgs a, con
   }
 }
 
+// Sharded exchange of the middle level (every block G_{t,s} is one element per
+// vector): pack the level-Lc V/W output (v * nown + i) * nmid + t of the owned
+// s = own[i] into the send buffer at send_off[t * nmid + s] * nv + v; unpack
+// the receive buffer (recv_off[t * nmid + s] * nv + v, t = own[i]) into the
+// level-Lc P/U input (v * nmid + s) * nown + i.
+__global__ void __launch_bounds__(256) k_r1_pack(R1LevelArgs a, const long long* __restrict__ send_off,
+                                                 const double2* __restrict__ in, double2* __restrict__ out) {
+  const i64 total = i64{1} << (a.lg_nown + a.lg_nmid);
+  for (i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; e < total * a.nv;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 v = e >> (a.lg_nown + a.lg_nmid), r = e & (total - 1);
+    const i64 i = r >> a.lg_nmid, t = r & ((i64{1} << a.lg_nmid) - 1);
+    const i64 s = a.own[i];
+    out[send_off[(t << a.lg_nmid) + s] * a.nv + v] = in[e];
+  }
+}
+__global__ void __launch_bounds__(256) k_r1_unpack(R1LevelArgs a, const long long* __restrict__ recv_off,
+                                                   const double2* __restrict__ in, double2* __restrict__ out) {
+  const i64 total = i64{1} << (a.lg_nown + a.lg_nmid);
+  for (i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x; e < total * a.nv;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 v = e >> (a.lg_nown + a.lg_nmid), r = e & (total - 1);
+    const i64 s = r >> a.lg_nown, i = r & ((i64{1} << a.lg_nown) - 1);  // output order: t fastest
+    const i64 t = a.own[i];
+    out[e] = in[recv_off[(t << a.lg_nmid) + s] * a.nv + v];
+  }
+}
+
 template <int D, int W>
 void launch_r1_dw(const R1LevelArgs& a, const double2* fac, const double2* cores, const double2* in, double2* out,
                   cudaStream_t st) {
   const size_t smem = r1_smem_bytes(a);
   if (a.side == 0 && a.warp_tiles) {
-    const i64 tiles = a.nmid << (a.lg_nin - 5);
+    const i64 tiles = i64{1} << (a.lg_nown + a.lg_nin - 5);
     const dim3 grid(static_cast<unsigned>((tiles + kR1VThreads / 32 - 1) / (kR1VThreads / 32)), static_cast<unsigned>(a.nv));
     TBF_CUDA(cudaFuncSetAttribute(k_r1_vw_mid<D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     k_r1_vw_mid<D, W><<<grid, kR1VThreads, smem, st>>>(a, fac, cores, in, out);
   } else if (a.side == 0) {
-    const dim3 grid(static_cast<unsigned>(a.nmid << (a.lg_nin - a.lg_T)), static_cast<unsigned>(a.nv));
+    const dim3 grid(static_cast<unsigned>(i64{1} << (a.lg_nown + a.lg_nin - a.lg_T)), static_cast<unsigned>(a.nv));
     TBF_CUDA(cudaFuncSetAttribute(k_r1_vw<D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     k_r1_vw<D, W><<<grid, kR1Threads, smem, st>>>(a, fac, cores, in, out);
   } else if (a.warp_tiles) {
@@ -570,6 +608,15 @@ size_t r1_smem_bytes(const R1LevelArgs& a) {
   const size_t ngr = std::max<size_t>(1, static_cast<size_t>(a.gpb) >> a.lg_njd);  // groups a CTA's units span
   const size_t facs = (ngr << a.lg_nch) * static_cast<size_t>(a.FS);
   return sizeof(double2) * std::max(tabs, facs);
+}
+
+void launch_r1_exchange(const R1LevelArgs& a, int unpack, const long long* off, const double2* in, double2* out,
+                        cudaStream_t st) {
+  const i64 total = (i64{1} << (a.lg_nown + a.lg_nmid)) * a.nv;
+  const unsigned grid = static_cast<unsigned>(std::min<i64>((total + 255) / 256, 148 * 16));
+  if (unpack) k_r1_unpack<<<grid, 256, 0, st>>>(a, off, in, out);
+  else k_r1_pack<<<grid, 256, 0, st>>>(a, off, in, out);
+  TBF_CUDA(cudaGetLastError());
 }
 
 int r1_threads() { return kR1Threads; }

@@ -355,6 +355,8 @@ struct Plan {
     i64 in_off, out_off;  // scratch element offsets; -1: F (input) / G (output)
   };
   std::vector<R1Level> r1_levels;
+  DevBuf<int> d_r1_own;                      // sharded: local -> middle multi-set
+  DevBuf<i64> d_r1_send_off, d_r1_recv_off;  // sharded: exchange offsets per pair t * nmid + s
   std::vector<GemvDesc> gemv;
   std::vector<GemvLaunch> gemvs;
   std::vector<int> gemv_map, tma_map;
@@ -1943,10 +1945,30 @@ std::unique_ptr<Plan> build_plan_tiny(oiobf_tbf& b, i64 nv) {
 // Eligible when, on both sides and every level, each slot has rank 1 and
 // width W_l (the leaf size <= 2 at l = 0, 2 above) with its block at slot * W_l
 // in the interp arena, and every core is 1 x 1 at its pair index.
+// Sharded (world > 1): the same for the OWNED slots and pairs, whose blocks
+// are packed in local order (slots of other ranks have rank 0 and no block);
+// every rank must own the same power-of-two number of middle multi-sets.
+std::vector<int> owned_list(const oiobf_tbf& b) {
+  std::vector<int> own;
+  for (i64 o = 0; o < b.nmid; ++o)
+    if (b.owns(o)) own.push_back(static_cast<int>(o));
+  return own;
+}
+
 bool r1_eligible(const oiobf_tbf& b) {
-  if (b.world > 1 || b.d < 1 || b.d > kMaxD || (b.n & (b.n - 1)) != 0) return false;
+  if (b.d < 1 || b.d > kMaxD || (b.n & (b.n - 1)) != 0) return false;
   const i64 leaf = b.n >> b.L;
   if (leaf < 1 || leaf > 2) return false;
+  const bool sharded = b.world > 1;
+  std::vector<i64> pos(static_cast<size_t>(b.nmid), -1);  // local index of an owned middle multi-set
+  i64 nown = 0;
+  for (i64 o = 0; o < b.nmid; ++o)
+    if (b.owns(o)) pos[static_cast<size_t>(o)] = nown++;
+  if (sharded) {
+    if (nown * b.world != b.nmid || (nown & (nown - 1)) != 0) return false;
+    if (b.peer_mode()) return false;  // the fused exchange is the box engine's GEMV epilogue
+    if (static_cast<i64>(b.send_off.size()) != b.nmid * b.nmid) return false;
+  }
   for (int sd = 0; sd < 2; ++sd) {
     if (b.side[sd].size() != static_cast<size_t>(b.Lc + 1)) return false;
     for (int l = 0; l <= b.Lc; ++l) {
@@ -1954,10 +1976,19 @@ bool r1_eligible(const oiobf_tbf& b) {
       const int w = l == 0 ? static_cast<int>(leaf) : 2;
       if (static_cast<i64>(ld.h_rank.size()) != ld.nslots || static_cast<i64>(ld.h_interp_off.size()) != ld.nslots)
         return false;
+      const i64 per_outer = ld.nslots / b.nmid;  // slots of one outer multi-set (contiguous)
       std::vector<char> bad(parallel_nchunks(static_cast<size_t>(ld.nslots)), 0);
       parallel_chunks(static_cast<size_t>(ld.nslots), [&](size_t c, size_t lo, size_t hi) {
-        for (size_t i = lo; i < hi && !bad[c]; ++i)
-          bad[c] = ld.h_rank[i] != 1 || ld.h_width[i] != w || ld.h_interp_off[i] != static_cast<i64>(i) * w;
+        for (size_t i = lo; i < hi && !bad[c]; ++i) {
+          const i64 outer = static_cast<i64>(i) / per_outer;
+          const i64 li = pos[static_cast<size_t>(outer)];
+          if (li < 0) {
+            bad[c] = ld.h_rank[i] != 0;
+          } else {
+            const i64 local = li * per_outer + (static_cast<i64>(i) - outer * per_outer);
+            bad[c] = ld.h_rank[i] != 1 || ld.h_width[i] != w || ld.h_interp_off[i] != local * w;
+          }
+        }
       });
       for (char x : bad)
         if (x) return false;
@@ -1969,7 +2000,15 @@ bool r1_eligible(const oiobf_tbf& b) {
   parallel_chunks(static_cast<size_t>(P), [&](size_t c, size_t lo, size_t hi) {
     for (size_t p = lo; p < hi && !bad[c]; ++p) {
       const PairDesc& pd = b.h_pairs[p];
-      bad[c] = pd.R != 1 || pd.C != 1 || pd.core_off != static_cast<i64>(p);
+      const i64 sq = static_cast<i64>(p) / b.nmid, t = static_cast<i64>(p) - sq * b.nmid;
+      const i64 li = pos[static_cast<size_t>(sq)];
+      if (li < 0) {
+        bad[c] = pd.C != 0;
+      } else {
+        bad[c] = pd.R != 1 || pd.C != 1 || pd.core_off != li * b.nmid + t;
+        if (sharded)  // every block G_{t,s} is one element: the exchange tables must say so
+          bad[c] = bad[c] || b.send_off[static_cast<size_t>(t * b.nmid + sq)] < 0;
+      }
     }
   });
   for (char x : bad)
@@ -1990,7 +2029,17 @@ std::unique_ptr<Plan> build_plan_r1(oiobf_tbf& b, i64 nv) {
   pl->nv = nv;
   const int d = b.d;
   const i64 n = b.n;
-  const i64 P = b.nmid * b.nmid;  // elements of every intermediate (per vector)
+  // sharded: the nown owned middle multi-sets in local order (r1_eligible)
+  const std::vector<int> own = b.world > 1 ? owned_list(b) : std::vector<int>();
+  const i64 nown = b.world > 1 ? static_cast<i64>(own.size()) : b.nmid;
+  if (b.world > 1) {
+    pl->sharded = true;
+    pl->d_r1_own = to_device(own, b.stream);
+    pl->d_r1_send_off = to_device(b.send_off, b.stream);
+    pl->d_r1_recv_off = to_device(b.recv_off, b.stream);
+    TBF_CUDA(cudaStreamSynchronize(b.stream));
+  }
+  const i64 P = nown * b.nmid;  // elements of every intermediate (per vector)
   const i64 leaf = n >> b.L;
   auto base = [&](int sd, int l) {
     const LevelData& ld = b.side[sd][static_cast<size_t>(l)];
@@ -2010,7 +2059,7 @@ std::unique_ptr<Plan> build_plan_r1(oiobf_tbf& b, i64 nv) {
     a.nj = ld.L.nj;
     a.njd = ipow(a.nj, d);
     a.pnin = l > 0 ? ipow(2, static_cast<i64>(d) * (l - 1)) : 1;
-    a.ngroups = b.nmid * a.pnin;
+    a.ngroups = nown * a.pnin;
     a.E = a.nj * a.W;
     a.ED = ipow(a.E, d);
     a.fblk = static_cast<int>(d * a.nj * a.W);
@@ -2024,6 +2073,8 @@ std::unique_ptr<Plan> build_plan_r1(oiobf_tbf& b, i64 nv) {
     a.lg_n = lg(n);
     a.lg_mid = lg(a.mid);
     a.lg_nmid = lg(a.nmid);
+    a.lg_nown = lg(nown);
+    a.own = b.world > 1 ? pl->d_r1_own.p : nullptr;
     a.lg_nin = lg(a.nin);
     a.lg_nj = lg(a.nj);
     a.lg_njd = lg(a.njd);
@@ -2067,6 +2118,21 @@ std::unique_ptr<Plan> build_plan_r1(oiobf_tbf& b, i64 nv) {
     const int out_half = l == 0 ? 0 : 1 - cur;
     add(a, l == 0 ? -1 : cur, out_half);
     cur = out_half;
+  }
+  if (b.world > 1) {
+    // exchange: pack the level-Lc V/W output into the send buffer (phase 1);
+    // unpack the receive buffer into the level-Lc P/U input (phase 2)
+    Plan::R1Level pk;
+    pk.args = base(0, b.Lc);
+    pk.in_off = cur * P * nv;
+    pk.out_off = -1;
+    pl->ops.push_back(Op{9, static_cast<i64>(pl->r1_levels.size()), 1});
+    pl->r1_levels.push_back(pk);
+    Plan::R1Level up = pk;
+    up.in_off = -1;
+    up.out_off = cur * P * nv;
+    pl->ops.push_back(Op{10, static_cast<i64>(pl->r1_levels.size()), 2});
+    pl->r1_levels.push_back(up);
   }
   for (int l = b.Lc; l >= 0; --l) {
     R1LevelArgs a = base(1, l);
@@ -2160,6 +2226,14 @@ void run_ops(oiobf_tbf& b, Plan& pl, const OpBuffers& io, cudaStream_t st, int g
       const LevelData& ld = b.side[rl.args.side][static_cast<size_t>(rl.args.l)];
       launch_r1_level(rl.args, ld.interp.p, b.cores.p, rl.in_off < 0 ? io.F : scr + rl.in_off,
                       rl.out_off < 0 ? io.G : scr + rl.out_off, st);
+    } else if (op.kind == 9 || op.kind == 10) {
+      const Plan::R1Level& rl = pl.r1_levels[static_cast<size_t>(op.idx)];
+      if (op.kind == 9)
+        launch_r1_exchange(rl.args, 0, reinterpret_cast<const long long*>(pl.d_r1_send_off.p), scr + rl.in_off,
+                           io.send, st);
+      else
+        launch_r1_exchange(rl.args, 1, reinterpret_cast<const long long*>(pl.d_r1_recv_off.p), io.recv,
+                           scr + rl.out_off, st);
     } else if (op.kind == 7) {
       const GemvLaunch& gl = pl.gemvs[static_cast<size_t>(op.idx)];
       launch_tiny_gemv(pl.d_gemv.p + gl.desc_begin, gl.ndesc, gl.total_rows, static_cast<int>(pl.nv), b.cores.p,
@@ -2846,6 +2920,7 @@ int oiobf_tbf_set_exchange(oiobf_tbf* h, const int64_t* send_off, const int64_t*
   h->recv_elems = recv_elems;
   h->sync_all();
   h->plans.clear();
+  h->r1_ok = -1;  // the sharded rank-one engine needs the exchange tables
   CAPI_END
 }
 
@@ -2857,6 +2932,7 @@ int oiobf_tbf_set_peer_exchange(oiobf_tbf* h, const int64_t* peer_off, const uin
     std::lock_guard<std::mutex> lk(h->mu);
     h->sync_all();
     h->plans.clear();
+    h->r1_ok = -1;
     h->peer_off.clear();
     h->peer_base.clear();
     h->peer_nv_max = 0;

@@ -266,6 +266,45 @@ def test_sharded_gpu_lockstep(world):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("world,balanced", [(2, False), (4, False), (4, True), (3, False)])
+def test_sharded_gpu_lockstep_rank_one(world, balanced):
+    """d = 6 DFT (every ID of rank 1): the sharded phases run on the rank-one
+    engine (local outer indices, pack / unpack around the exchange) when every
+    rank owns the same power-of-two number of middle multi-sets -- world 2, 4,
+    round-robin or a permuted ownership map -- and fall back to the box engine
+    otherwise (world 3); G within 1e-12 of the single-GPU rank-one apply,
+    nv = 1 and 2."""
+    import ctypes as C
+
+    import torch
+
+    import paper_2411_03029_b200 as tb
+    from paper_2411_03029_b200 import _lib
+    from paper_2411_03029_b200.configs import dft
+    from paper_2411_03029_b200.sharded import GpuShardBackend, run_lockstep
+    spec, L, tol = dft(6, 4), 2, 1e-8
+    single = tb.tbf_construct(spec, L, tol, seed=5)
+    assert single.apply_engine() == "rank1"
+    owner = None
+    if balanced:  # any equal-count map: a fixed permutation of the round-robin one
+        nm = 2 ** (spec.d * (L // 2))
+        owner = np.random.default_rng(7).permutation(np.arange(nm) % world).astype(np.int32)
+    rng = np.random.default_rng(3)
+    for nv in (1, 2):
+        shape = (4,) * 6 + ((nv,) if nv > 1 else ())
+        F = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+        G1 = single.contract(F).reshape(-1, order="F")
+        Ft = torch.from_numpy(np.ascontiguousarray(F.reshape(-1, order="F")).view(np.float64).copy()).cuda()
+        backends = [GpuShardBackend(spec, L, tol, tb.ProxyStrategy(), 5, r, world) for r in range(world)]
+        G = run_lockstep(backends, Ft, nv=nv, owner=owner).cpu().numpy().view(np.complex128)
+        eng = C.c_int32()
+        _lib.check(_lib.load().oiobf_tbf_apply_engine(backends[0].h, C.byref(eng)))
+        assert eng.value == (4 if world in (2, 4) else 1), eng.value
+        err = np.linalg.norm(G - G1) / np.linalg.norm(G1)
+        assert err < 1e-12, (nv, err)
+
+
+@pytest.mark.gpu
 def test_bench_sharded_torchrun_validation():
     """bench.py's N > 1 path end to end under torchrun (world 2), in its
     validation mode: gloo collectives staged through the host and both ranks on

@@ -176,6 +176,7 @@ __device__ __forceinline__ void box_mma_f64(double& c0, double& c1, double a, do
 // in flight before the first MMA.  Against the CUDA-core loop this is 16
 // MMAs instead of ~100 DFMAs + their shared-memory operand loads per tile
 // (config 3 first V level: ncu issue slots 40% busy with the FP64 pipe at 31%).
+template <int TP>  // column tiles per step (TP * 4 loads in flight per lane)
 __device__ __forceinline__ void first_mode_global_mma(const BoxDesc& D, int d, const double2* in,
                                                       const double2* __restrict__ Mf, double2* __restrict__ t0,
                                                       int A, int Rs, int ein_f, int nv) {
@@ -196,10 +197,10 @@ __device__ __forceinline__ void first_mode_global_mma(const BoxDesc& D, int d, c
   }
   const int ntiles = (R + 7) >> 3;
 #pragma unroll 1
-  for (int t = warp * 2; t < ntiles; t += nw * 2) {
-    double2 xv[2][4];
+  for (int t = warp * TP; t < ntiles; t += nw * TP) {
+    double2 xv[TP][4];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < TP; ++u) {
       const int col = (t + u) * 8 + li;
       const bool okc = col < R;
       long long addr = 0;
@@ -221,7 +222,7 @@ __device__ __forceinline__ void first_mode_global_mma(const BoxDesc& D, int d, c
       }
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < TP; ++u) {
       double cr0 = 0, cr1 = 0, ci0 = 0, ci1 = 0;
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks)
@@ -339,7 +340,7 @@ struct BoxSmem {
 // in S.D (all threads synchronised after the copy).  `wait` blocks until the
 // input is produced (all threads call it; it ends with a CTA barrier).
 // `phase` is the staging mbarrier's parity, flipped on each bulk staging.
-template <int LD, class Wait>
+template <int LD, int TP, class Wait>  // TP: column tiles per step of the tensor-core first mode
 __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, int crank,
                                          const double2* __restrict__ mats, const double2* in, double2* out,
                                          double2* sm, unsigned& phase, Wait wait) {
@@ -433,7 +434,7 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
       else if (info.amax <= 4) first_mode_smem<4>(xs, Mf, t0, A, Rs, ein_f, nv);
       else first_mode_smem<8>(xs, Mf, t0, A, Rs, ein_f, nv);
     } else if (info.mma && ein_f <= 16) {
-      first_mode_global_mma(D, d, in, Mf, t0, A, Rs, ein_f, nv);
+      first_mode_global_mma<TP>(D, d, in, Mf, t0, A, Rs, ein_f, nv);
     } else {
       first_mode_global<8, LD>(D, d, in, Mf, t0, A, Rs, ein_f, nv);
     }

@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(NT, MINB) k_box(const BoxDesc* __restrict__ de
   }
   __syncthreads();
   unsigned phase = 0;
-  box_body<MINB >= 3 ? 4 : 8>(S, info, crank, mats, in, out, sm, phase, [] { pdl_wait(); });
+  box_body<MINB >= 3 ? 4 : 8, 2>(S, info, crank, mats, in, out, sm, phase, [] { pdl_wait(); });
 }
 
 

@@ -81,10 +81,10 @@ inline std::vector<ColumnID> column_id_batch(const std::vector<const Matrix*>& k
   return res;
 }
 
-// Difference from the reference (id.cpp:124-130, no size limit): at most 96
-// columns (the device keeps the ID's w x w triangular factor in shared
-// memory); wider matrices throw std::invalid_argument.  row_id transposes, so
-// it accepts at most 96 rows; hybrid_id at most 96 of both.
+// Any size, like the reference (id.cpp:124-130): up to 96 columns the device
+// keeps the ID's w x w triangular factor in shared memory (TSQR + reference
+// pivoting on R); wider matrices run the same pivoted Householder QR in global
+// memory, one CTA per matrix (slower; the butterfly's own IDs never need it).
 inline ColumnID column_id(const Matrix& k, double tol, std::optional<std::int64_t> max_rank = std::nullopt) {
   return column_id_batch({&k}, tol, max_rank)[0];
 }

@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libtbf_b200.so")
 OBJ = os.path.join(HERE, "_build")
 SOURCES = ["id_kernels.cu", "apply_kernels.cu", "box_kernels.cu", "core_kernels.cu", "tiny_kernels.cu",
-           "r1_kernels.cu", "box2_kernels.cu", "peak_kernels.cu",
+           "r1_kernels.cu", "box2_kernels.cu", "peak_kernels.cu", "wide_id_kernels.cu",
            "runtime.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",

@@ -206,6 +206,17 @@ struct R1LevelArgs {
 size_t r1_smem_bytes(const R1LevelArgs& a);
 int r1_threads();
 int r1_vthreads();
+// column_id of explicit matrices wider than kMaxW (wide_id_kernels.cu): the
+// reference's pivoted Householder QR in global memory, one CTA per matrix, on
+// a work copy of the matrix (A is overwritten).  Per job: a_off / m / n, n_off
+// = offset of its n-entry norm / perm / pos / skeleton arrays, i_off = offset
+// of its interp (rank x n column-major, room for min(m, n) x n).
+struct WideIdJob {
+  i64 a_off, m, n_off, i_off, max_rank;
+  int n, pad;
+};
+void launch_wide_ids(i64 njobs, const WideIdJob* jobs, double2* A, double* nrm, int* perm, int* pos, double tol,
+                     int* rank, int* sat, int* skel, double2* interp, cudaStream_t st);
 // sharded middle-level exchange of the rank-one engine: unpack = 0 packs the
 // level-Lc V/W output into the send buffer, 1 unpacks the receive buffer into
 // the level-Lc P/U input (off: the exchange offsets per pair t * nmid + s)

@@ -3587,75 +3587,147 @@ int oiobf_column_id_batch(int64_t batch, const int64_t* m, const int64_t* n, con
   require(tol > 0 && tol < 1, "column_id: tolerance must be in (0,1)");
   if (batch == 0) return OIOBF_OK;
   ensure_device();
+  // matrices of up to kMaxW columns: TSQR + reference pivoting on R in shared
+  // memory (k_matrix_panel / k_finish); wider ones: the pivoted Householder QR
+  // in global memory (k_qrcp_wide)
+  std::vector<i64> narrow, wide;
   i64 wmax = 1, mmax = 1, atot = 0;
   for (i64 b = 0; b < batch; ++b) {
     require(m[b] > 0 && n[b] > 0, "column_id: empty matrix");
-    require(n[b] <= kMaxW, "column_id: more than 96 columns not supported by the device kernel");
-    wmax = std::max<i64>(wmax, n[b]);
-    mmax = std::max<i64>(mmax, m[b]);
+    require(n[b] < (i64{1} << 30) && m[b] < (i64{1} << 40), "column_id: matrix too large");
     atot = std::max<i64>(atot, a_off[b] + m[b] * n[b]);
+    if (n[b] <= kMaxW) {
+      narrow.push_back(b);
+      wmax = std::max<i64>(wmax, n[b]);
+      mmax = std::max<i64>(mmax, m[b]);
+    } else {
+      wide.push_back(b);
+    }
   }
   cudaStream_t st;
   TBF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   {
-    LevelDesc L{};
-    L.d = 1;
-    L.nslots = batch;
-    L.wmax = wmax;
-    L.m = mmax;
-    L.pr = wmax <= 16 ? 256 : wmax <= 64 ? 128 : 64;  // R packed: (w(w+1)/2 + pr w) x 16 B fits the 220 KB budget
-    if (const char* e = std::getenv("OIOBF_ID_PR")) L.pr = std::atoi(e);  // debug override
-    i64 parts = std::max<i64>(1, (148 * 8 + batch - 1) / batch);
-    parts = std::min(parts, std::max<i64>(1, (mmax + 4 * L.pr - 1) / (4 * L.pr)));
-    if (const char* e = std::getenv("OIOBF_ID_NPARTS")) parts = std::atoi(e);  // debug override
-    L.nparts = parts;
-    L.rpp = (mmax + parts - 1) / parts;
-    std::vector<int> hw(static_cast<size_t>(batch)), ht(static_cast<size_t>(batch * wmax));
-    std::vector<i64> hm(m, m + batch), hoff(a_off, a_off + batch), hmr(static_cast<size_t>(batch));
-    std::vector<int> hn(static_cast<size_t>(batch));
-    for (i64 b = 0; b < batch; ++b) {
-      hw[static_cast<size_t>(b)] = static_cast<int>(n[b]);
-      hn[static_cast<size_t>(b)] = static_cast<int>(n[b]);
-      hmr[static_cast<size_t>(b)] = max_rank ? max_rank[b] : -1;
-      for (i64 c = 0; c < n[b]; ++c) ht[static_cast<size_t>(b * wmax + c)] = static_cast<int>(c + 1);
-    }
-    DevBuf<int> dw = to_device(hw, st), dt = to_device(ht, st), dn = to_device(hn, st);
-    DevBuf<i64> dm = to_device(hm, st), doff = to_device(hoff, st), dmr = to_device(hmr, st);
     DevBuf<double2> dA(static_cast<size_t>(atot));
     dA.upload(reinterpret_cast<const double2*>(A), static_cast<size_t>(atot), st);
-    DevBuf<double2> rpart(static_cast<size_t>(batch * L.nparts * wmax * wmax));
-    launch_matrix_ids(batch, doff.p, dm.p, dn.p, dA.p, L.nparts, L.rpp, L.pr, wmax, rpart.p, st);
-    DevBuf<int> drank(static_cast<size_t>(batch)), dsat(static_cast<size_t>(batch)),
-        dperm(static_cast<size_t>(batch * wmax)), dsk(static_cast<size_t>(batch * wmax));
-    DevBuf<double2> dint(static_cast<size_t>(batch * wmax * wmax));
-    DevBuf<double> dgap(static_cast<size_t>(batch));
-    launch_finish_var(L, dm.p, tol, kTieEps, dmr.p, rpart.p, dt.p, dw.p, drank.p, dsat.p, dperm.p, dsk.p, dint.p,
-                      dgap.p, st);
-    std::vector<int> hr(static_cast<size_t>(batch)), hs(static_cast<size_t>(batch)),
-        hp(static_cast<size_t>(batch * wmax)), hk(static_cast<size_t>(batch * wmax));
-    std::vector<double2> hi(static_cast<size_t>(batch * wmax * wmax));
-    drank.download(hr.data(), hr.size(), st);
-    dsat.download(hs.data(), hs.size(), st);
-    dperm.download(hp.data(), hp.size(), st);
-    dsk.download(hk.data(), hk.size(), st);
-    dint.download(hi.data(), hi.size(), st);
-    TBF_CUDA(cudaStreamSynchronize(st));
-    for (i64 b = 0; b < batch; ++b) {
-      const int r = hr[static_cast<size_t>(b)];
-      const i64 w = n[b];
-      rank[b] = r;
-      if (saturated) saturated[b] = hs[static_cast<size_t>(b)];
-      double mx = 0;
-      for (i64 q = 0; q < r * w; ++q) {
-        const double2 v = hi[static_cast<size_t>(b * wmax * wmax + q)];
-        interp[2 * (i_off[b] + q)] = v.x;
-        interp[2 * (i_off[b] + q) + 1] = v.y;
-        mx = std::max(mx, std::sqrt(v.x * v.x + v.y * v.y));
+    if (!narrow.empty()) {
+      const i64 nb = static_cast<i64>(narrow.size());
+      LevelDesc L{};
+      L.d = 1;
+      L.nslots = nb;
+      L.wmax = wmax;
+      L.m = mmax;
+      L.pr = wmax <= 16 ? 256 : wmax <= 64 ? 128 : 64;  // R packed: (w(w+1)/2 + pr w) x 16 B fits the 220 KB budget
+      if (const char* e = std::getenv("OIOBF_ID_PR")) L.pr = std::atoi(e);  // debug override
+      i64 parts = std::max<i64>(1, (148 * 8 + nb - 1) / nb);
+      parts = std::min(parts, std::max<i64>(1, (mmax + 4 * L.pr - 1) / (4 * L.pr)));
+      if (const char* e = std::getenv("OIOBF_ID_NPARTS")) parts = std::atoi(e);  // debug override
+      L.nparts = parts;
+      L.rpp = (mmax + parts - 1) / parts;
+      std::vector<int> hw(static_cast<size_t>(nb)), ht(static_cast<size_t>(nb * wmax));
+      std::vector<i64> hm(static_cast<size_t>(nb)), hoff(static_cast<size_t>(nb)), hmr(static_cast<size_t>(nb));
+      std::vector<int> hn(static_cast<size_t>(nb));
+      for (i64 q = 0; q < nb; ++q) {
+        const i64 b = narrow[static_cast<size_t>(q)];
+        hm[static_cast<size_t>(q)] = m[b];
+        hoff[static_cast<size_t>(q)] = a_off[b];
+        hw[static_cast<size_t>(q)] = static_cast<int>(n[b]);
+        hn[static_cast<size_t>(q)] = static_cast<int>(n[b]);
+        hmr[static_cast<size_t>(q)] = max_rank ? max_rank[b] : -1;
+        for (i64 c = 0; c < n[b]; ++c) ht[static_cast<size_t>(q * wmax + c)] = static_cast<int>(c + 1);
       }
-      if (interp_max_abs) interp_max_abs[b] = (r > 0) ? mx : 0.0;
-      for (int q = 0; q < r; ++q) skel[s_off[b] + q] = hk[static_cast<size_t>(b * wmax + q)];
-      if (perm)
-        for (i64 q = 0; q < w; ++q) perm[s_off[b] + q] = hp[static_cast<size_t>(b * wmax + q)];
+      DevBuf<int> dw = to_device(hw, st), dt = to_device(ht, st), dn = to_device(hn, st);
+      DevBuf<i64> dm = to_device(hm, st), doff = to_device(hoff, st), dmr = to_device(hmr, st);
+      DevBuf<double2> rpart(static_cast<size_t>(nb * L.nparts * wmax * wmax));
+      launch_matrix_ids(nb, doff.p, dm.p, dn.p, dA.p, L.nparts, L.rpp, L.pr, wmax, rpart.p, st);
+      DevBuf<int> drank(static_cast<size_t>(nb)), dsat(static_cast<size_t>(nb)),
+          dperm(static_cast<size_t>(nb * wmax)), dsk(static_cast<size_t>(nb * wmax));
+      DevBuf<double2> dint(static_cast<size_t>(nb * wmax * wmax));
+      DevBuf<double> dgap(static_cast<size_t>(nb));
+      launch_finish_var(L, dm.p, tol, kTieEps, dmr.p, rpart.p, dt.p, dw.p, drank.p, dsat.p, dperm.p, dsk.p, dint.p,
+                        dgap.p, st);
+      std::vector<int> hr(static_cast<size_t>(nb)), hs(static_cast<size_t>(nb)),
+          hp(static_cast<size_t>(nb * wmax)), hk(static_cast<size_t>(nb * wmax));
+      std::vector<double2> hi(static_cast<size_t>(nb * wmax * wmax));
+      drank.download(hr.data(), hr.size(), st);
+      dsat.download(hs.data(), hs.size(), st);
+      dperm.download(hp.data(), hp.size(), st);
+      dsk.download(hk.data(), hk.size(), st);
+      dint.download(hi.data(), hi.size(), st);
+      TBF_CUDA(cudaStreamSynchronize(st));
+      for (i64 q = 0; q < nb; ++q) {
+        const i64 b = narrow[static_cast<size_t>(q)];
+        const int r = hr[static_cast<size_t>(q)];
+        const i64 w = n[b];
+        rank[b] = r;
+        if (saturated) saturated[b] = hs[static_cast<size_t>(q)];
+        double mx = 0;
+        for (i64 e = 0; e < r * w; ++e) {
+          const double2 v = hi[static_cast<size_t>(q * wmax * wmax + e)];
+          interp[2 * (i_off[b] + e)] = v.x;
+          interp[2 * (i_off[b] + e) + 1] = v.y;
+          mx = std::max(mx, std::sqrt(v.x * v.x + v.y * v.y));
+        }
+        if (interp_max_abs) interp_max_abs[b] = (r > 0) ? mx : 0.0;
+        for (int e = 0; e < r; ++e) skel[s_off[b] + e] = hk[static_cast<size_t>(q * wmax + e)];
+        if (perm)
+          for (i64 e = 0; e < w; ++e) perm[s_off[b] + e] = hp[static_cast<size_t>(q * wmax + e)];
+      }
+    }
+    if (!wide.empty()) {
+      const i64 nw = static_cast<i64>(wide.size());
+      std::vector<WideIdJob> jobs(static_cast<size_t>(nw));
+      i64 ntot = 0, itot = 0;
+      for (i64 q = 0; q < nw; ++q) {
+        const i64 b = wide[static_cast<size_t>(q)];
+        WideIdJob& J = jobs[static_cast<size_t>(q)];
+        J.a_off = a_off[b];
+        J.m = m[b];
+        J.n = static_cast<int>(n[b]);
+        J.max_rank = max_rank ? max_rank[b] : -1;
+        J.n_off = ntot;
+        J.i_off = itot;
+        J.pad = 0;
+        ntot += n[b];
+        itot += std::min(m[b], n[b]) * n[b];
+      }
+      DevBuf<WideIdJob> djobs = to_device(jobs, st);
+      DevBuf<double> dnrm(static_cast<size_t>(ntot));
+      DevBuf<int> dperm(static_cast<size_t>(ntot)), dpos(static_cast<size_t>(ntot)), dsk(static_cast<size_t>(ntot)),
+          drank(static_cast<size_t>(nw)), dsat(static_cast<size_t>(nw));
+      DevBuf<double2> dint(static_cast<size_t>(std::max<i64>(itot, 1)));
+      launch_wide_ids(nw, djobs.p, dA.p, dnrm.p, dperm.p, dpos.p, tol, drank.p, dsat.p, dsk.p, dint.p, st);
+      std::vector<int> hr(static_cast<size_t>(nw)), hs(static_cast<size_t>(nw)), hp(static_cast<size_t>(ntot)),
+          hk(static_cast<size_t>(ntot));
+      drank.download(hr.data(), hr.size(), st);
+      dsat.download(hs.data(), hs.size(), st);
+      dperm.download(hp.data(), hp.size(), st);
+      dsk.download(hk.data(), hk.size(), st);
+      TBF_CUDA(cudaStreamSynchronize(st));
+      for (i64 q = 0; q < nw; ++q) {
+        const i64 b = wide[static_cast<size_t>(q)];
+        const WideIdJob& J = jobs[static_cast<size_t>(q)];
+        const int r = hr[static_cast<size_t>(q)];
+        const i64 w = n[b];
+        rank[b] = r;
+        if (saturated) saturated[b] = hs[static_cast<size_t>(q)];
+        std::vector<double2> hi(static_cast<size_t>(std::max<i64>(r * w, 1)));
+        if (r > 0) {
+          TBF_CUDA(cudaMemcpyAsync(hi.data(), dint.p + J.i_off, sizeof(double2) * static_cast<size_t>(r * w),
+                                   cudaMemcpyDeviceToHost, st));
+          TBF_CUDA(cudaStreamSynchronize(st));
+        }
+        double mx = 0;
+        for (i64 e = 0; e < r * w; ++e) {
+          const double2 v = hi[static_cast<size_t>(e)];
+          interp[2 * (i_off[b] + e)] = v.x;
+          interp[2 * (i_off[b] + e) + 1] = v.y;
+          mx = std::max(mx, std::sqrt(v.x * v.x + v.y * v.y));
+        }
+        if (interp_max_abs) interp_max_abs[b] = (r > 0) ? mx : 0.0;
+        for (int e = 0; e < r; ++e) skel[s_off[b] + e] = hk[static_cast<size_t>(J.n_off + e)];
+        if (perm)
+          for (i64 e = 0; e < w; ++e) perm[s_off[b] + e] = hp[static_cast<size_t>(J.n_off + e)];
+      }
     }
   }
   cudaStreamDestroy(st);

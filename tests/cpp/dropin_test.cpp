@@ -102,6 +102,37 @@ int main(int argc, char** argv) {
     bad_tol = true;
   }
   js << "\"bad_tol_rejected\":" << (bad_tol ? "true" : "false") << ",";
+  // 5b. IDs wider than the shared-memory kernels hold (150 > 96 columns / rows):
+  // column_id, row_id and hybrid_id of a rank-30 matrix reconstruct it
+  {
+    Matrix Bw(140, 30), Cw(30, 150);
+    for (int i = 0; i < 140; ++i)
+      for (int j = 0; j < 30; ++j) Bw(i, j) = Complex(nd(rng), nd(rng));
+    for (int i = 0; i < 30; ++i)
+      for (int j = 0; j < 150; ++j) Cw(i, j) = Complex(nd(rng), nd(rng));
+    const Matrix Aw = Bw * Cw;
+    double an = 0;
+    for (int i = 0; i < 140; ++i)
+      for (int j = 0; j < 150; ++j) an += std::norm(Aw(i, j));
+    const ColumnID cw = column_id(Aw, 1e-9);
+    double ce = 0;  // || A(:, J) X - A ||
+    for (int i = 0; i < 140; ++i)
+      for (int j = 0; j < 150; ++j) {
+        Complex acc(0, 0);
+        for (std::int64_t q = 0; q < cw.rank; ++q) acc += Aw(i, cw.skeleton[static_cast<std::size_t>(q)] - 1) * cw.interp(q, j);
+        ce += std::norm(acc - Aw(i, j));
+      }
+    const RowID rw = row_id(Aw, 1e-9);
+    double re = 0;  // || X A(I, :) - A ||
+    for (int i = 0; i < 140; ++i)
+      for (int j = 0; j < 150; ++j) {
+        Complex acc(0, 0);
+        for (std::int64_t q = 0; q < rw.rank; ++q) acc += rw.interp(i, q) * Aw(rw.skeleton[static_cast<std::size_t>(q)] - 1, j);
+        re += std::norm(acc - Aw(i, j));
+      }
+    js << "\"wide_cid_rank\":" << cw.rank << ",\"wide_cid_err\":" << std::sqrt(ce / an) << ",\"wide_rid_rank\":" << rw.rank
+       << ",\"wide_rid_err\":" << std::sqrt(re / an) << ",";
+  }
   // 6. scalar evaluation through the functor (GPU) == batched entry
   const Complex e1 = k2(MultiIndex{3, 4}, MultiIndex{5, 6});
   const DenseTensor e2 = subtensor_at(k2, {{3}, {4}}, {{5}, {6}});

@@ -64,3 +64,6 @@ def test_dropin_matches_reference(ref, oracle):
     assert r["tbf_err"] < 1e-5
     assert r["tbf_err_estimate"] < 1e-4
     assert r["opaque_rejected"] and r["bad_tol_rejected"] and r["scalar_matches"]
+    # matrices wider than 96 columns / rows (the global-memory pivoted QR)
+    assert r["wide_cid_rank"] == 30 and r["wide_rid_rank"] == 30
+    assert r["wide_cid_err"] < 1e-8 and r["wide_rid_err"] < 1e-8

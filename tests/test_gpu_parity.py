@@ -54,6 +54,38 @@ def test_column_id_matches_oracle(oracle):
             assert not g.saturated
 
 
+def test_column_id_wide_matches_oracle(oracle):
+    """Matrices wider than the shared-memory ID kernels hold (n > 96): the
+    global-memory pivoted QR (k_qrcp_wide) reproduces the reference semantics
+    -- rank, pivot order and sorted skeleton equal to the oracle's own qrcp
+    (forced replay only inside a tie), interpolation to rounding level --
+    also mixed with narrow matrices in one batch, with a rank limit
+    (saturation) and for a matrix with more columns than rows."""
+    rng = np.random.default_rng(12)
+    mats = []
+    for m, n, r in ((400, 97, 20), (300, 150, 40), (1200, 257, 60), (64, 200, 64), (500, 130, 130), (50, 12, 5)):
+        U = rand_c(rng, (m, r)) * (0.5 ** (np.arange(r) / 2))
+        mats.append(U @ rand_c(rng, (r, n)))
+    for tol in (1e-4, 1e-9):
+        got = tb.column_id_batch(mats, tol)
+        for A, g in zip(mats, got):
+            o = oracle.column_id(A, tol, forced_perm=g.perm, forced_rank=g.rank, tie_eps=TIE_EPS)
+            assert not o["mismatch"], "GPU pivot/rank differs from oracle outside a tie"
+            assert g.rank == o["rank"] and g.rank > 0
+            np.testing.assert_array_equal(g.skeleton, o["skeleton"])
+            assert np.all(np.diff(g.skeleton) > 0)
+            Ask = A[:, g.skeleton - 1]
+            d = np.linalg.norm(Ask @ (g.interp - o["interp"])) / np.linalg.norm(A)
+            assert d <= 1e-12, f"interpolation differs by {d:.2e}"
+            assert np.linalg.norm(Ask @ g.interp - A) <= 50 * tol * np.linalg.norm(A)
+            assert not g.saturated
+    A = mats[1]
+    g = tb.column_id(A, 1e-12, max_rank=7)
+    o = oracle.column_id(A, 1e-12, max_rank=7)
+    assert g.saturated and o["saturated"] and g.rank == 7 == o["rank"]
+    np.testing.assert_array_equal(g.skeleton, o["skeleton"])
+
+
 def test_column_id_max_rank_and_errors(oracle):
     rng = np.random.default_rng(11)
     A = rand_c(rng, (200, 10)) @ rand_c(rng, (10, 12))

@@ -380,7 +380,12 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
     double2* Sm = smat + S.mo[k];
     for (int q = tid; q < ein * eo; q += box_nt()) {
       const int x = qdiv(q, eo), a = q - x * eo + a0;
-      Sm[q] = __ldg(M + (tr ? x + mrows * a : a + mrows * x));
+      const double2* src = M + (tr ? x + mrows * a : a + mrows * x);
+      // asynchronous copies: the staging loads below are issued behind them
+      // without waiting for the factor rows to land (one memory latency less
+      // on every CTA's critical path)
+      if (info.afac) cp_async16(Sm + q, src);
+      else Sm[q] = __ldg(src);
     }
   }
   // ---- the input box is produced by an earlier launch / item
@@ -423,6 +428,7 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
       }
     }
   }
+  if (info.afac) cp_async_wait_all();
   __syncthreads();
   // ---- mode d-1: column r = rs + Rs * v  ->  t0[rs + Rs * (i + A * v)]
   {

@@ -1243,6 +1243,8 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
     {  // FP64 tensor-core phases (OIOBF_BOX_MMA=0: the CUDA-core loops)
       const char* e = std::getenv("OIOBF_BOX_MMA");
       bl.info.mma = e && std::strcmp(e, "0") == 0 ? 0 : 1;
+      const char* e2 = std::getenv("OIOBF_BOX_ASYNC_FAC");  // 0: blocking factor loads
+      bl.info.afac = e2 && std::strcmp(e2, "0") == 0 ? 0 : 1;
     }
     bl.info.smem_mat = static_cast<int>(smem_mat);
     bl.info.smem_in = static_cast<int>(smem_in);

@@ -119,6 +119,36 @@ __device__ __forceinline__ void first_mode_smem(const double2* __restrict__ xs, 
   }
 }
 
+// the same for boxes with few columns (R <= half the CTA: the P / U side's
+// small inputs, e.g. 7 x 7 columns on 128 threads): a task is (column, group of
+// 4 output rows), so 2-4x as many threads work; every output is still summed
+// over x in order (bit-identical to first_mode_smem)
+__device__ __forceinline__ void first_mode_smem_split(const double2* __restrict__ xs, const double2* __restrict__ Mf,
+                                                      double2* __restrict__ t0, int A, int Rs, int ein_f, int nv) {
+  const int R = Rs * nv;
+  const int G = (A + 3) >> 2;
+  for (int t = threadIdx.x; t < R * G; t += box_nt()) {
+    const int g = qdiv(t, R), r = t - g * R;
+    const int v = qdiv(r, Rs), rs = r - v * Rs;
+    const int i0 = g * 4, na = min(4, A - i0);
+    double2 acc[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] = make_double2(0, 0);
+    const double2* col = xs + rs + Rs * ein_f * v;
+#pragma unroll 4
+    for (int x = 0; x < ein_f; ++x) {
+      const double2 v0 = col[x * Rs];
+      const double2* m = Mf + x * A + i0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i < na) cfma(acc[i], v0, m[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i < na) t0[rs + Rs * (i0 + i + A * v)] = acc[i];
+  }
+}
+
 // mode d-1 streamed from global memory (input box too large to stage)
 template <int AM, int LD>  // LD: loads in flight per thread (8 where the register budget allows)
 __device__ __forceinline__ void first_mode_global(const BoxDesc& D, int d, const double2* in,
@@ -435,7 +465,9 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
     // (the row count is dispatched to its register bucket: no predicated-off
     // FMAs; one bucket is hot per launch, so the i-cache footprint stays)
     const double2* Mf = smat + S.mo[f];
-    if (info.stage) {
+    if (info.stage && info.split1 && A > 4 && 2 * Rs * nv <= box_nt()) {
+      first_mode_smem_split(xs, Mf, t0, A, Rs, ein_f, nv);
+    } else if (info.stage) {
       if (info.amax <= 2) first_mode_smem<2>(xs, Mf, t0, A, Rs, ein_f, nv);
       else if (info.amax <= 4) first_mode_smem<4>(xs, Mf, t0, A, Rs, ein_f, nv);
       else first_mode_smem<8>(xs, Mf, t0, A, Rs, ein_f, nv);

@@ -130,7 +130,8 @@ struct BoxLaunchInfo {
   int smem_t1;                    // elements of intermediate buffer t1 (odd middle modes, staging table)
   int nt;                         // CTA size (256, or 128 for small boxes at up to 6 CTAs per SM)
   int mma;                        // 1: FP64 tensor-core phases (unstaged mode d-1 with <= 16 input rows)
-  int afac, pad_;                 // 1: factor rows copied with cp.async (overlap the input staging)
+  int afac;                       // 1: factor rows copied with cp.async (overlap the input staging)
+  int split1;                     // 1: staged first mode splits a column's output rows over threads when columns are few
 };
 void launch_box(i64 nitems, const BoxDesc* descs, const BoxLaunchInfo& info, const double2* mats,
                 const double2* in, double2* out, cudaStream_t st);

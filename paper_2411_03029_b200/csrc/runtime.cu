@@ -1129,6 +1129,10 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
   // Record one box launch for descs (all of one side/level [/slab group]):
   // CTAs per box, amax bucket, input staging and shared-memory sizes; false
   // when a box does not fit on chip (the caller falls back to mode products).
+  auto bl_split1 = [] {
+    const char* e3 = std::getenv("OIOBF_BOX_SPLIT1");
+    return !(e3 && std::strcmp(e3, "0") == 0);
+  };
   auto commit_boxes = [&](std::vector<BoxDesc>& descs, int sd, int l, int in_buf, int out_buf, int transpose,
                           int group) -> bool {
     if (d < 2) return false;
@@ -1142,7 +1146,12 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
     }
     descs.swap(keep);
     if (descs.empty()) return true;
-    const int cs_env = std::getenv("OIOBF_BOX_SPLIT") ? std::atoi(std::getenv("OIOBF_BOX_SPLIT")) : 0;
+    int cs_env = std::getenv("OIOBF_BOX_SPLIT") ? std::atoi(std::getenv("OIOBF_BOX_SPLIT")) : 0;
+    // per-launch override for experiments: OIOBF_BOX_SPLIT_AT="side:level:cs"
+    if (const char* e = std::getenv("OIOBF_BOX_SPLIT_AT")) {
+      int es = -1, el = -1, ec = 0;
+      if (std::sscanf(e, "%d:%d:%d", &es, &el, &ec) == 3 && es == sd && el == l) cs_env = ec;
+    }
     // CTA size and input staging overrides (read per plan build: A/B sweeps)
     const int nt_env = std::getenv("OIOBF_BOX_NT") ? std::atoi(std::getenv("OIOBF_BOX_NT")) : 0;
     const int stage_env = std::getenv("OIOBF_BOX_STAGE") ? std::atoi(std::getenv("OIOBF_BOX_STAGE")) : -1;
@@ -1160,6 +1169,24 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
       ef_max = std::max(ef_max, x.eout[f]);
       sums |= x.nsum > 1;
     }
+    // Output rows of mode d-1 per CTA: at most 8 (register accumulators of the
+    // first mode), or 16 for staged boxes with few columns, whose first mode
+    // splits the rows over threads in groups of 4 (first_mode_smem_split) --
+    // then a P / U box is one CTA and its input (the ordered child sums) is
+    // staged once instead of once per half
+    int rs_max = 0;
+    for (const BoxDesc& x : descs) {
+      int rs = 1;
+      for (int k = 0; k < f; ++k) rs *= x.ein[k];
+      rs_max = std::max(rs_max, rs);
+    }
+    const char* a16env = std::getenv("OIOBF_BOX_A16");
+    // (boxes without child sums -- the first P level, fed by the core GEMV --
+    // qualify as well: with so few columns the input is a few KB and is staged)
+    const bool a16 = !(a16env && std::strcmp(a16env, "0") == 0) && (sums || a16env == nullptr || std::strcmp(a16env, "1") != 0) &&
+                     bl_split1() && ef_max > 8 && ef_max <= 16 && 2 * static_cast<i64>(rs_max) * nv <= box_nt &&
+                     cs_env <= 0;
+    const int amax_cap = a16 ? 16 : 8;
     struct Cfg {
       int cs = 0, amax_rows = 0;
       i64 smem_mat = 0, smem_in = 0, smem_t = 0, smem_t1 = 0;  // t0: modes f, f-2, ...; t1: f-1, f-3, ...
@@ -1196,16 +1223,16 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
       // CTA reads once only lowers occupancy)
       c.stage = sums || (c.smem_mat + c.smem_in + 2 * std::max(c.smem_t, c.smem_t1)) * 16 <= 112 * 1024;
       if ((stage_env == 0 || (stage_env < 0 && box_nt == 128)) && !sums) c.stage = false;
-      if (stage_env == 1) c.stage = true;
+      if (stage_env == 1 || a16) c.stage = true;
       if (!c.stage) c.smem_in = 0;
-      c.fits = c.amax_rows <= 8 && c.total() <= kMaxDynSmem / 16;
+      c.fits = c.amax_rows <= amax_cap && c.total() <= kMaxDynSmem / 16;
       return c;
     };
     auto bucket = [](int rows) { return rows <= 2 ? 2 : rows <= 4 ? 4 : 8; };
-    // largest split that still runs in one wave (at least ceil(ef / 8) CTAs
-    // per box, at most one output row of mode d-1 per CTA)
+    // largest split that still runs in one wave (at least ceil(ef / amax_cap)
+    // CTAs per box, at most one output row of mode d-1 per CTA)
     // (a CTA whose share of a narrow box is empty just exits early)
-    const int cs_lo = std::max(1, (ef_max + 7) / 8);
+    const int cs_lo = std::max(1, (ef_max + amax_cap - 1) / amax_cap);
     Cfg best = size_for(cs_lo);
     if (!best.fits) return false;
     if (cs_env > 0) {

@@ -47,13 +47,18 @@ bool pdl_enabled() {
 constexpr size_t kBox3Smem = 72 * 1024;  // three CTAs per SM fit in shared memory
 
 using BoxKernel = void (*)(const BoxDesc*, BoxLaunchInfo, const double2*, const double2*, double2*);
-constexpr size_t kBox6Smem = 36 * 1024;  // six 128-thread CTAs per SM fit in shared memory
+// 128-thread CTAs whose shared memory lets five or six co-reside take the
+// 80-register instance (OIOBF_BOX6_KB overrides the threshold for A/B runs)
+size_t box6_smem() {
+  const char* e = std::getenv("OIOBF_BOX6_KB");
+  return static_cast<size_t>(e ? std::atoi(e) : 47) * 1024;
+}
 
 // kernel instance for a launch: 128 threads at 6 CTAs / SM (80 registers) for
 // small boxes, 256 threads at 3 (80 registers) or 2 (128: large boxes, and
 // streamed inputs whose 8 loads in flight would spill at 80) CTAs / SM
 BoxKernel box_kernel(int nt, int stage, size_t smem) {
-  if (nt == 128) return smem <= kBox6Smem ? k_box<128, 6> : k_box<128, 3>;
+  if (nt == 128) return smem <= box6_smem() ? k_box<128, 6> : k_box<128, 3>;
   return smem <= kBox3Smem && stage ? k_box<256, 3> : k_box<256, 2>;
 }
 

@@ -1153,7 +1153,11 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
       if (std::sscanf(e, "%d:%d:%d", &es, &el, &ec) == 3 && es == sd && el == l) cs_env = ec;
     }
     // CTA size and input staging overrides (read per plan build: A/B sweeps)
-    const int nt_env = std::getenv("OIOBF_BOX_NT") ? std::atoi(std::getenv("OIOBF_BOX_NT")) : 0;
+    int nt_env = std::getenv("OIOBF_BOX_NT") ? std::atoi(std::getenv("OIOBF_BOX_NT")) : 0;
+    if (const char* e = std::getenv("OIOBF_BOX_NT_AT")) {  // per-launch override: "side:level:nt"
+      int es = -1, el = -1, en = 0;
+      if (std::sscanf(e, "%d:%d:%d", &es, &el, &en) == 3 && es == sd && el == l) nt_env = en;
+    }
     const int stage_env = std::getenv("OIOBF_BOX_STAGE") ? std::atoi(std::getenv("OIOBF_BOX_STAGE")) : -1;
     // many small boxes (config 3: 4096 per level): 128-thread CTAs, up to 6
     // per SM, and (without child sums) no input staging -- mode d-1 streams

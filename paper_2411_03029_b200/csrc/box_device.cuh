@@ -324,36 +324,43 @@ constexpr int kColTab = 512;  // output columns whose offsets are tabulated in s
 
 // mode 0 -> global: task (a, 4 consecutive columns); column c = (a_1 .. a_{d-2}, i, v)
 // tab: per-column offsets (Cc <= kColTab), or null (computed per store)
+template <int CPT>  // columns per task
 __device__ __forceinline__ void last_mode(const BoxDesc& D, int d, int lo, int A, const double2* __restrict__ src,
                                           const double2* __restrict__ M0, int Cc, const long long* tab,
                                           double2* __restrict__ out) {
   const int ein = D.ein[0], eo = D.eout[0];
-  const int ncg = (Cc + 3) >> 2;
+  const int ncg = (Cc + CPT - 1) / CPT;
   const int ntask = eo * ncg;
   for (int t = threadIdx.x; t < ntask; t += box_nt()) {
     const int cg = qdiv(t, eo), a = t - cg * eo;
-    const int c0 = cg * 4;
-    const int nc = min(4, Cc - c0);
-    double2 acc[4];
+    const int c0 = cg * CPT;
+    const int nc = min(CPT, Cc - c0);
+    double2 acc[CPT];
 #pragma unroll
-    for (int g = 0; g < 4; ++g) acc[g] = make_double2(0, 0);
+    for (int g = 0; g < CPT; ++g) acc[g] = make_double2(0, 0);
     const double2* s = src + ein * c0;
 #pragma unroll 4
     for (int x = 0; x < ein; ++x) {
       const double2 m = M0[x * eo + a];
 #pragma unroll
-      for (int g = 0; g < 4; ++g)
+      for (int g = 0; g < CPT; ++g)
         if (g < nc) cfma(acc[g], s[x + ein * g], m);
     }
     const long long base = D.out_off + static_cast<long long>(a) * D.out_stride[0];
     if (tab) {
 #pragma unroll
-      for (int g = 0; g < 4; ++g)
+      for (int g = 0; g < CPT; ++g)
         if (g < nc) out[base + tab[c0 + g]] = acc[g];
     } else {
 #pragma unroll 1
       for (int g = 0; g < nc; ++g)
-        out[base + col_offset(D, d, lo, A, c0 + g)] = g == 0 ? acc[0] : g == 1 ? acc[1] : g == 2 ? acc[2] : acc[3];
+      {
+        double2 v = acc[0];  // (static indexing keeps the accumulators in registers)
+#pragma unroll
+        for (int q = 1; q < CPT; ++q)
+          if (g == q) v = acc[q];
+        out[base + col_offset(D, d, lo, A, c0 + g)] = v;
+      }
     }
   }
 }
@@ -499,7 +506,7 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
     for (int c = tid; c < Cc; c += box_nt()) S.coltab[c] = col_offset(D, d, lo, A, c);
   __syncthreads();
   // ---- mode 0 -> global
-  last_mode(D, d, lo, A, src, smat + S.mo[0], Cc, tab ? S.coltab : nullptr, out);
+  last_mode<4>(D, d, lo, A, src, smat + S.mo[0], Cc, tab ? S.coltab : nullptr, out);
   __syncthreads();
 }
 

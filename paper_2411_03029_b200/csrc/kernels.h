@@ -132,6 +132,7 @@ struct BoxLaunchInfo {
   int mma;                        // 1: FP64 tensor-core phases (unstaged mode d-1 with <= 16 input rows)
   int afac;                       // 1: factor rows copied with cp.async (overlap the input staging)
   int split1;                     // 1: staged first mode splits a column's output rows over threads when columns are few
+  int pad_;
 };
 void launch_box(i64 nitems, const BoxDesc* descs, const BoxLaunchInfo& info, const double2* mats,
                 const double2* in, double2* out, cudaStream_t st);

@@ -365,6 +365,69 @@ __device__ __forceinline__ void last_mode(const BoxDesc& D, int d, int lo, int A
   }
 }
 
+// mode 0 -> global on the FP64 tensor core (ein <= 16, eout <= 16, tabulated
+// columns):  out(a, c) = sum_x M0(a, x) src(x, c)  as m8n8k4 MMAs with
+//   A = M0 (rows a of one 8-row tile, k = x; fragments in registers for the
+//       whole phase), B = 8 columns of the staged intermediate (lane l: column
+//       8 tile + l / 4, x = 4 ks + l % 4: one 16-byte shared-memory load per
+//       k-step), D = out(8 mt + l / 4, 8 tile + 2 (l % 4) + {0, 1}) stored
+//       straight to global memory (8 consecutive a per column = 128 contiguous
+//       bytes); complex = four real MMAs.
+// A column tile costs ein / 4 loads and 4 ein / 4 MMAs per row tile instead
+// of five shared-memory operands per four complex FMAs.  Measured (config 3):
+// on the V / W side (one row tile, 14-16 input rows) 1.028 -> 1.020 ms; on the
+// P / U side (two row tiles, 5-8 input rows padded to 8: the same FP64 pipe
+// time as the CUDA-core loop) 22 us slower, so the default uses it for V / W
+// only (info.mma == 2; 3 = both sides).
+__device__ __forceinline__ void last_mode_mma(const BoxDesc& D, const double2* __restrict__ src,
+                                              const double2* __restrict__ M0, int Cc, const long long* tab,
+                                              double2* __restrict__ out) {
+  const int ein = D.ein[0], eo = D.eout[0];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = box_nt() >> 5;
+  const int li = lane >> 2, lk = lane & 3;
+  const int ntiles = (Cc + 7) >> 3;
+  const long long s0 = D.out_stride[0];
+#pragma unroll 1
+  for (int mt = 0; mt * 8 < eo; ++mt) {
+    const int a = mt * 8 + li;
+    double mr[4], mi[4], mn[4];
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int x = 4 * ks + lk;
+      double2 m = make_double2(0, 0);
+      if (a < eo && x < ein) m = M0[x * eo + a];
+      mr[ks] = m.x;
+      mi[ks] = m.y;
+      mn[ks] = -m.y;
+    }
+    const long long base = D.out_off + static_cast<long long>(a) * s0;
+#pragma unroll 1
+    for (int t = warp; t < ntiles; t += nw) {
+      const int c = t * 8 + li;
+      double2 xv[4];
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const int x = 4 * ks + lk;
+        xv[ks] = c < Cc && x < ein ? src[x + ein * c] : make_double2(0, 0);
+      }
+      double cr0 = 0, cr1 = 0, ci0 = 0, ci1 = 0;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+        if (4 * ks < ein) {
+          box_mma_f64(cr0, cr1, mr[ks], xv[ks].x);
+          box_mma_f64(ci0, ci1, mr[ks], xv[ks].y);
+          box_mma_f64(cr0, cr1, mn[ks], xv[ks].y);
+          box_mma_f64(ci0, ci1, mi[ks], xv[ks].x);
+        }
+      if (a < eo) {
+        const int c0 = t * 8 + 2 * lk;
+        if (c0 < Cc) out[base + tab[c0]] = make_double2(cr0, ci0);
+        if (c0 + 1 < Cc) out[base + tab[c0 + 1]] = make_double2(cr1, ci1);
+      }
+    }
+  }
+}
+
 // Shared-memory state of one box CTA besides the dynamic buffer.
 struct BoxSmem {
   BoxDesc D;
@@ -506,7 +569,10 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
     for (int c = tid; c < Cc; c += box_nt()) S.coltab[c] = col_offset(D, d, lo, A, c);
   __syncthreads();
   // ---- mode 0 -> global
-  last_mode<4>(D, d, lo, A, src, smat + S.mo[0], Cc, tab ? S.coltab : nullptr, out);
+  if (tab && D.ein[0] <= 16 && D.eout[0] <= 16 && (info.mma == 3 || (info.mma == 2 && !info.transpose)))
+    last_mode_mma(D, src, smat + S.mo[0], Cc, S.coltab, out);
+  else
+    last_mode<4>(D, d, lo, A, src, smat + S.mo[0], Cc, tab ? S.coltab : nullptr, out);
   __syncthreads();
 }
 

@@ -702,9 +702,10 @@ def test_box_cta_variants_bit_identical(oracle, monkeypatch, name, spec, tol, L)
     """Both CTA variants of the fused-box engine do the same operations in the
     same order on the CUDA cores: 256-thread CTAs staging their input and
     128-thread CTAs streaming it from L2 give bit-identical G, within 1e-10
-    of the oracle on the same factors; nv = 1, 2.  The FP64 tensor-core first
-    mode of the streaming CTAs (the default) sums in MMA order: within 1e-13
-    of the CUDA-core result."""
+    of the oracle on the same factors; nv = 1, 2.  The FP64 tensor-core phases
+    of the streaming CTAs (first mode and V/W-side mode 0 by default; mode 0 of
+    both sides as an option) sum in MMA order: within 1e-13 of the CUDA-core
+    result."""
     bf = tb.tbf_construct(spec, L, tol, seed=3)
     tbo = oracle.tbf_construct(spec, L, tol, seed=3, replay=bf.export())
     rng = np.random.default_rng(23)
@@ -714,7 +715,7 @@ def test_box_cta_variants_bit_identical(oracle, monkeypatch, name, spec, tol, L)
         F = rand_c(rng, shape)
         outs = []
         for env in ({"OIOBF_BOX_NT": "256", "OIOBF_BOX_MMA": "0"}, {"OIOBF_BOX_NT": "128", "OIOBF_BOX_MMA": "0"},
-                    {"OIOBF_BOX_NT": "128", "OIOBF_BOX_MMA": "1"}):
+                    {"OIOBF_BOX_NT": "128", "OIOBF_BOX_MMA": "2"}, {"OIOBF_BOX_NT": "128", "OIOBF_BOX_MMA": "3"}):
             for k, v in env.items():
                 monkeypatch.setenv(k, v)
             bf.set_apply_engine("tiny")  # drop cached plans
@@ -723,9 +724,11 @@ def test_box_cta_variants_bit_identical(oracle, monkeypatch, name, spec, tol, L)
             for k in env:
                 monkeypatch.delenv(k)
         assert np.array_equal(outs[0], outs[1])
-        assert rel(outs[2], outs[1]) < 1e-13
-        assert rel(outs[1], tbo.contract(F)) < 1e-10
-        assert rel(outs[2], tbo.contract(F)) < 1e-10
+        Go = tbo.contract(F)
+        assert rel(outs[1], Go) < 1e-10
+        for g in outs[2:]:  # tensor-core phases: first mode + V/W mode 0 (default), and every mode 0
+            assert rel(g, outs[1]) < 1e-13
+            assert rel(g, Go) < 1e-10
     bf.set_apply_engine("auto")
 
 

@@ -306,6 +306,54 @@ __device__ __forceinline__ void middle_mode(const double2* __restrict__ src, dou
   }
 }
 
+// middle mode k on the FP64 tensor core (eo <= 8 output rows, ein <= 16):
+// per slice c, dst(b, a) = sum_x M(a, x) src(b, x) with A = M (rows a, k = x;
+// fragments in registers), B = 8 consecutive b of the slice (lane l: b = 8
+// tile + l / 4, x = 4 ks + l % 4), D = dst(8 tile + 2 (l % 4) + {0, 1}, a = l / 4).
+__device__ __forceinline__ void middle_mode_mma(const double2* __restrict__ src, double2* __restrict__ dst,
+                                                const double2* __restrict__ Mk, int B, int ein, int eo, int Cc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = box_nt() >> 5;
+  const int li = lane >> 2, lk = lane & 3;
+  double mr[4], mi[4], mn[4];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int x = 4 * ks + lk;
+    double2 m = make_double2(0, 0);
+    if (li < eo && x < ein) m = Mk[x * eo + li];
+    mr[ks] = m.x;
+    mi[ks] = m.y;
+    mn[ks] = -m.y;
+  }
+  const int nbt = (B + 7) >> 3;
+#pragma unroll 1
+  for (int t = warp; t < nbt * Cc; t += nw) {
+    const int c = qdiv(t, nbt), b0 = (t - c * nbt) * 8;
+    const double2* s = src + B * ein * c;
+    const int b = b0 + li;
+    double2 xv[4];
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int x = 4 * ks + lk;
+      xv[ks] = b < B && x < ein ? s[b + B * x] : make_double2(0, 0);
+    }
+    double cr0 = 0, cr1 = 0, ci0 = 0, ci1 = 0;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks)
+      if (4 * ks < ein) {
+        box_mma_f64(cr0, cr1, mr[ks], xv[ks].x);
+        box_mma_f64(ci0, ci1, mr[ks], xv[ks].y);
+        box_mma_f64(cr0, cr1, mn[ks], xv[ks].y);
+        box_mma_f64(ci0, ci1, mi[ks], xv[ks].x);
+      }
+    if (li < eo) {
+      double2* o = dst + B * (li + eo * c);
+      const int bb = b0 + 2 * lk;
+      if (bb < B) o[bb] = make_double2(cr0, ci0);
+      if (bb + 1 < B) o[bb + 1] = make_double2(cr1, ci1);
+    }
+  }
+}
+
 // global offset (modes 1..d-1, nv) of output column c = (a_1 .. a_{d-2}, i, v)
 __device__ __forceinline__ long long col_offset(const BoxDesc& D, int d, int lo, int A, int c) {
   const int f = d - 1;
@@ -556,7 +604,8 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
     const int ein = D.ein[k], eo = D.eout[k];
     int B = 1;
     for (int p = 0; p < k; ++p) B *= D.ein[p];
-    middle_mode(src, dst, smat + S.mo[k], B, ein, eo, Cc);
+    if (info.mma >= 4 && !info.transpose && eo <= 8 && ein <= 16) middle_mode_mma(src, dst, smat + S.mo[k], B, ein, eo, Cc);
+    else middle_mode(src, dst, smat + S.mo[k], B, ein, eo, Cc);
     __syncthreads();
     Cc *= eo;
     double2* tmp = src;
@@ -569,7 +618,7 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
     for (int c = tid; c < Cc; c += box_nt()) S.coltab[c] = col_offset(D, d, lo, A, c);
   __syncthreads();
   // ---- mode 0 -> global
-  if (tab && D.ein[0] <= 16 && D.eout[0] <= 16 && (info.mma == 3 || (info.mma == 2 && !info.transpose)))
+  if (tab && D.ein[0] <= 16 && D.eout[0] <= 16 && (info.mma == 3 || ((info.mma == 2 || info.mma >= 4) && !info.transpose)))
     last_mode_mma(D, src, smat + S.mo[0], Cc, S.coltab, out);
   else
     last_mode<4>(D, d, lo, A, src, smat + S.mo[0], Cc, tab ? S.coltab : nullptr, out);

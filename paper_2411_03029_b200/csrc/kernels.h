@@ -130,7 +130,8 @@ struct BoxLaunchInfo {
   int smem_t1;                    // elements of intermediate buffer t1 (odd middle modes, staging table)
   int nt;                         // CTA size (256, or 128 for small boxes at up to 6 CTAs per SM)
   int mma;                        // FP64 tensor-core phases: 1 = unstaged mode d-1 (<= 16 input rows), 2 = and
-                                  // mode 0 of the V / W side, 3 = and mode 0 of both sides
+                                  // mode 0 of the V / W side, 3 = and mode 0 of both sides, 4 = 2 and the V / W
+                                  // side's middle modes (default)
   int afac;                       // 1: factor rows copied with cp.async (overlap the input staging)
   int split1;                     // 1: staged first mode splits a column's output rows over threads when columns are few
   int pad_;

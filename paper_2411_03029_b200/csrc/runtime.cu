@@ -1273,8 +1273,9 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
     bl.info.nt = box_nt;
     {  // FP64 tensor-core phases (OIOBF_BOX_MMA=0: the CUDA-core loops)
       const char* e = std::getenv("OIOBF_BOX_MMA");
-      // 0: CUDA-core loops; 1: first mode; 2: and mode 0 of the V / W side (default); 3: and mode 0 of both sides
-      bl.info.mma = e ? std::atoi(e) : 2;
+      // 0: CUDA-core loops; 1: first mode; 2: and mode 0 of the V / W side; 3: and mode 0 of both sides;
+      // 4 (default): first mode, and the middle modes and mode 0 of the V / W side
+      bl.info.mma = e ? std::atoi(e) : 4;
       const char* e2 = std::getenv("OIOBF_BOX_ASYNC_FAC");  // 0: blocking factor loads
       bl.info.afac = e2 && std::strcmp(e2, "0") == 0 ? 0 : 1;
       const char* e3 = std::getenv("OIOBF_BOX_SPLIT1");  // 0: one thread per column in the staged first mode

@@ -356,9 +356,12 @@ __device__ __forceinline__ void reflect_col2_r(const Bcast& b, double2* __restri
   }
 }
 
-template <int NW, int RPL>
+// `hook(j, owns_next)` runs at the end of column step j, before its barrier
+// (the pipelined panel kernel generates entries of the NEXT panel there, into
+// columns of X that are already dead)
+template <int NW, int RPL, class Hook>
 __device__ void absorb_panel_r(double2* __restrict__ R, double2* __restrict__ X, int w, int nrows, int pr,
-                               Bcast* bc) {
+                               Bcast* bc, Hook hook) {
   constexpr int kWarps = NW;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) panel_reflector(R, X, w, 0, nrows, pr, &bc[0]);
@@ -389,6 +392,7 @@ __device__ void absorb_panel_r(double2* __restrict__ R, double2* __restrict__ X,
     } else if (owns_next) {
       panel_reflector(R, X, w, j + 1, nrows, pr, &bc[(j + 1) & 1]);
     }
+    hook(j, owns_next);
     __syncthreads();
   }
 }
@@ -422,7 +426,14 @@ __device__ void absorb_panel(double2* __restrict__ R, double2* __restrict__ X, i
 // memory) so each column step spreads over 16 warps
 // DIAG (timing diagnostics only, OIOBF_PANEL_DIAG): 1 = entry generation
 // alone (no absorb), 2 = absorb alone (cheap synthetic entries)
-template <int NT, int RPL, int MINB = (NT >= 512 ? 1 : (RPL >= 8 ? 2 : 3)), int DIAG = 0>  // RPL: panel rows / 32
+// PIPE (Green kernel, one thread per panel row, register-cached absorb): the
+// entries of panel p + 1 are generated inside the column steps of panel p --
+// a thread produces its row's entry of column c once that column of X is dead
+// (step c's barrier has passed), up to two per step, skipping the steps in
+// which its warp builds the next reflector -- so the FP64-heavy generation
+// fills the latency bubbles of the barrier-bound absorb instead of running
+// between absorbs.  Same entries, same absorb order: bit-identical R.
+template <int NT, int RPL, int MINB = (NT >= 512 ? 1 : (RPL >= 8 ? 2 : 3)), int DIAG = 0, int PIPE = 0>  // RPL: panel rows / 32
 __global__ void __launch_bounds__(NT, MINB) k_panel(LevelDesc L, KSpec ks, const int* __restrict__ proxies,
                                                     const int* __restrict__ targets, const int* __restrict__ width,
                                                     double2* __restrict__ rpart) {
@@ -469,6 +480,71 @@ __global__ void __launch_bounds__(NT, MINB) k_panel(LevelDesc L, KSpec ks, const
   const int ncg = NT / pr;  // column groups per row
   const int my_row = threadIdx.x % pr, my_cg = threadIdx.x / pr;
   double diag_acc = 0;
+  if constexpr (PIPE && RPL > 0 && DIAG == 0) {
+    // (host: Green kernel, pr == NT -- thread = panel row, all w columns)
+    const bool tgt = sk < L.d;
+    const int q = tgt ? sk : sk - L.d;
+    // row-invariant coordinates of panel row `row` (kernel_entry's operations)
+    auto row_coords = [&](i64 row, double* xs, double* ys) {
+      int ii[kMaxD], jj[kMaxD];
+      i64 rem = row;
+      for (int p = 0; p < D; ++p) {
+        if (p == sk) continue;
+        const int c = cnt[p];
+        const int v = sprox[off[p] + static_cast<int>(rem % c)];
+        rem /= c;
+        if (p < L.d) ii[p] = v;
+        else jj[p - L.d] = v;
+      }
+      xs[0] = xs[1] = xs[2] = 0;
+      ys[0] = ks.off0;
+      ys[1] = ks.off1;
+      ys[2] = ks.off2;
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+        if (p < L.d) {
+          if (p != sk) xs[p] = green_x(ks, ii[p]);
+          if (p + L.d != sk) ys[p] = green_y(ks, p, jj[p]);
+        }
+    };
+    auto entry = [&](int c, const double* xs, const double* ys) {
+      const double v = csin[c];  // green_x / green_y of the candidate (hoisted per column)
+      double xc[3], yc[3];
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        xc[p] = (tgt && p == q) ? v : xs[p];
+        yc[p] = (!tgt && p == q) ? v : ys[p];
+      }
+      return green_from_coords_rcp(ks, xc, yc);
+    };
+    const int row_t = threadIdx.x;  // pr == NT
+    double xs[3], ys[3];
+    {  // first panel: all columns up front
+      const bool valid = r_begin + row_t < r_end;
+      if (valid) row_coords(r_begin + row_t, xs, ys);
+      for (int c = 0; c < w; ++c) X[row_t + c * pr] = valid ? entry(c, xs, ys) : make_double2(0, 0);
+    }
+    __syncthreads();
+    for (i64 r0 = r_begin; r0 < r_end; r0 += pr) {
+      const i64 rn = r0 + pr + row_t;  // this thread's row of the next panel
+      const bool more = r0 + pr < r_end;
+      const bool valid = more && rn < r_end;
+      if (valid) row_coords(rn, xs, ys);
+      int g = more ? 0 : w;  // next column of the next panel this thread generates
+      absorb_panel_r<NT / 32, RPL>(R, X, w, pr, pr, bc, [&](int j, bool owns_next) {
+        if (owns_next) return;  // this warp is on the step's critical path
+        // one entry per step (about one reflector chain's worth of FP64 work
+        // per SM sub-partition), two when a skipped owner step left it behind
+        const int nmax = g + 1 < j ? 2 : 1;
+#pragma unroll 1
+        for (int n = 0; n < nmax && g < j && g < w; ++n, ++g)
+          X[row_t + g * pr] = valid ? entry(g, xs, ys) : make_double2(0, 0);
+      });
+      // (the last step's barrier has passed: every column is dead)
+      for (; g < w; ++g) X[row_t + g * pr] = valid ? entry(g, xs, ys) : make_double2(0, 0);
+      __syncthreads();
+    }
+  } else
   for (i64 r0 = r_begin; r0 < r_end; r0 += pr) {
     const int nrows = static_cast<int>((r_end - r0) < pr ? (r_end - r0) : pr);
     if (DIAG == 2) {
@@ -568,7 +644,7 @@ __global__ void __launch_bounds__(NT, MINB) k_panel(LevelDesc L, KSpec ks, const
       for (int i = threadIdx.x; i < pr * w; i += NT) diag_acc += X[i].x;
       __syncthreads();
     } else if constexpr (RPL > 0) {
-      absorb_panel_r<NT / 32, RPL>(R, X, w, pr, pr, bc);
+      absorb_panel_r<NT / 32, RPL>(R, X, w, pr, pr, bc, [](int, bool) {});
     } else {
       absorb_panel<NT / 32>(R, X, w, nrows, pr, bc);
     }
@@ -894,12 +970,13 @@ void launch_targets(const LevelDesc& L, const int* crank, const i64* cskel_off, 
   TBF_CUDA(cudaGetLastError());
 }
 
-template <int NT, int RPL, int DIAG = 0, int MINB = (NT >= 512 ? 1 : (RPL >= 8 ? 2 : 3))>
+template <int NT, int RPL, int DIAG = 0, int PIPE = 0, int MINB = (NT >= 512 ? 1 : (RPL >= 8 ? 2 : 3))>
 void launch_panel_t(const LevelDesc& L, const KSpec& ks, const int* proxies, const int* targets, const int* width,
                     double2* rpart, size_t smem, i64 grid, cudaStream_t st) {
-  TBF_CUDA(cudaFuncSetAttribute(k_panel<NT, RPL, MINB, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  TBF_CUDA(cudaFuncSetAttribute(k_panel<NT, RPL, MINB, DIAG, PIPE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kMaxDynSmem));
-  k_panel<NT, RPL, MINB, DIAG><<<static_cast<unsigned>(grid), NT, smem, st>>>(L, ks, proxies, targets, width, rpart);
+  k_panel<NT, RPL, MINB, DIAG, PIPE><<<static_cast<unsigned>(grid), NT, smem, st>>>(L, ks, proxies, targets, width,
+                                                                                   rpart);
 }
 
 // Panel rows and resident CTAs per SM for a level of width wmax.  The column
@@ -947,7 +1024,11 @@ void launch_panel_mode(const LevelDesc& L, const KSpec& ks, const int* proxies, 
     // one column update at a time): bit-identical to the generic absorb,
     // config 2 panel 20.4 -> 17.2 ms, config 3 unchanged
     static const int rc = std::getenv("OIOBF_PANEL_NARROW_RC") ? std::atoi(std::getenv("OIOBF_PANEL_NARROW_RC")) : 1;
-    if (rc && !generic && L.pr == 256) launch_panel_t<kThreads, 8, DIAG>(L, ks, proxies, targets, width, rpart, smem, grid, st);
+    // (Green entries of the next panel generated inside the column steps: OIOBF_PANEL_PIPE=0 disables)
+    static const bool pipe = !(std::getenv("OIOBF_PANEL_PIPE") && std::getenv("OIOBF_PANEL_PIPE")[0] == '0');
+    if (rc && !generic && L.pr == 256 && DIAG == 0 && pipe && ks.kind == OIOBF_KERNEL_GREEN)
+      launch_panel_t<kThreads, 8, 0, 1>(L, ks, proxies, targets, width, rpart, smem, grid, st);
+    else if (rc && !generic && L.pr == 256) launch_panel_t<kThreads, 8, DIAG>(L, ks, proxies, targets, width, rpart, smem, grid, st);
     else launch_panel_t<kThreads, 0, DIAG>(L, ks, proxies, targets, width, rpart, smem, grid, st);
   }
   TBF_CUDA(cudaGetLastError());

@@ -397,9 +397,9 @@ __device__ void absorb_panel_r(double2* __restrict__ R, double2* __restrict__ X,
   }
 }
 
-template <int NW>  // warps in the CTA (columns are owned round-robin)
+template <int NW, class Hook>  // warps in the CTA (columns are owned round-robin)
 __device__ void absorb_panel(double2* __restrict__ R, double2* __restrict__ X, int w, int nrows, int pr,
-                             Bcast* bc) {
+                             Bcast* bc, Hook hook) {
   constexpr int kWarps = NW;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) panel_reflector(R, X, w, 0, nrows, pr, &bc[0]);
@@ -418,6 +418,7 @@ __device__ void absorb_panel(double2* __restrict__ R, double2* __restrict__ X, i
     } else if (owns_next) {
       panel_reflector(R, X, w, j + 1, nrows, pr, &bc[(j + 1) & 1]);
     }
+    hook(j, owns_next);
     __syncthreads();
   }
 }
@@ -531,7 +532,7 @@ __global__ void __launch_bounds__(NT, MINB) k_panel(LevelDesc L, KSpec ks, const
       const bool valid = more && rn < r_end;
       if (valid) row_coords(rn, xs, ys);
       int g = more ? 0 : w;  // next column of the next panel this thread generates
-      absorb_panel_r<NT / 32, RPL>(R, X, w, pr, pr, bc, [&](int j, bool owns_next) {
+      auto hook = [&](int j, bool owns_next) {
         if (owns_next) return;  // this warp is on the step's critical path
         // one entry per step (about one reflector chain's worth of FP64 work
         // per SM sub-partition), two when a skipped owner step left it behind
@@ -539,7 +540,8 @@ __global__ void __launch_bounds__(NT, MINB) k_panel(LevelDesc L, KSpec ks, const
 #pragma unroll 1
         for (int n = 0; n < nmax && g < j && g < w; ++n, ++g)
           X[row_t + g * pr] = valid ? entry(g, xs, ys) : make_double2(0, 0);
-      });
+      };
+      absorb_panel_r<NT / 32, RPL>(R, X, w, pr, pr, bc, hook);
       // (the last step's barrier has passed: every column is dead)
       for (; g < w; ++g) X[row_t + g * pr] = valid ? entry(g, xs, ys) : make_double2(0, 0);
       __syncthreads();
@@ -646,7 +648,7 @@ __global__ void __launch_bounds__(NT, MINB) k_panel(LevelDesc L, KSpec ks, const
     } else if constexpr (RPL > 0) {
       absorb_panel_r<NT / 32, RPL>(R, X, w, pr, pr, bc, [](int, bool) {});
     } else {
-      absorb_panel<NT / 32>(R, X, w, nrows, pr, bc);
+      absorb_panel<NT / 32>(R, X, w, nrows, pr, bc, [](int, bool) {});
     }
   }
   if (DIAG == 1 && diag_acc == 12345.678) R[0].x += 1;  // keeps the generation live
@@ -926,7 +928,7 @@ __global__ void __launch_bounds__(kThreads) k_matrix_panel(i64 nparts, i64 rpp, 
       X[i + c * pr] = i < nrows ? a[r0 + i + static_cast<i64>(c) * m] : make_double2(0, 0);
     }
     __syncthreads();
-    absorb_panel<kWarps>(R, X, w, nrows, pr, bc);
+    absorb_panel<kWarps>(R, X, w, nrows, pr, bc, [](int, bool) {});
   }
   double2* out = rpart + (slot * nparts + part) * wmax * wmax;
   for (int i = threadIdx.x; i < w * w; i += kThreads) {  // unpack to w x w column-major

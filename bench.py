@@ -470,7 +470,12 @@ def run_b200(args):
         "fp64_peak": fp64,
         "accuracy": {"sampled_rel_err": samp_err, "tol": cfg.tol, "ratio_to_tol": samp_err / cfg.tol,
                      "samples": 1000, "reference": "direct dense sums on the GPU (oiobf_dense_rows)",
-                     "strategy": args.strategy},
+                     "strategy": args.strategy,
+                     "note": "the default strategy is the reference's own ProxyStrategy (q = 3, row_cap = 2^17), "
+                             "whose proxy sample is what limits the accuracy (DESIGN.md §4); with "
+                             "configs.ACCURACY_STRATEGY (`--strategy accuracy`) every BASELINE config is within "
+                             "tol on 1000 samples -- measured offline, profiles/r2_accuracy_sweep.jsonl: "
+                             "green_cubes_n256 (q = 6, row_cap = 2^27) 0.97 tol, radon2d_n1024 (12, 2^23) 0.87 tol"},
         "cpu_baseline": cpu,
         "compressed_cores": bfp,
         "extras": extras,

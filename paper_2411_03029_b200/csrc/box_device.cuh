@@ -372,7 +372,7 @@ constexpr int kColTab = 512;  // output columns whose offsets are tabulated in s
 
 // mode 0 -> global: task (a, 4 consecutive columns); column c = (a_1 .. a_{d-2}, i, v)
 // tab: per-column offsets (Cc <= kColTab), or null (computed per store)
-template <int CPT>  // columns per task
+template <int CPT, bool STREAM = false>  // columns per task; streaming stores
 __device__ __forceinline__ void last_mode(const BoxDesc& D, int d, int lo, int A, const double2* __restrict__ src,
                                           const double2* __restrict__ M0, int Cc, const long long* tab,
                                           double2* __restrict__ out) {
@@ -398,7 +398,10 @@ __device__ __forceinline__ void last_mode(const BoxDesc& D, int d, int lo, int A
     if (tab) {
 #pragma unroll
       for (int g = 0; g < CPT; ++g)
-        if (g < nc) out[base + tab[c0 + g]] = acc[g];
+        if (g < nc) {
+          if (STREAM) __stcs(out + base + tab[c0 + g], acc[g]);  // the result tensor G: written once, never re-read
+          else out[base + tab[c0 + g]] = acc[g];
+        }
     } else {
 #pragma unroll 1
       for (int g = 0; g < nc; ++g)
@@ -620,6 +623,8 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
   // ---- mode 0 -> global
   if (tab && D.ein[0] <= 16 && D.eout[0] <= 16 && (info.mma == 3 || ((info.mma == 2 || info.mma >= 4) && !info.transpose)))
     last_mode_mma(D, src, smat + S.mo[0], Cc, S.coltab, out);
+  else if (info.stream_out)
+    last_mode<4, true>(D, d, lo, A, src, smat + S.mo[0], Cc, tab ? S.coltab : nullptr, out);
   else
     last_mode<4>(D, d, lo, A, src, smat + S.mo[0], Cc, tab ? S.coltab : nullptr, out);
   __syncthreads();

@@ -134,7 +134,7 @@ struct BoxLaunchInfo {
                                   // side's middle modes (default)
   int afac;                       // 1: factor rows copied with cp.async (overlap the input staging)
   int split1;                     // 1: staged first mode splits a column's output rows over threads when columns are few
-  int pad_;
+  int stream_out;                 // 1: mode 0 stores with the streaming hint (the output is the result tensor G)
 };
 void launch_box(i64 nitems, const BoxDesc* descs, const BoxLaunchInfo& info, const double2* mats,
                 const double2* in, double2* out, cudaStream_t st);

@@ -1278,6 +1278,8 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
       bl.info.mma = e ? std::atoi(e) : 4;
       const char* e2 = std::getenv("OIOBF_BOX_ASYNC_FAC");  // 0: blocking factor loads
       bl.info.afac = e2 && std::strcmp(e2, "0") == 0 ? 0 : 1;
+      const char* e6 = std::getenv("OIOBF_BOX_STREAM_OUT");  // 0: default-policy stores to G
+      bl.info.stream_out = out_buf == BUF_G && !(e6 && std::strcmp(e6, "0") == 0) ? 1 : 0;
       const char* e3 = std::getenv("OIOBF_BOX_SPLIT1");  // 0: one thread per column in the staged first mode
       bl.info.split1 = e3 && std::strcmp(e3, "0") == 0 ? 0 : 1;
     }

@@ -49,9 +49,9 @@ constexpr size_t kBox3Smem = 72 * 1024;  // three CTAs per SM fit in shared memo
 using BoxKernel = void (*)(const BoxDesc*, BoxLaunchInfo, const double2*, const double2*, double2*);
 // 128-thread CTAs whose shared memory lets five or six co-reside take the
 // 80-register instance (OIOBF_BOX6_KB overrides the threshold for A/B runs)
-size_t box6_smem() {
-  const char* e = std::getenv("OIOBF_BOX6_KB");
-  return static_cast<size_t>(e ? std::atoi(e) : 47) * 1024;
+size_t box6_smem() {  // (read once: launch_box runs per launch outside graphs)
+  static const size_t kb = std::getenv("OIOBF_BOX6_KB") ? static_cast<size_t>(std::atoi(std::getenv("OIOBF_BOX6_KB"))) : 47;
+  return kb * 1024;
 }
 
 // kernel instance for a launch: 128 threads at 6 CTAs / SM (80 registers) for

@@ -491,14 +491,25 @@ struct BoxSmem {
 // in S.D (all threads synchronised after the copy).  `wait` blocks until the
 // input is produced (all threads call it; it ends with a CTA barrier).
 // `phase` is the staging mbarrier's parity, flipped on each bulk staging.
-template <int LD, int TP, class Wait>  // TP: column tiles per step of the tensor-core first mode
+// PATH (compile time; the host picks it per launch, info.path): 0 = every
+// variant behind run-time branches; 1 = the V / W side's tensor-core box
+// (unstaged first mode, middle modes and mode 0 by MMA; the launch's boxes all
+// meet the MMA size limits); 2 = staged CUDA-core box (child sums / copied
+// rows, row-split first mode): the same code paths with the other variants
+// compiled out and d fixed to 3 -- these 80-register kernels are sensitive to
+// code size.
+constexpr int kPathAny = 0, kPathVmma = 1, kPathStaged = 2;
+template <int LD, int TP, int PATH, class Wait>  // TP: column tiles per step of the tensor-core first mode
 __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, int crank,
                                          const double2* __restrict__ mats, const double2* in, double2* out,
                                          double2* sm, unsigned& phase, Wait wait) {
   const BoxDesc& D = S.D;
   const int tid = threadIdx.x;
   const int cs = info.cs;
-  const int d = info.d, f = d - 1, nv = info.nv, tr = info.transpose;
+  // (the specialised variants are built for d = 3 -- the host selects them only then -- so the
+  // mode loops and the index decompositions below unroll)
+  const int d = PATH != kPathAny ? 3 : info.d;
+  const int f = d - 1, nv = info.nv, tr = PATH == kPathVmma ? 0 : info.transpose;
   const int ef = D.eout[f];
   const int lo = qdiv(crank * ef, cs), hi = qdiv((crank + 1) * ef, cs);
   const int A = hi - lo;  // 0 <= A <= 8 (host)
@@ -512,7 +523,7 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
   const int e0n = D.ein[0];
   const int total_in = Rs * ein_f * nv;
   // bulk staging needs contiguous 16-B rows (every double2 row qualifies)
-  const bool bulk = info.stage && D.nsum == 1 && D.in_stride[0] == 1;
+  const bool bulk = PATH != kPathVmma && info.stage && D.nsum == 1 && D.in_stride[0] == 1;
   if (tid == 0) {
     S.mo[0] = 0;
     for (int k = 0; k < d; ++k) S.mo[k + 1] = S.mo[k] + D.ein[k] * (k == f ? A : D.eout[k]);
@@ -541,7 +552,7 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
   }
   // ---- the input box is produced by an earlier launch / item
   wait();
-  if (info.stage) {
+  if (PATH != kPathVmma && (PATH == kPathStaged || info.stage)) {
     const int nrows = total_in / e0n;
     if (bulk) {
       const unsigned rbytes = static_cast<unsigned>(e0n) * 16u;
@@ -586,7 +597,14 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
     // (the row count is dispatched to its register bucket: no predicated-off
     // FMAs; one bucket is hot per launch, so the i-cache footprint stays)
     const double2* Mf = smat + S.mo[f];
-    if (info.stage && info.split1 && A > 4 && 2 * Rs * nv <= box_nt()) {
+    if constexpr (PATH == kPathVmma) {
+      first_mode_global_mma<TP>(D, d, in, Mf, t0, A, Rs, ein_f, nv);
+    } else if constexpr (PATH == kPathStaged) {
+      if (info.split1 && A > 4 && 2 * Rs * nv <= box_nt()) first_mode_smem_split(xs, Mf, t0, A, Rs, ein_f, nv);
+      else if (info.amax <= 2) first_mode_smem<2>(xs, Mf, t0, A, Rs, ein_f, nv);
+      else if (info.amax <= 4) first_mode_smem<4>(xs, Mf, t0, A, Rs, ein_f, nv);
+      else first_mode_smem<8>(xs, Mf, t0, A, Rs, ein_f, nv);
+    } else if (info.stage && info.split1 && A > 4 && 2 * Rs * nv <= box_nt()) {
       first_mode_smem_split(xs, Mf, t0, A, Rs, ein_f, nv);
     } else if (info.stage) {
       if (info.amax <= 2) first_mode_smem<2>(xs, Mf, t0, A, Rs, ein_f, nv);
@@ -607,7 +625,9 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
     const int ein = D.ein[k], eo = D.eout[k];
     int B = 1;
     for (int p = 0; p < k; ++p) B *= D.ein[p];
-    if (info.mma >= 4 && !info.transpose && eo <= 8 && ein <= 16) middle_mode_mma(src, dst, smat + S.mo[k], B, ein, eo, Cc);
+    if constexpr (PATH == kPathVmma) middle_mode_mma(src, dst, smat + S.mo[k], B, ein, eo, Cc);
+    else if constexpr (PATH == kPathStaged) middle_mode(src, dst, smat + S.mo[k], B, ein, eo, Cc);
+    else if (info.mma >= 4 && !info.transpose && eo <= 8 && ein <= 16) middle_mode_mma(src, dst, smat + S.mo[k], B, ein, eo, Cc);
     else middle_mode(src, dst, smat + S.mo[k], B, ein, eo, Cc);
     __syncthreads();
     Cc *= eo;
@@ -621,7 +641,12 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
     for (int c = tid; c < Cc; c += box_nt()) S.coltab[c] = col_offset(D, d, lo, A, c);
   __syncthreads();
   // ---- mode 0 -> global
-  if (tab && D.ein[0] <= 16 && D.eout[0] <= 16 && (info.mma == 3 || ((info.mma == 2 || info.mma >= 4) && !info.transpose)))
+  if constexpr (PATH == kPathVmma) {
+    last_mode_mma(D, src, smat + S.mo[0], Cc, S.coltab, out);
+  } else if constexpr (PATH == kPathStaged) {
+    if (info.stream_out) last_mode<4, true>(D, d, lo, A, src, smat + S.mo[0], Cc, tab ? S.coltab : nullptr, out);
+    else last_mode<4>(D, d, lo, A, src, smat + S.mo[0], Cc, tab ? S.coltab : nullptr, out);
+  } else if (tab && D.ein[0] <= 16 && D.eout[0] <= 16 && (info.mma == 3 || ((info.mma == 2 || info.mma >= 4) && !info.transpose)))
     last_mode_mma(D, src, smat + S.mo[0], Cc, S.coltab, out);
   else if (info.stream_out)
     last_mode<4, true>(D, d, lo, A, src, smat + S.mo[0], Cc, tab ? S.coltab : nullptr, out);

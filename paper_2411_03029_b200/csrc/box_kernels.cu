@@ -16,7 +16,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // memory lets three CTAs co-reside (latency-bound small boxes: config 3's
 // levels 1.65 -> 1.56 ms), 2 otherwise (the 80-register cap spills on large
 // boxes: config 5 was 4% slower with it)
-template <int NT, int MINB>
+template <int NT, int MINB, int PATH = 0>
 __global__ void __launch_bounds__(NT, MINB) k_box(const BoxDesc* __restrict__ descs, BoxLaunchInfo info,
                                                         const double2* __restrict__ mats,
                                                         const double2* __restrict__ in, double2* __restrict__ out) {
@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(NT, MINB) k_box(const BoxDesc* __restrict__ de
   }
   __syncthreads();
   unsigned phase = 0;
-  box_body<MINB >= 3 ? 4 : 8, 2>(S, info, crank, mats, in, out, sm, phase, [] { pdl_wait(); });
+  box_body<MINB >= 3 ? 4 : 8, 2, PATH>(S, info, crank, mats, in, out, sm, phase, [] { pdl_wait(); });
 }
 
 
@@ -57,14 +57,16 @@ size_t box6_smem() {  // (read once: launch_box runs per launch outside graphs)
 // kernel instance for a launch: 128 threads at 6 CTAs / SM (80 registers) for
 // small boxes, 256 threads at 3 (80 registers) or 2 (128: large boxes, and
 // streamed inputs whose 8 loads in flight would spill at 80) CTAs / SM
-BoxKernel box_kernel(int nt, int stage, size_t smem) {
+BoxKernel box_kernel(int nt, int stage, size_t smem, int path) {
+  if (nt == 128 && path == 1) return smem <= box6_smem() ? k_box<128, 6, 1> : k_box<128, 3, 1>;
+  if (nt == 128 && path == 2) return smem <= box6_smem() ? k_box<128, 6, 2> : k_box<128, 3, 2>;
   if (nt == 128) return smem <= box6_smem() ? k_box<128, 6> : k_box<128, 3>;
   return smem <= kBox3Smem && stage ? k_box<256, 3> : k_box<256, 2>;
 }
 
 int box_ctas_per_sm(int nt, int stage, size_t smem) {
   int n = 0;
-  const BoxKernel k = box_kernel(nt, stage, smem);
+  const BoxKernel k = box_kernel(nt, stage, smem, 0);
   TBF_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   TBF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, nt, smem));
   return n;
@@ -84,7 +86,7 @@ void launch_box(i64 nitems, const BoxDesc* descs, const BoxLaunchInfo& info, con
   if (info.amax > 8) throw std::runtime_error("launch_box: more than 8 rows of mode d-1 per CTA");
   const size_t smem = box_smem_bytes(info);
   const int nt = info.nt > 0 ? info.nt : kBoxThreads;
-  const BoxKernel kern = box_kernel(nt, info.stage, smem);
+  const BoxKernel kern = box_kernel(nt, info.stage, smem, info.path);
   TBF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(nitems * info.cs));

@@ -1280,6 +1280,25 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
       bl.info.afac = e2 && std::strcmp(e2, "0") == 0 ? 0 : 1;
       const char* e6 = std::getenv("OIOBF_BOX_STREAM_OUT");  // 0: default-policy stores to G
       bl.info.stream_out = out_buf == BUF_G && !(e6 && std::strcmp(e6, "0") == 0) ? 1 : 0;
+      // compile-time kernel variant (OIOBF_BOX_PATH=0: the all-variants kernel everywhere)
+      {
+        const char* e8 = std::getenv("OIOBF_BOX_PATH");
+        const bool spec = !(e8 && std::strcmp(e8, "0") == 0) && box_nt == 128 && d == 3;
+        bool vmma = spec && !stage && bl.info.mma >= 4 && !transpose;
+        for (const BoxDesc& x : descs) {
+          if (!vmma) break;
+          i64 cc = static_cast<i64>(amax_rows) * nv;
+          for (int k = 1; k < f; ++k) {
+            vmma = vmma && x.ein[k] <= 16 && x.eout[k] <= 8;
+            cc *= x.eout[k];
+          }
+          vmma = vmma && x.ein[f] <= 16 && x.ein[0] <= 16 && x.eout[0] <= 16 && cc <= 512;
+        }
+        // (the staged variant has CUDA-core middle modes and mode 0: what the P / U side runs unless
+        // OIOBF_BOX_MMA=3, and the V / W side only below OIOBF_BOX_MMA=2)
+        const bool staged = spec && stage && (transpose ? bl.info.mma != 3 : bl.info.mma < 2);
+        bl.info.path = vmma ? 1 : staged ? 2 : 0;
+      }
       const char* e3 = std::getenv("OIOBF_BOX_SPLIT1");  // 0: one thread per column in the staged first mode
       bl.info.split1 = e3 && std::strcmp(e3, "0") == 0 ? 0 : 1;
     }

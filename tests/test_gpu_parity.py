@@ -715,7 +715,8 @@ def test_box_cta_variants_bit_identical(oracle, monkeypatch, name, spec, tol, L)
         F = rand_c(rng, shape)
         outs = []
         for env in ({"OIOBF_BOX_NT": "256", "OIOBF_BOX_MMA": "0"}, {"OIOBF_BOX_NT": "128", "OIOBF_BOX_MMA": "0"},
-                    {"OIOBF_BOX_NT": "128", "OIOBF_BOX_MMA": "4"}, {"OIOBF_BOX_NT": "128", "OIOBF_BOX_MMA": "3"}):
+                    {"OIOBF_BOX_NT": "128", "OIOBF_BOX_MMA": "4"}, {"OIOBF_BOX_NT": "128", "OIOBF_BOX_MMA": "3"},
+                    {"OIOBF_BOX_NT": "128", "OIOBF_BOX_MMA": "4", "OIOBF_BOX_PATH": "0"}):
             for k, v in env.items():
                 monkeypatch.setenv(k, v)
             bf.set_apply_engine("tiny")  # drop cached plans
@@ -726,6 +727,8 @@ def test_box_cta_variants_bit_identical(oracle, monkeypatch, name, spec, tol, L)
         assert np.array_equal(outs[0], outs[1])
         Go = tbo.contract(F)
         assert rel(outs[1], Go) < 1e-10
+        # the compile-time specialised kernels (default) run the same code paths as the all-variants kernel
+        assert np.array_equal(outs[2], outs[4])
         for g in outs[2:]:  # tensor-core phases: the default set (first mode, V/W middle modes and mode 0), and every mode 0
             assert rel(g, outs[1]) < 1e-13
             assert rel(g, Go) < 1e-10

@@ -57,10 +57,25 @@ size_t box6_smem() {  // (read once: launch_box runs per launch outside graphs)
 // kernel instance for a launch: 128 threads at 6 CTAs / SM (80 registers) for
 // small boxes, 256 threads at 3 (80 registers) or 2 (128: large boxes, and
 // streamed inputs whose 8 loads in flight would spill at 80) CTAs / SM
+// 128-thread instance for `path` whose register budget matches the CTAs per SM
+// that shared memory allows anyway (6: 80 registers ... 3: 170): a launch held
+// to 4-5 CTAs by its shared memory gets 128 / 102 registers instead of spilling
+// at 80.  OIOBF_BOX_MINB=0 restores the two-instance rule (80 registers up to
+// OIOBF_BOX6_KB of shared memory).
+template <int PATH>
+BoxKernel box_kernel128(size_t smem) {
+  static const bool fixed = std::getenv("OIOBF_BOX_MINB") && std::getenv("OIOBF_BOX_MINB")[0] == '0';
+  if (fixed) return smem <= box6_smem() ? k_box<128, 6, PATH> : k_box<128, 3, PATH>;
+  const size_t per_cta = smem + sizeof(BoxSmem) + 1024;  // static shared memory and the per-CTA reserve
+  const size_t n = (227 * 1024) / per_cta;
+  if (n >= 6) return k_box<128, 6, PATH>;
+  if (n == 5) return k_box<128, 5, PATH>;
+  if (n == 4) return k_box<128, 4, PATH>;
+  return k_box<128, 3, PATH>;
+}
+
 BoxKernel box_kernel(int nt, int stage, size_t smem, int path) {
-  if (nt == 128 && path == 1) return smem <= box6_smem() ? k_box<128, 6, 1> : k_box<128, 3, 1>;
-  if (nt == 128 && path == 2) return smem <= box6_smem() ? k_box<128, 6, 2> : k_box<128, 3, 2>;
-  if (nt == 128) return smem <= box6_smem() ? k_box<128, 6> : k_box<128, 3>;
+  if (nt == 128) return path == 1 ? box_kernel128<1>(smem) : path == 2 ? box_kernel128<2>(smem) : box_kernel128<0>(smem);
   return smem <= kBox3Smem && stage ? k_box<256, 3> : k_box<256, 2>;
 }
 

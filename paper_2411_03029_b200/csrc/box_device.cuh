@@ -374,7 +374,7 @@ constexpr int kColTab = 512;  // output columns whose offsets are tabulated in s
 // tab: per-column offsets (Cc <= kColTab), or null (computed per store)
 template <int CPT, bool STREAM = false>  // columns per task; streaming stores
 __device__ __forceinline__ void last_mode(const BoxDesc& D, int d, int lo, int A, const double2* __restrict__ src,
-                                          const double2* __restrict__ M0, int Cc, const long long* tab,
+                                          const double2* __restrict__ M0, int Cc, const int* tab,
                                           double2* __restrict__ out) {
   const int ein = D.ein[0], eo = D.eout[0];
   const int ncg = (Cc + CPT - 1) / CPT;
@@ -431,7 +431,7 @@ __device__ __forceinline__ void last_mode(const BoxDesc& D, int d, int lo, int A
 // time as the CUDA-core loop) 22 us slower, so the default uses it for V / W
 // only (info.mma == 2; 3 = both sides).
 __device__ __forceinline__ void last_mode_mma(const BoxDesc& D, const double2* __restrict__ src,
-                                              const double2* __restrict__ M0, int Cc, const long long* tab,
+                                              const double2* __restrict__ M0, int Cc, const int* tab,
                                               double2* __restrict__ out) {
   const int ein = D.ein[0], eo = D.eout[0];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = box_nt() >> 5;
@@ -482,7 +482,8 @@ __device__ __forceinline__ void last_mode_mma(const BoxDesc& D, const double2* _
 // Shared-memory state of one box CTA besides the dynamic buffer.
 struct BoxSmem {
   BoxDesc D;
-  long long coltab[kColTab];  // output column offsets of mode 0's stores
+  int coltab[kColTab];  // output column offsets of mode 0's stores, relative to the box origin (32 bits: the
+                        // host enables the table only when every box's span fits, info.tab_ok)
   int mo[kMaxD + 1];
   unsigned long long bar;  // staging mbarrier (initialised once per CTA)
 };
@@ -636,9 +637,9 @@ __device__ __forceinline__ void box_body(BoxSmem& S, const BoxLaunchInfo& info, 
     dst = tmp;
   }
   // output column offsets of mode 0's stores (computed once, not per store)
-  const bool tab = Cc <= kColTab;
+  const bool tab = Cc <= kColTab && info.tab_ok;
   if (tab)
-    for (int c = tid; c < Cc; c += box_nt()) S.coltab[c] = col_offset(D, d, lo, A, c);
+    for (int c = tid; c < Cc; c += box_nt()) S.coltab[c] = static_cast<int>(col_offset(D, d, lo, A, c));
   __syncthreads();
   // ---- mode 0 -> global
   if constexpr (PATH == kPathVmma) {

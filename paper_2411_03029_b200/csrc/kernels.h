@@ -135,6 +135,7 @@ struct BoxLaunchInfo {
   int afac;                       // 1: factor rows copied with cp.async (overlap the input staging)
   int split1;                     // 1: staged first mode splits a column's output rows over threads when columns are few
   int stream_out;                 // 1: mode 0 stores with the streaming hint (the output is the result tensor G)
+  int tab_ok;                     // 1: every box's output span fits 32-bit column offsets (the mode-0 column table)
   int path;                       // compile-time variant of k_box for this launch (box_device.cuh: 0 any, 1 V / W
                                   // tensor-core box, 2 staged CUDA-core box)
 };

@@ -1280,6 +1280,15 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
       bl.info.afac = e2 && std::strcmp(e2, "0") == 0 ? 0 : 1;
       const char* e6 = std::getenv("OIOBF_BOX_STREAM_OUT");  // 0: default-policy stores to G
       bl.info.stream_out = out_buf == BUF_G && !(e6 && std::strcmp(e6, "0") == 0) ? 1 : 0;
+      {  // 32-bit column table: offsets relative to the box origin
+        bool ok = true;
+        for (const BoxDesc& x : descs) {
+          i64 span = 0;
+          for (int k = 1; k <= d; ++k) span += static_cast<i64>(std::max(0, x.eout[k] - 1)) * std::llabs(x.out_stride[k]);
+          ok = ok && span < (i64{1} << 31);
+        }
+        bl.info.tab_ok = ok ? 1 : 0;
+      }
       // compile-time kernel variant (OIOBF_BOX_PATH=0: the all-variants kernel everywhere)
       {
         const char* e8 = std::getenv("OIOBF_BOX_PATH");
@@ -1292,7 +1301,7 @@ std::unique_ptr<Plan> build_plan(oiobf_tbf& b, i64 nv, bool chunked, int parity 
             vmma = vmma && x.ein[k] <= 16 && x.eout[k] <= 8;
             cc *= x.eout[k];
           }
-          vmma = vmma && x.ein[f] <= 16 && x.ein[0] <= 16 && x.eout[0] <= 16 && cc <= 512;
+          vmma = vmma && x.ein[f] <= 16 && x.ein[0] <= 16 && x.eout[0] <= 16 && cc <= 512 && bl.info.tab_ok;
         }
         // (the staged variant has CUDA-core middle modes and mode 0: what the P / U side runs unless
         // OIOBF_BOX_MMA=3, and the V / W side only below OIOBF_BOX_MMA=2)

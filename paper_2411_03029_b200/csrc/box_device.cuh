@@ -15,11 +15,17 @@
 //             child contributions, batched register loads (8 children in
 //             flight) summed in ascending child order
 //   mode d-1  thread per input column, this CTA's A output rows in registers
+//             (few columns: a column's rows split over threads in groups of 4)
 //   modes d-2..1  smem -> smem, 4 output rows per thread-task
 //   mode 0    4 columns per thread-task, written straight to global memory
 //             (consecutive threads = consecutive rows of mode 0: coalesced)
-// The code is latency/issue bound (boxes are small); the layout choices above
-// minimise instructions per useful FMA.  32-bit index math inside a box.
+// On the V / W side (unstaged input, <= 16 input rows and <= 8 output rows per
+// mode) the three mode phases run on the FP64 tensor core instead
+// (mma.sync.m8n8k4.f64: first_mode_global_mma, middle_mode_mma, last_mode_mma).
+// The code is latency/issue bound (boxes are small) and sensitive to occupancy
+// and code size: k_box is instantiated per register budget (CTAs per SM that
+// shared memory allows) and per PATH (variants compiled out), see box_body.
+// 32-bit index math inside a box.
 #pragma once
 
 #include "kernels.h"

@@ -17,6 +17,16 @@ using namespace oiobf;
 
 int main(int argc, char** argv) {
   if (argc > 1 && std::string(argv[1]) == "--compile-only") return 0;
+  if (argc > 3 && std::string(argv[1]) == "--owners") {  // balanced_owners(weights, world): host logic only
+    const std::int64_t world = std::atoll(argv[2]);
+    std::vector<double> w;
+    for (int i = 3; i < argc; ++i) w.push_back(std::atof(argv[i]));
+    const std::vector<std::int32_t> own = balanced_owners(w, world);
+    std::cout << "[";
+    for (std::size_t i = 0; i < own.size(); ++i) std::cout << (i ? "," : "") << own[i];
+    std::cout << "]" << std::endl;
+    return 0;
+  }
   const int world = argc > 1 ? std::atoi(argv[1]) : 2;
   const std::string which = argc > 2 ? argv[2] : "cubes32";
   KernelSpec s;

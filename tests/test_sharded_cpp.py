@@ -29,6 +29,24 @@ def test_sharded_headers_compile():
     assert subprocess.run([EXE, "--compile-only"]).returncode == 0
 
 
+def test_balanced_owners_cpp_equals_python():
+    """The C++ driver's balanced_owners (sharded.hpp) and the Python one
+    (sharded.py) compute the same ownership map -- ranks in one job may mix the
+    two orchestrations only if they agree."""
+    import numpy as np
+
+    from paper_2411_03029_b200.sharded import balanced_owners
+    _build()
+    rng = np.random.default_rng(5)
+    for n, world in ((64, 8), (64, 4), (8, 2), (16, 3), (8, 8), (12, 5)):
+        w = rng.integers(10, 90, n).astype(np.float64)
+        w[: n // 4] *= 3
+        w[n // 2] = w[n // 2 + 1]  # a tie
+        r = subprocess.run([EXE, "--owners", str(world)] + [repr(float(x)) for x in w], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr[-500:]
+        assert json.loads(r.stdout.strip()) == balanced_owners(w, world).tolist(), (n, world)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,case", [(2, "cubes32"), (4, "cubes32"), (8, "cubes32"), (3, "radon64"),
                                         (8, "plates64L4"), (4, "dft6")])

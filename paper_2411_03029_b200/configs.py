@@ -114,9 +114,9 @@ BY_NAME = {c.name: c for c in CONFIGS}
 # Cartesian-product row sample, not the composition; the error falls
 # monotonically with the row cap.  Measured sampled error / tol:
 #   green_plates_n64  (4, 2^17): 0.69          green_cubes_n64 (3, 2^23): 0.65
-#   green_cubes_n256  (6, 2^27): 0.97 (1248 s construction; (4, 2^25): 1.23, 2^23: 2.0-2.5, 2^21: 6.8)
+#   green_cubes_n256  (6, 2^27): 0.97 (1058 s construction, 1248 s before the pipelined panels; (4, 2^25): 1.23, 2^23: 2.0-2.5, 2^21: 6.8)
 #   dft6_n16          (3, 2^17): 1e-7 (exact: every ID has rank 1)
-#   radon2d_n1024     (12, 2^23): 0.87 (615 s construction; (8, 2^21): 5.3, default 2256-4375)
+#   radon2d_n1024     (12, 2^23): 0.87 (609 s construction; (8, 2^21): 5.3, default 2256-4375)
 ACCURACY_STRATEGY = {
     "green_plates_n64": (4, 1 << 17),
     "green_cubes_n64": (3, 1 << 23),
